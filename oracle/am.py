@@ -1,0 +1,271 @@
+"""Load-step nonlinear solvers -- oracle (test infrastructure only).
+
+Restates ``solver.py`` of the reference: the optimality residual
+(``solver.py:104-118``), the elastic and damage half-steps (``:129-160``),
+alternate minimisation with over-relaxation and midpoint feasibility
+backtracking (``:166-241``), the coupled active-set Newton solve with a
+field-split MINRES inner solver (``:247-330``), ORAM-N outer cycles with the
+energy-acceptance rule (``:333-387``) and the dispatcher (``:390-417``).
+
+Extension: ``am_switch_atol`` -- an absolute hand-off threshold for ORAM-N
+(BASELINE config 2, "switch to Newton once the AM residual falls below
+1e-3"); with it the hand-off target is max(am_switch_atol, outer_atol) and the
+settled test is skipped.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Callable, Optional
+
+import numpy as np
+
+from . import krylov as kr
+from .mcp import RSLSConfig, fb_box, rsls
+from .p1 import EnergyParts, P1Model
+
+
+@dataclass
+class LoadState:
+    u: np.ndarray
+    alpha: np.ndarray
+    alpha_lb: np.ndarray
+    load: float = 0.0
+
+    @classmethod
+    def zeros(cls, model: P1Model, alpha_lb=None):
+        lb = np.zeros(model.nv) if alpha_lb is None else np.asarray(alpha_lb, float).copy()
+        return cls(np.zeros(model.nu_dofs), lb.copy(), lb, 0.0)
+
+    def copy(self):
+        return LoadState(self.u.copy(), self.alpha.copy(), self.alpha_lb.copy(), self.load)
+
+
+@dataclass
+class AMConfig:
+    method: str = "am"            # am | oram_newton | newton_only
+    omega: float = 1.0
+    outer_atol: float = 1e-7
+    am_rtol: float = 1e-1
+    am_switch_atol: Optional[float] = None
+    max_am_iterations: int = 1000
+    max_newton_iterations: int = 30
+    max_outer_cycles: int = 20
+    elastic_solver: str = "direct"   # direct | cg
+    elastic_rtol: float = 1e-10
+    elastic_precond: str = "jacobi"  # jacobi | chebyshev
+    coupled_solver: str = "fieldsplit"  # direct | fieldsplit
+    fieldsplit_inner: str = "direct"
+    fieldsplit_rtol: float = 1e-6
+    damage_atol_factor: float = 0.1
+    max_vi_iterations: int = 200
+    newton_dalpha: float = 1e-6
+    log: Optional[Callable[[dict], None]] = None
+
+    def __post_init__(self):
+        if not 0.0 < self.omega < 2.0:
+            raise ValueError("omega must lie strictly inside (0, 2)")
+
+
+@dataclass
+class StepStats:
+    converged: bool = False
+    final_residual_norm: float = np.inf
+    am_iterations: int = 0
+    newton_iterations: int = 0
+    newton_attempts: int = 0
+    total_krylov_iterations: int = 0
+    omega_bar_min: float = 1.0
+    energy_history: list = field(default_factory=list)
+    residual_history: list = field(default_factory=list)
+
+
+def optimality_residual(st: LoadState, m: P1Model):
+    ru = m.residual_u(st.u, st.alpha, bc_rows="zero")
+    ra = m.residual_alpha(st.u, st.alpha)
+    return np.concatenate([ru, fb_box(st.alpha, ra, st.alpha_lb, np.ones_like(st.alpha))])
+
+
+def optimality_norm(st, m) -> float:
+    return float(np.linalg.norm(optimality_residual(st, m)))
+
+
+def _snap(st, m):
+    if m.bc is not None:
+        st.u[m.bc[0]] = m.bc[1]
+
+
+def elastic_half_step(st: LoadState, m: P1Model, cfg: AMConfig):
+    K, f = m.lift(m.Kuu(st.alpha, eliminate=False), m.load_u(st.alpha))
+    if cfg.elastic_solver == "direct":
+        return kr.lu_solver(K)(f), 0
+    M = kr.Jacobi(K) if cfg.elastic_precond == "jacobi" else kr.Chebyshev(K)
+    u, rep = kr.pcg(K, f, M, rtol=cfg.elastic_rtol)
+    if not rep.converged:
+        raise kr.SolverFailure(f"elastic CG stalled at residual {rep.residual:.3e}")
+    return u, rep.iterations
+
+
+def damage_half_step(st: LoadState, m: P1Model, cfg: AMConfig):
+    K = m.Kaa(st.u, st.alpha)
+    c = m.residual_alpha(st.u, st.alpha) - K @ st.alpha
+    rc = RSLSConfig(abs_tol=cfg.damage_atol_factor * cfg.outer_atol,
+                    max_iterations=cfg.max_vi_iterations)
+    return rsls(lambda a: K @ a + c, lambda a: K, st.alpha_lb, np.ones_like(st.alpha),
+                st.alpha, rc, jac_matvec=lambda J: (lambda v: J.T @ v))
+
+
+def relax_damage(a_prev, a_star, lb, omega):
+    """Over-relaxed damage update with midpoint backtracking (solver.py:202-215)."""
+    wb = omega
+    cand = a_star if wb == 1.0 else a_prev + wb * (a_star - a_prev)
+    k = 0
+    while np.any(cand < lb) or np.any(cand > 1.0):
+        wb = 0.5 * (1.0 + wb)
+        k += 1
+        if k >= 60 or wb == 1.0:
+            wb, cand = 1.0, a_star
+            break
+        cand = a_prev + wb * (a_star - a_prev)
+    return np.clip(cand, lb, 1.0), wb
+
+
+def am_loop(st: LoadState, m: P1Model, cfg: AMConfig, rtol=None, cycle=0) -> StepStats:
+    _snap(st, m)
+    phi0 = optimality_norm(st, m)
+    if rtol is None:
+        target, need_settle = cfg.outer_atol, False
+    elif cfg.am_switch_atol is not None:
+        target, need_settle = max(cfg.am_switch_atol, cfg.outer_atol), False
+    else:
+        target, need_settle = max(rtol * phi0, cfg.outer_atol), True
+    rep = StepStats(omega_bar_min=cfg.omega)
+    rep.energy_history.append(m.energy(st.u, st.alpha))
+    rep.residual_history.append(phi0)
+    d_prev = None
+    while rep.am_iterations < cfg.max_am_iterations:
+        rep.am_iterations += 1
+        u0 = st.u.copy()
+        us, kit = elastic_half_step(st, m, cfg)
+        rep.total_krylov_iterations += kit
+        st.u = u0 + cfg.omega * (us - u0)
+        _snap(st, m)
+        a0 = st.alpha.copy()
+        a_star, vrep = damage_half_step(st, m, cfg)
+        rep.total_krylov_iterations += vrep.total_krylov_iterations
+        st.alpha, wb = relax_damage(a0, a_star, st.alpha_lb, cfg.omega)
+        rep.omega_bar_min = min(rep.omega_bar_min, wb)
+        dal = float(np.max(np.abs(st.alpha - a0), initial=0.0))
+        res = optimality_norm(st, m)
+        en = m.energy(st.u, st.alpha)
+        rep.energy_history.append(en)
+        rep.residual_history.append(res)
+        if cfg.log is not None:
+            cfg.log({"phase": "am", "cycle": cycle, "iteration": rep.am_iterations,
+                     "residual": res, "omega_bar": wb, "elastic": en.elastic,
+                     "dissipated": en.dissipated, "total": en.total})
+        if not need_settle or dal == 0.0:
+            settled = True
+        elif d_prev is not None and dal < d_prev:
+            settled = dal * dal / (d_prev - dal) <= cfg.newton_dalpha
+        else:
+            settled = False
+        d_prev = dal
+        if res <= cfg.outer_atol or (res <= target and settled):
+            rep.converged = True
+            break
+    rep.final_residual_norm = rep.residual_history[-1]
+    return rep
+
+
+def _coupled_linear(cfg: AMConfig, nu: int):
+    def solve(J: kr.Block2x2, idx, rhs):
+        if cfg.coupled_solver == "direct":
+            return kr.lu_solver(kr.sub(J.csr(), idx, idx))(rhs), None
+        iu = idx[idx < nu]
+        ia = idx[idx >= nu] - nu
+        red = kr.Block2x2(kr.sub(J.A, iu, iu), kr.sub(J.B, iu, ia), kr.sub(J.C, ia, ia))
+        P = kr.FieldSplit(red, kr.lu_solver(red.A), kr.lu_solver(red.C))
+        d, rep = kr.minres(red, rhs, P, rtol=cfg.fieldsplit_rtol)
+        if not rep.converged:
+            raise kr.SolverFailure(f"field-split MINRES stalled at {rep.residual:.3e}")
+        return d, rep
+    return solve
+
+
+def newton_coupled(st: LoadState, m: P1Model, cfg: AMConfig):
+    """Active-set Newton on the stacked system (solver.py:274-330); returns (state, stats)."""
+    nu = m.nu_dofs
+    w = st.copy()
+
+    def F(x):
+        w.u, w.alpha = x[:nu], x[nu:]
+        return np.concatenate([m.residual_u(w.u, w.alpha, bc_rows="value"),
+                               m.residual_alpha(w.u, w.alpha)])
+
+    def J(x):
+        w.u, w.alpha = x[:nu], x[nu:]
+        return kr.Block2x2(m.Kuu(w.alpha, eliminate=True), m.Kua(w.u, w.alpha, mask_bc=True),
+                           m.Kaa(w.u, w.alpha))
+
+    lo = np.concatenate([np.full(nu, -np.inf), st.alpha_lb])
+    hi = np.concatenate([np.full(nu, np.inf), np.ones(m.nv)])
+    x0 = np.concatenate([st.u, st.alpha])
+    x, rep = rsls(F, J, lo, hi, x0, RSLSConfig(abs_tol=cfg.outer_atol,
+                                               max_iterations=cfg.max_newton_iterations),
+                  linear=_coupled_linear(cfg, nu))
+    out = st.copy()
+    out.u, out.alpha = x[:nu].copy(), x[nu:].copy()
+    return out, rep
+
+
+def oram_newton(st: LoadState, m: P1Model, cfg: AMConfig) -> StepStats:
+    rep = StepStats(omega_bar_min=cfg.omega)
+    _snap(st, m)
+    for cycle in range(cfg.max_outer_cycles):
+        if optimality_norm(st, m) <= cfg.outer_atol:
+            rep.converged = True
+            break
+        ar = am_loop(st, m, cfg, rtol=cfg.am_rtol, cycle=cycle)
+        rep.am_iterations += ar.am_iterations
+        rep.total_krylov_iterations += ar.total_krylov_iterations
+        rep.omega_bar_min = min(rep.omega_bar_min, ar.omega_bar_min)
+        s = 1 if rep.energy_history else 0
+        rep.energy_history.extend(ar.energy_history[s:])
+        rep.residual_history.extend(ar.residual_history[s:])
+        if ar.final_residual_norm <= cfg.outer_atol:
+            rep.converged = True
+            break
+        e0 = ar.energy_history[-1].total
+        ns, nr = newton_coupled(st, m, cfg)
+        rep.newton_attempts += 1
+        rep.newton_iterations += nr.iterations
+        rep.total_krylov_iterations += nr.total_krylov_iterations
+        en = m.energy(ns.u, ns.alpha)
+        if nr.converged and en.total <= e0 + 1e-12 * (1.0 + abs(e0)):
+            st.u, st.alpha = ns.u, ns.alpha
+            rep.energy_history.append(en)
+            rep.residual_history.append(nr.final_residual_norm)
+            break
+    rep.final_residual_norm = optimality_norm(st, m)
+    rep.converged = rep.final_residual_norm <= cfg.outer_atol
+    return rep
+
+
+def load_step(st: LoadState, m: P1Model, cfg: AMConfig) -> StepStats:
+    if cfg.method == "oram_newton":
+        return oram_newton(st, m, cfg)
+    if cfg.method == "newton_only":
+        st.u, kit = elastic_half_step(st, m, cfg)
+        ns, nr = newton_coupled(st, m, cfg)
+        st.u, st.alpha = ns.u, ns.alpha
+        return StepStats(converged=nr.converged, final_residual_norm=nr.final_residual_norm,
+                         newton_iterations=nr.iterations, newton_attempts=1,
+                         total_krylov_iterations=nr.total_krylov_iterations + kit,
+                         energy_history=[m.energy(st.u, st.alpha)],
+                         residual_history=list(nr.residual_history))
+    return am_loop(st, m, cfg)
+
+
+def energy_of(st: LoadState, m: P1Model) -> EnergyParts:
+    return m.energy(st.u, st.alpha)

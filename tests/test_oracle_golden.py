@@ -1,0 +1,172 @@
+"""Pin the CPU oracle against golden vectors produced by the reference itself.
+
+Fixtures: tests/golden/ref_*.npz from tests/golden/make_golden.py (which imports
+/root/reference/pkg/src/phasefrac).  CPU only.
+"""
+
+import os
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from conftest import GOLDEN
+from oracle import am, krylov, mcp, problems
+from oracle.meshgen import grid_mesh
+from oracle.p1 import MaterialSpec, P1Model
+
+OPS = np.load(os.path.join(GOLDEN, "ref_operators.npz"))
+VI = np.load(os.path.join(GOLDEN, "ref_vi.npz"))
+KR = np.load(os.path.join(GOLDEN, "ref_krylov.npz"))
+ST = np.load(os.path.join(GOLDEN, "ref_steps.npz"))
+
+
+def rel(a, b):
+    return np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300)
+
+
+def model_for(tag):
+    L, H, h, E, nu, Gc, ell, k = OPS[f"{tag}_params"]
+    nx, ny = max(1, round(L / h)), max(1, round(H / h))
+    spec = MaterialSpec(E=E, nu=nu, Gc=Gc, ell=ell, k_ell=k)
+    m = P1Model(grid_mesh(nx, ny, L, H, "union_jack"), spec)
+    m.eps0 = OPS[f"{tag}_eps0"].copy()
+    m.bc = (OPS[f"{tag}_bc_dofs"], OPS[f"{tag}_bc_vals"])
+    return m
+
+
+@pytest.mark.parametrize("tag", ["sq4", "bar", "rect"])
+def test_operators_match_reference(tag):
+    m = model_for(tag)
+    u, a, lb = OPS[f"{tag}_u"], OPS[f"{tag}_alpha"], OPS[f"{tag}_alpha_lb"]
+    xu, xa = OPS[f"{tag}_xu"], OPS[f"{tag}_xa"]
+    assert np.allclose(np.array(m.energy(u, a)), OPS[f"{tag}_energy"], rtol=1e-13, atol=0)
+    assert rel(m.residual_u(u, a, "value"), OPS[f"{tag}_ru_bc"]) < 1e-13
+    assert rel(m.residual_u(u, a, "none"), OPS[f"{tag}_ru_raw"]) < 1e-13
+    assert rel(m.residual_alpha(u, a), OPS[f"{tag}_ra"]) < 1e-13
+    assert rel(m.load_u(a), OPS[f"{tag}_f"]) < 1e-13
+    Kraw = m.Kuu(a, eliminate=False)
+    assert rel(Kraw @ xu, OPS[f"{tag}_Kuu_raw_x"]) < 1e-13
+    assert rel(m.Kuu(a) @ xu, OPS[f"{tag}_Kuu_bc_x"]) < 1e-13
+    assert rel(m.Kua(u, a) @ xa, OPS[f"{tag}_Kua_x"]) < 1e-13
+    assert rel(m.Kua(u, a, mask_bc=False) @ xa, OPS[f"{tag}_Kua_raw_x"]) < 1e-13
+    assert rel(m.Kua(u, a).T @ xu, OPS[f"{tag}_KuaT_x"]) < 1e-13
+    assert rel(m.Kaa(u, a) @ xa, OPS[f"{tag}_Kaa_x"]) < 1e-13
+    assert rel(m.lift(Kraw, m.load_u(a))[1], OPS[f"{tag}_lifted_rhs"]) < 1e-13
+    assert rel(Kraw.diagonal(), OPS[f"{tag}_Kuu_diag"]) < 1e-13
+    assert rel(m.Kaa(u, a).diagonal(), OPS[f"{tag}_Kaa_diag"]) < 1e-13
+    st = am.LoadState(u, a, lb)
+    assert rel(am.optimality_residual(st, m), OPS[f"{tag}_first_order"]) < 1e-13
+    assert Kraw.nnz == OPS[f"{tag}_Kuu_nnz"][0]
+
+
+def test_fb_values_match_reference():
+    assert np.allclose(mcp.fb(VI["fb_a"], VI["fb_b"]), VI["fb_phi"], rtol=0, atol=1e-15)
+    got = mcp.fb_box(VI["fbc_x"], VI["fbc_F"], VI["fbc_lo"], VI["fbc_hi"])
+    assert np.allclose(got, VI["fbc_phi"], rtol=0, atol=1e-15)
+
+
+@pytest.mark.parametrize("k", range(40))
+def test_rsls_matches_reference(k):
+    H = sp.csr_matrix(VI[f"qp{k}_H"])
+    c = VI[f"qp{k}_c"]
+    x, st = mcp.rsls(lambda x: H @ x + c, lambda x: H, VI[f"qp{k}_lo"], VI[f"qp{k}_hi"],
+                     VI[f"qp{k}_x0"], mcp.RSLSConfig(abs_tol=1e-12, max_iterations=100),
+                     jac_matvec=lambda J: (lambda v: J.T @ v))
+    assert np.max(np.abs(x - VI[f"qp{k}_x"])) < 1e-12
+    hist = VI[f"qp{k}_hist"]
+    assert len(st.residual_history) == len(hist)
+    assert np.allclose(st.residual_history, hist, rtol=1e-8, atol=1e-14)
+
+
+def test_krylov_matches_reference():
+    S = sp.csr_matrix(KR["cg_S"])
+    x, rep = krylov.pcg(S, KR["cg_b"], krylov.Jacobi(S), rtol=1e-10)
+    assert rep.iterations == KR["cg_it"][0]
+    assert rel(x, KR["cg_x"]) < 1e-12
+    assert rel(krylov.Chebyshev(S).matvec(KR["cheb_r"]), KR["cheb_z"]) < 1e-13
+    blk = krylov.Block2x2(sp.csr_matrix(KR["mr_A"]), sp.csr_matrix(KR["mr_B"]),
+                          sp.csr_matrix(KR["mr_C"]))
+    P = krylov.FieldSplit(blk, krylov.lu_solver(blk.A), krylov.lu_solver(blk.C))
+    assert rel(P.matvec(KR["fs_r"]), KR["fs_z"]) < 1e-12
+    xm, rm = krylov.minres(blk, KR["mr_rhs"], P, rtol=1e-10)
+    assert rm.iterations == KR["mr_it"][0]
+    assert rel(xm, KR["mr_x"]) < 1e-10
+    xm2, rm2 = krylov.minres(blk, KR["mr_rhs"], None, rtol=1e-10)
+    assert rm2.iterations == KR["mr_noprec_it"][0]
+    assert rel(xm2, KR["mr_noprec_x"]) < 1e-9
+
+
+def traction_setup(n_steps):
+    spec = MaterialSpec(E=1.0, nu=0.3, Gc=1.0, ell=0.1, k_ell=1e-6)
+    return problems.traction(spec, L=1.0, H=0.3, nx=20, ny=6, n_steps=n_steps)
+
+
+def seeded_state(setup, factor=1.4):
+    m = setup.model
+    st = am.LoadState.zeros(m)
+    t = factor * setup.params["critical_traction"]
+    setup.apply_load(m, st, t)
+    st.load = t
+    st.u[m.bc[0]] = m.bc[1]
+    st.alpha = np.maximum(st.alpha, setup.seed_alpha)
+    return st
+
+
+def test_half_steps_match_reference():
+    s = traction_setup(4)
+    st = seeded_state(s)
+    assert np.array_equal(st.u, ST["half_u0"]) and np.array_equal(st.alpha, ST["half_alpha0"])
+    cfg = am.AMConfig(outer_atol=1e-9)
+    u1, _ = am.elastic_half_step(st, s.model, cfg)
+    assert rel(u1, ST["half_u_star"]) < 1e-11
+    st.u = ST["half_u_star"].copy()
+    a1, rep = am.damage_half_step(st, s.model, cfg)
+    assert np.max(np.abs(a1 - ST["half_a_star"])) < 1e-11
+    assert rep.iterations == ST["half_vi_it"][0]
+    st.alpha = ST["half_a_star"].copy()
+    assert abs(am.optimality_norm(st, s.model) - ST["half_resnorm"][0]) < 1e-12
+
+
+def test_am_and_oram_match_reference():
+    s = traction_setup(4)
+    st = seeded_state(s)
+    rep = am.am_loop(st, s.model, am.AMConfig(outer_atol=1e-9))
+    assert rep.am_iterations == ST["am_its"][0]
+    assert np.max(np.abs(st.alpha - ST["am_alpha"])) < 1e-9
+    # the nucleation transient amplifies round-off (~10x per sweep, then contracts),
+    # so compare the histories at their ends, where both sides are converged
+    hist = np.array([e.total for e in rep.energy_history])
+    ref = ST["am_energy_hist"]
+    assert np.allclose(hist[:8], ref[:8], rtol=1e-12)
+    assert np.allclose(hist[-3:], ref[-3:], rtol=1e-12)
+    st3 = seeded_state(s)
+    r3 = am.am_loop(st3, s.model, am.AMConfig(outer_atol=1e-9, omega=1.6))
+    assert r3.am_iterations == ST["oram_its"][0]
+    assert abs(r3.omega_bar_min - ST["oram_wbmin"][0]) < 1e-15
+    assert np.max(np.abs(st3.alpha - ST["oram_alpha"])) < 1e-9
+
+
+def test_oram_newton_matches_reference():
+    s = traction_setup(4)
+    st = seeded_state(s)
+    rep = am.oram_newton(st, s.model, am.AMConfig(method="oram_newton", omega=1.3,
+                                                  outer_atol=1e-9))
+    assert [rep.am_iterations, rep.newton_iterations, rep.newton_attempts] == \
+        list(ST["oramn_counts"])
+    assert np.max(np.abs(st.alpha - ST["oramn_alpha"])) < 1e-9
+    assert np.allclose(np.array(s.model.energy(st.u, st.alpha)), ST["oramn_energy"], rtol=1e-10)
+
+
+def test_quasistatic_run_matches_reference():
+    s = traction_setup(8)
+    rows, st = problems.run(s, am.AMConfig(outer_atol=1e-9))
+    assert np.allclose([r.load for r in rows], ST["run_loads"], rtol=0, atol=0)
+    assert [r.stats.am_iterations for r in rows] == list(ST["run_its"])
+    E = np.array([list(r.energy) for r in rows])
+    # post-fracture elastic energy is ~1e-3 of the total, so its relative parity is
+    # governed by where each side stops inside outer_atol (SURVEY 8(c) parity floor)
+    assert np.allclose(E[:, 2], ST["run_energy"][:, 2], rtol=1e-12, atol=0)
+    assert np.allclose(E[:, 1], ST["run_energy"][:, 1], rtol=1e-10, atol=0)
+    assert np.allclose(E[:, 0], ST["run_energy"][:, 0], rtol=1e-8, atol=0)
+    assert np.max(np.abs(rows[-1].alpha - ST["run_alpha_final"])) < 1e-8
