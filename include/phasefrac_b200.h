@@ -1,0 +1,185 @@
+/*
+ * phasefrac_b200.h -- C ABI of the B200 (sm_100a) phase-field fracture load-step library.
+ *
+ * The reference (arXiv:1511.08463 package `phasefrac`, pure Python) has no FFI; its
+ * drop-in seams are Python callables.  Each entry point below
+ * replaces one of them; the Python host package `paper_1511_08463_b200` binds them
+ * with ctypes (INTEGRATION.md shows the binding a maintainer would add to the
+ * reference).  Reference paths are relative to /root/reference/pkg/src/phasefrac.
+ *
+ * Conventions
+ *  - fp64 everywhere; all field / vector pointers are DEVICE pointers into
+ *    caller-owned (PyTorch) memory unless stated "host".
+ *  - Layout contract (mesh.py:3-10): u interleaved per vertex (d comps), vertex
+ *    (i,j) = i*(ny+1)+j; crossed centre vertices follow the corners (index
+ *    (nx+1)(ny+1) + I*ny + J); 3D vertex (i,j,k) = (i*(ny+1)+j)*(nz+1)+k.
+ *  - Every call takes a cudaStream_t (passed as void*); work is enqueued on it.
+ *    Calls that return host scalars synchronise that stream.
+ *  - Return value: PF_OK or an error code (pf_last_error gives the message).
+ *    Codes map to the reference exceptions: PF_EBREAKDOWN -> BreakdownError
+ *    (linalg.py:25), PF_ESTALL -> LinearSolverError "elastic CG stalled"
+ *    (solver.py:139-141), PF_EINNER -> InnerSolverError (linalg.py:37),
+ *    PF_EINVAL -> ValueError, PF_ECUDA -> RuntimeError.
+ *    Non-convergence of a VI / Newton solve is a report flag, not an error
+ *    (vi.py:262-264).
+ *  - One context per stream; not thread-safe (SPEC threading model).
+ */
+#ifndef PHASEFRAC_B200_H
+#define PHASEFRAC_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PF_OK 0
+#define PF_EINVAL 1
+#define PF_ECUDA 2
+#define PF_EBREAKDOWN 3
+#define PF_ESTALL 4
+#define PF_EINNER 5
+#define PF_ENOWS 6
+
+enum { PF_UNION_JACK = 0, PF_RIGHT = 1, PF_CROSSED = 2, PF_KUHN6 = 3 };
+enum { PF_PLANE_STRESS = 0, PF_PLANE_STRAIN = 1, PF_3D = 2 };
+enum { PF_AT1 = 0, PF_AT2 = 1 };
+enum { PF_BC_NONE = 0, PF_BC_ELIMINATE = 1 };          /* operator row/col treatment   */
+enum { PF_ROWS_RAW = 0, PF_ROWS_ZERO = 1, PF_ROWS_VALUE = 2 }; /* residual Dirichlet rows */
+enum { PF_PREC_JACOBI = 0, PF_PREC_GMG = 1 };
+
+/* Mesh + material descriptor (replaces Mesh/Material/Discretization construction,
+ * mesh.py:112-142, model.py:23-61, fem.py:101-145).  Geometry is implicit. */
+typedef struct pf_desc {
+    int32_t dim;       /* 2 or 3 */
+    int32_t pattern;   /* PF_UNION_JACK | PF_RIGHT | PF_CROSSED | PF_KUHN6 */
+    int32_t regime;    /* PF_PLANE_STRESS | PF_PLANE_STRAIN | PF_3D */
+    int32_t model;     /* PF_AT1 | PF_AT2 */
+    int64_t nx, ny, nz;            /* cells per direction (nz ignored in 2D) */
+    double lx, ly, lz;             /* extents */
+    double E, nu, Gc, ell, k_ell;  /* scalar material (per-cell fields override E/Gc) */
+} pf_desc;
+
+typedef struct pf_ctx pf_ctx;
+
+/* Linear solve options / report (cg_solve linalg.py:106-152 semantics:
+ * stop when ||r|| <= max(rtol*||b||, atol); maxit <= 0 -> 10*n). */
+typedef struct pf_lin_opts {
+    int32_t precond;      /* PF_PREC_JACOBI | PF_PREC_GMG */
+    int32_t warm_start;   /* 1: start from the u0 argument; 0: x0 = 0 as the reference */
+    int64_t maxit;
+    double rtol, atol;
+    int32_t check_every;  /* host convergence poll interval (iterations) */
+    int32_t gmg_levels;   /* 0 = automatic */
+    int32_t cheb_degree;  /* GMG smoother degree */
+    int32_t reserved;
+} pf_lin_opts;
+
+typedef struct pf_lin_report {
+    int64_t iterations;
+    double final_residual_norm;
+    double b_norm;
+    int32_t converged;
+    int32_t status;
+} pf_lin_report;
+
+/* Reduced-space active-set VI options / report (VIConfig vi.py:68-75, ActiveSetReport
+ * vi.py:78-86). */
+typedef struct pf_vi_opts {
+    double abs_tol;
+    int32_t max_iterations;
+    int32_t precond;        /* inner PCG preconditioner */
+    double ls_backtrack, ls_min_step, armijo;
+    double inner_rtol;      /* relative tolerance of the inactive-block PCG */
+    int64_t inner_maxit;
+    double zero_tol;        /* <= 0 -> 1e-10 (1 + |x0|_inf) as the reference */
+    double fieldsplit_rtol; /* Newton only: MINRES rtol (solver.py:64) */
+    int32_t inner_cycles;   /* Newton only: V-cycles / PCG its per inner block solve */
+    int32_t reserved;
+} pf_vi_opts;
+
+typedef struct pf_vi_report {
+    int32_t iterations;
+    int32_t converged;
+    double final_residual_norm;
+    int64_t total_krylov_iterations;
+    int32_t steepest_descent_steps;
+    int32_t linear_failures;
+    int32_t status;
+    int32_t n_history;
+    double history[64];     /* sqrt(merit) per accepted iterate (first 64) */
+} pf_vi_report;
+
+/* ---- lifecycle (fem.py:93-105) ---------------------------------------------- */
+int pf_ctx_create(const pf_desc* desc, pf_ctx** out);
+void pf_ctx_destroy(pf_ctx* ctx);
+const char* pf_last_error(const pf_ctx* ctx);       /* ctx may be NULL (creation errors) */
+/* out: [n_vertices, n_udofs, n_elements, n_cells, n_corner_vertices, dim, elems_per_cell, 0] */
+int pf_query(const pf_ctx* ctx, int64_t out[8]);
+int64_t pf_workspace_bytes(const pf_ctx* ctx);
+int pf_bind_workspace(pf_ctx* ctx, void* dev_ptr, int64_t bytes);
+
+/* ---- per-step data ------------------------------------------------------------ */
+/* Per-cell E / Gc (device, n_cells, cell index I-major); NULL -> scalar. */
+int pf_set_cell_fields(pf_ctx* ctx, const double* E_cell, const double* Gc_cell);
+/* Dirichlet data (DirichletBC fem.py:58-90): HOST sorted unique dofs + values; every dof
+ * must belong to a boundary vertex.  n = 0 clears.  Enqueued on `stream`. */
+int pf_set_dirichlet(pf_ctx* ctx, const int64_t* dofs, const double* vals, int64_t n,
+                     void* stream);
+/* Isotropic inelastic strain eps0 = e*(1,1,0) per element, given as a HOST table
+ * e[type*ny + J] for element type `type` in cell row J (2D; profile in y only, as the
+ * thermal-shock setups need, cases.py:66-80).  NULL clears. */
+int pf_set_eps0_rows(pf_ctx* ctx, const double* table, void* stream);
+
+/* ---- operators (fem.py:162-276) -------------------------------------------- */
+/* y = Kuu(alpha) x; bc_mode PF_BC_ELIMINATE applies eliminate_dirichlet (fem.py:282-294). */
+int pf_apply_Kuu(pf_ctx* ctx, const double* alpha, const double* x, double* y, int32_t bc_mode,
+                 void* stream);
+/* y = Kaa(u, alpha) x  (fem.py:266-276; AT2 adds the w'' reaction). */
+int pf_apply_Kaa(pf_ctx* ctx, const double* u, const double* alpha, const double* x, double* y,
+                 void* stream);
+/* yu = Kua xa (fem.py:246-263), ya = Kua^T xu; bc_mode PF_BC_ELIMINATE zeroes Dirichlet rows. */
+int pf_apply_Kua(pf_ctx* ctx, const double* u, const double* alpha, const double* xa, double* yu,
+                 int32_t bc_mode, void* stream);
+int pf_apply_Kau(pf_ctx* ctx, const double* u, const double* alpha, const double* xu, double* ya,
+                 int32_t bc_mode, void* stream);
+/* Fused physics pass: energies (assemble_energy fem.py:162-174), r_u (fem.py:177-189; rows
+ * per `rows`), r_alpha (fem.py:202-218), the FB optimality residual Phi (solver.py:104-118,
+ * vi.py:89-115).  Any of r_u / r_a / phi may be NULL.  out (HOST, may be NULL):
+ * [E_el, E_d, E_tot, ||r_u||^2, ||Phi_alpha||^2, ||(r_u,Phi)||, 0, 0]. */
+int pf_physics(pf_ctx* ctx, const double* u, const double* alpha, const double* alpha_lb,
+               double* r_u, double* r_a, double* phi, int32_t rows, double* out, void* stream);
+/* f = inelastic-strain load (assemble_load_u fem.py:192-199). */
+int pf_load_u(pf_ctx* ctx, const double* alpha, double* f, void* stream);
+
+/* ---- solvers (solver.py:129-241) ----------------------------------------------- */
+/* elastic_step: u_out = argmin_u E(u, alpha) with Dirichlet data; u0 = initial guess
+ * (NULL or warm_start = 0 -> zero).  u_out may alias u0. */
+int pf_elastic_solve(pf_ctx* ctx, const double* alpha, const double* u0, double* u_out,
+                     const pf_lin_opts* opts, pf_lin_report* rep, void* stream);
+/* damage_step: alpha_out = rsls solution of the box QP at fixed u (vi.py:187-264). */
+int pf_damage_solve(pf_ctx* ctx, const double* u, const double* alpha_lb, const double* alpha_in,
+                    double* alpha_out, const pf_vi_opts* opts, pf_vi_report* rep, void* stream);
+/* u_out = u_prev + omega (u_star - u_prev), then Dirichlet snap (solver.py:193-197). */
+int pf_relax_u(pf_ctx* ctx, const double* u_prev, const double* u_star, double omega,
+               double* u_out, void* stream);
+/* Over-relaxed projected damage update with midpoint backtracking and d_alpha
+ * (solver.py:202-216).  out (HOST): [omega_bar, d_alpha, halvings]. */
+int pf_relax_alpha(pf_ctx* ctx, const double* a_prev, const double* a_star,
+                   const double* alpha_lb, double omega, double* alpha_out, double* out,
+                   void* stream);
+/* u[bc] = ubar (solver.py:121-123). */
+int pf_snap_bc(pf_ctx* ctx, double* u, void* stream);
+/* coupled_newton_solve (solver.py:303-330): reduced-space active-set Newton on (u, alpha)
+ * with field-split preconditioned MINRES; writes the last merit-nonincreasing iterate. */
+int pf_newton(pf_ctx* ctx, const double* u_in, const double* alpha_in, const double* alpha_lb,
+              double* u_out, double* alpha_out, const pf_vi_opts* opts, pf_vi_report* rep,
+              void* stream);
+
+/* Counters for the bench: kernel launches issued by this context since creation. */
+int64_t pf_launch_count(const pf_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

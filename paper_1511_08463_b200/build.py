@@ -1,0 +1,34 @@
+"""Build the sm_100a shared library in-tree: paper_1511_08463_b200/libphasefrac_b200.so."""
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SRC = ["pf_core.cu", "pf_ops2d.cu", "pf_newton.cu"]
+LIB = os.path.join(HERE, "libphasefrac_b200.so")
+FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+         "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"]
+
+
+def build(verbose=False, force=False):
+    srcs = [os.path.join(HERE, "csrc", s) for s in SRC]
+    deps = srcs + [os.path.join(HERE, "csrc", "pf_internal.cuh"),
+                   os.path.join(os.path.dirname(HERE), "include", "phasefrac_b200.h")]
+    if not force and os.path.exists(LIB):
+        t = os.path.getmtime(LIB)
+        if all(os.path.getmtime(d) <= t for d in deps):
+            return LIB
+    nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+    cmd = [nvcc] + FLAGS + srcs + ["-o", LIB + ".tmp"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if verbose or r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+    if r.returncode != 0:
+        raise RuntimeError("nvcc failed building libphasefrac_b200.so")
+    os.replace(LIB + ".tmp", LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    build(verbose="-v" in sys.argv, force=True)
+    print(LIB)

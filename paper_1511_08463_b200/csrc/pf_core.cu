@@ -1,0 +1,826 @@
+// pf_core.cu -- context, workspace, vector kernels and the device solvers behind the C ABI.
+//
+// Solvers keep all scalars on the device (scal[]); the host loop only polls a done/fail flag
+// every `check_every` iterations (one 64-byte D2H read), so Krylov iterations run back to back.
+// Reference semantics:
+//   PCG       linalg.py:106-152  (stop ||r|| <= max(rtol ||b||, atol); breakdown on p'Ap<=0, r'z<=0)
+//   rsls      vi.py:187-264      (active set, projected Armijo search, steepest-descent fallback)
+//   AM pieces solver.py:129-216  (half-steps, over-relaxation with midpoint backtracking)
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+
+#include "pf_internal.cuh"
+
+namespace pf {
+
+static thread_local std::string g_create_error;
+
+int set_error(Ctx* c, int code, const std::string& msg) {
+    if (c) c->err = msg;
+    else g_create_error = msg;
+    return code;
+}
+int check_cuda(Ctx* c, cudaError_t e, const char* where) {
+    if (e == cudaSuccess) return PF_OK;
+    return set_error(c, PF_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define PF_TRY(x)                       \
+    do {                                \
+        int _rc = (x);                  \
+        if (_rc != PF_OK) return _rc;   \
+    } while (0)
+#define PF_CU(c, x, where) PF_TRY(check_cuda((c), (x), (where)))
+
+// ---- vector kernels ------------------------------------------------------------------------
+constexpr int kVecBlock = 256;
+static int vec_blocks(long long n) {
+    long long b = (n + kVecBlock - 1) / kVecBlock;
+    return (int)std::max(1LL, std::min(b, (long long)148 * 8));
+}
+
+__device__ __forceinline__ bool solver_live(const double* s) { return s[S_DONE] == 0.0 && s[S_FAIL] == 0.0; }
+
+// r = b - q ; z = dinv r ; rr, rz.  Last block: ||b||, target, convergence at iteration 0.
+__global__ void k_cg_init(long long n, const double* __restrict__ b, const double* __restrict__ q,
+                          const double* __restrict__ dinv, double* __restrict__ r, double* __restrict__ z,
+                          double* s, RedBuf rb, double rtol, double atol, double maxit, int zero_x0) {
+    double acc[2] = {0.0, 0.0};
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const double ri = b[i] - (zero_x0 ? 0.0 : q[i]);
+        const double zi = dinv[i] * ri;
+        r[i] = ri;
+        z[i] = zi;
+        acc[0] += ri * ri;
+        acc[1] += ri * zi;
+    }
+    grid_reduce<2>(acc, rb, 4, [=](double* t) {
+        const double bn = sqrt(s[S_AUX0]);
+        s[S_BNORM] = bn;
+        s[S_TARGET] = fmax(rtol * bn, atol);
+        s[S_RNORM] = sqrt(t[0]);
+        s[S_ITER] = 0.0;
+        s[S_MAXIT] = maxit;
+        s[S_DONE] = 0.0;
+        s[S_FAIL] = 0.0;
+        s[S_BETA] = 0.0;
+        s[S_RZ] = t[1];
+        if (zero_x0 && bn == 0.0) { s[S_DONE] = 2.0; return; }  // x = 0 exactly (linalg.py:119-120)
+        if (s[S_RNORM] <= s[S_TARGET]) { s[S_DONE] = 1.0; return; }
+        if (!(t[1] > 0.0)) s[S_FAIL] = 2.0;
+    });
+}
+
+// x += gamma p ; r -= gamma q ; z = dinv r ; reductions -> beta / convergence (linalg.py:137-150)
+__global__ void k_cg_update(long long n, double* __restrict__ x, double* __restrict__ r,
+                            double* __restrict__ z, const double* __restrict__ p,
+                            const double* __restrict__ q, const double* __restrict__ dinv, double* s,
+                            RedBuf rb) {
+    if (!solver_live(s)) return;
+    const double gm = s[S_GAMMA];
+    double acc[2] = {0.0, 0.0};
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        x[i] += gm * p[i];
+        const double ri = r[i] - gm * q[i];
+        r[i] = ri;
+        const double zi = dinv[i] * ri;
+        z[i] = zi;
+        acc[0] += ri * ri;
+        acc[1] += ri * zi;
+    }
+    grid_reduce<2>(acc, rb, 5, [=](double* t) {
+        const double rn = sqrt(t[0]);
+        s[S_RNORM] = rn;
+        s[S_ITER] += 1.0;
+        if (rn <= s[S_TARGET]) { s[S_DONE] = 1.0; return; }
+        if (!(t[1] > 0.0)) { s[S_FAIL] = 2.0; return; }
+        s[S_BETA] = t[1] / s[S_RZ];
+        s[S_RZ] = t[1];
+        if (s[S_ITER] >= s[S_MAXIT]) s[S_DONE] = 3.0;
+    });
+}
+
+__global__ void k_relax_u(long long nv, long long nc, int nvy, int nx, int ny, const double* __restrict__ up,
+                          const double* __restrict__ us, double om, double* __restrict__ uo,
+                          const unsigned char* __restrict__ mask, const double* __restrict__ ubar, int has_bc,
+                          int snap_only) {
+    for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < nv;
+         v += (long long)gridDim.x * blockDim.x) {
+        double2 a;
+        if (snap_only) {
+            a = reinterpret_cast<const double2*>(uo)[v];
+        } else {
+            const double2 p = reinterpret_cast<const double2*>(up)[v];
+            const double2 q = reinterpret_cast<const double2*>(us)[v];
+            a = make_double2(p.x + om * (q.x - p.x), p.y + om * (q.y - p.y));
+        }
+        if (has_bc && v < nc) {
+            const int i = (int)(v / nvy), j = (int)(v % nvy);
+            if (i == 0 || i == nx || j == 0 || j == ny) {
+                const unsigned m = mask[v];
+                if (m) {
+                    const double2 b = reinterpret_cast<const double2*>(ubar)[v];
+                    if (m & 1u) a.x = b.x;
+                    if (m & 2u) a.y = b.y;
+                }
+            }
+        }
+        reinterpret_cast<double2*>(uo)[v] = a;
+    }
+}
+
+// over-relaxed damage candidates: bit k of the OR-reduced word is set if candidate k is
+// infeasible somewhere (solver.py:202-213); k = 0..59, omega_k = (1 + omega_{k-1}) / 2.
+__global__ void k_relax_bits(long long n, const double* __restrict__ ap, const double* __restrict__ as,
+                             const double* __restrict__ lb, double omega, unsigned long long* bits) {
+    unsigned long long m = 0ull;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const double a0 = ap[i], d = as[i] - a0, l = lb[i];
+        double w = omega;
+        for (int k = 0; k < 60; ++k) {
+            if (k > 0 && w == 1.0) break;
+            const double cand = a0 + w * d;
+            if (cand < l || cand > 1.0) m |= (1ull << k);
+            w = 0.5 * (1.0 + w);
+        }
+    }
+    unsigned lo = __reduce_or_sync(PF_FULL, (unsigned)(m & 0xffffffffull));
+    unsigned hi = __reduce_or_sync(PF_FULL, (unsigned)(m >> 32));
+    if ((threadIdx.x & 31) == 0 && (lo | hi)) atomicOr(bits, ((unsigned long long)hi << 32) | lo);
+}
+
+__device__ __forceinline__ void choose_omega(double omega, unsigned long long bits, double& wb, int& kk,
+                                             bool& use_star) {
+    // first feasible k in 0..59 with (k == 0 or w_k != 1); else the unrelaxed update
+    double w = omega;
+    use_star = true;
+    wb = 1.0;
+    kk = 60;
+    if (omega == 1.0) { kk = 0; return; }
+    for (int k = 0; k < 60; ++k) {
+        if (k > 0 && w == 1.0) { kk = k; return; }
+        if (!((bits >> k) & 1ull)) { wb = w; kk = k; use_star = false; return; }
+        w = 0.5 * (1.0 + w);
+    }
+}
+
+__global__ void k_relax_apply(long long n, const double* __restrict__ ap, const double* __restrict__ as,
+                              const double* __restrict__ lb, double omega, const unsigned long long* bits,
+                              double* __restrict__ out, unsigned long long* dmax, double* s) {
+    double wb;
+    int kk;
+    bool star;
+    choose_omega(omega, bits[0], wb, kk, star);
+    double dm = 0.0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const double a0 = ap[i];
+        const double cand = star ? as[i] : a0 + wb * (as[i] - a0);
+        const double a = fmin(fmax(cand, lb[i]), 1.0);
+        out[i] = a;
+        dm = fmax(dm, fabs(a - a0));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dm = fmax(dm, __shfl_xor_sync(PF_FULL, dm, o));
+    if ((threadIdx.x & 31) == 0 && dm > 0.0) atomicMax(dmax, (unsigned long long)__double_as_longlong(dm));
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        s[S_OMEGABAR] = wb;
+        s[S_AUX1] = (double)kk;
+    }
+}
+
+// x = clip(x0, lb, 1) and max|x| (vi.py:197-201)
+__global__ void k_clip_max(long long n, const double* __restrict__ x0, const double* __restrict__ lb,
+                           double* __restrict__ x, unsigned long long* xmax) {
+    double m = 0.0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const double v = fmin(fmax(x0[i], lb[i]), 1.0);
+        x[i] = v;
+        m = fmax(m, fabs(v));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(PF_FULL, m, o));
+    if ((threadIdx.x & 31) == 0 && m > 0.0) atomicMax(xmax, (unsigned long long)__double_as_longlong(m));
+}
+
+// activity classification (vi.py:127-141) + masked right-hand side rhs = F on N, 0 on A.
+__global__ void k_classify(long long n, const double* __restrict__ x, const double* __restrict__ F,
+                           const double* __restrict__ lb, unsigned char* __restrict__ act,
+                           double* __restrict__ rhs, double* s, RedBuf rb) {
+    const double zeta = s[S_ZETA];
+    double acc[2] = {0.0, 0.0};
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const double xv = x[i], Fv = F[i];
+        const bool lo = (xv - lb[i] <= zeta) && (Fv > 0.0);
+        const bool up = (1.0 - xv <= zeta) && (Fv < 0.0) && !lo;
+        const bool a = lo || up;
+        act[i] = lo ? 1 : (up ? 2 : 0);
+        rhs[i] = a ? 0.0 : Fv;
+        acc[0] += a ? 0.0 : 1.0;
+        acc[1] += a ? 0.0 : Fv * Fv;
+    }
+    grid_reduce<2>(acc, rb, 6, [=](double* t) {
+        s[S_NINACT] = t[0];
+        s[S_AUX0] = t[1];  // |rhs|^2 for the inner PCG stopping rule
+    });
+}
+
+__global__ void k_scale(long long n, double* __restrict__ x, double a) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        x[i] *= a;
+}
+
+// merit-gradient ingredients for the two-sided box (vi.py:144-178): p, q partials and w = q*phi.
+__device__ __forceinline__ void fb_part(double a, double b, double& pa, double& pb) {
+    const double rho = hypot(a, b);
+    if (rho > 0.0) { pa = a / rho - 1.0; pb = b / rho - 1.0; }
+    else { pa = 0.70710678118654752440 - 1.0; pb = pa; }
+}
+__global__ void k_merit_parts(long long n, const double* __restrict__ x, const double* __restrict__ F,
+                              const double* __restrict__ lb, double* __restrict__ pphi,
+                              double* __restrict__ w) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const double xv = x[i], Fv = F[i], sl = 1.0 - xv;
+        const double inner = hypot(sl, -Fv) - sl + Fv;
+        double pao, pbo, pai, pbi;
+        fb_part(xv - lb[i], inner, pao, pbo);
+        fb_part(sl, -Fv, pai, pbi);
+        const double ph = hypot(xv - lb[i], inner) - (xv - lb[i]) - inner;
+        const double p = pao - pbo * pai;
+        const double q = -pbo * pbi;
+        pphi[i] = p * ph;
+        w[i] = q * ph;
+    }
+}
+// g = 2 (p phi + Kaa w) in place on kw; reduces |g|^2
+__global__ void k_grad_finish(long long n, const double* __restrict__ pphi, double* __restrict__ kw,
+                              double* s, RedBuf rb) {
+    double acc[1] = {0.0};
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const double gv = 2.0 * (pphi[i] + kw[i]);
+        kw[i] = gv;
+        acc[0] += gv * gv;
+    }
+    grid_reduce<1>(acc, rb, 7, [=](double* t) { s[S_GNORM2] = t[0]; });
+}
+
+// ---- host helpers ---------------------------------------------------------------------------
+static int read_scal(Ctx* c, cudaStream_t st, int first, int count) {
+    PF_CU(c, cudaMemcpyAsync(c->h_scal + first, c->scal + first, sizeof(double) * count,
+                             cudaMemcpyDeviceToHost, st), "scalar readback");
+    PF_CU(c, cudaStreamSynchronize(st), "stream sync");
+    return PF_OK;
+}
+static int set_scal(Ctx* c, cudaStream_t st, int slot, double v) {
+    c->h_scal[64 + (slot & 63)] = v;
+    // small synchronous-ordered upload via cudaMemcpyAsync from pinned memory
+    PF_CU(c, cudaMemcpyAsync(c->scal + slot, c->h_scal + 64 + (slot & 63), sizeof(double),
+                             cudaMemcpyHostToDevice, st), "scalar upload");
+    return PF_OK;
+}
+
+// ---- generic PCG on device --------------------------------------------------------------------
+// Operator kind: 0 = Kuu (alpha_ws, eliminated), 1 = Kaa masked by c->act (kappa).
+struct PcgBuffers {
+    double *x, *r, *z, *p0, *p1, *q, *dinv, *b;
+    long long n;
+};
+
+static int pcg_run(Ctx* c, int kind, const PcgBuffers& B, const double* coef, const unsigned char* act,
+                   double rtol, double atol, long long maxit, int zero_x0, int check_every,
+                   pf_lin_report* rep, cudaStream_t st) {
+    const RedBuf rb{c->partials, c->tickets, c->scal};
+    const int vb = vec_blocks(B.n);
+    // q = A x0 (if warm)
+    if (!zero_x0) {
+        if (kind == 0) PF_TRY(launch_Kuu(c, coef, B.x, B.q, PF_BC_ELIMINATE, st));
+        else PF_TRY(launch_Kaa(c, coef, B.x, B.q, act, st));
+    } else {
+        PF_CU(c, cudaMemsetAsync(B.x, 0, sizeof(double) * B.n, st), "memset");
+    }
+    k_cg_init<<<vb, kVecBlock, 0, st>>>(B.n, B.b, B.q, B.dinv, B.r, B.z, c->scal, rb, rtol, atol,
+                                        (double)maxit, zero_x0);
+    c->launches++;
+    PF_CU(c, cudaGetLastError(), "cg init");
+    PF_TRY(read_scal(c, st, 0, 24));
+    long long k = 0;
+    int batch = std::max(1, check_every);
+    while (c->h_scal[S_DONE] == 0.0 && c->h_scal[S_FAIL] == 0.0) {
+        for (int t = 0; t < batch; ++t, ++k) {
+            double* pin = (k & 1) ? B.p1 : B.p0;
+            double* pout = (k & 1) ? B.p0 : B.p1;
+            if (kind == 0) PF_TRY(launch_Kuu_cgA(c, coef, B.z, pin, pout, B.q, st));
+            else PF_TRY(launch_Kaa_cgA(c, coef, B.z, pin, pout, B.q, act, st));
+            k_cg_update<<<vb, kVecBlock, 0, st>>>(B.n, B.x, B.r, B.z, pout, B.q, B.dinv, c->scal, rb);
+            c->launches++;
+        }
+        PF_CU(c, cudaGetLastError(), "cg iteration");
+        PF_TRY(read_scal(c, st, 0, 24));
+        batch = std::min(batch * 2, 64);
+    }
+    rep->iterations = (long long)c->h_scal[S_ITER];
+    rep->final_residual_norm = c->h_scal[S_RNORM];
+    rep->b_norm = c->h_scal[S_BNORM];
+    rep->converged = (c->h_scal[S_FAIL] == 0.0) && (c->h_scal[S_RNORM] <= c->h_scal[S_TARGET] ||
+                                                    c->h_scal[S_DONE] == 2.0);
+    rep->status = PF_OK;
+    if (c->h_scal[S_DONE] == 2.0) {
+        PF_CU(c, cudaMemsetAsync(B.x, 0, sizeof(double) * B.n, st), "memset");
+        rep->iterations = 0;
+        rep->final_residual_norm = 0.0;
+    }
+    if (c->h_scal[S_FAIL] != 0.0) {
+        char msg[160];
+        if (c->h_scal[S_FAIL] == 1.0)
+            snprintf(msg, sizeof msg, "cg: p'Ap = %.3e <= 0 at iteration %lld (operator not positive definite)",
+                     c->h_scal[S_PAP], (long long)c->h_scal[S_ITER] + 1);
+        else
+            snprintf(msg, sizeof msg, "cg: preconditioner not SPD at iteration %lld",
+                     (long long)c->h_scal[S_ITER]);
+        rep->status = PF_EBREAKDOWN;
+        return set_error(c, PF_EBREAKDOWN, msg);
+    }
+    return PF_OK;
+}
+
+int elastic_solve(Ctx* c, const double* alpha, const double* u0, double* u_out, const pf_lin_opts* o,
+                  pf_lin_report* rep, cudaStream_t st) {
+    if (o->precond != PF_PREC_JACOBI)
+        return set_error(c, PF_EINVAL, "elastic solve: only PF_PREC_JACOBI is built in this version");
+    PF_CU(c, cudaMemcpyAsync(c->alpha_ws, alpha, sizeof(double) * c->n_a, cudaMemcpyDeviceToDevice, st),
+          "alpha copy");
+    PcgBuffers B{c->cg_x, c->cg_r, c->cg_z, c->cg_p0, c->cg_p1, c->cg_q, c->cg_dinv, c->cg_b, c->n_u};
+    PF_TRY(launch_Kuu_diag(c, c->alpha_ws, B.dinv, st));
+    PF_TRY(launch_load(c, c->alpha_ws, B.b, nullptr, 1, st));   // b = M(f - K g) + (I-M) ubar
+    const int warm = (o->warm_start && u0) ? 1 : 0;
+    if (warm)
+        PF_CU(c, cudaMemcpyAsync(B.x, u0, sizeof(double) * c->n_u, cudaMemcpyDeviceToDevice, st), "u0 copy");
+    const long long maxit = o->maxit > 0 ? o->maxit : 10 * c->n_u;
+    int rc = pcg_run(c, 0, B, c->alpha_ws, nullptr, o->rtol, o->atol, maxit, warm ? 0 : 1,
+                     o->check_every > 0 ? o->check_every : 8, rep, st);
+    if (rc != PF_OK) return rc;
+    PF_CU(c, cudaMemcpyAsync(u_out, B.x, sizeof(double) * c->n_u, cudaMemcpyDeviceToDevice, st), "u copy");
+    if (!rep->converged) {
+        char msg[128];
+        snprintf(msg, sizeof msg, "elastic CG stalled at residual %.3e", rep->final_residual_norm);
+        rep->status = PF_ESTALL;
+        return set_error(c, PF_ESTALL, msg);
+    }
+    return PF_OK;
+}
+
+// ---- damage VI: rsls on the box QP F(a) = Kaa a + c, lb <= a <= 1 (vi.py:187-264) --------------
+int damage_solve(Ctx* c, const double* u, const double* lb, const double* a_in, double* a_out,
+                 const pf_vi_opts* o, pf_vi_report* rep, cudaStream_t st) {
+    const long long n = c->n_a;
+    const int vb = vec_blocks(n);
+    const RedBuf rb{c->partials, c->tickets, c->scal};
+    memset(rep, 0, sizeof(*rep));
+    // element reaction coefficients + affine remainder (solver.py:152-153)
+    PF_TRY(launch_kappa(c, u, a_in, c->kappa, c->vi_c, st));
+    // x = clip(a_in), zeta
+    PF_CU(c, cudaMemsetAsync(c->bits, 0, sizeof(unsigned long long) * 8, st), "memset bits");
+    k_clip_max<<<vb, kVecBlock, 0, st>>>(n, a_in, lb, c->vi_x, c->bits + 1);
+    c->launches++;
+    PF_CU(c, cudaMemcpyAsync(c->h_scal + 100, c->bits + 1, sizeof(double), cudaMemcpyDeviceToHost, st),
+          "xmax");
+    PF_CU(c, cudaStreamSynchronize(st), "sync");
+    double xmax;
+    memcpy(&xmax, c->h_scal + 100, sizeof(double));
+    const double zeta = o->zero_tol > 0.0 ? o->zero_tol : 1e-10 * (1.0 + xmax);
+    PF_TRY(set_scal(c, st, S_ZETA, zeta));
+    double *x = c->vi_x, *F = c->vi_F, *tx = c->vi_tx, *tF = c->vi_tF;
+    PF_TRY(launch_Kaa_trial(c, c->kappa, c->vi_c, x, nullptr, lb, tx, F, nullptr, S_MERIT, st));
+    PF_TRY(read_scal(c, st, 0, 24));
+    double merit = c->h_scal[S_MERIT];
+    auto push_hist = [&](double m) {
+        if (rep->n_history < 64) rep->history[rep->n_history] = std::sqrt(m);
+        rep->n_history++;
+    };
+    push_hist(merit);
+    PcgBuffers B{c->da_x, c->da_r, c->da_z, c->da_p0, c->da_p1, c->da_q, c->da_dinv, c->vi_d, n};
+    auto line_search = [&](const double* dir, double bound0, double slope, bool newton, bool& ok) -> int {
+        double mu = 1.0;
+        ok = false;
+        while (mu >= o->ls_min_step) {
+            PF_TRY(set_scal(c, st, S_MU, mu));
+            PF_TRY(launch_Kaa_trial(c, c->kappa, c->vi_c, x, dir, lb, tx, tF, nullptr, S_TMERIT, st));
+            PF_TRY(read_scal(c, st, S_TMERIT, 1));
+            const double mt = c->h_scal[S_TMERIT];
+            const double bound = newton ? (1.0 - 2.0 * o->armijo * mu) * bound0 : bound0 - slope * mu;
+            if (mt <= bound) {
+                ok = true;
+                merit = mt;
+                std::swap(x, tx);
+                std::swap(F, tF);
+                return PF_OK;
+            }
+            mu *= o->ls_backtrack;
+        }
+        return PF_OK;
+    };
+    for (int it = 1; it <= o->max_iterations; ++it) {
+        if (std::sqrt(merit) <= o->abs_tol) break;
+        rep->iterations = it;
+        k_classify<<<vb, kVecBlock, 0, st>>>(n, x, F, lb, c->act, c->vi_d, c->scal, rb);
+        c->launches++;
+        PF_TRY(read_scal(c, st, S_NINACT, 1));
+        bool ok = false;
+        if (c->h_scal[S_NINACT] > 0.0) {
+            PF_TRY(launch_Kaa_diag(c, c->kappa, B.dinv, c->act, st));
+            pf_lin_report lr{};
+            int rc;
+            const long long maxit = o->inner_maxit > 0 ? o->inner_maxit : 10 * n;
+            rc = pcg_run(c, 1, B, c->kappa, c->act, o->inner_rtol, 0.0, maxit, 1, 8, &lr, st);
+            rep->total_krylov_iterations += lr.iterations;
+            if (rc == PF_EBREAKDOWN) {
+                rep->linear_failures++;
+            } else if (rc != PF_OK) {
+                return rc;
+            } else {
+                k_scale<<<vb, kVecBlock, 0, st>>>(n, B.x, -1.0);  // d = -d_N
+                c->launches++;
+                PF_TRY(line_search(B.x, merit, 0.0, true, ok));
+            }
+        }
+        if (!ok) {
+            // steepest descent on the merit (vi.py:241-252); Kaa is symmetric (J^T = J)
+            k_merit_parts<<<vb, kVecBlock, 0, st>>>(n, x, F, lb, c->vi_g, c->vi_w);
+            c->launches++;
+            PF_TRY(launch_Kaa(c, c->kappa, c->vi_w, B.r, nullptr, st));
+            k_grad_finish<<<vb, kVecBlock, 0, st>>>(n, c->vi_g, B.r, c->scal, rb);
+            c->launches++;
+            PF_TRY(read_scal(c, st, S_GNORM2, 1));
+            const double gn = std::sqrt(c->h_scal[S_GNORM2]);
+            if (gn > 0.0) {
+                const double sc = 1.0 / std::max(1.0, gn);
+                k_scale<<<vb, kVecBlock, 0, st>>>(n, B.r, -sc);
+                c->launches++;
+                PF_TRY(line_search(B.r, merit, o->armijo * sc * gn * gn, false, ok));
+                rep->steepest_descent_steps++;
+            }
+        }
+        if (!ok) break;
+        push_hist(merit);
+    }
+    rep->final_residual_norm = std::sqrt(merit);
+    rep->converged = rep->final_residual_norm <= o->abs_tol;
+    PF_CU(c, cudaMemcpyAsync(a_out, x, sizeof(double) * n, cudaMemcpyDeviceToDevice, st), "alpha out");
+    PF_CU(c, cudaStreamSynchronize(st), "sync");
+    return PF_OK;
+}
+
+}  // namespace pf
+
+// =====================================================================================================
+// C ABI
+// =====================================================================================================
+using namespace pf;
+
+struct pf_ctx : public Ctx {};
+
+static void geometry_2d(Ctx* c) {
+    Geo2& g = c->g;
+    const pf_desc& d = c->d;
+    g.nx = (int)d.nx;
+    g.ny = (int)d.ny;
+    g.nvy = g.ny + 1;
+    g.pattern = d.pattern;
+    g.npc = d.pattern == PF_CROSSED ? 4 : 2;
+    g.nc = (long long)(g.nx + 1) * g.nvy;
+    g.ncell = (long long)g.nx * g.ny;
+    g.nv = g.nc + (d.pattern == PF_CROSSED ? g.ncell : 0);
+    g.hx = d.lx / g.nx;
+    g.hy = d.ly / g.ny;
+    const double P[5][2] = {{0, 0}, {g.hx, 0}, {0, g.hy}, {g.hx, g.hy}, {0.5 * g.hx, 0.5 * g.hy}};
+    int L[4][3];
+    if (d.pattern == PF_UNION_JACK) {
+        const int t[4][3] = {{0, 1, 3}, {0, 3, 2}, {0, 1, 2}, {1, 3, 2}};
+        memcpy(L, t, sizeof t);
+    } else if (d.pattern == PF_RIGHT) {
+        const int t[4][3] = {{0, 1, 3}, {0, 3, 2}, {0, 1, 3}, {0, 3, 2}};
+        memcpy(L, t, sizeof t);
+    } else {
+        const int t[4][3] = {{0, 1, 4}, {1, 3, 4}, {3, 2, 4}, {2, 0, 4}};
+        memcpy(L, t, sizeof t);
+    }
+    for (int t = 0; t < 4; ++t) {
+        const double* p1 = P[L[t][0]];
+        const double* p2 = P[L[t][1]];
+        const double* p3 = P[L[t][2]];
+        const double det = (p2[0] - p1[0]) * (p3[1] - p1[1]) - (p2[1] - p1[1]) * (p3[0] - p1[0]);
+        g.area[t] = 0.5 * det;
+        g.gb[t][0] = (p2[1] - p3[1]) / det;
+        g.gb[t][1] = (p3[1] - p1[1]) / det;
+        g.gb[t][2] = (p1[1] - p2[1]) / det;
+        g.gc[t][0] = (p3[0] - p2[0]) / det;
+        g.gc[t][1] = (p1[0] - p3[0]) / det;
+        g.gc[t][2] = (p2[0] - p1[0]) / det;
+    }
+    const double nu = d.nu;
+    if (d.regime == PF_PLANE_STRESS) {
+        const double s = 1.0 / (1.0 - nu * nu);
+        g.D00 = s; g.D01 = s * nu; g.D11 = s; g.D22 = s * 0.5 * (1.0 - nu);
+    } else {
+        const double s = 1.0 / ((1.0 + nu) * (1.0 - 2.0 * nu));
+        g.D00 = s * (1.0 - nu); g.D01 = s * nu; g.D11 = s * (1.0 - nu); g.D22 = s * 0.5 * (1.0 - 2.0 * nu);
+    }
+    g.E = d.E;
+    g.kell = d.k_ell;
+    g.Gc = d.Gc;
+    g.ell = d.ell;
+    g.at2 = d.model == PF_AT2;
+    g.cw = g.at2 ? 2.0 : 8.0 / 3.0;
+    g.E_cell = nullptr;
+    g.Gc_cell = nullptr;
+    g.eps0 = nullptr;
+    g.has_bc = 0;
+    g.nwj = (g.nvy + kLanesOut - 1) / kLanesOut;
+    const long long rows = g.nx + 1;
+    const long long target_warps = 148LL * 24;
+    long long S = (rows * g.nwj + target_warps - 1) / target_warps;
+    S = std::max(8LL, std::min(64LL, S));
+    g.S = (int)S;
+    g.nstrips = (int)((rows + S - 1) / S);
+}
+
+static void plan_workspace(Ctx* c) {
+    c->layout.clear();
+    auto add = [&](void** p, size_t bytes) { c->layout.push_back({p, (bytes + 255) & ~size_t(255)}); };
+    const size_t U = sizeof(double) * c->n_u, A = sizeof(double) * c->n_a;
+    double** uvecs[] = {&c->cg_x, &c->cg_r, &c->cg_z, &c->cg_p0, &c->cg_p1, &c->cg_q, &c->cg_dinv, &c->cg_b,
+                        &c->u_ws, &c->ubar};
+    for (auto p : uvecs) add((void**)p, U);
+    double** avecs[] = {&c->da_x, &c->da_r, &c->da_z, &c->da_p0, &c->da_p1, &c->da_q, &c->da_dinv,
+                        &c->vi_x, &c->vi_F, &c->vi_c, &c->vi_d, &c->vi_tx, &c->vi_tF, &c->vi_g, &c->vi_w,
+                        &c->alpha_ws};
+    for (auto p : avecs) add((void**)p, A);
+    add((void**)&c->kappa, sizeof(double) * c->n_el);
+    add((void**)&c->bcmask, c->n_a);
+    add((void**)&c->act, c->n_a);
+    add((void**)&c->eps0_tab, sizeof(double) * 4 * (c->d.ny + 1));
+    add((void**)&c->partials, sizeof(double) * kMaxRed * kMaxBlocksRed);
+    add((void**)&c->scal, sizeof(double) * S_COUNT);
+    add((void**)&c->tickets, sizeof(unsigned) * 64);
+    add((void**)&c->bits, sizeof(unsigned long long) * 8);
+    c->n_newton_vec = c->n_u + c->n_a;
+    add((void**)&c->newton, sizeof(double) * c->n_newton_vec * 16);
+    size_t tot = 0;
+    for (auto& e : c->layout) tot += e.second;
+    c->ws_bytes = tot;
+}
+
+extern "C" {
+
+int pf_ctx_create(const pf_desc* desc, pf_ctx** out) {
+    if (!desc || !out) return set_error(nullptr, PF_EINVAL, "null argument");
+    *out = nullptr;
+    if (desc->dim != 2) return set_error(nullptr, PF_EINVAL, "only dim = 2 is built in this version");
+    if (desc->pattern < 0 || desc->pattern > 2)
+        return set_error(nullptr, PF_EINVAL, "2D pattern must be union_jack, right or crossed");
+    if (desc->nx < 1 || desc->ny < 1 || desc->ny > (1 << 30) || desc->nx > (1 << 30))
+        return set_error(nullptr, PF_EINVAL, "bad grid size");
+    if (!(desc->E > 0 && desc->Gc > 0 && desc->ell > 0 && desc->lx > 0 && desc->ly > 0))
+        return set_error(nullptr, PF_EINVAL, "E, Gc, ell and extents must be positive");
+    if (!(desc->nu > -1.0 && desc->nu < 0.5)) return set_error(nullptr, PF_EINVAL, "nu out of (-1, 0.5)");
+    if (desc->regime != PF_PLANE_STRESS && desc->regime != PF_PLANE_STRAIN)
+        return set_error(nullptr, PF_EINVAL, "2D regime must be plane stress or plane strain");
+    if (desc->model != PF_AT1 && desc->model != PF_AT2) return set_error(nullptr, PF_EINVAL, "unknown model");
+    pf_ctx* c = new pf_ctx();
+    c->d = *desc;
+    c->dim = 2;
+    c->dof = 2;
+    geometry_2d(c);
+    c->n_a = c->g.nv;
+    c->n_u = 2 * c->g.nv;
+    c->n_el = c->g.ncell * c->g.npc;
+    plan_workspace(c);
+    if (cudaHostAlloc((void**)&c->h_scal, sizeof(double) * 256, cudaHostAllocDefault) != cudaSuccess) {
+        delete c;
+        return set_error(nullptr, PF_ECUDA, "cudaHostAlloc failed (is a CUDA device present?)");
+    }
+    *out = c;
+    return PF_OK;
+}
+
+void pf_ctx_destroy(pf_ctx* c) {
+    if (!c) return;
+    if (c->h_scal) cudaFreeHost(c->h_scal);
+    delete c;
+}
+
+const char* pf_last_error(const pf_ctx* c) { return c ? c->err.c_str() : g_create_error.c_str(); }
+
+int pf_query(const pf_ctx* c, int64_t out[8]) {
+    if (!c || !out) return PF_EINVAL;
+    out[0] = c->n_a;
+    out[1] = c->n_u;
+    out[2] = c->n_el;
+    out[3] = c->g.ncell;
+    out[4] = c->g.nc;
+    out[5] = c->dim;
+    out[6] = c->g.npc;
+    out[7] = c->g.S;
+    return PF_OK;
+}
+
+int64_t pf_workspace_bytes(const pf_ctx* c) { return c ? (int64_t)c->ws_bytes : -1; }
+
+int pf_bind_workspace(pf_ctx* c, void* p, int64_t bytes) {
+    if (!c || !p) return PF_EINVAL;
+    if ((size_t)bytes < c->ws_bytes) return set_error(c, PF_ENOWS, "workspace too small");
+    if (((uintptr_t)p & 255) != 0) return set_error(c, PF_EINVAL, "workspace must be 256-byte aligned");
+    char* base = (char*)p;
+    size_t off = 0;
+    for (auto& e : c->layout) {
+        *e.first = base + off;
+        off += e.second;
+    }
+    c->ws = base;
+    c->bound = 1;
+    // zero scalars / tickets / bits / masks (synchronous; binding is a setup step)
+    if (cudaMemset(c->scal, 0, sizeof(double) * S_COUNT) != cudaSuccess ||
+        cudaMemset(c->tickets, 0, sizeof(unsigned) * 64) != cudaSuccess ||
+        cudaMemset(c->bits, 0, sizeof(unsigned long long) * 8) != cudaSuccess ||
+        cudaMemset(c->bcmask, 0, c->n_a) != cudaSuccess || cudaMemset(c->act, 0, c->n_a) != cudaSuccess ||
+        cudaMemset(c->ubar, 0, sizeof(double) * c->n_u) != cudaSuccess ||
+        cudaMemset(c->cg_p0, 0, sizeof(double) * c->n_u) != cudaSuccess ||
+        cudaMemset(c->da_p0, 0, sizeof(double) * c->n_a) != cudaSuccess ||
+        cudaDeviceSynchronize() != cudaSuccess)
+        return set_error(c, PF_ECUDA, "workspace initialisation failed");
+    c->g.bcmask = c->bcmask;
+    c->g.ubar = c->ubar;
+    return PF_OK;
+}
+
+#define NEED_WS(c)                                                                 \
+    do {                                                                           \
+        if (!(c)) return PF_EINVAL;                                                \
+        if (!(c)->bound) return set_error((c), PF_ENOWS, "workspace not bound");   \
+    } while (0)
+
+int pf_set_cell_fields(pf_ctx* c, const double* E_cell, const double* Gc_cell) {
+    if (!c) return PF_EINVAL;
+    c->g.E_cell = E_cell;
+    c->g.Gc_cell = Gc_cell;
+    return PF_OK;
+}
+
+int pf_set_dirichlet(pf_ctx* c, const int64_t* dofs, const double* vals, int64_t n, void* stream) {
+    NEED_WS(c);
+    cudaStream_t st = (cudaStream_t)stream;
+    const Geo2& g = c->g;
+    std::vector<unsigned char> mask(g.nc, 0);
+    std::vector<double> ub(2 * g.nc, 0.0);
+    for (int64_t k = 0; k < n; ++k) {
+        const int64_t dof = dofs[k];
+        if (dof < 0 || dof >= 2 * g.nc) return set_error(c, PF_EINVAL, "Dirichlet dof out of range");
+        const int64_t v = dof / 2;
+        const int comp = (int)(dof % 2);
+        const int i = (int)(v / g.nvy), j = (int)(v % g.nvy);
+        if (!(i == 0 || i == g.nx || j == 0 || j == g.ny))
+            return set_error(c, PF_EINVAL, "Dirichlet dofs must lie on boundary vertices");
+        mask[v] |= (unsigned char)(1u << comp);
+        ub[dof] = vals[k];
+    }
+    PF_CU(c, cudaMemcpyAsync(c->bcmask, mask.data(), g.nc, cudaMemcpyHostToDevice, st), "bc mask");
+    PF_CU(c, cudaMemcpyAsync(c->ubar, ub.data(), sizeof(double) * 2 * g.nc, cudaMemcpyHostToDevice, st),
+          "ubar");
+    PF_CU(c, cudaStreamSynchronize(st), "sync");
+    c->g.has_bc = n > 0;
+    return PF_OK;
+}
+
+int pf_set_eps0_rows(pf_ctx* c, const double* table, void* stream) {
+    NEED_WS(c);
+    if (!table) {
+        c->g.eps0 = nullptr;
+        return PF_OK;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    PF_CU(c, cudaMemcpyAsync(c->eps0_tab, table, sizeof(double) * 4 * c->g.ny, cudaMemcpyHostToDevice, st),
+          "eps0 table");
+    PF_CU(c, cudaStreamSynchronize(st), "sync");
+    c->g.eps0 = c->eps0_tab;
+    return PF_OK;
+}
+
+int pf_apply_Kuu(pf_ctx* c, const double* alpha, const double* x, double* y, int32_t bc_mode, void* s) {
+    NEED_WS(c);
+    return launch_Kuu(c, alpha, x, y, bc_mode, (cudaStream_t)s);
+}
+int pf_apply_Kaa(pf_ctx* c, const double* u, const double* alpha, const double* x, double* y, void* s) {
+    NEED_WS(c);
+    cudaStream_t st = (cudaStream_t)s;
+    PF_TRY(launch_kappa(c, u, alpha, c->kappa, c->vi_c, st));
+    return launch_Kaa(c, c->kappa, x, y, nullptr, st);
+}
+int pf_apply_Kua(pf_ctx* c, const double* u, const double* alpha, const double* xa, double* yu, int32_t bc,
+                 void* s) {
+    NEED_WS(c);
+    return launch_Kua(c, u, alpha, xa, yu, bc, (cudaStream_t)s);
+}
+int pf_apply_Kau(pf_ctx* c, const double* u, const double* alpha, const double* xu, double* ya, int32_t bc,
+                 void* s) {
+    NEED_WS(c);
+    return launch_Kau(c, u, alpha, xu, ya, bc, (cudaStream_t)s);
+}
+int pf_physics(pf_ctx* c, const double* u, const double* alpha, const double* lb, double* ru, double* ra,
+               double* phi, int32_t rows, double* out, void* s) {
+    NEED_WS(c);
+    cudaStream_t st = (cudaStream_t)s;
+    PF_TRY(launch_physics(c, u, alpha, lb, ru, ra, phi, rows, st));
+    if (out) {
+        PF_TRY(read_scal(c, st, S_PHYS0, 4));
+        const double* h = c->h_scal + S_PHYS0;
+        out[0] = h[0];
+        out[1] = h[1];
+        out[2] = h[0] + h[1];
+        out[3] = h[2];
+        out[4] = h[3];
+        out[5] = std::sqrt(h[2] + h[3]);
+        out[6] = 0.0;
+        out[7] = 0.0;
+    }
+    return PF_OK;
+}
+int pf_load_u(pf_ctx* c, const double* alpha, double* f, void* s) {
+    NEED_WS(c);
+    return launch_load(c, alpha, f, nullptr, 0, (cudaStream_t)s);
+}
+int pf_elastic_solve(pf_ctx* c, const double* alpha, const double* u0, double* u_out, const pf_lin_opts* o,
+                     pf_lin_report* rep, void* s) {
+    NEED_WS(c);
+    if (!o || !rep) return set_error(c, PF_EINVAL, "null options/report");
+    return elastic_solve(c, alpha, u0, u_out, o, rep, (cudaStream_t)s);
+}
+int pf_damage_solve(pf_ctx* c, const double* u, const double* lb, const double* a_in, double* a_out,
+                    const pf_vi_opts* o, pf_vi_report* rep, void* s) {
+    NEED_WS(c);
+    if (!o || !rep) return set_error(c, PF_EINVAL, "null options/report");
+    return damage_solve(c, u, lb, a_in, a_out, o, rep, (cudaStream_t)s);
+}
+int pf_relax_u(pf_ctx* c, const double* u_prev, const double* u_star, double omega, double* u_out, void* s) {
+    NEED_WS(c);
+    const Geo2& g = c->g;
+    k_relax_u<<<vec_blocks(g.nv), kVecBlock, 0, (cudaStream_t)s>>>(g.nv, g.nc, g.nvy, g.nx, g.ny, u_prev,
+                                                                    u_star, omega, u_out, c->bcmask,
+                                                                    c->ubar, g.has_bc, 0);
+    c->launches++;
+    return check_cuda(c, cudaGetLastError(), "relax_u");
+}
+int pf_snap_bc(pf_ctx* c, double* u, void* s) {
+    NEED_WS(c);
+    const Geo2& g = c->g;
+    if (!g.has_bc) return PF_OK;
+    k_relax_u<<<vec_blocks(g.nv), kVecBlock, 0, (cudaStream_t)s>>>(g.nv, g.nc, g.nvy, g.nx, g.ny, nullptr,
+                                                                    nullptr, 0.0, u, c->bcmask, c->ubar,
+                                                                    g.has_bc, 1);
+    c->launches++;
+    return check_cuda(c, cudaGetLastError(), "snap_bc");
+}
+int pf_relax_alpha(pf_ctx* c, const double* a_prev, const double* a_star, const double* lb, double omega,
+                   double* a_out, double* out, void* s) {
+    NEED_WS(c);
+    cudaStream_t st = (cudaStream_t)s;
+    const long long n = c->n_a;
+    const int vb = vec_blocks(n);
+    PF_CU(c, cudaMemsetAsync(c->bits, 0, sizeof(unsigned long long) * 8, st), "memset");
+    if (omega != 1.0) {
+        k_relax_bits<<<vb, kVecBlock, 0, st>>>(n, a_prev, a_star, lb, omega, c->bits);
+        c->launches++;
+    }
+    k_relax_apply<<<vb, kVecBlock, 0, st>>>(n, a_prev, a_star, lb, omega, c->bits, a_out, c->bits + 1, c->scal);
+    c->launches++;
+    PF_CU(c, cudaGetLastError(), "relax_alpha");
+    if (out) {
+        PF_CU(c, cudaMemcpyAsync(c->h_scal + 100, c->bits + 1, sizeof(double), cudaMemcpyDeviceToHost, st), "d");
+        PF_TRY(read_scal(c, st, S_OMEGABAR, 1));
+        PF_TRY(read_scal(c, st, S_AUX1, 1));
+        double dmax;
+        memcpy(&dmax, c->h_scal + 100, sizeof(double));
+        out[0] = c->h_scal[S_OMEGABAR];
+        out[1] = dmax;
+        out[2] = c->h_scal[S_AUX1];
+    }
+    return PF_OK;
+}
+int pf_newton(pf_ctx* c, const double* u_in, const double* a_in, const double* lb, double* u_out,
+              double* a_out, const pf_vi_opts* o, pf_vi_report* rep, void* s) {
+    NEED_WS(c);
+    if (!o || !rep) return set_error(c, PF_EINVAL, "null options/report");
+    return newton_solve(c, u_in, a_in, lb, u_out, a_out, o, rep, (cudaStream_t)s);
+}
+int64_t pf_launch_count(const pf_ctx* c) { return c ? c->launches : -1; }
+
+}  // extern "C"

@@ -1,0 +1,210 @@
+// pf_internal.cuh -- shared internals of the sm_100a phase-field load-step library.
+//
+// Design: structured P1 meshes with implicit geometry.  Every operator is a
+// matrix-free "strip" kernel: a warp owns 30 vertex columns (j, the contiguous index) plus a
+// one-column halo and walks a strip of S vertex rows (i); vertex data of row i+1 is loaded
+// once (coalesced along j), the right neighbour column comes from the next lane by shuffle,
+// and element contributions to the next row / next column are carried in registers /
+// shuffled left->right, so every vertex value is read once from HBM and every output is
+// written once, with no atomics (deterministic).  Reductions are per-block partials summed by
+// the last block in a fixed order (bitwise reproducible run to run).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+#include <vector>
+
+#include "../../include/phasefrac_b200.h"
+
+#define PF_FULL 0xffffffffu
+
+namespace pf {
+
+constexpr int kBlock = 256;        // threads per block for strip kernels
+constexpr int kLanesOut = 30;      // output columns per warp
+constexpr int kMaxRed = 8;         // max values per fused reduction
+constexpr int kMaxBlocksRed = 8192;  // partials capacity per reduction value
+
+// ---- geometry / material descriptor passed by value to every 2D kernel ------------------
+struct Geo2 {
+    int nx, ny, nvy;          // cells, ny+1
+    int pattern, npc;         // PF_*, elements per cell
+    long long nc, ncell, nv;  // corner vertices, cells, all vertices
+    double hx, hy;
+    // element types (local nodes 0=v00 1=v10 2=v01 3=v11 4=centre)
+    double area[4];
+    double gb[4][3], gc[4][3];
+    // unit-E stiffness (Voigt e11, e22, g12)
+    double D00, D01, D11, D22;
+    double E, kell, Gc, ell, cw;
+    int at2;
+    const double* E_cell;     // nullable, per cell (I*ny + J)
+    const double* Gc_cell;    // nullable
+    const double* eps0;       // nullable, isotropic strain per (type, J): t*ny + J
+    const unsigned char* bcmask;  // per corner vertex, bit c = component c constrained
+    const double* ubar;       // n_u (values on constrained dofs)
+    int has_bc;
+    // strip decomposition
+    int nwj, S, nstrips;
+};
+
+// ---- reductions --------------------------------------------------------------------------
+struct RedBuf {
+    double* partials;      // [kMaxRed][kMaxBlocksRed]
+    unsigned int* ticket;  // one counter per reduction site
+    double* out;           // result slots
+};
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(PF_FULL, v, o);
+    return v;
+}
+
+// Block-reduce NV values, store per-block partials, and let the last block sum them in a
+// fixed order; `fin(vals)` runs on thread 0 of the last block with the grid totals.
+template <int NV, class Fin>
+__device__ __forceinline__ void grid_reduce(double (&v)[NV], const RedBuf& rb, int slot, Fin fin) {
+    __shared__ double sm[NV][32];
+    __shared__ bool s_last;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int nb = gridDim.x;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+        double t = warp_sum(v[k]);
+        if (lane == 0) sm[k][warp] = t;
+    }
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            double t = lane < nw ? sm[k][lane] : 0.0;
+            t = warp_sum(t);
+            if (lane == 0) rb.partials[(size_t)k * kMaxBlocksRed + blockIdx.x] = t;
+        }
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned int t = atomicAdd(rb.ticket + slot, 1u);
+        s_last = (t == (unsigned)nb - 1u);
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (warp == 0) {
+        double tot[NV];
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            double t = 0.0;
+            for (int b = lane; b < nb; b += 32) t += __ldcg(rb.partials + (size_t)k * kMaxBlocksRed + b);
+            tot[k] = warp_sum(t);
+        }
+        if (lane == 0) {
+            fin(tot);
+            rb.ticket[slot] = 0u;
+        }
+    }
+}
+
+// ---- device scalar block (solver state kept on device) -----------------------------------
+enum ScalarSlot {
+    S_RZ = 0, S_PAP, S_GAMMA, S_BETA, S_RR, S_BNORM, S_TARGET, S_RNORM,
+    S_ITER, S_DONE, S_FAIL, S_MAXIT, S_RZNEW, S_MU, S_MERIT, S_TMERIT,
+    S_ZETA, S_NINACT, S_XMAX, S_GNORM2, S_DALPHA, S_OMEGABAR, S_AUX0, S_AUX1,
+    S_PHYS0 = 32,  // 8 slots of physics-pass outputs
+    S_CGVEC0 = 48,
+    S_COUNT = 128
+};
+
+// ---- context -------------------------------------------------------------------------
+struct Ctx {
+    pf_desc d;
+    Geo2 g;
+    std::string err;
+    long long n_u = 0, n_a = 0, n_el = 0;
+    int dim = 2, dof = 2;
+    // workspace
+    size_t ws_bytes = 0;
+    char* ws = nullptr;
+    std::vector<std::pair<void**, size_t>> layout;
+    // named buffers (device)
+    double *cg_x, *cg_r, *cg_z, *cg_p0, *cg_p1, *cg_q, *cg_dinv, *cg_b;     // n_u
+    double *da_x, *da_r, *da_z, *da_p0, *da_p1, *da_q, *da_dinv;             // n_a (damage CG)
+    double *vi_x, *vi_F, *vi_c, *vi_d, *vi_tx, *vi_tF, *vi_g, *vi_w;          // n_a
+    double *kappa;                                                           // n_el
+    double *alpha_ws, *u_ws;                                                 // n_a, n_u
+    double *ubar;                                                            // n_u
+    unsigned char *bcmask, *act;                                             // n_a
+    double *eps0_tab;                                                        // 4*ny
+    double *partials, *scal;
+    unsigned int* tickets;
+    unsigned long long* bits;                                                // 8 words
+    double* newton;                                                          // Newton block vectors
+    long long n_newton_vec = 0;
+    // host pinned mirror of scalars
+    double* h_scal = nullptr;
+    long long launches = 0;
+    cudaStream_t cur = nullptr;
+    int has_eps0 = 0;
+    int bound = 0;
+    int blocks_per_strip_grid = 0;
+};
+
+int set_error(Ctx* c, int code, const std::string& msg);
+int check_cuda(Ctx* c, cudaError_t e, const char* where);
+
+// strip grid
+inline int strip_blocks(const Geo2& g) {
+    long long warps = (long long)g.nwj * g.nstrips;
+    return (int)((warps * 32 + kBlock - 1) / kBlock);
+}
+
+// ---- 2D operator launchers (pf_ops2d.cu) -------------------------------------------------
+struct CgScal {  // pointers into the scalar block used by fused CG kernels
+    double* s;
+};
+
+// y = K x (mode: PF_BC_*) ; if fused: p_out = z + beta p_in (beta from scal, 0 at iter 0),
+// y = K p_out and pAp reduced into scal (CG step A).
+int launch_Kuu(Ctx* c, const double* alpha, const double* x, double* y, int bcmode,
+               cudaStream_t st);
+int launch_Kuu_cgA(Ctx* c, const double* alpha, const double* z, const double* p_in,
+                   double* p_out, double* q, cudaStream_t st);
+int launch_Kuu_diag(Ctx* c, const double* alpha, double* dinv, cudaStream_t st);
+int launch_kappa(Ctx* c, const double* u, const double* alpha, double* kappa, double* cvec,
+                 cudaStream_t st);
+int launch_Kaa(Ctx* c, const double* kappa, const double* x, double* y, const unsigned char* act,
+               cudaStream_t st);
+int launch_Kaa_cgA(Ctx* c, const double* kappa, const double* z, const double* p_in,
+                   double* p_out, double* q, const unsigned char* act, cudaStream_t st);
+int launch_Kaa_diag(Ctx* c, const double* kappa, double* dinv, const unsigned char* act,
+                    cudaStream_t st);
+// F = Kaa trial + c with trial = clip(x + mu d, lb, 1) (mu from scal S_MU, or d == null ->
+// trial = x); writes trial, F, the activity mask (classification with zeta) and reduces
+// merit = |Phi|^2 into scal[slot_merit].
+int launch_Kaa_trial(Ctx* c, const double* kappa, const double* cvec, const double* x,
+                     const double* d, const double* lb, double* trial, double* F,
+                     unsigned char* act, int merit_slot, cudaStream_t st);
+int launch_physics(Ctx* c, const double* u, const double* alpha, const double* lb, double* ru,
+                   double* ra, double* phi, int rows, cudaStream_t st);
+int launch_load(Ctx* c, const double* alpha, double* f, const double* u_or_null,
+                int rows, cudaStream_t st);
+int launch_Kua(Ctx* c, const double* u, const double* alpha, const double* xa, double* yu,
+               int bcmode, cudaStream_t st);
+int launch_Kau(Ctx* c, const double* u, const double* alpha, const double* xu, double* ya,
+               int bcmode, cudaStream_t st);
+// Newton: reduced coupled Jacobian apply [Kuu_bc Kua_bc; Kau Kaa] on inactive set
+int launch_jac(Ctx* c, const double* u, const double* alpha, const double* xu, const double* xa,
+               double* yu, double* ya, const unsigned char* act, cudaStream_t st);
+
+// ---- vector kernels + solvers (pf_core.cu) ---------------------------------------------
+int elastic_solve(Ctx* c, const double* alpha, const double* u0, double* u_out,
+                  const pf_lin_opts* o, pf_lin_report* rep, cudaStream_t st);
+int damage_solve(Ctx* c, const double* u, const double* lb, const double* a_in, double* a_out,
+                 const pf_vi_opts* o, pf_vi_report* rep, cudaStream_t st);
+int newton_solve(Ctx* c, const double* u_in, const double* a_in, const double* lb, double* u_out,
+                 double* a_out, const pf_vi_opts* o, pf_vi_report* rep, cudaStream_t st);
+
+}  // namespace pf

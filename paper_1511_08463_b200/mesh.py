@@ -1,0 +1,135 @@
+"""Structured mesh descriptors (reference mesh.py).
+
+The device never sees an element list: geometry is implicit in (pattern, nx, ny,
+extents).  This module keeps the reference's layout contract (mesh.py:3-10):
+vertex (i, j) = i*(ny+1) + j, displacement interleaved per vertex, triangles
+type-major in I-major cell order; crossed centre vertices follow the corners.
+Host-side coordinates and boundary sets are produced lazily for BC setup and
+post-processing only.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+BOUNDARY_TAGS = ("left", "right", "bottom", "top")
+PATTERNS_2D = ("union_jack", "right", "crossed")
+_FIELDS = {"displacement_x1": (2, 0), "displacement_x2": (2, 1), "damage": (1, 0)}
+
+
+@dataclass
+class StructuredMesh:
+    """Structured triangulation of [x0, x0+lx] x [y0, y0+ly] with nx x ny cells."""
+
+    nx: int
+    ny: int
+    lx: float = 1.0
+    ly: float = 1.0
+    pattern: str = "union_jack"
+    x0: float = 0.0
+    y0: float = 0.0
+    _vertices: np.ndarray | None = field(default=None, repr=False)
+
+    def __post_init__(self):
+        if self.nx < 1 or self.ny < 1:
+            raise ValueError("StructuredMesh needs nx, ny >= 1")
+        if self.pattern not in PATTERNS_2D:
+            raise ValueError(f"unknown pattern {self.pattern!r}; choose from {PATTERNS_2D}")
+        if self.lx <= 0 or self.ly <= 0:
+            raise ValueError("extents must be positive")
+
+    dim = 2
+
+    @property
+    def n_corner_vertices(self) -> int:
+        return (self.nx + 1) * (self.ny + 1)
+
+    @property
+    def n_cells(self) -> int:
+        return self.nx * self.ny
+
+    @property
+    def n_vertices(self) -> int:
+        return self.n_corner_vertices + (self.n_cells if self.pattern == "crossed" else 0)
+
+    @property
+    def n_triangles(self) -> int:
+        return self.n_cells * (4 if self.pattern == "crossed" else 2)
+
+    @property
+    def hx(self) -> float:
+        return self.lx / self.nx
+
+    @property
+    def hy(self) -> float:
+        return self.ly / self.ny
+
+    @property
+    def vertices(self) -> np.ndarray:
+        if self._vertices is None:
+            xs = np.linspace(self.x0, self.x0 + self.lx, self.nx + 1)
+            ys = np.linspace(self.y0, self.y0 + self.ly, self.ny + 1)
+            X, Y = np.meshgrid(xs, ys, indexing="ij")
+            v = np.column_stack([X.ravel(), Y.ravel()])
+            if self.pattern == "crossed":
+                I, J = np.meshgrid(np.arange(self.nx), np.arange(self.ny), indexing="ij")
+                cx = 0.5 * (xs[I.ravel()] + xs[I.ravel() + 1])
+                cy = 0.5 * (ys[J.ravel()] + ys[J.ravel() + 1])
+                v = np.vstack([v, np.column_stack([cx, cy])])
+            self._vertices = v
+        return self._vertices
+
+    def vid(self, i, j):
+        return np.asarray(i) * (self.ny + 1) + np.asarray(j)
+
+    def boundary_vertices(self, tag: str) -> np.ndarray:
+        jj = np.arange(self.ny + 1)
+        ii = np.arange(self.nx + 1)
+        if tag == "left":
+            return self.vid(0, jj)
+        if tag == "right":
+            return self.vid(self.nx, jj)
+        if tag == "bottom":
+            return self.vid(ii, 0)
+        if tag == "top":
+            return self.vid(ii, self.ny)
+        raise KeyError(f"unknown boundary tag {tag!r}; have {BOUNDARY_TAGS}")
+
+    def all_boundary_vertices(self) -> np.ndarray:
+        return np.unique(np.concatenate([self.boundary_vertices(t) for t in BOUNDARY_TAGS]))
+
+    def cell_row_centroid_y(self) -> np.ndarray:
+        """(n_types, ny) centroid heights of each element type per cell row (for eps0 tables)."""
+        ys = np.linspace(self.y0, self.y0 + self.ly, self.ny + 1)
+        y0, y1 = ys[:-1], ys[1:]
+        yc = 0.5 * (y0 + y1)
+        if self.pattern == "union_jack":
+            # even-parity types (0,1,3),(0,3,2); odd (0,1,2),(1,3,2); local y: 0,0,1,1
+            t = [(y0 + y0 + y1), (y0 + y1 + y1), (y0 + y0 + y1), (y0 + y1 + y1)]
+            return np.stack([v / 3.0 for v in t])
+        if self.pattern == "right":
+            t = [(y0 + y0 + y1), (y0 + y1 + y1)]
+            return np.stack([v / 3.0 for v in t] + [v / 3.0 for v in t])
+        t = [(y0 + y0 + yc), (y0 + y1 + yc), (y1 + y1 + yc), (y1 + y0 + yc)]
+        return np.stack([v / 3.0 for v in t])
+
+
+def rect_mesh(L: float, H: float, h: float, origin_x2: float = 0.0,
+              pattern: str = "union_jack") -> StructuredMesh:
+    """Uniform mesh of [0, L] x [origin_x2, origin_x2 + H] with target size h (mesh.py:112-142;
+    jitter is not supported on the structured device path)."""
+    if L <= 0 or H <= 0 or h <= 0:
+        raise ValueError(f"rect_mesh needs positive L, H, h; got L={L}, H={H}, h={h}")
+    nx = max(1, round(L / h))
+    ny = max(1, round(H / h))
+    return StructuredMesh(nx, ny, L, H, pattern, 0.0, origin_x2)
+
+
+def boundary_dofs(mesh: StructuredMesh, tag: str, fieldname: str) -> np.ndarray:
+    """Sorted global dof indices of ``fieldname`` on the tagged boundary (mesh.py:193-205)."""
+    if fieldname not in _FIELDS:
+        raise KeyError(f"unknown field {fieldname!r}; have {sorted(_FIELDS)}")
+    stride, offset = _FIELDS[fieldname]
+    return (stride * np.sort(mesh.boundary_vertices(tag)) + offset).astype(np.intp)
