@@ -86,7 +86,11 @@ EXPORTS = {
     "pf_newton": (C.c_int, [C.c_void_p] * 6 + [C.POINTER(VIOpts), C.POINTER(VIReport),
                                                 C.c_void_p]),
     "pf_launch_count": (C.c_int64, [C.c_void_p]),
+    "pf_profile": (C.c_int, [C.c_void_p, C.c_int32]),
+    "pf_profile_read": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
 }
+KERNEL_KINDS = ["Kuu", "Kuu_cg", "Kuu_diag", "kappa", "Kaa", "Kaa_cg", "Kaa_diag", "Kaa_trial",
+                "physics", "rhs", "Kua", "Kau", "jacobian", "cg_vec", "vec", "gmg"]
 
 _lib = None
 

@@ -27,6 +27,23 @@ int check_cuda(Ctx* c, cudaError_t e, const char* where) {
     return set_error(c, PF_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
 }
 
+int prof_begin(Ctx* c, cudaStream_t st) {
+    if (!c->prof.on) return -1;
+    const int idx = (int)c->prof.log.size();
+    while ((int)c->prof.ev.size() < 2 * (idx + 1)) {
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) return -1;
+        c->prof.ev.push_back(e);
+    }
+    cudaEventRecord(c->prof.ev[2 * idx], st);
+    return idx;
+}
+void prof_end(Ctx* c, cudaStream_t st, int slot, int kind, double bytes) {
+    if (slot < 0) return;
+    cudaEventRecord(c->prof.ev[2 * slot + 1], st);
+    c->prof.log.push_back(ProfEntry{kind, slot, bytes});
+}
+
 #define PF_TRY(x)                       \
     do {                                \
         int _rc = (x);                  \
@@ -308,8 +325,12 @@ static int pcg_run(Ctx* c, int kind, const PcgBuffers& B, const double* coef, co
     } else {
         PF_CU(c, cudaMemsetAsync(B.x, 0, sizeof(double) * B.n, st), "memset");
     }
-    k_cg_init<<<vb, kVecBlock, 0, st>>>(B.n, B.b, B.q, B.dinv, B.r, B.z, c->scal, rb, rtol, atol,
-                                        (double)maxit, zero_x0);
+    {
+        const int ps = prof_begin(c, st);
+        k_cg_init<<<vb, kVecBlock, 0, st>>>(B.n, B.b, B.q, B.dinv, B.r, B.z, c->scal, rb, rtol, atol,
+                                            (double)maxit, zero_x0);
+        prof_end(c, st, ps, K_CG_VEC, 8.0 * B.n * 5);
+    }
     c->launches++;
     PF_CU(c, cudaGetLastError(), "cg init");
     PF_TRY(read_scal(c, st, 0, 24));
@@ -321,7 +342,9 @@ static int pcg_run(Ctx* c, int kind, const PcgBuffers& B, const double* coef, co
             double* pout = (k & 1) ? B.p0 : B.p1;
             if (kind == 0) PF_TRY(launch_Kuu_cgA(c, coef, B.z, pin, pout, B.q, st));
             else PF_TRY(launch_Kaa_cgA(c, coef, B.z, pin, pout, B.q, act, st));
+            const int ps = prof_begin(c, st);
             k_cg_update<<<vb, kVecBlock, 0, st>>>(B.n, B.x, B.r, B.z, pout, B.q, B.dinv, c->scal, rb);
+            prof_end(c, st, ps, K_CG_VEC, 8.0 * B.n * 8);  // x,p,r,q,dinv -> x,r,z
             c->launches++;
         }
         PF_CU(c, cudaGetLastError(), "cg iteration");
@@ -615,6 +638,7 @@ int pf_ctx_create(const pf_desc* desc, pf_ctx** out) {
 
 void pf_ctx_destroy(pf_ctx* c) {
     if (!c) return;
+    for (auto e : c->prof.ev) cudaEventDestroy(e);
     if (c->h_scal) cudaFreeHost(c->h_scal);
     delete c;
 }
@@ -822,5 +846,34 @@ int pf_newton(pf_ctx* c, const double* u_in, const double* a_in, const double* l
     return newton_solve(c, u_in, a_in, lb, u_out, a_out, o, rep, (cudaStream_t)s);
 }
 int64_t pf_launch_count(const pf_ctx* c) { return c ? c->launches : -1; }
+
+int pf_profile(pf_ctx* c, int32_t enable) {
+    if (!c) return PF_EINVAL;
+    c->prof.on = enable;
+    return PF_OK;
+}
+
+// out[3*k + {0,1,2}] = (launches, total ms, algorithmic bytes) of kernel class k; resets.
+int pf_profile_read(pf_ctx* c, double* out, int32_t nkinds) {
+    if (!c || !out) return PF_EINVAL;
+    if (cudaDeviceSynchronize() != cudaSuccess) return set_error(c, PF_ECUDA, "sync");
+    for (auto& e : c->prof.log) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, c->prof.ev[2 * e.ev], c->prof.ev[2 * e.ev + 1]);
+        c->prof.ms[e.kind] += ms;
+        c->prof.bytes[e.kind] += e.bytes;
+        c->prof.count[e.kind] += 1;
+    }
+    c->prof.log.clear();
+    for (int k = 0; k < nkinds && k < K_NKINDS; ++k) {
+        out[3 * k] = (double)c->prof.count[k];
+        out[3 * k + 1] = c->prof.ms[k];
+        out[3 * k + 2] = c->prof.bytes[k];
+        c->prof.count[k] = 0;
+        c->prof.ms[k] = 0;
+        c->prof.bytes[k] = 0;
+    }
+    return PF_OK;
+}
 
 }  // extern "C"

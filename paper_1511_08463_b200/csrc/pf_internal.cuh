@@ -118,6 +118,21 @@ enum ScalarSlot {
     S_COUNT = 128
 };
 
+// ---- per-kernel-class profiling (CUDA events around launches; read after the timed region) --
+enum KernelKind {
+    K_KUU = 0, K_KUU_CG, K_KUU_DIAG, K_KAPPA, K_KAA, K_KAA_CG, K_KAA_DIAG, K_KAA_TRIAL, K_PHYS,
+    K_RHS, K_KUA, K_KAU, K_JAC, K_CG_VEC, K_VEC, K_GMG, K_NKINDS
+};
+struct ProfEntry { int kind; int ev; double bytes; };
+struct Prof {
+    int on = 0;
+    std::vector<cudaEvent_t> ev;   // pairs (start, stop)
+    std::vector<ProfEntry> log;
+    double ms[K_NKINDS] = {0};
+    double bytes[K_NKINDS] = {0};
+    long long count[K_NKINDS] = {0};
+};
+
 // ---- context -------------------------------------------------------------------------
 struct Ctx {
     pf_desc d;
@@ -150,7 +165,12 @@ struct Ctx {
     int has_eps0 = 0;
     int bound = 0;
     int blocks_per_strip_grid = 0;
+    Prof prof;
 };
+
+// profiling brackets (no-ops unless enabled)
+int prof_begin(Ctx* c, cudaStream_t st);
+void prof_end(Ctx* c, cudaStream_t st, int slot, int kind, double bytes);
 
 int set_error(Ctx* c, int code, const std::string& msg);
 int check_cuda(Ctx* c, cudaError_t e, const char* where);

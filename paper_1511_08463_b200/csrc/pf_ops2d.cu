@@ -984,16 +984,40 @@ struct OpJac : NoRed {
 };
 
 // ---- launch plumbing ------------------------------------------------------------------------
+// algorithmic bytes per vertex (read every input once, write every output once) by kind;
+// element arrays (kappa) are charged 8 B per element.
+static double alg_bytes(const Ctx* c, int kind, int nvec_r, int nvec_w) {
+    const double V = (double)c->g.nv, T = (double)c->n_el;
+    switch (kind) {
+        case K_KUU: return V * (16 + 8 + 16);                 // x, alpha -> y
+        case K_KUU_CG: return V * (16 + 16 + 8 + 16 + 16);    // z, p_in, alpha -> p_out, q
+        case K_KUU_DIAG: return V * (8 + 16);
+        case K_KAPPA: return V * (16 + 8) + T * 8;            // u -> c, kappa
+        case K_KAA: return V * (8 + 8) + T * 8;               // x, kappa -> y
+        case K_KAA_CG: return V * (8 + 8 + 8 + 8 + 1) + T * 8;
+        case K_KAA_DIAG: return V * 8 + T * 8;
+        case K_KAA_TRIAL: return V * (8 + 8 + 8 + 8 + 8 + 8) + T * 8;  // x, d, lb, c -> trial, F
+        case K_PHYS: return V * (16 + 8 + 8) + V * 8.0 * nvec_w;
+        case K_RHS: return V * (8 + 16);
+        case K_KUA: return V * (16 + 8 + 8 + 16);
+        case K_KAU: return V * (16 + 8 + 16 + 8);
+        case K_JAC: return V * (16 + 8 + 16 + 8 + 16 + 8);
+        default: return V * 8.0 * (nvec_r + nvec_w);
+    }
+}
+
 template <class Op>
-static int run_strip(Ctx* c, Op op, cudaStream_t st) {
+static int run_strip(Ctx* c, Op op, cudaStream_t st, int kind = K_VEC, int nw = 0) {
     const Geo2& g = c->g;
     const int nb = strip_blocks(g);
     if (nb > kMaxBlocksRed) return set_error(c, PF_EINVAL, "grid too large for reduction buffer");
+    const int slot = prof_begin(c, st);
     switch (g.pattern) {
         case PF_UNION_JACK: k_strip2d<Op, PF_UNION_JACK><<<nb, kBlock, 0, st>>>(g, op); break;
         case PF_RIGHT: k_strip2d<Op, PF_RIGHT><<<nb, kBlock, 0, st>>>(g, op); break;
         default: k_strip2d<Op, PF_CROSSED><<<nb, kBlock, 0, st>>>(g, op); break;
     }
+    prof_end(c, st, slot, kind, alg_bytes(c, kind, 0, nw));
     c->launches++;
     return check_cuda(c, cudaGetLastError(), "strip kernel launch");
 }
@@ -1002,75 +1026,76 @@ static RedBuf redbuf(Ctx* c) { return RedBuf{c->partials, c->tickets, c->scal}; 
 
 int launch_Kuu(Ctx* c, const double* alpha, const double* x, double* y, int bcmode, cudaStream_t st) {
     OpKuu<false> op{alpha, x, nullptr, nullptr, y, bcmode, c->scal, redbuf(c), 0.0};
-    return run_strip(c, op, st);
+    return run_strip(c, op, st, K_KUU);
 }
 int launch_Kuu_cgA(Ctx* c, const double* alpha, const double* z, const double* p_in, double* p_out,
                    double* q, cudaStream_t st) {
     OpKuu<true> op{alpha, z, p_in, p_out, q, PF_BC_ELIMINATE, c->scal, redbuf(c), 0.0};
-    return run_strip(c, op, st);
+    return run_strip(c, op, st, K_KUU_CG);
 }
 int launch_Kuu_diag(Ctx* c, const double* alpha, double* dinv, cudaStream_t st) {
     OpKuuDiag op;
     op.alpha = alpha;
     op.dinv = dinv;
-    return run_strip(c, op, st);
+    return run_strip(c, op, st, K_KUU_DIAG);
 }
 int launch_kappa(Ctx* c, const double* u, const double* alpha, double* kappa, double* cvec,
                  cudaStream_t st) {
     (void)alpha;
     OpKappa op;
     op.u = u; op.kappa = kappa; op.cvec = cvec;
-    return run_strip(c, op, st);
+    return run_strip(c, op, st, K_KAPPA);
 }
 int launch_Kaa(Ctx* c, const double* kappa, const double* x, double* y, const unsigned char* act,
                cudaStream_t st) {
     if (act) {
         OpKaa<false, true> op{kappa, x, nullptr, nullptr, y, act, c->scal, redbuf(c), 0.0};
-        return run_strip(c, op, st);
+        return run_strip(c, op, st, K_KAA);
     }
     OpKaa<false, false> op{kappa, x, nullptr, nullptr, y, nullptr, c->scal, redbuf(c), 0.0};
-    return run_strip(c, op, st);
+    return run_strip(c, op, st, K_KAA);
 }
 int launch_Kaa_cgA(Ctx* c, const double* kappa, const double* z, const double* p_in, double* p_out,
                    double* q, const unsigned char* act, cudaStream_t st) {
     if (act) {
         OpKaa<true, true> op{kappa, z, p_in, p_out, q, act, c->scal, redbuf(c), 0.0};
-        return run_strip(c, op, st);
+        return run_strip(c, op, st, K_KAA_CG);
     }
     OpKaa<true, false> op{kappa, z, p_in, p_out, q, nullptr, c->scal, redbuf(c), 0.0};
-    return run_strip(c, op, st);
+    return run_strip(c, op, st, K_KAA_CG);
 }
 int launch_Kaa_diag(Ctx* c, const double* kappa, double* dinv, const unsigned char* act,
                     cudaStream_t st) {
     if (act) {
         OpKaaDiag<true> op;
         op.kappa = kappa; op.dinv = dinv; op.act = act;
-        return run_strip(c, op, st);
+        return run_strip(c, op, st, K_KAA_DIAG);
     }
     OpKaaDiag<false> op;
     op.kappa = kappa; op.dinv = dinv; op.act = nullptr;
-    return run_strip(c, op, st);
+    return run_strip(c, op, st, K_KAA_DIAG);
 }
 int launch_Kaa_trial(Ctx* c, const double* kappa, const double* cvec, const double* x,
                      const double* d, const double* lb, double* trial, double* F,
                      unsigned char* act, int merit_slot, cudaStream_t st) {
     OpKaaTrial op{kappa, cvec, x, d, lb, trial, F, act, c->scal, merit_slot, redbuf(c), 0.0, 0.0};
-    return run_strip(c, op, st);
+    return run_strip(c, op, st, K_KAA_TRIAL);
 }
 int launch_physics(Ctx* c, const double* u, const double* alpha, const double* lb, double* ru,
                    double* ra, double* phi, int rows, cudaStream_t st) {
+    const int nw = (ru ? 2 : 0) + (ra ? 1 : 0) + (phi ? 1 : 0);
     switch (rows) {
         case PF_ROWS_ZERO: {
             OpPhys<PF_ROWS_ZERO> op{u, alpha, lb, ru, ra, phi, c->scal, redbuf(c), 0, 0, 0, 0};
-            return run_strip(c, op, st);
+            return run_strip(c, op, st, K_PHYS, nw);
         }
         case PF_ROWS_VALUE: {
             OpPhys<PF_ROWS_VALUE> op{u, alpha, lb, ru, ra, phi, c->scal, redbuf(c), 0, 0, 0, 0};
-            return run_strip(c, op, st);
+            return run_strip(c, op, st, K_PHYS, nw);
         }
         default: {
             OpPhys<PF_ROWS_RAW> op{u, alpha, lb, ru, ra, phi, c->scal, redbuf(c), 0, 0, 0, 0};
-            return run_strip(c, op, st);
+            return run_strip(c, op, st, K_PHYS, nw);
         }
     }
 }
@@ -1079,28 +1104,28 @@ int launch_load(Ctx* c, const double* alpha, double* f, const double* u_or_null,
     (void)u_or_null;
     if (rows == 0) {
         OpRhs<true> op{alpha, f, c->scal, redbuf(c), 0.0};
-        return run_strip(c, op, st);
+        return run_strip(c, op, st, K_RHS);
     }
     OpRhs<false> op{alpha, f, c->scal, redbuf(c), 0.0};
-    return run_strip(c, op, st);
+    return run_strip(c, op, st, K_RHS);
 }
 int launch_Kua(Ctx* c, const double* u, const double* alpha, const double* xa, double* yu,
                int bcmode, cudaStream_t st) {
     OpKua op;
     op.u = u; op.alpha = alpha; op.xa = xa; op.yu = yu; op.bcmode = bcmode;
-    return run_strip(c, op, st);
+    return run_strip(c, op, st, K_KUA);
 }
 int launch_Kau(Ctx* c, const double* u, const double* alpha, const double* xu, double* ya,
                int bcmode, cudaStream_t st) {
     OpKau op;
     op.u = u; op.alpha = alpha; op.xu = xu; op.ya = ya; op.bcmode = bcmode;
-    return run_strip(c, op, st);
+    return run_strip(c, op, st, K_KAU);
 }
 int launch_jac(Ctx* c, const double* u, const double* alpha, const double* xu, const double* xa,
                double* yu, double* ya, const unsigned char* act, cudaStream_t st) {
     OpJac op;
     op.u = u; op.alpha = alpha; op.xu = xu; op.xa = xa; op.yu = yu; op.ya = ya; op.act = act;
-    return run_strip(c, op, st);
+    return run_strip(c, op, st, K_JAC);
 }
 
 }  // namespace pf
