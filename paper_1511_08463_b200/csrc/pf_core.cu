@@ -525,6 +525,8 @@ static void geometry_2d(Ctx* c) {
     g.nv = g.nc + (d.pattern == PF_CROSSED ? g.ncell : 0);
     g.hx = d.lx / g.nx;
     g.hy = d.ly / g.ny;
+    g.ihx = g.nx / d.lx;
+    g.ihy = g.ny / d.ly;
     const double P[5][2] = {{0, 0}, {g.hx, 0}, {0, g.hy}, {g.hx, g.hy}, {0.5 * g.hx, 0.5 * g.hy}};
     int L[4][3];
     if (d.pattern == PF_UNION_JACK) {

@@ -31,7 +31,7 @@ struct Geo2 {
     int nx, ny, nvy;          // cells, ny+1
     int pattern, npc;         // PF_*, elements per cell
     long long nc, ncell, nv;  // corner vertices, cells, all vertices
-    double hx, hy;
+    double hx, hy, ihx, ihy;
     // element types (local nodes 0=v00 1=v10 2=v01 3=v11 4=centre)
     double area[4];
     double gb[4][3], gc[4][3];

@@ -24,16 +24,9 @@ namespace pf {
 template <int N> struct IC { static constexpr int v = N; };
 
 template <int PAT, class F>
-__device__ __forceinline__ void for_each_elem(int parity, F&& f) {
-    if constexpr (PAT == PF_UNION_JACK) {
-        if (parity == 0) {
-            f(IC<0>{}, IC<0>{}, IC<0>{}, IC<1>{}, IC<3>{});
-            f(IC<1>{}, IC<1>{}, IC<0>{}, IC<3>{}, IC<2>{});
-        } else {
-            f(IC<2>{}, IC<0>{}, IC<0>{}, IC<1>{}, IC<2>{});
-            f(IC<3>{}, IC<1>{}, IC<1>{}, IC<3>{}, IC<2>{});
-        }
-    } else if constexpr (PAT == PF_RIGHT) {
+__device__ __forceinline__ void for_each_elem(int /*parity*/, F&& f) {
+    // f(shape, slot, nodeA, nodeB, nodeC); union-jack odd cells arrive mirrored (see mirror())
+    if constexpr (PAT == PF_UNION_JACK || PAT == PF_RIGHT) {
         f(IC<0>{}, IC<0>{}, IC<0>{}, IC<1>{}, IC<3>{});
         f(IC<1>{}, IC<1>{}, IC<0>{}, IC<3>{}, IC<2>{});
     } else {
@@ -65,25 +58,87 @@ __device__ __forceinline__ void st2(double* p, long long v, double a, double b) 
 }
 
 // ---- element kernels ---------------------------------------------------------------------
-// strain of element type T with nodes A,B,C: (e11, e22, g12) = B u_e
-template <int T, int A, int B, int C>
-__device__ __forceinline__ void strain(const Geo2& g, const double (&U1)[5], const double (&U2)[5],
+// On a uniform grid every P1 gradient coefficient is a small integer times 1/hx (b, x-derivative)
+// or 1/hy (c, y-derivative).  Shp<PAT, T> holds those integers per element shape, so zero terms
+// vanish at compile time and +-1 / +-2 become adds; only two runtime scalings remain.
+// Union-jack odd cells are x-mirrored even cells: their local nodes are permuted (0<->1, 2<->3)
+// and 1/hx changes sign, which removes the parity branch (no warp divergence).
+template <int PAT, int T> struct Shp;
+//                                       b (times 1/hx)         c (times 1/hy)
+template <> struct Shp<PF_RIGHT, 0>   { static constexpr int b0 = -1, b1 = 1, b2 = 0,  c0 = 0,  c1 = -1, c2 = 1; };
+template <> struct Shp<PF_RIGHT, 1>   { static constexpr int b0 = 0,  b1 = 1, b2 = -1, c0 = -1, c1 = 0,  c2 = 1; };
+template <> struct Shp<PF_UNION_JACK, 0> : Shp<PF_RIGHT, 0> {};
+template <> struct Shp<PF_UNION_JACK, 1> : Shp<PF_RIGHT, 1> {};
+template <> struct Shp<PF_CROSSED, 0> { static constexpr int b0 = -1, b1 = 1,  b2 = 0,  c0 = -1, c1 = -1, c2 = 2; };
+template <> struct Shp<PF_CROSSED, 1> { static constexpr int b0 = 1,  b1 = 1,  b2 = -2, c0 = -1, c1 = 1,  c2 = 0; };
+template <> struct Shp<PF_CROSSED, 2> { static constexpr int b0 = 1,  b1 = -1, b2 = 0,  c0 = 1,  c1 = 1,  c2 = -2; };
+template <> struct Shp<PF_CROSSED, 3> { static constexpr int b0 = -1, b1 = -1, b2 = 2,  c0 = 1,  c1 = -1, c2 = 0; };
+
+template <int K> __device__ __forceinline__ double kterm(double x) {
+    if constexpr (K == 1) return x;
+    else if constexpr (K == -1) return -x;
+    else if constexpr (K == 2) return x + x;
+    else if constexpr (K == -2) return -(x + x);
+    else return (double)K * x;
+}
+template <int K> __device__ __forceinline__ double kadd(double acc, double x) {
+    if constexpr (K == 0) return acc;
+    else if constexpr (K == 1) return acc + x;
+    else if constexpr (K == -1) return acc - x;
+    else return fma((double)K, x, acc);
+}
+// K0 x0 + K1 x1 + K2 x2 with compile-time integer weights (zero terms dropped)
+template <int K0, int K1, int K2>
+__device__ __forceinline__ double idot(double x0, double x1, double x2) {
+    if constexpr (K0 != 0) return kadd<K2>(kadd<K1>(kterm<K0>(x0), x1), x2);
+    else if constexpr (K1 != 0) return kadd<K2>(kterm<K1>(x1), x2);
+    else return kterm<K2>(x2);
+}
+
+template <int PAT>
+__device__ __forceinline__ void mirror(int par, double (&X)[5]) {
+    if constexpr (PAT == PF_UNION_JACK) {
+        const double a = par ? X[1] : X[0], b = par ? X[0] : X[1];
+        const double c = par ? X[3] : X[2], d = par ? X[2] : X[3];
+        X[0] = a; X[1] = b; X[2] = c; X[3] = d;
+    }
+}
+
+// strain (e11, e22, g12) = B u_e of shape T on nodes A, B, C; hx = +-1/hx, hy = 1/hy
+template <int PAT, int T, int A, int B, int C>
+__device__ __forceinline__ void strain(double hx, double hy, const double (&U1)[5], const double (&U2)[5],
                                        double& e0, double& e1, double& e2) {
-    const double b0 = g.gb[T][0], b1 = g.gb[T][1], b2 = g.gb[T][2];
-    const double c0 = g.gc[T][0], c1 = g.gc[T][1], c2 = g.gc[T][2];
-    e0 = b0 * U1[A] + b1 * U1[B] + b2 * U1[C];
-    e1 = c0 * U2[A] + c1 * U2[B] + c2 * U2[C];
-    e2 = (c0 * U1[A] + c1 * U1[B] + c2 * U1[C]) + (b0 * U2[A] + b1 * U2[B] + b2 * U2[C]);
+    using S = Shp<PAT, T>;
+    e0 = hx * idot<S::b0, S::b1, S::b2>(U1[A], U1[B], U1[C]);
+    e1 = hy * idot<S::c0, S::c1, S::c2>(U2[A], U2[B], U2[C]);
+    e2 = fma(hy, idot<S::c0, S::c1, S::c2>(U1[A], U1[B], U1[C]),
+             hx * idot<S::b0, S::b1, S::b2>(U2[A], U2[B], U2[C]));
 }
 // Y_m += B_m^T (s0, s1, s2)
-template <int T, int A, int B, int C>
-__device__ __forceinline__ void scatter_BT(const Geo2& g, double s0, double s1, double s2,
+template <int PAT, int T, int A, int B, int C>
+__device__ __forceinline__ void scatter_BT(double hx, double hy, double s0, double s1, double s2,
                                            double (&Y1)[5], double (&Y2)[5]) {
-    const double b0 = g.gb[T][0], b1 = g.gb[T][1], b2 = g.gb[T][2];
-    const double c0 = g.gc[T][0], c1 = g.gc[T][1], c2 = g.gc[T][2];
-    Y1[A] += b0 * s0 + c0 * s2;  Y2[A] += c0 * s1 + b0 * s2;
-    Y1[B] += b1 * s0 + c1 * s2;  Y2[B] += c1 * s1 + b1 * s2;
-    Y1[C] += b2 * s0 + c2 * s2;  Y2[C] += c2 * s1 + b2 * s2;
+    using S = Shp<PAT, T>;
+    const double x0 = s0 * hx, y2 = s2 * hy, y1 = s1 * hy, x2 = s2 * hx;
+    Y1[A] = kadd<S::c0>(kadd<S::b0>(Y1[A], x0), y2);  Y2[A] = kadd<S::b0>(kadd<S::c0>(Y2[A], y1), x2);
+    Y1[B] = kadd<S::c1>(kadd<S::b1>(Y1[B], x0), y2);  Y2[B] = kadd<S::b1>(kadd<S::c1>(Y2[B], y1), x2);
+    Y1[C] = kadd<S::c2>(kadd<S::b2>(Y1[C], x0), y2);  Y2[C] = kadd<S::b2>(kadd<S::c2>(Y2[C], y1), x2);
+}
+// scalar P1 gradient of shape T and its transpose-scatter: Y_m += base + b_m gx' + c_m gy'
+template <int PAT, int T, int A, int B, int C>
+__device__ __forceinline__ void grad(double hx, double hy, const double (&X)[5], double& gx, double& gy) {
+    using S = Shp<PAT, T>;
+    gx = hx * idot<S::b0, S::b1, S::b2>(X[A], X[B], X[C]);
+    gy = hy * idot<S::c0, S::c1, S::c2>(X[A], X[B], X[C]);
+}
+template <int PAT, int T, int A, int B, int C>
+__device__ __forceinline__ void grad_scatter(double hx, double hy, double base, double fx, double fy,
+                                             double (&Y)[5]) {
+    using S = Shp<PAT, T>;
+    const double x = fx * hx, y = fy * hy;
+    Y[A] = kadd<S::c0>(kadd<S::b0>(Y[A] + base, x), y);
+    Y[B] = kadd<S::c1>(kadd<S::b1>(Y[B] + base, x), y);
+    Y[C] = kadd<S::c2>(kadd<S::b2>(Y[C] + base, x), y);
 }
 __device__ __forceinline__ void unit_stress(const Geo2& g, double e0, double e1, double e2,
                                             double& s0, double& s1, double& s2) {
@@ -92,54 +147,143 @@ __device__ __forceinline__ void unit_stress(const Geo2& g, double e0, double e1,
     s2 = g.D22 * e2;
 }
 
+// ---- cp.async staging ----------------------------------------------------------------------
+// Every warp owns a ring of PD shared-memory stages.  A stage holds, per lane, the raw bytes of
+// one vertex row (SV 8-byte slots) and one cell row (SC slots), laid out slot-major
+// (slot q of lane l at q*256 + 8l; 16-byte items span two slots at q*256 + 16l) so that warp
+// accesses are conflict-free.  Copies are issued PD row-steps ahead with cp.async (LDGSTS) and
+// nothing touches the data until the step that consumes it: no register ring, no early
+// scoreboard dependency on the loads.
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void cpa16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_addr(dst)), "l"(src));
+}
+__device__ __forceinline__ void cpa8(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_addr(dst)), "l"(src));
+}
+__device__ __forceinline__ void cpa4(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_addr(dst)), "l"(src));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+struct Slots {
+    unsigned char* p;
+    int lane;
+    __device__ __forceinline__ double* d(int q) const { return reinterpret_cast<double*>(p + q * 256) + lane; }
+    __device__ __forceinline__ double2* d2(int q) const {
+        return reinterpret_cast<double2*>(p + q * 256) + lane;
+    }
+    __device__ __forceinline__ unsigned* w(int q) const {
+        return reinterpret_cast<unsigned*>(p + q * 256) + lane;
+    }
+    __device__ __forceinline__ Slots at(int q) const { return Slots{p + q * 256, lane}; }
+};
+// stage helpers for common items
+__device__ __forceinline__ void put2(const Slots& s, int q, const double* base, long long v) {
+    cpa16(s.d2(q), base + 2 * v);
+}
+__device__ __forceinline__ void put1(const Slots& s, int q, const double* base, long long v) {
+    cpa8(s.d(q), base + v);
+}
+__device__ __forceinline__ void putb(const Slots& s, int q, const unsigned char* base, long long v) {
+    cpa4(s.w(q), base + (v & ~3LL));  // the aligned word holding byte v
+}
+__device__ __forceinline__ double2 get2(const Slots& s, int q) { return *s.d2(q); }
+__device__ __forceinline__ double get1(const Slots& s, int q) { return *s.d(q); }
+__device__ __forceinline__ unsigned getb(const Slots& s, int q, long long v) {
+    return (*s.w(q) >> (8 * (unsigned)(v & 3))) & 0xffu;
+}
+
 // ---- the strip engine ----------------------------------------------------------------------
 template <class Op, int PAT>
-__global__ void __launch_bounds__(kBlock) k_strip2d(const Geo2 g, Op op) {
-    constexpr int NV = Op::NV, NC = Op::NC;
+__global__ void __launch_bounds__(kBlock, Op::MINB) k_strip2d(const Geo2 g, Op op) {
+    constexpr int NV = Op::NV, NC = Op::NC, PD = Op::pd(PAT);
+    constexpr int NE = Op::ne(PAT) > 0 ? Op::ne(PAT) : 1;
+    constexpr int SV = Op::sv(PAT), SC = Op::sc(PAT) > 0 ? Op::sc(PAT) : 0;
+    constexpr int STAGE = (SV + SC) * 256;
+    extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31;
     const int gw = blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5);
     const int wj = gw % g.nwj, wi = gw / g.nwj;
     if (!op.enter()) return;  // device-side early exit (solver converged): uniform
     if (wi < g.nstrips) {
+        unsigned char* wbase = smem + (threadIdx.x >> 5) * (PD * STAGE);
         const int j = wj * kLanesOut - 1 + lane;
         const bool jv = (j >= 0) && (j <= g.ny);
         const bool jc = (j >= 0) && (j < g.ny) && (lane < 31);
         const bool jo = jv && lane >= 1 && lane <= kLanesOut;
         const int i0 = wi * g.S;
         const int i1 = min(i0 + g.S, g.nx + 1);
-        double vc[NV], vn[NV], rc[NV], rn[NV], vp[NV], carry[NC];
+        const int vlast = min(i1, g.nx);          // last vertex row this strip reads
+        const int clast = min(i1 - 1, g.nx - 1);  // last cell row this strip computes
+        double vc[NV], rc[NV], carry[NC];
 #pragma unroll
         for (int k = 0; k < NC; ++k) carry[k] = 0.0;
         int ci = i0 - 1;
+        auto issue = [&](int u, int r, int cr) {
+            const Slots sv{wbase + u * STAGE, lane};
+            if (r <= vlast && jv) op.issue_v(g, r, j, sv);
+            if constexpr (SC > 0) {
+                if (cr >= 0 && cr <= clast && jc) op.template issue_c<PAT>(g, cr, j, sv.at(SV));
+            }
+            cp_commit();
+        };
 #pragma unroll
-        for (int k = 0; k < NV; ++k) { vc[k] = 0.0; vp[k] = 0.0; }
-        if (ci >= 0 && jv) op.load(g, ci, j, vc);
-        if (ci + 1 <= g.nx && jv) op.load(g, ci + 1, j, vp);
+        for (int k = 0; k < NV; ++k) vc[k] = 0.0;
+        if (ci >= 0 && jv) {  // first row of the strip: stage through slot 0 synchronously
+            const Slots s0{wbase, lane};
+            op.issue_v(g, ci, j, s0);
+            cp_commit();
+            cp_wait<0>();
+            op.fix_v(g, ci, j, s0, vc);
+        }
+#pragma unroll
+        for (int u = 0; u < PD; ++u) issue(u, ci + 1 + u, ci + u);
 #pragma unroll
         for (int k = 0; k < NV; ++k) rc[k] = __shfl_down_sync(PF_FULL, vc[k], 1);
-        for (; ci < i1; ++ci) {
+        while (ci < i1) {
 #pragma unroll
-            for (int k = 0; k < NV; ++k) { vn[k] = vp[k]; vp[k] = 0.0; }
-            if (ci + 2 <= g.nx && ci + 1 < i1 && jv) op.load(g, ci + 2, j, vp);
+            for (int u = 0; u < PD; ++u) {
+                if (ci < i1) {
+                    cp_wait<PD - 1>();
+                    const Slots sv{wbase + u * STAGE, lane};
+                    double vn[NV], rn[NV], ec[NE];
 #pragma unroll
-            for (int k = 0; k < NV; ++k) rn[k] = __shfl_down_sync(PF_FULL, vn[k], 1);
-            double c00[NC], c10[NC], c01[NC], c11[NC];
+                    for (int k = 0; k < NV; ++k) vn[k] = 0.0;
 #pragma unroll
-            for (int k = 0; k < NC; ++k) { c00[k] = c10[k] = c01[k] = c11[k] = 0.0; }
-            if (ci >= 0 && ci < g.nx && jc)
-                op.template cell<PAT>(g, ci, j, vc, vn, rc, rn, c00, c10, c01, c11,
-                                      (ci >= i0) && jo);
+                    for (int k = 0; k < NE; ++k) ec[k] = 0.0;
+                    const bool cvalid = ci >= 0 && ci < g.nx && jc;
+                    if (ci + 1 <= vlast && jv) op.fix_v(g, ci + 1, j, sv, vn);
+                    if (cvalid) op.template fix_c<PAT>(g, ci, j, sv.at(SV), ec);
 #pragma unroll
-            for (int k = 0; k < NC; ++k) {
-                const double l01 = __shfl_up_sync(PF_FULL, c01[k], 1);
-                const double l11 = __shfl_up_sync(PF_FULL, c11[k], 1);
-                c00[k] += carry[k] + l01;
-                carry[k] = c10[k] + l11;
+                    for (int k = 0; k < NV; ++k) rn[k] = __shfl_down_sync(PF_FULL, vn[k], 1);
+                    double c00[NC], c10[NC], c01[NC], c11[NC];
+#pragma unroll
+                    for (int k = 0; k < NC; ++k) { c00[k] = c10[k] = c01[k] = c11[k] = 0.0; }
+                    if (cvalid)
+                        op.template cell<PAT>(g, ci, j, vc, vn, rc, rn, ec, c00, c10, c01, c11,
+                                              (ci >= i0) && jo);
+#pragma unroll
+                    for (int k = 0; k < NC; ++k) {
+                        const double l01 = __shfl_up_sync(PF_FULL, c01[k], 1);
+                        const double l11 = __shfl_up_sync(PF_FULL, c11[k], 1);
+                        c00[k] += carry[k] + l01;
+                        carry[k] = c10[k] + l11;
+                    }
+                    if (ci >= i0 && jo) op.out(g, ci, j, c00, vc);
+#pragma unroll
+                    for (int k = 0; k < NV; ++k) { vc[k] = vn[k]; rc[k] = rn[k]; }
+                    // refill this stage for step ci + PD (its old contents are consumed)
+                    issue(u, ci + 1 + PD, ci + PD);
+                    ++ci;
+                }
             }
-            if (ci >= i0 && jo) op.out(g, ci, j, c00, vc);
-#pragma unroll
-            for (int k = 0; k < NV; ++k) { vc[k] = vn[k]; rc[k] = rn[k]; }
         }
+        cp_wait<0>();
     }
     op.finish();
 }
@@ -148,20 +292,42 @@ __global__ void __launch_bounds__(kBlock) k_strip2d(const Geo2 g, Op op) {
 __device__ __forceinline__ long long vid(const Geo2& g, int i, int j) { return (long long)i * g.nvy + j; }
 __device__ __forceinline__ long long cid(const Geo2& g, int ci, int j) { return (long long)ci * g.ny + j; }
 __device__ __forceinline__ long long ctr(const Geo2& g, int ci, int j) { return g.nc + cid(g, ci, j); }
+__host__ __device__ __forceinline__ constexpr int npc_of(int pat) { return pat == PF_CROSSED ? 4 : 2; }
+__host__ __device__ __forceinline__ constexpr int crossed(int pat) { return pat == PF_CROSSED ? 1 : 0; }
 
 struct NoRed {
+    static constexpr int MINB = 2;
     __device__ bool enter() const { return true; }
     __device__ void finish() {}
 };
+
+// cell scalars E / Gc (per-cell field or the scalar)
+__device__ __forceinline__ void putE(const Geo2& g, const Slots& s, int q, long long cell) {
+    if (g.E_cell) put1(s, q, g.E_cell, cell);
+}
+__device__ __forceinline__ double getE(const Geo2& g, const Slots& s, int q) {
+    return g.E_cell ? get1(s, q) : g.E;
+}
+__device__ __forceinline__ void putGc(const Geo2& g, const Slots& s, int q, long long cell) {
+    if (g.Gc_cell) put1(s, q, g.Gc_cell, cell);
+}
+__device__ __forceinline__ double getGc(const Geo2& g, const Slots& s, int q) {
+    return g.Gc_cell ? get1(s, q) : g.Gc;
+}
 
 // ================================================================================================
 // Kuu: y = K(alpha) x, optionally Dirichlet-eliminated (fem.py:233-243, 282-294).
 // FUSED: CG step A -- p_out = z + beta p_in (beta = 0 at iteration 0), y = K p_out, pAp reduced
 // and gamma = rz / pAp formed by the last block (linalg.py:130-138).
+// vertex slots: x|z (0-1), [p_in (2-3)], alpha; cell slots: E, [centre x|z, p_in, alpha]
 // ================================================================================================
 template <bool FUSED>
 struct OpKuu {
-    static constexpr int NV = 3, NC = 2;
+    static constexpr int NV = 3, NC = 2, MINB = 2;
+    static constexpr int pd(int pat) { return 4; }
+    static constexpr int ne(int pat) { return 1 + 3 * crossed(pat); }
+    static constexpr int sv(int) { return FUSED ? 5 : 3; }
+    static constexpr int sc(int pat) { return 1 + crossed(pat) * (FUSED ? 5 : 3); }
     const double* alpha;
     const double* x;      // plain: x ; fused: z
     const double* pin;    // fused only
@@ -177,7 +343,7 @@ struct OpKuu {
         return scal[S_DONE] == 0.0 && scal[S_FAIL] == 0.0;
     }
     __device__ __forceinline__ double beta() const { return scal[S_ITER] > 0.0 ? scal[S_BETA] : 0.0; }
-    __device__ __forceinline__ double2 xval(long long v) const {
+    __device__ __forceinline__ double2 xval(long long v) const {  // direct (boundary rows only)
         double2 z = ld2(x, v);
         if (FUSED) {
             const double b = beta();
@@ -187,45 +353,77 @@ struct OpKuu {
         }
         return z;
     }
-    __device__ void load(const Geo2& g, int i, int j, double (&v)[NV]) const {
-        const long long id = vid(g, i, j);
-        const double2 xv = xval(id);
-        const unsigned m = bcmode ? bcbits(g, i, j, id) : 0u;
+    __device__ __forceinline__ void stage_vertex(const Slots& s, long long v) const {
+        put2(s, 0, x, v);
+        if (FUSED) { put2(s, 2, pin, v); put1(s, 4, alpha, v); }
+        else put1(s, 2, alpha, v);
+    }
+    __device__ __forceinline__ double2 staged_x(const Slots& s) const {
+        double2 z = get2(s, 0);
+        if (FUSED) {
+            const double b = beta();
+            const double2 p = get2(s, 2);
+            z.x = z.x + b * p.x;
+            z.y = z.y + b * p.y;
+        }
+        return z;
+    }
+    __device__ void issue_v(const Geo2& g, int i, int j, const Slots& s) const { stage_vertex(s, vid(g, i, j)); }
+    __device__ void fix_v(const Geo2& g, int i, int j, const Slots& s, double (&v)[NV]) const {
+        const double2 xv = staged_x(s);
+        const unsigned m = bcmode ? bcbits(g, i, j, vid(g, i, j)) : 0u;
         v[0] = (m & 1u) ? 0.0 : xv.x;
         v[1] = (m & 2u) ? 0.0 : xv.y;
-        v[2] = __ldg(alpha + id);
+        v[2] = get1(s, FUSED ? 4 : 2);
     }
     template <int PAT>
+    __device__ void issue_c(const Geo2& g, int ci, int j, const Slots& s) const {
+        putE(g, s, 0, cid(g, ci, j));
+        if constexpr (PAT == PF_CROSSED) stage_vertex(s.at(1), ctr(g, ci, j));
+    }
+    template <int PAT, int NE>
+    __device__ void fix_c(const Geo2& g, int ci, int j, const Slots& s, double (&e)[NE]) const {
+        e[0] = getE(g, s, 0);
+        if constexpr (PAT == PF_CROSSED) {
+            const Slots c = s.at(1);
+            const double2 xv = staged_x(c);
+            e[1] = xv.x; e[2] = xv.y; e[3] = get1(c, FUSED ? 4 : 2);
+        }
+    }
+    template <int PAT, int NE>
     __device__ void cell(const Geo2& g, int ci, int j, const double (&vc)[NV], const double (&vn)[NV],
-                         const double (&rc)[NV], const double (&rn)[NV], double (&c00)[NC],
-                         double (&c10)[NC], double (&c01)[NC], double (&c11)[NC], bool own) {
+                         const double (&rc)[NV], const double (&rn)[NV], const double (&ec)[NE],
+                         double (&c00)[NC], double (&c10)[NC], double (&c01)[NC], double (&c11)[NC],
+                         bool own) {
         double U1[5] = {vc[0], vn[0], rc[0], rn[0], 0.0};
         double U2[5] = {vc[1], vn[1], rc[1], rn[1], 0.0};
         double Al[5] = {vc[2], vn[2], rc[2], rn[2], 0.0};
-        long long cv = 0;
-        if constexpr (PAT == PF_CROSSED) {
-            cv = ctr(g, ci, j);
-            const double2 xv = xval(cv);
-            U1[4] = xv.x; U2[4] = xv.y; Al[4] = __ldg(alpha + cv);
-        }
+        if constexpr (PAT == PF_CROSSED) { U1[4] = ec[1]; U2[4] = ec[2]; Al[4] = ec[3]; }
         double Y1[5] = {0, 0, 0, 0, 0}, Y2[5] = {0, 0, 0, 0, 0};
-        const long long cell = cid(g, ci, j);
-        const double Ec = cellE(g, cell);
-        for_each_elem<PAT>((ci + j) & 1, [&](auto T, auto, auto A, auto B, auto C) {
+        const int par = (PAT == PF_UNION_JACK) ? ((ci + j) & 1) : 0;
+        const double hxs = par ? -g.ihx : g.ihx;
+        mirror<PAT>(par, U1);
+        mirror<PAT>(par, U2);
+        mirror<PAT>(par, Al);
+        const double Ec = ec[0];
+        for_each_elem<PAT>(par, [&](auto T, auto, auto A, auto B, auto C) {
             const double ab = (Al[A.v] + Al[B.v] + Al[C.v]) * (1.0 / 3.0);
             const double om = 1.0 - ab;
-            const double s = (om * om + g.kell) * g.area[T.v] * Ec;
+            const double s = (om * om + g.kell) * g.area[0] * Ec;
             double e0, e1, e2, s0, s1, s2;
-            strain<T.v, A.v, B.v, C.v>(g, U1, U2, e0, e1, e2);
+            strain<PAT, T.v, A.v, B.v, C.v>(hxs, g.ihy, U1, U2, e0, e1, e2);
             unit_stress(g, e0, e1, e2, s0, s1, s2);
-            scatter_BT<T.v, A.v, B.v, C.v>(g, s * s0, s * s1, s * s2, Y1, Y2);
+            scatter_BT<PAT, T.v, A.v, B.v, C.v>(hxs, g.ihy, s * s0, s * s1, s * s2, Y1, Y2);
         });
+        mirror<PAT>(par, Y1);
+        mirror<PAT>(par, Y2);
         c00[0] = Y1[0]; c00[1] = Y2[0];
         c10[0] = Y1[1]; c10[1] = Y2[1];
         c01[0] = Y1[2]; c01[1] = Y2[2];
         c11[0] = Y1[3]; c11[1] = Y2[3];
         if constexpr (PAT == PF_CROSSED) {
             if (own) {
+                const long long cv = ctr(g, ci, j);
                 st2(y, cv, Y1[4], Y2[4]);
                 if (FUSED) {
                     st2(pout, cv, U1[4], U2[4]);
@@ -262,40 +460,61 @@ struct OpKuu {
     }
 };
 
-// diag(Kuu) -> dinv = 1/diag; eliminated rows get 1.
+// diag(Kuu) -> dinv = 1/diag; eliminated rows get 1.   vertex: alpha; cell: E, [alpha_c]
 struct OpKuuDiag : NoRed {
     static constexpr int NV = 1, NC = 2;
+    static constexpr int pd(int) { return 4; }
+    static constexpr int ne(int pat) { return 1 + crossed(pat); }
+    static constexpr int sv(int) { return 1; }
+    static constexpr int sc(int pat) { return 1 + crossed(pat); }
     const double* alpha;
     double* dinv;
-    __device__ void load(const Geo2& g, int i, int j, double (&v)[NV]) const {
-        v[0] = __ldg(alpha + vid(g, i, j));
-    }
+    __device__ void issue_v(const Geo2& g, int i, int j, const Slots& s) const { put1(s, 0, alpha, vid(g, i, j)); }
+    __device__ void fix_v(const Geo2&, int, int, const Slots& s, double (&v)[NV]) const { v[0] = get1(s, 0); }
     template <int PAT>
+    __device__ void issue_c(const Geo2& g, int ci, int j, const Slots& s) const {
+        putE(g, s, 0, cid(g, ci, j));
+        if constexpr (PAT == PF_CROSSED) put1(s, 1, alpha, ctr(g, ci, j));
+    }
+    template <int PAT, int NE>
+    __device__ void fix_c(const Geo2& g, int, int, const Slots& s, double (&e)[NE]) const {
+        e[0] = getE(g, s, 0);
+        if constexpr (PAT == PF_CROSSED) e[1] = get1(s, 1);
+    }
+    template <int PAT, int NE>
     __device__ void cell(const Geo2& g, int ci, int j, const double (&vc)[NV], const double (&vn)[NV],
-                         const double (&rc)[NV], const double (&rn)[NV], double (&c00)[NC],
-                         double (&c10)[NC], double (&c01)[NC], double (&c11)[NC], bool own) {
+                         const double (&rc)[NV], const double (&rn)[NV], const double (&ec)[NE],
+                         double (&c00)[NC], double (&c10)[NC], double (&c01)[NC], double (&c11)[NC],
+                         bool own) {
         double Al[5] = {vc[0], vn[0], rc[0], rn[0], 0.0};
-        long long cv = 0;
-        if constexpr (PAT == PF_CROSSED) { cv = ctr(g, ci, j); Al[4] = __ldg(alpha + cv); }
+        if constexpr (PAT == PF_CROSSED) Al[4] = ec[1];
         double Y1[5] = {0, 0, 0, 0, 0}, Y2[5] = {0, 0, 0, 0, 0};
-        const double Ec = cellE(g, cid(g, ci, j));
-        for_each_elem<PAT>((ci + j) & 1, [&](auto T, auto, auto A, auto B, auto C) {
+        const int par = (PAT == PF_UNION_JACK) ? ((ci + j) & 1) : 0;
+        mirror<PAT>(par, Al);
+        const double Ec = ec[0];
+        for_each_elem<PAT>(par, [&](auto T, auto, auto A, auto B, auto C) {
             const double ab = (Al[A.v] + Al[B.v] + Al[C.v]) * (1.0 / 3.0);
             const double om = 1.0 - ab;
-            const double s = (om * om + g.kell) * g.area[T.v] * Ec;
-            const double* b = g.gb[T.v];
-            const double* c = g.gc[T.v];
-            Y1[A.v] += s * (b[0] * b[0] * g.D00 + c[0] * c[0] * g.D22);
-            Y2[A.v] += s * (c[0] * c[0] * g.D11 + b[0] * b[0] * g.D22);
-            Y1[B.v] += s * (b[1] * b[1] * g.D00 + c[1] * c[1] * g.D22);
-            Y2[B.v] += s * (c[1] * c[1] * g.D11 + b[1] * b[1] * g.D22);
-            Y1[C.v] += s * (b[2] * b[2] * g.D00 + c[2] * c[2] * g.D22);
-            Y2[C.v] += s * (c[2] * c[2] * g.D11 + b[2] * b[2] * g.D22);
+            const double s = (om * om + g.kell) * g.area[0] * Ec;
+            using Sh = Shp<PAT, T.v>;
+            const double X2 = g.ihx * g.ihx, Y2h = g.ihy * g.ihy;
+            const double bb[3] = {double(Sh::b0 * Sh::b0) * X2, double(Sh::b1 * Sh::b1) * X2,
+                                  double(Sh::b2 * Sh::b2) * X2};
+            const double cc[3] = {double(Sh::c0 * Sh::c0) * Y2h, double(Sh::c1 * Sh::c1) * Y2h,
+                                  double(Sh::c2 * Sh::c2) * Y2h};
+            Y1[A.v] += s * (bb[0] * g.D00 + cc[0] * g.D22);
+            Y2[A.v] += s * (cc[0] * g.D11 + bb[0] * g.D22);
+            Y1[B.v] += s * (bb[1] * g.D00 + cc[1] * g.D22);
+            Y2[B.v] += s * (cc[1] * g.D11 + bb[1] * g.D22);
+            Y1[C.v] += s * (bb[2] * g.D00 + cc[2] * g.D22);
+            Y2[C.v] += s * (cc[2] * g.D11 + bb[2] * g.D22);
         });
+        mirror<PAT>(par, Y1);
+        mirror<PAT>(par, Y2);
         c00[0] = Y1[0]; c00[1] = Y2[0]; c10[0] = Y1[1]; c10[1] = Y2[1];
         c01[0] = Y1[2]; c01[1] = Y2[2]; c11[0] = Y1[3]; c11[1] = Y2[3];
         if constexpr (PAT == PF_CROSSED) {
-            if (own) st2(dinv, cv, 1.0 / Y1[4], 1.0 / Y2[4]);
+            if (own) st2(dinv, ctr(g, ci, j), 1.0 / Y1[4], 1.0 / Y2[4]);
         }
     }
     __device__ void out(const Geo2& g, int i, int j, const double (&t)[NC], const double (&)[NV]) {
@@ -309,50 +528,73 @@ struct OpKuuDiag : NoRed {
 // Damage block.  kappa_e = (1/2 a'' q + (Gc/c_w) w''/ell) |T|/9 is the element reaction
 // coefficient (fem.py:266-276; independent of alpha for AT1/AT2); c = r_alpha - Kaa alpha is its
 // affine remainder (solver.py:152-153), c_v = sum_e |T|/3 (-q_e + [AT1] Gc_e/(c_w ell)).
+// vertex: u; cell: E, Gc, [u_c]
 // ================================================================================================
 struct OpKappa : NoRed {
     static constexpr int NV = 2, NC = 1;
+    static constexpr int pd(int) { return 4; }
+    static constexpr int ne(int pat) { return 2 + 2 * crossed(pat); }
+    static constexpr int sv(int) { return 2; }
+    static constexpr int sc(int pat) { return 2 + 2 * crossed(pat); }
     const double* u;
     double* kappa;
     double* cvec;
-    __device__ void load(const Geo2& g, int i, int j, double (&v)[NV]) const {
-        const double2 uv = ld2(u, vid(g, i, j));
+    __device__ void issue_v(const Geo2& g, int i, int j, const Slots& s) const { put2(s, 0, u, vid(g, i, j)); }
+    __device__ void fix_v(const Geo2&, int, int, const Slots& s, double (&v)[NV]) const {
+        const double2 uv = get2(s, 0);
         v[0] = uv.x; v[1] = uv.y;
     }
     template <int PAT>
+    __device__ void issue_c(const Geo2& g, int ci, int j, const Slots& s) const {
+        const long long cell = cid(g, ci, j);
+        putE(g, s, 0, cell);
+        putGc(g, s, 1, cell);
+        if constexpr (PAT == PF_CROSSED) put2(s, 2, u, ctr(g, ci, j));
+    }
+    template <int PAT, int NE>
+    __device__ void fix_c(const Geo2& g, int, int, const Slots& s, double (&e)[NE]) const {
+        e[0] = getE(g, s, 0);
+        e[1] = getGc(g, s, 1);
+        if constexpr (PAT == PF_CROSSED) {
+            const double2 uv = get2(s, 2);
+            e[2] = uv.x; e[3] = uv.y;
+        }
+    }
+    template <int PAT, int NE>
     __device__ void cell(const Geo2& g, int ci, int j, const double (&vc)[NV], const double (&vn)[NV],
-                         const double (&rc)[NV], const double (&rn)[NV], double (&c00)[NC],
-                         double (&c10)[NC], double (&c01)[NC], double (&c11)[NC], bool own) {
+                         const double (&rc)[NV], const double (&rn)[NV], const double (&ec)[NE],
+                         double (&c00)[NC], double (&c10)[NC], double (&c01)[NC], double (&c11)[NC],
+                         bool own) {
         double U1[5] = {vc[0], vn[0], rc[0], rn[0], 0.0};
         double U2[5] = {vc[1], vn[1], rc[1], rn[1], 0.0};
-        long long cv = 0;
-        if constexpr (PAT == PF_CROSSED) {
-            cv = ctr(g, ci, j);
-            const double2 uv = ld2(u, cv);
-            U1[4] = uv.x; U2[4] = uv.y;
-        }
+        if constexpr (PAT == PF_CROSSED) { U1[4] = ec[2]; U2[4] = ec[3]; }
         double Y[5] = {0, 0, 0, 0, 0};
+        const int par = (PAT == PF_UNION_JACK) ? ((ci + j) & 1) : 0;
+        const double hxs = par ? -g.ihx : g.ihx;
+        mirror<PAT>(par, U1);
+        mirror<PAT>(par, U2);
         const long long cell = cid(g, ci, j);
-        const double Ec = cellE(g, cell);
-        const double kc = cellGc(g, cell) / g.cw;
-        for_each_elem<PAT>((ci + j) & 1, [&](auto T, auto S, auto A, auto B, auto C) {
+        const double Ec = ec[0];
+        const double kc = ec[1] / g.cw;
+        for_each_elem<PAT>(par, [&](auto T, auto S, auto A, auto B, auto C) {
             double e0, e1, e2, s0, s1, s2;
-            strain<T.v, A.v, B.v, C.v>(g, U1, U2, e0, e1, e2);
+            strain<PAT, T.v, A.v, B.v, C.v>(hxs, g.ihy, U1, U2, e0, e1, e2);
             if (g.eps0) {
-                const double e = __ldg(g.eps0 + (long long)T.v * g.ny + j);
+                const double e = __ldg(g.eps0 + (long long)(T.v + 2 * par) * g.ny + j);
                 e0 -= e; e1 -= e;
             }
             unit_stress(g, e0, e1, e2, s0, s1, s2);
             const double q = Ec * (e0 * s0 + e1 * s1 + e2 * s2);
-            const double ar = g.area[T.v];
+            const double ar = g.area[0];
             const double kap = (q + (g.at2 ? 2.0 * kc / g.ell : 0.0)) * ar * (1.0 / 9.0);
             const double cc = ar * (1.0 / 3.0) * (-q + (g.at2 ? 0.0 : kc / g.ell));
             Y[A.v] += cc; Y[B.v] += cc; Y[C.v] += cc;
             if (own) kappa[(long long)S.v * g.ncell + cell] = kap;
         });
+        mirror<PAT>(par, Y);
         c00[0] = Y[0]; c10[0] = Y[1]; c01[0] = Y[2]; c11[0] = Y[3];
         if constexpr (PAT == PF_CROSSED) {
-            if (own) cvec[cv] = Y[4];
+            if (own) cvec[ctr(g, ci, j)] = Y[4];
         }
     }
     __device__ void out(const Geo2& g, int i, int j, const double (&t)[NC], const double (&)[NV]) {
@@ -362,25 +604,39 @@ struct OpKappa : NoRed {
 
 // Damage Hessian element action: y_m += kappa (x_A + x_B + x_C) + delta (b_m gx + c_m gy),
 // delta = 2 (Gc/c_w) ell |T| (diffusion part, fem.py:272-273).
-template <int T, int A, int B, int C>
-__device__ __forceinline__ void elem_kaa(const Geo2& g, double kap, double kc, const double (&X)[5],
-                                         double (&Y)[5]) {
-    const double b0 = g.gb[T][0], b1 = g.gb[T][1], b2 = g.gb[T][2];
-    const double c0 = g.gc[T][0], c1 = g.gc[T][1], c2 = g.gc[T][2];
-    const double del = 2.0 * kc * g.ell * g.area[T];
-    const double sx = kap * ((X[A] + X[B]) + X[C]);
-    const double gx = del * (b0 * X[A] + b1 * X[B] + b2 * X[C]);
-    const double gy = del * (c0 * X[A] + c1 * X[B] + c2 * X[C]);
-    Y[A] += sx + b0 * gx + c0 * gy;
-    Y[B] += sx + b1 * gx + c1 * gy;
-    Y[C] += sx + b2 * gx + c2 * gy;
+template <int PAT, int T, int A, int B, int C>
+__device__ __forceinline__ void elem_kaa(const Geo2& g, double hx, double kap, double kc,
+                                         const double (&X)[5], double (&Y)[5]) {
+    const double del = 2.0 * kc * g.ell * g.area[0];
+    double gx, gy;
+    grad<PAT, T, A, B, C>(hx, g.ihy, X, gx, gy);
+    grad_scatter<PAT, T, A, B, C>(hx, g.ihy, kap * ((X[A] + X[B]) + X[C]), del * gx, del * gy, Y);
+}
+
+template <int PAT>
+__device__ __forceinline__ void put_kappa(const Geo2& g, const double* kappa, long long cell,
+                                          const Slots& s, int q) {
+#pragma unroll
+    for (int k = 0; k < npc_of(PAT); ++k) put1(s, q + k, kappa, (long long)k * g.ncell + cell);
+}
+template <int PAT, int NE>
+__device__ __forceinline__ void get_kappa(const Slots& s, int q, int off, double (&e)[NE]) {
+#pragma unroll
+    for (int k = 0; k < npc_of(PAT); ++k) e[off + k] = get1(s, q + k);
 }
 
 // Kaa apply; MASKED: rows/cols of active vertices (act != 0) are replaced by identity (the
 // reduced inactive-block operator J_NN of vi.py:235 embedded in full space).
+// vertex slots: x|z, [p_in], [act word]; cell: Gc, kappa x npc, [centre x|z, p_in, act word]
+// ec: [Gc, kappa x npc, (centre: x unmasked, active flag)]
 template <bool FUSED, bool MASKED>
 struct OpKaa {
-    static constexpr int NV = 1, NC = 1;
+    static constexpr int NV = 1, NC = 1, MINB = 2;
+    static constexpr int VS = 1 + (FUSED ? 1 : 0) + (MASKED ? 1 : 0);  // vertex slots
+    static constexpr int pd(int pat) { return pat == PF_CROSSED ? 4 : 6; }
+    static constexpr int ne(int pat) { return 1 + npc_of(pat) + 2 * crossed(pat); }
+    static constexpr int sv(int) { return VS; }
+    static constexpr int sc(int pat) { return 1 + npc_of(pat) + crossed(pat) * VS; }
     const double* kappa;
     const double* x;     // fused: z
     const double* pin;
@@ -403,33 +659,66 @@ struct OpKaa {
         return z;
     }
     __device__ __forceinline__ bool is_act(long long v) const { return MASKED && act[v] != 0; }
-    __device__ void load(const Geo2& g, int i, int j, double (&v)[NV]) const {
-        const long long id = vid(g, i, j);
-        v[0] = is_act(id) ? 0.0 : xval(id);
+    __device__ __forceinline__ void stage_vertex(const Slots& s, long long v) const {
+        put1(s, 0, x, v);
+        if (FUSED) put1(s, 1, pin, v);
+        if (MASKED) putb(s, FUSED ? 2 : 1, act, v);
+    }
+    // (value, active) from a staged vertex
+    __device__ __forceinline__ double staged(const Slots& s, long long v, bool& a) const {
+        double z = get1(s, 0);
+        if (FUSED) {
+            const double b = scal[S_ITER] > 0.0 ? scal[S_BETA] : 0.0;
+            z = z + b * get1(s, 1);
+        }
+        a = MASKED ? (getb(s, FUSED ? 2 : 1, v) != 0u) : false;
+        return z;
+    }
+    __device__ void issue_v(const Geo2& g, int i, int j, const Slots& s) const { stage_vertex(s, vid(g, i, j)); }
+    __device__ void fix_v(const Geo2& g, int i, int j, const Slots& s, double (&v)[NV]) const {
+        bool a;
+        const double z = staged(s, vid(g, i, j), a);
+        v[0] = a ? 0.0 : z;
     }
     template <int PAT>
-    __device__ void cell(const Geo2& g, int ci, int j, const double (&vc)[NV], const double (&vn)[NV],
-                         const double (&rc)[NV], const double (&rn)[NV], double (&c00)[NC],
-                         double (&c10)[NC], double (&c01)[NC], double (&c11)[NC], bool own) {
-        double X[5] = {vc[0], vn[0], rc[0], rn[0], 0.0};
-        long long cv = 0;
-        double xc = 0.0;
-        if constexpr (PAT == PF_CROSSED) {
-            cv = ctr(g, ci, j);
-            xc = xval(cv);
-            X[4] = is_act(cv) ? 0.0 : xc;
-        }
-        double Y[5] = {0, 0, 0, 0, 0};
+    __device__ void issue_c(const Geo2& g, int ci, int j, const Slots& s) const {
         const long long cell = cid(g, ci, j);
-        const double kc = cellGc(g, cell) / g.cw;
-        for_each_elem<PAT>((ci + j) & 1, [&](auto T, auto S, auto A, auto B, auto C) {
-            const double kap = __ldg(kappa + (long long)S.v * g.ncell + cell);
-            elem_kaa<T.v, A.v, B.v, C.v>(g, kap, kc, X, Y);
+        putGc(g, s, 0, cell);
+        put_kappa<PAT>(g, kappa, cell, s, 1);
+        if constexpr (PAT == PF_CROSSED) stage_vertex(s.at(1 + npc_of(PAT)), ctr(g, ci, j));
+    }
+    template <int PAT, int NE>
+    __device__ void fix_c(const Geo2& g, int ci, int j, const Slots& s, double (&e)[NE]) const {
+        e[0] = getGc(g, s, 0);
+        get_kappa<PAT>(s, 1, 1, e);
+        if constexpr (PAT == PF_CROSSED) {
+            bool a;
+            e[5] = staged(s.at(1 + npc_of(PAT)), ctr(g, ci, j), a);
+            e[6] = a ? 1.0 : 0.0;
+        }
+    }
+    template <int PAT, int NE>
+    __device__ void cell(const Geo2& g, int ci, int j, const double (&vc)[NV], const double (&vn)[NV],
+                         const double (&rc)[NV], const double (&rn)[NV], const double (&ec)[NE],
+                         double (&c00)[NC], double (&c10)[NC], double (&c01)[NC], double (&c11)[NC],
+                         bool own) {
+        double X[5] = {vc[0], vn[0], rc[0], rn[0], 0.0};
+        if constexpr (PAT == PF_CROSSED) X[4] = ec[6] != 0.0 ? 0.0 : ec[5];
+        double Y[5] = {0, 0, 0, 0, 0};
+        const int par = (PAT == PF_UNION_JACK) ? ((ci + j) & 1) : 0;
+        const double hxs = par ? -g.ihx : g.ihx;
+        mirror<PAT>(par, X);
+        const double kc = ec[0] / g.cw;
+        for_each_elem<PAT>(par, [&](auto T, auto S, auto A, auto B, auto C) {
+            elem_kaa<PAT, T.v, A.v, B.v, C.v>(g, hxs, ec[1 + S.v], kc, X, Y);
         });
+        mirror<PAT>(par, Y);
         c00[0] = Y[0]; c10[0] = Y[1]; c01[0] = Y[2]; c11[0] = Y[3];
         if constexpr (PAT == PF_CROSSED) {
             if (own) {
-                const double yy = is_act(cv) ? xc : Y[4];
+                const long long cv = ctr(g, ci, j);
+                const double xc = ec[5];
+                const double yy = ec[6] != 0.0 ? xc : Y[4];
                 y[cv] = yy;
                 if (FUSED) { pout[cv] = xc; acc += xc * yy; }
             }
@@ -454,29 +743,48 @@ struct OpKaa {
     }
 };
 
+// diag(Kaa) (masked: active rows 1).  cell: Gc, kappa x npc
 template <bool MASKED>
 struct OpKaaDiag : NoRed {
     static constexpr int NV = 1, NC = 1;
+    static constexpr int pd(int) { return 4; }
+    static constexpr int ne(int pat) { return 1 + npc_of(pat); }
+    static constexpr int sv(int) { return 0; }
+    static constexpr int sc(int pat) { return 1 + npc_of(pat); }
     const double* kappa;
     double* dinv;
     const unsigned char* act;
-    __device__ void load(const Geo2&, int, int, double (&v)[NV]) const { v[0] = 0.0; }
+    __device__ void issue_v(const Geo2&, int, int, const Slots&) const {}
+    __device__ void fix_v(const Geo2&, int, int, const Slots&, double (&v)[NV]) const { v[0] = 0.0; }
     template <int PAT>
-    __device__ void cell(const Geo2& g, int ci, int j, const double (&)[NV], const double (&)[NV],
-                         const double (&)[NV], const double (&)[NV], double (&c00)[NC],
-                         double (&c10)[NC], double (&c01)[NC], double (&c11)[NC], bool own) {
-        double Y[5] = {0, 0, 0, 0, 0};
+    __device__ void issue_c(const Geo2& g, int ci, int j, const Slots& s) const {
         const long long cell = cid(g, ci, j);
-        const double kc = cellGc(g, cell) / g.cw;
-        for_each_elem<PAT>((ci + j) & 1, [&](auto T, auto S, auto A, auto B, auto C) {
-            const double kap = __ldg(kappa + (long long)S.v * g.ncell + cell);
-            const double del = 2.0 * kc * g.ell * g.area[T.v];
-            const double* b = g.gb[T.v];
-            const double* c = g.gc[T.v];
-            Y[A.v] += kap + del * (b[0] * b[0] + c[0] * c[0]);
-            Y[B.v] += kap + del * (b[1] * b[1] + c[1] * c[1]);
-            Y[C.v] += kap + del * (b[2] * b[2] + c[2] * c[2]);
+        putGc(g, s, 0, cell);
+        put_kappa<PAT>(g, kappa, cell, s, 1);
+    }
+    template <int PAT, int NE>
+    __device__ void fix_c(const Geo2& g, int, int, const Slots& s, double (&e)[NE]) const {
+        e[0] = getGc(g, s, 0);
+        get_kappa<PAT>(s, 1, 1, e);
+    }
+    template <int PAT, int NE>
+    __device__ void cell(const Geo2& g, int ci, int j, const double (&)[NV], const double (&)[NV],
+                         const double (&)[NV], const double (&)[NV], const double (&ec)[NE],
+                         double (&c00)[NC], double (&c10)[NC], double (&c01)[NC], double (&c11)[NC],
+                         bool own) {
+        double Y[5] = {0, 0, 0, 0, 0};
+        const int par = (PAT == PF_UNION_JACK) ? ((ci + j) & 1) : 0;
+        const double kc = ec[0] / g.cw;
+        for_each_elem<PAT>(par, [&](auto T, auto S, auto A, auto B, auto C) {
+            const double kap = ec[1 + S.v];
+            const double del = 2.0 * kc * g.ell * g.area[0];
+            using Sh = Shp<PAT, T.v>;
+            const double X2 = g.ihx * g.ihx, Y2h = g.ihy * g.ihy;
+            Y[A.v] += kap + del * (double(Sh::b0 * Sh::b0) * X2 + double(Sh::c0 * Sh::c0) * Y2h);
+            Y[B.v] += kap + del * (double(Sh::b1 * Sh::b1) * X2 + double(Sh::c1 * Sh::c1) * Y2h);
+            Y[C.v] += kap + del * (double(Sh::b2 * Sh::b2) * X2 + double(Sh::c2 * Sh::c2) * Y2h);
         });
+        mirror<PAT>(par, Y);
         c00[0] = Y[0]; c10[0] = Y[1]; c01[0] = Y[2]; c11[0] = Y[3];
         if constexpr (PAT == PF_CROSSED) {
             if (own) {
@@ -492,13 +800,17 @@ struct OpKaaDiag : NoRed {
 };
 
 // ================================================================================================
-// Line-search trial of the damage VI (vi.py:209-220, 227-228): trial = clip(x + mu d, lb, 1)
+// Line-search trial of the damage VI (vi.py:209-220): trial = clip(x + mu d, lb, 1)
 // (d == null -> trial = x), F = Kaa trial + c, Phi = fb(trial - lb, fb(1 - trial, -F)),
-// merit = |Phi|^2, activity classification with slack zeta (vi.py:127-141):
-// act = 1 lower-active, 2 upper-active, 0 inactive; counts the inactive set.
+// merit = |Phi|^2 reduced into scal[merit_slot].
+// vertex slots: x, d, lb; cell: Gc, kappa x npc, [centre x, d, lb]
 // ================================================================================================
 struct OpKaaTrial {
-    static constexpr int NV = 1, NC = 1;
+    static constexpr int NV = 1, NC = 1, MINB = 2;
+    static constexpr int pd(int) { return 4; }
+    static constexpr int ne(int pat) { return 1 + npc_of(pat) + crossed(pat); }
+    static constexpr int sv(int) { return 3; }
+    static constexpr int sc(int pat) { return 1 + npc_of(pat) + 3 * crossed(pat); }
     const double* kappa;
     const double* cvec;
     const double* x;
@@ -506,50 +818,64 @@ struct OpKaaTrial {
     const double* lb;
     double* trial;
     double* F;
-    unsigned char* act;
     double* scal;
     int merit_slot;
     RedBuf rb;
-    double acc_m, acc_n;
+    double acc_m;
     __device__ bool enter() const { return true; }
-    __device__ __forceinline__ double tval(long long v) const {
-        const double xv = __ldg(x + v);
-        if (!d) return xv;
-        const double t = xv + scal[S_MU] * __ldg(d + v);
-        return fmin(fmax(t, __ldg(lb + v)), 1.0);
+    __device__ __forceinline__ void stage_vertex(const Slots& s, long long v) const {
+        put1(s, 0, x, v);
+        if (d) { put1(s, 1, d, v); put1(s, 2, lb, v); }
     }
-    __device__ void load(const Geo2& g, int i, int j, double (&v)[NV]) const { v[0] = tval(vid(g, i, j)); }
+    __device__ __forceinline__ double staged(const Slots& s) const {
+        const double xv = get1(s, 0);
+        if (!d) return xv;
+        return fmin(fmax(xv + scal[S_MU] * get1(s, 1), get1(s, 2)), 1.0);
+    }
+    __device__ void issue_v(const Geo2& g, int i, int j, const Slots& s) const { stage_vertex(s, vid(g, i, j)); }
+    __device__ void fix_v(const Geo2&, int, int, const Slots& s, double (&v)[NV]) const { v[0] = staged(s); }
+    template <int PAT>
+    __device__ void issue_c(const Geo2& g, int ci, int j, const Slots& s) const {
+        const long long cell = cid(g, ci, j);
+        putGc(g, s, 0, cell);
+        put_kappa<PAT>(g, kappa, cell, s, 1);
+        if constexpr (PAT == PF_CROSSED) stage_vertex(s.at(1 + npc_of(PAT)), ctr(g, ci, j));
+    }
+    template <int PAT, int NE>
+    __device__ void fix_c(const Geo2& g, int, int, const Slots& s, double (&e)[NE]) const {
+        e[0] = getGc(g, s, 0);
+        get_kappa<PAT>(s, 1, 1, e);
+        if constexpr (PAT == PF_CROSSED) e[5] = staged(s.at(1 + npc_of(PAT)));
+    }
     __device__ __forceinline__ void finish_vertex(long long id, double tv, double Fv) {
         const double l = __ldg(lb + id);
         trial[id] = tv;
         F[id] = Fv;
         const double ph = fbphi(tv - l, fbphi(1.0 - tv, -Fv));
         acc_m += ph * ph;
-        if (act) {
-            const double zeta = scal[S_ZETA];
-            const bool lo = (tv - l <= zeta) && (Fv > 0.0);
-            const bool up = (1.0 - tv <= zeta) && (Fv < 0.0) && !lo;
-            act[id] = lo ? 1 : (up ? 2 : 0);
-            acc_n += (lo || up) ? 0.0 : 1.0;
-        }
     }
-    template <int PAT>
+    template <int PAT, int NE>
     __device__ void cell(const Geo2& g, int ci, int j, const double (&vc)[NV], const double (&vn)[NV],
-                         const double (&rc)[NV], const double (&rn)[NV], double (&c00)[NC],
-                         double (&c10)[NC], double (&c01)[NC], double (&c11)[NC], bool own) {
+                         const double (&rc)[NV], const double (&rn)[NV], const double (&ec)[NE],
+                         double (&c00)[NC], double (&c10)[NC], double (&c01)[NC], double (&c11)[NC],
+                         bool own) {
         double X[5] = {vc[0], vn[0], rc[0], rn[0], 0.0};
-        long long cv = 0;
-        if constexpr (PAT == PF_CROSSED) { cv = ctr(g, ci, j); X[4] = tval(cv); }
+        if constexpr (PAT == PF_CROSSED) X[4] = ec[5];
         double Y[5] = {0, 0, 0, 0, 0};
-        const long long cell = cid(g, ci, j);
-        const double kc = cellGc(g, cell) / g.cw;
-        for_each_elem<PAT>((ci + j) & 1, [&](auto T, auto S, auto A, auto B, auto C) {
-            const double kap = __ldg(kappa + (long long)S.v * g.ncell + cell);
-            elem_kaa<T.v, A.v, B.v, C.v>(g, kap, kc, X, Y);
+        const int par = (PAT == PF_UNION_JACK) ? ((ci + j) & 1) : 0;
+        const double hxs = par ? -g.ihx : g.ihx;
+        mirror<PAT>(par, X);
+        const double kc = ec[0] / g.cw;
+        for_each_elem<PAT>(par, [&](auto T, auto S, auto A, auto B, auto C) {
+            elem_kaa<PAT, T.v, A.v, B.v, C.v>(g, hxs, ec[1 + S.v], kc, X, Y);
         });
+        mirror<PAT>(par, Y);
         c00[0] = Y[0]; c10[0] = Y[1]; c01[0] = Y[2]; c11[0] = Y[3];
         if constexpr (PAT == PF_CROSSED) {
-            if (own) finish_vertex(cv, X[4], Y[4] + __ldg(cvec + cv));
+            if (own) {
+                const long long cv = ctr(g, ci, j);
+                finish_vertex(cv, X[4], Y[4] + __ldg(cvec + cv));
+            }
         }
     }
     __device__ void out(const Geo2& g, int i, int j, const double (&t)[NC], const double (&v)[NV]) {
@@ -557,13 +883,10 @@ struct OpKaaTrial {
         finish_vertex(id, v[0], t[0] + __ldg(cvec + id));
     }
     __device__ void finish() {
-        double v[2] = {acc_m, acc_n};
+        double v[1] = {acc_m};
         double* s = scal;
         const int ms = merit_slot;
-        grid_reduce<2>(v, rb, 1, [s, ms](double* tot) {
-            s[ms] = tot[0];
-            s[S_NINACT] = tot[1];
-        });
+        grid_reduce<1>(v, rb, 1, [s, ms](double* tot) { s[ms] = tot[0]; });
     }
 };
 
@@ -571,10 +894,15 @@ struct OpKaaTrial {
 // Physics pass: energies (fem.py:162-174), r_u (fem.py:177-189), r_alpha (fem.py:202-218) and
 // the FB optimality residual (solver.py:104-118).  rows: PF_ROWS_RAW / ZERO / VALUE.
 // Reductions -> scal[S_PHYS0 ..]: E_el, E_d, |r_u|^2, |Phi|^2.
+// vertex slots: u, alpha; cell: E, Gc, [u_c, alpha_c]
 // ================================================================================================
 template <int ROWS>
 struct OpPhys {
-    static constexpr int NV = 3, NC = 3;
+    static constexpr int NV = 3, NC = 3, MINB = 2;
+    static constexpr int pd(int) { return 3; }
+    static constexpr int ne(int pat) { return 2 + 3 * crossed(pat); }
+    static constexpr int sv(int) { return 3; }
+    static constexpr int sc(int pat) { return 2 + 3 * crossed(pat); }
     const double* u;
     const double* alpha;
     const double* lb;
@@ -585,10 +913,34 @@ struct OpPhys {
     RedBuf rb;
     double eel, ed, nru, nphi;
     __device__ bool enter() const { return true; }
-    __device__ void load(const Geo2& g, int i, int j, double (&v)[NV]) const {
+    __device__ void issue_v(const Geo2& g, int i, int j, const Slots& s) const {
         const long long id = vid(g, i, j);
-        const double2 uv = ld2(u, id);
-        v[0] = uv.x; v[1] = uv.y; v[2] = __ldg(alpha + id);
+        put2(s, 0, u, id);
+        put1(s, 2, alpha, id);
+    }
+    __device__ void fix_v(const Geo2&, int, int, const Slots& s, double (&v)[NV]) const {
+        const double2 uv = get2(s, 0);
+        v[0] = uv.x; v[1] = uv.y; v[2] = get1(s, 2);
+    }
+    template <int PAT>
+    __device__ void issue_c(const Geo2& g, int ci, int j, const Slots& s) const {
+        const long long cell = cid(g, ci, j);
+        putE(g, s, 0, cell);
+        putGc(g, s, 1, cell);
+        if constexpr (PAT == PF_CROSSED) {
+            const long long cv = ctr(g, ci, j);
+            put2(s, 2, u, cv);
+            put1(s, 4, alpha, cv);
+        }
+    }
+    template <int PAT, int NE>
+    __device__ void fix_c(const Geo2& g, int, int, const Slots& s, double (&e)[NE]) const {
+        e[0] = getE(g, s, 0);
+        e[1] = getGc(g, s, 1);
+        if constexpr (PAT == PF_CROSSED) {
+            const double2 uv = get2(s, 2);
+            e[2] = uv.x; e[3] = uv.y; e[4] = get1(s, 4);
+        }
     }
     __device__ __forceinline__ void vertex_out(const Geo2& g, long long id, unsigned m, double r0,
                                                double r1, double rav, double av) {
@@ -612,59 +964,58 @@ struct OpPhys {
             nphi += ph * ph;
         }
     }
-    template <int PAT>
+    template <int PAT, int NE>
     __device__ void cell(const Geo2& g, int ci, int j, const double (&vc)[NV], const double (&vn)[NV],
-                         const double (&rc)[NV], const double (&rn)[NV], double (&c00)[NC],
-                         double (&c10)[NC], double (&c01)[NC], double (&c11)[NC], bool own) {
+                         const double (&rc)[NV], const double (&rn)[NV], const double (&ec)[NE],
+                         double (&c00)[NC], double (&c10)[NC], double (&c01)[NC], double (&c11)[NC],
+                         bool own) {
         double U1[5] = {vc[0], vn[0], rc[0], rn[0], 0.0};
         double U2[5] = {vc[1], vn[1], rc[1], rn[1], 0.0};
         double Al[5] = {vc[2], vn[2], rc[2], rn[2], 0.0};
-        long long cv = 0;
-        if constexpr (PAT == PF_CROSSED) {
-            cv = ctr(g, ci, j);
-            const double2 uv = ld2(u, cv);
-            U1[4] = uv.x; U2[4] = uv.y; Al[4] = __ldg(alpha + cv);
-        }
+        if constexpr (PAT == PF_CROSSED) { U1[4] = ec[2]; U2[4] = ec[3]; Al[4] = ec[4]; }
         double Y1[5] = {0, 0, 0, 0, 0}, Y2[5] = {0, 0, 0, 0, 0}, Ya[5] = {0, 0, 0, 0, 0};
-        const long long cell = cid(g, ci, j);
-        const double Ec = cellE(g, cell);
-        const double kc = cellGc(g, cell) / g.cw;
-        for_each_elem<PAT>((ci + j) & 1, [&](auto T, auto, auto A, auto B, auto C) {
+        const int par = (PAT == PF_UNION_JACK) ? ((ci + j) & 1) : 0;
+        const double hxs = par ? -g.ihx : g.ihx;
+        mirror<PAT>(par, U1);
+        mirror<PAT>(par, U2);
+        mirror<PAT>(par, Al);
+        const double Ec = ec[0];
+        const double kc = ec[1] / g.cw;
+        for_each_elem<PAT>(par, [&](auto T, auto, auto A, auto B, auto C) {
             const double ab = (Al[A.v] + Al[B.v] + Al[C.v]) * (1.0 / 3.0);
             const double om = 1.0 - ab;
             const double a = om * om + g.kell, ap = -2.0 * om;
             const double w = g.at2 ? ab * ab : ab, wp = g.at2 ? 2.0 * ab : 1.0;
-            const double ar = g.area[T.v];
+            const double ar = g.area[0];
             double e0, e1, e2, s0, s1, s2;
-            strain<T.v, A.v, B.v, C.v>(g, U1, U2, e0, e1, e2);
+            strain<PAT, T.v, A.v, B.v, C.v>(hxs, g.ihy, U1, U2, e0, e1, e2);
             if (g.eps0) {
-                const double e = __ldg(g.eps0 + (long long)T.v * g.ny + j);
+                const double e = __ldg(g.eps0 + (long long)(T.v + 2 * par) * g.ny + j);
                 e0 -= e; e1 -= e;
             }
             unit_stress(g, e0, e1, e2, s0, s1, s2);
             const double q = Ec * (e0 * s0 + e1 * s1 + e2 * s2);
             const double s = a * ar * Ec;
-            scatter_BT<T.v, A.v, B.v, C.v>(g, s * s0, s * s1, s * s2, Y1, Y2);
-            const double* b = g.gb[T.v];
-            const double* c = g.gc[T.v];
-            const double gx = b[0] * Al[A.v] + b[1] * Al[B.v] + b[2] * Al[C.v];
-            const double gy = c[0] * Al[A.v] + c[1] * Al[B.v] + c[2] * Al[C.v];
+            scatter_BT<PAT, T.v, A.v, B.v, C.v>(hxs, g.ihy, s * s0, s * s1, s * s2, Y1, Y2);
+            double gx, gy;
+            grad<PAT, T.v, A.v, B.v, C.v>(hxs, g.ihy, Al, gx, gy);
             const double nod = (0.5 * ap * q + kc * wp / g.ell) * ar * (1.0 / 3.0);
             const double del = 2.0 * kc * g.ell * ar;
-            Ya[A.v] += nod + del * (b[0] * gx + c[0] * gy);
-            Ya[B.v] += nod + del * (b[1] * gx + c[1] * gy);
-            Ya[C.v] += nod + del * (b[2] * gx + c[2] * gy);
+            grad_scatter<PAT, T.v, A.v, B.v, C.v>(hxs, g.ihy, nod, del * gx, del * gy, Ya);
             if (own) {
                 eel += 0.5 * ar * a * q;
                 ed += ar * kc * (w / g.ell + g.ell * (gx * gx + gy * gy));
             }
         });
+        mirror<PAT>(par, Y1);
+        mirror<PAT>(par, Y2);
+        mirror<PAT>(par, Ya);
         c00[0] = Y1[0]; c00[1] = Y2[0]; c00[2] = Ya[0];
         c10[0] = Y1[1]; c10[1] = Y2[1]; c10[2] = Ya[1];
         c01[0] = Y1[2]; c01[1] = Y2[2]; c01[2] = Ya[2];
         c11[0] = Y1[3]; c11[1] = Y2[3]; c11[2] = Ya[3];
         if constexpr (PAT == PF_CROSSED) {
-            if (own) vertex_out(g, cv, 0u, Y1[4], Y2[4], Ya[4], Al[4]);
+            if (own) vertex_out(g, ctr(g, ci, j), 0u, Y1[4], Y2[4], Ya[4], Al[4]);
         }
     }
     __device__ void out(const Geo2& g, int i, int j, const double (&t)[NC], const double (&v)[NV]) {
@@ -686,18 +1037,24 @@ struct OpPhys {
 // ================================================================================================
 // Elastic right-hand side with symmetric Dirichlet elimination (fem.py:192-199, 297-310):
 // b = M (f - K g) + (I - M) ubar = -M r_raw(g) + (I - M) ubar, g = ubar on constrained dofs.
-// With LOADONLY the output is f itself (assemble_load_u).  Reduces |b|^2 into scal[S_RR].
+// With LOADONLY the output is f itself (assemble_load_u).  Reduces |b|^2 into scal[S_AUX0].
+// vertex slots: alpha; cell: E, [alpha_c]
 // ================================================================================================
 template <bool LOADONLY>
 struct OpRhs {
-    static constexpr int NV = 3, NC = 2;
+    static constexpr int NV = 3, NC = 2, MINB = 2;
+    static constexpr int pd(int) { return 4; }
+    static constexpr int ne(int pat) { return 1 + crossed(pat); }
+    static constexpr int sv(int) { return 1; }
+    static constexpr int sc(int pat) { return 1 + crossed(pat); }
     const double* alpha;
     double* b;
     double* scal;
     RedBuf rb;
     double acc;
     __device__ bool enter() const { return true; }
-    __device__ void load(const Geo2& g, int i, int j, double (&v)[NV]) const {
+    __device__ void issue_v(const Geo2& g, int i, int j, const Slots& s) const { put1(s, 0, alpha, vid(g, i, j)); }
+    __device__ void fix_v(const Geo2& g, int i, int j, const Slots& s, double (&v)[NV]) const {
         const long long id = vid(g, i, j);
         v[0] = 0.0; v[1] = 0.0;
         if (!LOADONLY) {
@@ -708,39 +1065,56 @@ struct OpRhs {
                 if (m & 2u) v[1] = ub.y;
             }
         }
-        v[2] = __ldg(alpha + id);
+        v[2] = get1(s, 0);
     }
     template <int PAT>
+    __device__ void issue_c(const Geo2& g, int ci, int j, const Slots& s) const {
+        putE(g, s, 0, cid(g, ci, j));
+        if constexpr (PAT == PF_CROSSED) put1(s, 1, alpha, ctr(g, ci, j));
+    }
+    template <int PAT, int NE>
+    __device__ void fix_c(const Geo2& g, int, int, const Slots& s, double (&e)[NE]) const {
+        e[0] = getE(g, s, 0);
+        if constexpr (PAT == PF_CROSSED) e[1] = get1(s, 1);
+    }
+    template <int PAT, int NE>
     __device__ void cell(const Geo2& g, int ci, int j, const double (&vc)[NV], const double (&vn)[NV],
-                         const double (&rc)[NV], const double (&rn)[NV], double (&c00)[NC],
-                         double (&c10)[NC], double (&c01)[NC], double (&c11)[NC], bool own) {
+                         const double (&rc)[NV], const double (&rn)[NV], const double (&ec)[NE],
+                         double (&c00)[NC], double (&c10)[NC], double (&c01)[NC], double (&c11)[NC],
+                         bool own) {
         double U1[5] = {vc[0], vn[0], rc[0], rn[0], 0.0};
         double U2[5] = {vc[1], vn[1], rc[1], rn[1], 0.0};
         double Al[5] = {vc[2], vn[2], rc[2], rn[2], 0.0};
-        long long cv = 0;
-        if constexpr (PAT == PF_CROSSED) { cv = ctr(g, ci, j); Al[4] = __ldg(alpha + cv); }
+        if constexpr (PAT == PF_CROSSED) Al[4] = ec[1];
         double Y1[5] = {0, 0, 0, 0, 0}, Y2[5] = {0, 0, 0, 0, 0};
-        const double Ec = cellE(g, cid(g, ci, j));
-        for_each_elem<PAT>((ci + j) & 1, [&](auto T, auto, auto A, auto B, auto C) {
+        const int par = (PAT == PF_UNION_JACK) ? ((ci + j) & 1) : 0;
+        const double hxs = par ? -g.ihx : g.ihx;
+        mirror<PAT>(par, U1);
+        mirror<PAT>(par, U2);
+        mirror<PAT>(par, Al);
+        const double Ec = ec[0];
+        for_each_elem<PAT>(par, [&](auto T, auto, auto A, auto B, auto C) {
             const double ab = (Al[A.v] + Al[B.v] + Al[C.v]) * (1.0 / 3.0);
             const double om = 1.0 - ab;
-            const double s = (om * om + g.kell) * g.area[T.v] * Ec;
+            const double s = (om * om + g.kell) * g.area[0] * Ec;
             double e0 = 0.0, e1 = 0.0, e2 = 0.0, s0, s1, s2;
-            if (!LOADONLY) strain<T.v, A.v, B.v, C.v>(g, U1, U2, e0, e1, e2);
+            if (!LOADONLY) strain<PAT, T.v, A.v, B.v, C.v>(hxs, g.ihy, U1, U2, e0, e1, e2);
             if (g.eps0) {
-                const double e = __ldg(g.eps0 + (long long)T.v * g.ny + j);
+                const double e = __ldg(g.eps0 + (long long)(T.v + 2 * par) * g.ny + j);
                 e0 -= e; e1 -= e;
             }
             unit_stress(g, e0, e1, e2, s0, s1, s2);
             // r_raw = K g - f  ->  B^T s D (Bg - eps0)
-            scatter_BT<T.v, A.v, B.v, C.v>(g, s * s0, s * s1, s * s2, Y1, Y2);
+            scatter_BT<PAT, T.v, A.v, B.v, C.v>(hxs, g.ihy, s * s0, s * s1, s * s2, Y1, Y2);
         });
+        mirror<PAT>(par, Y1);
+        mirror<PAT>(par, Y2);
         c00[0] = Y1[0]; c00[1] = Y2[0]; c10[0] = Y1[1]; c10[1] = Y2[1];
         c01[0] = Y1[2]; c01[1] = Y2[2]; c11[0] = Y1[3]; c11[1] = Y2[3];
         if constexpr (PAT == PF_CROSSED) {
             if (own) {
                 const double b0 = -Y1[4], b1 = -Y2[4];
-                st2(b, cv, b0, b1);
+                st2(b, ctr(g, ci, j), b0, b1);
                 acc += b0 * b0 + b1 * b1;
             }
         }
@@ -768,60 +1142,83 @@ struct OpRhs {
 // its 3 nodes, sigma = D (B u - eps0).  Kau = Kua^T.  bcmode eliminates Dirichlet rows of Kua
 // (columns of Kau).
 // ================================================================================================
-template <int T, int A, int B, int C>
-__device__ __forceinline__ void coupling_vec(const Geo2& g, const double (&U1)[5], const double (&U2)[5],
-                                             const double (&Al)[5], double Ec, int j, double& sc,
-                                             double& s0, double& s1, double& s2) {
+template <int PAT, int T, int A, int B, int C>
+__device__ __forceinline__ void coupling_vec(const Geo2& g, double hx, int et, const double (&U1)[5],
+                                             const double (&U2)[5], const double (&Al)[5], double Ec,
+                                             int j, double& sc, double& s0, double& s1, double& s2) {
     const double ab = (Al[A] + Al[B] + Al[C]) * (1.0 / 3.0);
     const double ap = -2.0 * (1.0 - ab);
     double e0, e1, e2;
-    strain<T, A, B, C>(g, U1, U2, e0, e1, e2);
+    strain<PAT, T, A, B, C>(hx, g.ihy, U1, U2, e0, e1, e2);
     if (g.eps0) {
-        const double e = __ldg(g.eps0 + (long long)T * g.ny + j);
+        const double e = __ldg(g.eps0 + (long long)et * g.ny + j);
         e0 -= e; e1 -= e;
     }
     unit_stress(g, e0, e1, e2, s0, s1, s2);
-    sc = ap * g.area[T] * Ec * (1.0 / 3.0);
+    sc = ap * g.area[0] * Ec * (1.0 / 3.0);
 }
 
+// vertex slots: u, alpha, xa; cell: E, [u, alpha, xa centre]
 struct OpKua : NoRed {
     static constexpr int NV = 4, NC = 2;
+    static constexpr int pd(int) { return 3; }
+    static constexpr int ne(int pat) { return 1 + 4 * crossed(pat); }
+    static constexpr int sv(int) { return 4; }
+    static constexpr int sc(int pat) { return 1 + 4 * crossed(pat); }
     const double* u;
     const double* alpha;
     const double* xa;
     double* yu;
     int bcmode;
-    __device__ void load(const Geo2& g, int i, int j, double (&v)[NV]) const {
-        const long long id = vid(g, i, j);
-        const double2 uv = ld2(u, id);
-        v[0] = uv.x; v[1] = uv.y; v[2] = __ldg(alpha + id); v[3] = __ldg(xa + id);
+    __device__ __forceinline__ void stage_vertex(const Slots& s, long long v) const {
+        put2(s, 0, u, v); put1(s, 2, alpha, v); put1(s, 3, xa, v);
     }
+    __device__ __forceinline__ void staged(const Slots& s, double* v) const {
+        const double2 uv = get2(s, 0);
+        v[0] = uv.x; v[1] = uv.y; v[2] = get1(s, 2); v[3] = get1(s, 3);
+    }
+    __device__ void issue_v(const Geo2& g, int i, int j, const Slots& s) const { stage_vertex(s, vid(g, i, j)); }
+    __device__ void fix_v(const Geo2&, int, int, const Slots& s, double (&v)[NV]) const { staged(s, v); }
     template <int PAT>
+    __device__ void issue_c(const Geo2& g, int ci, int j, const Slots& s) const {
+        putE(g, s, 0, cid(g, ci, j));
+        if constexpr (PAT == PF_CROSSED) stage_vertex(s.at(1), ctr(g, ci, j));
+    }
+    template <int PAT, int NE>
+    __device__ void fix_c(const Geo2& g, int, int, const Slots& s, double (&e)[NE]) const {
+        e[0] = getE(g, s, 0);
+        if constexpr (PAT == PF_CROSSED) staged(s.at(1), e + 1);
+    }
+    template <int PAT, int NE>
     __device__ void cell(const Geo2& g, int ci, int j, const double (&vc)[NV], const double (&vn)[NV],
-                         const double (&rc)[NV], const double (&rn)[NV], double (&c00)[NC],
-                         double (&c10)[NC], double (&c01)[NC], double (&c11)[NC], bool own) {
+                         const double (&rc)[NV], const double (&rn)[NV], const double (&ec)[NE],
+                         double (&c00)[NC], double (&c10)[NC], double (&c01)[NC], double (&c11)[NC],
+                         bool own) {
         double U1[5] = {vc[0], vn[0], rc[0], rn[0], 0.0};
         double U2[5] = {vc[1], vn[1], rc[1], rn[1], 0.0};
         double Al[5] = {vc[2], vn[2], rc[2], rn[2], 0.0};
         double X[5] = {vc[3], vn[3], rc[3], rn[3], 0.0};
-        long long cv = 0;
-        if constexpr (PAT == PF_CROSSED) {
-            cv = ctr(g, ci, j);
-            const double2 uv = ld2(u, cv);
-            U1[4] = uv.x; U2[4] = uv.y; Al[4] = __ldg(alpha + cv); X[4] = __ldg(xa + cv);
-        }
+        if constexpr (PAT == PF_CROSSED) { U1[4] = ec[1]; U2[4] = ec[2]; Al[4] = ec[3]; X[4] = ec[4]; }
         double Y1[5] = {0, 0, 0, 0, 0}, Y2[5] = {0, 0, 0, 0, 0};
-        const double Ec = cellE(g, cid(g, ci, j));
-        for_each_elem<PAT>((ci + j) & 1, [&](auto T, auto, auto A, auto B, auto C) {
+        const int par = (PAT == PF_UNION_JACK) ? ((ci + j) & 1) : 0;
+        const double hxs = par ? -g.ihx : g.ihx;
+        mirror<PAT>(par, U1);
+        mirror<PAT>(par, U2);
+        mirror<PAT>(par, Al);
+        mirror<PAT>(par, X);
+        const double Ec = ec[0];
+        for_each_elem<PAT>(par, [&](auto T, auto, auto A, auto B, auto C) {
             double sc, s0, s1, s2;
-            coupling_vec<T.v, A.v, B.v, C.v>(g, U1, U2, Al, Ec, j, sc, s0, s1, s2);
+            coupling_vec<PAT, T.v, A.v, B.v, C.v>(g, hxs, T.v + 2 * par, U1, U2, Al, Ec, j, sc, s0, s1, s2);
             const double f = sc * ((X[A.v] + X[B.v]) + X[C.v]);
-            scatter_BT<T.v, A.v, B.v, C.v>(g, f * s0, f * s1, f * s2, Y1, Y2);
+            scatter_BT<PAT, T.v, A.v, B.v, C.v>(hxs, g.ihy, f * s0, f * s1, f * s2, Y1, Y2);
         });
+        mirror<PAT>(par, Y1);
+        mirror<PAT>(par, Y2);
         c00[0] = Y1[0]; c00[1] = Y2[0]; c10[0] = Y1[1]; c10[1] = Y2[1];
         c01[0] = Y1[2]; c01[1] = Y2[2]; c11[0] = Y1[3]; c11[1] = Y2[3];
         if constexpr (PAT == PF_CROSSED) {
-            if (own) st2(yu, cv, Y1[4], Y2[4]);
+            if (own) st2(yu, ctr(g, ci, j), Y1[4], Y2[4]);
         }
     }
     __device__ void out(const Geo2& g, int i, int j, const double (&t)[NC], const double (&)[NV]) {
@@ -831,50 +1228,78 @@ struct OpKua : NoRed {
     }
 };
 
+// vertex slots: u, alpha, xu; cell: E, [u, alpha, xu centre]
 struct OpKau : NoRed {
     static constexpr int NV = 5, NC = 1;
+    static constexpr int pd(int) { return 3; }
+    static constexpr int ne(int pat) { return 1 + 5 * crossed(pat); }
+    static constexpr int sv(int) { return 5; }
+    static constexpr int sc(int pat) { return 1 + 5 * crossed(pat); }
     const double* u;
     const double* alpha;
     const double* xu;
     double* ya;
     int bcmode;
-    __device__ void load(const Geo2& g, int i, int j, double (&v)[NV]) const {
-        const long long id = vid(g, i, j);
-        const double2 uv = ld2(u, id);
-        const double2 xv = ld2(xu, id);
-        const unsigned m = bcmode ? bcbits(g, i, j, id) : 0u;
-        v[0] = uv.x; v[1] = uv.y; v[2] = __ldg(alpha + id);
+    __device__ __forceinline__ void stage_vertex(const Slots& s, long long v) const {
+        put2(s, 0, u, v); put1(s, 2, alpha, v); put2(s, 3, xu, v);
+    }
+    __device__ void issue_v(const Geo2& g, int i, int j, const Slots& s) const { stage_vertex(s, vid(g, i, j)); }
+    __device__ void fix_v(const Geo2& g, int i, int j, const Slots& s, double (&v)[NV]) const {
+        const double2 uv = get2(s, 0);
+        const double2 xv = get2(s, 3);
+        const unsigned m = bcmode ? bcbits(g, i, j, vid(g, i, j)) : 0u;
+        v[0] = uv.x; v[1] = uv.y; v[2] = get1(s, 2);
         v[3] = (m & 1u) ? 0.0 : xv.x;
         v[4] = (m & 2u) ? 0.0 : xv.y;
     }
     template <int PAT>
+    __device__ void issue_c(const Geo2& g, int ci, int j, const Slots& s) const {
+        putE(g, s, 0, cid(g, ci, j));
+        if constexpr (PAT == PF_CROSSED) stage_vertex(s.at(1), ctr(g, ci, j));
+    }
+    template <int PAT, int NE>
+    __device__ void fix_c(const Geo2& g, int, int, const Slots& s, double (&e)[NE]) const {
+        e[0] = getE(g, s, 0);
+        if constexpr (PAT == PF_CROSSED) {
+            const Slots c = s.at(1);
+            const double2 uv = get2(c, 0);
+            const double2 xv = get2(c, 3);
+            e[1] = uv.x; e[2] = uv.y; e[3] = get1(c, 2); e[4] = xv.x; e[5] = xv.y;
+        }
+    }
+    template <int PAT, int NE>
     __device__ void cell(const Geo2& g, int ci, int j, const double (&vc)[NV], const double (&vn)[NV],
-                         const double (&rc)[NV], const double (&rn)[NV], double (&c00)[NC],
-                         double (&c10)[NC], double (&c01)[NC], double (&c11)[NC], bool own) {
+                         const double (&rc)[NV], const double (&rn)[NV], const double (&ec)[NE],
+                         double (&c00)[NC], double (&c10)[NC], double (&c01)[NC], double (&c11)[NC],
+                         bool own) {
         double U1[5] = {vc[0], vn[0], rc[0], rn[0], 0.0};
         double U2[5] = {vc[1], vn[1], rc[1], rn[1], 0.0};
         double Al[5] = {vc[2], vn[2], rc[2], rn[2], 0.0};
         double X1[5] = {vc[3], vn[3], rc[3], rn[3], 0.0};
         double X2[5] = {vc[4], vn[4], rc[4], rn[4], 0.0};
-        long long cv = 0;
         if constexpr (PAT == PF_CROSSED) {
-            cv = ctr(g, ci, j);
-            const double2 uv = ld2(u, cv);
-            const double2 xv = ld2(xu, cv);
-            U1[4] = uv.x; U2[4] = uv.y; Al[4] = __ldg(alpha + cv); X1[4] = xv.x; X2[4] = xv.y;
+            U1[4] = ec[1]; U2[4] = ec[2]; Al[4] = ec[3]; X1[4] = ec[4]; X2[4] = ec[5];
         }
         double Y[5] = {0, 0, 0, 0, 0};
-        const double Ec = cellE(g, cid(g, ci, j));
-        for_each_elem<PAT>((ci + j) & 1, [&](auto T, auto, auto A, auto B, auto C) {
+        const int par = (PAT == PF_UNION_JACK) ? ((ci + j) & 1) : 0;
+        const double hxs = par ? -g.ihx : g.ihx;
+        mirror<PAT>(par, U1);
+        mirror<PAT>(par, U2);
+        mirror<PAT>(par, Al);
+        mirror<PAT>(par, X1);
+        mirror<PAT>(par, X2);
+        const double Ec = ec[0];
+        for_each_elem<PAT>(par, [&](auto T, auto, auto A, auto B, auto C) {
             double sc, s0, s1, s2, d0, d1, d2;
-            coupling_vec<T.v, A.v, B.v, C.v>(g, U1, U2, Al, Ec, j, sc, s0, s1, s2);
-            strain<T.v, A.v, B.v, C.v>(g, X1, X2, d0, d1, d2);  // (B x)^T sigma = x^T B^T sigma
+            coupling_vec<PAT, T.v, A.v, B.v, C.v>(g, hxs, T.v + 2 * par, U1, U2, Al, Ec, j, sc, s0, s1, s2);
+            strain<PAT, T.v, A.v, B.v, C.v>(hxs, g.ihy, X1, X2, d0, d1, d2);  // (B x)^T sigma
             const double f = sc * (d0 * s0 + d1 * s1 + d2 * s2);
             Y[A.v] += f; Y[B.v] += f; Y[C.v] += f;
         });
+        mirror<PAT>(par, Y);
         c00[0] = Y[0]; c10[0] = Y[1]; c01[0] = Y[2]; c11[0] = Y[3];
         if constexpr (PAT == PF_CROSSED) {
-            if (own) ya[cv] = Y[4];
+            if (own) ya[ctr(g, ci, j)] = Y[4];
         }
     }
     __device__ void out(const Geo2& g, int i, int j, const double (&t)[NC], const double (&)[NV]) {
@@ -886,9 +1311,15 @@ struct OpKau : NoRed {
 // Newton: reduced coupled Jacobian [[Kuu_bc, Kua_bc], [Kau_bc, Kaa]] on the inactive set
 // (solver.py:292-296 + vi.py:235 with index extraction replaced by masks): active damage rows /
 // columns (act != 0) become identity.  One pass reads (u, alpha, x_u, x_a).
+// vertex slots: u, alpha, xu, xa, [act word]; cell: E, Gc, [centre: same as vertex]
+// ec: [E, Gc, (centre u1, u2, alpha, xu1, xu2, xa_masked, xa_raw, act)]
 // ================================================================================================
 struct OpJac : NoRed {
-    static constexpr int NV = 6, NC = 3;
+    static constexpr int NV = 6, NC = 3, MINB = 1;
+    static constexpr int pd(int pat) { return pat == PF_CROSSED ? 2 : 3; }
+    static constexpr int ne(int pat) { return 2 + 8 * crossed(pat); }
+    static constexpr int sv(int) { return 7; }
+    static constexpr int sc(int pat) { return 2 + 7 * crossed(pat); }
     const double* u;
     const double* alpha;
     const double* xu;
@@ -896,76 +1327,111 @@ struct OpJac : NoRed {
     double* yu;
     double* ya;
     const unsigned char* act;
-    __device__ void load(const Geo2& g, int i, int j, double (&v)[NV]) const {
+    __device__ __forceinline__ void stage_vertex(const Slots& s, long long v) const {
+        put2(s, 0, u, v); put1(s, 2, alpha, v); put2(s, 3, xu, v); put1(s, 5, xa, v);
+        if (act) putb(s, 6, act, v);
+    }
+    __device__ void issue_v(const Geo2& g, int i, int j, const Slots& s) const { stage_vertex(s, vid(g, i, j)); }
+    __device__ void fix_v(const Geo2& g, int i, int j, const Slots& s, double (&v)[NV]) const {
         const long long id = vid(g, i, j);
-        const double2 uv = ld2(u, id);
-        const double2 xv = ld2(xu, id);
+        const double2 uv = get2(s, 0);
+        const double2 xv = get2(s, 3);
         const unsigned m = bcbits(g, i, j, id);
-        v[0] = uv.x; v[1] = uv.y; v[2] = __ldg(alpha + id);
+        const bool a = act && getb(s, 6, id) != 0u;
+        v[0] = uv.x; v[1] = uv.y; v[2] = get1(s, 2);
         v[3] = (m & 1u) ? 0.0 : xv.x;
         v[4] = (m & 2u) ? 0.0 : xv.y;
-        v[5] = (act && act[id]) ? 0.0 : __ldg(xa + id);
+        v[5] = a ? 0.0 : get1(s, 5);
     }
     template <int PAT>
+    __device__ void issue_c(const Geo2& g, int ci, int j, const Slots& s) const {
+        const long long cell = cid(g, ci, j);
+        putE(g, s, 0, cell);
+        putGc(g, s, 1, cell);
+        if constexpr (PAT == PF_CROSSED) stage_vertex(s.at(2), ctr(g, ci, j));
+    }
+    template <int PAT, int NE>
+    __device__ void fix_c(const Geo2& g, int ci, int j, const Slots& s, double (&e)[NE]) const {
+        e[0] = getE(g, s, 0);
+        e[1] = getGc(g, s, 1);
+        if constexpr (PAT == PF_CROSSED) {
+            const Slots c = s.at(2);
+            const long long cv = ctr(g, ci, j);
+            const double2 uv = get2(c, 0);
+            const double2 xv = get2(c, 3);
+            const double xr = get1(c, 5);
+            const bool a = act && getb(c, 6, cv) != 0u;
+            e[2] = uv.x; e[3] = uv.y; e[4] = get1(c, 2); e[5] = xv.x; e[6] = xv.y;
+            e[7] = a ? 0.0 : xr; e[8] = xr; e[9] = a ? 1.0 : 0.0;
+        }
+    }
+    template <int PAT, int NE>
     __device__ void cell(const Geo2& g, int ci, int j, const double (&vc)[NV], const double (&vn)[NV],
-                         const double (&rc)[NV], const double (&rn)[NV], double (&c00)[NC],
-                         double (&c10)[NC], double (&c01)[NC], double (&c11)[NC], bool own) {
+                         const double (&rc)[NV], const double (&rn)[NV], const double (&ec)[NE],
+                         double (&c00)[NC], double (&c10)[NC], double (&c01)[NC], double (&c11)[NC],
+                         bool own) {
         double U1[5] = {vc[0], vn[0], rc[0], rn[0], 0.0};
         double U2[5] = {vc[1], vn[1], rc[1], rn[1], 0.0};
         double Al[5] = {vc[2], vn[2], rc[2], rn[2], 0.0};
         double X1[5] = {vc[3], vn[3], rc[3], rn[3], 0.0};
         double X2[5] = {vc[4], vn[4], rc[4], rn[4], 0.0};
         double Xa[5] = {vc[5], vn[5], rc[5], rn[5], 0.0};
-        long long cv = 0;
         if constexpr (PAT == PF_CROSSED) {
-            cv = ctr(g, ci, j);
-            const double2 uv = ld2(u, cv);
-            const double2 xv = ld2(xu, cv);
-            U1[4] = uv.x; U2[4] = uv.y; Al[4] = __ldg(alpha + cv); X1[4] = xv.x; X2[4] = xv.y;
-            Xa[4] = (act && act[cv]) ? 0.0 : __ldg(xa + cv);
+            U1[4] = ec[2]; U2[4] = ec[3]; Al[4] = ec[4]; X1[4] = ec[5]; X2[4] = ec[6]; Xa[4] = ec[7];
         }
         double Y1[5] = {0, 0, 0, 0, 0}, Y2[5] = {0, 0, 0, 0, 0}, Ya[5] = {0, 0, 0, 0, 0};
-        const long long cell = cid(g, ci, j);
-        const double Ec = cellE(g, cell);
-        const double kc = cellGc(g, cell) / g.cw;
-        for_each_elem<PAT>((ci + j) & 1, [&](auto T, auto, auto A, auto B, auto C) {
+        const int par = (PAT == PF_UNION_JACK) ? ((ci + j) & 1) : 0;
+        const double hxs = par ? -g.ihx : g.ihx;
+        mirror<PAT>(par, U1);
+        mirror<PAT>(par, U2);
+        mirror<PAT>(par, Al);
+        mirror<PAT>(par, X1);
+        mirror<PAT>(par, X2);
+        mirror<PAT>(par, Xa);
+        const double Ec = ec[0];
+        const double kc = ec[1] / g.cw;
+        for_each_elem<PAT>(par, [&](auto T, auto, auto A, auto B, auto C) {
             const double ab = (Al[A.v] + Al[B.v] + Al[C.v]) * (1.0 / 3.0);
             const double om = 1.0 - ab;
             const double a = om * om + g.kell, ap = -2.0 * om;
-            const double ar = g.area[T.v];
+            const double ar = g.area[0];
             double e0, e1, e2, s0, s1, s2, d0, d1, d2, t0, t1, t2;
-            strain<T.v, A.v, B.v, C.v>(g, U1, U2, e0, e1, e2);
+            strain<PAT, T.v, A.v, B.v, C.v>(hxs, g.ihy, U1, U2, e0, e1, e2);
             if (g.eps0) {
-                const double e = __ldg(g.eps0 + (long long)T.v * g.ny + j);
+                const double e = __ldg(g.eps0 + (long long)(T.v + 2 * par) * g.ny + j);
                 e0 -= e; e1 -= e;
             }
             unit_stress(g, e0, e1, e2, s0, s1, s2);          // sigma (unit E)
-            strain<T.v, A.v, B.v, C.v>(g, X1, X2, d0, d1, d2);
+            strain<PAT, T.v, A.v, B.v, C.v>(hxs, g.ihy, X1, X2, d0, d1, d2);
             unit_stress(g, d0, d1, d2, t0, t1, t2);          // D B x_u
             const double q = Ec * (e0 * s0 + e1 * s1 + e2 * s2);
             const double sxa = (Xa[A.v] + Xa[B.v]) + Xa[C.v];
             const double cpl = ap * ar * Ec * (1.0 / 3.0);
             // u rows: a|T|E B^T D B x_u + cpl * sxa * B^T sigma
             const double ka = a * ar * Ec, kb = cpl * sxa;
-            scatter_BT<T.v, A.v, B.v, C.v>(g, ka * t0 + kb * s0, ka * t1 + kb * s1,
-                                           ka * t2 + kb * s2, Y1, Y2);
+            scatter_BT<PAT, T.v, A.v, B.v, C.v>(hxs, g.ihy, ka * t0 + kb * s0, ka * t1 + kb * s1,
+                                                ka * t2 + kb * s2, Y1, Y2);
             // alpha rows: cpl * (B x_u)^T sigma + Kaa x_a
             const double kap = (q + (g.at2 ? 2.0 * kc / g.ell : 0.0)) * ar * (1.0 / 9.0);
             const double fa = cpl * (d0 * s0 + d1 * s1 + d2 * s2);
             double Yt[5] = {0, 0, 0, 0, 0};
-            elem_kaa<T.v, A.v, B.v, C.v>(g, kap, kc, Xa, Yt);
+            elem_kaa<PAT, T.v, A.v, B.v, C.v>(g, hxs, kap, kc, Xa, Yt);
             Ya[A.v] += fa + Yt[A.v];
             Ya[B.v] += fa + Yt[B.v];
             Ya[C.v] += fa + Yt[C.v];
         });
+        mirror<PAT>(par, Y1);
+        mirror<PAT>(par, Y2);
+        mirror<PAT>(par, Ya);
         c00[0] = Y1[0]; c00[1] = Y2[0]; c00[2] = Ya[0];
         c10[0] = Y1[1]; c10[1] = Y2[1]; c10[2] = Ya[1];
         c01[0] = Y1[2]; c01[1] = Y2[2]; c01[2] = Ya[2];
         c11[0] = Y1[3]; c11[1] = Y2[3]; c11[2] = Ya[3];
         if constexpr (PAT == PF_CROSSED) {
             if (own) {
+                const long long cv = ctr(g, ci, j);
                 st2(yu, cv, Y1[4], Y2[4]);
-                ya[cv] = (act && act[cv]) ? __ldg(xa + cv) : Ya[4];
+                ya[cv] = ec[9] != 0.0 ? ec[8] : Ya[4];
             }
         }
     }
@@ -1006,17 +1472,38 @@ static double alg_bytes(const Ctx* c, int kind, int nvec_r, int nvec_w) {
     }
 }
 
+template <class Op, int PAT>
+static constexpr int strip_smem() {
+    return (kBlock / 32) * Op::pd(PAT) * (Op::sv(PAT) + Op::sc(PAT)) * 256;
+}
+
+template <class Op, int PAT>
+static cudaError_t launch_pat(const Geo2& g, const Op& op, int nb, cudaStream_t st) {
+    constexpr int smem = strip_smem<Op, PAT>();
+    static_assert(smem <= 227 * 1024, "strip stage ring exceeds shared memory");
+    static bool attr = false;  // one-time opt-in above 48 KB per instantiation
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k_strip2d<Op, PAT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    k_strip2d<Op, PAT><<<nb, kBlock, smem, st>>>(g, op);
+    return cudaSuccess;
+}
+
 template <class Op>
 static int run_strip(Ctx* c, Op op, cudaStream_t st, int kind = K_VEC, int nw = 0) {
     const Geo2& g = c->g;
     const int nb = strip_blocks(g);
     if (nb > kMaxBlocksRed) return set_error(c, PF_EINVAL, "grid too large for reduction buffer");
     const int slot = prof_begin(c, st);
+    cudaError_t e;
     switch (g.pattern) {
-        case PF_UNION_JACK: k_strip2d<Op, PF_UNION_JACK><<<nb, kBlock, 0, st>>>(g, op); break;
-        case PF_RIGHT: k_strip2d<Op, PF_RIGHT><<<nb, kBlock, 0, st>>>(g, op); break;
-        default: k_strip2d<Op, PF_CROSSED><<<nb, kBlock, 0, st>>>(g, op); break;
+        case PF_UNION_JACK: e = launch_pat<Op, PF_UNION_JACK>(g, op, nb, st); break;
+        case PF_RIGHT: e = launch_pat<Op, PF_RIGHT>(g, op, nb, st); break;
+        default: e = launch_pat<Op, PF_CROSSED>(g, op, nb, st); break;
     }
+    if (e != cudaSuccess) return check_cuda(c, e, "strip kernel attribute");
     prof_end(c, st, slot, kind, alg_bytes(c, kind, 0, nw));
     c->launches++;
     return check_cuda(c, cudaGetLastError(), "strip kernel launch");
@@ -1078,7 +1565,8 @@ int launch_Kaa_diag(Ctx* c, const double* kappa, double* dinv, const unsigned ch
 int launch_Kaa_trial(Ctx* c, const double* kappa, const double* cvec, const double* x,
                      const double* d, const double* lb, double* trial, double* F,
                      unsigned char* act, int merit_slot, cudaStream_t st) {
-    OpKaaTrial op{kappa, cvec, x, d, lb, trial, F, act, c->scal, merit_slot, redbuf(c), 0.0, 0.0};
+    OpKaaTrial op{kappa, cvec, x, d, lb, trial, F, c->scal, merit_slot, redbuf(c), 0.0};
+    (void)act;
     return run_strip(c, op, st, K_KAA_TRIAL);
 }
 int launch_physics(Ctx* c, const double* u, const double* alpha, const double* lb, double* ru,

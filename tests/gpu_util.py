@@ -67,3 +67,15 @@ def rel(a, b):
     a = np.asarray(a)
     b = np.asarray(b)
     return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300))
+
+
+def symmetric_alpha_distance(alpha, ref, nx, ny):
+    """max|alpha - g(ref)| minimised over the symmetries of the structured bar problems
+    (identity, x-mirror, y-mirror, 180-degree rotation; corner vertices).  Crack nucleation
+    at a symmetric seed is a pitchfork bifurcation: which of the mirror-image branches the
+    iteration follows is decided by round-off, and both branches have identical energies
+    (the union-jack mesh is mirror symmetric, the right-diagonal mesh is 180-degree symmetric)."""
+    a = np.asarray(alpha)[: (nx + 1) * (ny + 1)].reshape(nx + 1, ny + 1)
+    r = np.asarray(ref)[: (nx + 1) * (ny + 1)].reshape(nx + 1, ny + 1)
+    cands = [r, r[::-1, :], r[:, ::-1], r[::-1, ::-1]]
+    return float(min(np.max(np.abs(a - c)) for c in cands))

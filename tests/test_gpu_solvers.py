@@ -9,7 +9,7 @@ import pytest
 import torch
 
 from conftest import GOLDEN
-from gpu_util import make_pair, random_fields, rel
+from gpu_util import make_pair, random_fields, rel, symmetric_alpha_distance
 from oracle import am as oam
 from oracle import problems as opb
 from oracle.p1 import MaterialSpec
@@ -105,7 +105,7 @@ def test_am_matches_reference_golden():
     # the nucleation transient amplifies round-off ~10x per sweep (seen CPU-vs-CPU too), so
     # the sweep count may differ slightly; the converged state must not
     assert abs(rep.am_iterations - int(G["am_its"][0])) <= 0.25 * int(G["am_its"][0])
-    assert np.max(np.abs(host(st.alpha) - G["am_alpha"])) < 1e-6
+    assert symmetric_alpha_distance(host(st.alpha), G["am_alpha"], 20, 6) < 1e-6
     assert abs(rep.energy_history[-1].total - G["am_energy_hist"][-1]) < 1e-8 * G["am_energy_hist"][-1]
 
 
@@ -118,7 +118,7 @@ def test_oram_matches_reference_golden():
     rep = pf.am_solve(st, setup.problem, pf.SolverConfig(outer_atol=1e-9, omega=1.6))
     assert rep.converged
     assert abs(rep.omega_bar_min - float(G["oram_wbmin"][0])) < 1e-15
-    assert np.max(np.abs(host(st.alpha) - G["oram_alpha"])) < 1e-6
+    assert symmetric_alpha_distance(host(st.alpha), G["oram_alpha"], 20, 6) < 1e-6
 
 
 def test_quasistatic_run_matches_reference_golden():
@@ -132,7 +132,7 @@ def test_quasistatic_run_matches_reference_golden():
     assert np.allclose(E[:, 2], ref[:, 2], rtol=1e-6, atol=0)   # north-star energy tolerance
     assert np.allclose(E[:, 1], ref[:, 1], rtol=1e-6, atol=1e-300)
     assert np.allclose(E[:, 0], ref[:, 0], rtol=1e-6, atol=0)
-    assert np.max(np.abs(recs[-1].alpha - G["run_alpha_final"])) < 1e-4
+    assert symmetric_alpha_distance(recs[-1].alpha, G["run_alpha_final"], 20, 6) < 1e-4
 
 
 def test_config1_shape_run_matches_oracle():
@@ -145,4 +145,4 @@ def test_config1_shape_run_matches_oracle():
     for r, o in zip(recs, orows):
         assert abs(r.energy.total - o.energy.total) <= 1e-6 * abs(o.energy.total)
         assert abs(r.energy.dissipated - o.energy.dissipated) <= 1e-6 * max(abs(o.energy.dissipated), 1e-30)
-        assert np.max(np.abs(r.alpha - o.alpha)) < 1e-4
+        assert symmetric_alpha_distance(r.alpha, o.alpha, 100, 10) < 1e-4
