@@ -138,6 +138,11 @@ int pf_apply_Kuu(pf_ctx* ctx, const double* alpha, const double* x, double* y, i
 /* y = Kaa(u, alpha) x  (fem.py:266-276; AT2 adds the w'' reaction). */
 int pf_apply_Kaa(pf_ctx* ctx, const double* u, const double* alpha, const double* x, double* y,
                  void* stream);
+/* Damage-block coefficients at fixed u (alpha-independent for AT1/AT2): per-element reaction
+ * kappa_e (n_elements, slot-major) and the affine remainder c = r_alpha - Kaa alpha (n_vertices;
+ * may be NULL).  pf_apply_Kaa_coef then applies Kaa from those coefficients alone. */
+int pf_kaa_coefficients(pf_ctx* ctx, const double* u, double* kappa, double* c, void* stream);
+int pf_apply_Kaa_coef(pf_ctx* ctx, const double* kappa, const double* x, double* y, void* stream);
 /* yu = Kua xa (fem.py:246-263), ya = Kua^T xu; bc_mode PF_BC_ELIMINATE zeroes Dirichlet rows. */
 int pf_apply_Kua(pf_ctx* ctx, const double* u, const double* alpha, const double* xa, double* yu,
                  int32_t bc_mode, void* stream);

@@ -71,6 +71,8 @@ EXPORTS = {
     "pf_set_eps0_rows": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "pf_apply_Kuu": (C.c_int, [C.c_void_p] * 4 + [C.c_int32, C.c_void_p]),
     "pf_apply_Kaa": (C.c_int, [C.c_void_p] * 5 + [C.c_void_p]),
+    "pf_kaa_coefficients": (C.c_int, [C.c_void_p] * 5),
+    "pf_apply_Kaa_coef": (C.c_int, [C.c_void_p] * 5),
     "pf_apply_Kua": (C.c_int, [C.c_void_p] * 5 + [C.c_int32, C.c_void_p]),
     "pf_apply_Kau": (C.c_int, [C.c_void_p] * 5 + [C.c_int32, C.c_void_p]),
     "pf_physics": (C.c_int, [C.c_void_p] * 7 + [C.c_int32, C.c_void_p, C.c_void_p]),

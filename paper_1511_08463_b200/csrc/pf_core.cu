@@ -68,12 +68,15 @@ __global__ void k_cg_init(long long n, const double* __restrict__ b, const doubl
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
         const double ri = b[i] - (zero_x0 ? 0.0 : q[i]);
-        const double zi = dinv[i] * ri;
         r[i] = ri;
-        z[i] = zi;
         acc[0] += ri * ri;
-        acc[1] += ri * zi;
+        if (dinv) {
+            const double zi = dinv[i] * ri;
+            z[i] = zi;
+            acc[1] += ri * zi;
+        }
     }
+    const bool check_rz = dinv != nullptr;
     grid_reduce<2>(acc, rb, 4, [=](double* t) {
         const double bn = sqrt(s[S_AUX0]);
         s[S_BNORM] = bn;
@@ -87,7 +90,43 @@ __global__ void k_cg_init(long long n, const double* __restrict__ b, const doubl
         s[S_RZ] = t[1];
         if (zero_x0 && bn == 0.0) { s[S_DONE] = 2.0; return; }  // x = 0 exactly (linalg.py:119-120)
         if (s[S_RNORM] <= s[S_TARGET]) { s[S_DONE] = 1.0; return; }
-        if (!(t[1] > 0.0)) s[S_FAIL] = 2.0;
+        if (check_rz && !(t[1] > 0.0)) s[S_FAIL] = 2.0;
+    });
+}
+
+// preconditioned-PCG pieces for an external preconditioner (GMG): x += gamma p; r -= gamma q; |r|
+__global__ void k_cg_update_nz(long long n, double* __restrict__ x, double* __restrict__ r,
+                               const double* __restrict__ p, const double* __restrict__ q, double* s, RedBuf rb) {
+    if (!solver_live(s)) return;
+    const double gm = s[S_GAMMA];
+    double acc[1] = {0.0};
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        x[i] += gm * p[i];
+        const double ri = r[i] - gm * q[i];
+        r[i] = ri;
+        acc[0] += ri * ri;
+    }
+    grid_reduce<1>(acc, rb, 5, [=](double* t) {
+        const double rn = sqrt(t[0]);
+        s[S_RNORM] = rn;
+        s[S_ITER] += 1.0;
+        if (rn <= s[S_TARGET]) { s[S_DONE] = 1.0; return; }
+        if (s[S_ITER] >= s[S_MAXIT]) s[S_DONE] = 3.0;
+    });
+}
+// rz = r . z ; first: S_RZ = rz ; else beta = rz / rz_old  (breakdown if rz <= 0)
+__global__ void k_cg_rz(long long n, const double* __restrict__ r, const double* __restrict__ z, double* s,
+                        RedBuf rb, int first) {
+    if (!solver_live(s)) return;
+    double acc[1] = {0.0};
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        acc[0] += r[i] * z[i];
+    grid_reduce<1>(acc, rb, 6, [=](double* t) {
+        if (!(t[0] > 0.0)) { s[S_FAIL] = 2.0; return; }
+        if (!first) s[S_BETA] = t[0] / s[S_RZ];
+        s[S_RZ] = t[0];
     });
 }
 
@@ -318,38 +357,90 @@ static int pcg_run(Ctx* c, int kind, const PcgBuffers& B, const double* coef, co
                    pf_lin_report* rep, cudaStream_t st) {
     const RedBuf rb{c->partials, c->tickets, c->scal};
     const int vb = vec_blocks(B.n);
+    const bool gmg = (kind == 2);
     // q = A x0 (if warm)
     if (!zero_x0) {
-        if (kind == 0) PF_TRY(launch_Kuu(c, coef, B.x, B.q, PF_BC_ELIMINATE, st));
+        if (kind == 0 || kind == 2) PF_TRY(launch_Kuu(c, coef, B.x, B.q, PF_BC_ELIMINATE, st));
         else PF_TRY(launch_Kaa(c, coef, B.x, B.q, act, st));
     } else {
         PF_CU(c, cudaMemsetAsync(B.x, 0, sizeof(double) * B.n, st), "memset");
     }
     {
         const int ps = prof_begin(c, st);
-        k_cg_init<<<vb, kVecBlock, 0, st>>>(B.n, B.b, B.q, B.dinv, B.r, B.z, c->scal, rb, rtol, atol,
-                                            (double)maxit, zero_x0);
+        k_cg_init<<<vb, kVecBlock, 0, st>>>(B.n, B.b, B.q, gmg ? nullptr : B.dinv, B.r, B.z, c->scal, rb, rtol,
+                                            atol, (double)maxit, zero_x0);
         prof_end(c, st, ps, K_CG_VEC, 8.0 * B.n * 5);
     }
     c->launches++;
     PF_CU(c, cudaGetLastError(), "cg init");
+    if (gmg) {
+        PF_TRY(gmg_vcycle(c, B.r, B.z, st, c->scal));
+        k_cg_rz<<<vb, kVecBlock, 0, st>>>(B.n, B.r, B.z, c->scal, rb, 1);
+        c->launches++;
+    }
     PF_TRY(read_scal(c, st, 0, 24));
+    // one Krylov iteration k (ping-pong search-direction buffers by parity)
+    auto issue_iter = [&](long long k, cudaStream_t s) -> int {
+        double* pin = (k & 1) ? B.p1 : B.p0;
+        double* pout = (k & 1) ? B.p0 : B.p1;
+        if (gmg) {
+            PF_TRY(launch_Kuu_cgA(c, coef, B.z, pin, pout, B.q, s));
+            const int ps = prof_begin(c, s);
+            k_cg_update_nz<<<vb, kVecBlock, 0, s>>>(B.n, B.x, B.r, pout, B.q, c->scal, rb);
+            prof_end(c, s, ps, K_CG_VEC, 8.0 * B.n * 6);
+            PF_TRY(gmg_vcycle(c, B.r, B.z, s, c->scal));
+            const int ps2 = prof_begin(c, s);
+            k_cg_rz<<<vb, kVecBlock, 0, s>>>(B.n, B.r, B.z, c->scal, rb, 0);
+            prof_end(c, s, ps2, K_CG_VEC, 8.0 * B.n * 2);
+            c->launches += 2;
+            return PF_OK;
+        }
+        if (kind == 0) PF_TRY(launch_Kuu_cgA(c, coef, B.z, pin, pout, B.q, s));
+        else PF_TRY(launch_Kaa_cgA(c, coef, B.z, pin, pout, B.q, act, s));
+        const int ps = prof_begin(c, s);
+        k_cg_update<<<vb, kVecBlock, 0, s>>>(B.n, B.x, B.r, B.z, pout, B.q, B.dinv, c->scal, rb);
+        prof_end(c, s, ps, K_CG_VEC, 8.0 * B.n * 8);  // x,p,r,q,dinv -> x,r,z
+        c->launches++;
+        return PF_OK;
+    };
+    // CUDA graph of an iteration pair (kernels read all scalars from device memory, so the pair
+    // is replayed unchanged); disabled while per-kernel profiling is on.
+    const bool graphs = c->use_graphs && !c->prof.on;
+    const long long key = c->geo_version * 16 + (gmg ? c->gmg_degree : 0);
+    if (graphs && c->graph_key[kind] != key) {
+        if (c->graph_exec[kind]) { cudaGraphExecDestroy(c->graph_exec[kind]); c->graph_exec[kind] = nullptr; }
+        if (!c->cap_stream) PF_CU(c, cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking), "stream");
+        PF_CU(c, cudaStreamSynchronize(st), "sync");
+        const long long l0 = c->launches;
+        PF_CU(c, cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal), "begin capture");
+        int rc1 = issue_iter(0, c->cap_stream);
+        int rc2 = rc1 == PF_OK ? issue_iter(1, c->cap_stream) : rc1;
+        cudaGraph_t graph = nullptr;
+        cudaError_t ce = cudaStreamEndCapture(c->cap_stream, &graph);
+        if (rc2 != PF_OK) return rc2;
+        PF_CU(c, ce, "end capture");
+        PF_CU(c, cudaGraphInstantiate(&c->graph_exec[kind], graph, 0), "graph instantiate");
+        cudaGraphDestroy(graph);
+        c->graph_nodes[kind] = c->launches - l0;
+        c->launches = l0;
+        c->graph_key[kind] = key;
+    }
     long long k = 0;
-    int batch = std::max(1, check_every);
+    int batch = std::max(2, check_every + (check_every & 1));
     while (c->h_scal[S_DONE] == 0.0 && c->h_scal[S_FAIL] == 0.0) {
-        for (int t = 0; t < batch; ++t, ++k) {
-            double* pin = (k & 1) ? B.p1 : B.p0;
-            double* pout = (k & 1) ? B.p0 : B.p1;
-            if (kind == 0) PF_TRY(launch_Kuu_cgA(c, coef, B.z, pin, pout, B.q, st));
-            else PF_TRY(launch_Kaa_cgA(c, coef, B.z, pin, pout, B.q, act, st));
-            const int ps = prof_begin(c, st);
-            k_cg_update<<<vb, kVecBlock, 0, st>>>(B.n, B.x, B.r, B.z, pout, B.q, B.dinv, c->scal, rb);
-            prof_end(c, st, ps, K_CG_VEC, 8.0 * B.n * 8);  // x,p,r,q,dinv -> x,r,z
-            c->launches++;
+        if (graphs) {
+            for (int t = 0; t < batch; t += 2, k += 2) {
+                PF_CU(c, cudaGraphLaunch(c->graph_exec[kind], st), "graph launch");
+                c->launches += c->graph_nodes[kind];
+            }
+        } else {
+            for (int t = 0; t < batch; ++t, ++k) PF_TRY(issue_iter(k, st));
         }
         PF_CU(c, cudaGetLastError(), "cg iteration");
         PF_TRY(read_scal(c, st, 0, 24));
-        batch = std::min(batch * 2, 64);
+        // cheap iterations (Jacobi): grow the poll interval; GMG iterations are ~100x dearer
+        // than a poll, so poll every pair to avoid launching no-op iterations after convergence
+        if (!gmg) batch = std::min(batch * 2, 64);
     }
     rep->iterations = (long long)c->h_scal[S_ITER];
     rep->final_residual_norm = c->h_scal[S_RNORM];
@@ -378,19 +469,25 @@ static int pcg_run(Ctx* c, int kind, const PcgBuffers& B, const double* coef, co
 
 int elastic_solve(Ctx* c, const double* alpha, const double* u0, double* u_out, const pf_lin_opts* o,
                   pf_lin_report* rep, cudaStream_t st) {
-    if (o->precond != PF_PREC_JACOBI)
-        return set_error(c, PF_EINVAL, "elastic solve: only PF_PREC_JACOBI is built in this version");
+    if (o->precond != PF_PREC_JACOBI && o->precond != PF_PREC_GMG)
+        return set_error(c, PF_EINVAL, "elastic solve: unknown preconditioner");
+    const bool gmg = o->precond == PF_PREC_GMG;
     PF_CU(c, cudaMemcpyAsync(c->alpha_ws, alpha, sizeof(double) * c->n_a, cudaMemcpyDeviceToDevice, st),
           "alpha copy");
     PcgBuffers B{c->cg_x, c->cg_r, c->cg_z, c->cg_p0, c->cg_p1, c->cg_q, c->cg_dinv, c->cg_b, c->n_u};
-    PF_TRY(launch_Kuu_diag(c, c->alpha_ws, B.dinv, st));
+    if (gmg) {
+        c->gmg_degree = o->cheb_degree > 0 ? o->cheb_degree : 2;
+        PF_TRY(gmg_setup(c, st));
+    } else {
+        PF_TRY(launch_Kuu_diag(c, c->alpha_ws, B.dinv, st));
+    }
     PF_TRY(launch_load(c, c->alpha_ws, B.b, nullptr, 1, st));   // b = M(f - K g) + (I-M) ubar
     const int warm = (o->warm_start && u0) ? 1 : 0;
     if (warm)
         PF_CU(c, cudaMemcpyAsync(B.x, u0, sizeof(double) * c->n_u, cudaMemcpyDeviceToDevice, st), "u0 copy");
     const long long maxit = o->maxit > 0 ? o->maxit : 10 * c->n_u;
-    int rc = pcg_run(c, 0, B, c->alpha_ws, nullptr, o->rtol, o->atol, maxit, warm ? 0 : 1,
-                     o->check_every > 0 ? o->check_every : 8, rep, st);
+    int rc = pcg_run(c, gmg ? 2 : 0, B, c->alpha_ws, nullptr, o->rtol, o->atol, maxit, warm ? 0 : 1,
+                     o->check_every > 0 ? o->check_every : (gmg ? 2 : 8), rep, st);
     if (rc != PF_OK) return rc;
     PF_CU(c, cudaMemcpyAsync(u_out, B.x, sizeof(double) * c->n_u, cudaMemcpyDeviceToDevice, st), "u copy");
     if (!rep->converged) {
@@ -600,6 +697,8 @@ static void plan_workspace(Ctx* c) {
     add((void**)&c->bits, sizeof(unsigned long long) * 8);
     c->n_newton_vec = c->n_u + c->n_a;
     add((void**)&c->newton, sizeof(double) * c->n_newton_vec * 16);
+    gmg_plan(c);
+    add((void**)&c->gmg_base, gmg_bytes(c));
     size_t tot = 0;
     for (auto& e : c->layout) tot += e.second;
     c->ws_bytes = tot;
@@ -641,6 +740,9 @@ int pf_ctx_create(const pf_desc* desc, pf_ctx** out) {
 void pf_ctx_destroy(pf_ctx* c) {
     if (!c) return;
     for (auto e : c->prof.ev) cudaEventDestroy(e);
+    for (auto& ge : c->graph_exec)
+        if (ge) cudaGraphExecDestroy(ge);
+    if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
     if (c->h_scal) cudaFreeHost(c->h_scal);
     delete c;
 }
@@ -674,6 +776,7 @@ int pf_bind_workspace(pf_ctx* c, void* p, int64_t bytes) {
     }
     c->ws = base;
     c->bound = 1;
+    gmg_bind(c, c->gmg_base);
     // zero scalars / tickets / bits / masks (synchronous; binding is a setup step)
     if (cudaMemset(c->scal, 0, sizeof(double) * S_COUNT) != cudaSuccess ||
         cudaMemset(c->tickets, 0, sizeof(unsigned) * 64) != cudaSuccess ||
@@ -699,6 +802,7 @@ int pf_set_cell_fields(pf_ctx* c, const double* E_cell, const double* Gc_cell) {
     if (!c) return PF_EINVAL;
     c->g.E_cell = E_cell;
     c->g.Gc_cell = Gc_cell;
+    c->geo_version++;
     return PF_OK;
 }
 
@@ -723,6 +827,7 @@ int pf_set_dirichlet(pf_ctx* c, const int64_t* dofs, const double* vals, int64_t
     PF_CU(c, cudaMemcpyAsync(c->ubar, ub.data(), sizeof(double) * 2 * g.nc, cudaMemcpyHostToDevice, st),
           "ubar");
     PF_CU(c, cudaStreamSynchronize(st), "sync");
+    if (c->g.has_bc != (n > 0)) c->geo_version++;
     c->g.has_bc = n > 0;
     return PF_OK;
 }
@@ -730,9 +835,11 @@ int pf_set_dirichlet(pf_ctx* c, const int64_t* dofs, const double* vals, int64_t
 int pf_set_eps0_rows(pf_ctx* c, const double* table, void* stream) {
     NEED_WS(c);
     if (!table) {
+        if (c->g.eps0) c->geo_version++;
         c->g.eps0 = nullptr;
         return PF_OK;
     }
+    if (!c->g.eps0) c->geo_version++;
     cudaStream_t st = (cudaStream_t)stream;
     PF_CU(c, cudaMemcpyAsync(c->eps0_tab, table, sizeof(double) * 4 * c->g.ny, cudaMemcpyHostToDevice, st),
           "eps0 table");
@@ -750,6 +857,14 @@ int pf_apply_Kaa(pf_ctx* c, const double* u, const double* alpha, const double* 
     cudaStream_t st = (cudaStream_t)s;
     PF_TRY(launch_kappa(c, u, alpha, c->kappa, c->vi_c, st));
     return launch_Kaa(c, c->kappa, x, y, nullptr, st);
+}
+int pf_kaa_coefficients(pf_ctx* c, const double* u, double* kappa, double* cvec, void* s) {
+    NEED_WS(c);
+    return launch_kappa(c, u, nullptr, kappa, cvec ? cvec : c->vi_c, (cudaStream_t)s);
+}
+int pf_apply_Kaa_coef(pf_ctx* c, const double* kappa, const double* x, double* y, void* s) {
+    NEED_WS(c);
+    return launch_Kaa(c, kappa, x, y, nullptr, (cudaStream_t)s);
 }
 int pf_apply_Kua(pf_ctx* c, const double* u, const double* alpha, const double* xa, double* yu, int32_t bc,
                  void* s) {

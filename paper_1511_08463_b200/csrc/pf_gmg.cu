@@ -1,0 +1,902 @@
+// pf_gmg.cu -- geometric multigrid preconditioner for the degraded elasticity operator.
+//
+// The reference solves the elastic half-step with SuperLU (linalg.py:250-262; 88 s per
+// factorisation at 512^2) or Jacobi/SSOR/Chebyshev-PCG (linalg.py:294-378; ~4000 iterations at
+// 512^2).  North-star part (3) replaces it by PCG with a Chebyshev-smoothed geometric multigrid
+// V-cycle on the structured hierarchy:
+//   level 0 : the fine mesh, matrix-free (strip kernels), block-Jacobi (2x2) Chebyshev smoother;
+//   level 1 : crossed pattern -> corner grid with centres condensed (P0: centre = mean of its cell
+//             corners); other patterns -> 2:1 coarsening;
+//   level l : 9-point 2x2-block stencils, Galerkin A_{l+1} = P^T A_l P with bilinear P and a
+//             ceil rule for odd cell counts (the last odd fine vertex is injected);
+//   coarsest: dense inverse (n <= 2*kCoarseMaxV dofs), applied as one matvec.
+// Dirichlet dofs: the fine operator is the eliminated one (fem.py:282-294); P has zero rows on
+// constrained fine dofs and zero columns on coarse dofs injected from constrained fine dofs, so
+// coarse corrections never touch them and every level stays SPD.  Coefficient jumps (cracks,
+// a = k_ell) are seen by the coarse operators because they are Galerkin products.
+// Stencil layout: A[(k*4 + e)*nv + v], k = (di+1)*3 + (dj+1) neighbour, e = 2r + c block entry.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "pf_elem.cuh"
+
+namespace pf {
+
+constexpr int kCoarseMaxV = 64;   // coarsest level: at most this many vertices (dense inverse)
+constexpr int kGB = 256;          // block size of the GMG kernels
+
+__device__ __forceinline__ bool gmg_live(const double* s) {
+    return s == nullptr || (s[S_DONE] == 0.0 && s[S_FAIL] == 0.0);
+}
+__device__ __forceinline__ void atomic_max_pos(double* addr, double v) {
+    if (v > 0.0) atomicMax(reinterpret_cast<unsigned long long*>(addr), (unsigned long long)__double_as_longlong(v));
+}
+
+// ---- element matrix blocks (setup only; runtime gradient values) ----------------------------
+// 2x2 block K_e[m][n] = s B_m^T D B_n for P1 triangles with gradients (b, c).
+__device__ __forceinline__ void ke_block(const Geo2& g, double s, double bm, double cm, double bn, double cn,
+                                         double (&K)[4]) {
+    K[0] = s * (bm * bn * g.D00 + cm * cn * g.D22);
+    K[1] = s * (bm * cn * g.D01 + cm * bn * g.D22);
+    K[2] = s * (cm * bn * g.D01 + bm * cn * g.D22);
+    K[3] = s * (cm * cn * g.D11 + bm * bn * g.D22);
+}
+
+// Gradients (b, c) of shape T's three local nodes, with the union-jack mirror sign.
+template <int PAT, int T>
+__device__ __forceinline__ void shape_grads(const Geo2& g, double hxs, double (&b)[3], double (&c)[3]) {
+    using S = Shp<PAT, T>;
+    b[0] = S::b0 * hxs; b[1] = S::b1 * hxs; b[2] = S::b2 * hxs;
+    c[0] = S::c0 * g.ihy; c[1] = S::c1 * g.ihy; c[2] = S::c2 * g.ihy;
+}
+
+// Cell matrix on the cell's local nodes (0..3 corners, 4 centre): M[(r*5 + s)][4] blocks.
+// Union-jack odd cells are handled by mirroring the local node order (see pf_elem.cuh).
+template <int PAT>
+__device__ void cell_matrix(const Geo2& g, int ci, int cj, const double* alpha, double (&M)[25][4]) {
+    const long long cell = (long long)ci * g.ny + cj;
+    const double Ec = g.E_cell ? g.E_cell[cell] : g.E;
+    double Al[5];
+    const long long v00 = (long long)ci * g.nvy + cj;
+    Al[0] = alpha[v00];
+    Al[1] = alpha[v00 + g.nvy];
+    Al[2] = alpha[v00 + 1];
+    Al[3] = alpha[v00 + g.nvy + 1];
+    Al[4] = PAT == PF_CROSSED ? alpha[g.nc + cell] : 0.0;
+    const int par = (PAT == PF_UNION_JACK) ? ((ci + cj) & 1) : 0;
+    const double hxs = par ? -g.ihx : g.ihx;
+    mirror<PAT>(par, Al);
+#pragma unroll
+    for (int k = 0; k < 25; ++k) M[k][0] = M[k][1] = M[k][2] = M[k][3] = 0.0;
+    // perm maps mirrored local slot -> physical local node
+    const int perm[5] = {par ? 1 : 0, par ? 0 : 1, par ? 3 : 2, par ? 2 : 3, 4};
+    for_each_elem<PAT>(par, [&](auto T, auto, auto A, auto B, auto C) {
+        const int nodes[3] = {A.v, B.v, C.v};
+        const double ab = (Al[A.v] + Al[B.v] + Al[C.v]) * (1.0 / 3.0);
+        const double om = 1.0 - ab;
+        const double s = (om * om + g.kell) * g.area[0] * Ec;
+        double b[3], c[3];
+        shape_grads<PAT, T.v>(g, hxs, b, c);
+        for (int m = 0; m < 3; ++m)
+            for (int n = 0; n < 3; ++n) {
+                double K[4];
+                ke_block(g, s, b[m], c[m], b[n], c[n], K);
+                const int r = perm[nodes[m]], q = perm[nodes[n]];
+                M[r * 5 + q][0] += K[0]; M[r * 5 + q][1] += K[1];
+                M[r * 5 + q][2] += K[2]; M[r * 5 + q][3] += K[3];
+            }
+    });
+}
+
+// local corner slot -> offset of that corner from the cell origin
+__device__ __forceinline__ int cdi(int k) { return (k == 1 || k == 3) ? 1 : 0; }
+__device__ __forceinline__ int cdj(int k) { return (k >= 2) ? 1 : 0; }
+
+__device__ __forceinline__ unsigned vmask(const unsigned char* mask, long long v) { return mask ? mask[v] : 0u; }
+
+// finalize a stencil row: Dirichlet elimination, block-Jacobi inverse, Gershgorin bound of D^-1 A
+__device__ void finish_row(double (&S)[9][4], unsigned mrow, const unsigned* mcol, long long v, long long nv,
+                           double* A, double* Dinv, double* lam) {
+    for (int k = 0; k < 9; ++k) {
+        for (int r = 0; r < 2; ++r)
+            for (int c = 0; c < 2; ++c) {
+                const bool kill = ((mrow >> r) & 1u) || ((mcol[k] >> c) & 1u);
+                if (kill) S[k][2 * r + c] = 0.0;
+            }
+    }
+    if (mrow & 1u) S[4][0] = 1.0;
+    if (mrow & 2u) S[4][3] = 1.0;
+    // coarse dofs with no coupling at all (fully masked support) become identity
+    if (S[4][0] == 0.0 && S[4][1] == 0.0 && S[4][2] == 0.0) S[4][0] = 1.0;
+    if (S[4][3] == 0.0 && S[4][1] == 0.0 && S[4][2] == 0.0) S[4][3] = 1.0;
+    const double a = S[4][0], b = S[4][1], c = S[4][2], d = S[4][3];
+    const double idet = 1.0 / (a * d - b * c);
+    const double Di[4] = {d * idet, -b * idet, -c * idet, a * idet};
+    double rs0 = 0.0, rs1 = 0.0;
+    for (int k = 0; k < 9; ++k) {
+        const double* B = S[k];
+        rs0 += fabs(Di[0] * B[0] + Di[1] * B[2]) + fabs(Di[0] * B[1] + Di[1] * B[3]);
+        rs1 += fabs(Di[2] * B[0] + Di[3] * B[2]) + fabs(Di[2] * B[1] + Di[3] * B[3]);
+    }
+    if (A)
+        for (int k = 0; k < 9; ++k)
+            for (int e = 0; e < 4; ++e) A[(size_t)(k * 4 + e) * nv + v] = S[k][e];
+    for (int e = 0; e < 4; ++e) Dinv[(size_t)e * nv + v] = Di[e];
+    atomic_max_pos(lam, fmax(rs0, rs1));
+}
+
+// Fine level: the true rows of A0 (all vertices, incl. crossed centres), one thread per vertex
+// -> 2x2 block-Jacobi inverse Dinv0 and the Gershgorin bound lambda_0 of D^-1 A0.
+template <int PAT>
+__global__ void k_fine_rows(const Geo2 g, const double* alpha, const unsigned char* mask, double* Dinv,
+                            double* lam) {
+    const long long nv = g.nv;
+    for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < nv;
+         v += (long long)gridDim.x * blockDim.x) {
+        // row blocks keyed by neighbour: 9 corner neighbours + 4 adjacent centres (crossed)
+        double S[13][4];
+        unsigned mcol[13];
+        for (int k = 0; k < 13; ++k) { S[k][0] = S[k][1] = S[k][2] = S[k][3] = 0.0; mcol[k] = 0u; }
+        unsigned mrow = 0u;
+        if (v < g.nc) {
+            const int i = (int)(v / g.nvy), j = (int)(v % g.nvy);
+            mrow = vmask(mask, v);
+            for (int ci = i - 1; ci <= i; ++ci)
+                for (int cj = j - 1; cj <= j; ++cj) {
+                    if (ci < 0 || cj < 0 || ci >= g.nx || cj >= g.ny) continue;
+                    double M[25][4];
+                    cell_matrix<PAT>(g, ci, cj, alpha, M);
+                    const int me = (i - ci) == 0 ? ((j - cj) == 0 ? 0 : 2) : ((j - cj) == 0 ? 1 : 3);
+                    for (int q = 0; q < (PAT == PF_CROSSED ? 5 : 4); ++q) {
+                        int k;
+                        if (q < 4) k = (ci + cdi(q) - i + 1) * 3 + (cj + cdj(q) - j + 1);
+                        else k = 9 + (ci - i + 1) * 2 + (cj - j + 1);
+                        for (int e = 0; e < 4; ++e) S[k][e] += M[me * 5 + q][e];
+                        if (q < 4) mcol[k] = vmask(mask, (long long)(ci + cdi(q)) * g.nvy + cj + cdj(q));
+                    }
+                }
+        } else {
+            const long long cell = v - g.nc;
+            const int ci = (int)(cell / g.ny), cj = (int)(cell % g.ny);
+            double M[25][4];
+            cell_matrix<PF_CROSSED>(g, ci, cj, alpha, M);
+            for (int q = 0; q < 4; ++q) {
+                for (int e = 0; e < 4; ++e) S[5 + q][e] = M[4 * 5 + q][e];
+                mcol[5 + q] = vmask(mask, (long long)(ci + cdi(q)) * g.nvy + cj + cdj(q));
+            }
+            for (int e = 0; e < 4; ++e) S[4][e] = M[4 * 5 + 4][e];
+        }
+        for (int k = 0; k < 13; ++k)
+            for (int r = 0; r < 2; ++r)
+                for (int c = 0; c < 2; ++c)
+                    if (((mrow >> r) & 1u) || ((mcol[k] >> c) & 1u)) S[k][2 * r + c] = 0.0;
+        if (mrow & 1u) S[4][0] = 1.0;
+        if (mrow & 2u) S[4][3] = 1.0;
+        const double a = S[4][0], b = S[4][1], c = S[4][2], d = S[4][3];
+        const double idet = 1.0 / (a * d - b * c);
+        const double Di[4] = {d * idet, -b * idet, -c * idet, a * idet};
+        double rs0 = 0.0, rs1 = 0.0;
+        for (int k = 0; k < 13; ++k) {
+            const double* B = S[k];
+            rs0 += fabs(Di[0] * B[0] + Di[1] * B[2]) + fabs(Di[0] * B[1] + Di[1] * B[3]);
+            rs1 += fabs(Di[2] * B[0] + Di[3] * B[2]) + fabs(Di[2] * B[1] + Di[3] * B[3]);
+        }
+        for (int e = 0; e < 4; ++e) Dinv[(size_t)e * nv + v] = Di[e];
+        atomic_max_pos(lam, fmax(rs0, rs1));
+    }
+}
+
+// ---- 1D transfer weights with the ceil rule ---------------------------------------------------
+__device__ __forceinline__ int p1d(int f, int nf, int (&c)[2], double (&w)[2]) {
+    if ((f & 1) == 0) { c[0] = f >> 1; w[0] = 1.0; return 1; }
+    if (f == nf) { c[0] = (f + 1) >> 1; w[0] = 1.0; return 1; }
+    c[0] = (f - 1) >> 1; c[1] = (f + 1) >> 1; w[0] = w[1] = 0.5; return 2;
+}
+__device__ __forceinline__ int finj(int C, int nf) { return (2 * C <= nf) ? 2 * C : nf; }
+
+// Weights of fine node `node` (local slot of cell (ci, cj): corners 0..3, centre 4) on the 3x3
+// coarse neighbourhood of coarse vertex (I, J): w[k] (k = (dK+1)*3 + dL+1), 2:1 bilinear with the
+// ceil rule; the crossed centre is the mean of its cell's corners.  Masks are applied by callers.
+__device__ __forceinline__ void node_weights(int fi, int fj, int nfx, int nfy, int I, int J, double (&w)[9]) {
+    int cx[2], cy[2];
+    double wx[2], wy[2];
+    const int nxw = p1d(fi, nfx, cx, wx), nyw = p1d(fj, nfy, cy, wy);
+    for (int a = 0; a < nxw; ++a)
+        for (int b = 0; b < nyw; ++b) {
+            const int dK = cx[a] - I, dL = cy[b] - J;
+            if (dK < -1 || dK > 1 || dL < -1 || dL > 1) continue;
+            w[(dK + 1) * 3 + (dL + 1)] += wx[a] * wy[b];
+        }
+}
+
+// First coarse level straight from the fine cell matrices (element Galerkin): one thread per
+// coarse vertex C; A1[C, C'] = sum over fine cells in C's support of w_C^T M_cell w_C'.
+template <int PAT>
+__global__ void k_galerkin_cells(const Geo2 g, const double* alpha, const unsigned char* mask0, int ncx, int ncy,
+                                 double* A1, double* Dinv1, unsigned char* mask1, double* lam) {
+    const int nvyc = ncy + 1;
+    const long long nvc = (long long)(ncx + 1) * nvyc;
+    for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < nvc;
+         v += (long long)gridDim.x * blockDim.x) {
+        const int I = (int)(v / nvyc), J = (int)(v % nvyc);
+        auto fmask = [&](int fi, int fj) -> unsigned { return vmask(mask0, (long long)fi * g.nvy + fj); };
+        const unsigned mC = fmask(finj(I, g.nx), finj(J, g.ny));
+        mask1[v] = (unsigned char)mC;
+        double S[9][4];
+        for (int k = 0; k < 9; ++k) S[k][0] = S[k][1] = S[k][2] = S[k][3] = 0.0;
+        // coarse-neighbour masks (for the column side)
+        unsigned mN[9];
+        for (int k = 0; k < 9; ++k) {
+            const int K = I + k / 3 - 1, L = J + k % 3 - 1;
+            mN[k] = (K >= 0 && L >= 0 && K <= ncx && L <= ncy) ? fmask(finj(K, g.nx), finj(L, g.ny)) : 0u;
+        }
+        for (int ci = 2 * I - 2; ci <= 2 * I + 1; ++ci) {
+            if (ci < 0 || ci >= g.nx) continue;
+            for (int cj = 2 * J - 2; cj <= 2 * J + 1; ++cj) {
+                if (cj < 0 || cj >= g.ny) continue;
+                // weights of the cell's nodes on the 3x3 coarse neighbourhood of C
+                double W[5][9];
+                unsigned nm[5];
+                for (int q = 0; q < 5; ++q)
+                    for (int k = 0; k < 9; ++k) W[q][k] = 0.0;
+                for (int q = 0; q < 4; ++q) {
+                    node_weights(ci + cdi(q), cj + cdj(q), g.nx, g.ny, I, J, W[q]);
+                    nm[q] = fmask(ci + cdi(q), cj + cdj(q));
+                }
+                nm[4] = 0u;
+                if (PAT == PF_CROSSED)
+                    for (int q = 0; q < 4; ++q)
+                        for (int k = 0; k < 9; ++k) W[4][k] += 0.25 * W[q][k];
+                // skip cells whose nodes do not interpolate from C at all
+                bool touches = false;
+                for (int q = 0; q < 5; ++q) touches |= (W[q][4] != 0.0);
+                if (!touches) continue;
+                double M[25][4];
+                cell_matrix<PAT>(g, ci, cj, alpha, M);
+                for (int m = 0; m < (PAT == PF_CROSSED ? 5 : 4); ++m) {
+                    const double wm = W[m][4];
+                    if (wm == 0.0) continue;
+                    const double wm0 = ((nm[m] | mC) & 1u) ? 0.0 : wm;
+                    const double wm1 = ((nm[m] | mC) & 2u) ? 0.0 : wm;
+                    for (int n = 0; n < (PAT == PF_CROSSED ? 5 : 4); ++n) {
+                        const double* B = M[m * 5 + n];
+                        for (int k = 0; k < 9; ++k) {
+                            const double wn = W[n][k];
+                            if (wn == 0.0) continue;
+                            const double wn0 = ((nm[n] | mN[k]) & 1u) ? 0.0 : wn;
+                            const double wn1 = ((nm[n] | mN[k]) & 2u) ? 0.0 : wn;
+                            S[k][0] += wm0 * B[0] * wn0;
+                            S[k][1] += wm0 * B[1] * wn1;
+                            S[k][2] += wm1 * B[2] * wn0;
+                            S[k][3] += wm1 * B[3] * wn1;
+                        }
+                    }
+                }
+            }
+        }
+        finish_row(S, mC, mN, v, nvc, A1, Dinv1, lam);
+    }
+}
+
+// level 0 -> level 1 restriction b1 = P0^T r0 (fine corners 2:1 bilinear, crossed centres via the
+// mean of their cell corners), one thread per coarse vertex
+__global__ void k_restrict0(const Geo2 g, const unsigned char* mask0, int ncx, int ncy, const unsigned char* mask1,
+                            const double* r, double* b1, const double* live) {
+    if (!gmg_live(live)) return;
+    const int nvyc = ncy + 1;
+    const long long nvc = (long long)(ncx + 1) * nvyc;
+    for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < nvc;
+         v += (long long)gridDim.x * blockDim.x) {
+        const int I = (int)(v / nvyc), J = (int)(v % nvyc);
+        const unsigned mC = mask1[v];
+        double s0 = 0.0, s1 = 0.0;
+        for (int fi = 2 * I - 1; fi <= 2 * I + 1; ++fi) {
+            if (fi < 0 || fi > g.nx) continue;
+            for (int fj = 2 * J - 1; fj <= 2 * J + 1; ++fj) {
+                if (fj < 0 || fj > g.ny) continue;
+                double w[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+                node_weights(fi, fj, g.nx, g.ny, I, J, w);
+                if (w[4] == 0.0) continue;
+                const long long f = (long long)fi * g.nvy + fj;
+                const unsigned mf = vmask(mask0, f);
+                const double2 rv = reinterpret_cast<const double2*>(r)[f];
+                if (!(mf & 1u)) s0 += w[4] * rv.x;
+                if (!(mf & 2u)) s1 += w[4] * rv.y;
+            }
+        }
+        if (g.pattern == PF_CROSSED) {
+            for (int ci = 2 * I - 2; ci <= 2 * I + 1; ++ci) {
+                if (ci < 0 || ci >= g.nx) continue;
+                for (int cj = 2 * J - 2; cj <= 2 * J + 1; ++cj) {
+                    if (cj < 0 || cj >= g.ny) continue;
+                    double wc = 0.0;
+                    for (int q = 0; q < 4; ++q) {
+                        double w[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+                        node_weights(ci + cdi(q), cj + cdj(q), g.nx, g.ny, I, J, w);
+                        wc += 0.25 * w[4];
+                    }
+                    if (wc == 0.0) continue;
+                    const double2 rv = reinterpret_cast<const double2*>(r)[g.nc + (long long)ci * g.ny + cj];
+                    s0 += wc * rv.x;
+                    s1 += wc * rv.y;
+                }
+            }
+        }
+        reinterpret_cast<double2*>(b1)[v] = make_double2((mC & 1u) ? 0.0 : s0, (mC & 2u) ? 0.0 : s1);
+    }
+}
+
+// level 1 -> level 0 prolongation x0 += P0 x1, one thread per fine vertex (corners + centres)
+__global__ void k_prolong0(const Geo2 g, const unsigned char* mask0, int ncx, int ncy, const unsigned char* mask1,
+                           const double* x1, double* x0, const double* live) {
+    if (!gmg_live(live)) return;
+    const int nvyc = ncy + 1;
+    for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < g.nv;
+         v += (long long)gridDim.x * blockDim.x) {
+        auto corner_val = [&](int fi, int fj, double& a0, double& a1) {
+            int cx[2], cy[2];
+            double wx[2], wy[2];
+            const int nxw = p1d(fi, g.nx, cx, wx), nyw = p1d(fj, g.ny, cy, wy);
+            a0 = 0.0; a1 = 0.0;
+            for (int a = 0; a < nxw; ++a)
+                for (int b = 0; b < nyw; ++b) {
+                    const long long cidx = (long long)cx[a] * nvyc + cy[b];
+                    const unsigned mC = mask1[cidx];
+                    const double2 xv = reinterpret_cast<const double2*>(x1)[cidx];
+                    const double w = wx[a] * wy[b];
+                    if (!(mC & 1u)) a0 += w * xv.x;
+                    if (!(mC & 2u)) a1 += w * xv.y;
+                }
+        };
+        double2 o = reinterpret_cast<double2*>(x0)[v];
+        if (v < g.nc) {
+            const int fi = (int)(v / g.nvy), fj = (int)(v % g.nvy);
+            const unsigned mf = vmask(mask0, v);
+            double a0, a1;
+            corner_val(fi, fj, a0, a1);
+            if (!(mf & 1u)) o.x += a0;
+            if (!(mf & 2u)) o.y += a1;
+        } else {  // centre: mean of its corners' interpolants (centres are never constrained)
+            const long long cell = v - g.nc;
+            const int ci = (int)(cell / g.ny), cj = (int)(cell % g.ny);
+            for (int q = 0; q < 4; ++q) {
+                double a0, a1;
+                corner_val(ci + cdi(q), cj + cdj(q), a0, a1);
+                o.x += 0.25 * a0;
+                o.y += 0.25 * a1;
+            }
+        }
+        reinterpret_cast<double2*>(x0)[v] = o;
+    }
+}
+
+struct LevelDev {
+    int nx, ny;          // cells
+    long long nv;
+    const double* A;
+    const double* Dinv;
+    const unsigned char* mask;
+};
+
+// Galerkin RAP: one thread per coarse vertex.
+__global__ void k_rap(LevelDev F, LevelDev Cd, double* Ac, double* Dinvc, unsigned char* maskc, double* lam) {
+    const int nvyf = F.ny + 1, nvyc = Cd.ny + 1;
+    for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < Cd.nv;
+         v += (long long)gridDim.x * blockDim.x) {
+        const int I = (int)(v / nvyc), J = (int)(v % nvyc);
+        const unsigned mC = F.mask ? F.mask[(long long)finj(I, F.nx) * nvyf + finj(J, F.ny)] : 0u;
+        maskc[v] = (unsigned char)mC;
+        double S[9][4];
+        for (int k = 0; k < 9; ++k) S[k][0] = S[k][1] = S[k][2] = S[k][3] = 0.0;
+        for (int fi = 2 * I - 1; fi <= 2 * I + 1; ++fi) {
+            if (fi < 0 || fi > F.nx) continue;
+            int cx[2]; double wx[2];
+            const int nxw = p1d(fi, F.nx, cx, wx);
+            double wfx = 0.0;
+            for (int a = 0; a < nxw; ++a) if (cx[a] == I) wfx = wx[a];
+            if (wfx == 0.0) continue;
+            for (int fj = 2 * J - 1; fj <= 2 * J + 1; ++fj) {
+                if (fj < 0 || fj > F.ny) continue;
+                int cy[2]; double wy[2];
+                const int nyw = p1d(fj, F.ny, cy, wy);
+                double wfy = 0.0;
+                for (int b = 0; b < nyw; ++b) if (cy[b] == J) wfy = wy[b];
+                if (wfy == 0.0) continue;
+                const long long f = (long long)fi * nvyf + fj;
+                const unsigned mf = F.mask ? F.mask[f] : 0u;
+                const double wf0 = ((mf | mC) & 1u) ? 0.0 : wfx * wfy;
+                const double wf1 = ((mf | mC) & 2u) ? 0.0 : wfx * wfy;
+                if (wf0 == 0.0 && wf1 == 0.0) continue;
+                for (int k = 0; k < 9; ++k) {
+                    const int gi = fi + k / 3 - 1, gj = fj + k % 3 - 1;
+                    if (gi < 0 || gj < 0 || gi > F.nx || gj > F.ny) continue;
+                    double B[4];
+                    for (int e = 0; e < 4; ++e) B[e] = F.A[(size_t)(k * 4 + e) * F.nv + f];
+                    if (B[0] == 0.0 && B[1] == 0.0 && B[2] == 0.0 && B[3] == 0.0) continue;
+                    const long long gv = (long long)gi * nvyf + gj;
+                    const unsigned mg = F.mask ? F.mask[gv] : 0u;
+                    int gx[2], gy[2]; double vx[2], vy[2];
+                    const int ngx = p1d(gi, F.nx, gx, vx), ngy = p1d(gj, F.ny, gy, vy);
+                    for (int a = 0; a < ngx; ++a)
+                        for (int b = 0; b < ngy; ++b) {
+                            const int K = gx[a], L = gy[b];
+                            const int dk = (K - I + 1) * 3 + (L - J + 1);
+                            const unsigned mK = F.mask ? F.mask[(long long)finj(K, F.nx) * nvyf + finj(L, F.ny)] : 0u;
+                            const double w = vx[a] * vy[b];
+                            const double wg0 = ((mg | mK) & 1u) ? 0.0 : w;
+                            const double wg1 = ((mg | mK) & 2u) ? 0.0 : w;
+                            S[dk][0] += wf0 * B[0] * wg0;
+                            S[dk][1] += wf0 * B[1] * wg1;
+                            S[dk][2] += wf1 * B[2] * wg0;
+                            S[dk][3] += wf1 * B[3] * wg1;
+                        }
+                }
+            }
+        }
+        unsigned mcol[9];
+        for (int k = 0; k < 9; ++k) {
+            const int K = I + k / 3 - 1, L = J + k % 3 - 1;
+            mcol[k] = (K >= 0 && L >= 0 && K <= Cd.nx && L <= Cd.ny && F.mask)
+                          ? F.mask[(long long)finj(K, F.nx) * nvyf + finj(L, F.ny)] : 0u;
+        }
+        finish_row(S, mC, mcol, v, Cd.nv, Ac, Dinvc, lam);
+    }
+}
+
+// Dense coarsest operator -> Cholesky -> explicit inverse, all in shared memory (single block;
+// n <= 2*kCoarseMaxV).  Once per setup.
+__global__ void k_coarse_inverse(LevelDev L, double* Ainv) {
+    extern __shared__ double Ms[];  // n*n factor
+    const int n = (int)(2 * L.nv);
+    const int nvy = L.ny + 1;
+    for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) Ms[idx] = 0.0;
+    __syncthreads();
+    for (int v = threadIdx.x; v < (int)L.nv; v += blockDim.x) {
+        const int i = v / nvy, j = v % nvy;
+        for (int k = 0; k < 9; ++k) {
+            const int ni = i + k / 3 - 1, nj = j + k % 3 - 1;
+            if (ni < 0 || nj < 0 || ni > L.nx || nj > L.ny) continue;
+            const int w = ni * nvy + nj;
+            for (int r = 0; r < 2; ++r)
+                for (int c = 0; c < 2; ++c)
+                    Ms[(2 * v + r) * n + 2 * w + c] = L.A[(size_t)(k * 4 + 2 * r + c) * L.nv + v];
+        }
+    }
+    __syncthreads();
+    for (int k = 0; k < n; ++k) {  // right-looking Cholesky, lower triangle
+        if (threadIdx.x == 0) Ms[k * n + k] = sqrt(Ms[k * n + k]);
+        __syncthreads();
+        const double piv = Ms[k * n + k];
+        for (int i = k + 1 + threadIdx.x; i < n; i += blockDim.x) Ms[i * n + k] /= piv;
+        __syncthreads();
+        const int m = n - k - 1;
+        for (int idx = threadIdx.x; idx < m * m; idx += blockDim.x) {
+            const int i = k + 1 + idx / m, j = k + 1 + idx % m;
+            if (j <= i) Ms[i * n + j] -= Ms[i * n + k] * Ms[j * n + k];
+        }
+        __syncthreads();
+    }
+    // inverse columns: L L^T x = e_c (one column per thread; results to global)
+    for (int c = threadIdx.x; c < n; c += blockDim.x) {
+        double* x = Ainv + (size_t)c * n;
+        for (int i = 0; i < n; ++i) {
+            double s = (i == c) ? 1.0 : 0.0;
+            for (int k = 0; k < i; ++k) s -= Ms[i * n + k] * x[k];
+            x[i] = s / Ms[i * n + i];
+        }
+        for (int i = n - 1; i >= 0; --i) {
+            double s = x[i];
+            for (int k = i + 1; k < n; ++k) s -= Ms[k * n + i] * x[k];
+            x[i] = s / Ms[i * n + i];
+        }
+    }
+}
+
+// x = Ainv b, one warp per row (coalesced over columns)
+__global__ void k_coarse_solve(int n, const double* Ainv, const double* b, double* x, const double* live) {
+    if (!gmg_live(live)) return;
+    const int lane = threadIdx.x & 31;
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    for (int r = warp; r < n; r += nw) {
+        double s = 0.0;
+        for (int c = lane; c < n; c += 32) s += Ainv[(size_t)r * n + c] * b[c];  // symmetric
+        s = warp_sum(s);
+        if (lane == 0) x[r] = s;
+    }
+}
+
+// ---- Chebyshev smoother pieces ----------------------------------------------------------------
+struct Cheb {
+    double theta, delta, sigma;
+};
+__device__ __forceinline__ Cheb cheb_of(const double* lam, double ratio) {
+    const double hi = *lam, lo = hi * ratio;
+    Cheb c;
+    c.theta = 0.5 * (hi + lo);
+    c.delta = 0.5 * (hi - lo);
+    c.sigma = c.theta / c.delta;
+    return c;
+}
+__device__ __forceinline__ double cheb_rho(const Cheb& c, int k) {  // rho_k, rho_0 = 1/sigma
+    double rho = 1.0 / c.sigma;
+    for (int t = 1; t <= k; ++t) rho = 1.0 / (2.0 * c.sigma - rho);
+    return rho;
+}
+__device__ __forceinline__ double2 bmul(const double* Dinv, long long nv, long long v, double r0, double r1) {
+    return make_double2(Dinv[v] * r0 + Dinv[nv + v] * r1, Dinv[2 * nv + v] * r0 + Dinv[3 * nv + v] * r1);
+}
+
+// res = D^-1 src ; d = res / theta ; x (=|+=) d
+__global__ void k_cheb0(long long nv, const double* Dinv, const double* src, double* res, double* d, double* x,
+                        int accumulate, const double* lam, double ratio, const double* live) {
+    if (!gmg_live(live)) return;
+    const Cheb c = cheb_of(lam, ratio);
+    for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < nv;
+         v += (long long)gridDim.x * blockDim.x) {
+        const double2 s = reinterpret_cast<const double2*>(src)[v];
+        const double2 r = bmul(Dinv, nv, v, s.x, s.y);
+        const double2 dd = make_double2(r.x / c.theta, r.y / c.theta);
+        reinterpret_cast<double2*>(res)[v] = r;
+        reinterpret_cast<double2*>(d)[v] = dd;
+        double2 xo = dd;
+        if (accumulate) {
+            const double2 xv = reinterpret_cast<const double2*>(x)[v];
+            xo = make_double2(xv.x + dd.x, xv.y + dd.y);
+        }
+        reinterpret_cast<double2*>(x)[v] = xo;
+    }
+}
+
+// stencil apply helper: (A d)_v
+__device__ __forceinline__ double2 st_apply(const LevelDev& L, const double* d, long long v) {
+    const int nvy = L.ny + 1;
+    const int i = (int)(v / nvy), j = (int)(v % nvy);
+    double y0 = 0.0, y1 = 0.0;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+        const int ni = i + k / 3 - 1, nj = j + k % 3 - 1;
+        if (ni < 0 || nj < 0 || ni > L.nx || nj > L.ny) continue;
+        const long long w = (long long)ni * nvy + nj;
+        const double2 dv = reinterpret_cast<const double2*>(d)[w];
+        y0 += L.A[(size_t)(k * 4 + 0) * L.nv + v] * dv.x + L.A[(size_t)(k * 4 + 1) * L.nv + v] * dv.y;
+        y1 += L.A[(size_t)(k * 4 + 2) * L.nv + v] * dv.x + L.A[(size_t)(k * 4 + 3) * L.nv + v] * dv.y;
+    }
+    return make_double2(y0, y1);
+}
+
+// One Chebyshev step k >= 1 (linalg.py:366-376): w = A d (stencil, or precomputed Ad when
+// Ad != null); res -= D^-1 w; d' = rho_k rho_{k-1} d + (2 rho_k / delta) res; x += d'.
+__global__ void k_cheb_step(LevelDev L, const double* Ad, const double* d, double* dnext, double* res, double* x,
+                            int k, const double* lam, double ratio, const double* live) {
+    if (!gmg_live(live)) return;
+    const Cheb c = cheb_of(lam, ratio);
+    const double rp = cheb_rho(c, k - 1), rn = cheb_rho(c, k);
+    const double a = rn * rp, b = 2.0 * rn / c.delta;
+    for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < L.nv;
+         v += (long long)gridDim.x * blockDim.x) {
+        const double2 w = Ad ? reinterpret_cast<const double2*>(Ad)[v] : st_apply(L, d, v);
+        const double2 dw = bmul(L.Dinv, L.nv, v, w.x, w.y);
+        double2 r = reinterpret_cast<double2*>(res)[v];
+        r.x -= dw.x;
+        r.y -= dw.y;
+        const double2 dv = reinterpret_cast<const double2*>(d)[v];
+        const double2 dn = make_double2(a * dv.x + b * r.x, a * dv.y + b * r.y);
+        reinterpret_cast<double2*>(res)[v] = r;
+        reinterpret_cast<double2*>(dnext)[v] = dn;
+        double2 xv = reinterpret_cast<double2*>(x)[v];
+        xv.x += dn.x;
+        xv.y += dn.y;
+        reinterpret_cast<double2*>(x)[v] = xv;
+    }
+}
+
+// r = b - A x (stencil) or r = b - Ax (precomputed)
+__global__ void k_resid(LevelDev L, const double* Ax, const double* x, const double* b, double* r, const double* live) {
+    if (!gmg_live(live)) return;
+    for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < L.nv;
+         v += (long long)gridDim.x * blockDim.x) {
+        const double2 w = Ax ? reinterpret_cast<const double2*>(Ax)[v] : st_apply(L, x, v);
+        const double2 bv = reinterpret_cast<const double2*>(b)[v];
+        reinterpret_cast<double2*>(r)[v] = make_double2(bv.x - w.x, bv.y - w.y);
+    }
+}
+
+// 2:1 restriction b_c = P^T r_f (with masks), one thread per coarse vertex
+__global__ void k_restrict(LevelDev F, LevelDev Cd, const unsigned char* maskc, const double* r, double* bc,
+                           const double* live) {
+    if (!gmg_live(live)) return;
+    const int nvyf = F.ny + 1, nvyc = Cd.ny + 1;
+    for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < Cd.nv;
+         v += (long long)gridDim.x * blockDim.x) {
+        const int I = (int)(v / nvyc), J = (int)(v % nvyc);
+        const unsigned mC = maskc[v];
+        double s0 = 0.0, s1 = 0.0;
+        for (int fi = 2 * I - 1; fi <= 2 * I + 1; ++fi) {
+            if (fi < 0 || fi > F.nx) continue;
+            int cx[2]; double wx[2];
+            const int nxw = p1d(fi, F.nx, cx, wx);
+            double wfx = 0.0;
+            for (int a = 0; a < nxw; ++a) if (cx[a] == I) wfx = wx[a];
+            if (wfx == 0.0) continue;
+            for (int fj = 2 * J - 1; fj <= 2 * J + 1; ++fj) {
+                if (fj < 0 || fj > F.ny) continue;
+                int cy[2]; double wy[2];
+                const int nyw = p1d(fj, F.ny, cy, wy);
+                double wfy = 0.0;
+                for (int b = 0; b < nyw; ++b) if (cy[b] == J) wfy = wy[b];
+                if (wfy == 0.0) continue;
+                const long long f = (long long)fi * nvyf + fj;
+                const unsigned mf = F.mask ? F.mask[f] : 0u;
+                const double2 rv = reinterpret_cast<const double2*>(r)[f];
+                const double w = wfx * wfy;
+                if (!(mf & 1u)) s0 += w * rv.x;
+                if (!(mf & 2u)) s1 += w * rv.y;
+            }
+        }
+        reinterpret_cast<double2*>(bc)[v] = make_double2((mC & 1u) ? 0.0 : s0, (mC & 2u) ? 0.0 : s1);
+    }
+}
+
+// 2:1 prolongation x_f += P x_c (with masks), one thread per fine vertex
+__global__ void k_prolong(LevelDev F, LevelDev Cd, const unsigned char* maskc, const double* xc, double* xf,
+                          const double* live) {
+    if (!gmg_live(live)) return;
+    const int nvyf = F.ny + 1, nvyc = Cd.ny + 1;
+    for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < F.nv;
+         v += (long long)gridDim.x * blockDim.x) {
+        const int fi = (int)(v / nvyf), fj = (int)(v % nvyf);
+        const unsigned mf = F.mask ? F.mask[v] : 0u;
+        int cx[2], cy[2]; double wx[2], wy[2];
+        const int nxw = p1d(fi, F.nx, cx, wx), nyw = p1d(fj, F.ny, cy, wy);
+        double s0 = 0.0, s1 = 0.0;
+        for (int a = 0; a < nxw; ++a)
+            for (int b = 0; b < nyw; ++b) {
+                const long long c = (long long)cx[a] * nvyc + cy[b];
+                const unsigned mC = maskc[c];
+                const double2 xv = reinterpret_cast<const double2*>(xc)[c];
+                const double w = wx[a] * wy[b];
+                if (!(mC & 1u)) s0 += w * xv.x;
+                if (!(mC & 2u)) s1 += w * xv.y;
+            }
+        double2 o = reinterpret_cast<double2*>(xf)[v];
+        if (!(mf & 1u)) o.x += s0;
+        if (!(mf & 2u)) o.y += s1;
+        reinterpret_cast<double2*>(xf)[v] = o;
+    }
+}
+
+// z_f = 0 helper + level-0 vector ops
+__global__ void k_fill0(long long n, double* x) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        x[i] = 0.0;
+}
+
+// ---- host side ----------------------------------------------------------------------------------
+static int gblocks(long long n) {
+    long long b = (n + kGB - 1) / kGB;
+    return (int)std::max(1LL, std::min(b, (long long)148 * 16));
+}
+
+void gmg_plan(Ctx* c) {
+    c->glev.clear();
+    const Geo2& g = c->g;
+    GLevel L0;
+    L0.nx = g.nx;
+    L0.ny = g.ny;
+    L0.nv = g.nv;  // incl. centres (crossed); matrix-free, no stencil
+    c->glev.push_back(L0);
+    int nx = g.nx, ny = g.ny;
+    do {  // level 1 always exists (element Galerkin); then 2:1 while above the dense size
+        nx = (nx + 1) / 2;
+        ny = (ny + 1) / 2;
+        GLevel L;
+        L.nx = nx; L.ny = ny; L.nv = (long long)(nx + 1) * (ny + 1);
+        c->glev.push_back(L);
+    } while (c->glev.back().nv > kCoarseMaxV && (nx > 1 || ny > 1));
+}
+
+size_t gmg_bytes(const Ctx* c) {
+    size_t tot = 0;
+    auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+    for (size_t l = 0; l < c->glev.size(); ++l) {
+        const GLevel& L = c->glev[l];
+        const long long nvc = (l == 0) ? c->g.nc : L.nv;
+        if (l > 0) tot += al(sizeof(double) * 36 * L.nv);
+        tot += al(sizeof(double) * 4 * L.nv);          // Dinv
+        tot += al(nvc);                                 // mask
+        tot += 7 * al(sizeof(double) * 2 * L.nv);      // x b r d0 d1 res w
+    }
+    const long long nco = 2 * c->glev.back().nv;
+    tot += 2 * al(sizeof(double) * nco * nco);
+    return tot + 4096;
+}
+
+void gmg_bind(Ctx* c, char* base) {
+    size_t off = 0;
+    auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+    auto take = [&](size_t b) { char* p = base + off; off += al(b); return p; };
+    for (size_t l = 0; l < c->glev.size(); ++l) {
+        GLevel& L = c->glev[l];
+        const long long nvc = (l == 0) ? c->g.nc : L.nv;
+        L.A = (l > 0) ? (double*)take(sizeof(double) * 36 * L.nv) : nullptr;
+        L.Dinv = (double*)take(sizeof(double) * 4 * L.nv);
+        L.mask = (unsigned char*)take(nvc);
+        L.x = (double*)take(sizeof(double) * 2 * L.nv);
+        L.b = (double*)take(sizeof(double) * 2 * L.nv);
+        L.r = (double*)take(sizeof(double) * 2 * L.nv);
+        L.d0 = (double*)take(sizeof(double) * 2 * L.nv);
+        L.d1 = (double*)take(sizeof(double) * 2 * L.nv);
+        L.res = (double*)take(sizeof(double) * 2 * L.nv);
+        L.w = (double*)take(sizeof(double) * 2 * L.nv);
+    }
+    const long long nco = 2 * c->glev.back().nv;
+    c->gmg_dense = (double*)take(sizeof(double) * nco * nco);
+    c->gmg_ainv = (double*)take(sizeof(double) * nco * nco);
+}
+
+static LevelDev ldev(const Ctx* c, int l) {
+    const GLevel& L = c->glev[l];
+    LevelDev d;
+    d.nx = L.nx;
+    d.ny = L.ny;
+    d.nv = (l == 0) ? c->g.nc : L.nv;  // stencil / transfer view of level 0 = corners
+    d.A = L.A;
+    d.Dinv = L.Dinv;
+    d.mask = L.mask;
+    return d;
+}
+
+#define GK(c, expr)                                             \
+    do {                                                        \
+        const int _ps = prof_begin((c), st);                    \
+        expr;                                                   \
+        prof_end((c), st, _ps, K_GMG, 0.0);                     \
+        (c)->launches++;                                        \
+    } while (0)
+
+// Build the hierarchy for the current alpha (c->alpha_ws) and Dirichlet mask.
+int gmg_setup(Ctx* c, cudaStream_t st) {
+    const Geo2& g = c->g;
+    const int nl = (int)c->glev.size();
+    double* lam = c->scal + S_GMG0;
+    if (cudaMemsetAsync(lam, 0, sizeof(double) * 16, st) != cudaSuccess) return set_error(c, PF_ECUDA, "memset");
+    // level-0 mask = Dirichlet mask of the corners (centres never constrained)
+    if (cudaMemcpyAsync(c->glev[0].mask, c->bcmask, g.nc, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+        return set_error(c, PF_ECUDA, "mask copy");
+    const unsigned char* m0 = g.has_bc ? c->glev[0].mask : nullptr;
+    if (!g.has_bc) cudaMemsetAsync(c->glev[0].mask, 0, g.nc, st);
+    {
+        GLevel& L1 = c->glev[1];
+        const long long nv1 = L1.nv;
+        switch (g.pattern) {
+            case PF_UNION_JACK:
+                GK(c, (k_fine_rows<PF_UNION_JACK><<<gblocks(g.nv), kGB, 0, st>>>(g, c->alpha_ws, m0, c->glev[0].Dinv, lam)));
+                GK(c, (k_galerkin_cells<PF_UNION_JACK><<<gblocks(nv1), kGB, 0, st>>>(
+                          g, c->alpha_ws, m0, L1.nx, L1.ny, L1.A, L1.Dinv, L1.mask, lam + 1)));
+                break;
+            case PF_RIGHT:
+                GK(c, (k_fine_rows<PF_RIGHT><<<gblocks(g.nv), kGB, 0, st>>>(g, c->alpha_ws, m0, c->glev[0].Dinv, lam)));
+                GK(c, (k_galerkin_cells<PF_RIGHT><<<gblocks(nv1), kGB, 0, st>>>(
+                          g, c->alpha_ws, m0, L1.nx, L1.ny, L1.A, L1.Dinv, L1.mask, lam + 1)));
+                break;
+            default:
+                GK(c, (k_fine_rows<PF_CROSSED><<<gblocks(g.nv), kGB, 0, st>>>(g, c->alpha_ws, m0, c->glev[0].Dinv, lam)));
+                GK(c, (k_galerkin_cells<PF_CROSSED><<<gblocks(nv1), kGB, 0, st>>>(
+                          g, c->alpha_ws, m0, L1.nx, L1.ny, L1.A, L1.Dinv, L1.mask, lam + 1)));
+                break;
+        }
+    }
+    for (int l = 1; l + 1 < nl; ++l) {
+        LevelDev F = ldev(c, l), Cd = ldev(c, l + 1);
+        GK(c, (k_rap<<<gblocks(Cd.nv), kGB, 0, st>>>(F, Cd, c->glev[l + 1].A, c->glev[l + 1].Dinv,
+                                                      c->glev[l + 1].mask, lam + l + 1)));
+    }
+    {
+        const int n = (int)(2 * c->glev[nl - 1].nv);
+        const int smem = (int)sizeof(double) * n * n;
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_coarse_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sizeof(double) * 4 * kCoarseMaxV * kCoarseMaxV);
+            attr = true;
+        }
+        GK(c, (k_coarse_inverse<<<1, 512, smem, st>>>(ldev(c, nl - 1), c->gmg_ainv)));
+    }
+    return check_cuda(c, cudaGetLastError(), "gmg setup");
+}
+
+// z = M r : one V-cycle, level 0 vectors are the PCG r (input) and z (output).
+int gmg_vcycle(Ctx* c, const double* r_in, double* z_out, cudaStream_t st, const double* live) {
+    const Geo2& g = c->g;
+    const int nl = (int)c->glev.size();
+    const int deg = std::max(1, c->gmg_degree);
+    const double ratio = c->gmg_ratio;
+    double* lam = c->scal + S_GMG0;
+    // descend
+    for (int l = 0; l < nl - 1; ++l) {
+        GLevel& L = c->glev[l];
+        const long long nv = L.nv;
+        const double* b = (l == 0) ? r_in : L.b;
+        double* x = (l == 0) ? z_out : L.x;
+        LevelDev Ld = ldev(c, l);
+        Ld.nv = nv;
+        // pre-smooth from x = 0
+        GK(c, (k_cheb0<<<gblocks(nv), kGB, 0, st>>>(nv, L.Dinv, b, L.res, L.d0, x, 0, lam + l, ratio, live)));
+        double* d = L.d0;
+        double* dn = L.d1;
+        for (int k = 1; k < deg; ++k) {
+            if (l == 0) {
+                PF_TRY_GMG(launch_Kuu(c, c->alpha_ws, d, L.w, PF_BC_ELIMINATE, st));
+                GK(c, (k_cheb_step<<<gblocks(nv), kGB, 0, st>>>(Ld, L.w, d, dn, L.res, x, k, lam + l, ratio, live)));
+            } else {
+                GK(c, (k_cheb_step<<<gblocks(nv), kGB, 0, st>>>(Ld, nullptr, d, dn, L.res, x, k, lam + l, ratio, live)));
+            }
+            std::swap(d, dn);
+        }
+        // residual
+        if (l == 0) {
+            PF_TRY_GMG(launch_Kuu(c, c->alpha_ws, x, L.w, PF_BC_ELIMINATE, st));
+            GK(c, (k_resid<<<gblocks(nv), kGB, 0, st>>>(Ld, L.w, x, b, L.r, live)));
+        } else {
+            GK(c, (k_resid<<<gblocks(nv), kGB, 0, st>>>(Ld, nullptr, x, b, L.r, live)));
+        }
+        // restrict
+        GLevel& C = c->glev[l + 1];
+        if (l == 0) {
+            GK(c, (k_restrict0<<<gblocks(C.nv), kGB, 0, st>>>(g, g.has_bc ? c->glev[0].mask : nullptr, C.nx, C.ny,
+                                                               C.mask, L.r, C.b, live)));
+        } else {
+            LevelDev F = ldev(c, l), Cd = ldev(c, l + 1);
+            GK(c, (k_restrict<<<gblocks(Cd.nv), kGB, 0, st>>>(F, Cd, C.mask, L.r, C.b, live)));
+        }
+    }
+    // coarsest
+    {
+        GLevel& L = c->glev[nl - 1];
+        const int n = (int)(2 * L.nv);
+        double* x = (nl == 1) ? z_out : L.x;
+        const double* b = (nl == 1) ? r_in : L.b;
+        GK(c, (k_coarse_solve<<<std::max(1, (n + 7) / 8), 256, 0, st>>>(n, c->gmg_ainv, b, x, live)));
+    }
+    // ascend
+    for (int l = nl - 2; l >= 0; --l) {
+        GLevel& L = c->glev[l];
+        GLevel& C = c->glev[l + 1];
+        const long long nv = L.nv;
+        const double* b = (l == 0) ? r_in : L.b;
+        double* x = (l == 0) ? z_out : L.x;
+        LevelDev Ld = ldev(c, l);
+        Ld.nv = nv;
+        if (l == 0) {
+            GK(c, (k_prolong0<<<gblocks(g.nv), kGB, 0, st>>>(g, g.has_bc ? c->glev[0].mask : nullptr, C.nx, C.ny,
+                                                              C.mask, C.x, x, live)));
+        } else {
+            LevelDev F = ldev(c, l), Cd = ldev(c, l + 1);
+            GK(c, (k_prolong<<<gblocks(F.nv), kGB, 0, st>>>(F, Cd, C.mask, C.x, x, live)));
+        }
+        // post-smooth: r = b - A x ; x += p(D^-1 A) D^-1 r
+        if (l == 0) {
+            PF_TRY_GMG(launch_Kuu(c, c->alpha_ws, x, L.w, PF_BC_ELIMINATE, st));
+            GK(c, (k_resid<<<gblocks(nv), kGB, 0, st>>>(Ld, L.w, x, b, L.r, live)));
+        } else {
+            GK(c, (k_resid<<<gblocks(nv), kGB, 0, st>>>(Ld, nullptr, x, b, L.r, live)));
+        }
+        GK(c, (k_cheb0<<<gblocks(nv), kGB, 0, st>>>(nv, L.Dinv, L.r, L.res, L.d0, x, 1, lam + l, ratio, live)));
+        double* d = L.d0;
+        double* dn = L.d1;
+        for (int k = 1; k < deg; ++k) {
+            if (l == 0) {
+                PF_TRY_GMG(launch_Kuu(c, c->alpha_ws, d, L.w, PF_BC_ELIMINATE, st));
+                GK(c, (k_cheb_step<<<gblocks(nv), kGB, 0, st>>>(Ld, L.w, d, dn, L.res, x, k, lam + l, ratio, live)));
+            } else {
+                GK(c, (k_cheb_step<<<gblocks(nv), kGB, 0, st>>>(Ld, nullptr, d, dn, L.res, x, k, lam + l, ratio, live)));
+            }
+            std::swap(d, dn);
+        }
+    }
+    return check_cuda(c, cudaGetLastError(), "gmg vcycle");
+}
+
+}  // namespace pf

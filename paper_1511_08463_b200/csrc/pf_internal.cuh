@@ -115,6 +115,7 @@ enum ScalarSlot {
     S_ZETA, S_NINACT, S_XMAX, S_GNORM2, S_DALPHA, S_OMEGABAR, S_AUX0, S_AUX1,
     S_PHYS0 = 32,  // 8 slots of physics-pass outputs
     S_CGVEC0 = 48,
+    S_GMG0 = 64,   // 16 slots: per-level lambda_max bounds
     S_COUNT = 128
 };
 
@@ -131,6 +132,16 @@ struct Prof {
     double ms[K_NKINDS] = {0};
     double bytes[K_NKINDS] = {0};
     long long count[K_NKINDS] = {0};
+};
+
+// ---- multigrid level (pf_gmg.cu) -------------------------------------------------------------
+struct GLevel {
+    int nx = 0, ny = 0;        // cells
+    long long nv = 0;          // vertices (level 0: incl. crossed centres)
+    double* A = nullptr;       // 9-point 2x2-block stencil [36][nv_corner] (null on crossed level 0)
+    double* Dinv = nullptr;    // 2x2 block-Jacobi inverse [4][nv]
+    unsigned char* mask = nullptr;  // Dirichlet component bits per corner vertex
+    double *x = nullptr, *b = nullptr, *r = nullptr, *d0 = nullptr, *d1 = nullptr, *res = nullptr, *w = nullptr;
 };
 
 // ---- context -------------------------------------------------------------------------
@@ -166,7 +177,27 @@ struct Ctx {
     int bound = 0;
     int blocks_per_strip_grid = 0;
     Prof prof;
+    // multigrid
+    std::vector<GLevel> glev;
+    char* gmg_base = nullptr;
+    double* gmg_dense = nullptr;
+    double* gmg_ainv = nullptr;
+    int gmg_degree = 2;
+    double gmg_ratio = 0.1;
+    // CUDA graphs of two Krylov iterations per solver kind (0 Kuu-Jacobi, 1 Kaa-masked, 2 Kuu-GMG)
+    int use_graphs = 1;
+    cudaStream_t cap_stream = nullptr;
+    cudaGraphExec_t graph_exec[3] = {nullptr, nullptr, nullptr};
+    long long graph_nodes[3] = {0, 0, 0};
+    long long graph_key[3] = {-1, -1, -1};
+    long long geo_version = 0;   // bumped whenever Geo2 fields baked into kernels change
 };
+
+#define PF_TRY_GMG(x)                   \
+    do {                                \
+        int _rc = (x);                  \
+        if (_rc != PF_OK) return _rc;   \
+    } while (0)
 
 // profiling brackets (no-ops unless enabled)
 int prof_begin(Ctx* c, cudaStream_t st);
@@ -224,6 +255,11 @@ int elastic_solve(Ctx* c, const double* alpha, const double* u0, double* u_out,
                   const pf_lin_opts* o, pf_lin_report* rep, cudaStream_t st);
 int damage_solve(Ctx* c, const double* u, const double* lb, const double* a_in, double* a_out,
                  const pf_vi_opts* o, pf_vi_report* rep, cudaStream_t st);
+void gmg_plan(Ctx* c);
+size_t gmg_bytes(const Ctx* c);
+void gmg_bind(Ctx* c, char* base);
+int gmg_setup(Ctx* c, cudaStream_t st);
+int gmg_vcycle(Ctx* c, const double* r_in, double* z_out, cudaStream_t st, const double* live);
 int newton_solve(Ctx* c, const double* u_in, const double* a_in, const double* lb, double* u_out,
                  double* a_out, const pf_vi_opts* o, pf_vi_report* rep, cudaStream_t st);
 

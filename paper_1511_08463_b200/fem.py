@@ -277,8 +277,11 @@ def assemble_Kua(state: State, problem: Discretization, apply_bc: bool = True) -
 
 
 def assemble_Kaa(state: State, problem: Discretization) -> DeviceOperator:
-    """Damage block (fem.py:266-276; AT2 adds the w'' reaction)."""
-    u, a = state.u.clone(), state.alpha.clone()
+    """Damage block (fem.py:266-276; AT2 adds the w'' reaction).  The "assembly" is one pass
+    computing the per-element reaction coefficients at the current u (the block does not
+    depend on alpha); applies then read only x and those coefficients."""
+    kappa = _empty(problem, problem.n_elements)
+    problem.call("pf_kaa_coefficients", _lib.ptr(state.u), _lib.ptr(kappa), None, _stream())
     n = problem.n_vertices
     return DeviceOperator(problem, (n, n), lambda x, y: problem.call(
-        "pf_apply_Kaa", _lib.ptr(u), _lib.ptr(a), _lib.ptr(x), _lib.ptr(y), _stream()))
+        "pf_apply_Kaa_coef", _lib.ptr(kappa), _lib.ptr(x), _lib.ptr(y), _stream()))
