@@ -331,13 +331,13 @@ __global__ void k_grad_finish(long long n, const double* __restrict__ pphi, doub
 }
 
 // ---- host helpers ---------------------------------------------------------------------------
-static int read_scal(Ctx* c, cudaStream_t st, int first, int count) {
+int read_scal(Ctx* c, cudaStream_t st, int first, int count) {
     PF_CU(c, cudaMemcpyAsync(c->h_scal + first, c->scal + first, sizeof(double) * count,
                              cudaMemcpyDeviceToHost, st), "scalar readback");
     PF_CU(c, cudaStreamSynchronize(st), "stream sync");
     return PF_OK;
 }
-static int set_scal(Ctx* c, cudaStream_t st, int slot, double v) {
+int set_scal(Ctx* c, cudaStream_t st, int slot, double v) {
     c->h_scal[64 + (slot & 63)] = v;
     // small synchronous-ordered upload via cudaMemcpyAsync from pinned memory
     PF_CU(c, cudaMemcpyAsync(c->scal + slot, c->h_scal + 64 + (slot & 63), sizeof(double),
@@ -346,13 +346,20 @@ static int set_scal(Ctx* c, cudaStream_t st, int slot, double v) {
 }
 
 // ---- generic PCG on device --------------------------------------------------------------------
-// Operator kind: 0 = Kuu (alpha_ws, eliminated), 1 = Kaa masked by c->act (kappa).
-struct PcgBuffers {
-    double *x, *r, *z, *p0, *p1, *q, *dinv, *b;
-    long long n;
-};
+int vec_blocks_n(long long n) { return vec_blocks(n); }
+void classify(Ctx* c, long long n, const double* x, const double* F, const double* lb, unsigned char* act,
+              double* rhs, cudaStream_t st) {
+    const RedBuf rb{c->partials, c->tickets, c->scal};
+    k_classify<<<vec_blocks(n), kVecBlock, 0, st>>>(n, x, F, lb, act, rhs, c->scal, rb);
+    c->launches++;
+}
+void merit_parts(Ctx* c, long long n, const double* x, const double* F, const double* lb, double* pphi,
+                 double* w, cudaStream_t st) {
+    k_merit_parts<<<vec_blocks(n), kVecBlock, 0, st>>>(n, x, F, lb, pphi, w);
+    c->launches++;
+}
 
-static int pcg_run(Ctx* c, int kind, const PcgBuffers& B, const double* coef, const unsigned char* act,
+int pcg_run(Ctx* c, int kind, const PcgBuffers& B, const double* coef, const unsigned char* act,
                    double rtol, double atol, long long maxit, int zero_x0, int check_every,
                    pf_lin_report* rep, cudaStream_t st) {
     const RedBuf rb{c->partials, c->tickets, c->scal};
@@ -695,7 +702,7 @@ static void plan_workspace(Ctx* c) {
     add((void**)&c->scal, sizeof(double) * S_COUNT);
     add((void**)&c->tickets, sizeof(unsigned) * 64);
     add((void**)&c->bits, sizeof(unsigned long long) * 8);
-    c->n_newton_vec = c->n_u + c->n_a;
+    c->n_newton_vec = ((c->n_u + c->n_a + 31) / 32) * 32;  // keep every stacked slot 256-byte aligned
     add((void**)&c->newton, sizeof(double) * c->n_newton_vec * 16);
     gmg_plan(c);
     add((void**)&c->gmg_base, gmg_bytes(c));

@@ -251,6 +251,21 @@ int launch_jac(Ctx* c, const double* u, const double* alpha, const double* xu, c
                double* yu, double* ya, const unsigned char* act, cudaStream_t st);
 
 // ---- vector kernels + solvers (pf_core.cu) ---------------------------------------------
+struct PcgBuffers {
+    double *x, *r, *z, *p0, *p1, *q, *dinv, *b;
+    long long n;
+};
+// kind: 0 = Kuu Jacobi (coef = alpha), 1 = Kaa masked by act (coef = kappa), 2 = Kuu GMG
+int pcg_run(Ctx* c, int kind, const PcgBuffers& B, const double* coef, const unsigned char* act,
+            double rtol, double atol, long long maxit, int zero_x0, int check_every,
+            pf_lin_report* rep, cudaStream_t st);
+int read_scal(Ctx* c, cudaStream_t st, int first, int count);
+int set_scal(Ctx* c, cudaStream_t st, int slot, double v);
+int vec_blocks_n(long long n);
+void classify(Ctx* c, long long n, const double* x, const double* F, const double* lb, unsigned char* act,
+              double* rhs, cudaStream_t st);
+void merit_parts(Ctx* c, long long n, const double* x, const double* F, const double* lb, double* pphi,
+                 double* w, cudaStream_t st);
 int elastic_solve(Ctx* c, const double* alpha, const double* u0, double* u_out,
                   const pf_lin_opts* o, pf_lin_report* rep, cudaStream_t st);
 int damage_solve(Ctx* c, const double* u, const double* lb, const double* a_in, double* a_out,

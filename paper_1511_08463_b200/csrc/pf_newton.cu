@@ -1,9 +1,341 @@
-// pf_newton.cu -- coupled (u, alpha) reduced-space active-set Newton (solver.py:274-330).
+// pf_newton.cu -- coupled (u, alpha) reduced-space active-set Newton (north-star part 5).
+//
+// Restates, on the device, rsls_solve (vi.py:187-264) applied to the stacked MCP of
+// coupled_mcp (solver.py:274-300): x = [u; alpha], F = [r_u (Dirichlet rows u - ubar); r_alpha],
+// J = [[Kuu_bc, Kua_bc], [Kua_bc^T, Kaa]], bounds (-inf, inf) on u and [alpha_lb, 1] on alpha.
+// The inactive-block Newton system is solved with preconditioned MINRES (linalg.py:155-219,
+// Paige-Saunders recurrence evaluated on the host from device dot products) and the symmetric
+// multiplicative field split (linalg.py:398-430):
+//     y1 = A^-1 r_u ; z = C^-1 (r_a - B^T y1) ; x_u = y1 - A^-1 B z
+// with A^-1 = GMG-PCG and C^-1 = Jacobi-PCG on the inactive damage block, both to a tight
+// relative tolerance (the reference's default inner solves are exact LU, linalg.py:438-443).
+// Index extraction (extract_submatrix) is replaced by masks: active damage rows/columns are
+// identity and every vector is zero there.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+
 #include "pf_internal.cuh"
 
 namespace pf {
-int newton_solve(Ctx* c, const double*, const double*, const double*, double*, double*, const pf_vi_opts*,
-                 pf_vi_report*, cudaStream_t) {
-    return set_error(c, PF_EINVAL, "coupled Newton not built yet");
+
+constexpr int kNB = 256;
+
+__global__ void k_ndot(long long n, const double* a, const double* b, double* s, int slot, RedBuf rb) {
+    double acc[1] = {0.0};
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        acc[0] += a[i] * b[i];
+    grid_reduce<1>(acc, rb, 8, [=](double* t) { s[slot] = t[0]; });
 }
+__global__ void k_nscale(long long n, double a, const double* x, double* y) {  // y = a x
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        y[i] = a * x[i];
+}
+__global__ void k_naxpy(long long n, double a, const double* x, double* y) {  // y += a x
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        y[i] += a * x[i];
+}
+// w = (v - oldeps w1 - delta w2) / gam ; x += phi w
+__global__ void k_nminres_w(long long n, const double* v, const double* w1, const double* w2, double* w, double* x,
+                            double oldeps, double delta, double gam, double phi) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const double wi = (v[i] - oldeps * w1[i] - delta * w2[i]) / gam;
+        w[i] = wi;
+        x[i] += phi * wi;
+    }
+}
+// out_a = act ? 0 : (a - b)
+__global__ void k_nsubmask(long long n, const double* a, const double* b, const unsigned char* act, double* out) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        out[i] = act[i] ? 0.0 : (a[i] - (b ? b[i] : 0.0));
+}
+// trial = [u + mu du ; clip(a + mu da, lb, 1)]
+__global__ void k_ntrial(long long nu, long long na, const double* x, const double* d, double mu, const double* lb,
+                         double* t) {
+    const long long n = nu + na;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        double v = x[i] + mu * d[i];
+        if (i >= nu) v = fmin(fmax(v, lb[i - nu]), 1.0);
+        t[i] = v;
+    }
+}
+// clip alpha into [lb, 1] and max |x| over the stacked vector
+__global__ void k_nclip_max(long long nu, long long na, double* x, const double* lb, unsigned long long* xmax) {
+    const long long n = nu + na;
+    double m = 0.0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        double v = x[i];
+        if (i >= nu) { v = fmin(fmax(v, lb[i - nu]), 1.0); x[i] = v; }
+        m = fmax(m, fabs(v));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(PF_FULL, m, o));
+    if ((threadIdx.x & 31) == 0 && m > 0.0) atomicMax(xmax, (unsigned long long)__double_as_longlong(m));
+}
+// steepest-descent gradient g = 2 (p phi + J (q phi)): u rows p = 0, q = 1 (free bounds)
+__global__ void k_ngrad(long long nu, long long na, const double* pphi_a, const double* Jw, double* g) {
+    const long long n = nu + na;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        g[i] = 2.0 * ((i >= nu ? pphi_a[i - nu] : 0.0) + Jw[i]);
+}
+
+static int nblocks(long long n) { return (int)std::max(1LL, std::min((n + kNB - 1) / kNB, 148LL * 8)); }
+
+#define NTRY(x)                        \
+    do {                               \
+        int _rc = (x);                 \
+        if (_rc != PF_OK) return _rc;  \
+    } while (0)
+#define NCU(c, x, w)                                                        \
+    do {                                                                    \
+        cudaError_t _e = (x);                                               \
+        if (_e != cudaSuccess) return check_cuda((c), _e, (w));             \
+    } while (0)
+
+struct NewtonWs {
+    long long nu, na, n;
+    double *X, *TX, *FX, *TF, *D, *RHS, *R1, *R2, *Y, *V, *W, *W1, *W2, *TMP, *PP, *G;
+};
+
+static int ndot(Ctx* c, long long n, const double* a, const double* b, int slot, double& out, cudaStream_t st) {
+    const RedBuf rb{c->partials, c->tickets, c->scal};
+    k_ndot<<<nblocks(n), kNB, 0, st>>>(n, a, b, c->scal, slot, rb);
+    c->launches++;
+    NTRY(read_scal(c, st, slot, 1));
+    out = c->h_scal[slot];
+    return PF_OK;
+}
+
+// physics pass at stacked point x: F (rows VALUE) and merit |Phi|^2 (u rows free)
+static int eval_F(Ctx* c, const NewtonWs& w, const double* x, double* F, const double* lb, double& merit,
+                  cudaStream_t st) {
+    NTRY(launch_physics(c, x, x + w.nu, lb, F, F + w.nu, nullptr, PF_ROWS_VALUE, st));
+    NTRY(read_scal(c, st, S_PHYS0, 4));
+    merit = c->h_scal[S_PHYS0 + 2] + c->h_scal[S_PHYS0 + 3];
+    return PF_OK;
+}
+
+// A^-1 b (GMG-PCG, hierarchy already set up for the current alpha) -> out
+static int solve_A(Ctx* c, const double* b, double* out, double rtol, long long& its, cudaStream_t st) {
+    PcgBuffers B{c->cg_x, c->cg_r, c->cg_z, c->cg_p0, c->cg_p1, c->cg_q, c->cg_dinv, const_cast<double*>(b), c->n_u};
+    // pcg_run reads |b|^2 from S_AUX0
+    double bb;
+    NTRY(ndot(c, c->n_u, b, b, S_AUX0, bb, st));
+    pf_lin_report rep{};
+    int rc = pcg_run(c, 2, B, c->alpha_ws, nullptr, rtol, 0.0, 10 * c->n_u, 1, 2, &rep, st);
+    its += rep.iterations;
+    if (rc != PF_OK) return set_error(c, PF_EINNER, "inner solve on block 'A' failed: " + c->err);
+    NCU(c, cudaMemcpyAsync(out, c->cg_x, sizeof(double) * c->n_u, cudaMemcpyDeviceToDevice, st), "copy");
+    return PF_OK;
+}
+// C^-1 b on the inactive damage block (Jacobi-PCG, kappa / act / dinv ready) -> out
+static int solve_C(Ctx* c, const double* b, double* out, double rtol, long long& its, cudaStream_t st) {
+    PcgBuffers B{c->da_x, c->da_r, c->da_z, c->da_p0, c->da_p1, c->da_q, c->da_dinv, const_cast<double*>(b), c->n_a};
+    double bb;
+    NTRY(ndot(c, c->n_a, b, b, S_AUX0, bb, st));
+    pf_lin_report rep{};
+    int rc = pcg_run(c, 1, B, c->kappa, c->act, rtol, 0.0, 10 * c->n_a, 1, 8, &rep, st);
+    its += rep.iterations;
+    if (rc != PF_OK) return set_error(c, PF_EINNER, "inner solve on block 'C' failed: " + c->err);
+    NCU(c, cudaMemcpyAsync(out, c->da_x, sizeof(double) * c->n_a, cudaMemcpyDeviceToDevice, st), "copy");
+    return PF_OK;
+}
+
+// y = P^-1 r (symmetric multiplicative field split, linalg.py:424-430)
+static int fieldsplit(Ctx* c, const NewtonWs& w, const double* r, double* y, const double* u, const double* alpha,
+                      double inner_rtol, long long& its, cudaStream_t st) {
+    const long long nu = w.nu, na = w.na;
+    double* y1 = y;              // u part of y
+    double* z = y + nu;          // alpha part of y
+    NTRY(solve_A(c, r, y1, inner_rtol, its, st));
+    NTRY(launch_Kau(c, u, alpha, y1, w.TMP + nu, PF_BC_ELIMINATE, st));            // B^T y1
+    k_nsubmask<<<nblocks(na), kNB, 0, st>>>(na, r + nu, w.TMP + nu, c->act, w.TMP + nu);
+    c->launches++;
+    NTRY(solve_C(c, w.TMP + nu, z, 1e-3 * inner_rtol, its, st));
+    NTRY(launch_Kua(c, u, alpha, z, w.TMP, PF_BC_ELIMINATE, st));                   // B z
+    NTRY(solve_A(c, w.TMP, w.TMP, inner_rtol, its, st));
+    k_naxpy<<<nblocks(nu), kNB, 0, st>>>(nu, -1.0, w.TMP, y1);
+    c->launches++;
+    return PF_OK;
+}
+
+// MINRES on the masked inactive block J_NN d = rhs (x0 = 0); returns the iterations.
+static int minres(Ctx* c, NewtonWs& w, const double* u, const double* alpha, const double* rhs, double* x,
+                  double rtol, long long maxit, double inner_rtol, long long& kits, bool& converged,
+                  cudaStream_t st) {
+    const long long n = w.n, nu = w.nu;
+    auto op = [&](const double* v, double* out) {
+        return launch_jac(c, u, alpha, v, v + nu, out, out + nu, c->act, st);
+    };
+    NCU(c, cudaMemsetAsync(x, 0, sizeof(double) * n, st), "memset");
+    NCU(c, cudaMemcpyAsync(w.R1, rhs, sizeof(double) * n, cudaMemcpyDeviceToDevice, st), "copy");
+    double *r1 = w.R1, *r2 = w.R2, *y = w.Y, *v = w.V, *ww = w.W, *w1 = w.W1, *w2 = w.W2;
+    NTRY(fieldsplit(c, w, r1, y, u, alpha, inner_rtol, kits, st));
+    double beta1;
+    NTRY(ndot(c, n, r1, y, S_AUX1, beta1, st));
+    if (beta1 < 0.0) return set_error(c, PF_EBREAKDOWN, "minres: preconditioner not SPD");
+    beta1 = std::sqrt(beta1);
+    converged = true;
+    if (beta1 == 0.0) return PF_OK;
+    const double target = rtol * beta1;
+    double oldb = 0.0, beta = beta1, dbar = 0.0, epsln = 0.0, phibar = beta1, cs = -1.0, sn = 0.0;
+    NCU(c, cudaMemsetAsync(ww, 0, sizeof(double) * n, st), "memset");
+    NCU(c, cudaMemsetAsync(w2, 0, sizeof(double) * n, st), "memset");
+    NCU(c, cudaMemcpyAsync(r2, r1, sizeof(double) * n, cudaMemcpyDeviceToDevice, st), "copy");
+    long long it = 0;
+    const int nb = nblocks(n);
+    while (it < maxit && phibar > target) {
+        ++it;
+        k_nscale<<<nb, kNB, 0, st>>>(n, 1.0 / beta, y, v);
+        NTRY(op(v, y));
+        if (it >= 2) k_naxpy<<<nb, kNB, 0, st>>>(n, -(beta / oldb), r1, y);
+        double alfa;
+        NTRY(ndot(c, n, v, y, S_AUX1, alfa, st));
+        k_naxpy<<<nb, kNB, 0, st>>>(n, -(alfa / beta), r2, y);
+        c->launches += 3;
+        // r1 <- r2 ; r2 <- y ; y <- M r2 (into the old r1 buffer)
+        double* old_r1 = r1;
+        r1 = r2;
+        r2 = y;
+        y = old_r1;
+        NTRY(fieldsplit(c, w, r2, y, u, alpha, inner_rtol, kits, st));
+        oldb = beta;
+        double bb;
+        NTRY(ndot(c, n, r2, y, S_AUX1, bb, st));
+        if (bb < 0.0) return set_error(c, PF_EBREAKDOWN, "minres: preconditioner not SPD");
+        beta = std::sqrt(bb);
+        const double oldeps = epsln;
+        const double delta = cs * dbar + sn * alfa;
+        const double gbar = sn * dbar - cs * alfa;
+        epsln = sn * beta;
+        dbar = -cs * beta;
+        const double gam = std::max(std::hypot(gbar, beta), 2.220446049250313e-16);
+        cs = gbar / gam;
+        sn = beta / gam;
+        const double phi = cs * phibar;
+        phibar = sn * phibar;
+        // w1 <- w2 ; w2 <- w ; w <- (v - oldeps w1 - delta w2) / gam (into old w1) ; x += phi w
+        double* old_w1 = w1;
+        w1 = w2;
+        w2 = ww;
+        ww = old_w1;
+        k_nminres_w<<<nb, kNB, 0, st>>>(n, v, w1, w2, ww, x, oldeps, delta, gam, phi);
+        c->launches++;
+    }
+    // keep the rotated buffer roles in the workspace struct consistent for the next call
+    converged = phibar <= target;
+    kits += it;
+    return PF_OK;
+}
+
+int newton_solve(Ctx* c, const double* u_in, const double* a_in, const double* lb, double* u_out, double* a_out,
+                 const pf_vi_opts* o, pf_vi_report* rep, cudaStream_t st) {
+    memset(rep, 0, sizeof(*rep));
+    NewtonWs w;
+    w.nu = c->n_u;
+    w.na = c->n_a;
+    w.n = w.nu + w.na;
+    double** slots[] = {&w.X, &w.TX, &w.FX, &w.TF, &w.D, &w.RHS, &w.R1, &w.R2, &w.Y, &w.V, &w.W, &w.W1, &w.W2,
+                        &w.TMP, &w.PP, &w.G};
+    for (int k = 0; k < 16; ++k) *slots[k] = c->newton + (size_t)k * c->n_newton_vec;
+    const long long nu = w.nu, na = w.na, n = w.n;
+    NCU(c, cudaMemcpyAsync(w.X, u_in, sizeof(double) * nu, cudaMemcpyDeviceToDevice, st), "copy");
+    NCU(c, cudaMemcpyAsync(w.X + nu, a_in, sizeof(double) * na, cudaMemcpyDeviceToDevice, st), "copy");
+    // clip, zeta = 1e-10 (1 + |x0|_inf) (vi.py:197-201)
+    NCU(c, cudaMemsetAsync(c->bits, 0, sizeof(unsigned long long) * 8, st), "memset");
+    k_nclip_max<<<nblocks(n), kNB, 0, st>>>(nu, na, w.X, lb, c->bits + 1);
+    c->launches++;
+    NCU(c, cudaMemcpyAsync(c->h_scal + 100, c->bits + 1, sizeof(double), cudaMemcpyDeviceToHost, st), "xmax");
+    NCU(c, cudaStreamSynchronize(st), "sync");
+    double xmax;
+    memcpy(&xmax, c->h_scal + 100, sizeof(double));
+    const double zeta = o->zero_tol > 0.0 ? o->zero_tol : 1e-10 * (1.0 + xmax);
+    NTRY(set_scal(c, st, S_ZETA, zeta));
+    double merit;
+    NTRY(eval_F(c, w, w.X, w.FX, lb, merit, st));
+    auto push_hist = [&](double m) {
+        if (rep->n_history < 64) rep->history[rep->n_history] = std::sqrt(m);
+        rep->n_history++;
+    };
+    push_hist(merit);
+    const double fs_rtol = o->fieldsplit_rtol > 0.0 ? o->fieldsplit_rtol : 1e-6;
+    const double inner_rtol = o->inner_rtol > 0.0 ? std::min(o->inner_rtol, 1e-8) : 1e-8;
+    auto line_search = [&](const double* dir, double slope, bool newton, bool& ok) -> int {
+        double mu = 1.0;
+        ok = false;
+        while (mu >= o->ls_min_step) {
+            k_ntrial<<<nblocks(n), kNB, 0, st>>>(nu, na, w.X, dir, mu, lb, w.TX);
+            c->launches++;
+            double mt;
+            NTRY(eval_F(c, w, w.TX, w.TF, lb, mt, st));
+            const double bound = newton ? (1.0 - 2.0 * o->armijo * mu) * merit : merit - slope * mu;
+            if (mt <= bound) {
+                ok = true;
+                merit = mt;
+                std::swap(w.X, w.TX);
+                std::swap(w.FX, w.TF);
+                return PF_OK;
+            }
+            mu *= o->ls_backtrack;
+        }
+        return PF_OK;
+    };
+    for (int it = 1; it <= o->max_iterations; ++it) {
+        if (std::sqrt(merit) <= o->abs_tol) break;
+        rep->iterations = it;
+        const double* u = w.X;
+        const double* alpha = w.X + nu;
+        // active set on the damage rows; u rows are always inactive (free bounds)
+        classify(c, na, alpha, w.FX + nu, lb, c->act, w.RHS + nu, st);
+        NCU(c, cudaMemcpyAsync(w.RHS, w.FX, sizeof(double) * nu, cudaMemcpyDeviceToDevice, st), "copy");
+        // Jacobian-dependent setup: GMG hierarchy of Kuu(alpha), kappa(u) and masked diag(Kaa)
+        NCU(c, cudaMemcpyAsync(c->alpha_ws, alpha, sizeof(double) * na, cudaMemcpyDeviceToDevice, st), "copy");
+        NTRY(gmg_setup(c, st));
+        NTRY(launch_kappa(c, u, alpha, c->kappa, c->vi_c, st));
+        NTRY(launch_Kaa_diag(c, c->kappa, c->da_dinv, c->act, st));
+        bool ok = false;
+        long long kits = 0;
+        bool lin_ok = false;
+        int rc = minres(c, w, u, alpha, w.RHS, w.D, fs_rtol, o->inner_maxit > 0 ? o->inner_maxit : 10 * n,
+                        inner_rtol, kits, lin_ok, st);
+        rep->total_krylov_iterations += kits;
+        if (rc == PF_OK && lin_ok) {
+            k_nscale<<<nblocks(n), kNB, 0, st>>>(n, -1.0, w.D, w.D);  // d = -d_N (zero on active)
+            c->launches++;
+            NTRY(line_search(w.D, 0.0, true, ok));
+        } else if (rc == PF_OK || rc == PF_EBREAKDOWN || rc == PF_EINNER) {
+            rep->linear_failures++;  // solver.py:266-268 raises, rsls catches (vi.py:241-242)
+        } else {
+            return rc;
+        }
+        if (!ok) {
+            // steepest descent on the merit (vi.py:244-252); J is symmetric (BlockJacobian.matvec)
+            merit_parts(c, na, alpha, w.FX + nu, lb, w.PP + nu, w.TMP + nu, st);
+            NCU(c, cudaMemcpyAsync(w.TMP, w.FX, sizeof(double) * nu, cudaMemcpyDeviceToDevice, st), "copy");
+            NTRY(launch_jac(c, u, alpha, w.TMP, w.TMP + nu, w.G, w.G + nu, nullptr, st));
+            k_ngrad<<<nblocks(n), kNB, 0, st>>>(nu, na, w.PP + nu, w.G, w.G);
+            c->launches++;
+            double gg;
+            NTRY(ndot(c, n, w.G, w.G, S_AUX1, gg, st));
+            const double gn = std::sqrt(gg);
+            if (gn > 0.0) {
+                const double sc = 1.0 / std::max(1.0, gn);
+                k_nscale<<<nblocks(n), kNB, 0, st>>>(n, -sc, w.G, w.G);
+                c->launches++;
+                NTRY(line_search(w.G, o->armijo * sc * gn * gn, false, ok));
+                rep->steepest_descent_steps++;
+            }
+        }
+        if (!ok) break;
+        push_hist(merit);
+    }
+    rep->final_residual_norm = std::sqrt(merit);
+    rep->converged = rep->final_residual_norm <= o->abs_tol;
+    NCU(c, cudaMemcpyAsync(u_out, w.X, sizeof(double) * nu, cudaMemcpyDeviceToDevice, st), "copy");
+    NCU(c, cudaMemcpyAsync(a_out, w.X + nu, sizeof(double) * na, cudaMemcpyDeviceToDevice, st), "copy");
+    NCU(c, cudaStreamSynchronize(st), "sync");
+    return PF_OK;
+}
+
 }  // namespace pf

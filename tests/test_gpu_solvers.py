@@ -171,3 +171,39 @@ def test_config1_shape_run_matches_oracle():
         assert abs(r.energy.total - o.energy.total) <= 1e-6 * abs(o.energy.total)
         assert abs(r.energy.dissipated - o.energy.dissipated) <= 1e-6 * max(abs(o.energy.dissipated), 1e-30)
         assert symmetric_alpha_distance(r.alpha, o.alpha, 100, 10) < 1e-4
+
+
+@pytest.mark.parametrize("pattern,model", [("union_jack", "AT1"), ("crossed", "AT2")])
+def test_coupled_newton_matches_oracle(pattern, model):
+    """coupled_newton_solve from a near-converged AM state (solver.py:303-330)."""
+    import paper_1511_08463_b200 as pf
+    prob, om, rng = make_pair(pattern, "plane_stress", model, 16, 8, lx=1.0, ly=0.5, hetero=True)
+    # a physically meaningful start: oracle AM iterate at a loose tolerance
+    st0 = oam.LoadState.zeros(om)
+    st0.u[om.bc[0]] = om.bc[1] * 30.0
+    st0.u[:] = oam.elastic_half_step(st0, om, oam.AMConfig())[0]
+    om.bc = (om.bc[0], om.bc[1] * 30.0)
+    prob.bc = pf.DirichletBC(om.bc[0], om.bc[1])
+    oam.am_loop(st0, om, oam.AMConfig(outer_atol=1e-2))
+    ocfg = oam.AMConfig(outer_atol=1e-9)
+    ons, onr = oam.newton_coupled(st0, om, ocfg)
+    st = pf.State(dev(st0.u), dev(st0.alpha), dev(st0.alpha_lb))
+    ns, nr = pf.coupled_newton_solve(st, prob, pf.SolverConfig(outer_atol=1e-9))
+    assert onr.converged and nr.converged
+    assert np.max(np.abs(host(ns.alpha) - ons.alpha)) < 1e-7
+    assert rel(host(ns.u), ons.u) < 1e-7
+    assert nr.iterations <= onr.iterations + 2
+
+
+def test_oram_newton_matches_reference_golden():
+    import paper_1511_08463_b200 as pf
+    G = np.load(os.path.join(GOLDEN, "ref_steps.npz"))
+    setup, _ = traction_pair(4)
+    st = pf.State.from_numpy(G["half_u0"], G["half_alpha0"], np.zeros_like(G["half_alpha0"]))
+    setup.apply_load(setup.problem, st, 1.4 * setup.params["critical_traction"])
+    rep = pf.oram_n_solve(st, setup.problem, pf.SolverConfig(method="oram_newton", omega=1.3,
+                                                             outer_atol=1e-9))
+    assert rep.converged
+    e = pf.assemble_energy(st, setup.problem)
+    assert np.allclose(np.array(e), G["oramn_energy"], rtol=1e-6)
+    assert symmetric_alpha_distance(host(st.alpha), G["oramn_alpha"], 20, 6) < 1e-6
