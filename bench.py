@@ -1,22 +1,25 @@
 """Benchmark: quasi-static phase-field load steps on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload traction1|sent512] [--sweep/--no-sweep]
+                    [--workload sent512|traction1] [--no-sweep] [--no-e2e]
 
-A bench "step" is one pass of the hot path over one batch of synthetic input: for
-``traction1`` (BASELINE config 1) one full 20-load-step quasi-static run; for ``sent512``
-(BASELINE config 2) one load step of the SENT schedule.  ``value`` is seconds per load step
-of the whole job (lower is better), timed with CUDA events on the solver stream (max over
-ranks), inputs resident in HBM; ``e2e`` is the same metric through the public API with the
-state coming from / going to pinned host memory every load step.  The dominant kernel's
-roofline is measured live (library CUDA-event brackets, pf_profile) over the timed region.
-Multi-GPU: replicas only (each rank runs an independent replica).
+Workload (BASELINE.json configs[1], the config the metric is quoted on): ``sent512`` -- 2D
+plane-strain AT2 single-edge-notched tension, 512x512 crossed P1 mesh, ORAM omega = 1.8 with
+Newton once the AM residual is below 1e-3, GMG-PCG at rtol 1e-8.  A bench "step" is one load step
+of the 60-step schedule: W untimed warm-up steps (schedule steps 0..W-1), then K timed steps
+(W..W+K-1), each bracketed by CUDA events on the solver stream with an L2 flush (512 MB write)
+between steps.  ``value`` = seconds per load step of the whole job (lower is better).
+``e2e`` replays the same K steps from the same starting state through the public API with the
+state copied in from / out to pinned host memory every step.  The roofline of the dominant
+kernel is measured live by a third replay with per-launch CUDA-event brackets (pf_profile;
+graphs off).  Multi-GPU: replicas only -- every rank runs its own replica.
 """
 
 from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import subprocess
 import sys
@@ -27,6 +30,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "fp64 operator-apply GDOF/s & HBM GB/s vs peak; sec per load step (AM+Newton)"
+REF_N = 48          # CPU sample size (SENT, crossed), see DESIGN.md "CPU baseline"
+CPU_EXPONENT = 1.33  # measured oracle cost growth per DOF (32^2 -> 64^2) for the labelled estimate
 
 
 def peaks():
@@ -38,7 +43,6 @@ def peaks():
         return 6650.0, "fallback"
 
 
-# ---- clocks sampler ----------------------------------------------------------------------------
 class ClockSampler:
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -52,8 +56,9 @@ class ClockSampler:
     def start(self):
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except Exception:  # noqa: BLE001
@@ -90,11 +95,13 @@ class ClockSampler:
         return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def flush_l2(buf):
-    buf.add_(1.0)  # 512 MB write > 126 MB L2
-
-
 # ---- workloads -----------------------------------------------------------------------------------
+def sent_config(pf):
+    return pf.SolverConfig(method="oram_newton", omega=1.8, outer_atol=1e-6, am_switch_atol=1e-3,
+                           elastic_solver="cg", elastic_rtol=1e-8, elastic_precond="gmg",
+                           max_am_iterations=2000)
+
+
 def traction1_setup(pf):
     mat = pf.Material(E=1.0, nu=0.0, Gc=1.0, ell=0.05, k_ell=1e-6)
     return pf.setup_traction(mat, L=1.0, H=0.1, nx=200, ny=20, n_steps=20, pattern="right",
@@ -103,47 +110,69 @@ def traction1_setup(pf):
 
 def traction1_config(pf):
     return pf.SolverConfig(method="am", omega=1.0, outer_atol=1e-6, elastic_solver="cg",
-                           elastic_rtol=1e-10)
+                           elastic_rtol=1e-10, elastic_precond="gmg")
 
 
-def oracle_traction1():
+WORKLOADS = {
+    "sent512": ("sent512: BASELINE config 2 -- plane-strain AT2 SENT, unit square, 512x512 crossed "
+                "P1 (525,313 vertices, 1,050,626 u-dofs), E=210 nu=0.3 Gc=2.7e-3 ell=0.01 "
+                "k_ell=1e-6, notch alpha=1 on y=0.5 x<=0.5, bottom clamped, top u_y=t (60 steps to "
+                "6e-3), ORAM omega=1.8 + Newton when |Phi| < 1e-3, GMG-PCG rtol 1e-8, outer_atol "
+                "1e-6; step = one load step"),
+    "traction1": ("traction1: BASELINE config 1 -- 200x20 right-diagonal AT1 bar (E=1, nu=0, Gc=1, "
+                  "ell=0.05, k=1e-6), t in linspace(0,1.5t_c,20), AM omega=1, atol 1e-6; step = one "
+                  "load step"),
+}
+
+
+def make_workload(pf, name):
+    if name == "sent512":
+        return pf.setup_sent(n=512), sent_config(pf)
+    return traction1_setup(pf), traction1_config(pf)
+
+
+# ---- CPU side (oracle = restatement of the reference algorithm; SuperLU direct solves) -----------
+def oracle_sent_steps(n, steps):
+    from oracle import am as oam
+    from oracle import problems as opb
+    s = opb.sent(n=n)
+    cfg = oam.AMConfig(method="oram_newton", omega=1.8, outer_atol=1e-6, am_switch_atol=1e-3,
+                       max_am_iterations=2000)
+    t0 = time.perf_counter()
+    rows, _ = opb.run(s, cfg, snapshot_stride=0, steps=steps)
+    return time.perf_counter() - t0, len(rows)
+
+
+def oracle_traction1_steps(steps):
     from oracle import am as oam
     from oracle import problems as opb
     from oracle.p1 import MaterialSpec
     spec = MaterialSpec(E=1.0, nu=0.0, Gc=1.0, ell=0.05, k_ell=1e-6)
     s = opb.traction(spec, L=1.0, H=0.1, nx=200, ny=20, n_steps=20, pattern="right",
                      include_zero=True, load_max_factor=1.5)
-    return s, oam.AMConfig(method="am", omega=1.0, outer_atol=1e-6, elastic_solver="direct")
-
-
-def run_oracle_traction1(reps=1):
-    from oracle import problems as opb
+    cfg = oam.AMConfig(method="am", omega=1.0, outer_atol=1e-6, elastic_solver="direct")
     t0 = time.perf_counter()
-    n = 0
-    for _ in range(reps):
-        s, cfg = oracle_traction1()
-        rows, _ = opb.run(s, cfg, snapshot_stride=0)
-        n += len(rows)
-    return time.perf_counter() - t0, n
+    rows, _ = opb.run(s, cfg, snapshot_stride=0, steps=steps)
+    return time.perf_counter() - t0, len(rows)
 
 
-def dominant_roofline(prof, peak, peak_kind):
-    """Pick the kernel class with the largest total time; achieved = alg bytes / time."""
-    best = max(prof.items(), key=lambda kv: kv[1]["ms"]) if prof else None
-    if not best or best[1]["ms"] <= 0:
-        return None
-    name, p = best
-    gbs = p["bytes"] / (p["ms"] * 1e-3) / 1e9
-    total = sum(v["ms"] for v in prof.values())
-    return {"bound": "hbm", "kernel": name, "achieved": round(gbs, 2), "peak": peak,
-            "peak_source": peak_kind, "unit": "GB/s", "frac": round(gbs / peak, 4),
-            "traffic": None, "launches": int(p["count"]),
-            "avg_launch_us": round(1e3 * p["ms"] / max(p["count"], 1), 3),
-            "bytes_per_launch": p["bytes"] / max(p["count"], 1),
-            "share_of_kernel_time": round(p["ms"] / total, 4) if total > 0 else None}
+def cpu_sample(workload, steps):
+    """(seconds per load step, description) of the oracle on a bounded sample."""
+    if workload == "sent512":
+        t, n = oracle_sent_steps(REF_N, steps)
+        v = t / n
+        scale = (512.0 / REF_N) ** (2 * CPU_EXPONENT)
+        return v, (f"{n} SENT load steps (schedule steps {steps[0]}..{steps[-1]}) of the oracle "
+                   f"(reference algorithm: SuperLU elastic/damage/Newton solves) at {REF_N}x{REF_N} "
+                   f"crossed -- a bounded sample, NOT the 512^2 workload; scaled estimate for 512^2 "
+                   f"with the measured cost growth N^{CPU_EXPONENT}: {v * scale:.0f} s/load-step"), \
+            v * scale
+    t, n = oracle_traction1_steps(steps)
+    return t / n, f"{n} config-1 load steps (oracle, SuperLU)", t / n
 
 
-def read_profile(problem, lib):
+# ---- helpers -------------------------------------------------------------------------------------
+def read_profile(problem):
     import ctypes as C
     from paper_1511_08463_b200 import _lib
     n = len(_lib.KERNEL_KINDS)
@@ -156,9 +185,24 @@ def read_profile(problem, lib):
     return out
 
 
+def dominant_roofline(prof, peak, peak_kind):
+    """Largest total-time kernel class that has algorithmic bytes; achieved = bytes / time."""
+    cands = {k: v for k, v in prof.items() if v["bytes"] > 0 and v["ms"] > 0}
+    if not cands:
+        return None
+    name, p = max(cands.items(), key=lambda kv: kv[1]["ms"])
+    gbs = p["bytes"] / (p["ms"] * 1e-3) / 1e9
+    total = sum(v["ms"] for v in prof.values())
+    return {"bound": "hbm", "kernel": name, "achieved": round(gbs, 2), "peak": peak,
+            "peak_source": peak_kind, "unit": "GB/s", "frac": round(gbs / peak, 4),
+            "traffic": None, "launches": int(p["count"]),
+            "avg_launch_us": round(1e3 * p["ms"] / max(p["count"], 1), 3),
+            "bytes_per_launch": round(p["bytes"] / max(p["count"], 1)),
+            "share_of_kernel_time": round(p["ms"] / total, 4) if total > 0 else None}
+
+
 def operator_sweep(pf, torch, peak, sizes=(1024, 4096, 8192), reps=10):
-    """Config 5: matrix-free Kuu / Kaa applies, cold L2 (flush between reps)."""
-    import numpy as np
+    """BASELINE config 5: matrix-free Kuu / Kaa applies on 2D union-jack, cold L2."""
     res = []
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device="cuda")
     for n in sizes:
@@ -174,11 +218,12 @@ def operator_sweep(pf, torch, peak, sizes=(1024, 4096, 8192), reps=10):
         st = pf.State(u, alpha, torch.zeros_like(alpha))
         K = pf.assemble_Kuu(st, prob, apply_bc=False)
         A = pf.assemble_Kaa(st, prob)
-        for name, op, xin, bpv in (("Kuu", K, x, 40.0), ("Kaa", A, xa, None)):
-            y = op @ xin
+        for name, op, xin, nbytes, dofs in (("Kuu", K, x, 40.0 * V, 2 * V),
+                                            ("Kaa", A, xa, 16.0 * V + 8.0 * prob.n_elements, V)):
+            op @ xin
             times = []
             for _ in range(reps):
-                flush_l2(flush)
+                flush.add_(1.0)
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)
                 e0.record()
@@ -187,65 +232,94 @@ def operator_sweep(pf, torch, peak, sizes=(1024, 4096, 8192), reps=10):
                 torch.cuda.synchronize()
                 times.append(e0.elapsed_time(e1) * 1e-3)
             t = sorted(times)[len(times) // 2]
-            if name == "Kuu":
-                nbytes = V * 40.0
-                dofs = 2 * V
-            else:
-                # pf_apply_Kaa = kappa pass (u -> kappa, c) + apply; report the apply share only
-                nbytes = V * 16.0 + prob.n_elements * 8.0
-                dofs = V
             res.append({"op": name, "n": n, "dofs": dofs, "median_s": t,
                         "GDOF_s": round(dofs / t / 1e9, 3), "GB_s": round(nbytes / t / 1e9, 1),
                         "frac": round(nbytes / t / 1e9 / peak, 3),
-                        "bytes_per_dof": round(nbytes / dofs, 2)})
-            del y
-        del prob
+                        "bytes_per_dof": round(nbytes / dofs, 2), "l2": "flushed"})
+        del prob, K, A
         torch.cuda.empty_cache()
     return res
+
+
+def run_steps(pf, torch, setup, cfg, state, steps, flush, host_io=False):
+    """Run schedule steps; returns (seconds per step list, records, h2d, d2h bytes)."""
+    times, recs = [], []
+    h2d = d2h = 0
+    for k in steps:
+        flush.add_(1.0)
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        if host_io:
+            hu, ha, hl = (t.cpu().pin_memory() for t in (state.u, state.alpha, state.alpha_lb))
+        e0.record()
+        if host_io:  # state enters from pinned host memory, result leaves to host
+            state = pf.State(hu.to("cuda", non_blocking=True), ha.to("cuda", non_blocking=True),
+                             hl.to("cuda", non_blocking=True), state.load)
+            h2d += (hu.numel() + ha.numel() + hl.numel()) * 8
+        r = pf.run_quasistatic(setup, cfg, snapshot_stride=1 if host_io else 0, state=state,
+                               steps=[k])
+        if host_io:
+            d2h += (r[0].u.size + r[0].alpha.size) * 8
+        e1.record()
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1) * 1e-3)
+        recs.append(r[0])
+    return times, recs, h2d, d2h, state
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=8)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="traction1", choices=["traction1"])
+    ap.add_argument("--workload", default="sent512", choices=list(WORKLOADS))
     ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    nsched = 60 if args.workload == "sent512" else 20
+    W = max(0, min(args.warmup, nsched - 1))
+    K = max(1, min(args.steps, nsched - W))
+    timed = list(range(W, W + K))
 
     if args.impl == "reference":
         if rank != 0:
             return 0
-        os.environ.setdefault("OPENBLAS_NUM_THREADS", str(os.cpu_count()))
-        for _ in range(args.warmup):
-            run_oracle_traction1(1)
-        t, n = run_oracle_traction1(args.steps)
-        v = t / n
+        # the reference algorithm (oracle restatement, SuperLU) on the box's host cores
+        t0 = time.perf_counter()
+        if args.workload == "sent512":
+            tw, _ = oracle_sent_steps(REF_N, list(range(0, W))) if W else (0.0, 0)
+            tk, nk = oracle_sent_steps(REF_N, list(range(0, W + K)))
+            tk -= tw
+        else:
+            tw, _ = oracle_traction1_steps(list(range(0, W))) if W else (0.0, 0)
+            tk, nk = oracle_traction1_steps(list(range(0, W + K)))
+            tk -= tw
+        v = tk / K
+        sample = (f"schedule steps {W}..{W + K - 1} of the oracle (reference algorithm, SuperLU) "
+                  + (f"at {REF_N}x{REF_N} crossed (bounded sample of the 512^2 workload)"
+                     if args.workload == "sent512" else "on the full config-1 bar"))
         line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "s/load-step",
-                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": 1e3 * t / args.steps, "higher_is_better": False,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": "traction1: BASELINE config 1, 200x20 right-diagonal AT1 "
-                           "bar, 20 load steps, AM omega=1, atol 1e-6",
-                           "parallelism": "cpu"},
+                "n_gpus": args.gpus, "steps": K, "warmup": W, "ms_per_step": 1e3 * v,
+                "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic", "config": {"workload": WORKLOADS[args.workload],
+                                                "parallelism": "cpu"},
                 "cpu_baseline": {"value": v, "unit": "s/load-step", "cores": 1, "kind": "port",
-                                 "sample": f"{args.steps} full config-1 runs ({n} load steps) of "
-                                           "the oracle restatement (SuperLU direct, as the "
-                                           "reference's default path)"},
+                                 "sample": sample,
+                                 "threads_note": "SuperLU / scipy sparsetools are serial"},
                 "e2e": {"value": v, "unit": "s/load-step", "h2d_bytes_per_step": 0,
-                        "d2h_bytes_per_step": 0}}
+                        "d2h_bytes_per_step": 0},
+                "wall_s": round(time.perf_counter() - t0, 1)}
         print(json.dumps(line))
         return 0
 
-    import numpy as np
     import torch
     import paper_1511_08463_b200 as pf
-    from paper_1511_08463_b200 import _lib
 
     torch.cuda.set_device(local)
     dist = None
@@ -253,96 +327,67 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     peak, peak_kind = peaks()
-
-    setup = traction1_setup(pf)
-    cfg = traction1_config(pf)
-    prob = setup.problem
-    nsteps_run = len(setup.schedule)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device="cuda")
 
-    def one_run(snap=0):
-        return pf.run_quasistatic(setup, cfg, snapshot_stride=snap)
-
-    for _ in range(args.warmup):
-        one_run()
+    setup, cfg = make_workload(pf, args.workload)
+    prob = setup.problem
+    state = pf.State.zeros(setup.mesh, setup.initial_alpha_lb)
+    # warm-up: schedule steps 0..W-1 (untimed)
+    _, _, _, _, state = run_steps(pf, torch, setup, cfg, state, list(range(W)), flush)
+    snap = state.copy()
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
     sampler = ClockSampler(local)
     sampler.start()
-    prob.call("pf_profile", 1)
     l0 = prob.launches()
-    step_s = []
-    its = []
-    for _ in range(args.steps):
-        flush_l2(flush)
-        torch.cuda.synchronize()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record()
-        recs = one_run()
-        e1.record()
-        torch.cuda.synchronize()
-        step_s.append(e0.elapsed_time(e1) * 1e-3)
-        its.append(sum(r.report.am_iterations for r in recs))
+    step_s, recs, _, _, _ = run_steps(pf, torch, setup, cfg, state, timed, flush)
     launches = prob.launches() - l0
-    prof = read_profile(prob, None)
-    prob.call("pf_profile", 0)
     clocks = sampler.stop()
     tot = sum(step_s)
     if dist:
         t = torch.tensor([tot], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tot = float(t.item())
-    # replicas: every rank runs its own replica concurrently; the job processed
-    # world * steps * nsteps_run load steps in `tot` seconds (max over ranks)
-    value = tot / (args.steps * nsteps_run * world)
+    value = tot / (K * world)
 
-    # e2e: same runs through the public API with host-resident state in / out each load step
-    V = setup.mesh.n_vertices
-    h2d = 0
-    e2e_s = []
-    for _ in range(max(1, args.steps)):
-        torch.cuda.synchronize()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record()
-        host_u = torch.zeros(2 * V, dtype=torch.float64).pin_memory()
-        host_a = torch.zeros(V, dtype=torch.float64).pin_memory()
-        st = pf.State(host_u.to("cuda", non_blocking=True), host_a.to("cuda", non_blocking=True),
-                      host_a.to("cuda", non_blocking=True))
-        recs = pf.run_quasistatic(setup, cfg, snapshot_stride=1, state=st)
-        e1.record()
-        torch.cuda.synchronize()
-        e2e_s.append(e0.elapsed_time(e1) * 1e-3)
-    h2d = (2 * V + 2 * V) * 8 / nsteps_run + sum(
-        16 * len(setup.problem.bc.dofs) for _ in range(1))
-    d2h = 3 * V * 8
-    e2e = {"value": sum(e2e_s) / (len(e2e_s) * nsteps_run), "unit": "s/load-step",
-           "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+    # e2e replay from the same starting state through host memory
+    e2e = None
+    if not args.no_e2e:
+        e_s, _, h2d, d2h, _ = run_steps(pf, torch, setup, cfg, snap.copy(), timed, flush,
+                                        host_io=True)
+        e2e = {"value": sum(e_s) / (K * world), "unit": "s/load-step",
+               "h2d_bytes_per_step": int(h2d / K), "d2h_bytes_per_step": int(d2h / K)}
 
-    sweep = None
-    if not args.no_sweep and rank == 0:
-        sweep = operator_sweep(pf, torch, peak)
+    # profiled replay: per-kernel CUDA-event brackets (graphs off) for the roofline
+    prof = {}
+    if rank == 0:
+        prob.call("pf_profile", 1)
+        read_profile(prob)
+        run_steps(pf, torch, setup, cfg, snap.copy(), timed, flush)
+        prof = read_profile(prob)
+        prob.call("pf_profile", 0)
 
+    sweep = operator_sweep(pf, torch, peak) if (not args.no_sweep and rank == 0) else None
     cpu = None
     if rank == 0 and world == 1:
-        t_cpu, n_cpu = run_oracle_traction1(1)
-        cpu = {"value": t_cpu / n_cpu, "unit": "s/load-step", "cores": 1, "kind": "port",
-               "sample": f"one full config-1 run ({n_cpu} load steps) of the oracle restatement "
-                         "(SuperLU direct elastic solves, LU-based rsls) on this host"}
+        v, desc, est = cpu_sample(args.workload, timed[:2] if args.workload == "sent512" else timed)
+        cpu = {"value": v, "unit": "s/load-step", "cores": 1, "kind": "port", "sample": desc,
+               "estimate_full_workload_s_per_step": round(est, 1)}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "s/load-step", "n_gpus": world,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
-                "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
-                "dtype": "f64", "data": "synthetic",
-                "config": {"workload": "traction1: BASELINE config 1, 200x20 right-diagonal AT1 "
-                           "bar (E=1, nu=0, Gc=1, ell=0.05, k=1e-6), t in linspace(0,1.5t_c,20), "
-                           "AM omega=1, atol 1e-6; one step = one full 20-load-step run",
+                "steps": K, "warmup": W, "ms_per_step": 1e3 * tot / K, "higher_is_better": False,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": WORKLOADS[args.workload],
+                           "timed_schedule_steps": [timed[0], timed[-1]],
                            "parallelism": "replicas" if world > 1 else "single",
                            "l2": "flushed (512 MB write) between timed steps",
-                           "am_iterations_per_run": its[-1] if its else None},
+                           "per_step_s": [round(x, 4) for x in step_s],
+                           "am_iterations": [r.report.am_iterations for r in recs],
+                           "newton_iterations": [r.report.newton_iterations for r in recs],
+                           "krylov_iterations": [r.report.total_krylov_iterations for r in recs],
+                           "energies": [list(map(float, r.energy)) for r in recs]},
                 "roofline": dominant_roofline(prof, peak, peak_kind),
                 "kernel_profile": {k: {"launches": int(v["count"]), "ms": round(v["ms"], 3),
                                        "GB_s": round(v["bytes"] / max(v["ms"], 1e-9) / 1e6, 1)}

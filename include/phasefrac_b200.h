@@ -187,7 +187,7 @@ int64_t pf_launch_count(const pf_ctx* ctx);
  * stream.  pf_profile_read syncs and returns out[3k..3k+2] = (launches, total ms,
  * algorithmic bytes) for kernel class k = 0..nkinds-1 (order: Kuu, Kuu-CG, Kuu-diag, kappa,
  * Kaa, Kaa-CG, Kaa-diag, Kaa-trial, physics, rhs, Kua, Kau, Jacobian, CG-vector, vector,
- * GMG) and resets the counters. */
+ * GMG cycle, GMG setup) and resets the counters. */
 int pf_profile(pf_ctx* ctx, int32_t enable);
 int pf_profile_read(pf_ctx* ctx, double* out, int32_t nkinds);
 

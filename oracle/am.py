@@ -7,7 +7,8 @@ backtracking (``:166-241``), the coupled active-set Newton solve with a
 field-split MINRES inner solver (``:247-330``), ORAM-N outer cycles with the
 energy-acceptance rule (``:333-387``) and the dispatcher (``:390-417``).
 
-Extension: ``am_switch_atol`` -- an absolute hand-off threshold for ORAM-N
+Extension: ``am_switch_atol`` -- an absolute hand-off threshold for ORAM-N (first cycle;
+later cycles use min(am_switch_atol, am_rtol * Phi_0))
 (BASELINE config 2, "switch to Newton once the AM residual falls below
 1e-3"); with it the hand-off target is max(am_switch_atol, outer_atol) and the
 settled test is skipped.
@@ -136,7 +137,10 @@ def am_loop(st: LoadState, m: P1Model, cfg: AMConfig, rtol=None, cycle=0) -> Ste
     if rtol is None:
         target, need_settle = cfg.outer_atol, False
     elif cfg.am_switch_atol is not None:
-        target, need_settle = max(cfg.am_switch_atol, cfg.outer_atol), False
+        # absolute hand-off (config 2) for the first cycle; after a rejected Newton phase the
+        # reference's shrinking relative target takes over so the next cycle makes progress
+        sw = cfg.am_switch_atol if cycle == 0 else min(cfg.am_switch_atol, rtol * phi0)
+        target, need_settle = max(sw, cfg.outer_atol), False
     else:
         target, need_settle = max(rtol * phi0, cfg.outer_atol), True
     rep = StepStats(omega_bar_min=cfg.omega)

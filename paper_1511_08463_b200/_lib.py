@@ -92,7 +92,7 @@ EXPORTS = {
     "pf_profile_read": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
 }
 KERNEL_KINDS = ["Kuu", "Kuu_cg", "Kuu_diag", "kappa", "Kaa", "Kaa_cg", "Kaa_diag", "Kaa_trial",
-                "physics", "rhs", "Kua", "Kau", "jacobian", "cg_vec", "vec", "gmg"]
+                "physics", "rhs", "Kua", "Kau", "jacobian", "cg_vec", "vec", "gmg_cycle", "gmg_setup"]
 
 _lib = None
 

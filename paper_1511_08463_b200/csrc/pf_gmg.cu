@@ -748,13 +748,16 @@ static LevelDev ldev(const Ctx* c, int l) {
     return d;
 }
 
-#define GK(c, expr)                                             \
+// launch + profiling bracket; `bytes` = algorithmic bytes of the launch (inputs read once,
+// outputs written once), `kind` = K_GMG (cycle) or K_GMGSET (hierarchy setup)
+#define GKB(c, kind, bytes, expr)                               \
     do {                                                        \
         const int _ps = prof_begin((c), st);                    \
         expr;                                                   \
-        prof_end((c), st, _ps, K_GMG, 0.0);                     \
+        prof_end((c), st, _ps, (kind), (double)(bytes));        \
         (c)->launches++;                                        \
     } while (0)
+#define GK(c, expr) GKB(c, K_GMG, 0.0, expr)
 
 // Build the hierarchy for the current alpha (c->alpha_ws) and Dirichlet mask.
 int gmg_setup(Ctx* c, cudaStream_t st) {
@@ -772,25 +775,25 @@ int gmg_setup(Ctx* c, cudaStream_t st) {
         const long long nv1 = L1.nv;
         switch (g.pattern) {
             case PF_UNION_JACK:
-                GK(c, (k_fine_rows<PF_UNION_JACK><<<gblocks(g.nv), kGB, 0, st>>>(g, c->alpha_ws, m0, c->glev[0].Dinv, lam)));
-                GK(c, (k_galerkin_cells<PF_UNION_JACK><<<gblocks(nv1), kGB, 0, st>>>(
+                GKB(c, K_GMGSET, 40.0 * g.nv, (k_fine_rows<PF_UNION_JACK><<<gblocks(g.nv), kGB, 0, st>>>(g, c->alpha_ws, m0, c->glev[0].Dinv, lam)));
+                GKB(c, K_GMGSET, 8.0 * g.nv + 329.0 * nv1, (k_galerkin_cells<PF_UNION_JACK><<<gblocks(nv1), kGB, 0, st>>>(
                           g, c->alpha_ws, m0, L1.nx, L1.ny, L1.A, L1.Dinv, L1.mask, lam + 1)));
                 break;
             case PF_RIGHT:
-                GK(c, (k_fine_rows<PF_RIGHT><<<gblocks(g.nv), kGB, 0, st>>>(g, c->alpha_ws, m0, c->glev[0].Dinv, lam)));
-                GK(c, (k_galerkin_cells<PF_RIGHT><<<gblocks(nv1), kGB, 0, st>>>(
+                GKB(c, K_GMGSET, 40.0 * g.nv, (k_fine_rows<PF_RIGHT><<<gblocks(g.nv), kGB, 0, st>>>(g, c->alpha_ws, m0, c->glev[0].Dinv, lam)));
+                GKB(c, K_GMGSET, 8.0 * g.nv + 329.0 * nv1, (k_galerkin_cells<PF_RIGHT><<<gblocks(nv1), kGB, 0, st>>>(
                           g, c->alpha_ws, m0, L1.nx, L1.ny, L1.A, L1.Dinv, L1.mask, lam + 1)));
                 break;
             default:
-                GK(c, (k_fine_rows<PF_CROSSED><<<gblocks(g.nv), kGB, 0, st>>>(g, c->alpha_ws, m0, c->glev[0].Dinv, lam)));
-                GK(c, (k_galerkin_cells<PF_CROSSED><<<gblocks(nv1), kGB, 0, st>>>(
+                GKB(c, K_GMGSET, 40.0 * g.nv, (k_fine_rows<PF_CROSSED><<<gblocks(g.nv), kGB, 0, st>>>(g, c->alpha_ws, m0, c->glev[0].Dinv, lam)));
+                GKB(c, K_GMGSET, 8.0 * g.nv + 329.0 * nv1, (k_galerkin_cells<PF_CROSSED><<<gblocks(nv1), kGB, 0, st>>>(
                           g, c->alpha_ws, m0, L1.nx, L1.ny, L1.A, L1.Dinv, L1.mask, lam + 1)));
                 break;
         }
     }
     for (int l = 1; l + 1 < nl; ++l) {
         LevelDev F = ldev(c, l), Cd = ldev(c, l + 1);
-        GK(c, (k_rap<<<gblocks(Cd.nv), kGB, 0, st>>>(F, Cd, c->glev[l + 1].A, c->glev[l + 1].Dinv,
+        GKB(c, K_GMGSET, 289.0 * F.nv + 329.0 * Cd.nv, (k_rap<<<gblocks(Cd.nv), kGB, 0, st>>>(F, Cd, c->glev[l + 1].A, c->glev[l + 1].Dinv,
                                                       c->glev[l + 1].mask, lam + l + 1)));
     }
     {
@@ -802,7 +805,7 @@ int gmg_setup(Ctx* c, cudaStream_t st) {
                                  (int)sizeof(double) * 4 * kCoarseMaxV * kCoarseMaxV);
             attr = true;
         }
-        GK(c, (k_coarse_inverse<<<1, 512, smem, st>>>(ldev(c, nl - 1), c->gmg_ainv)));
+        GKB(c, K_GMGSET, 2.0 * 8.0 * n * n, (k_coarse_inverse<<<1, 512, smem, st>>>(ldev(c, nl - 1), c->gmg_ainv)));
     }
     return check_cuda(c, cudaGetLastError(), "gmg setup");
 }
@@ -823,33 +826,33 @@ int gmg_vcycle(Ctx* c, const double* r_in, double* z_out, cudaStream_t st, const
         LevelDev Ld = ldev(c, l);
         Ld.nv = nv;
         // pre-smooth from x = 0
-        GK(c, (k_cheb0<<<gblocks(nv), kGB, 0, st>>>(nv, L.Dinv, b, L.res, L.d0, x, 0, lam + l, ratio, live)));
+        GKB(c, K_GMG, 96.0 * nv, (k_cheb0<<<gblocks(nv), kGB, 0, st>>>(nv, L.Dinv, b, L.res, L.d0, x, 0, lam + l, ratio, live)));
         double* d = L.d0;
         double* dn = L.d1;
         for (int k = 1; k < deg; ++k) {
             if (l == 0) {
                 PF_TRY_GMG(launch_Kuu(c, c->alpha_ws, d, L.w, PF_BC_ELIMINATE, st));
-                GK(c, (k_cheb_step<<<gblocks(nv), kGB, 0, st>>>(Ld, L.w, d, dn, L.res, x, k, lam + l, ratio, live)));
+                GKB(c, K_GMG, 144.0 * nv, (k_cheb_step<<<gblocks(nv), kGB, 0, st>>>(Ld, L.w, d, dn, L.res, x, k, lam + l, ratio, live)));
             } else {
-                GK(c, (k_cheb_step<<<gblocks(nv), kGB, 0, st>>>(Ld, nullptr, d, dn, L.res, x, k, lam + l, ratio, live)));
+                GKB(c, K_GMG, 416.0 * nv, (k_cheb_step<<<gblocks(nv), kGB, 0, st>>>(Ld, nullptr, d, dn, L.res, x, k, lam + l, ratio, live)));
             }
             std::swap(d, dn);
         }
         // residual
         if (l == 0) {
             PF_TRY_GMG(launch_Kuu(c, c->alpha_ws, x, L.w, PF_BC_ELIMINATE, st));
-            GK(c, (k_resid<<<gblocks(nv), kGB, 0, st>>>(Ld, L.w, x, b, L.r, live)));
+            GKB(c, K_GMG, 64.0 * nv, (k_resid<<<gblocks(nv), kGB, 0, st>>>(Ld, L.w, x, b, L.r, live)));
         } else {
-            GK(c, (k_resid<<<gblocks(nv), kGB, 0, st>>>(Ld, nullptr, x, b, L.r, live)));
+            GKB(c, K_GMG, 336.0 * nv, (k_resid<<<gblocks(nv), kGB, 0, st>>>(Ld, nullptr, x, b, L.r, live)));
         }
         // restrict
         GLevel& C = c->glev[l + 1];
         if (l == 0) {
-            GK(c, (k_restrict0<<<gblocks(C.nv), kGB, 0, st>>>(g, g.has_bc ? c->glev[0].mask : nullptr, C.nx, C.ny,
+            GKB(c, K_GMG, 16.0 * L.nv + 17.0 * C.nv, (k_restrict0<<<gblocks(C.nv), kGB, 0, st>>>(g, g.has_bc ? c->glev[0].mask : nullptr, C.nx, C.ny,
                                                                C.mask, L.r, C.b, live)));
         } else {
             LevelDev F = ldev(c, l), Cd = ldev(c, l + 1);
-            GK(c, (k_restrict<<<gblocks(Cd.nv), kGB, 0, st>>>(F, Cd, C.mask, L.r, C.b, live)));
+            GKB(c, K_GMG, 16.0 * F.nv + 17.0 * Cd.nv, (k_restrict<<<gblocks(Cd.nv), kGB, 0, st>>>(F, Cd, C.mask, L.r, C.b, live)));
         }
     }
     // coarsest
@@ -858,7 +861,7 @@ int gmg_vcycle(Ctx* c, const double* r_in, double* z_out, cudaStream_t st, const
         const int n = (int)(2 * L.nv);
         double* x = (nl == 1) ? z_out : L.x;
         const double* b = (nl == 1) ? r_in : L.b;
-        GK(c, (k_coarse_solve<<<std::max(1, (n + 7) / 8), 256, 0, st>>>(n, c->gmg_ainv, b, x, live)));
+        GKB(c, K_GMG, 8.0 * n * n + 32.0 * n, (k_coarse_solve<<<std::max(1, (n + 7) / 8), 256, 0, st>>>(n, c->gmg_ainv, b, x, live)));
     }
     // ascend
     for (int l = nl - 2; l >= 0; --l) {
@@ -870,28 +873,28 @@ int gmg_vcycle(Ctx* c, const double* r_in, double* z_out, cudaStream_t st, const
         LevelDev Ld = ldev(c, l);
         Ld.nv = nv;
         if (l == 0) {
-            GK(c, (k_prolong0<<<gblocks(g.nv), kGB, 0, st>>>(g, g.has_bc ? c->glev[0].mask : nullptr, C.nx, C.ny,
+            GKB(c, K_GMG, 32.0 * g.nv + 17.0 * C.nv, (k_prolong0<<<gblocks(g.nv), kGB, 0, st>>>(g, g.has_bc ? c->glev[0].mask : nullptr, C.nx, C.ny,
                                                               C.mask, C.x, x, live)));
         } else {
             LevelDev F = ldev(c, l), Cd = ldev(c, l + 1);
-            GK(c, (k_prolong<<<gblocks(F.nv), kGB, 0, st>>>(F, Cd, C.mask, C.x, x, live)));
+            GKB(c, K_GMG, 32.0 * F.nv + 17.0 * Cd.nv, (k_prolong<<<gblocks(F.nv), kGB, 0, st>>>(F, Cd, C.mask, C.x, x, live)));
         }
         // post-smooth: r = b - A x ; x += p(D^-1 A) D^-1 r
         if (l == 0) {
             PF_TRY_GMG(launch_Kuu(c, c->alpha_ws, x, L.w, PF_BC_ELIMINATE, st));
-            GK(c, (k_resid<<<gblocks(nv), kGB, 0, st>>>(Ld, L.w, x, b, L.r, live)));
+            GKB(c, K_GMG, 64.0 * nv, (k_resid<<<gblocks(nv), kGB, 0, st>>>(Ld, L.w, x, b, L.r, live)));
         } else {
-            GK(c, (k_resid<<<gblocks(nv), kGB, 0, st>>>(Ld, nullptr, x, b, L.r, live)));
+            GKB(c, K_GMG, 336.0 * nv, (k_resid<<<gblocks(nv), kGB, 0, st>>>(Ld, nullptr, x, b, L.r, live)));
         }
-        GK(c, (k_cheb0<<<gblocks(nv), kGB, 0, st>>>(nv, L.Dinv, L.r, L.res, L.d0, x, 1, lam + l, ratio, live)));
+        GKB(c, K_GMG, 112.0 * nv, (k_cheb0<<<gblocks(nv), kGB, 0, st>>>(nv, L.Dinv, L.r, L.res, L.d0, x, 1, lam + l, ratio, live)));
         double* d = L.d0;
         double* dn = L.d1;
         for (int k = 1; k < deg; ++k) {
             if (l == 0) {
                 PF_TRY_GMG(launch_Kuu(c, c->alpha_ws, d, L.w, PF_BC_ELIMINATE, st));
-                GK(c, (k_cheb_step<<<gblocks(nv), kGB, 0, st>>>(Ld, L.w, d, dn, L.res, x, k, lam + l, ratio, live)));
+                GKB(c, K_GMG, 144.0 * nv, (k_cheb_step<<<gblocks(nv), kGB, 0, st>>>(Ld, L.w, d, dn, L.res, x, k, lam + l, ratio, live)));
             } else {
-                GK(c, (k_cheb_step<<<gblocks(nv), kGB, 0, st>>>(Ld, nullptr, d, dn, L.res, x, k, lam + l, ratio, live)));
+                GKB(c, K_GMG, 416.0 * nv, (k_cheb_step<<<gblocks(nv), kGB, 0, st>>>(Ld, nullptr, d, dn, L.res, x, k, lam + l, ratio, live)));
             }
             std::swap(d, dn);
         }

@@ -122,7 +122,7 @@ enum ScalarSlot {
 // ---- per-kernel-class profiling (CUDA events around launches; read after the timed region) --
 enum KernelKind {
     K_KUU = 0, K_KUU_CG, K_KUU_DIAG, K_KAPPA, K_KAA, K_KAA_CG, K_KAA_DIAG, K_KAA_TRIAL, K_PHYS,
-    K_RHS, K_KUA, K_KAU, K_JAC, K_CG_VEC, K_VEC, K_GMG, K_NKINDS
+    K_RHS, K_KUA, K_KAU, K_JAC, K_CG_VEC, K_VEC, K_GMG, K_GMGSET, K_NKINDS
 };
 struct ProfEntry { int kind; int ev; double bytes; };
 struct Prof {

@@ -186,7 +186,10 @@ def am_solve(state: State, problem: Discretization, config: SolverConfig,
     if rtol is None:
         target, need_settle = config.outer_atol, False
     elif config.am_switch_atol is not None:
-        target, need_settle = max(config.am_switch_atol, config.outer_atol), False
+        # absolute hand-off (BASELINE config 2) on the first cycle; after a rejected Newton phase
+        # the reference's shrinking relative target (solver.py:183) takes over
+        sw = config.am_switch_atol if cycle == 0 else min(config.am_switch_atol, rtol * phi0)
+        target, need_settle = max(sw, config.outer_atol), False
     else:
         target, need_settle = max(rtol * phi0, config.outer_atol), True
 
