@@ -568,7 +568,9 @@ int damage_solve(Ctx* c, const double* u, const double* lb, const double* a_in, 
             pf_lin_report lr{};
             int rc;
             const long long maxit = o->inner_maxit > 0 ? o->inner_maxit : 10 * n;
-            rc = pcg_run(c, 1, B, c->kappa, c->act, o->inner_rtol, 0.0, maxit, 1, 8, &lr, st);
+            // atol floor: after an exact-active-set Newton step the VI merit equals the reduced
+            // residual, so converging it below 0.1*abs_tol buys nothing (vi.py:222-240)
+            rc = pcg_run(c, 1, B, c->kappa, c->act, o->inner_rtol, 0.1 * o->abs_tol, maxit, 1, 8, &lr, st);
             rep->total_krylov_iterations += lr.iterations;
             if (rc == PF_EBREAKDOWN) {
                 rep->linear_failures++;

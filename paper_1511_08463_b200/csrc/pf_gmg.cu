@@ -279,98 +279,6 @@ __global__ void k_galerkin_cells(const Geo2 g, const double* alpha, const unsign
     }
 }
 
-// level 0 -> level 1 restriction b1 = P0^T r0 (fine corners 2:1 bilinear, crossed centres via the
-// mean of their cell corners), one thread per coarse vertex
-__global__ void k_restrict0(const Geo2 g, const unsigned char* mask0, int ncx, int ncy, const unsigned char* mask1,
-                            const double* r, double* b1, const double* live) {
-    if (!gmg_live(live)) return;
-    const int nvyc = ncy + 1;
-    const long long nvc = (long long)(ncx + 1) * nvyc;
-    for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < nvc;
-         v += (long long)gridDim.x * blockDim.x) {
-        const int I = (int)(v / nvyc), J = (int)(v % nvyc);
-        const unsigned mC = mask1[v];
-        double s0 = 0.0, s1 = 0.0;
-        for (int fi = 2 * I - 1; fi <= 2 * I + 1; ++fi) {
-            if (fi < 0 || fi > g.nx) continue;
-            for (int fj = 2 * J - 1; fj <= 2 * J + 1; ++fj) {
-                if (fj < 0 || fj > g.ny) continue;
-                double w[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-                node_weights(fi, fj, g.nx, g.ny, I, J, w);
-                if (w[4] == 0.0) continue;
-                const long long f = (long long)fi * g.nvy + fj;
-                const unsigned mf = vmask(mask0, f);
-                const double2 rv = reinterpret_cast<const double2*>(r)[f];
-                if (!(mf & 1u)) s0 += w[4] * rv.x;
-                if (!(mf & 2u)) s1 += w[4] * rv.y;
-            }
-        }
-        if (g.pattern == PF_CROSSED) {
-            for (int ci = 2 * I - 2; ci <= 2 * I + 1; ++ci) {
-                if (ci < 0 || ci >= g.nx) continue;
-                for (int cj = 2 * J - 2; cj <= 2 * J + 1; ++cj) {
-                    if (cj < 0 || cj >= g.ny) continue;
-                    double wc = 0.0;
-                    for (int q = 0; q < 4; ++q) {
-                        double w[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-                        node_weights(ci + cdi(q), cj + cdj(q), g.nx, g.ny, I, J, w);
-                        wc += 0.25 * w[4];
-                    }
-                    if (wc == 0.0) continue;
-                    const double2 rv = reinterpret_cast<const double2*>(r)[g.nc + (long long)ci * g.ny + cj];
-                    s0 += wc * rv.x;
-                    s1 += wc * rv.y;
-                }
-            }
-        }
-        reinterpret_cast<double2*>(b1)[v] = make_double2((mC & 1u) ? 0.0 : s0, (mC & 2u) ? 0.0 : s1);
-    }
-}
-
-// level 1 -> level 0 prolongation x0 += P0 x1, one thread per fine vertex (corners + centres)
-__global__ void k_prolong0(const Geo2 g, const unsigned char* mask0, int ncx, int ncy, const unsigned char* mask1,
-                           const double* x1, double* x0, const double* live) {
-    if (!gmg_live(live)) return;
-    const int nvyc = ncy + 1;
-    for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < g.nv;
-         v += (long long)gridDim.x * blockDim.x) {
-        auto corner_val = [&](int fi, int fj, double& a0, double& a1) {
-            int cx[2], cy[2];
-            double wx[2], wy[2];
-            const int nxw = p1d(fi, g.nx, cx, wx), nyw = p1d(fj, g.ny, cy, wy);
-            a0 = 0.0; a1 = 0.0;
-            for (int a = 0; a < nxw; ++a)
-                for (int b = 0; b < nyw; ++b) {
-                    const long long cidx = (long long)cx[a] * nvyc + cy[b];
-                    const unsigned mC = mask1[cidx];
-                    const double2 xv = reinterpret_cast<const double2*>(x1)[cidx];
-                    const double w = wx[a] * wy[b];
-                    if (!(mC & 1u)) a0 += w * xv.x;
-                    if (!(mC & 2u)) a1 += w * xv.y;
-                }
-        };
-        double2 o = reinterpret_cast<double2*>(x0)[v];
-        if (v < g.nc) {
-            const int fi = (int)(v / g.nvy), fj = (int)(v % g.nvy);
-            const unsigned mf = vmask(mask0, v);
-            double a0, a1;
-            corner_val(fi, fj, a0, a1);
-            if (!(mf & 1u)) o.x += a0;
-            if (!(mf & 2u)) o.y += a1;
-        } else {  // centre: mean of its corners' interpolants (centres are never constrained)
-            const long long cell = v - g.nc;
-            const int ci = (int)(cell / g.ny), cj = (int)(cell % g.ny);
-            for (int q = 0; q < 4; ++q) {
-                double a0, a1;
-                corner_val(ci + cdi(q), cj + cdj(q), a0, a1);
-                o.x += 0.25 * a0;
-                o.y += 0.25 * a1;
-            }
-        }
-        reinterpret_cast<double2*>(x0)[v] = o;
-    }
-}
-
 struct LevelDev {
     int nx, ny;          // cells
     long long nv;
@@ -667,6 +575,53 @@ __global__ void k_prolong(LevelDev F, LevelDev Cd, const unsigned char* maskc, c
     }
 }
 
+// crossed level 0 <-> corner grid, factored as P0 = (corner identity + centre mean) o P_{2:1}:
+// z[c] = m_c r[c] + 1/4 sum_{adjacent centres} r[ctr]  (then unmasked-fine 2:1 restriction)
+__global__ void k_collapse_centres(const Geo2 g, const unsigned char* mask0, const double* r, double* z,
+                                   const double* live) {
+    if (!gmg_live(live)) return;
+    for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < g.nc;
+         v += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(v / g.nvy), j = (int)(v % g.nvy);
+        const unsigned m = vmask(mask0, v);
+        const double2 rv = reinterpret_cast<const double2*>(r)[v];
+        double s0 = (m & 1u) ? 0.0 : rv.x, s1 = (m & 2u) ? 0.0 : rv.y;
+        for (int ci = i - 1; ci <= i; ++ci)
+            for (int cj = j - 1; cj <= j; ++cj) {
+                if (ci < 0 || cj < 0 || ci >= g.nx || cj >= g.ny) continue;
+                const double2 rc = reinterpret_cast<const double2*>(r)[g.nc + (long long)ci * g.ny + cj];
+                s0 += 0.25 * rc.x;
+                s1 += 0.25 * rc.y;
+            }
+        reinterpret_cast<double2*>(z)[v] = make_double2(s0, s1);
+    }
+}
+// x[c] += m_c y[c] ; x[ctr] += 1/4 sum of its corners' y  (y = P_{2:1} x1 on the corner grid)
+__global__ void k_expand_centres(const Geo2 g, const unsigned char* mask0, const double* y, double* x,
+                                 const double* live) {
+    if (!gmg_live(live)) return;
+    for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < g.nv;
+         v += (long long)gridDim.x * blockDim.x) {
+        double2 o = reinterpret_cast<double2*>(x)[v];
+        if (v < g.nc) {
+            const unsigned m = vmask(mask0, v);
+            const double2 a = reinterpret_cast<const double2*>(y)[v];
+            if (!(m & 1u)) o.x += a.x;
+            if (!(m & 2u)) o.y += a.y;
+        } else {
+            const long long cell = v - g.nc;
+            const long long v00 = (cell / g.ny) * g.nvy + cell % g.ny;
+            const long long cs[4] = {v00, v00 + g.nvy, v00 + 1, v00 + g.nvy + 1};
+            for (int q = 0; q < 4; ++q) {
+                const double2 a = reinterpret_cast<const double2*>(y)[cs[q]];
+                o.x += 0.25 * a.x;
+                o.y += 0.25 * a.y;
+            }
+        }
+        reinterpret_cast<double2*>(x)[v] = o;
+    }
+}
+
 // z_f = 0 helper + level-0 vector ops
 __global__ void k_fill0(long long n, double* x) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
@@ -847,9 +802,18 @@ int gmg_vcycle(Ctx* c, const double* r_in, double* z_out, cudaStream_t st, const
         }
         // restrict
         GLevel& C = c->glev[l + 1];
-        if (l == 0) {
-            GKB(c, K_GMG, 16.0 * L.nv + 17.0 * C.nv, (k_restrict0<<<gblocks(C.nv), kGB, 0, st>>>(g, g.has_bc ? c->glev[0].mask : nullptr, C.nx, C.ny,
-                                                               C.mask, L.r, C.b, live)));
+        if (l == 0 && g.pattern == PF_CROSSED) {
+            LevelDev F = ldev(c, 0), Cd = ldev(c, 1);
+            F.mask = nullptr;  // fine masks were applied by the collapse
+            GKB(c, K_GMG, 48.0 * g.nc, (k_collapse_centres<<<gblocks(g.nc), kGB, 0, st>>>(
+                                           g, g.has_bc ? c->glev[0].mask : nullptr, L.r, L.w, live)));
+            GKB(c, K_GMG, 16.0 * F.nv + 17.0 * Cd.nv, (k_restrict<<<gblocks(Cd.nv), kGB, 0, st>>>(
+                                                         F, Cd, C.mask, L.w, C.b, live)));
+        } else if (l == 0) {
+            LevelDev F = ldev(c, 0), Cd = ldev(c, 1);
+            F.mask = g.has_bc ? c->glev[0].mask : nullptr;
+            GKB(c, K_GMG, 16.0 * F.nv + 17.0 * Cd.nv, (k_restrict<<<gblocks(Cd.nv), kGB, 0, st>>>(
+                                                         F, Cd, C.mask, L.r, C.b, live)));
         } else {
             LevelDev F = ldev(c, l), Cd = ldev(c, l + 1);
             GKB(c, K_GMG, 16.0 * F.nv + 17.0 * Cd.nv, (k_restrict<<<gblocks(Cd.nv), kGB, 0, st>>>(F, Cd, C.mask, L.r, C.b, live)));
@@ -872,9 +836,19 @@ int gmg_vcycle(Ctx* c, const double* r_in, double* z_out, cudaStream_t st, const
         double* x = (l == 0) ? z_out : L.x;
         LevelDev Ld = ldev(c, l);
         Ld.nv = nv;
-        if (l == 0) {
-            GKB(c, K_GMG, 32.0 * g.nv + 17.0 * C.nv, (k_prolong0<<<gblocks(g.nv), kGB, 0, st>>>(g, g.has_bc ? c->glev[0].mask : nullptr, C.nx, C.ny,
-                                                              C.mask, C.x, x, live)));
+        if (l == 0 && g.pattern == PF_CROSSED) {
+            LevelDev F = ldev(c, 0), Cd = ldev(c, 1);
+            F.mask = nullptr;
+            GK(c, (k_fill0<<<gblocks(2 * g.nc), kGB, 0, st>>>(2 * g.nc, L.w)));
+            GKB(c, K_GMG, 32.0 * F.nv + 17.0 * Cd.nv, (k_prolong<<<gblocks(F.nv), kGB, 0, st>>>(
+                                                         F, Cd, C.mask, C.x, L.w, live)));
+            GKB(c, K_GMG, 48.0 * g.nv, (k_expand_centres<<<gblocks(g.nv), kGB, 0, st>>>(
+                                           g, g.has_bc ? c->glev[0].mask : nullptr, L.w, x, live)));
+        } else if (l == 0) {
+            LevelDev F = ldev(c, 0), Cd = ldev(c, 1);
+            F.mask = g.has_bc ? c->glev[0].mask : nullptr;
+            GKB(c, K_GMG, 32.0 * F.nv + 17.0 * Cd.nv, (k_prolong<<<gblocks(F.nv), kGB, 0, st>>>(
+                                                         F, Cd, C.mask, C.x, x, live)));
         } else {
             LevelDev F = ldev(c, l), Cd = ldev(c, l + 1);
             GKB(c, K_GMG, 32.0 * F.nv + 17.0 * Cd.nv, (k_prolong<<<gblocks(F.nv), kGB, 0, st>>>(F, Cd, C.mask, C.x, x, live)));
