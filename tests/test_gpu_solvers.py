@@ -207,3 +207,21 @@ def test_oram_newton_matches_reference_golden():
     e = pf.assemble_energy(st, setup.problem)
     assert np.allclose(np.array(e), G["oramn_energy"], rtol=1e-6)
     assert symmetric_alpha_distance(host(st.alpha), G["oramn_alpha"], 20, 6) < 1e-6
+
+
+def test_thermal_slab_config3_matches_oracle():
+    """BASELINE config 3 physics (erf-profile eps0 ramp, E noise, plane strain AT1, ORAM-N) on a
+    coarse 48x12 slab, through the nucleation steps."""
+    import paper_1511_08463_b200 as pf
+    setup = pf.setup_thermal_slab(nx=48, ny=12, n_steps=12, dT_factor=3.0)
+    osetup = opb.thermal_slab(nx=48, ny=12, n_steps=12, dT_factor=3.0)
+    assert np.array_equal(setup.params["E_cell"], osetup.params["E_cell"])
+    cfg = pf.SolverConfig(method="oram_newton", omega=1.5, outer_atol=1e-9, elastic_solver="cg",
+                          elastic_rtol=1e-12, elastic_precond="gmg")
+    recs = pf.run_quasistatic(setup, cfg)
+    orows, _ = opb.run(osetup, oam.AMConfig(method="oram_newton", omega=1.5, outer_atol=1e-9))
+    assert max(float(np.max(o.alpha)) for o in orows) > 0.1   # the slab does crack
+    for r, o in zip(recs, orows):
+        for k in range(3):
+            assert abs(r.energy[k] - o.energy[k]) <= 1e-6 * abs(o.energy[k]) + 1e-14, (r.step, k)
+        assert np.max(np.abs(r.alpha - o.alpha)) < 1e-4
