@@ -19,7 +19,7 @@ from scipy.special import erf
 
 from .fem import (Discretization, DirichletBC, EnergyBreakdown, State, assemble_energy,
                   combine_bcs)
-from .mesh import StructuredMesh, boundary_dofs, rect_mesh
+from .mesh import StructuredMesh, StructuredMesh3D, boundary_dofs, rect_mesh
 from .model import DamageModel, Material, critical_shock, critical_traction
 from .solver import NonlinearReport, SolverConfig, solve_load_step
 
@@ -135,6 +135,46 @@ def setup_thermal_slab(nx: int = 2048, ny: int = 512, material: Optional[Materia
 
     return ProblemSetup("thermal_slab", mesh, problem, schedule, apply_load,
                         params={"critical_shock": dTc, "tau": tau, "E_cell": E_cell})
+
+
+def lognormal_gc(n, sigma=0.1, seed=0, Gc=1.0):
+    """Per-hex Gc exp(N(0, sigma^2)) (default_rng(seed)), then one Jacobi pass: the mean of each
+    cell with its face neighbours (config 4)."""
+    rng = np.random.default_rng(seed)
+    g = Gc * np.exp(rng.normal(0.0, sigma, (n, n, n)))
+    s = g.copy()
+    c = np.ones_like(g)
+    for ax in range(3):
+        for sh in (1, -1):
+            r = np.roll(g, sh, axis=ax)
+            valid = np.ones_like(g, dtype=bool)
+            idx = [slice(None)] * 3
+            idx[ax] = 0 if sh == 1 else -1
+            valid[tuple(idx)] = False
+            s += np.where(valid, r, 0.0)
+            c += valid
+    return (s / c).ravel()
+
+
+def setup_traction3d(n: int = 128, material: Optional[Material] = None, n_steps: int = 30,
+                     load_max_factor: float = 1.5, sigma: float = 0.1, seed: int = 0) -> ProblemSetup:
+    """3D AT1 traction of the unit cube with a lognormal Gc field (BASELINE config 4): z=0 face
+    clamped, z=1 face u_z = t, t in linspace(0, f t_c, n+1)[1:]."""
+    material = material or Material(E=1.0, nu=0.3, Gc=1.0, ell=0.03, k_ell=1e-6, regime="3d")
+    mesh = StructuredMesh3D(n, n, n)
+    Gc_cell = lognormal_gc(n, sigma, seed, material.Gc)
+    problem = Discretization(mesh, material, DamageModel("AT1"), Gc_cell=Gc_cell)
+    tc = critical_traction(material)
+    schedule = np.linspace(0.0, load_max_factor * tc, n_steps + 1)[1:]
+    z0 = mesh.face_vertices("z0")
+    z1 = mesh.face_vertices("z1")
+    clamp = np.concatenate([3 * z0, 3 * z0 + 1, 3 * z0 + 2])
+    pull = 3 * z1 + 2
+    def apply_load(problem, state, t):
+        problem.bc = combine_bcs(DirichletBC(clamp, np.zeros(clamp.size)),
+                                 DirichletBC(pull, np.full(pull.size, t)))
+    return ProblemSetup("traction3d", mesh, problem, schedule, apply_load,
+                        params={"critical_traction": tc, "Gc_cell": Gc_cell})
 
 
 # -- quasi-static driver (cases.py:241-306) ---------------------------------------------------------

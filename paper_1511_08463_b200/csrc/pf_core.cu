@@ -479,6 +479,7 @@ int elastic_solve(Ctx* c, const double* alpha, const double* u0, double* u_out, 
     if (o->precond != PF_PREC_JACOBI && o->precond != PF_PREC_GMG)
         return set_error(c, PF_EINVAL, "elastic solve: unknown preconditioner");
     const bool gmg = o->precond == PF_PREC_GMG;
+    if (gmg && c->dim == 3) return set_error(c, PF_EINVAL, "GMG is built for 2D meshes only in this version");
     PF_CU(c, cudaMemcpyAsync(c->alpha_ws, alpha, sizeof(double) * c->n_a, cudaMemcpyDeviceToDevice, st),
           "alpha copy");
     PcgBuffers B{c->cg_x, c->cg_r, c->cg_z, c->cg_p0, c->cg_p1, c->cg_q, c->cg_dinv, c->cg_b, c->n_u};
@@ -685,6 +686,54 @@ static void geometry_2d(Ctx* c) {
     g.nstrips = (int)((rows + S - 1) / S);
 }
 
+static void geometry_3d(Ctx* c) {
+    Geo3& g = c->g3;
+    const pf_desc& d = c->d;
+    g.nx = (int)d.nx; g.ny = (int)d.ny; g.nz = (int)d.nz;
+    g.nvy = g.ny + 1; g.nvz = g.nz + 1;
+    g.nv = (long long)(g.nx + 1) * g.nvy * g.nvz;
+    g.ncell = (long long)g.nx * g.ny * g.nz;
+    g.ihx = g.nx / d.lx; g.ihy = g.ny / d.ly; g.ihz = g.nz / d.lz;
+    g.vol = (d.lx / g.nx) * (d.ly / g.ny) * (d.lz / g.nz) / 6.0;
+    const double nu = d.nu;
+    g.lam = nu / ((1.0 + nu) * (1.0 - 2.0 * nu));
+    g.mu = 1.0 / (2.0 * (1.0 + nu));
+    g.E = d.E; g.kell = d.k_ell; g.Gc = d.Gc; g.ell = d.ell;
+    g.at2 = d.model == PF_AT2;
+    g.cw = g.at2 ? 2.0 : 8.0 / 3.0;
+    g.E_cell = nullptr; g.Gc_cell = nullptr; g.has_bc = 0;
+    g.nbj = (g.nvy + 13) / 14;
+    g.nbk = (g.nvz + 29) / 30;
+    const long long per = (long long)g.nbj * g.nbk;
+    long long S = ((g.nx + 1) * per + 148LL * 4 - 1) / (148LL * 4);
+    S = std::max(4LL, std::min(64LL, S));
+    g.S = (int)S;
+    g.nstrips = (int)((g.nx + 1 + S - 1) / S);
+}
+
+__global__ void k_relax_u3(long long nv, int nvy, int nvz, int nx, int ny, int nz, const double* __restrict__ up,
+                           const double* __restrict__ us, double om, double* __restrict__ uo,
+                           const unsigned char* __restrict__ mask, const double* __restrict__ ubar, int has_bc,
+                           int snap_only) {
+    for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < nv;
+         v += (long long)gridDim.x * blockDim.x) {
+        double a[3];
+        for (int c = 0; c < 3; ++c)
+            a[c] = snap_only ? uo[3 * v + c] : up[3 * v + c] + om * (us[3 * v + c] - up[3 * v + c]);
+        if (has_bc) {
+            const int k = (int)(v % nvz);
+            const long long ij = v / nvz;
+            const int j = (int)(ij % nvy), i = (int)(ij / nvy);
+            if (i == 0 || i == nx || j == 0 || j == ny || k == 0 || k == nz) {
+                const unsigned m = mask[v];
+                for (int c = 0; c < 3; ++c)
+                    if ((m >> c) & 1u) a[c] = ubar[3 * v + c];
+            }
+        }
+        for (int c = 0; c < 3; ++c) uo[3 * v + c] = a[c];
+    }
+}
+
 static void plan_workspace(Ctx* c) {
     c->layout.clear();
     auto add = [&](void** p, size_t bytes) { c->layout.push_back({p, (bytes + 255) & ~size_t(255)}); };
@@ -706,8 +755,10 @@ static void plan_workspace(Ctx* c) {
     add((void**)&c->bits, sizeof(unsigned long long) * 8);
     c->n_newton_vec = ((c->n_u + c->n_a + 31) / 32) * 32;  // keep every stacked slot 256-byte aligned
     add((void**)&c->newton, sizeof(double) * c->n_newton_vec * 16);
-    gmg_plan(c);
-    add((void**)&c->gmg_base, gmg_bytes(c));
+    if (c->dim == 2) {
+        gmg_plan(c);
+        add((void**)&c->gmg_base, gmg_bytes(c));
+    }
     size_t tot = 0;
     for (auto& e : c->layout) tot += e.second;
     c->ws_bytes = tot;
@@ -718,25 +769,41 @@ extern "C" {
 int pf_ctx_create(const pf_desc* desc, pf_ctx** out) {
     if (!desc || !out) return set_error(nullptr, PF_EINVAL, "null argument");
     *out = nullptr;
-    if (desc->dim != 2) return set_error(nullptr, PF_EINVAL, "only dim = 2 is built in this version");
-    if (desc->pattern < 0 || desc->pattern > 2)
+    const bool d3 = desc->dim == 3;
+    if (desc->dim != 2 && !d3) return set_error(nullptr, PF_EINVAL, "dim must be 2 or 3");
+    if (!d3 && (desc->pattern < 0 || desc->pattern > 2))
         return set_error(nullptr, PF_EINVAL, "2D pattern must be union_jack, right or crossed");
-    if (desc->nx < 1 || desc->ny < 1 || desc->ny > (1 << 30) || desc->nx > (1 << 30))
+    if (d3 && desc->pattern != PF_KUHN6) return set_error(nullptr, PF_EINVAL, "3D pattern must be kuhn6");
+    if (desc->nx < 1 || desc->ny < 1 || desc->ny > (1 << 30) || desc->nx > (1 << 30) ||
+        (d3 && (desc->nz < 1 || desc->nz > (1 << 30))))
         return set_error(nullptr, PF_EINVAL, "bad grid size");
-    if (!(desc->E > 0 && desc->Gc > 0 && desc->ell > 0 && desc->lx > 0 && desc->ly > 0))
+    if (!(desc->E > 0 && desc->Gc > 0 && desc->ell > 0 && desc->lx > 0 && desc->ly > 0 && (!d3 || desc->lz > 0)))
         return set_error(nullptr, PF_EINVAL, "E, Gc, ell and extents must be positive");
     if (!(desc->nu > -1.0 && desc->nu < 0.5)) return set_error(nullptr, PF_EINVAL, "nu out of (-1, 0.5)");
-    if (desc->regime != PF_PLANE_STRESS && desc->regime != PF_PLANE_STRAIN)
+    if (!d3 && desc->regime != PF_PLANE_STRESS && desc->regime != PF_PLANE_STRAIN)
         return set_error(nullptr, PF_EINVAL, "2D regime must be plane stress or plane strain");
+    if (d3 && desc->regime != PF_3D) return set_error(nullptr, PF_EINVAL, "3D regime must be PF_3D");
     if (desc->model != PF_AT1 && desc->model != PF_AT2) return set_error(nullptr, PF_EINVAL, "unknown model");
     pf_ctx* c = new pf_ctx();
     c->d = *desc;
-    c->dim = 2;
-    c->dof = 2;
-    geometry_2d(c);
-    c->n_a = c->g.nv;
-    c->n_u = 2 * c->g.nv;
-    c->n_el = c->g.ncell * c->g.npc;
+    if (d3) {
+        c->dim = 3;
+        c->dof = 3;
+        geometry_3d(c);
+        // the 2D descriptor is unused in 3D; keep it benign for shared sizing code
+        c->g = Geo2{};
+        c->g.ny = 1;
+        c->n_a = c->g3.nv;
+        c->n_u = 3 * c->g3.nv;
+        c->n_el = 6 * c->g3.ncell;
+    } else {
+        c->dim = 2;
+        c->dof = 2;
+        geometry_2d(c);
+        c->n_a = c->g.nv;
+        c->n_u = 2 * c->g.nv;
+        c->n_el = c->g.ncell * c->g.npc;
+    }
     plan_workspace(c);
     if (cudaHostAlloc((void**)&c->h_scal, sizeof(double) * 256, cudaHostAllocDefault) != cudaSuccess) {
         delete c;
@@ -763,11 +830,11 @@ int pf_query(const pf_ctx* c, int64_t out[8]) {
     out[0] = c->n_a;
     out[1] = c->n_u;
     out[2] = c->n_el;
-    out[3] = c->g.ncell;
-    out[4] = c->g.nc;
+    out[3] = c->dim == 3 ? c->g3.ncell : c->g.ncell;
+    out[4] = c->dim == 3 ? c->g3.nv : c->g.nc;
     out[5] = c->dim;
-    out[6] = c->g.npc;
-    out[7] = c->g.S;
+    out[6] = c->dim == 3 ? 6 : c->g.npc;
+    out[7] = c->dim == 3 ? c->g3.S : c->g.S;
     return PF_OK;
 }
 
@@ -785,7 +852,7 @@ int pf_bind_workspace(pf_ctx* c, void* p, int64_t bytes) {
     }
     c->ws = base;
     c->bound = 1;
-    gmg_bind(c, c->gmg_base);
+    if (c->dim == 2) gmg_bind(c, c->gmg_base);
     // zero scalars / tickets / bits / masks (synchronous; binding is a setup step)
     if (cudaMemset(c->scal, 0, sizeof(double) * S_COUNT) != cudaSuccess ||
         cudaMemset(c->tickets, 0, sizeof(unsigned) * 64) != cudaSuccess ||
@@ -798,6 +865,8 @@ int pf_bind_workspace(pf_ctx* c, void* p, int64_t bytes) {
         return set_error(c, PF_ECUDA, "workspace initialisation failed");
     c->g.bcmask = c->bcmask;
     c->g.ubar = c->ubar;
+    c->g3.bcmask = c->bcmask;
+    c->g3.ubar = c->ubar;
     return PF_OK;
 }
 
@@ -811,6 +880,8 @@ int pf_set_cell_fields(pf_ctx* c, const double* E_cell, const double* Gc_cell) {
     if (!c) return PF_EINVAL;
     c->g.E_cell = E_cell;
     c->g.Gc_cell = Gc_cell;
+    c->g3.E_cell = E_cell;
+    c->g3.Gc_cell = Gc_cell;
     c->geo_version++;
     return PF_OK;
 }
@@ -818,6 +889,30 @@ int pf_set_cell_fields(pf_ctx* c, const double* E_cell, const double* Gc_cell) {
 int pf_set_dirichlet(pf_ctx* c, const int64_t* dofs, const double* vals, int64_t n, void* stream) {
     NEED_WS(c);
     cudaStream_t st = (cudaStream_t)stream;
+    if (c->dim == 3) {
+        const Geo3& g = c->g3;
+        std::vector<unsigned char> mask(g.nv, 0);
+        std::vector<double> ub(3 * g.nv, 0.0);
+        for (int64_t q = 0; q < n; ++q) {
+            const int64_t dof = dofs[q];
+            if (dof < 0 || dof >= 3 * g.nv) return set_error(c, PF_EINVAL, "Dirichlet dof out of range");
+            const int64_t v = dof / 3;
+            const int comp = (int)(dof % 3);
+            const int k = (int)(v % g.nvz);
+            const int64_t ij = v / g.nvz;
+            const int j = (int)(ij % g.nvy), i = (int)(ij / g.nvy);
+            if (!(i == 0 || i == g.nx || j == 0 || j == g.ny || k == 0 || k == g.nz))
+                return set_error(c, PF_EINVAL, "Dirichlet dofs must lie on boundary vertices");
+            mask[v] |= (unsigned char)(1u << comp);
+            ub[dof] = vals[q];
+        }
+        PF_CU(c, cudaMemcpyAsync(c->bcmask, mask.data(), g.nv, cudaMemcpyHostToDevice, st), "bc mask");
+        PF_CU(c, cudaMemcpyAsync(c->ubar, ub.data(), sizeof(double) * 3 * g.nv, cudaMemcpyHostToDevice, st), "ubar");
+        PF_CU(c, cudaStreamSynchronize(st), "sync");
+        if (c->g3.has_bc != (n > 0)) c->geo_version++;
+        c->g3.has_bc = n > 0;
+        return PF_OK;
+    }
     const Geo2& g = c->g;
     std::vector<unsigned char> mask(g.nc, 0);
     std::vector<double> ub(2 * g.nc, 0.0);
@@ -843,6 +938,7 @@ int pf_set_dirichlet(pf_ctx* c, const int64_t* dofs, const double* vals, int64_t
 
 int pf_set_eps0_rows(pf_ctx* c, const double* table, void* stream) {
     NEED_WS(c);
+    if (c->dim == 3) return table ? set_error(c, PF_EINVAL, "eps0 rows are 2D only") : PF_OK;
     if (!table) {
         if (c->g.eps0) c->geo_version++;
         c->g.eps0 = nullptr;
@@ -922,6 +1018,14 @@ int pf_damage_solve(pf_ctx* c, const double* u, const double* lb, const double* 
 }
 int pf_relax_u(pf_ctx* c, const double* u_prev, const double* u_star, double omega, double* u_out, void* s) {
     NEED_WS(c);
+    if (c->dim == 3) {
+        const Geo3& g = c->g3;
+        k_relax_u3<<<vec_blocks(g.nv), kVecBlock, 0, (cudaStream_t)s>>>(g.nv, g.nvy, g.nvz, g.nx, g.ny, g.nz, u_prev,
+                                                                         u_star, omega, u_out, c->bcmask, c->ubar,
+                                                                         g.has_bc, 0);
+        c->launches++;
+        return check_cuda(c, cudaGetLastError(), "relax_u3");
+    }
     const Geo2& g = c->g;
     k_relax_u<<<vec_blocks(g.nv), kVecBlock, 0, (cudaStream_t)s>>>(g.nv, g.nc, g.nvy, g.nx, g.ny, u_prev,
                                                                     u_star, omega, u_out, c->bcmask,
@@ -931,6 +1035,15 @@ int pf_relax_u(pf_ctx* c, const double* u_prev, const double* u_star, double ome
 }
 int pf_snap_bc(pf_ctx* c, double* u, void* s) {
     NEED_WS(c);
+    if (c->dim == 3) {
+        const Geo3& g = c->g3;
+        if (!g.has_bc) return PF_OK;
+        k_relax_u3<<<vec_blocks(g.nv), kVecBlock, 0, (cudaStream_t)s>>>(g.nv, g.nvy, g.nvz, g.nx, g.ny, g.nz, nullptr,
+                                                                         nullptr, 0.0, u, c->bcmask, c->ubar,
+                                                                         g.has_bc, 1);
+        c->launches++;
+        return check_cuda(c, cudaGetLastError(), "snap_bc3");
+    }
     const Geo2& g = c->g;
     if (!g.has_bc) return PF_OK;
     k_relax_u<<<vec_blocks(g.nv), kVecBlock, 0, (cudaStream_t)s>>>(g.nv, g.nc, g.nvy, g.nx, g.ny, nullptr,

@@ -49,6 +49,22 @@ struct Geo2 {
     int nwj, S, nstrips;
 };
 
+// ---- 3D (Kuhn tetrahedra) descriptor ------------------------------------------------------------
+struct Geo3 {
+    int nx, ny, nz, nvy, nvz;     // cells; ny+1, nz+1
+    long long nv, ncell;
+    double ihx, ihy, ihz, vol;    // 1/h per axis, tet volume hx hy hz / 6
+    double lam, mu;               // unit-E Lame constants
+    double E, kell, Gc, ell, cw;
+    int at2;
+    const double* E_cell;
+    const double* Gc_cell;
+    const unsigned char* bcmask;  // per vertex, bit c = component c constrained
+    const double* ubar;           // 3 nv
+    int has_bc;
+    int nbj, nbk, S, nstrips;     // block tiling
+};
+
 // ---- reductions --------------------------------------------------------------------------
 struct RedBuf {
     double* partials;      // [kMaxRed][kMaxBlocksRed]
@@ -148,6 +164,7 @@ struct GLevel {
 struct Ctx {
     pf_desc d;
     Geo2 g;
+    Geo3 g3;
     std::string err;
     long long n_u = 0, n_a = 0, n_el = 0;
     int dim = 2, dof = 2;
@@ -249,6 +266,24 @@ int launch_Kau(Ctx* c, const double* u, const double* alpha, const double* xu, d
 // Newton: reduced coupled Jacobian apply [Kuu_bc Kua_bc; Kau Kaa] on inactive set
 int launch_jac(Ctx* c, const double* u, const double* alpha, const double* xu, const double* xa,
                double* yu, double* ya, const unsigned char* act, cudaStream_t st);
+
+// ---- 3D operator launchers (pf_ops3d.cu) --------------------------------------------------------
+int launch3_Kuu(Ctx* c, const double* alpha, const double* x, double* y, int bcmode, cudaStream_t st);
+int launch3_Kuu_cgA(Ctx* c, const double* alpha, const double* z, const double* p_in, double* p_out, double* q,
+                    cudaStream_t st);
+int launch3_Kuu_diag(Ctx* c, const double* alpha, double* dinv, cudaStream_t st);
+int launch3_kappa(Ctx* c, const double* u, double* kappa, double* cvec, cudaStream_t st);
+int launch3_Kaa(Ctx* c, const double* kappa, const double* x, double* y, const unsigned char* act, cudaStream_t st);
+int launch3_Kaa_cgA(Ctx* c, const double* kappa, const double* z, const double* p_in, double* p_out, double* q,
+                    const unsigned char* act, cudaStream_t st);
+int launch3_Kaa_diag(Ctx* c, const double* kappa, double* dinv, const unsigned char* act, cudaStream_t st);
+int launch3_Kaa_trial(Ctx* c, const double* kappa, const double* cvec, const double* x, const double* d,
+                      const double* lb, double* trial, double* F, int merit_slot, cudaStream_t st);
+int launch3_physics(Ctx* c, const double* u, const double* alpha, const double* lb, double* ru, double* ra,
+                    double* phi, int rows, cudaStream_t st);
+int launch3_load(Ctx* c, const double* alpha, double* f, int rows, cudaStream_t st);
+int launch3_jac(Ctx* c, const double* u, const double* alpha, const double* xu, const double* xa, double* yu,
+                double* ya, const unsigned char* act, int mode, int bcmode, cudaStream_t st);
 
 // ---- vector kernels + solvers (pf_core.cu) ---------------------------------------------
 struct PcgBuffers {

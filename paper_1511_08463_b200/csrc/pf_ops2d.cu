@@ -1386,15 +1386,18 @@ static int run_strip(Ctx* c, Op op, cudaStream_t st, int kind = K_VEC, int nw = 
 static RedBuf redbuf(Ctx* c) { return RedBuf{c->partials, c->tickets, c->scal}; }
 
 int launch_Kuu(Ctx* c, const double* alpha, const double* x, double* y, int bcmode, cudaStream_t st) {
+    if (c->dim == 3) return launch3_Kuu(c, alpha, x, y, bcmode, st);
     OpKuu<false> op{alpha, x, nullptr, nullptr, y, bcmode, c->scal, redbuf(c), 0.0};
     return run_strip(c, op, st, K_KUU);
 }
 int launch_Kuu_cgA(Ctx* c, const double* alpha, const double* z, const double* p_in, double* p_out,
                    double* q, cudaStream_t st) {
+    if (c->dim == 3) return launch3_Kuu_cgA(c, alpha, z, p_in, p_out, q, st);
     OpKuu<true> op{alpha, z, p_in, p_out, q, PF_BC_ELIMINATE, c->scal, redbuf(c), 0.0};
     return run_strip(c, op, st, K_KUU_CG);
 }
 int launch_Kuu_diag(Ctx* c, const double* alpha, double* dinv, cudaStream_t st) {
+    if (c->dim == 3) return launch3_Kuu_diag(c, alpha, dinv, st);
     OpKuuDiag op;
     op.alpha = alpha;
     op.dinv = dinv;
@@ -1402,6 +1405,7 @@ int launch_Kuu_diag(Ctx* c, const double* alpha, double* dinv, cudaStream_t st) 
 }
 int launch_kappa(Ctx* c, const double* u, const double* alpha, double* kappa, double* cvec,
                  cudaStream_t st) {
+    if (c->dim == 3) return launch3_kappa(c, u, kappa, cvec, st);
     (void)alpha;
     OpKappa op;
     op.u = u; op.kappa = kappa; op.cvec = cvec;
@@ -1409,6 +1413,7 @@ int launch_kappa(Ctx* c, const double* u, const double* alpha, double* kappa, do
 }
 int launch_Kaa(Ctx* c, const double* kappa, const double* x, double* y, const unsigned char* act,
                cudaStream_t st) {
+    if (c->dim == 3) return launch3_Kaa(c, kappa, x, y, act, st);
     if (act) {
         OpKaa<false, true> op{kappa, x, nullptr, nullptr, y, act, c->scal, redbuf(c), 0.0};
         return run_strip(c, op, st, K_KAA);
@@ -1418,6 +1423,7 @@ int launch_Kaa(Ctx* c, const double* kappa, const double* x, double* y, const un
 }
 int launch_Kaa_cgA(Ctx* c, const double* kappa, const double* z, const double* p_in, double* p_out,
                    double* q, const unsigned char* act, cudaStream_t st) {
+    if (c->dim == 3) return launch3_Kaa_cgA(c, kappa, z, p_in, p_out, q, act, st);
     if (act) {
         OpKaa<true, true> op{kappa, z, p_in, p_out, q, act, c->scal, redbuf(c), 0.0};
         return run_strip(c, op, st, K_KAA_CG);
@@ -1427,6 +1433,7 @@ int launch_Kaa_cgA(Ctx* c, const double* kappa, const double* z, const double* p
 }
 int launch_Kaa_diag(Ctx* c, const double* kappa, double* dinv, const unsigned char* act,
                     cudaStream_t st) {
+    if (c->dim == 3) return launch3_Kaa_diag(c, kappa, dinv, act, st);
     if (act) {
         OpKaaDiag<true> op;
         op.kappa = kappa; op.dinv = dinv; op.act = act;
@@ -1439,12 +1446,14 @@ int launch_Kaa_diag(Ctx* c, const double* kappa, double* dinv, const unsigned ch
 int launch_Kaa_trial(Ctx* c, const double* kappa, const double* cvec, const double* x,
                      const double* d, const double* lb, double* trial, double* F,
                      unsigned char* act, int merit_slot, cudaStream_t st) {
+    if (c->dim == 3) return launch3_Kaa_trial(c, kappa, cvec, x, d, lb, trial, F, merit_slot, st);
     OpKaaTrial op{kappa, cvec, x, d, lb, trial, F, c->scal, merit_slot, redbuf(c), 0.0};
     (void)act;
     return run_strip(c, op, st, K_KAA_TRIAL);
 }
 int launch_physics(Ctx* c, const double* u, const double* alpha, const double* lb, double* ru,
                    double* ra, double* phi, int rows, cudaStream_t st) {
+    if (c->dim == 3) return launch3_physics(c, u, alpha, lb, ru, ra, phi, rows, st);
     const int nw = (ru ? 2 : 0) + (ra ? 1 : 0) + (phi ? 1 : 0);
     switch (rows) {
         case PF_ROWS_ZERO: {
@@ -1463,6 +1472,7 @@ int launch_physics(Ctx* c, const double* u, const double* alpha, const double* l
 }
 int launch_load(Ctx* c, const double* alpha, double* f, const double* u_or_null, int rows,
                 cudaStream_t st) {
+    if (c->dim == 3) return launch3_load(c, alpha, f, rows, st);
     (void)u_or_null;
     if (rows == 0) {
         OpRhs<true> op{alpha, f, c->scal, redbuf(c), 0.0};
@@ -1473,18 +1483,21 @@ int launch_load(Ctx* c, const double* alpha, double* f, const double* u_or_null,
 }
 int launch_Kua(Ctx* c, const double* u, const double* alpha, const double* xa, double* yu,
                int bcmode, cudaStream_t st) {
+    if (c->dim == 3) return launch3_jac(c, u, alpha, nullptr, xa, yu, nullptr, nullptr, 1, bcmode, st);
     OpKua op;
     op.u = u; op.alpha = alpha; op.xa = xa; op.yu = yu; op.bcmode = bcmode;
     return run_strip(c, op, st, K_KUA);
 }
 int launch_Kau(Ctx* c, const double* u, const double* alpha, const double* xu, double* ya,
                int bcmode, cudaStream_t st) {
+    if (c->dim == 3) return launch3_jac(c, u, alpha, xu, nullptr, nullptr, ya, nullptr, 2, bcmode, st);
     OpKau op;
     op.u = u; op.alpha = alpha; op.xu = xu; op.ya = ya; op.bcmode = bcmode;
     return run_strip(c, op, st, K_KAU);
 }
 int launch_jac(Ctx* c, const double* u, const double* alpha, const double* xu, const double* xa,
                double* yu, double* ya, const unsigned char* act, cudaStream_t st) {
+    if (c->dim == 3) return launch3_jac(c, u, alpha, xu, xa, yu, ya, act, 0, PF_BC_ELIMINATE, st);
     OpJac op;
     op.u = u; op.alpha = alpha; op.xu = xu; op.xa = xa; op.yu = yu; op.ya = ya; op.act = act;
     return run_strip(c, op, st, K_JAC);

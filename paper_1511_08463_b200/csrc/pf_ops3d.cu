@@ -1,0 +1,958 @@
+// pf_ops3d.cu -- matrix-free P1 operators on structured 3D Kuhn-tetrahedra meshes (sm_100a, fp64).
+//
+// Each hex cell (I,J,K) is split into the 6 Kuhn tetrahedra around its v000-v111 diagonal; tet
+// s = the s-th permutation (a,b,c) of the axes in itertools order (oracle/meshgen.py:kuhn_paths)
+// with nodes v000, v000+e_a, v000+e_a+e_b, v111.  Its barycentric gradients are
+// -e_a/h_a, e_a/h_a - e_b/h_b, e_b/h_b - e_c/h_c, e_c/h_c, so every strain is three differences
+// along the tet's axis path and every nodal force is a difference of three "axis fluxes".
+//
+// Engine (k_strip3d): a 512-thread block = 16 warps; warp w owns the vertex pencil
+// j = 14*bj - 1 + w, lanes own k = 30*bk - 1 + lane (lanes 1..30 and warps 1..14 produce output),
+// and the block walks vertex rows i of its strip.  Per row step:
+//   * the pencil row ci+1 (and the cell data of row ci) arrive by cp.async PD steps ahead;
+//   * j+1 neighbour values come from warp w+1 through shared memory (barrier A);
+//   * k+1 neighbour values come from lane+1 by shuffle;
+//   * contributions to k+1 go to lane+1 by shuffle, to j+1 to warp w+1 through shared memory
+//     (barrier B), to i+1 are carried in registers.
+// Every input is read once from HBM, every output written once, no atomics (deterministic).
+// Reference formulas: fem.py:149-276 (dim-generic restatement in oracle/p1.py).
+#include "pf_internal.cuh"
+
+namespace pf {
+
+constexpr int kW3 = 16;       // warps per block
+constexpr int kOutJ3 = kW3 - 2;  // output pencils per block
+constexpr int kBlock3 = kW3 * 32;
+
+template <int N> struct IC3 { static constexpr int v = N; };
+
+// the 6 Kuhn paths, itertools.permutations((0,1,2)) order
+template <class F>
+__device__ __forceinline__ void for_each_tet(F&& f) {
+    f(IC3<0>{}, IC3<0>{}, IC3<1>{}, IC3<2>{});
+    f(IC3<1>{}, IC3<0>{}, IC3<2>{}, IC3<1>{});
+    f(IC3<2>{}, IC3<1>{}, IC3<0>{}, IC3<2>{});
+    f(IC3<3>{}, IC3<1>{}, IC3<2>{}, IC3<0>{});
+    f(IC3<4>{}, IC3<2>{}, IC3<0>{}, IC3<1>{});
+    f(IC3<5>{}, IC3<2>{}, IC3<1>{}, IC3<0>{});
+}
+// corner index q = 4*di + 2*dj + dk ; axis bit: i -> 4, j -> 2, k -> 1
+template <int AX> struct Bit { static constexpr int v = AX == 0 ? 4 : (AX == 1 ? 2 : 1); };
+
+__device__ __forceinline__ double ihof(const Geo3& g, int ax) { return ax == 0 ? g.ihx : (ax == 1 ? g.ihy : g.ihz); }
+
+// displacement-gradient based strain of tet (A,B,C): G[comp][axis]
+template <int A, int B, int C>
+__device__ __forceinline__ void tet_grad(const Geo3& g, const double (&U)[3][8], double (&G)[3][3]) {
+    constexpr int q1 = Bit<A>::v, q2 = Bit<A>::v | Bit<B>::v;
+    const double ha = ihof(g, A), hb = ihof(g, B), hc = ihof(g, C);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        G[c][A] = (U[c][q1] - U[c][0]) * ha;
+        G[c][B] = (U[c][q2] - U[c][q1]) * hb;
+        G[c][C] = (U[c][7] - U[c][q2]) * hc;
+    }
+}
+// Voigt strain (e11,e22,e33,g23,g13,g12) from G
+__device__ __forceinline__ void voigt(const double (&G)[3][3], double (&e)[6]) {
+    e[0] = G[0][0]; e[1] = G[1][1]; e[2] = G[2][2];
+    e[3] = G[1][2] + G[2][1]; e[4] = G[0][2] + G[2][0]; e[5] = G[0][1] + G[1][0];
+}
+// unit-E isotropic stress sigma (Voigt) = D e
+__device__ __forceinline__ void stress3(const Geo3& g, const double (&e)[6], double (&s)[6]) {
+    const double tr = g.lam * (e[0] + e[1] + e[2]);
+    s[0] = tr + 2.0 * g.mu * e[0]; s[1] = tr + 2.0 * g.mu * e[1]; s[2] = tr + 2.0 * g.mu * e[2];
+    s[3] = g.mu * e[3]; s[4] = g.mu * e[4]; s[5] = g.mu * e[5];
+}
+// Y_m += k * B_m^T s  for tet (A,B,C): node forces from the axis fluxes F_ax = k s(:,ax) ih_ax
+template <int A, int B, int C>
+__device__ __forceinline__ void tet_scatter(const Geo3& g, double k, const double (&s)[6], double (&Y)[3][8]) {
+    constexpr int q1 = Bit<A>::v, q2 = Bit<A>::v | Bit<B>::v;
+    // sigma as 3x3: [[s0,s5,s4],[s5,s1,s3],[s4,s3,s2]]
+    const double S[3][3] = {{s[0], s[5], s[4]}, {s[5], s[1], s[3]}, {s[4], s[3], s[2]}};
+    const double ka = k * ihof(g, A), kb = k * ihof(g, B), kc = k * ihof(g, C);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const double fa = ka * S[c][A], fb = kb * S[c][B], fc = kc * S[c][C];
+        Y[c][0] -= fa;
+        Y[c][q1] += fa - fb;
+        Y[c][q2] += fb - fc;
+        Y[c][7] += fc;
+    }
+}
+// scalar gradient of tet (A,B,C) and its transpose scatter  Y_m += base + del * grad(lam_m).g
+template <int A, int B, int C>
+__device__ __forceinline__ void tet_sgrad(const Geo3& g, const double (&X)[8], double (&gr)[3]) {
+    constexpr int q1 = Bit<A>::v, q2 = Bit<A>::v | Bit<B>::v;
+    gr[A] = (X[q1] - X[0]) * ihof(g, A);
+    gr[B] = (X[q2] - X[q1]) * ihof(g, B);
+    gr[C] = (X[7] - X[q2]) * ihof(g, C);
+}
+template <int A, int B, int C>
+__device__ __forceinline__ void tet_sscatter(const Geo3& g, double base, double del, const double (&gr)[3],
+                                             double (&Y)[8]) {
+    constexpr int q1 = Bit<A>::v, q2 = Bit<A>::v | Bit<B>::v;
+    const double fa = del * gr[A] * ihof(g, A), fb = del * gr[B] * ihof(g, B), fc = del * gr[C] * ihof(g, C);
+    Y[0] += base - fa;
+    Y[q1] += base + fa - fb;
+    Y[q2] += base + fb - fc;
+    Y[7] += base + fc;
+}
+template <int A, int B, int C>
+__device__ __forceinline__ double tet_abar(const double (&Al)[8]) {
+    constexpr int q1 = Bit<A>::v, q2 = Bit<A>::v | Bit<B>::v;
+    return ((Al[0] + Al[q1]) + (Al[q2] + Al[7])) * 0.25;
+}
+
+// ---- staging helpers (same conventions as 2D: slot q of lane l at q*256 + 8l) ------------------
+__device__ __forceinline__ unsigned smem_addr3(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void cp8(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_addr3(dst)), "l"(src));
+}
+__device__ __forceinline__ void cp4(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_addr3(dst)), "l"(src));
+}
+__device__ __forceinline__ void cp_commit3() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait3() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+struct S3 {
+    unsigned char* p;
+    int lane;
+    __device__ __forceinline__ double* d(int q) const { return reinterpret_cast<double*>(p + q * 256) + lane; }
+    __device__ __forceinline__ unsigned* w(int q) const { return reinterpret_cast<unsigned*>(p + q * 256) + lane; }
+    __device__ __forceinline__ S3 at(int q) const { return S3{p + q * 256, lane}; }
+};
+__device__ __forceinline__ void put1_3(const S3& s, int q, const double* b, long long v) { cp8(s.d(q), b + v); }
+__device__ __forceinline__ void put3_3(const S3& s, int q, const double* b, long long v) {
+    cp8(s.d(q), b + 3 * v); cp8(s.d(q + 1), b + 3 * v + 1); cp8(s.d(q + 2), b + 3 * v + 2);
+}
+__device__ __forceinline__ void putb_3(const S3& s, int q, const unsigned char* b, long long v) {
+    cp4(s.w(q), b + (v & ~3LL));
+}
+__device__ __forceinline__ double get1_3(const S3& s, int q) { return *s.d(q); }
+__device__ __forceinline__ unsigned getb_3(const S3& s, int q, long long v) {
+    return (*s.w(q) >> (8 * (unsigned)(v & 3))) & 0xffu;
+}
+
+__device__ __forceinline__ long long vid3(const Geo3& g, int i, int j, int k) {
+    return ((long long)i * g.nvy + j) * g.nvz + k;
+}
+__device__ __forceinline__ long long cid3(const Geo3& g, int i, int j, int k) {
+    return ((long long)i * g.ny + j) * g.nz + k;
+}
+__device__ __forceinline__ bool onb3(const Geo3& g, int i, int j, int k) {
+    return i == 0 || i == g.nx || j == 0 || j == g.ny || k == 0 || k == g.nz;
+}
+__device__ __forceinline__ unsigned bc3(const Geo3& g, int i, int j, int k, long long v) {
+    return (g.has_bc && onb3(g, i, j, k)) ? (unsigned)g.bcmask[v] : 0u;
+}
+
+// ---- the 3D strip engine ----------------------------------------------------------------------
+template <class Op>
+__global__ void __launch_bounds__(kBlock3, 1) k_strip3d(const Geo3 g, Op op) {
+    constexpr int NV = Op::NV, NC = Op::NC, PD = Op::PD, NE = Op::NE, SV = Op::SV, SC = Op::SC;
+    constexpr int STAGE = (SV + SC) * 256;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double* vx = reinterpret_cast<double*>(smem + kW3 * PD * STAGE);   // [kW3][NV][32]
+    double* cx = vx + kW3 * NV * 32;                                     // [kW3][2][NC][32]
+    if (!op.enter()) return;
+    const int bk = blockIdx.x % g.nbk;
+    const int rest = blockIdx.x / g.nbk;
+    const int bj = rest % g.nbj;
+    const int bs = rest / g.nbj;
+    const int j = bj * kOutJ3 - 1 + w, k = bk * 30 - 1 + lane;
+    const bool vv = j >= 0 && j <= g.ny && k >= 0 && k <= g.nz;
+    const bool cv = j >= 0 && j < g.ny && k >= 0 && k < g.nz && w < kW3 - 1 && lane < 31;
+    const bool ov = vv && w >= 1 && w <= kOutJ3 && lane >= 1 && lane <= 30;
+    const int i0 = bs * g.S;
+    const int i1 = min(i0 + g.S, g.nx + 1);
+    const int vlast = min(i1, g.nx), clast = min(i1 - 1, g.nx - 1);
+    unsigned char* wbase = smem + w * (PD * STAGE);
+    double vc[NV], rc[NV], carry[NC];
+#pragma unroll
+    for (int q = 0; q < NC; ++q) carry[q] = 0.0;
+    int ci = i0 - 1;
+    auto issue = [&](int u, int r, int cr) {
+        const S3 s{wbase + u * STAGE, lane};
+        if (r <= vlast && vv) op.issue_v(g, r, j, k, s);
+        if (cr >= 0 && cr <= clast && cv) op.issue_c(g, cr, j, k, s.at(SV));
+        cp_commit3();
+    };
+#pragma unroll
+    for (int q = 0; q < NV; ++q) vc[q] = 0.0;
+    if (ci >= 0 && vv) {
+        const S3 s0{wbase, lane};
+        op.issue_v(g, ci, j, k, s0);
+        cp_commit3();
+        cp_wait3<0>();
+        op.fix_v(g, ci, j, k, s0, vc);
+    }
+    // j+1 neighbour at row ci through shared memory
+#pragma unroll
+    for (int q = 0; q < NV; ++q) vx[(w * NV + q) * 32 + lane] = vc[q];
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < NV; ++q) rc[q] = (w + 1 < kW3) ? vx[((w + 1) * NV + q) * 32 + lane] : 0.0;
+    __syncthreads();  // every warp has its initial neighbour values before vx is overwritten
+#pragma unroll
+    for (int u = 0; u < PD; ++u) issue(u, ci + 1 + u, ci + u);
+    while (ci < i1) {
+#pragma unroll
+        for (int u = 0; u < PD; ++u) {
+            if (ci < i1) {
+                cp_wait3<PD - 1>();
+                const S3 s{wbase + u * STAGE, lane};
+                double vn[NV], rn[NV], ec[NE];
+#pragma unroll
+                for (int q = 0; q < NV; ++q) vn[q] = 0.0;
+#pragma unroll
+                for (int q = 0; q < NE; ++q) ec[q] = 0.0;
+                const bool cell_ok = ci >= 0 && ci < g.nx && cv;
+                if (ci + 1 <= vlast && vv) op.fix_v(g, ci + 1, j, k, s, vn);
+                if (cell_ok) op.fix_c(g, ci, j, k, s.at(SV), ec);
+                // vx / cx readers of the previous step finished before its barrier B
+#pragma unroll
+                for (int q = 0; q < NV; ++q) vx[(w * NV + q) * 32 + lane] = vn[q];
+                __syncthreads();  // barrier A
+#pragma unroll
+                for (int q = 0; q < NV; ++q) rn[q] = (w + 1 < kW3) ? vx[((w + 1) * NV + q) * 32 + lane] : 0.0;
+                // corners: q = 4 di + 2 dj + dk
+                double X[NV][8];
+#pragma unroll
+                for (int q = 0; q < NV; ++q) {
+                    X[q][0] = vc[q]; X[q][2] = rc[q]; X[q][4] = vn[q]; X[q][6] = rn[q];
+                    X[q][1] = __shfl_down_sync(PF_FULL, vc[q], 1);
+                    X[q][3] = __shfl_down_sync(PF_FULL, rc[q], 1);
+                    X[q][5] = __shfl_down_sync(PF_FULL, vn[q], 1);
+                    X[q][7] = __shfl_down_sync(PF_FULL, rn[q], 1);
+                }
+                double Y[NC][8];
+#pragma unroll
+                for (int q = 0; q < NC; ++q)
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) Y[q][c] = 0.0;
+                if (cell_ok) op.cell(g, ci, j, k, X, ec, Y, (ci >= i0) && ov);
+                // k-combine: T_ab = Y[ab0] + shfl_up(Y[ab1])
+                double T00[NC], T01[NC], T10[NC], T11[NC];
+#pragma unroll
+                for (int q = 0; q < NC; ++q) {
+                    T00[q] = Y[q][0] + __shfl_up_sync(PF_FULL, Y[q][1], 1);
+                    T01[q] = Y[q][2] + __shfl_up_sync(PF_FULL, Y[q][3], 1);
+                    T10[q] = Y[q][4] + __shfl_up_sync(PF_FULL, Y[q][5], 1);
+                    T11[q] = Y[q][6] + __shfl_up_sync(PF_FULL, Y[q][7], 1);
+                }
+#pragma unroll
+                for (int q = 0; q < NC; ++q) {
+                    cx[((w * 2 + 0) * NC + q) * 32 + lane] = T01[q];
+                    cx[((w * 2 + 1) * NC + q) * 32 + lane] = T11[q];
+                }
+                __syncthreads();  // barrier B
+                double tot[NC];
+#pragma unroll
+                for (int q = 0; q < NC; ++q) {
+                    const double l01 = w > 0 ? cx[(((w - 1) * 2 + 0) * NC + q) * 32 + lane] : 0.0;
+                    const double l11 = w > 0 ? cx[(((w - 1) * 2 + 1) * NC + q) * 32 + lane] : 0.0;
+                    tot[q] = carry[q] + T00[q] + l01;
+                    carry[q] = T10[q] + l11;
+                }
+                if (ci >= i0 && ov) op.out(g, ci, j, k, tot, vc);
+#pragma unroll
+                for (int q = 0; q < NV; ++q) { vc[q] = vn[q]; rc[q] = rn[q]; }
+                issue(u, ci + 1 + PD, ci + PD);
+                ++ci;
+            }
+        }
+    }
+    cp_wait3<0>();
+    op.finish();
+}
+
+struct NoRed3 {
+    __device__ bool enter() const { return true; }
+    __device__ void finish() {}
+};
+__device__ __forceinline__ double getE3(const Geo3& g, const S3& s, int q) { return g.E_cell ? get1_3(s, q) : g.E; }
+__device__ __forceinline__ double getGc3(const Geo3& g, const S3& s, int q) { return g.Gc_cell ? get1_3(s, q) : g.Gc; }
+__device__ __forceinline__ void putE3(const Geo3& g, const S3& s, int q, long long c) { if (g.E_cell) put1_3(s, q, g.E_cell, c); }
+__device__ __forceinline__ void putGc3(const Geo3& g, const S3& s, int q, long long c) { if (g.Gc_cell) put1_3(s, q, g.Gc_cell, c); }
+
+// ================================================================================================
+// Kuu (plain or fused CG step A).  vertex slots: x|z (3), [p_in (3)], alpha ; cell: E
+// ================================================================================================
+template <bool FUSED>
+struct Op3Kuu {
+    static constexpr int NV = 4, NC = 3, PD = 3, NE = 1, SV = FUSED ? 7 : 4, SC = 1;
+    const double* alpha;
+    const double* x;
+    const double* pin;
+    double* pout;
+    double* y;
+    int bcmode;
+    double* scal;
+    RedBuf rb;
+    double acc;
+    __device__ bool enter() const { return !FUSED || (scal[S_DONE] == 0.0 && scal[S_FAIL] == 0.0); }
+    __device__ __forceinline__ double beta() const { return scal[S_ITER] > 0.0 ? scal[S_BETA] : 0.0; }
+    __device__ void issue_v(const Geo3& g, int i, int j, int k, const S3& s) const {
+        const long long v = vid3(g, i, j, k);
+        put3_3(s, 0, x, v);
+        if (FUSED) { put3_3(s, 3, pin, v); put1_3(s, 6, alpha, v); }
+        else put1_3(s, 3, alpha, v);
+    }
+    __device__ void fix_v(const Geo3& g, int i, int j, int k, const S3& s, double (&v)[NV]) const {
+        const unsigned m = bcmode ? bc3(g, i, j, k, vid3(g, i, j, k)) : 0u;
+        const double b = FUSED ? beta() : 0.0;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            double xv = get1_3(s, c);
+            if (FUSED) xv += b * get1_3(s, 3 + c);
+            v[c] = ((m >> c) & 1u) ? 0.0 : xv;
+        }
+        v[3] = get1_3(s, FUSED ? 6 : 3);
+    }
+    __device__ void issue_c(const Geo3& g, int ci, int j, int k, const S3& s) const { putE3(g, s, 0, cid3(g, ci, j, k)); }
+    __device__ void fix_c(const Geo3& g, int, int, int, const S3& s, double (&e)[NE]) const { e[0] = getE3(g, s, 0); }
+    __device__ void cell(const Geo3& g, int, int, int, const double (&X)[NV][8], const double (&ec)[NE],
+                         double (&Y)[NC][8], bool) {
+        const double (&U)[3][8] = *reinterpret_cast<const double(*)[3][8]>(&X[0][0]);
+        for_each_tet([&](auto, auto A, auto B, auto C) {
+            const double ab = tet_abar<A.v, B.v, C.v>(X[3]);
+            const double om = 1.0 - ab;
+            const double s = (om * om + g.kell) * g.vol * ec[0];
+            double G[3][3], e[6], sg[6];
+            tet_grad<A.v, B.v, C.v>(g, U, G);
+            voigt(G, e);
+            stress3(g, e, sg);
+            tet_scatter<A.v, B.v, C.v>(g, s, sg, Y);
+        });
+    }
+    __device__ __forceinline__ double xval(const Geo3&, long long v, int c) const {
+        double z = __ldg(x + 3 * v + c);
+        if (FUSED) z += beta() * __ldg(pin + 3 * v + c);
+        return z;
+    }
+    __device__ void out(const Geo3& g, int i, int j, int k, const double (&t)[NC], const double (&v)[NV]) {
+        const long long id = vid3(g, i, j, k);
+        const unsigned m = bcmode ? bc3(g, i, j, k, id) : 0u;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            double yy = t[c], p = v[c];
+            if ((m >> c) & 1u) { p = xval(g, id, c); yy = p; }
+            y[3 * id + c] = yy;
+            if (FUSED) { pout[3 * id + c] = p; acc += p * yy; }
+        }
+    }
+    __device__ void finish() {
+        if (!FUSED) return;
+        double vv[1] = {acc};
+        double* s = scal;
+        grid_reduce<1>(vv, rb, 0, [s](double* tot) {
+            s[S_PAP] = tot[0];
+            if (!(tot[0] > 0.0)) s[S_FAIL] = 1.0;
+            else s[S_GAMMA] = s[S_RZ] / tot[0];
+        });
+    }
+};
+
+// diag(Kuu) -> dinv (eliminated rows 1).  vertex: alpha ; cell: E
+struct Op3KuuDiag : NoRed3 {
+    static constexpr int NV = 1, NC = 3, PD = 3, NE = 1, SV = 1, SC = 1;
+    const double* alpha;
+    double* dinv;
+    __device__ void issue_v(const Geo3& g, int i, int j, int k, const S3& s) const { put1_3(s, 0, alpha, vid3(g, i, j, k)); }
+    __device__ void fix_v(const Geo3&, int, int, int, const S3& s, double (&v)[NV]) const { v[0] = get1_3(s, 0); }
+    __device__ void issue_c(const Geo3& g, int ci, int j, int k, const S3& s) const { putE3(g, s, 0, cid3(g, ci, j, k)); }
+    __device__ void fix_c(const Geo3& g, int, int, int, const S3& s, double (&e)[NE]) const { e[0] = getE3(g, s, 0); }
+    __device__ void cell(const Geo3& g, int, int, int, const double (&X)[NV][8], const double (&ec)[NE],
+                         double (&Y)[NC][8], bool) {
+        for_each_tet([&](auto, auto A, auto B, auto C) {
+            const double ab = tet_abar<A.v, B.v, C.v>(X[0]);
+            const double om = 1.0 - ab;
+            const double s = (om * om + g.kell) * g.vol * ec[0];
+            constexpr int q1 = Bit<A.v>::v, q2 = Bit<A.v>::v | Bit<B.v>::v;
+            const double ha = ihof(g, A.v), hb = ihof(g, B.v), hc = ihof(g, C.v);
+            // grad lambda per node: (axis weights); diag block entry for comp c:
+            // |grad|^2 mu + (lam + mu) grad_c^2
+            auto add = [&](int q, double ga, double gb, double gc) {
+                double gr[3] = {0, 0, 0};
+                gr[A.v] = ga; gr[B.v] = gb; gr[C.v] = gc;
+                const double n2 = gr[0] * gr[0] + gr[1] * gr[1] + gr[2] * gr[2];
+                for (int c = 0; c < 3; ++c) Y[c][q] += s * (g.mu * n2 + (g.lam + g.mu) * gr[c] * gr[c]);
+            };
+            add(0, -ha, 0.0, 0.0);
+            add(q1, ha, -hb, 0.0);
+            add(q2, 0.0, hb, -hc);
+            add(7, 0.0, 0.0, hc);
+        });
+    }
+    __device__ void out(const Geo3& g, int i, int j, int k, const double (&t)[NC], const double (&)[NV]) {
+        const long long id = vid3(g, i, j, k);
+        const unsigned m = bc3(g, i, j, k, id);
+        for (int c = 0; c < 3; ++c) dinv[3 * id + c] = ((m >> c) & 1u) ? 1.0 : 1.0 / t[c];
+    }
+};
+
+// ================================================================================================
+// Damage block: kappa_e = (q + [AT2] 2 kc/ell) |T| / 16 ; c_v = sum_e |T|/4 (-q + [AT1] kc/ell)
+// vertex: u (3) ; cell: E, Gc
+// ================================================================================================
+struct Op3Kappa : NoRed3 {
+    static constexpr int NV = 3, NC = 1, PD = 3, NE = 2, SV = 3, SC = 2;
+    const double* u;
+    double* kappa;
+    double* cvec;
+    __device__ void issue_v(const Geo3& g, int i, int j, int k, const S3& s) const { put3_3(s, 0, u, vid3(g, i, j, k)); }
+    __device__ void fix_v(const Geo3&, int, int, int, const S3& s, double (&v)[NV]) const {
+        v[0] = get1_3(s, 0); v[1] = get1_3(s, 1); v[2] = get1_3(s, 2);
+    }
+    __device__ void issue_c(const Geo3& g, int ci, int j, int k, const S3& s) const {
+        const long long c = cid3(g, ci, j, k);
+        putE3(g, s, 0, c);
+        putGc3(g, s, 1, c);
+    }
+    __device__ void fix_c(const Geo3& g, int, int, int, const S3& s, double (&e)[NE]) const {
+        e[0] = getE3(g, s, 0);
+        e[1] = getGc3(g, s, 1);
+    }
+    __device__ void cell(const Geo3& g, int ci, int j, int k, const double (&X)[NV][8], const double (&ec)[NE],
+                         double (&Y)[NC][8], bool own) {
+        const double (&U)[3][8] = *reinterpret_cast<const double(*)[3][8]>(&X[0][0]);
+        const long long cell = cid3(g, ci, j, k);
+        const double kc = ec[1] / g.cw;
+        for_each_tet([&](auto S, auto A, auto B, auto C) {
+            double G[3][3], e[6], sg[6];
+            tet_grad<A.v, B.v, C.v>(g, U, G);
+            voigt(G, e);
+            stress3(g, e, sg);
+            const double q = ec[0] * (e[0] * sg[0] + e[1] * sg[1] + e[2] * sg[2] + e[3] * sg[3] + e[4] * sg[4] +
+                                      e[5] * sg[5]);
+            const double kap = (q + (g.at2 ? 2.0 * kc / g.ell : 0.0)) * g.vol * (1.0 / 16.0);
+            const double cc = g.vol * 0.25 * (-q + (g.at2 ? 0.0 : kc / g.ell));
+            constexpr int q1 = Bit<A.v>::v, q2 = Bit<A.v>::v | Bit<B.v>::v;
+            Y[0][0] += cc; Y[0][q1] += cc; Y[0][q2] += cc; Y[0][7] += cc;
+            if (own) kappa[(long long)S.v * g.ncell + cell] = kap;
+        });
+    }
+    __device__ void out(const Geo3& g, int i, int j, int k, const double (&t)[NC], const double (&)[NV]) {
+        cvec[vid3(g, i, j, k)] = t[0];
+    }
+};
+
+template <int A, int B, int C>
+__device__ __forceinline__ void elem3_kaa(const Geo3& g, double kap, double kc, const double (&X)[8], double (&Y)[8]) {
+    constexpr int q1 = Bit<A>::v, q2 = Bit<A>::v | Bit<B>::v;
+    const double del = 2.0 * kc * g.ell * g.vol;
+    double gr[3];
+    tet_sgrad<A, B, C>(g, X, gr);
+    tet_sscatter<A, B, C>(g, kap * ((X[0] + X[q1]) + (X[q2] + X[7])), del, gr, Y);
+}
+
+// Kaa apply (plain / fused CG / masked).  vertex: x|z, [p_in], [act word] ; cell: Gc, kappa x 6
+template <bool FUSED, bool MASKED>
+struct Op3Kaa {
+    static constexpr int NV = 1, NC = 1, PD = 4, NE = 7;
+    static constexpr int SV = 1 + (FUSED ? 1 : 0) + (MASKED ? 1 : 0), SC = 7;
+    const double* kappa;
+    const double* x;
+    const double* pin;
+    double* pout;
+    double* y;
+    const unsigned char* act;
+    double* scal;
+    RedBuf rb;
+    double acc;
+    __device__ bool enter() const { return !FUSED || (scal[S_DONE] == 0.0 && scal[S_FAIL] == 0.0); }
+    __device__ __forceinline__ double bval() const { return scal[S_ITER] > 0.0 ? scal[S_BETA] : 0.0; }
+    __device__ void issue_v(const Geo3& g, int i, int j, int k, const S3& s) const {
+        const long long v = vid3(g, i, j, k);
+        put1_3(s, 0, x, v);
+        if (FUSED) put1_3(s, 1, pin, v);
+        if (MASKED) putb_3(s, FUSED ? 2 : 1, act, v);
+    }
+    __device__ void fix_v(const Geo3& g, int i, int j, int k, const S3& s, double (&v)[NV]) const {
+        double z = get1_3(s, 0);
+        if (FUSED) z += bval() * get1_3(s, 1);
+        const bool a = MASKED && getb_3(s, FUSED ? 2 : 1, vid3(g, i, j, k)) != 0u;
+        v[0] = a ? 0.0 : z;
+    }
+    __device__ void issue_c(const Geo3& g, int ci, int j, int k, const S3& s) const {
+        const long long c = cid3(g, ci, j, k);
+        putGc3(g, s, 0, c);
+#pragma unroll
+        for (int t = 0; t < 6; ++t) put1_3(s, 1 + t, kappa, (long long)t * g.ncell + c);
+    }
+    __device__ void fix_c(const Geo3& g, int, int, int, const S3& s, double (&e)[NE]) const {
+        e[0] = getGc3(g, s, 0);
+#pragma unroll
+        for (int t = 0; t < 6; ++t) e[1 + t] = get1_3(s, 1 + t);
+    }
+    __device__ void cell(const Geo3& g, int, int, int, const double (&X)[NV][8], const double (&ec)[NE],
+                         double (&Y)[NC][8], bool) {
+        const double kc = ec[0] / g.cw;
+        for_each_tet([&](auto S, auto A, auto B, auto C) { elem3_kaa<A.v, B.v, C.v>(g, ec[1 + S.v], kc, X[0], Y[0]); });
+    }
+    __device__ void out(const Geo3& g, int i, int j, int k, const double (&t)[NC], const double (&v)[NV]) {
+        const long long id = vid3(g, i, j, k);
+        double yy = t[0], p = v[0];
+        if (MASKED && act[id]) {
+            p = __ldg(x + id);
+            if (FUSED) p += bval() * __ldg(pin + id);
+            yy = p;
+        }
+        y[id] = yy;
+        if (FUSED) { pout[id] = p; acc += p * yy; }
+    }
+    __device__ void finish() {
+        if (!FUSED) return;
+        double vv[1] = {acc};
+        double* s = scal;
+        grid_reduce<1>(vv, rb, 0, [s](double* tot) {
+            s[S_PAP] = tot[0];
+            if (!(tot[0] > 0.0)) s[S_FAIL] = 1.0;
+            else s[S_GAMMA] = s[S_RZ] / tot[0];
+        });
+    }
+};
+
+template <bool MASKED>
+struct Op3KaaDiag : NoRed3 {
+    static constexpr int NV = 1, NC = 1, PD = 3, NE = 7, SV = 0, SC = 7;
+    const double* kappa;
+    double* dinv;
+    const unsigned char* act;
+    __device__ void issue_v(const Geo3&, int, int, int, const S3&) const {}
+    __device__ void fix_v(const Geo3&, int, int, int, const S3&, double (&v)[NV]) const { v[0] = 0.0; }
+    __device__ void issue_c(const Geo3& g, int ci, int j, int k, const S3& s) const {
+        const long long c = cid3(g, ci, j, k);
+        putGc3(g, s, 0, c);
+        for (int t = 0; t < 6; ++t) put1_3(s, 1 + t, kappa, (long long)t * g.ncell + c);
+    }
+    __device__ void fix_c(const Geo3& g, int, int, int, const S3& s, double (&e)[NE]) const {
+        e[0] = getGc3(g, s, 0);
+        for (int t = 0; t < 6; ++t) e[1 + t] = get1_3(s, 1 + t);
+    }
+    __device__ void cell(const Geo3& g, int, int, int, const double (&)[NV][8], const double (&ec)[NE],
+                         double (&Y)[NC][8], bool) {
+        const double kc = ec[0] / g.cw;
+        for_each_tet([&](auto S, auto A, auto B, auto C) {
+            constexpr int q1 = Bit<A.v>::v, q2 = Bit<A.v>::v | Bit<B.v>::v;
+            const double del = 2.0 * kc * g.ell * g.vol;
+            const double ha = ihof(g, A.v), hb = ihof(g, B.v), hc = ihof(g, C.v);
+            const double kap = ec[1 + S.v];
+            Y[0][0] += kap + del * ha * ha;
+            Y[0][q1] += kap + del * (ha * ha + hb * hb);
+            Y[0][q2] += kap + del * (hb * hb + hc * hc);
+            Y[0][7] += kap + del * hc * hc;
+        });
+    }
+    __device__ void out(const Geo3& g, int i, int j, int k, const double (&t)[NC], const double (&)[NV]) {
+        const long long id = vid3(g, i, j, k);
+        dinv[id] = (MASKED && act[id]) ? 1.0 : 1.0 / t[0];
+    }
+};
+
+// VI line-search trial: trial = clip(x + mu d, lb, 1) ; F = Kaa trial + c ; merit
+struct Op3KaaTrial {
+    static constexpr int NV = 1, NC = 1, PD = 3, NE = 7, SV = 3, SC = 7;
+    const double* kappa;
+    const double* cvec;
+    const double* x;
+    const double* d;
+    const double* lb;
+    double* trial;
+    double* F;
+    double* scal;
+    int merit_slot;
+    RedBuf rb;
+    double acc_m;
+    __device__ bool enter() const { return true; }
+    __device__ void issue_v(const Geo3& g, int i, int j, int k, const S3& s) const {
+        const long long v = vid3(g, i, j, k);
+        put1_3(s, 0, x, v);
+        if (d) { put1_3(s, 1, d, v); put1_3(s, 2, lb, v); }
+    }
+    __device__ void fix_v(const Geo3&, int, int, int, const S3& s, double (&v)[NV]) const {
+        const double xv = get1_3(s, 0);
+        v[0] = d ? fmin(fmax(xv + scal[S_MU] * get1_3(s, 1), get1_3(s, 2)), 1.0) : xv;
+    }
+    __device__ void issue_c(const Geo3& g, int ci, int j, int k, const S3& s) const {
+        const long long c = cid3(g, ci, j, k);
+        putGc3(g, s, 0, c);
+        for (int t = 0; t < 6; ++t) put1_3(s, 1 + t, kappa, (long long)t * g.ncell + c);
+    }
+    __device__ void fix_c(const Geo3& g, int, int, int, const S3& s, double (&e)[NE]) const {
+        e[0] = getGc3(g, s, 0);
+        for (int t = 0; t < 6; ++t) e[1 + t] = get1_3(s, 1 + t);
+    }
+    __device__ void cell(const Geo3& g, int, int, int, const double (&X)[NV][8], const double (&ec)[NE],
+                         double (&Y)[NC][8], bool) {
+        const double kc = ec[0] / g.cw;
+        for_each_tet([&](auto S, auto A, auto B, auto C) { elem3_kaa<A.v, B.v, C.v>(g, ec[1 + S.v], kc, X[0], Y[0]); });
+    }
+    __device__ void out(const Geo3& g, int i, int j, int k, const double (&t)[NC], const double (&v)[NV]) {
+        const long long id = vid3(g, i, j, k);
+        const double Fv = t[0] + __ldg(cvec + id), tv = v[0], l = __ldg(lb + id);
+        trial[id] = tv;
+        F[id] = Fv;
+        const double ph = (hypot(tv - l, hypot(1.0 - tv, -Fv) - (1.0 - tv) + Fv) - (tv - l) -
+                           (hypot(1.0 - tv, -Fv) - (1.0 - tv) + Fv));
+        acc_m += ph * ph;
+    }
+    __device__ void finish() {
+        double vv[1] = {acc_m};
+        double* s = scal;
+        const int ms = merit_slot;
+        grid_reduce<1>(vv, rb, 1, [s, ms](double* tot) { s[ms] = tot[0]; });
+    }
+};
+
+// ================================================================================================
+// Physics pass (energies, r_u, r_alpha, Phi, norms).  vertex: u (3), alpha ; cell: E, Gc
+// ================================================================================================
+template <int ROWS>
+struct Op3Phys {
+    static constexpr int NV = 4, NC = 4, PD = 2, NE = 2, SV = 4, SC = 2;
+    const double* u;
+    const double* alpha;
+    const double* lb;
+    double* ru;
+    double* ra;
+    double* phi;
+    double* scal;
+    RedBuf rb;
+    double eel, ed, nru, nphi;
+    __device__ bool enter() const { return true; }
+    __device__ void issue_v(const Geo3& g, int i, int j, int k, const S3& s) const {
+        const long long v = vid3(g, i, j, k);
+        put3_3(s, 0, u, v);
+        put1_3(s, 3, alpha, v);
+    }
+    __device__ void fix_v(const Geo3&, int, int, int, const S3& s, double (&v)[NV]) const {
+        for (int q = 0; q < 4; ++q) v[q] = get1_3(s, q);
+    }
+    __device__ void issue_c(const Geo3& g, int ci, int j, int k, const S3& s) const {
+        const long long c = cid3(g, ci, j, k);
+        putE3(g, s, 0, c);
+        putGc3(g, s, 1, c);
+    }
+    __device__ void fix_c(const Geo3& g, int, int, int, const S3& s, double (&e)[NE]) const {
+        e[0] = getE3(g, s, 0);
+        e[1] = getGc3(g, s, 1);
+    }
+    __device__ void cell(const Geo3& g, int, int, int, const double (&X)[NV][8], const double (&ec)[NE],
+                         double (&Y)[NC][8], bool own) {
+        const double (&U)[3][8] = *reinterpret_cast<const double(*)[3][8]>(&X[0][0]);
+        double (&YU)[3][8] = *reinterpret_cast<double(*)[3][8]>(&Y[0][0]);
+        const double Ec = ec[0], kc = ec[1] / g.cw;
+        for_each_tet([&](auto, auto A, auto B, auto C) {
+            const double ab = tet_abar<A.v, B.v, C.v>(X[3]);
+            const double om = 1.0 - ab;
+            const double a = om * om + g.kell, ap = -2.0 * om;
+            const double w = g.at2 ? ab * ab : ab, wp = g.at2 ? 2.0 * ab : 1.0;
+            double G[3][3], e[6], sg[6], gr[3];
+            tet_grad<A.v, B.v, C.v>(g, U, G);
+            voigt(G, e);
+            stress3(g, e, sg);
+            const double q = Ec * (e[0] * sg[0] + e[1] * sg[1] + e[2] * sg[2] + e[3] * sg[3] + e[4] * sg[4] +
+                                   e[5] * sg[5]);
+            tet_scatter<A.v, B.v, C.v>(g, a * g.vol * Ec, sg, YU);
+            tet_sgrad<A.v, B.v, C.v>(g, X[3], gr);
+            const double nod = (0.5 * ap * q + kc * wp / g.ell) * g.vol * 0.25;
+            tet_sscatter<A.v, B.v, C.v>(g, nod, 2.0 * kc * g.ell * g.vol, gr, Y[3]);
+            if (own) {
+                eel += 0.5 * g.vol * a * q;
+                ed += g.vol * kc * (w / g.ell + g.ell * (gr[0] * gr[0] + gr[1] * gr[1] + gr[2] * gr[2]));
+            }
+        });
+    }
+    __device__ void out(const Geo3& g, int i, int j, int k, const double (&t)[NC], const double (&v)[NV]) {
+        const long long id = vid3(g, i, j, k);
+        const unsigned m = bc3(g, i, j, k, id);
+        double r[3] = {t[0], t[1], t[2]};
+        for (int c = 0; c < 3; ++c) {
+            if ((m >> c) & 1u) {
+                if (ROWS == PF_ROWS_ZERO) r[c] = 0.0;
+                else if (ROWS == PF_ROWS_VALUE) r[c] = __ldg(u + 3 * id + c) - __ldg(g.ubar + 3 * id + c);
+            }
+            if (ru) ru[3 * id + c] = r[c];
+            nru += r[c] * r[c];
+        }
+        if (ra) ra[id] = t[3];
+        if (lb) {
+            const double av = v[3], rav = t[3];
+            const double inner = hypot(1.0 - av, -rav) - (1.0 - av) + rav;
+            const double ph = hypot(av - __ldg(lb + id), inner) - (av - __ldg(lb + id)) - inner;
+            if (phi) phi[id] = ph;
+            nphi += ph * ph;
+        }
+    }
+    __device__ void finish() {
+        double vv[4] = {eel, ed, nru, nphi};
+        double* s = scal;
+        grid_reduce<4>(vv, rb, 2, [s](double* tot) {
+            s[S_PHYS0 + 0] = tot[0]; s[S_PHYS0 + 1] = tot[1]; s[S_PHYS0 + 2] = tot[2]; s[S_PHYS0 + 3] = tot[3];
+        });
+    }
+};
+
+// Elastic right-hand side b = -M r_raw(g) + (I - M) ubar (or the load f).  vertex: alpha ; cell: E
+template <bool LOADONLY>
+struct Op3Rhs {
+    static constexpr int NV = 4, NC = 3, PD = 3, NE = 1, SV = 1, SC = 1;
+    const double* alpha;
+    double* b;
+    double* scal;
+    RedBuf rb;
+    double acc;
+    __device__ bool enter() const { return true; }
+    __device__ void issue_v(const Geo3& g, int i, int j, int k, const S3& s) const { put1_3(s, 0, alpha, vid3(g, i, j, k)); }
+    __device__ void fix_v(const Geo3& g, int i, int j, int k, const S3& s, double (&v)[NV]) const {
+        const long long id = vid3(g, i, j, k);
+        v[0] = v[1] = v[2] = 0.0;
+        if (!LOADONLY) {
+            const unsigned m = bc3(g, i, j, k, id);
+            for (int c = 0; c < 3; ++c)
+                if ((m >> c) & 1u) v[c] = __ldg(g.ubar + 3 * id + c);
+        }
+        v[3] = get1_3(s, 0);
+    }
+    __device__ void issue_c(const Geo3& g, int ci, int j, int k, const S3& s) const { putE3(g, s, 0, cid3(g, ci, j, k)); }
+    __device__ void fix_c(const Geo3& g, int, int, int, const S3& s, double (&e)[NE]) const { e[0] = getE3(g, s, 0); }
+    __device__ void cell(const Geo3& g, int, int, int, const double (&X)[NV][8], const double (&ec)[NE],
+                         double (&Y)[NC][8], bool) {
+        const double (&U)[3][8] = *reinterpret_cast<const double(*)[3][8]>(&X[0][0]);
+        for_each_tet([&](auto, auto A, auto B, auto C) {
+            const double ab = tet_abar<A.v, B.v, C.v>(X[3]);
+            const double om = 1.0 - ab;
+            const double s = (om * om + g.kell) * g.vol * ec[0];
+            double G[3][3], e[6] = {0, 0, 0, 0, 0, 0}, sg[6];
+            if (!LOADONLY) {
+                tet_grad<A.v, B.v, C.v>(g, U, G);
+                voigt(G, e);
+            }
+            stress3(g, e, sg);
+            tet_scatter<A.v, B.v, C.v>(g, s, sg, Y);
+        });
+    }
+    __device__ void out(const Geo3& g, int i, int j, int k, const double (&t)[NC], const double (&v)[NV]) {
+        const long long id = vid3(g, i, j, k);
+        const unsigned m = LOADONLY ? 0u : bc3(g, i, j, k, id);
+        for (int c = 0; c < 3; ++c) {
+            const double bv = ((m >> c) & 1u) ? v[c] : -t[c];
+            b[3 * id + c] = bv;
+            acc += bv * bv;
+        }
+    }
+    __device__ void finish() {
+        double vv[1] = {acc};
+        double* s = scal;
+        grid_reduce<1>(vv, rb, 3, [s](double* tot) { s[S_AUX0] = tot[0]; });
+    }
+};
+
+// Coupled Jacobian apply [[Kuu_bc, Kua_bc], [Kau_bc, Kaa]] (optionally masked by act), also used
+// for Kua (xu = 0) / Kau (xa = 0) alone.  vertex: u, alpha, xu, xa, [act] ; cell: E, Gc
+struct Op3Jac : NoRed3 {
+    static constexpr int NV = 8, NC = 4, PD = 2, NE = 2, SV = 9, SC = 2;
+    const double* u;
+    const double* alpha;
+    const double* xu;
+    const double* xa;
+    double* yu;
+    double* ya;
+    const unsigned char* act;
+    int mode;  // 0 full Jacobian (masked), 1 Kua (yu = Kua xa), 2 Kau (ya = Kau xu)
+    int bcmode;
+    __device__ void issue_v(const Geo3& g, int i, int j, int k, const S3& s) const {
+        const long long v = vid3(g, i, j, k);
+        put3_3(s, 0, u, v);
+        put1_3(s, 3, alpha, v);
+        if (xu) put3_3(s, 4, xu, v);
+        if (xa) put1_3(s, 7, xa, v);
+        if (act) putb_3(s, 8, act, v);
+    }
+    __device__ void fix_v(const Geo3& g, int i, int j, int k, const S3& s, double (&v)[NV]) const {
+        const long long id = vid3(g, i, j, k);
+        const unsigned m = bcmode ? bc3(g, i, j, k, id) : 0u;
+        for (int q = 0; q < 4; ++q) v[q] = get1_3(s, q);
+        for (int c = 0; c < 3; ++c) v[4 + c] = (xu && !((m >> c) & 1u)) ? get1_3(s, 4 + c) : 0.0;
+        const bool a = act && getb_3(s, 8, id) != 0u;
+        v[7] = (xa && !a) ? get1_3(s, 7) : 0.0;
+    }
+    __device__ void issue_c(const Geo3& g, int ci, int j, int k, const S3& s) const {
+        const long long c = cid3(g, ci, j, k);
+        putE3(g, s, 0, c);
+        putGc3(g, s, 1, c);
+    }
+    __device__ void fix_c(const Geo3& g, int, int, int, const S3& s, double (&e)[NE]) const {
+        e[0] = getE3(g, s, 0);
+        e[1] = getGc3(g, s, 1);
+    }
+    __device__ void cell(const Geo3& g, int, int, int, const double (&X)[NV][8], const double (&ec)[NE],
+                         double (&Y)[NC][8], bool) {
+        const double (&U)[3][8] = *reinterpret_cast<const double(*)[3][8]>(&X[0][0]);
+        const double (&XU)[3][8] = *reinterpret_cast<const double(*)[3][8]>(&X[4][0]);
+        double (&YU)[3][8] = *reinterpret_cast<double(*)[3][8]>(&Y[0][0]);
+        const double Ec = ec[0], kc = ec[1] / g.cw;
+        for_each_tet([&](auto, auto A, auto B, auto C) {
+            constexpr int q1 = Bit<A.v>::v, q2 = Bit<A.v>::v | Bit<B.v>::v;
+            const double ab = tet_abar<A.v, B.v, C.v>(X[3]);
+            const double om = 1.0 - ab;
+            const double a = om * om + g.kell, ap = -2.0 * om;
+            double G[3][3], e[6], sg[6], Gx[3][3], ex[6], tx[6];
+            tet_grad<A.v, B.v, C.v>(g, U, G);
+            voigt(G, e);
+            stress3(g, e, sg);
+            const double cpl = ap * g.vol * Ec * 0.25;
+            const double sxa = (X[7][0] + X[7][q1]) + (X[7][q2] + X[7][7]);
+            if (mode != 2) {
+                // u rows: a|T|E B^T D B x_u + cpl * sxa * B^T sigma
+                double comb[6];
+                if (mode == 0) {
+                    tet_grad<A.v, B.v, C.v>(g, XU, Gx);
+                    voigt(Gx, ex);
+                    stress3(g, ex, tx);
+                    for (int t = 0; t < 6; ++t) comb[t] = a * g.vol * Ec * tx[t] + cpl * sxa * sg[t];
+                } else {
+                    for (int t = 0; t < 6; ++t) comb[t] = cpl * sxa * sg[t];
+                }
+                tet_scatter<A.v, B.v, C.v>(g, 1.0, comb, YU);
+            }
+            if (mode != 1) {
+                tet_grad<A.v, B.v, C.v>(g, XU, Gx);
+                voigt(Gx, ex);
+                const double fa = cpl * (ex[0] * sg[0] + ex[1] * sg[1] + ex[2] * sg[2] + ex[3] * sg[3] +
+                                         ex[4] * sg[4] + ex[5] * sg[5]);
+                Y[3][0] += fa; Y[3][q1] += fa; Y[3][q2] += fa; Y[3][7] += fa;
+                if (mode == 0) {
+                    const double q = Ec * (e[0] * sg[0] + e[1] * sg[1] + e[2] * sg[2] + e[3] * sg[3] +
+                                           e[4] * sg[4] + e[5] * sg[5]);
+                    const double kap = (q + (g.at2 ? 2.0 * kc / g.ell : 0.0)) * g.vol * (1.0 / 16.0);
+                    elem3_kaa<A.v, B.v, C.v>(g, kap, kc, X[7], Y[3]);
+                }
+            }
+        });
+    }
+    __device__ void out(const Geo3& g, int i, int j, int k, const double (&t)[NC], const double (&)[NV]) {
+        const long long id = vid3(g, i, j, k);
+        const unsigned m = bcmode ? bc3(g, i, j, k, id) : 0u;
+        if (mode != 2) {
+            for (int c = 0; c < 3; ++c) {
+                double yv = t[c];
+                if ((m >> c) & 1u) yv = (mode == 0) ? __ldg(xu + 3 * id + c) : 0.0;
+                yu[3 * id + c] = yv;
+            }
+        }
+        if (mode != 1) ya[id] = (act && act[id]) ? __ldg(xa + id) : t[3];
+    }
+};
+
+// ---- launch plumbing -----------------------------------------------------------------------------
+template <class Op>
+static int run3(Ctx* c, Op op, cudaStream_t st, int kind, double bytes) {
+    const Geo3& g = c->g3;
+    constexpr int smem = kW3 * Op::PD * (Op::SV + Op::SC) * 256 + kW3 * Op::NV * 32 * 8 +
+                         kW3 * 2 * Op::NC * 32 * 8;
+    static_assert(smem <= 227 * 1024, "3D stage ring exceeds shared memory");
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k_strip3d<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return check_cuda(c, e, "3D kernel attribute");
+        attr = true;
+    }
+    const long long nb = (long long)g.nbj * g.nbk * g.nstrips;
+    if (nb > kMaxBlocksRed) return set_error(c, PF_EINVAL, "3D grid too large for the reduction buffer");
+    const int ps = prof_begin(c, st);
+    k_strip3d<Op><<<(int)nb, kBlock3, smem, st>>>(g, op);
+    prof_end(c, st, ps, kind, bytes);
+    c->launches++;
+    return check_cuda(c, cudaGetLastError(), "3D strip kernel launch");
+}
+static RedBuf rb3(Ctx* c) { return RedBuf{c->partials, c->tickets, c->scal}; }
+
+int launch3_Kuu(Ctx* c, const double* alpha, const double* x, double* y, int bcmode, cudaStream_t st) {
+    Op3Kuu<false> op{alpha, x, nullptr, nullptr, y, bcmode, c->scal, rb3(c), 0.0};
+    return run3(c, op, st, K_KUU, 56.0 * c->g3.nv);
+}
+int launch3_Kuu_cgA(Ctx* c, const double* alpha, const double* z, const double* p_in, double* p_out, double* q,
+                    cudaStream_t st) {
+    Op3Kuu<true> op{alpha, z, p_in, p_out, q, PF_BC_ELIMINATE, c->scal, rb3(c), 0.0};
+    return run3(c, op, st, K_KUU_CG, 104.0 * c->g3.nv);
+}
+int launch3_Kuu_diag(Ctx* c, const double* alpha, double* dinv, cudaStream_t st) {
+    Op3KuuDiag op;
+    op.alpha = alpha;
+    op.dinv = dinv;
+    return run3(c, op, st, K_KUU_DIAG, 32.0 * c->g3.nv);
+}
+int launch3_kappa(Ctx* c, const double* u, double* kappa, double* cvec, cudaStream_t st) {
+    Op3Kappa op;
+    op.u = u; op.kappa = kappa; op.cvec = cvec;
+    return run3(c, op, st, K_KAPPA, 32.0 * c->g3.nv + 8.0 * c->n_el);
+}
+int launch3_Kaa(Ctx* c, const double* kappa, const double* x, double* y, const unsigned char* act, cudaStream_t st) {
+    const double bytes = 16.0 * c->g3.nv + 8.0 * c->n_el;
+    if (act) {
+        Op3Kaa<false, true> op{kappa, x, nullptr, nullptr, y, act, c->scal, rb3(c), 0.0};
+        return run3(c, op, st, K_KAA, bytes);
+    }
+    Op3Kaa<false, false> op{kappa, x, nullptr, nullptr, y, nullptr, c->scal, rb3(c), 0.0};
+    return run3(c, op, st, K_KAA, bytes);
+}
+int launch3_Kaa_cgA(Ctx* c, const double* kappa, const double* z, const double* p_in, double* p_out, double* q,
+                    const unsigned char* act, cudaStream_t st) {
+    const double bytes = 33.0 * c->g3.nv + 8.0 * c->n_el;
+    if (act) {
+        Op3Kaa<true, true> op{kappa, z, p_in, p_out, q, act, c->scal, rb3(c), 0.0};
+        return run3(c, op, st, K_KAA_CG, bytes);
+    }
+    Op3Kaa<true, false> op{kappa, z, p_in, p_out, q, nullptr, c->scal, rb3(c), 0.0};
+    return run3(c, op, st, K_KAA_CG, bytes);
+}
+int launch3_Kaa_diag(Ctx* c, const double* kappa, double* dinv, const unsigned char* act, cudaStream_t st) {
+    if (act) {
+        Op3KaaDiag<true> op;
+        op.kappa = kappa; op.dinv = dinv; op.act = act;
+        return run3(c, op, st, K_KAA_DIAG, 8.0 * c->g3.nv + 8.0 * c->n_el);
+    }
+    Op3KaaDiag<false> op;
+    op.kappa = kappa; op.dinv = dinv; op.act = nullptr;
+    return run3(c, op, st, K_KAA_DIAG, 8.0 * c->g3.nv + 8.0 * c->n_el);
+}
+int launch3_Kaa_trial(Ctx* c, const double* kappa, const double* cvec, const double* x, const double* d,
+                      const double* lb, double* trial, double* F, int merit_slot, cudaStream_t st) {
+    Op3KaaTrial op{kappa, cvec, x, d, lb, trial, F, c->scal, merit_slot, rb3(c), 0.0};
+    return run3(c, op, st, K_KAA_TRIAL, 48.0 * c->g3.nv + 8.0 * c->n_el);
+}
+int launch3_physics(Ctx* c, const double* u, const double* alpha, const double* lb, double* ru, double* ra,
+                    double* phi, int rows, cudaStream_t st) {
+    const double bytes = c->g3.nv * (32.0 + 8.0 + (ru ? 24.0 : 0.0) + (ra ? 8.0 : 0.0) + (phi ? 8.0 : 0.0));
+    if (rows == PF_ROWS_ZERO) {
+        Op3Phys<PF_ROWS_ZERO> op{u, alpha, lb, ru, ra, phi, c->scal, rb3(c), 0, 0, 0, 0};
+        return run3(c, op, st, K_PHYS, bytes);
+    }
+    if (rows == PF_ROWS_VALUE) {
+        Op3Phys<PF_ROWS_VALUE> op{u, alpha, lb, ru, ra, phi, c->scal, rb3(c), 0, 0, 0, 0};
+        return run3(c, op, st, K_PHYS, bytes);
+    }
+    Op3Phys<PF_ROWS_RAW> op{u, alpha, lb, ru, ra, phi, c->scal, rb3(c), 0, 0, 0, 0};
+    return run3(c, op, st, K_PHYS, bytes);
+}
+int launch3_load(Ctx* c, const double* alpha, double* f, int rows, cudaStream_t st) {
+    if (rows == 0) {
+        Op3Rhs<true> op{alpha, f, c->scal, rb3(c), 0.0};
+        return run3(c, op, st, K_RHS, 32.0 * c->g3.nv);
+    }
+    Op3Rhs<false> op{alpha, f, c->scal, rb3(c), 0.0};
+    return run3(c, op, st, K_RHS, 32.0 * c->g3.nv);
+}
+int launch3_jac(Ctx* c, const double* u, const double* alpha, const double* xu, const double* xa, double* yu,
+                double* ya, const unsigned char* act, int mode, int bcmode, cudaStream_t st) {
+    Op3Jac op;
+    op.u = u; op.alpha = alpha; op.xu = xu; op.xa = xa; op.yu = yu; op.ya = ya; op.act = act;
+    op.mode = mode; op.bcmode = bcmode;
+    return run3(c, op, st, mode == 0 ? K_JAC : (mode == 1 ? K_KUA : K_KAU), 96.0 * c->g3.nv);
+}
+
+}  // namespace pf

@@ -43,12 +43,13 @@ class State:
     @classmethod
     def zeros(cls, mesh, alpha_lb=None, device="cuda") -> "State":
         n = mesh.n_vertices
+        d = getattr(mesh, "dim", 2)
         if alpha_lb is None:
             lb = torch.zeros(n, dtype=torch.float64, device=device)
         else:
             lb = torch.as_tensor(np.asarray(alpha_lb, dtype=float), dtype=torch.float64,
                                  device=device).clone()
-        return cls(u=torch.zeros(2 * n, dtype=torch.float64, device=device), alpha=lb.clone(),
+        return cls(u=torch.zeros(d * n, dtype=torch.float64, device=device), alpha=lb.clone(),
                    alpha_lb=lb, load=0.0)
 
     @classmethod
@@ -112,13 +113,15 @@ class Discretization:
         self.material = material
         self.damage = damage or DamageModel()
         self.device = torch.device(device)
-        if material.regime == "3d":
-            raise ValueError("3D materials need a 3D mesh (not built in this version)")
-        d = _lib.PfDesc(dim=2, pattern=_lib.PATTERNS[mesh.pattern],
+        dim = getattr(mesh, "dim", 2)
+        if (material.regime == "3d") != (dim == 3):
+            raise ValueError("3D meshes need Material(regime='3d') and vice versa")
+        d = _lib.PfDesc(dim=dim, pattern=_lib.PATTERNS[mesh.pattern],
                         regime=_lib.REGIMES[material.regime], model=_lib.MODELS[self.damage.kind],
-                        nx=mesh.nx, ny=mesh.ny, nz=0, lx=mesh.lx, ly=mesh.ly, lz=0.0,
-                        E=material.E, nu=material.nu, Gc=material.Gc, ell=material.ell,
-                        k_ell=material.k_ell)
+                        nx=mesh.nx, ny=mesh.ny, nz=getattr(mesh, "nz", 0), lx=mesh.lx, ly=mesh.ly,
+                        lz=getattr(mesh, "lz", 0.0), E=material.E, nu=material.nu, Gc=material.Gc,
+                        ell=material.ell, k_ell=material.k_ell)
+        self.dim = dim
         ctx = C.c_void_p()
         _lib.raise_for(self.lib.pf_ctx_create(C.byref(d), C.byref(ctx)), None)
         self._ctx = ctx

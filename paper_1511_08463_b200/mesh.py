@@ -116,6 +116,66 @@ class StructuredMesh:
         return np.stack([v / 3.0 for v in t])
 
 
+@dataclass
+class StructuredMesh3D:
+    """Structured hex grid of [0,lx]x[0,ly]x[0,lz], each hex split into 6 Kuhn tetrahedra.
+
+    Vertex (i, j, k) = (i*(ny+1) + j)*(nz+1) + k; u interleaved (3 comps per vertex);
+    tetrahedra type-major (the 6 axis permutations in itertools order) over I-major cells.
+    """
+
+    nx: int
+    ny: int
+    nz: int
+    lx: float = 1.0
+    ly: float = 1.0
+    lz: float = 1.0
+    pattern: str = "kuhn6"
+    _vertices: np.ndarray | None = field(default=None, repr=False)
+
+    dim = 3
+
+    def __post_init__(self):
+        if min(self.nx, self.ny, self.nz) < 1:
+            raise ValueError("StructuredMesh3D needs nx, ny, nz >= 1")
+        if self.pattern != "kuhn6":
+            raise ValueError("3D pattern must be 'kuhn6'")
+
+    @property
+    def n_vertices(self) -> int:
+        return (self.nx + 1) * (self.ny + 1) * (self.nz + 1)
+
+    @property
+    def n_cells(self) -> int:
+        return self.nx * self.ny * self.nz
+
+    @property
+    def n_tets(self) -> int:
+        return 6 * self.n_cells
+
+    @property
+    def vertices(self) -> np.ndarray:
+        if self._vertices is None:
+            xs = np.linspace(0.0, self.lx, self.nx + 1)
+            ys = np.linspace(0.0, self.ly, self.ny + 1)
+            zs = np.linspace(0.0, self.lz, self.nz + 1)
+            X, Y, Z = np.meshgrid(xs, ys, zs, indexing="ij")
+            self._vertices = np.column_stack([X.ravel(), Y.ravel(), Z.ravel()])
+        return self._vertices
+
+    def vid(self, i, j, k):
+        return (np.asarray(i) * (self.ny + 1) + np.asarray(j)) * (self.nz + 1) + np.asarray(k)
+
+    def face_vertices(self, tag: str) -> np.ndarray:
+        """Sorted vertex ids of a face: x0, x1, y0, y1, z0, z1."""
+        r = {"x": np.arange(self.nx + 1), "y": np.arange(self.ny + 1), "z": np.arange(self.nz + 1)}
+        ax, side = tag[0], tag[1]
+        n = {"x": self.nx, "y": self.ny, "z": self.nz}[ax]
+        r[ax] = np.array([0 if side == "0" else n])
+        I, J, K = np.meshgrid(r["x"], r["y"], r["z"], indexing="ij")
+        return np.sort(self.vid(I, J, K).ravel())
+
+
 def rect_mesh(L: float, H: float, h: float, origin_x2: float = 0.0,
               pattern: str = "union_jack") -> StructuredMesh:
     """Uniform mesh of [0, L] x [origin_x2, origin_x2 + H] with target size h (mesh.py:112-142;
