@@ -72,7 +72,11 @@ typedef struct pf_lin_opts {
     int32_t check_every;  /* host convergence poll interval (iterations) */
     int32_t gmg_levels;   /* 0 = automatic */
     int32_t cheb_degree;  /* GMG smoother degree */
-    int32_t reserved;
+    int32_t gmg_reuse;    /* 1: keep the GMG hierarchy of an earlier solve (same context) while
+                           * it stays effective -- rebuilt after a Dirichlet-mask / cell-field
+                           * change, when the iteration count grows past 1.5x that of the first
+                           * solve on it, or (with a retry) when PCG breaks down on it.
+                           * 0: rebuild for every solve (the hierarchy of the current alpha). */
 } pf_lin_opts;
 
 typedef struct pf_lin_report {

@@ -35,7 +35,7 @@ class PfDesc(C.Structure):
 class LinOpts(C.Structure):
     _fields_ = [("precond", C.c_int32), ("warm_start", C.c_int32), ("maxit", C.c_int64),
                 ("rtol", C.c_double), ("atol", C.c_double), ("check_every", C.c_int32),
-                ("gmg_levels", C.c_int32), ("cheb_degree", C.c_int32), ("reserved", C.c_int32)]
+                ("gmg_levels", C.c_int32), ("cheb_degree", C.c_int32), ("gmg_reuse", C.c_int32)]
 
 
 class LinReport(C.Structure):

@@ -1,3 +1,4 @@
+#include <cstdlib>
 // pf_core.cu -- context, workspace, vector kernels and the device solvers behind the C ABI.
 //
 // Solvers keep all scalars on the device (scal[]); the host loop only polls a done/fail flag
@@ -359,6 +360,11 @@ void merit_parts(Ctx* c, long long n, const double* x, const double* F, const do
     c->launches++;
 }
 
+// last node of the device-side Krylov loop body: continue while the solver is live
+__global__ void k_loop_cond(cudaGraphConditionalHandle h, const double* s) {
+    if (threadIdx.x == 0) cudaGraphSetConditional(h, (s[S_DONE] == 0.0 && s[S_FAIL] == 0.0) ? 1u : 0u);
+}
+
 int pcg_run(Ctx* c, int kind, const PcgBuffers& B, const double* coef, const unsigned char* act,
                    double rtol, double atol, long long maxit, int zero_x0, int check_every,
                    pf_lin_report* rep, cudaStream_t st) {
@@ -410,8 +416,11 @@ int pcg_run(Ctx* c, int kind, const PcgBuffers& B, const double* coef, const uns
         c->launches++;
         return PF_OK;
     };
-    // CUDA graph of an iteration pair (kernels read all scalars from device memory, so the pair
-    // is replayed unchanged); disabled while per-kernel profiling is on.
+    // The Krylov loop runs on the device: a CUDA graph whose WHILE conditional node replays the
+    // captured iteration pair until k_loop_cond (last node of the body) sees the solver done or
+    // failed -- no host polling, at most one no-op iteration after convergence.  Kernels read
+    // every scalar from device memory, so the body is replayed unchanged.  Disabled while
+    // per-kernel profiling is on (eager launches bracketed by events, host-polled batches).
     const bool graphs = c->use_graphs && !c->prof.on;
     const long long key = c->geo_version * 16 + (gmg ? c->gmg_degree : 0);
     if (graphs && c->graph_key[kind] != key) {
@@ -419,35 +428,62 @@ int pcg_run(Ctx* c, int kind, const PcgBuffers& B, const double* coef, const uns
         if (!c->cap_stream) PF_CU(c, cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking), "stream");
         PF_CU(c, cudaStreamSynchronize(st), "sync");
         const long long l0 = c->launches;
-        PF_CU(c, cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal), "begin capture");
+        cudaGraph_t graph = nullptr;
+        PF_CU(c, cudaGraphCreate(&graph, 0), "graph create");
+        cudaGraphConditionalHandle h;
+        cudaGraphNodeParams np = {};
+        cudaGraphNode_t node;
+        cudaError_t ce = cudaGraphConditionalHandleCreate(&h, graph, 1, cudaGraphCondAssignDefault);
+        if (ce == cudaSuccess) {
+            np.type = cudaGraphNodeTypeConditional;
+            np.conditional.handle = h;
+            np.conditional.type = cudaGraphCondTypeWhile;
+            np.conditional.size = 1;
+            ce = cudaGraphAddNode(&node, graph, nullptr, 0, &np);
+        }
+        if (ce != cudaSuccess) {
+            cudaGraphDestroy(graph);
+            return check_cuda(c, ce, "conditional graph node");
+        }
+        cudaGraph_t body = np.conditional.phGraph_out[0];
+        PF_CU(c, cudaStreamBeginCaptureToGraph(c->cap_stream, body, nullptr, nullptr, 0,
+                                               cudaStreamCaptureModeThreadLocal), "begin capture");
         int rc1 = issue_iter(0, c->cap_stream);
         int rc2 = rc1 == PF_OK ? issue_iter(1, c->cap_stream) : rc1;
-        cudaGraph_t graph = nullptr;
-        cudaError_t ce = cudaStreamEndCapture(c->cap_stream, &graph);
-        if (rc2 != PF_OK) return rc2;
-        PF_CU(c, ce, "end capture");
-        PF_CU(c, cudaGraphInstantiate(&c->graph_exec[kind], graph, 0), "graph instantiate");
+        if (rc2 == PF_OK) {
+            k_loop_cond<<<1, 32, 0, c->cap_stream>>>(h, c->scal);
+            c->launches++;
+        }
+        cudaGraph_t captured = nullptr;
+        ce = cudaStreamEndCapture(c->cap_stream, &captured);
+        if (rc2 != PF_OK) { cudaGraphDestroy(graph); return rc2; }
+        if (ce != cudaSuccess) { cudaGraphDestroy(graph); return check_cuda(c, ce, "end capture"); }
+        ce = cudaGraphInstantiate(&c->graph_exec[kind], graph, 0);
         cudaGraphDestroy(graph);
-        c->graph_nodes[kind] = c->launches - l0;
+        PF_CU(c, ce, "graph instantiate");
+        c->graph_nodes[kind] = c->launches - l0;  // launches per replayed pair
         c->launches = l0;
         c->graph_key[kind] = key;
     }
     long long k = 0;
     int batch = std::max(2, check_every + (check_every & 1));
-    while (c->h_scal[S_DONE] == 0.0 && c->h_scal[S_FAIL] == 0.0) {
-        if (graphs) {
-            for (int t = 0; t < batch; t += 2, k += 2) {
-                PF_CU(c, cudaGraphLaunch(c->graph_exec[kind], st), "graph launch");
-                c->launches += c->graph_nodes[kind];
-            }
-        } else {
-            for (int t = 0; t < batch; ++t, ++k) PF_TRY(issue_iter(k, st));
+    if (graphs) {
+        if (c->h_scal[S_DONE] == 0.0 && c->h_scal[S_FAIL] == 0.0) {
+            const double it0 = c->h_scal[S_ITER];
+            PF_CU(c, cudaGraphLaunch(c->graph_exec[kind], st), "graph launch");
+            PF_TRY(read_scal(c, st, 0, 24));
+            const long long pairs = ((long long)(c->h_scal[S_ITER] - it0) + 2) / 2;
+            c->launches += pairs * c->graph_nodes[kind];
         }
-        PF_CU(c, cudaGetLastError(), "cg iteration");
-        PF_TRY(read_scal(c, st, 0, 24));
-        // cheap iterations (Jacobi): grow the poll interval; GMG iterations are ~100x dearer
-        // than a poll, so poll every pair to avoid launching no-op iterations after convergence
-        if (!gmg) batch = std::min(batch * 2, 64);
+    } else {
+        while (c->h_scal[S_DONE] == 0.0 && c->h_scal[S_FAIL] == 0.0) {
+            for (int t = 0; t < batch; ++t, ++k) PF_TRY(issue_iter(k, st));
+            PF_CU(c, cudaGetLastError(), "cg iteration");
+            PF_TRY(read_scal(c, st, 0, 24));
+            // cheap iterations (Jacobi): grow the poll interval; GMG iterations are ~100x dearer
+            // than a poll, so poll every pair to avoid launching no-op iterations after convergence
+            if (!gmg) batch = std::min(batch * 2, 64);
+        }
     }
     rep->iterations = (long long)c->h_scal[S_ITER];
     rep->final_residual_norm = c->h_scal[S_RNORM];
@@ -483,9 +519,16 @@ int elastic_solve(Ctx* c, const double* alpha, const double* u0, double* u_out, 
     PF_CU(c, cudaMemcpyAsync(c->alpha_ws, alpha, sizeof(double) * c->n_a, cudaMemcpyDeviceToDevice, st),
           "alpha copy");
     PcgBuffers B{c->cg_x, c->cg_r, c->cg_z, c->cg_p0, c->cg_p1, c->cg_q, c->cg_dinv, c->cg_b, c->n_u};
+    bool reused = false;
     if (gmg) {
-        c->gmg_degree = o->cheb_degree > 0 ? o->cheb_degree : 2;
-        PF_TRY(gmg_setup(c, st));
+        const int deg = o->cheb_degree > 0 ? o->cheb_degree : 2;
+        reused = o->gmg_reuse && c->gmg_built && deg == c->gmg_degree;
+        c->gmg_degree = deg;
+        if (!reused) {
+            PF_TRY(gmg_setup(c, st));
+            c->gmg_built = 1;
+            c->gmg_its0 = -1;
+        }
     } else {
         PF_TRY(launch_Kuu_diag(c, c->alpha_ws, B.dinv, st));
     }
@@ -496,7 +539,23 @@ int elastic_solve(Ctx* c, const double* alpha, const double* u0, double* u_out, 
     const long long maxit = o->maxit > 0 ? o->maxit : 10 * c->n_u;
     int rc = pcg_run(c, gmg ? 2 : 0, B, c->alpha_ws, nullptr, o->rtol, o->atol, maxit, warm ? 0 : 1,
                      o->check_every > 0 ? o->check_every : (gmg ? 2 : 8), rep, st);
-    if (rc != PF_OK) return rc;
+    if (reused && (rc == PF_EBREAKDOWN || (rc == PF_OK && !rep->converged))) {
+        // the kept hierarchy no longer preconditions this alpha: rebuild and solve again
+        PF_TRY(gmg_setup(c, st));
+        c->gmg_its0 = -1;
+        if (warm)
+            PF_CU(c, cudaMemcpyAsync(B.x, u0, sizeof(double) * c->n_u, cudaMemcpyDeviceToDevice, st), "u0 copy");
+        rc = pcg_run(c, 2, B, c->alpha_ws, nullptr, o->rtol, o->atol, maxit, warm ? 0 : 1,
+                     o->check_every > 0 ? o->check_every : 2, rep, st);
+    }
+    if (rc != PF_OK) {
+        c->gmg_built = 0;
+        return rc;
+    }
+    if (gmg) {
+        if (c->gmg_its0 < 0) c->gmg_its0 = rep->iterations;
+        else if (rep->iterations > (3 * c->gmg_its0) / 2 + 2) c->gmg_built = 0;  // refresh next time
+    }
     PF_CU(c, cudaMemcpyAsync(u_out, B.x, sizeof(double) * c->n_u, cudaMemcpyDeviceToDevice, st), "u copy");
     if (!rep->converged) {
         char msg[128];
@@ -681,7 +740,7 @@ static void geometry_2d(Ctx* c) {
     const long long rows = g.nx + 1;
     const long long target_warps = 148LL * 24;
     long long S = (rows * g.nwj + target_warps - 1) / target_warps;
-    S = std::max(8LL, std::min(64LL, S));
+    S = std::max(4LL, std::min(64LL, S));
     g.S = (int)S;
     g.nstrips = (int)((rows + S - 1) / S);
 }
@@ -883,6 +942,7 @@ int pf_set_cell_fields(pf_ctx* c, const double* E_cell, const double* Gc_cell) {
     c->g3.E_cell = E_cell;
     c->g3.Gc_cell = Gc_cell;
     c->geo_version++;
+    c->gmg_built = 0;
     return PF_OK;
 }
 
@@ -909,6 +969,8 @@ int pf_set_dirichlet(pf_ctx* c, const int64_t* dofs, const double* vals, int64_t
         PF_CU(c, cudaMemcpyAsync(c->bcmask, mask.data(), g.nv, cudaMemcpyHostToDevice, st), "bc mask");
         PF_CU(c, cudaMemcpyAsync(c->ubar, ub.data(), sizeof(double) * 3 * g.nv, cudaMemcpyHostToDevice, st), "ubar");
         PF_CU(c, cudaStreamSynchronize(st), "sync");
+        if (mask != c->h_bcmask) c->gmg_built = 0;
+        c->h_bcmask.swap(mask);
         if (c->g3.has_bc != (n > 0)) c->geo_version++;
         c->g3.has_bc = n > 0;
         return PF_OK;
@@ -931,6 +993,8 @@ int pf_set_dirichlet(pf_ctx* c, const int64_t* dofs, const double* vals, int64_t
     PF_CU(c, cudaMemcpyAsync(c->ubar, ub.data(), sizeof(double) * 2 * g.nc, cudaMemcpyHostToDevice, st),
           "ubar");
     PF_CU(c, cudaStreamSynchronize(st), "sync");
+    if (mask != c->h_bcmask) c->gmg_built = 0;
+    c->h_bcmask.swap(mask);
     if (c->g.has_bc != (n > 0)) c->geo_version++;
     c->g.has_bc = n > 0;
     return PF_OK;

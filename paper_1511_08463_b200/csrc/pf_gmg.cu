@@ -16,6 +16,7 @@
 // a = k_ell) are seen by the coarse operators because they are Galerkin products.
 // Stencil layout: A[(k*4 + e)*nv + v], k = (di+1)*3 + (dj+1) neighbour, e = 2r + c block entry.
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 
@@ -433,32 +434,44 @@ __device__ __forceinline__ double cheb_rho(const Cheb& c, int k) {  // rho_k, rh
     return rho;
 }
 __device__ __forceinline__ double2 bmul(const double* Dinv, long long nv, long long v, double r0, double r1) {
-    return make_double2(Dinv[v] * r0 + Dinv[nv + v] * r1, Dinv[2 * nv + v] * r0 + Dinv[3 * nv + v] * r1);
+    return make_double2(__ldg(Dinv + v) * r0 + __ldg(Dinv + nv + v) * r1,
+                        __ldg(Dinv + 2 * nv + v) * r0 + __ldg(Dinv + 3 * nv + v) * r1);
+}
+// V-cycle vectors are streamed through L2 (ld.global.cg); operators/Dinv via the read-only path.
+__device__ __forceinline__ double2 ldv(const double* p, long long v) {
+    return __ldcg(reinterpret_cast<const double2*>(p) + v);
+}
+__device__ __forceinline__ void stv(double* p, long long v, double2 x) {
+    reinterpret_cast<double2*>(p)[v] = x;
 }
 
 // res = D^-1 src ; d = res / theta ; x (=|+=) d
+__device__ __forceinline__ void v_cheb0(long long nv, const double* Dinv, const double* src, double* res, double* d,
+                                        double* x, int accumulate, const Cheb& c, long long v) {
+    const double2 s = ldv(src, v);
+    const double2 r = bmul(Dinv, nv, v, s.x, s.y);
+    const double2 dd = make_double2(r.x / c.theta, r.y / c.theta);
+    stv(res, v, r);
+    stv(d, v, dd);
+    double2 xo = dd;
+    if (accumulate) {
+        const double2 xv = ldv(x, v);
+        xo = make_double2(xv.x + dd.x, xv.y + dd.y);
+    }
+    stv(x, v, xo);
+}
 __global__ void k_cheb0(long long nv, const double* Dinv, const double* src, double* res, double* d, double* x,
                         int accumulate, const double* lam, double ratio, const double* live) {
     if (!gmg_live(live)) return;
     const Cheb c = cheb_of(lam, ratio);
     for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < nv;
-         v += (long long)gridDim.x * blockDim.x) {
-        const double2 s = reinterpret_cast<const double2*>(src)[v];
-        const double2 r = bmul(Dinv, nv, v, s.x, s.y);
-        const double2 dd = make_double2(r.x / c.theta, r.y / c.theta);
-        reinterpret_cast<double2*>(res)[v] = r;
-        reinterpret_cast<double2*>(d)[v] = dd;
-        double2 xo = dd;
-        if (accumulate) {
-            const double2 xv = reinterpret_cast<const double2*>(x)[v];
-            xo = make_double2(xv.x + dd.x, xv.y + dd.y);
-        }
-        reinterpret_cast<double2*>(x)[v] = xo;
-    }
+         v += (long long)gridDim.x * blockDim.x)
+        v_cheb0(nv, Dinv, src, res, d, x, accumulate, c, v);
 }
 
-// stencil apply helper: (A d)_v
-__device__ __forceinline__ double2 st_apply(const LevelDev& L, const double* d, long long v) {
+// 9-point 2x2-block stencil apply (A y)_v with y_w = val(w)
+template <class F>
+__device__ __forceinline__ double2 st_apply_f(const LevelDev& L, long long v, F val) {
     const int nvy = L.ny + 1;
     const int i = (int)(v / nvy), j = (int)(v % nvy);
     double y0 = 0.0, y1 = 0.0;
@@ -467,112 +480,205 @@ __device__ __forceinline__ double2 st_apply(const LevelDev& L, const double* d, 
         const int ni = i + k / 3 - 1, nj = j + k % 3 - 1;
         if (ni < 0 || nj < 0 || ni > L.nx || nj > L.ny) continue;
         const long long w = (long long)ni * nvy + nj;
-        const double2 dv = reinterpret_cast<const double2*>(d)[w];
-        y0 += L.A[(size_t)(k * 4 + 0) * L.nv + v] * dv.x + L.A[(size_t)(k * 4 + 1) * L.nv + v] * dv.y;
-        y1 += L.A[(size_t)(k * 4 + 2) * L.nv + v] * dv.x + L.A[(size_t)(k * 4 + 3) * L.nv + v] * dv.y;
+        const double2 dv = val(w);
+        y0 += __ldg(L.A + (size_t)(k * 4 + 0) * L.nv + v) * dv.x + __ldg(L.A + (size_t)(k * 4 + 1) * L.nv + v) * dv.y;
+        y1 += __ldg(L.A + (size_t)(k * 4 + 2) * L.nv + v) * dv.x + __ldg(L.A + (size_t)(k * 4 + 3) * L.nv + v) * dv.y;
     }
     return make_double2(y0, y1);
 }
+__device__ __forceinline__ double2 st_apply(const LevelDev& L, const double* d, long long v) {
+    return st_apply_f(L, v, [&](long long w) { return ldv(d, w); });
+}
 
 // One Chebyshev step k >= 1 (linalg.py:366-376): w = A d (stencil, or precomputed Ad when
-// Ad != null); res -= D^-1 w; d' = rho_k rho_{k-1} d + (2 rho_k / delta) res; x += d'.
+// Ad != null); res -= D^-1 w; d' = rho_k rho_{k-1} d + (2 rho_k / delta) res; x (+= d) += d'.
+// `addd` folds a deferred cheb0 update (x += d) of the post-smoother into this pass.
+__device__ __forceinline__ void v_cheb_step(const LevelDev& L, const double* Ad, const double* d, double* dnext,
+                                            double* res, double* x, double a, double b, int addd, long long v) {
+    const double2 w = Ad ? ldv(Ad, v) : st_apply(L, d, v);
+    const double2 dw = bmul(L.Dinv, L.nv, v, w.x, w.y);
+    double2 r = ldv(res, v);
+    r.x -= dw.x;
+    r.y -= dw.y;
+    const double2 dv = ldv(d, v);
+    const double2 dn = make_double2(a * dv.x + b * r.x, a * dv.y + b * r.y);
+    stv(res, v, r);
+    stv(dnext, v, dn);
+    double2 xv = ldv(x, v);
+    if (addd) {
+        xv.x += dv.x;
+        xv.y += dv.y;
+    }
+    xv.x += dn.x;
+    xv.y += dn.y;
+    stv(x, v, xv);
+}
+__device__ __forceinline__ void cheb_ab(const Cheb& c, int k, double& a, double& b) {
+    const double rp = cheb_rho(c, k - 1), rn = cheb_rho(c, k);
+    a = rn * rp;
+    b = 2.0 * rn / c.delta;
+}
 __global__ void k_cheb_step(LevelDev L, const double* Ad, const double* d, double* dnext, double* res, double* x,
-                            int k, const double* lam, double ratio, const double* live) {
+                            int k, int addd, const double* lam, double ratio, const double* live) {
     if (!gmg_live(live)) return;
     const Cheb c = cheb_of(lam, ratio);
-    const double rp = cheb_rho(c, k - 1), rn = cheb_rho(c, k);
-    const double a = rn * rp, b = 2.0 * rn / c.delta;
+    double a, b;
+    cheb_ab(c, k, a, b);
     for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < L.nv;
-         v += (long long)gridDim.x * blockDim.x) {
-        const double2 w = Ad ? reinterpret_cast<const double2*>(Ad)[v] : st_apply(L, d, v);
-        const double2 dw = bmul(L.Dinv, L.nv, v, w.x, w.y);
-        double2 r = reinterpret_cast<double2*>(res)[v];
-        r.x -= dw.x;
-        r.y -= dw.y;
-        const double2 dv = reinterpret_cast<const double2*>(d)[v];
-        const double2 dn = make_double2(a * dv.x + b * r.x, a * dv.y + b * r.y);
-        reinterpret_cast<double2*>(res)[v] = r;
-        reinterpret_cast<double2*>(dnext)[v] = dn;
-        double2 xv = reinterpret_cast<double2*>(x)[v];
-        xv.x += dn.x;
-        xv.y += dn.y;
-        reinterpret_cast<double2*>(x)[v] = xv;
+         v += (long long)gridDim.x * blockDim.x)
+        v_cheb_step(L, Ad, d, dnext, res, x, a, b, addd, v);
+}
+
+// Pre-smoother from x = 0, cheb0 fused into step 1: d0 = D^-1 b / theta is recomputed at the
+// stencil neighbours, so one pass gives res, d0, d1 and x = d0 + d1 (x = d0 when deg == 1).
+__device__ __forceinline__ void v_pre_first(const LevelDev& L, const double* bvec, double* res, double* d0,
+                                            double* d1, double* x, const Cheb& c, double a, double b, int deg,
+                                            long long v) {
+    const double2 s = ldv(bvec, v);
+    const double2 r0 = bmul(L.Dinv, L.nv, v, s.x, s.y);
+    const double2 dd = make_double2(r0.x / c.theta, r0.y / c.theta);
+    stv(d0, v, dd);
+    if (deg <= 1) {
+        stv(res, v, r0);
+        stv(x, v, dd);
+        return;
     }
+    const double2 w = st_apply_f(L, v, [&](long long q) {
+        const double2 sq = ldv(bvec, q);
+        const double2 rq = bmul(L.Dinv, L.nv, q, sq.x, sq.y);
+        return make_double2(rq.x / c.theta, rq.y / c.theta);
+    });
+    const double2 dw = bmul(L.Dinv, L.nv, v, w.x, w.y);
+    const double2 r = make_double2(r0.x - dw.x, r0.y - dw.y);
+    const double2 dn = make_double2(a * dd.x + b * r.x, a * dd.y + b * r.y);
+    stv(res, v, r);
+    stv(d1, v, dn);
+    stv(x, v, make_double2(dd.x + dn.x, dd.y + dn.y));
+}
+__global__ void k_pre_first(LevelDev L, const double* bvec, double* res, double* d0, double* d1, double* x, int deg,
+                            const double* lam, double ratio, const double* live) {
+    if (!gmg_live(live)) return;
+    const Cheb c = cheb_of(lam, ratio);
+    double a = 0.0, b = 0.0;
+    if (deg > 1) cheb_ab(c, 1, a, b);
+    for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < L.nv;
+         v += (long long)gridDim.x * blockDim.x)
+        v_pre_first(L, bvec, res, d0, d1, x, c, a, b, deg, v);
 }
 
 // r = b - A x (stencil) or r = b - Ax (precomputed)
+__device__ __forceinline__ void v_resid(const LevelDev& L, const double* Ax, const double* x, const double* b,
+                                        double* r, long long v) {
+    const double2 w = Ax ? ldv(Ax, v) : st_apply(L, x, v);
+    const double2 bv = ldv(b, v);
+    stv(r, v, make_double2(bv.x - w.x, bv.y - w.y));
+}
 __global__ void k_resid(LevelDev L, const double* Ax, const double* x, const double* b, double* r, const double* live) {
     if (!gmg_live(live)) return;
     for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < L.nv;
+         v += (long long)gridDim.x * blockDim.x)
+        v_resid(L, Ax, x, b, r, v);
+}
+
+// Post-smoother entry with cheb0 fused into the residual: res = D^-1 (b - A x), d0 = res/theta.
+// x is NOT updated here (neighbours still read it); the following step adds d0 (addd).
+__device__ __forceinline__ void v_post_first(const LevelDev& L, const double* x, const double* b, double* res,
+                                             double* d0, const Cheb& c, long long v) {
+    const double2 w = st_apply(L, x, v);
+    const double2 bv = ldv(b, v);
+    const double2 s = make_double2(bv.x - w.x, bv.y - w.y);
+    const double2 r = bmul(L.Dinv, L.nv, v, s.x, s.y);
+    stv(res, v, r);
+    stv(d0, v, make_double2(r.x / c.theta, r.y / c.theta));
+}
+__global__ void k_post_first(LevelDev L, const double* x, const double* b, double* res, double* d0,
+                             const double* lam, double ratio, const double* live) {
+    if (!gmg_live(live)) return;
+    const Cheb c = cheb_of(lam, ratio);
+    for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < L.nv;
+         v += (long long)gridDim.x * blockDim.x)
+        v_post_first(L, x, b, res, d0, c, v);
+}
+__global__ void k_add(long long nv, const double* d, double* x, const double* live) {
+    if (!gmg_live(live)) return;
+    for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < nv;
          v += (long long)gridDim.x * blockDim.x) {
-        const double2 w = Ax ? reinterpret_cast<const double2*>(Ax)[v] : st_apply(L, x, v);
-        const double2 bv = reinterpret_cast<const double2*>(b)[v];
-        reinterpret_cast<double2*>(r)[v] = make_double2(bv.x - w.x, bv.y - w.y);
+        const double2 dv = ldv(d, v);
+        double2 xv = ldv(x, v);
+        xv.x += dv.x;
+        xv.y += dv.y;
+        stv(x, v, xv);
     }
 }
 
 // 2:1 restriction b_c = P^T r_f (with masks), one thread per coarse vertex
+__device__ __forceinline__ void v_restrict(const LevelDev& F, const LevelDev& Cd, const unsigned char* maskc,
+                                           const double* r, double* bc, long long v) {
+    const int nvyf = F.ny + 1, nvyc = Cd.ny + 1;
+    const int I = (int)(v / nvyc), J = (int)(v % nvyc);
+    const unsigned mC = maskc[v];
+    double s0 = 0.0, s1 = 0.0;
+    for (int fi = 2 * I - 1; fi <= 2 * I + 1; ++fi) {
+        if (fi < 0 || fi > F.nx) continue;
+        int cx[2]; double wx[2];
+        const int nxw = p1d(fi, F.nx, cx, wx);
+        double wfx = 0.0;
+        for (int a = 0; a < nxw; ++a) if (cx[a] == I) wfx = wx[a];
+        if (wfx == 0.0) continue;
+        for (int fj = 2 * J - 1; fj <= 2 * J + 1; ++fj) {
+            if (fj < 0 || fj > F.ny) continue;
+            int cy[2]; double wy[2];
+            const int nyw = p1d(fj, F.ny, cy, wy);
+            double wfy = 0.0;
+            for (int b = 0; b < nyw; ++b) if (cy[b] == J) wfy = wy[b];
+            if (wfy == 0.0) continue;
+            const long long f = (long long)fi * nvyf + fj;
+            const unsigned mf = F.mask ? F.mask[f] : 0u;
+            const double2 rv = ldv(r, f);
+            const double w = wfx * wfy;
+            if (!(mf & 1u)) s0 += w * rv.x;
+            if (!(mf & 2u)) s1 += w * rv.y;
+        }
+    }
+    stv(bc, v, make_double2((mC & 1u) ? 0.0 : s0, (mC & 2u) ? 0.0 : s1));
+}
 __global__ void k_restrict(LevelDev F, LevelDev Cd, const unsigned char* maskc, const double* r, double* bc,
                            const double* live) {
     if (!gmg_live(live)) return;
-    const int nvyf = F.ny + 1, nvyc = Cd.ny + 1;
     for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < Cd.nv;
-         v += (long long)gridDim.x * blockDim.x) {
-        const int I = (int)(v / nvyc), J = (int)(v % nvyc);
-        const unsigned mC = maskc[v];
-        double s0 = 0.0, s1 = 0.0;
-        for (int fi = 2 * I - 1; fi <= 2 * I + 1; ++fi) {
-            if (fi < 0 || fi > F.nx) continue;
-            int cx[2]; double wx[2];
-            const int nxw = p1d(fi, F.nx, cx, wx);
-            double wfx = 0.0;
-            for (int a = 0; a < nxw; ++a) if (cx[a] == I) wfx = wx[a];
-            if (wfx == 0.0) continue;
-            for (int fj = 2 * J - 1; fj <= 2 * J + 1; ++fj) {
-                if (fj < 0 || fj > F.ny) continue;
-                int cy[2]; double wy[2];
-                const int nyw = p1d(fj, F.ny, cy, wy);
-                double wfy = 0.0;
-                for (int b = 0; b < nyw; ++b) if (cy[b] == J) wfy = wy[b];
-                if (wfy == 0.0) continue;
-                const long long f = (long long)fi * nvyf + fj;
-                const unsigned mf = F.mask ? F.mask[f] : 0u;
-                const double2 rv = reinterpret_cast<const double2*>(r)[f];
-                const double w = wfx * wfy;
-                if (!(mf & 1u)) s0 += w * rv.x;
-                if (!(mf & 2u)) s1 += w * rv.y;
-            }
-        }
-        reinterpret_cast<double2*>(bc)[v] = make_double2((mC & 1u) ? 0.0 : s0, (mC & 2u) ? 0.0 : s1);
-    }
+         v += (long long)gridDim.x * blockDim.x)
+        v_restrict(F, Cd, maskc, r, bc, v);
 }
 
 // 2:1 prolongation x_f += P x_c (with masks), one thread per fine vertex
+__device__ __forceinline__ void v_prolong(const LevelDev& F, const LevelDev& Cd, const unsigned char* maskc,
+                                          const double* xc, double* xf, long long v) {
+    const int nvyf = F.ny + 1, nvyc = Cd.ny + 1;
+    const int fi = (int)(v / nvyf), fj = (int)(v % nvyf);
+    const unsigned mf = F.mask ? F.mask[v] : 0u;
+    int cx[2], cy[2]; double wx[2], wy[2];
+    const int nxw = p1d(fi, F.nx, cx, wx), nyw = p1d(fj, F.ny, cy, wy);
+    double s0 = 0.0, s1 = 0.0;
+    for (int a = 0; a < nxw; ++a)
+        for (int b = 0; b < nyw; ++b) {
+            const long long c = (long long)cx[a] * nvyc + cy[b];
+            const unsigned mC = maskc[c];
+            const double2 xv = ldv(xc, c);
+            const double w = wx[a] * wy[b];
+            if (!(mC & 1u)) s0 += w * xv.x;
+            if (!(mC & 2u)) s1 += w * xv.y;
+        }
+    double2 o = ldv(xf, v);
+    if (!(mf & 1u)) o.x += s0;
+    if (!(mf & 2u)) o.y += s1;
+    stv(xf, v, o);
+}
 __global__ void k_prolong(LevelDev F, LevelDev Cd, const unsigned char* maskc, const double* xc, double* xf,
                           const double* live) {
     if (!gmg_live(live)) return;
-    const int nvyf = F.ny + 1, nvyc = Cd.ny + 1;
     for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < F.nv;
-         v += (long long)gridDim.x * blockDim.x) {
-        const int fi = (int)(v / nvyf), fj = (int)(v % nvyf);
-        const unsigned mf = F.mask ? F.mask[v] : 0u;
-        int cx[2], cy[2]; double wx[2], wy[2];
-        const int nxw = p1d(fi, F.nx, cx, wx), nyw = p1d(fj, F.ny, cy, wy);
-        double s0 = 0.0, s1 = 0.0;
-        for (int a = 0; a < nxw; ++a)
-            for (int b = 0; b < nyw; ++b) {
-                const long long c = (long long)cx[a] * nvyc + cy[b];
-                const unsigned mC = maskc[c];
-                const double2 xv = reinterpret_cast<const double2*>(xc)[c];
-                const double w = wx[a] * wy[b];
-                if (!(mC & 1u)) s0 += w * xv.x;
-                if (!(mC & 2u)) s1 += w * xv.y;
-            }
-        double2 o = reinterpret_cast<double2*>(xf)[v];
-        if (!(mf & 1u)) o.x += s0;
-        if (!(mf & 2u)) o.y += s1;
-        reinterpret_cast<double2*>(xf)[v] = o;
-    }
+         v += (long long)gridDim.x * blockDim.x)
+        v_prolong(F, Cd, maskc, xc, xf, v);
 }
 
 // crossed level 0 <-> corner grid, factored as P0 = (corner identity + centre mean) o P_{2:1}:
@@ -772,32 +878,33 @@ int gmg_vcycle(Ctx* c, const double* r_in, double* z_out, cudaStream_t st, const
     const int deg = std::max(1, c->gmg_degree);
     const double ratio = c->gmg_ratio;
     double* lam = c->scal + S_GMG0;
-    // descend
-    for (int l = 0; l < nl - 1; ++l) {
+    const int lc = nl - 1;  // per-level kernels down to the dense coarse solve
+    // descend through the per-level kernels
+    for (int l = 0; l < lc; ++l) {
         GLevel& L = c->glev[l];
         const long long nv = L.nv;
         const double* b = (l == 0) ? r_in : L.b;
         double* x = (l == 0) ? z_out : L.x;
         LevelDev Ld = ldev(c, l);
         Ld.nv = nv;
-        // pre-smooth from x = 0
-        GKB(c, K_GMG, 96.0 * nv, (k_cheb0<<<gblocks(nv), kGB, 0, st>>>(nv, L.Dinv, b, L.res, L.d0, x, 0, lam + l, ratio, live)));
         double* d = L.d0;
         double* dn = L.d1;
-        for (int k = 1; k < deg; ++k) {
-            if (l == 0) {
+        if (l == 0) {  // pre-smooth from x = 0 with the matrix-free fine operator
+            GKB(c, K_GMG, 96.0 * nv, (k_cheb0<<<gblocks(nv), kGB, 0, st>>>(nv, L.Dinv, b, L.res, L.d0, x, 0, lam + l, ratio, live)));
+            for (int k = 1; k < deg; ++k) {
                 PF_TRY_GMG(launch_Kuu(c, c->alpha_ws, d, L.w, PF_BC_ELIMINATE, st));
-                GKB(c, K_GMG, 144.0 * nv, (k_cheb_step<<<gblocks(nv), kGB, 0, st>>>(Ld, L.w, d, dn, L.res, x, k, lam + l, ratio, live)));
-            } else {
-                GKB(c, K_GMG, 416.0 * nv, (k_cheb_step<<<gblocks(nv), kGB, 0, st>>>(Ld, nullptr, d, dn, L.res, x, k, lam + l, ratio, live)));
+                GKB(c, K_GMG, 144.0 * nv, (k_cheb_step<<<gblocks(nv), kGB, 0, st>>>(Ld, L.w, d, dn, L.res, x, k, 0, lam + l, ratio, live)));
+                std::swap(d, dn);
             }
-            std::swap(d, dn);
-        }
-        // residual
-        if (l == 0) {
             PF_TRY_GMG(launch_Kuu(c, c->alpha_ws, x, L.w, PF_BC_ELIMINATE, st));
             GKB(c, K_GMG, 64.0 * nv, (k_resid<<<gblocks(nv), kGB, 0, st>>>(Ld, L.w, x, b, L.r, live)));
         } else {
+            GKB(c, K_GMG, (deg > 1 ? 416.0 : 96.0) * nv, (k_pre_first<<<gblocks(nv), kGB, 0, st>>>(Ld, b, L.res, L.d0, L.d1, x, deg, lam + l, ratio, live)));
+            if (deg > 1) std::swap(d, dn);
+            for (int k = 2; k < deg; ++k) {
+                GKB(c, K_GMG, 416.0 * nv, (k_cheb_step<<<gblocks(nv), kGB, 0, st>>>(Ld, nullptr, d, dn, L.res, x, k, 0, lam + l, ratio, live)));
+                std::swap(d, dn);
+            }
             GKB(c, K_GMG, 336.0 * nv, (k_resid<<<gblocks(nv), kGB, 0, st>>>(Ld, nullptr, x, b, L.r, live)));
         }
         // restrict
@@ -819,16 +926,13 @@ int gmg_vcycle(Ctx* c, const double* r_in, double* z_out, cudaStream_t st, const
             GKB(c, K_GMG, 16.0 * F.nv + 17.0 * Cd.nv, (k_restrict<<<gblocks(Cd.nv), kGB, 0, st>>>(F, Cd, C.mask, L.r, C.b, live)));
         }
     }
-    // coarsest
-    {
+    {   // coarsest: dense inverse
         GLevel& L = c->glev[nl - 1];
         const int n = (int)(2 * L.nv);
-        double* x = (nl == 1) ? z_out : L.x;
-        const double* b = (nl == 1) ? r_in : L.b;
-        GKB(c, K_GMG, 8.0 * n * n + 32.0 * n, (k_coarse_solve<<<std::max(1, (n + 7) / 8), 256, 0, st>>>(n, c->gmg_ainv, b, x, live)));
+        GKB(c, K_GMG, 8.0 * n * n + 32.0 * n, (k_coarse_solve<<<std::max(1, (n + 7) / 8), 256, 0, st>>>(n, c->gmg_ainv, L.b, L.x, live)));
     }
     // ascend
-    for (int l = nl - 2; l >= 0; --l) {
+    for (int l = lc - 1; l >= 0; --l) {
         GLevel& L = c->glev[l];
         GLevel& C = c->glev[l + 1];
         const long long nv = L.nv;
@@ -853,24 +957,24 @@ int gmg_vcycle(Ctx* c, const double* r_in, double* z_out, cudaStream_t st, const
             LevelDev F = ldev(c, l), Cd = ldev(c, l + 1);
             GKB(c, K_GMG, 32.0 * F.nv + 17.0 * Cd.nv, (k_prolong<<<gblocks(F.nv), kGB, 0, st>>>(F, Cd, C.mask, C.x, x, live)));
         }
-        // post-smooth: r = b - A x ; x += p(D^-1 A) D^-1 r
-        if (l == 0) {
-            PF_TRY_GMG(launch_Kuu(c, c->alpha_ws, x, L.w, PF_BC_ELIMINATE, st));
-            GKB(c, K_GMG, 64.0 * nv, (k_resid<<<gblocks(nv), kGB, 0, st>>>(Ld, L.w, x, b, L.r, live)));
-        } else {
-            GKB(c, K_GMG, 336.0 * nv, (k_resid<<<gblocks(nv), kGB, 0, st>>>(Ld, nullptr, x, b, L.r, live)));
-        }
-        GKB(c, K_GMG, 112.0 * nv, (k_cheb0<<<gblocks(nv), kGB, 0, st>>>(nv, L.Dinv, L.r, L.res, L.d0, x, 1, lam + l, ratio, live)));
         double* d = L.d0;
         double* dn = L.d1;
-        for (int k = 1; k < deg; ++k) {
-            if (l == 0) {
+        if (l == 0) {  // post-smooth: r = b - A x ; x += p(D^-1 A) D^-1 r
+            PF_TRY_GMG(launch_Kuu(c, c->alpha_ws, x, L.w, PF_BC_ELIMINATE, st));
+            GKB(c, K_GMG, 64.0 * nv, (k_resid<<<gblocks(nv), kGB, 0, st>>>(Ld, L.w, x, b, L.r, live)));
+            GKB(c, K_GMG, 112.0 * nv, (k_cheb0<<<gblocks(nv), kGB, 0, st>>>(nv, L.Dinv, L.r, L.res, L.d0, x, 1, lam + l, ratio, live)));
+            for (int k = 1; k < deg; ++k) {
                 PF_TRY_GMG(launch_Kuu(c, c->alpha_ws, d, L.w, PF_BC_ELIMINATE, st));
-                GKB(c, K_GMG, 144.0 * nv, (k_cheb_step<<<gblocks(nv), kGB, 0, st>>>(Ld, L.w, d, dn, L.res, x, k, lam + l, ratio, live)));
-            } else {
-                GKB(c, K_GMG, 416.0 * nv, (k_cheb_step<<<gblocks(nv), kGB, 0, st>>>(Ld, nullptr, d, dn, L.res, x, k, lam + l, ratio, live)));
+                GKB(c, K_GMG, 144.0 * nv, (k_cheb_step<<<gblocks(nv), kGB, 0, st>>>(Ld, L.w, d, dn, L.res, x, k, 0, lam + l, ratio, live)));
+                std::swap(d, dn);
             }
-            std::swap(d, dn);
+        } else {  // residual + cheb0 in one pass; the x += d0 rides on step 1
+            GKB(c, K_GMG, 400.0 * nv, (k_post_first<<<gblocks(nv), kGB, 0, st>>>(Ld, x, b, L.res, L.d0, lam + l, ratio, live)));
+            if (deg <= 1) GKB(c, K_GMG, 48.0 * nv, (k_add<<<gblocks(nv), kGB, 0, st>>>(nv, L.d0, x, live)));
+            for (int k = 1; k < deg; ++k) {
+                GKB(c, K_GMG, 416.0 * nv, (k_cheb_step<<<gblocks(nv), kGB, 0, st>>>(Ld, nullptr, d, dn, L.res, x, k, k == 1, lam + l, ratio, live)));
+                std::swap(d, dn);
+            }
         }
     }
     return check_cuda(c, cudaGetLastError(), "gmg vcycle");

@@ -200,6 +200,9 @@ struct Ctx {
     double* gmg_dense = nullptr;
     double* gmg_ainv = nullptr;
     int gmg_degree = 2;
+    int gmg_built = 0;              // hierarchy valid for reuse (pf_lin_opts.gmg_reuse)
+    long long gmg_its0 = -1;        // iterations of the first elastic solve on it (-1: none yet)
+    std::vector<unsigned char> h_bcmask;  // last Dirichlet mask (detects mask changes)
     double gmg_ratio = 0.1;
     // CUDA graphs of two Krylov iterations per solver kind (0 Kuu-Jacobi, 1 Kaa-masked, 2 Kuu-GMG)
     int use_graphs = 1;

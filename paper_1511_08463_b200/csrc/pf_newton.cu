@@ -293,7 +293,11 @@ int newton_solve(Ctx* c, const double* u_in, const double* a_in, const double* l
         // Jacobian-dependent setup: GMG hierarchy of Kuu(alpha), kappa(u) and masked diag(Kaa)
         NCU(c, cudaMemcpyAsync(c->alpha_ws, alpha, sizeof(double) * na, cudaMemcpyDeviceToDevice, st), "copy");
         if (c->dim == 3) NTRY(launch_Kuu_diag(c, c->alpha_ws, c->cg_dinv, st));  // Jacobi inner A (3D)
-        else NTRY(gmg_setup(c, st));
+        else {
+            NTRY(gmg_setup(c, st));
+            c->gmg_built = 1;  // an elastic solve that follows may keep it (gmg_reuse)
+            c->gmg_its0 = -1;
+        }
         NTRY(launch_kappa(c, u, alpha, c->kappa, c->vi_c, st));
         NTRY(launch_Kaa_diag(c, c->kappa, c->da_dinv, c->act, st));
         bool ok = false;

@@ -68,6 +68,7 @@ class SolverConfig:
     damage_rtol: float = 1e-10
     warm_start: bool = True
     check_every: int = 8
+    gmg_reuse: bool = True   # keep the GMG hierarchy across solves while it stays effective
 
     def __post_init__(self):
         if not 0.0 < self.omega < 2.0:
@@ -132,7 +133,8 @@ def _lin_opts(config: SolverConfig, warm: bool) -> _lib.LinOpts:
     rtol = config.direct_rtol if config.elastic_solver == "direct" else config.elastic_rtol
     prec = _lib.PREC.get(config.elastic_precond, 0)
     return _lib.LinOpts(precond=prec, warm_start=1 if warm else 0, maxit=0, rtol=rtol, atol=0.0,
-                        check_every=config.check_every, gmg_levels=0, cheb_degree=2)
+                        check_every=config.check_every, gmg_levels=0, cheb_degree=2,
+                        gmg_reuse=1 if config.gmg_reuse else 0)
 
 
 def elastic_step(state: State, problem: Discretization, config: SolverConfig):

@@ -89,3 +89,14 @@ def test_stiffness_matches_oracle():
         mat = Material(E=2.1, nu=0.27, regime=regime)
         spec = MaterialSpec(E=2.1, nu=0.27, regime=regime)
         assert np.allclose(mat.stiffness_matrix(), spec.stiffness(), rtol=1e-15)
+
+
+def test_option_structs_built_from_config():
+    """SolverConfig -> pf_lin_opts / pf_vi_opts marshalling (no device needed)."""
+    from paper_1511_08463_b200 import solver as S
+    for reuse in (True, False):
+        cfg = S.SolverConfig(elastic_solver="cg", elastic_precond="gmg", elastic_rtol=1e-9, gmg_reuse=reuse)
+        o = S._lin_opts(cfg, True)
+        assert o.precond == 1 and o.warm_start == 1 and o.rtol == 1e-9 and o.gmg_reuse == int(reuse)
+    o = S._lin_opts(S.SolverConfig(), False)
+    assert o.rtol == S.SolverConfig().direct_rtol and o.warm_start == 0

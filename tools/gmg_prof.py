@@ -24,7 +24,7 @@ for prof in (0, 1):
     prob.call("pf_elastic_solve", _lib.ptr(st.alpha), _lib.ptr(st.u), _lib.ptr(out), C.byref(opts), C.byref(r), pf.fem._stream())
     torch.cuda.synchronize(); t1 = time.perf_counter()
     print(f"profile={prof} its={r.iterations} wall={1e3*(t1-t0):.2f} ms")
-p = read_profile(prob, None)
+p = read_profile(prob)
 tot = sum(v["ms"] for v in p.values())
 for k, v in sorted(p.items(), key=lambda kv: -kv[1]["ms"]):
     print(f"  {k:10s} n={int(v['count']):5d} ms={v['ms']:8.3f} avg_us={1e3*v['ms']/v['count']:7.2f}")

@@ -14,18 +14,23 @@ def main():
     n = int(sys.argv[2]) if len(sys.argv) > 2 else 4096
     pattern = sys.argv[3] if len(sys.argv) > 3 else "union_jack"
     reps = int(sys.argv[4]) if len(sys.argv) > 4 else 5
-    mesh = pf.StructuredMesh(n, n, 1.0, 1.0, pattern)
-    prob = pf.Discretization(mesh, pf.Material(E=1.0, nu=0.3, Gc=1.0, ell=0.1, k_ell=1e-6),
-                             pf.DamageModel("AT1"))
+    if pattern == "kuhn6":
+        mesh = pf.StructuredMesh3D(n, n, n)
+        mat = pf.Material(E=1.0, nu=0.3, Gc=1.0, ell=0.1, k_ell=1e-6, regime="3d")
+    else:
+        mesh = pf.StructuredMesh(n, n, 1.0, 1.0, pattern)
+        mat = pf.Material(E=1.0, nu=0.3, Gc=1.0, ell=0.1, k_ell=1e-6)
+    prob = pf.Discretization(mesh, mat, pf.DamageModel("AT1"))
     V = mesh.n_vertices
+    d = mesh.dim
     g = torch.Generator(device="cuda").manual_seed(1)
     a = torch.rand(V, dtype=torch.float64, device="cuda", generator=g)
-    u = torch.randn(2 * V, dtype=torch.float64, device="cuda", generator=g)
+    u = torch.randn(d * V, dtype=torch.float64, device="cuda", generator=g)
     xa = torch.randn(V, dtype=torch.float64, device="cuda", generator=g)
     st = pf.State(u, a, torch.zeros_like(a))
     if op == "Kuu":
         K = pf.assemble_Kuu(st, prob, apply_bc=False)
-        f, x, nbytes = K.matvec, u, 40.0 * V
+        f, x, nbytes = K.matvec, u, (40.0 if d == 2 else 56.0) * V
     elif op == "Kaa":
         K = pf.assemble_Kaa(st, prob)
         f, x, nbytes = K.matvec, xa, 16.0 * V + 8.0 * prob.n_elements
