@@ -94,7 +94,8 @@ typedef struct pf_vi_opts {
     int32_t max_iterations;
     int32_t precond;        /* inner PCG preconditioner */
     double ls_backtrack, ls_min_step, armijo;
-    double inner_rtol;      /* relative tolerance of the inactive-block PCG */
+    double inner_rtol;      /* relative tolerance of the inactive-block PCG (damage solve);
+                             * pf_newton: of the field-split block solves, <= 0 -> fieldsplit_rtol */
     int64_t inner_maxit;
     double zero_tol;        /* <= 0 -> 1e-10 (1 + |x0|_inf) as the reference */
     double fieldsplit_rtol; /* Newton only: MINRES rtol (solver.py:64) */

@@ -1,4 +1,3 @@
-#include <cstdlib>
 // pf_core.cu -- context, workspace, vector kernels and the device solvers behind the C ABI.
 //
 // Solvers keep all scalars on the device (scal[]); the host loop only polls a done/fail flag
@@ -423,7 +422,11 @@ int pcg_run(Ctx* c, int kind, const PcgBuffers& B, const double* coef, const uns
     // per-kernel profiling is on (eager launches bracketed by events, host-polled batches).
     const bool graphs = c->use_graphs && !c->prof.on;
     const long long key = c->geo_version * 16 + (gmg ? c->gmg_degree : 0);
-    if (graphs && c->graph_key[kind] != key) {
+    // the captured body bakes in these pointers: re-capture when any of them changes
+    const void* body_ptrs[Ctx::kGraphPtrs] = {B.x, B.r, B.z, B.p0, B.p1, B.q, B.dinv, coef, act};
+    const bool same_ptrs = memcmp(body_ptrs, c->graph_ptrs[kind], sizeof(body_ptrs)) == 0;
+    if (graphs && (c->graph_key[kind] != key || !same_ptrs)) {
+        memcpy(c->graph_ptrs[kind], body_ptrs, sizeof(body_ptrs));
         if (c->graph_exec[kind]) { cudaGraphExecDestroy(c->graph_exec[kind]); c->graph_exec[kind] = nullptr; }
         if (!c->cap_stream) PF_CU(c, cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking), "stream");
         PF_CU(c, cudaStreamSynchronize(st), "sync");

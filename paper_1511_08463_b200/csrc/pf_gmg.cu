@@ -16,7 +16,6 @@
 // a = k_ell) are seen by the coarse operators because they are Galerkin products.
 // Stencil layout: A[(k*4 + e)*nv + v], k = (di+1)*3 + (dj+1) neighbour, e = 2r + c block entry.
 #include <algorithm>
-#include <cstdlib>
 #include <cmath>
 #include <cstring>
 

@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/phasefrac_b200.h"
@@ -204,12 +205,15 @@ struct Ctx {
     long long gmg_its0 = -1;        // iterations of the first elastic solve on it (-1: none yet)
     std::vector<unsigned char> h_bcmask;  // last Dirichlet mask (detects mask changes)
     double gmg_ratio = 0.1;
-    // CUDA graphs of two Krylov iterations per solver kind (0 Kuu-Jacobi, 1 Kaa-masked, 2 Kuu-GMG)
+    // device-side Krylov loop graphs per solver kind (0 Kuu-Jacobi, 1 Kaa-masked, 2 Kuu-GMG):
+    // a WHILE node over a captured iteration pair
+    static constexpr int kGraphPtrs = 9;
     int use_graphs = 1;
     cudaStream_t cap_stream = nullptr;
     cudaGraphExec_t graph_exec[3] = {nullptr, nullptr, nullptr};
     long long graph_nodes[3] = {0, 0, 0};
     long long graph_key[3] = {-1, -1, -1};
+    const void* graph_ptrs[3][kGraphPtrs] = {};
     long long geo_version = 0;   // bumped whenever Geo2 fields baked into kernels change
 };
 

@@ -153,7 +153,7 @@ static int fieldsplit(Ctx* c, const NewtonWs& w, const double* r, double* y, con
     NTRY(launch_Kau(c, u, alpha, y1, w.TMP + nu, PF_BC_ELIMINATE, st));            // B^T y1
     k_nsubmask<<<nblocks(na), kNB, 0, st>>>(na, r + nu, w.TMP + nu, c->act, w.TMP + nu);
     c->launches++;
-    NTRY(solve_C(c, w.TMP + nu, z, 1e-3 * inner_rtol, its, st));
+    NTRY(solve_C(c, w.TMP + nu, z, inner_rtol, its, st));
     NTRY(launch_Kua(c, u, alpha, z, w.TMP, PF_BC_ELIMINATE, st));                   // B z
     NTRY(solve_A(c, w.TMP, w.TMP, inner_rtol, its, st));
     k_naxpy<<<nblocks(nu), kNB, 0, st>>>(nu, -1.0, w.TMP, y1);
@@ -261,7 +261,10 @@ int newton_solve(Ctx* c, const double* u_in, const double* a_in, const double* l
     };
     push_hist(merit);
     const double fs_rtol = o->fieldsplit_rtol > 0.0 ? o->fieldsplit_rtol : 1e-6;
-    const double inner_rtol = o->inner_rtol > 0.0 ? std::min(o->inner_rtol, 1e-8) : 1e-8;
+    // inner block solves (the reference's LU, linalg.py:424-430) run to the MINRES tolerance:
+    // tighter inner solves leave the MINRES history unchanged (measured on SENT 512^2 down to
+    // 1e-10) at 1.5-2x the cost
+    const double inner_rtol = o->inner_rtol > 0.0 ? o->inner_rtol : fs_rtol;
     auto line_search = [&](const double* dir, double slope, bool newton, bool& ok) -> int {
         double mu = 1.0;
         ok = false;

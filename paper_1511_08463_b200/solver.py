@@ -69,6 +69,7 @@ class SolverConfig:
     warm_start: bool = True
     check_every: int = 8
     gmg_reuse: bool = True   # keep the GMG hierarchy across solves while it stays effective
+    newton_inner_rtol: Optional[float] = None  # field-split block solves; None -> fieldsplit_rtol
 
     def __post_init__(self):
         if not 0.0 < self.omega < 2.0:
@@ -241,7 +242,8 @@ def coupled_newton_solve(state: State, problem: Discretization, config: SolverCo
                          cycle: int = 0):
     """Active-set Newton on the stacked (u, alpha) system; returns (new_state, report)."""
     vic = VIConfig(abs_tol=config.outer_atol, max_iterations=config.max_newton_iterations,
-                   fieldsplit_rtol=config.fieldsplit_rtol, inner_rtol=config.damage_rtol)
+                   fieldsplit_rtol=config.fieldsplit_rtol,
+                   inner_rtol=config.newton_inner_rtol or 0.0)
     opts = vic.to_c()
     rep = _lib.VIReport()
     out = state.copy()
