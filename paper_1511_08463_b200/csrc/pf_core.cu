@@ -115,6 +115,44 @@ __global__ void k_cg_update_nz(long long n, double* __restrict__ x, double* __re
         if (s[S_ITER] >= s[S_MAXIT]) s[S_DONE] = 3.0;
     });
 }
+// GMG-PCG update with the V-cycle's level-0 cheb0 fused in (per vertex, 2 dofs):
+// x += gamma p ; r -= gamma q ; |r| ; res = D0^-1 r ; d0 = z = res / theta
+__global__ void k_cg_update_gmg(long long nv, double* __restrict__ x, double* __restrict__ r,
+                                const double* __restrict__ p, const double* __restrict__ q, double* s, RedBuf rb,
+                                const double* __restrict__ Dinv, double* __restrict__ res, double* __restrict__ d0,
+                                double* __restrict__ z, const double* lam, double ratio) {
+    if (!solver_live(s)) return;
+    const double gm = s[S_GAMMA];
+    const Cheb c = cheb_of(lam, ratio);
+    double acc[1] = {0.0};
+    for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < nv;
+         v += (long long)gridDim.x * blockDim.x) {
+        double2 xv = reinterpret_cast<double2*>(x)[v];
+        const double2 pv = reinterpret_cast<const double2*>(p)[v];
+        const double2 qv = reinterpret_cast<const double2*>(q)[v];
+        double2 rv = reinterpret_cast<double2*>(r)[v];
+        xv.x += gm * pv.x;
+        xv.y += gm * pv.y;
+        rv.x = rv.x - gm * qv.x;
+        rv.y = rv.y - gm * qv.y;
+        reinterpret_cast<double2*>(x)[v] = xv;
+        reinterpret_cast<double2*>(r)[v] = rv;
+        acc[0] += rv.x * rv.x + rv.y * rv.y;
+        const double2 rr = bmul(Dinv, nv, v, rv.x, rv.y);
+        const double2 dd = make_double2(rr.x / c.theta, rr.y / c.theta);
+        reinterpret_cast<double2*>(res)[v] = rr;
+        reinterpret_cast<double2*>(d0)[v] = dd;
+        reinterpret_cast<double2*>(z)[v] = dd;
+    }
+    grid_reduce<1>(acc, rb, 5, [=](double* t) {
+        const double rn = sqrt(t[0]);
+        s[S_RNORM] = rn;
+        s[S_ITER] += 1.0;
+        if (rn <= s[S_TARGET]) { s[S_DONE] = 1.0; return; }
+        if (s[S_ITER] >= s[S_MAXIT]) s[S_DONE] = 3.0;
+    });
+}
+
 // rz = r . z ; first: S_RZ = rz ; else beta = rz / rz_old  (breakdown if rz <= 0)
 __global__ void k_cg_rz(long long n, const double* __restrict__ r, const double* __restrict__ z, double* s,
                         RedBuf rb, int first) {
@@ -386,9 +424,12 @@ int pcg_run(Ctx* c, int kind, const PcgBuffers& B, const double* coef, const uns
     c->launches++;
     PF_CU(c, cudaGetLastError(), "cg init");
     if (gmg) {
-        PF_TRY(gmg_vcycle(c, B.r, B.z, st, c->scal));
-        k_cg_rz<<<vb, kVecBlock, 0, st>>>(B.n, B.r, B.z, c->scal, rb, 1);
-        c->launches++;
+        bool rzd = false;
+        PF_TRY(gmg_vcycle(c, B.r, B.z, st, c->scal, false, 1, &rzd));
+        if (!rzd) {
+            k_cg_rz<<<vb, kVecBlock, 0, st>>>(B.n, B.r, B.z, c->scal, rb, 1);
+            c->launches++;
+        }
     }
     PF_TRY(read_scal(c, st, 0, 24));
     // one Krylov iteration k (ping-pong search-direction buffers by parity)
@@ -397,14 +438,22 @@ int pcg_run(Ctx* c, int kind, const PcgBuffers& B, const double* coef, const uns
         double* pout = (k & 1) ? B.p0 : B.p1;
         if (gmg) {
             PF_TRY(launch_Kuu_cgA(c, coef, B.z, pin, pout, B.q, s));
+            const GLevel& L0 = c->glev[0];
+            const long long nv0 = B.n / 2;
             const int ps = prof_begin(c, s);
-            k_cg_update_nz<<<vb, kVecBlock, 0, s>>>(B.n, B.x, B.r, pout, B.q, c->scal, rb);
-            prof_end(c, s, ps, K_CG_VEC, 8.0 * B.n * 6);
-            PF_TRY(gmg_vcycle(c, B.r, B.z, s, c->scal));
-            const int ps2 = prof_begin(c, s);
-            k_cg_rz<<<vb, kVecBlock, 0, s>>>(B.n, B.r, B.z, c->scal, rb, 0);
-            prof_end(c, s, ps2, K_CG_VEC, 8.0 * B.n * 2);
-            c->launches += 2;
+            k_cg_update_gmg<<<vec_blocks(nv0), kVecBlock, 0, s>>>(nv0, B.x, B.r, pout, B.q, c->scal, rb, L0.Dinv,
+                                                                   L0.res, L0.d0, B.z, c->scal + S_GMG0,
+                                                                   c->gmg_ratio);
+            prof_end(c, s, ps, K_CG_VEC, 8.0 * B.n * 6 + 8.0 * B.n * 5);  // + Dinv, res, d0, z
+            c->launches++;
+            bool rzd = false;
+            PF_TRY(gmg_vcycle(c, B.r, B.z, s, c->scal, true, 0, &rzd));
+            if (!rzd) {
+                const int ps2 = prof_begin(c, s);
+                k_cg_rz<<<vb, kVecBlock, 0, s>>>(B.n, B.r, B.z, c->scal, rb, 0);
+                prof_end(c, s, ps2, K_CG_VEC, 8.0 * B.n * 2);
+                c->launches++;
+            }
             return PF_OK;
         }
         if (kind == 0) PF_TRY(launch_Kuu_cgA(c, coef, B.z, pin, pout, B.q, s));

@@ -416,26 +416,6 @@ __global__ void k_coarse_solve(int n, const double* Ainv, const double* b, doubl
 }
 
 // ---- Chebyshev smoother pieces ----------------------------------------------------------------
-struct Cheb {
-    double theta, delta, sigma;
-};
-__device__ __forceinline__ Cheb cheb_of(const double* lam, double ratio) {
-    const double hi = *lam, lo = hi * ratio;
-    Cheb c;
-    c.theta = 0.5 * (hi + lo);
-    c.delta = 0.5 * (hi - lo);
-    c.sigma = c.theta / c.delta;
-    return c;
-}
-__device__ __forceinline__ double cheb_rho(const Cheb& c, int k) {  // rho_k, rho_0 = 1/sigma
-    double rho = 1.0 / c.sigma;
-    for (int t = 1; t <= k; ++t) rho = 1.0 / (2.0 * c.sigma - rho);
-    return rho;
-}
-__device__ __forceinline__ double2 bmul(const double* Dinv, long long nv, long long v, double r0, double r1) {
-    return make_double2(__ldg(Dinv + v) * r0 + __ldg(Dinv + nv + v) * r1,
-                        __ldg(Dinv + 2 * nv + v) * r0 + __ldg(Dinv + 3 * nv + v) * r1);
-}
 // V-cycle vectors are streamed through L2 (ld.global.cg); operators/Dinv via the read-only path.
 __device__ __forceinline__ double2 ldv(const double* p, long long v) {
     return __ldcg(reinterpret_cast<const double2*>(p) + v);
@@ -511,11 +491,6 @@ __device__ __forceinline__ void v_cheb_step(const LevelDev& L, const double* Ad,
     xv.x += dn.x;
     xv.y += dn.y;
     stv(x, v, xv);
-}
-__device__ __forceinline__ void cheb_ab(const Cheb& c, int k, double& a, double& b) {
-    const double rp = cheb_rho(c, k - 1), rn = cheb_rho(c, k);
-    a = rn * rp;
-    b = 2.0 * rn / c.delta;
 }
 __global__ void k_cheb_step(LevelDev L, const double* Ad, const double* d, double* dnext, double* res, double* x,
                             int k, int addd, const double* lam, double ratio, const double* live) {
@@ -870,8 +845,27 @@ int gmg_setup(Ctx* c, cudaStream_t st) {
     return check_cuda(c, cudaGetLastError(), "gmg setup");
 }
 
+static GmgEpi epi0(Ctx* c, const double* live) {
+    GLevel& L = c->glev[0];
+    GmgEpi e{};
+    e.Dinv = L.Dinv;
+    e.nvD = L.nv;
+    e.res = L.res;
+    e.lam = c->scal + S_GMG0;
+    e.ratio = c->gmg_ratio;
+    e.k = 1;
+    e.live = live;
+    e.rz_first = -1;
+    return e;
+}
+
 // z = M r : one V-cycle, level 0 vectors are the PCG r (input) and z (output).
-int gmg_vcycle(Ctx* c, const double* r_in, double* z_out, cudaStream_t st, const double* live) {
+// cheb0_done: the caller already wrote the level-0 cheb0 (res = D^-1 r, d0 = z = res / theta;
+// k_cg_update_gmg).  rz_first >= 0: fuse the PCG r . z into the last fine smoother step
+// (*rz_done reports whether it was fused; with degree 1 it is not).
+int gmg_vcycle(Ctx* c, const double* r_in, double* z_out, cudaStream_t st, const double* live, bool cheb0_done,
+               int rz_first, bool* rz_done) {
+    if (rz_done) *rz_done = false;
     const Geo2& g = c->g;
     const int nl = (int)c->glev.size();
     const int deg = std::max(1, c->gmg_degree);
@@ -888,15 +882,21 @@ int gmg_vcycle(Ctx* c, const double* r_in, double* z_out, cudaStream_t st, const
         Ld.nv = nv;
         double* d = L.d0;
         double* dn = L.d1;
-        if (l == 0) {  // pre-smooth from x = 0 with the matrix-free fine operator
-            GKB(c, K_GMG, 96.0 * nv, (k_cheb0<<<gblocks(nv), kGB, 0, st>>>(nv, L.Dinv, b, L.res, L.d0, x, 0, lam + l, ratio, live)));
+        if (l == 0) {  // pre-smooth from x = 0 with the matrix-free fine operator (fused epilogues)
+            if (!cheb0_done)
+                GKB(c, K_GMG, 96.0 * nv, (k_cheb0<<<gblocks(nv), kGB, 0, st>>>(nv, L.Dinv, b, L.res, L.d0, x, 0, lam + l, ratio, live)));
             for (int k = 1; k < deg; ++k) {
-                PF_TRY_GMG(launch_Kuu(c, c->alpha_ws, d, L.w, PF_BC_ELIMINATE, st));
-                GKB(c, K_GMG, 144.0 * nv, (k_cheb_step<<<gblocks(nv), kGB, 0, st>>>(Ld, L.w, d, dn, L.res, x, k, 0, lam + l, ratio, live)));
+                GmgEpi e = epi0(c, live);
+                e.dnext = dn;
+                e.xs = x;
+                e.k = k;
+                PF_TRY_GMG(launch_Kuu_smooth(c, EPI_CHEB, c->alpha_ws, d, e, st));
                 std::swap(d, dn);
             }
-            PF_TRY_GMG(launch_Kuu(c, c->alpha_ws, x, L.w, PF_BC_ELIMINATE, st));
-            GKB(c, K_GMG, 64.0 * nv, (k_resid<<<gblocks(nv), kGB, 0, st>>>(Ld, L.w, x, b, L.r, live)));
+            GmgEpi e = epi0(c, live);
+            e.bvec = b;
+            e.rout = L.r;
+            PF_TRY_GMG(launch_Kuu_smooth(c, EPI_RESID, c->alpha_ws, x, e, st));
         } else {
             GKB(c, K_GMG, (deg > 1 ? 416.0 : 96.0) * nv, (k_pre_first<<<gblocks(nv), kGB, 0, st>>>(Ld, b, L.res, L.d0, L.d1, x, deg, lam + l, ratio, live)));
             if (deg > 1) std::swap(d, dn);
@@ -958,13 +958,23 @@ int gmg_vcycle(Ctx* c, const double* r_in, double* z_out, cudaStream_t st, const
         }
         double* d = L.d0;
         double* dn = L.d1;
-        if (l == 0) {  // post-smooth: r = b - A x ; x += p(D^-1 A) D^-1 r
-            PF_TRY_GMG(launch_Kuu(c, c->alpha_ws, x, L.w, PF_BC_ELIMINATE, st));
-            GKB(c, K_GMG, 64.0 * nv, (k_resid<<<gblocks(nv), kGB, 0, st>>>(Ld, L.w, x, b, L.r, live)));
-            GKB(c, K_GMG, 112.0 * nv, (k_cheb0<<<gblocks(nv), kGB, 0, st>>>(nv, L.Dinv, L.r, L.res, L.d0, x, 1, lam + l, ratio, live)));
+        if (l == 0) {  // post-smooth: res = D^-1 (b - A x), d0 = res/theta ; steps (x += d0 on step 1)
+            GmgEpi e = epi0(c, live);
+            e.bvec = b;
+            e.dnext = L.d0;
+            PF_TRY_GMG(launch_Kuu_smooth(c, EPI_RESID_CHEB0, c->alpha_ws, x, e, st));
+            if (deg <= 1) GKB(c, K_GMG, 48.0 * nv, (k_add<<<gblocks(nv), kGB, 0, st>>>(nv, L.d0, x, live)));
             for (int k = 1; k < deg; ++k) {
-                PF_TRY_GMG(launch_Kuu(c, c->alpha_ws, d, L.w, PF_BC_ELIMINATE, st));
-                GKB(c, K_GMG, 144.0 * nv, (k_cheb_step<<<gblocks(nv), kGB, 0, st>>>(Ld, L.w, d, dn, L.res, x, k, 0, lam + l, ratio, live)));
+                GmgEpi es = epi0(c, live);
+                es.dnext = dn;
+                es.xs = x;
+                es.k = k;
+                if (k == deg - 1 && rz_first >= 0) {
+                    es.rcg = r_in;
+                    es.rz_first = rz_first;
+                    if (rz_done) *rz_done = true;
+                }
+                PF_TRY_GMG(launch_Kuu_smooth(c, k == 1 ? EPI_CHEB_ADDD : EPI_CHEB, c->alpha_ws, d, es, st));
                 std::swap(d, dn);
             }
         } else {  // residual + cheb0 in one pass; the x += d0 rides on step 1

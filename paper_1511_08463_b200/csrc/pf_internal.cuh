@@ -151,6 +151,60 @@ struct Prof {
     long long count[K_NKINDS] = {0};
 };
 
+// ---- Chebyshev smoother scalars (linalg.py:366-376) -------------------------------------------
+// Shared by the GMG level kernels (pf_gmg.cu) and the fused fine-level strip epilogues (pf_ops2d.cu)
+// so both evaluate the same expressions.
+struct Cheb {
+    double theta, delta, sigma;
+};
+__device__ __forceinline__ Cheb cheb_of(const double* lam, double ratio) {
+    const double hi = *lam, lo = hi * ratio;
+    Cheb c;
+    c.theta = 0.5 * (hi + lo);
+    c.delta = 0.5 * (hi - lo);
+    c.sigma = c.theta / c.delta;
+    return c;
+}
+__device__ __forceinline__ double cheb_rho(const Cheb& c, int k) {  // rho_k, rho_0 = 1/sigma
+    double rho = 1.0 / c.sigma;
+    for (int t = 1; t <= k; ++t) rho = 1.0 / (2.0 * c.sigma - rho);
+    return rho;
+}
+__device__ __forceinline__ void cheb_ab(const Cheb& c, int k, double& a, double& b) {
+    const double rp = cheb_rho(c, k - 1), rn = cheb_rho(c, k);
+    a = rn * rp;
+    b = 2.0 * rn / c.delta;
+}
+// 2x2 block-Jacobi inverse applied at vertex v: Dinv[(2r + c) * nv + v]
+__device__ __forceinline__ double2 bmul(const double* Dinv, long long nv, long long v, double r0, double r1) {
+    return make_double2(__ldg(Dinv + v) * r0 + __ldg(Dinv + nv + v) * r1,
+                        __ldg(Dinv + 2 * nv + v) * r0 + __ldg(Dinv + 3 * nv + v) * r1);
+}
+
+// ---- GMG fine-level smoother epilogues fused into the Kuu strip kernel (pf_ops2d.cu) -----------
+enum {
+    EPI_NONE = 0,
+    EPI_CHEB,         // Chebyshev step k on input d:  res -= D^-1 K d ; dnext = a d + b res ; x += dnext
+    EPI_CHEB_ADDD,    // the same, plus the post-smoother's deferred x += d  (first post step)
+    EPI_RESID,        // rout = b - K x
+    EPI_RESID_CHEB0,  // res = D^-1 (b - K x) ; dnext = res / theta  (post-smoother entry)
+};
+struct GmgEpi {
+    const double* Dinv;   // level-0 2x2 block-Jacobi inverse [4][nvD]
+    long long nvD;
+    double* res;
+    double* dnext;
+    double* xs;           // smoother iterate
+    const double* bvec;   // right-hand side (resid modes)
+    double* rout;         // residual out (EPI_RESID)
+    const double* lam;    // level-0 lambda_max bound (device)
+    double ratio;
+    int k;                // Chebyshev step index (>= 1)
+    const double* live;   // solver scalars (null: always live)
+    const double* rcg;    // PCG residual for the fused r . z (rz_first >= 0)
+    int rz_first;         // -1: no r . z ; 1: first (S_RZ only) ; 0: also S_BETA
+};
+
 // ---- multigrid level (pf_gmg.cu) -------------------------------------------------------------
 struct GLevel {
     int nx = 0, ny = 0;        // cells
@@ -245,6 +299,7 @@ struct CgScal {  // pointers into the scalar block used by fused CG kernels
 // y = K p_out and pAp reduced into scal (CG step A).
 int launch_Kuu(Ctx* c, const double* alpha, const double* x, double* y, int bcmode,
                cudaStream_t st);
+int launch_Kuu_smooth(Ctx* c, int epi, const double* alpha, const double* d, const GmgEpi& e, cudaStream_t st);
 int launch_Kuu_cgA(Ctx* c, const double* alpha, const double* z, const double* p_in,
                    double* p_out, double* q, cudaStream_t st);
 int launch_Kuu_diag(Ctx* c, const double* alpha, double* dinv, cudaStream_t st);
@@ -316,7 +371,8 @@ void gmg_plan(Ctx* c);
 size_t gmg_bytes(const Ctx* c);
 void gmg_bind(Ctx* c, char* base);
 int gmg_setup(Ctx* c, cudaStream_t st);
-int gmg_vcycle(Ctx* c, const double* r_in, double* z_out, cudaStream_t st, const double* live);
+int gmg_vcycle(Ctx* c, const double* r_in, double* z_out, cudaStream_t st, const double* live,
+               bool cheb0_done = false, int rz_first = -1, bool* rz_done = nullptr);
 int newton_solve(Ctx* c, const double* u_in, const double* a_in, const double* lb, double* u_out,
                  double* a_out, const pf_vi_opts* o, pf_vi_report* rep, cudaStream_t st);
 

@@ -195,7 +195,9 @@ __device__ __forceinline__ double getGc(const Geo2& g, const Slots& s, int q) {
 // and gamma = rz / pAp formed by the last block (linalg.py:130-138).
 // vertex slots: x|z (0-1), [p_in (2-3)], alpha; cell slots: E, [centre x|z, p_in, alpha]
 // ================================================================================================
-template <bool FUSED>
+// EPI != 0: GMG fine-level smoother epilogue (pf_gmg.cu), applied where each output vertex is
+// final instead of storing y = K x (see GmgEpi in pf_internal.cuh for the modes).
+template <bool FUSED, int EPI = EPI_NONE>
 struct OpKuu {
     static constexpr int NV = 3, NC = 2, MINB = 2;
     static constexpr int pd(int pat) { return 4; }
@@ -211,10 +213,53 @@ struct OpKuu {
     double* scal;
     RedBuf rb;
     double acc;
+    GmgEpi e{};
+    double ca = 0.0, cb = 0.0, th = 1.0;
 
-    __device__ bool enter() const {
+    __device__ bool enter() {
+        if constexpr (EPI != EPI_NONE) {
+            if (e.live && !(e.live[S_DONE] == 0.0 && e.live[S_FAIL] == 0.0)) return false;
+            const Cheb c = cheb_of(e.lam, e.ratio);
+            th = c.theta;
+            if (EPI == EPI_CHEB || EPI == EPI_CHEB_ADDD) cheb_ab(c, e.k, ca, cb);
+            return true;
+        }
         if (!FUSED) return true;
         return scal[S_DONE] == 0.0 && scal[S_FAIL] == 0.0;
+    }
+    // smoother epilogue at a final output vertex: y = (K d)_id, (d0, d1) = d_id (the raw input)
+    __device__ __forceinline__ void epi(long long id, double y0, double y1, double d0, double d1) {
+        if constexpr (EPI == EPI_CHEB || EPI == EPI_CHEB_ADDD) {
+            // res -= D^-1 y ; dnext = a d + b res ; x (+= d) += dnext   (k_cheb_step)
+            const double2 dw = bmul(e.Dinv, e.nvD, id, y0, y1);
+            double2 r = reinterpret_cast<const double2*>(e.res)[id];
+            r.x -= dw.x;
+            r.y -= dw.y;
+            const double2 dn = make_double2(ca * d0 + cb * r.x, ca * d1 + cb * r.y);
+            st2(e.res, id, r.x, r.y);
+            st2(e.dnext, id, dn.x, dn.y);
+            double2 xv = reinterpret_cast<const double2*>(e.xs)[id];
+            if (EPI == EPI_CHEB_ADDD) {
+                xv.x += d0;
+                xv.y += d1;
+            }
+            xv.x += dn.x;
+            xv.y += dn.y;
+            st2(e.xs, id, xv.x, xv.y);
+            if (e.rz_first >= 0) {  // PCG r . z with z = this final smoother iterate
+                const double2 rv = ld2(e.rcg, id);
+                acc += rv.x * xv.x + rv.y * xv.y;
+            }
+        } else if constexpr (EPI == EPI_RESID) {
+            const double2 bv = ld2(e.bvec, id);
+            st2(e.rout, id, bv.x - y0, bv.y - y1);
+        } else if constexpr (EPI == EPI_RESID_CHEB0) {
+            // res = D^-1 (b - y) ; d0 = res / theta   (k_resid + k_cheb0; x += d0 is deferred)
+            const double2 bv = ld2(e.bvec, id);
+            const double2 rr = bmul(e.Dinv, e.nvD, id, bv.x - y0, bv.y - y1);
+            st2(e.res, id, rr.x, rr.y);
+            st2(e.dnext, id, rr.x / th, rr.y / th);
+        }
     }
     __device__ __forceinline__ double beta() const { return scal[S_ITER] > 0.0 ? scal[S_BETA] : 0.0; }
     __device__ __forceinline__ double2 xval(long long v) const {  // direct (boundary rows only)
@@ -298,10 +343,14 @@ struct OpKuu {
         if constexpr (PAT == PF_CROSSED) {
             if (own) {
                 const long long cv = ctr(g, ci, j);
-                st2(y, cv, Y1[4], Y2[4]);
-                if (FUSED) {
-                    st2(pout, cv, U1[4], U2[4]);
-                    acc += U1[4] * Y1[4] + U2[4] * Y2[4];
+                if constexpr (EPI != EPI_NONE) {
+                    epi(cv, Y1[4], Y2[4], U1[4], U2[4]);
+                } else {
+                    st2(y, cv, Y1[4], Y2[4]);
+                    if (FUSED) {
+                        st2(pout, cv, U1[4], U2[4]);
+                        acc += U1[4] * Y1[4] + U2[4] * Y2[4];
+                    }
                 }
             }
         }
@@ -316,6 +365,10 @@ struct OpKuu {
             if (m & 1u) { y0 = xv.x; p0 = xv.x; }
             if (m & 2u) { y1 = xv.y; p1 = xv.y; }
         }
+        if constexpr (EPI != EPI_NONE) {
+            epi(id, y0, y1, p0, p1);
+            return;
+        }
         st2(y, id, y0, y1);
         if (FUSED) {
             st2(pout, id, p0, p1);
@@ -323,7 +376,19 @@ struct OpKuu {
         }
     }
     __device__ void finish() {
-        if (!FUSED) return;
+        if constexpr (EPI == EPI_CHEB || EPI == EPI_CHEB_ADDD) {
+            if (e.rz_first < 0) return;
+            double v[1] = {acc};
+            double* s = scal;
+            const int first = e.rz_first;
+            grid_reduce<1>(v, rb, 6, [s, first](double* t) {  // k_cg_rz
+                if (!(t[0] > 0.0)) { s[S_FAIL] = 2.0; return; }
+                if (!first) s[S_BETA] = t[0] / s[S_RZ];
+                s[S_RZ] = t[0];
+            });
+            return;
+        }
+        if (EPI != EPI_NONE || !FUSED) return;
         double v[1] = {acc};
         double* s = scal;
         grid_reduce<1>(v, rb, 0, [s](double* tot) {
@@ -1366,7 +1431,7 @@ static cudaError_t launch_pat(const Geo2& g, const Op& op, int nb, cudaStream_t 
 }
 
 template <class Op>
-static int run_strip(Ctx* c, Op op, cudaStream_t st, int kind = K_VEC, int nw = 0) {
+static int run_strip(Ctx* c, Op op, cudaStream_t st, int kind = K_VEC, int nw = 0, double bytes = -1.0) {
     const Geo2& g = c->g;
     const int nb = strip_blocks(g);
     if (nb > kMaxBlocksRed) return set_error(c, PF_EINVAL, "grid too large for reduction buffer");
@@ -1378,7 +1443,7 @@ static int run_strip(Ctx* c, Op op, cudaStream_t st, int kind = K_VEC, int nw = 
         default: e = launch_pat<Op, PF_CROSSED>(g, op, nb, st); break;
     }
     if (e != cudaSuccess) return check_cuda(c, e, "strip kernel attribute");
-    prof_end(c, st, slot, kind, alg_bytes(c, kind, 0, nw));
+    prof_end(c, st, slot, kind, bytes >= 0.0 ? bytes : alg_bytes(c, kind, 0, nw));
     c->launches++;
     return check_cuda(c, cudaGetLastError(), "strip kernel launch");
 }
@@ -1389,6 +1454,31 @@ int launch_Kuu(Ctx* c, const double* alpha, const double* x, double* y, int bcmo
     if (c->dim == 3) return launch3_Kuu(c, alpha, x, y, bcmode, st);
     OpKuu<false> op{alpha, x, nullptr, nullptr, y, bcmode, c->scal, redbuf(c), 0.0};
     return run_strip(c, op, st, K_KUU);
+}
+int launch_Kuu_smooth(Ctx* c, int epi, const double* alpha, const double* d, const GmgEpi& e, cudaStream_t st) {
+    if (c->dim == 3) return set_error(c, PF_EINVAL, "GMG smoother epilogues are 2D");
+    const double V = (double)c->g.nv;
+    double extra = 0.0;
+    switch (epi) {
+        case EPI_CHEB:
+        case EPI_CHEB_ADDD: {
+            OpKuu<false, EPI_CHEB> op{alpha, d, nullptr, nullptr, nullptr, PF_BC_ELIMINATE, c->scal, redbuf(c), 0.0, e};
+            extra = 32 + 32 + 16 + 32 + (e.rz_first >= 0 ? 16 : 0);  // Dinv, res, dnext, x, [r]
+            if (epi == EPI_CHEB) return run_strip(c, op, st, K_GMG, 0, V * (40 + extra));
+            OpKuu<false, EPI_CHEB_ADDD> op2{alpha, d, nullptr, nullptr, nullptr, PF_BC_ELIMINATE, c->scal, redbuf(c), 0.0, e};
+            return run_strip(c, op2, st, K_GMG, 0, V * (40 + extra));
+        }
+        case EPI_RESID: {
+            OpKuu<false, EPI_RESID> op{alpha, d, nullptr, nullptr, nullptr, PF_BC_ELIMINATE, c->scal, redbuf(c), 0.0, e};
+            return run_strip(c, op, st, K_GMG, 0, V * (40 - 16 + 32));  // b -> r instead of y
+        }
+        case EPI_RESID_CHEB0: {
+            OpKuu<false, EPI_RESID_CHEB0> op{alpha, d, nullptr, nullptr, nullptr, PF_BC_ELIMINATE, c->scal, redbuf(c), 0.0, e};
+            return run_strip(c, op, st, K_GMG, 0, V * (40 - 16 + 16 + 32 + 32));  // b, Dinv -> res, d0
+        }
+        default:
+            return set_error(c, PF_EINVAL, "unknown smoother epilogue");
+    }
 }
 int launch_Kuu_cgA(Ctx* c, const double* alpha, const double* z, const double* p_in, double* p_out,
                    double* q, cudaStream_t st) {
