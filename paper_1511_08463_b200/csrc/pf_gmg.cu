@@ -401,21 +401,6 @@ __global__ void k_coarse_inverse(LevelDev L, double* Ainv) {
     }
 }
 
-// x = Ainv b, one warp per row (coalesced over columns)
-__global__ void k_coarse_solve(int n, const double* Ainv, const double* b, double* x, const double* live) {
-    if (!gmg_live(live)) return;
-    const int lane = threadIdx.x & 31;
-    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int nw = (gridDim.x * blockDim.x) >> 5;
-    for (int r = warp; r < n; r += nw) {
-        double s = 0.0;
-        for (int c = lane; c < n; c += 32) s += Ainv[(size_t)r * n + c] * b[c];  // symmetric
-        s = warp_sum(s);
-        if (lane == 0) x[r] = s;
-    }
-}
-
-// ---- Chebyshev smoother pieces ----------------------------------------------------------------
 // V-cycle vectors are streamed through L2 (ld.global.cg); operators/Dinv via the read-only path.
 __device__ __forceinline__ double2 ldv(const double* p, long long v) {
     return __ldcg(reinterpret_cast<const double2*>(p) + v);
@@ -655,6 +640,93 @@ __global__ void k_prolong(LevelDev F, LevelDev Cd, const unsigned char* maskc, c
         v_prolong(F, Cd, maskc, xc, xf, v);
 }
 
+// ---- coarse tail of the V-cycle in one CTA ------------------------------------------------------
+// Levels lc..nl-1 (each <= kTailMaxV vertices, L2/L1-resident) run in a single 512-thread block:
+// per level pre-smooth (cheb0 fused into step 1), steps 2..deg-1, residual, restriction; the
+// dense coarse solve; then prolongation, residual + cheb0, steps (x += d0 on step 1) -- the same
+// per-vertex functions, in the same order, as the per-level kernels, separated by __syncthreads
+// instead of kernel boundaries.
+constexpr int kTailMaxV = 300;
+constexpr int kTailLev = 12;
+constexpr int kTB = 512;
+struct TLev {
+    LevelDev L;
+    double *x, *b, *r, *d0, *d1, *res;
+};
+struct TailArgs {
+    int lc, nl, deg, ncoarse;
+    double ratio;
+    const double* ainv;
+    TLev lev[kTailLev];
+};
+
+__global__ void __launch_bounds__(kTB, 1) k_gmg_tail(const __grid_constant__ TailArgs A, const double* lam,
+                                                     const double* live) {
+    if (!gmg_live(live)) return;  // uniform: the flags are not written during the launch
+    const int t0 = threadIdx.x;
+    const int deg = A.deg;
+    for (int l = A.lc; l < A.nl - 1; ++l) {
+        const TLev& V = A.lev[l];
+        const Cheb c = cheb_of(lam + l, A.ratio);
+        double a = 0.0, b = 0.0;
+        if (deg > 1) cheb_ab(c, 1, a, b);
+        for (long long v = t0; v < V.L.nv; v += kTB) v_pre_first(V.L, V.b, V.res, V.d0, V.d1, V.x, c, a, b, deg, v);
+        __syncthreads();
+        double* d = V.d1;
+        double* dn = V.d0;
+        for (int k = 2; k < deg; ++k) {
+            cheb_ab(c, k, a, b);
+            for (long long v = t0; v < V.L.nv; v += kTB) v_cheb_step(V.L, nullptr, d, dn, V.res, V.x, a, b, 0, v);
+            __syncthreads();
+            double* tmp = d; d = dn; dn = tmp;
+        }
+        for (long long v = t0; v < V.L.nv; v += kTB) v_resid(V.L, nullptr, V.x, V.b, V.r, v);
+        __syncthreads();
+        const TLev& C = A.lev[l + 1];
+        for (long long v = t0; v < C.L.nv; v += kTB) v_restrict(V.L, C.L, C.L.mask, V.r, C.b, v);
+        __syncthreads();
+    }
+    {   // coarsest: x = Ainv b, one warp per row
+        const TLev& C = A.lev[A.nl - 1];
+        const int n = A.ncoarse, lane = t0 & 31;
+        for (int r = t0 >> 5; r < n; r += kTB / 32) {
+            double s = 0.0;
+            for (int q = lane; q < n; q += 32) s += A.ainv[(size_t)r * n + q] * __ldcg(C.b + q);
+            s = warp_sum(s);
+            if (lane == 0) C.x[r] = s;
+        }
+        __syncthreads();
+    }
+    for (int l = A.nl - 2; l >= A.lc; --l) {
+        const TLev& V = A.lev[l];
+        const TLev& C = A.lev[l + 1];
+        const Cheb c = cheb_of(lam + l, A.ratio);
+        for (long long v = t0; v < V.L.nv; v += kTB) v_prolong(V.L, C.L, C.L.mask, C.x, V.x, v);
+        __syncthreads();
+        for (long long v = t0; v < V.L.nv; v += kTB) v_post_first(V.L, V.x, V.b, V.res, V.d0, c, v);
+        __syncthreads();
+        if (deg <= 1) {
+            for (long long v = t0; v < V.L.nv; v += kTB) {
+                const double2 dv = ldv(V.d0, v);
+                double2 xv = ldv(V.x, v);
+                xv.x += dv.x;
+                xv.y += dv.y;
+                stv(V.x, v, xv);
+            }
+            __syncthreads();
+        }
+        double* d = V.d0;
+        double* dn = V.d1;
+        for (int k = 1; k < deg; ++k) {
+            double a, b;
+            cheb_ab(c, k, a, b);
+            for (long long v = t0; v < V.L.nv; v += kTB) v_cheb_step(V.L, nullptr, d, dn, V.res, V.x, a, b, k == 1, v);
+            __syncthreads();
+            double* tmp = d; d = dn; dn = tmp;
+        }
+    }
+}
+
 // crossed level 0 <-> corner grid, factored as P0 = (corner identity + centre mean) o P_{2:1}:
 // z[c] = m_c r[c] + 1/4 sum_{adjacent centres} r[ctr]  (then unmasked-fine 2:1 restriction)
 __global__ void k_collapse_centres(const Geo2 g, const unsigned char* mask0, const double* r, double* z,
@@ -859,6 +931,37 @@ static GmgEpi epi0(Ctx* c, const double* live) {
     return e;
 }
 
+// first level of the single-CTA tail (>= 1; nl - 1 = the dense solve only)
+static int tail_level(const Ctx* c) {
+    const int nl = (int)c->glev.size();
+    int lc = nl - 1;
+    while (lc > 1 && c->glev[lc - 1].nv <= kTailMaxV && nl - (lc - 1) <= kTailLev) --lc;
+    return lc;
+}
+
+static int launch_tail(Ctx* c, int lc, cudaStream_t st, const double* live) {
+    const int nl = (int)c->glev.size();
+    TailArgs a;
+    memset(&a, 0, sizeof(a));
+    a.lc = lc;
+    a.nl = nl;
+    a.deg = std::max(1, c->gmg_degree);
+    a.ratio = c->gmg_ratio;
+    a.ainv = c->gmg_ainv;
+    a.ncoarse = (int)(2 * c->glev[nl - 1].nv);
+    double bytes = 8.0 * a.ncoarse * a.ncoarse + 32.0 * a.ncoarse;
+    for (int l = lc; l < nl; ++l) {
+        GLevel& L = c->glev[l];
+        a.lev[l].L = ldev(c, l);
+        a.lev[l].x = L.x; a.lev[l].b = L.b; a.lev[l].r = L.r;
+        a.lev[l].d0 = L.d0; a.lev[l].d1 = L.d1; a.lev[l].res = L.res;
+        if (l + 1 < nl)  // the same algorithmic bytes as the per-level kernels it replaces
+            bytes += (416.0 + 336.0 + 16.0 + 32.0 + 400.0 + 416.0) * L.nv + 34.0 * c->glev[l + 1].nv;
+    }
+    GKB(c, K_GMG, bytes, (k_gmg_tail<<<1, kTB, 0, st>>>(a, c->scal + S_GMG0, live)));
+    return PF_OK;
+}
+
 // z = M r : one V-cycle, level 0 vectors are the PCG r (input) and z (output).
 // cheb0_done: the caller already wrote the level-0 cheb0 (res = D^-1 r, d0 = z = res / theta;
 // k_cg_update_gmg).  rz_first >= 0: fuse the PCG r . z into the last fine smoother step
@@ -871,7 +974,7 @@ int gmg_vcycle(Ctx* c, const double* r_in, double* z_out, cudaStream_t st, const
     const int deg = std::max(1, c->gmg_degree);
     const double ratio = c->gmg_ratio;
     double* lam = c->scal + S_GMG0;
-    const int lc = nl - 1;  // per-level kernels down to the dense coarse solve
+    const int lc = tail_level(c);  // per-level kernels down to level lc, then the one-CTA tail
     // descend through the per-level kernels
     for (int l = 0; l < lc; ++l) {
         GLevel& L = c->glev[l];
@@ -925,11 +1028,7 @@ int gmg_vcycle(Ctx* c, const double* r_in, double* z_out, cudaStream_t st, const
             GKB(c, K_GMG, 16.0 * F.nv + 17.0 * Cd.nv, (k_restrict<<<gblocks(Cd.nv), kGB, 0, st>>>(F, Cd, C.mask, L.r, C.b, live)));
         }
     }
-    {   // coarsest: dense inverse
-        GLevel& L = c->glev[nl - 1];
-        const int n = (int)(2 * L.nv);
-        GKB(c, K_GMG, 8.0 * n * n + 32.0 * n, (k_coarse_solve<<<std::max(1, (n + 7) / 8), 256, 0, st>>>(n, c->gmg_ainv, L.b, L.x, live)));
-    }
+    PF_TRY_GMG(launch_tail(c, lc, st, live));  // levels lc..nl-1 incl. the dense coarse solve
     // ascend
     for (int l = lc - 1; l >= 0; --l) {
         GLevel& L = c->glev[l];
