@@ -18,6 +18,7 @@ graphs off).  Multi-GPU: replicas only -- every rank runs its own re
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import math
 import os
@@ -30,8 +31,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "fp64 operator-apply GDOF/s & HBM GB/s vs peak; sec per load step (AM+Newton)"
-REF_N = 48          # CPU sample size (SENT, crossed), see DESIGN.md "CPU baseline"
-CPU_EXPONENT = 1.33  # measured oracle cost growth per DOF (32^2 -> 64^2) for the labelled estimate
+REF_N = 48          # CPU sample sizes (SENT, crossed), see DESIGN.md "CPU baseline"
+REF_N_SMALL = 32
 
 
 def peaks():
@@ -132,18 +133,24 @@ def make_workload(pf, name):
 
 
 # ---- CPU side (oracle = restatement of the reference algorithm; SuperLU direct solves) -----------
-def oracle_sent_steps(n, steps):
+def _sent_vertices(n):
+    return (n + 1) ** 2 + n ** 2  # crossed: corners + centres
+
+
+def oracle_sent_steps(n, warm, timed):
+    """Oracle SENT at n x n: march the warm-up steps untimed, then time the timed steps."""
     from oracle import am as oam
     from oracle import problems as opb
     s = opb.sent(n=n)
     cfg = oam.AMConfig(method="oram_newton", omega=1.8, outer_atol=1e-6, am_switch_atol=1e-3,
                        max_am_iterations=2000)
+    _, st = opb.run(s, cfg, snapshot_stride=0, steps=list(warm))
     t0 = time.perf_counter()
-    rows, _ = opb.run(s, cfg, snapshot_stride=0, steps=steps)
-    return time.perf_counter() - t0, len(rows)
+    rows, _ = opb.run(s, cfg, snapshot_stride=0, steps=list(timed), state=st)
+    return (time.perf_counter() - t0) / len(rows)
 
 
-def oracle_traction1_steps(steps):
+def oracle_traction1_steps(warm, timed):
     from oracle import am as oam
     from oracle import problems as opb
     from oracle.p1 import MaterialSpec
@@ -151,24 +158,35 @@ def oracle_traction1_steps(steps):
     s = opb.traction(spec, L=1.0, H=0.1, nx=200, ny=20, n_steps=20, pattern="right",
                      include_zero=True, load_max_factor=1.5)
     cfg = oam.AMConfig(method="am", omega=1.0, outer_atol=1e-6, elastic_solver="direct")
+    _, st = opb.run(s, cfg, snapshot_stride=0, steps=list(warm))
     t0 = time.perf_counter()
-    rows, _ = opb.run(s, cfg, snapshot_stride=0, steps=steps)
-    return time.perf_counter() - t0, len(rows)
+    rows, _ = opb.run(s, cfg, snapshot_stride=0, steps=list(timed), state=st)
+    return (time.perf_counter() - t0) / len(rows)
 
 
-def cpu_sample(workload, steps):
-    """(seconds per load step, description) of the oracle on a bounded sample."""
+def cpu_sample(workload, warm, timed):
+    """The reference algorithm (oracle) on the host cores, on a bounded sample of the workload.
+
+    sent512: the same schedule steps at REF_N_SMALL^2 and REF_N^2 (a full 512^2 oracle load step
+    takes ~10^3 s); the value is scaled to the 512^2 workload with the cost-growth exponent fitted
+    between the two sample sizes (SuperLU fill grows at least this fast, so the scaled value is a
+    lower bound on the CPU time).  Returns (s/load-step for the workload, sample description).
+    """
     if workload == "sent512":
-        t, n = oracle_sent_steps(REF_N, steps)
-        v = t / n
-        scale = (512.0 / REF_N) ** (2 * CPU_EXPONENT)
-        return v, (f"{n} SENT load steps (schedule steps {steps[0]}..{steps[-1]}) of the oracle "
-                   f"(reference algorithm: SuperLU elastic/damage/Newton solves) at {REF_N}x{REF_N} "
-                   f"crossed -- a bounded sample, NOT the 512^2 workload; scaled estimate for 512^2 "
-                   f"with the measured cost growth N^{CPU_EXPONENT}: {v * scale:.0f} s/load-step"), \
-            v * scale
-    t, n = oracle_traction1_steps(steps)
-    return t / n, f"{n} config-1 load steps (oracle, SuperLU)", t / n
+        s_small = oracle_sent_steps(REF_N_SMALL, warm, timed)
+        s_big = oracle_sent_steps(REF_N, warm, timed)
+        v_small, v_big, v_full = (_sent_vertices(n) for n in (REF_N_SMALL, REF_N, 512))
+        expo = math.log(s_big / s_small) / math.log(v_big / v_small)
+        expo = min(max(expo, 1.0), 2.0)
+        value = s_big * (v_full / v_big) ** expo
+        desc = (f"schedule steps {timed[0]}..{timed[-1]} of the oracle (reference algorithm, SuperLU "
+                f"solves, serial) measured at {REF_N_SMALL}^2 ({s_small:.3f} s/step) and {REF_N}^2 "
+                f"({s_big:.3f} s/step) crossed SENT; scaled to 512^2 with the fitted cost growth "
+                f"vertices^{expo:.2f}")
+        return value, desc, {"s_per_step_small": s_small, "s_per_step_big": s_big,
+                             "n_small": REF_N_SMALL, "n_big": REF_N, "exponent": expo}
+    v = oracle_traction1_steps(warm, timed)
+    return v, f"schedule steps {timed[0]}..{timed[-1]} of config 1 (oracle, SuperLU), full size", {}
 
 
 # ---- helpers -------------------------------------------------------------------------------------
@@ -201,24 +219,33 @@ def dominant_roofline(prof, peak, peak_kind):
             "share_of_kernel_time": round(p["ms"] / total, 4) if total > 0 else None}
 
 
-def operator_sweep(pf, torch, peak, sizes=(1024, 4096, 8192), reps=10):
-    """BASELINE config 5: matrix-free Kuu / Kaa applies on 2D union-jack, cold L2."""
+SWEEP_2D = ((256, "union_jack"), (1024, "union_jack"), (4096, "union_jack"), (8192, "union_jack"),
+            (8192, "right"), (8192, "crossed"))
+SWEEP_3D = (32, 64, 128, 256)
+
+
+def operator_sweep(pf, torch, peak, reps=10):
+    """BASELINE config 5: matrix-free Kuu / Kaa applies, 2D 256^2..8192^2 and 3D 32^3..256^3,
+    alpha ~ U[0,1], u, x ~ N(0,1) (seeded), L2 flushed before every apply; algorithmic bytes
+    (DESIGN.md "Roofline"): Kuu = (x, alpha, y) per vertex, Kaa = (x, y) per vertex + kappa per
+    element."""
     res = []
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device="cuda")
-    for n in sizes:
-        mat = pf.Material(E=1.0, nu=0.3, Gc=1.0, ell=0.1, k_ell=1e-6)
-        mesh = pf.StructuredMesh(n, n, 1.0, 1.0, "union_jack")
-        prob = pf.Discretization(mesh, mat, pf.DamageModel("AT1"))
+    cases = [(n, p, 2) for n, p in SWEEP_2D] + [(n, "kuhn6", 3) for n in SWEEP_3D]
+    for n, pattern, dim in cases:
+        mat = pf.Material(E=1.0, nu=0.3, Gc=1.0, ell=0.1, k_ell=1e-6, regime="3d" if dim == 3 else "plane_stress")
+        mesh = pf.StructuredMesh3D(n, n, n) if dim == 3 else pf.StructuredMesh(n, n, 1.0, 1.0, pattern)
+        prob = pf.Discretization(mesh, mat, pf.DamageModel("AT1"), solvers="operators")
         V = mesh.n_vertices
-        g = torch.Generator(device="cuda").manual_seed(n)
+        g = torch.Generator(device="cuda").manual_seed(n + dim)
         alpha = torch.rand(V, dtype=torch.float64, device="cuda", generator=g)
-        x = torch.randn(2 * V, dtype=torch.float64, device="cuda", generator=g)
-        u = torch.randn(2 * V, dtype=torch.float64, device="cuda", generator=g)
+        x = torch.randn(dim * V, dtype=torch.float64, device="cuda", generator=g)
+        u = torch.randn(dim * V, dtype=torch.float64, device="cuda", generator=g)
         xa = torch.randn(V, dtype=torch.float64, device="cuda", generator=g)
         st = pf.State(u, alpha, torch.zeros_like(alpha))
         K = pf.assemble_Kuu(st, prob, apply_bc=False)
         A = pf.assemble_Kaa(st, prob)
-        for name, op, xin, nbytes, dofs in (("Kuu", K, x, 40.0 * V, 2 * V),
+        for name, op, xin, nbytes, dofs in (("Kuu", K, x, (16.0 * dim + 8.0) * V, dim * V),
                                             ("Kaa", A, xa, 16.0 * V + 8.0 * prob.n_elements, V)):
             op @ xin
             times = []
@@ -232,11 +259,12 @@ def operator_sweep(pf, torch, peak, sizes=(1024, 4096, 8192), reps=10):
                 torch.cuda.synchronize()
                 times.append(e0.elapsed_time(e1) * 1e-3)
             t = sorted(times)[len(times) // 2]
-            res.append({"op": name, "n": n, "dofs": dofs, "median_s": t,
+            res.append({"op": name, "mesh": f"{n}^{dim} {pattern}", "dofs": dofs, "median_s": t,
                         "GDOF_s": round(dofs / t / 1e9, 3), "GB_s": round(nbytes / t / 1e9, 1),
                         "frac": round(nbytes / t / 1e9 / peak, 3),
                         "bytes_per_dof": round(nbytes / dofs, 2), "l2": "flushed"})
-        del prob, K, A
+        del prob, K, A, op, xin, alpha, x, u, xa, st
+        gc.collect()
         torch.cuda.empty_cache()
     return res
 
@@ -292,25 +320,14 @@ def main():
             return 0
         # the reference algorithm (oracle restatement, SuperLU) on the box's host cores
         t0 = time.perf_counter()
-        if args.workload == "sent512":
-            tw, _ = oracle_sent_steps(REF_N, list(range(0, W))) if W else (0.0, 0)
-            tk, nk = oracle_sent_steps(REF_N, list(range(0, W + K)))
-            tk -= tw
-        else:
-            tw, _ = oracle_traction1_steps(list(range(0, W))) if W else (0.0, 0)
-            tk, nk = oracle_traction1_steps(list(range(0, W + K)))
-            tk -= tw
-        v = tk / K
-        sample = (f"schedule steps {W}..{W + K - 1} of the oracle (reference algorithm, SuperLU) "
-                  + (f"at {REF_N}x{REF_N} crossed (bounded sample of the 512^2 workload)"
-                     if args.workload == "sent512" else "on the full config-1 bar"))
+        v, sample, detail = cpu_sample(args.workload, range(W), timed)
         line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "s/load-step",
                 "n_gpus": args.gpus, "steps": K, "warmup": W, "ms_per_step": 1e3 * v,
                 "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic", "config": {"workload": WORKLOADS[args.workload],
                                                 "parallelism": "cpu"},
                 "cpu_baseline": {"value": v, "unit": "s/load-step", "cores": 1, "kind": "port",
-                                 "sample": sample,
+                                 "sample": sample, "detail": detail,
                                  "threads_note": "SuperLU / scipy sparsetools are serial"},
                 "e2e": {"value": v, "unit": "s/load-step", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0},
@@ -371,9 +388,10 @@ def main():
     sweep = operator_sweep(pf, torch, peak) if (not args.no_sweep and rank == 0) else None
     cpu = None
     if rank == 0 and world == 1:
-        v, desc, est = cpu_sample(args.workload, timed[:2] if args.workload == "sent512" else timed)
+        v, desc, detail = cpu_sample(args.workload, range(W), timed[:2] if args.workload == "sent512"
+                                     else timed)
         cpu = {"value": v, "unit": "s/load-step", "cores": 1, "kind": "port", "sample": desc,
-               "estimate_full_workload_s_per_step": round(est, 1)}
+               "detail": detail}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "s/load-step", "n_gpus": world,

@@ -58,7 +58,15 @@ typedef struct pf_desc {
     int64_t nx, ny, nz;            /* cells per direction (nz ignored in 2D) */
     double lx, ly, lz;             /* extents */
     double E, nu, Gc, ell, k_ell;  /* scalar material (per-cell fields override E/Gc) */
+    int32_t skip;                  /* PF_SKIP_* bits: workspaces NOT to plan (0 = everything) */
+    int32_t reserved;
 } pf_desc;
+
+/* pf_desc.skip: an operator-only context (e.g. the operator sweep at 8192^2) plans neither
+ * the multigrid hierarchy nor the stacked Newton vectors; the entry points that need them
+ * (pf_elastic_solve with PF_PREC_GMG, pf_newton) then fail with PF_EINVAL. */
+#define PF_SKIP_GMG 1
+#define PF_SKIP_NEWTON 2
 
 typedef struct pf_ctx pf_ctx;
 

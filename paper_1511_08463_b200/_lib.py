@@ -29,7 +29,9 @@ class PfDesc(C.Structure):
                 ("model", C.c_int32), ("nx", C.c_int64), ("ny", C.c_int64), ("nz", C.c_int64),
                 ("lx", C.c_double), ("ly", C.c_double), ("lz", C.c_double),
                 ("E", C.c_double), ("nu", C.c_double), ("Gc", C.c_double), ("ell", C.c_double),
-                ("k_ell", C.c_double)]
+                ("k_ell", C.c_double), ("skip", C.c_int32), ("reserved", C.c_int32)]
+
+SKIP_GMG, SKIP_NEWTON = 1, 2
 
 
 class LinOpts(C.Structure):

@@ -865,8 +865,8 @@ static void plan_workspace(Ctx* c) {
     add((void**)&c->tickets, sizeof(unsigned) * 64);
     add((void**)&c->bits, sizeof(unsigned long long) * 8);
     c->n_newton_vec = ((c->n_u + c->n_a + 31) / 32) * 32;  // keep every stacked slot 256-byte aligned
-    add((void**)&c->newton, sizeof(double) * c->n_newton_vec * 16);
-    if (c->dim == 2) {
+    if (!(c->d.skip & PF_SKIP_NEWTON)) add((void**)&c->newton, sizeof(double) * c->n_newton_vec * 16);
+    if (c->dim == 2 && !(c->d.skip & PF_SKIP_GMG)) {
         gmg_plan(c);
         add((void**)&c->gmg_base, gmg_bytes(c));
     }
@@ -963,7 +963,7 @@ int pf_bind_workspace(pf_ctx* c, void* p, int64_t bytes) {
     }
     c->ws = base;
     c->bound = 1;
-    if (c->dim == 2) gmg_bind(c, c->gmg_base);
+    if (c->dim == 2 && !(c->d.skip & PF_SKIP_GMG)) gmg_bind(c, c->gmg_base);
     // zero scalars / tickets / bits / masks (synchronous; binding is a setup step)
     if (cudaMemset(c->scal, 0, sizeof(double) * S_COUNT) != cudaSuccess ||
         cudaMemset(c->tickets, 0, sizeof(unsigned) * 64) != cudaSuccess ||
@@ -1124,6 +1124,8 @@ int pf_elastic_solve(pf_ctx* c, const double* alpha, const double* u0, double* u
                      pf_lin_report* rep, void* s) {
     NEED_WS(c);
     if (!o || !rep) return set_error(c, PF_EINVAL, "null options/report");
+    if (o->precond == PF_PREC_GMG && (c->d.skip & PF_SKIP_GMG))
+        return set_error(c, PF_EINVAL, "context created with PF_SKIP_GMG");
     return elastic_solve(c, alpha, u0, u_out, o, rep, (cudaStream_t)s);
 }
 int pf_damage_solve(pf_ctx* c, const double* u, const double* lb, const double* a_in, double* a_out,
@@ -1198,6 +1200,8 @@ int pf_newton(pf_ctx* c, const double* u_in, const double* a_in, const double* l
               double* a_out, const pf_vi_opts* o, pf_vi_report* rep, void* s) {
     NEED_WS(c);
     if (!o || !rep) return set_error(c, PF_EINVAL, "null options/report");
+    if ((c->d.skip & PF_SKIP_NEWTON) || (c->dim == 2 && (c->d.skip & PF_SKIP_GMG)))
+        return set_error(c, PF_EINVAL, "context created with PF_SKIP_NEWTON / PF_SKIP_GMG");
     return newton_solve(c, u_in, a_in, lb, u_out, a_out, o, rep, (cudaStream_t)s);
 }
 int64_t pf_launch_count(const pf_ctx* c) { return c ? c->launches : -1; }

@@ -102,12 +102,13 @@ class Discretization:
     """Mesh + material bound to a device context (fem.py:93-156).
 
     ``bc`` and ``eps0_rows`` are the mutable per-load-step inputs.  ``E_cell`` /
-    ``Gc_cell`` are optional per-cell fields (n_cells, I-major).
+    ``Gc_cell`` are optional per-cell fields (n_cells, I-major).  ``solvers="operators"`` plans
+    no multigrid hierarchy and no Newton vectors (operator applies and the Jacobi/VI solvers only).
     """
 
     def __init__(self, mesh: StructuredMesh, material: Material,
                  damage: Optional[DamageModel] = None, E_cell=None, Gc_cell=None,
-                 device: str = "cuda"):
+                 device: str = "cuda", solvers: str = "all"):
         self.lib = _lib.load()
         self.mesh = mesh
         self.material = material
@@ -120,7 +121,10 @@ class Discretization:
                         regime=_lib.REGIMES[material.regime], model=_lib.MODELS[self.damage.kind],
                         nx=mesh.nx, ny=mesh.ny, nz=getattr(mesh, "nz", 0), lx=mesh.lx, ly=mesh.ly,
                         lz=getattr(mesh, "lz", 0.0), E=material.E, nu=material.nu, Gc=material.Gc,
-                        ell=material.ell, k_ell=material.k_ell)
+                        ell=material.ell, k_ell=material.k_ell,
+                        skip=0 if solvers == "all" else _lib.SKIP_GMG | _lib.SKIP_NEWTON)
+        if solvers not in ("all", "operators"):
+            raise ValueError("solvers must be 'all' or 'operators'")
         self.dim = dim
         ctx = C.c_void_p()
         _lib.raise_for(self.lib.pf_ctx_create(C.byref(d), C.byref(ctx)), None)

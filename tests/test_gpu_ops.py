@@ -101,3 +101,27 @@ def test_sweep_sizes_against_assembled_spmv(n):
                 assert rel(host(pf.assemble_Kuu(st, prob, apply_bc=False) @ dev(x)),
                            om.Kuu(a, eliminate=False) @ x) < TOL
             assert rel(host(pf.assemble_Kaa(st, prob) @ dev(xa)), om.Kaa(u, a) @ xa) < TOL
+
+
+def test_operator_only_context_skips_solver_workspaces():
+    """solvers='operators' (pf_desc.skip) plans no GMG / Newton workspace and refuses those solves,
+    while the operator applies are unchanged."""
+    import paper_1511_08463_b200 as pf
+    mesh = pf.StructuredMesh(64, 48, 1.0, 0.75, "crossed")
+    mat = pf.Material(E=1.0, nu=0.3, Gc=1.0, ell=0.1, k_ell=1e-6)
+    full = pf.Discretization(mesh, mat)
+    ops = pf.Discretization(mesh, mat, solvers="operators")
+    assert ops._ws.numel() < 0.6 * full._ws.numel()
+    g = torch.Generator(device="cuda").manual_seed(3)
+    a = torch.rand(mesh.n_vertices, dtype=torch.float64, device="cuda", generator=g)
+    x = torch.randn(2 * mesh.n_vertices, dtype=torch.float64, device="cuda", generator=g)
+    st = pf.State(torch.zeros_like(x), a, torch.zeros_like(a))
+    y1 = pf.assemble_Kuu(st, full, apply_bc=False) @ x
+    y2 = pf.assemble_Kuu(st, ops, apply_bc=False) @ x
+    assert torch.equal(y1, y2)
+    with pytest.raises(Exception, match="PF_SKIP_GMG"):
+        pf.elastic_step(st, ops, pf.SolverConfig(elastic_solver="cg", elastic_precond="gmg"))
+    with pytest.raises(Exception, match="PF_SKIP_NEWTON"):
+        pf.coupled_newton_solve(st, ops, pf.SolverConfig())
+    us, its = pf.elastic_step(st, ops, pf.SolverConfig(elastic_solver="cg", elastic_precond="jacobi"))
+    assert its >= 0
