@@ -4,7 +4,7 @@ import subprocess
 import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SRC = ["pf_core.cu", "pf_ops2d.cu", "pf_ops3d.cu", "pf_gmg.cu", "pf_newton.cu"]
+SRC = ["pf_core.cu", "pf_ops2d.cu", "pf_ops3d.cu", "pf_gmg.cu", "pf_gmg3.cu", "pf_newton.cu"]
 LIB = os.path.join(HERE, "libphasefrac_b200.so")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"]

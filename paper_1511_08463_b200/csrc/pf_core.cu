@@ -425,7 +425,8 @@ int pcg_run(Ctx* c, int kind, const PcgBuffers& B, const double* coef, const uns
     PF_CU(c, cudaGetLastError(), "cg init");
     if (gmg) {
         bool rzd = false;
-        PF_TRY(gmg_vcycle(c, B.r, B.z, st, c->scal, false, 1, &rzd));
+        if (c->dim == 3) PF_TRY(gmg3_vcycle(c, B.r, B.z, st, c->scal));
+        else PF_TRY(gmg_vcycle(c, B.r, B.z, st, c->scal, false, 1, &rzd));
         if (!rzd) {
             k_cg_rz<<<vb, kVecBlock, 0, st>>>(B.n, B.r, B.z, c->scal, rb, 1);
             c->launches++;
@@ -436,6 +437,18 @@ int pcg_run(Ctx* c, int kind, const PcgBuffers& B, const double* coef, const uns
     auto issue_iter = [&](long long k, cudaStream_t s) -> int {
         double* pin = (k & 1) ? B.p1 : B.p0;
         double* pout = (k & 1) ? B.p0 : B.p1;
+        if (gmg && c->dim == 3) {  // 3D: plain PCG update, V-cycle, r.z
+            PF_TRY(launch_Kuu_cgA(c, coef, B.z, pin, pout, B.q, s));
+            const int ps = prof_begin(c, s);
+            k_cg_update_nz<<<vb, kVecBlock, 0, s>>>(B.n, B.x, B.r, pout, B.q, c->scal, rb);
+            prof_end(c, s, ps, K_CG_VEC, 8.0 * B.n * 6);
+            PF_TRY(gmg3_vcycle(c, B.r, B.z, s, c->scal));
+            const int ps2 = prof_begin(c, s);
+            k_cg_rz<<<vb, kVecBlock, 0, s>>>(B.n, B.r, B.z, c->scal, rb, 0);
+            prof_end(c, s, ps2, K_CG_VEC, 8.0 * B.n * 2);
+            c->launches += 2;
+            return PF_OK;
+        }
         if (gmg) {
             PF_TRY(launch_Kuu_cgA(c, coef, B.z, pin, pout, B.q, s));
             const GLevel& L0 = c->glev[0];
@@ -567,7 +580,6 @@ int elastic_solve(Ctx* c, const double* alpha, const double* u0, double* u_out, 
     if (o->precond != PF_PREC_JACOBI && o->precond != PF_PREC_GMG)
         return set_error(c, PF_EINVAL, "elastic solve: unknown preconditioner");
     const bool gmg = o->precond == PF_PREC_GMG;
-    if (gmg && c->dim == 3) return set_error(c, PF_EINVAL, "GMG is built for 2D meshes only in this version");
     PF_CU(c, cudaMemcpyAsync(c->alpha_ws, alpha, sizeof(double) * c->n_a, cudaMemcpyDeviceToDevice, st),
           "alpha copy");
     PcgBuffers B{c->cg_x, c->cg_r, c->cg_z, c->cg_p0, c->cg_p1, c->cg_q, c->cg_dinv, c->cg_b, c->n_u};
@@ -577,7 +589,7 @@ int elastic_solve(Ctx* c, const double* alpha, const double* u0, double* u_out, 
         reused = o->gmg_reuse && c->gmg_built && deg == c->gmg_degree;
         c->gmg_degree = deg;
         if (!reused) {
-            PF_TRY(gmg_setup(c, st));
+            PF_TRY(c->dim == 3 ? gmg3_setup(c, st) : gmg_setup(c, st));
             c->gmg_built = 1;
             c->gmg_its0 = -1;
         }
@@ -593,7 +605,7 @@ int elastic_solve(Ctx* c, const double* alpha, const double* u0, double* u_out, 
                      o->check_every > 0 ? o->check_every : (gmg ? 2 : 8), rep, st);
     if (reused && (rc == PF_EBREAKDOWN || (rc == PF_OK && !rep->converged))) {
         // the kept hierarchy no longer preconditions this alpha: rebuild and solve again
-        PF_TRY(gmg_setup(c, st));
+        PF_TRY(c->dim == 3 ? gmg3_setup(c, st) : gmg_setup(c, st));
         c->gmg_its0 = -1;
         if (warm)
             PF_CU(c, cudaMemcpyAsync(B.x, u0, sizeof(double) * c->n_u, cudaMemcpyDeviceToDevice, st), "u0 copy");
@@ -813,6 +825,12 @@ static void geometry_3d(Ctx* c) {
     g.at2 = d.model == PF_AT2;
     g.cw = g.at2 ? 2.0 : 8.0 / 3.0;
     g.E_cell = nullptr; g.Gc_cell = nullptr; g.has_bc = 0;
+    tile3(g);
+}
+
+// 3D strip tiling: blocks of 14 j-pencils x 30 k-lanes, strips of S vertex rows sized for ~4
+// blocks per SM across the 148 SMs
+void pf::tile3(Geo3& g) {
     g.nbj = (g.nvy + 13) / 14;
     g.nbk = (g.nvz + 29) / 30;
     const long long per = (long long)g.nbj * g.nbk;
@@ -869,6 +887,10 @@ static void plan_workspace(Ctx* c) {
     if (c->dim == 2 && !(c->d.skip & PF_SKIP_GMG)) {
         gmg_plan(c);
         add((void**)&c->gmg_base, gmg_bytes(c));
+    }
+    if (c->dim == 3 && !(c->d.skip & PF_SKIP_GMG)) {
+        gmg3_plan(c);
+        add((void**)&c->gmg3_base, gmg3_bytes(c));
     }
     size_t tot = 0;
     for (auto& e : c->layout) tot += e.second;
@@ -964,6 +986,7 @@ int pf_bind_workspace(pf_ctx* c, void* p, int64_t bytes) {
     c->ws = base;
     c->bound = 1;
     if (c->dim == 2 && !(c->d.skip & PF_SKIP_GMG)) gmg_bind(c, c->gmg_base);
+    if (c->dim == 3 && !(c->d.skip & PF_SKIP_GMG)) gmg3_bind(c, c->gmg3_base);
     // zero scalars / tickets / bits / masks (synchronous; binding is a setup step)
     if (cudaMemset(c->scal, 0, sizeof(double) * S_COUNT) != cudaSuccess ||
         cudaMemset(c->tickets, 0, sizeof(unsigned) * 64) != cudaSuccess ||

@@ -215,6 +215,16 @@ struct GLevel {
     double *x = nullptr, *b = nullptr, *r = nullptr, *d0 = nullptr, *d1 = nullptr, *res = nullptr, *w = nullptr;
 };
 
+// ---- 3D multigrid level (pf_gmg3.cu) ---------------------------------------------------------
+struct G3Level {
+    Geo3 g;                          // level geometry (coarse: 2:1 with the ceil rule)
+    double* alpha = nullptr;         // level damage (coarse: max-pooled)
+    double* E = nullptr;             // per-cell E (coarse: averaged), when the fine level has one
+    unsigned char* mask = nullptr;   // Dirichlet bits (coarse: injected)
+    double* dinv = nullptr;          // 1 / diag(K_l) (3 nv)
+    double *x = nullptr, *b = nullptr, *r = nullptr, *d0 = nullptr, *d1 = nullptr, *res = nullptr, *w = nullptr;
+};
+
 // ---- context -------------------------------------------------------------------------
 struct Ctx {
     pf_desc d;
@@ -251,6 +261,8 @@ struct Ctx {
     Prof prof;
     // multigrid
     std::vector<GLevel> glev;
+    std::vector<G3Level> g3lev;
+    char* gmg3_base = nullptr;
     char* gmg_base = nullptr;
     double* gmg_dense = nullptr;
     double* gmg_ainv = nullptr;
@@ -299,6 +311,10 @@ struct CgScal {  // pointers into the scalar block used by fused CG kernels
 // y = K p_out and pAp reduced into scal (CG step A).
 int launch_Kuu(Ctx* c, const double* alpha, const double* x, double* y, int bcmode,
                cudaStream_t st);
+void tile3(Geo3& g);
+int launch3_Kuu_on(Ctx* c, const Geo3& g, const double* alpha, const double* x, double* y, int bcmode,
+                   cudaStream_t st, int kind);
+int launch3_Kuu_diag_on(Ctx* c, const Geo3& g, const double* alpha, double* dinv, cudaStream_t st, int kind);
 int launch_Kuu_smooth(Ctx* c, int epi, const double* alpha, const double* d, const GmgEpi& e, cudaStream_t st);
 int launch_Kuu_cgA(Ctx* c, const double* alpha, const double* z, const double* p_in,
                    double* p_out, double* q, cudaStream_t st);
@@ -371,6 +387,11 @@ void gmg_plan(Ctx* c);
 size_t gmg_bytes(const Ctx* c);
 void gmg_bind(Ctx* c, char* base);
 int gmg_setup(Ctx* c, cudaStream_t st);
+void gmg3_plan(Ctx* c);
+size_t gmg3_bytes(const Ctx* c);
+void gmg3_bind(Ctx* c, char* base);
+int gmg3_setup(Ctx* c, cudaStream_t st);
+int gmg3_vcycle(Ctx* c, const double* r_in, double* z_out, cudaStream_t st, const double* live);
 int gmg_vcycle(Ctx* c, const double* r_in, double* z_out, cudaStream_t st, const double* live,
                bool cheb0_done = false, int rz_first = -1, bool* rz_done = nullptr);
 int newton_solve(Ctx* c, const double* u_in, const double* a_in, const double* lb, double* u_out,

@@ -123,8 +123,7 @@ static int solve_A(Ctx* c, const double* b, double* out, double rtol, long long&
     double bb;
     NTRY(ndot(c, c->n_u, b, b, S_AUX0, bb, st));
     pf_lin_report rep{};
-    int rc = pcg_run(c, c->dim == 3 ? 0 : 2, B, c->alpha_ws, nullptr, rtol, 0.0, 10 * c->n_u, 1,
-                     c->dim == 3 ? 16 : 2, &rep, st);
+    int rc = pcg_run(c, 2, B, c->alpha_ws, nullptr, rtol, 0.0, 10 * c->n_u, 1, 2, &rep, st);
     its += rep.iterations;
     if (rc != PF_OK) return set_error(c, PF_EINNER, "inner solve on block 'A' failed: " + c->err);
     NCU(c, cudaMemcpyAsync(out, c->cg_x, sizeof(double) * c->n_u, cudaMemcpyDeviceToDevice, st), "copy");
@@ -295,12 +294,9 @@ int newton_solve(Ctx* c, const double* u_in, const double* a_in, const double* l
         NCU(c, cudaMemcpyAsync(w.RHS, w.FX, sizeof(double) * nu, cudaMemcpyDeviceToDevice, st), "copy");
         // Jacobian-dependent setup: GMG hierarchy of Kuu(alpha), kappa(u) and masked diag(Kaa)
         NCU(c, cudaMemcpyAsync(c->alpha_ws, alpha, sizeof(double) * na, cudaMemcpyDeviceToDevice, st), "copy");
-        if (c->dim == 3) NTRY(launch_Kuu_diag(c, c->alpha_ws, c->cg_dinv, st));  // Jacobi inner A (3D)
-        else {
-            NTRY(gmg_setup(c, st));
-            c->gmg_built = 1;  // an elastic solve that follows may keep it (gmg_reuse)
-            c->gmg_its0 = -1;
-        }
+        NTRY(c->dim == 3 ? gmg3_setup(c, st) : gmg_setup(c, st));
+        c->gmg_built = 1;  // an elastic solve that follows may keep it (gmg_reuse)
+        c->gmg_its0 = -1;
         NTRY(launch_kappa(c, u, alpha, c->kappa, c->vi_c, st));
         NTRY(launch_Kaa_diag(c, c->kappa, c->da_dinv, c->act, st));
         bool ok = false;

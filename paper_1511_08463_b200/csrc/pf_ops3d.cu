@@ -850,8 +850,7 @@ struct Op3Jac : NoRed3 {
 
 // ---- launch plumbing -----------------------------------------------------------------------------
 template <class Op>
-static int run3(Ctx* c, Op op, cudaStream_t st, int kind, double bytes) {
-    const Geo3& g = c->g3;
+static int run3g(Ctx* c, const Geo3& g, Op op, cudaStream_t st, int kind, double bytes) {
     constexpr int smem = kW3 * Op::PD * (Op::SV + Op::SC) * 256 + kW3 * Op::NV * 32 * 8 +
                          kW3 * 2 * Op::NC * 32 * 8;
     static_assert(smem <= 227 * 1024, "3D stage ring exceeds shared memory");
@@ -869,7 +868,24 @@ static int run3(Ctx* c, Op op, cudaStream_t st, int kind, double bytes) {
     c->launches++;
     return check_cuda(c, cudaGetLastError(), "3D strip kernel launch");
 }
+template <class Op>
+static int run3(Ctx* c, Op op, cudaStream_t st, int kind, double bytes) {
+    return run3g(c, c->g3, op, st, kind, bytes);
+}
 static RedBuf rb3(Ctx* c) { return RedBuf{c->partials, c->tickets, c->scal}; }
+
+// operators on an explicit (e.g. coarse multigrid level) geometry
+int launch3_Kuu_on(Ctx* c, const Geo3& g, const double* alpha, const double* x, double* y, int bcmode,
+                   cudaStream_t st, int kind) {
+    Op3Kuu<false> op{alpha, x, nullptr, nullptr, y, bcmode, c->scal, rb3(c), 0.0};
+    return run3g(c, g, op, st, kind, 56.0 * g.nv);
+}
+int launch3_Kuu_diag_on(Ctx* c, const Geo3& g, const double* alpha, double* dinv, cudaStream_t st, int kind) {
+    Op3KuuDiag op;
+    op.alpha = alpha;
+    op.dinv = dinv;
+    return run3g(c, g, op, st, kind, 32.0 * g.nv);
+}
 
 int launch3_Kuu(Ctx* c, const double* alpha, const double* x, double* y, int bcmode, cudaStream_t st) {
     Op3Kuu<false> op{alpha, x, nullptr, nullptr, y, bcmode, c->scal, rb3(c), 0.0};

@@ -114,3 +114,44 @@ def test_traction3d_config4_shape_run_matches_oracle():
         for k in range(3):
             assert abs(r.energy[k] - o.energy[k]) <= 1e-6 * abs(o.energy[k]) + 1e-14, (r.step, k)
         assert np.max(np.abs(r.alpha - o.alpha)) < 1e-4
+
+
+@pytest.mark.parametrize("shape", [(12, 10, 14), (7, 5, 9), (16, 16, 16)], ids=lambda s: "x".join(map(str, s)))
+def test_gmg3_elastic_step_matches_oracle(shape):
+    """3D multigrid-PCG (pf_gmg3.cu) converges to the oracle's direct elastic solution, in fewer
+    iterations than Jacobi-PCG; odd sizes exercise the ceil-rule coarsening."""
+    import paper_1511_08463_b200 as pf
+    prob, om, rng = make3(*shape, model="AT1")
+    nv = om.nv
+    lb = rng.uniform(0, 0.3, nv)
+    a = lb + rng.uniform(0, 1, nv) * (1 - lb)
+    a[rng.uniform(size=nv) < 0.05] = 1.0  # crack-like spots: a = k_ell there
+    u = 0.3 * rng.standard_normal(3 * nv)
+    st = pf.State(dev(u), dev(a), dev(lb))
+    ou, _ = oam.elastic_half_step(oam.LoadState(u, a, lb), om, oam.AMConfig())
+    ug, kg = pf.elastic_step(st, prob, pf.SolverConfig(elastic_solver="cg", elastic_rtol=1e-12,
+                                                       elastic_precond="gmg", gmg_reuse=False))
+    uj, kj = pf.elastic_step(st, prob, pf.SolverConfig(elastic_solver="cg", elastic_rtol=1e-12,
+                                                       elastic_precond="jacobi"))
+    assert rel(host(ug), ou) < 1e-8 and rel(host(uj), ou) < 1e-8
+    assert kg < kj, (kg, kj)
+
+
+def test_traction3d_config4_shape_gmg_matches_oracle():
+    """Config-4 physics through the 3D multigrid path (elastic half-steps and Newton's A block)."""
+    import paper_1511_08463_b200 as pf
+    from oracle import problems as opb
+    n, steps = 8, 6
+    mat = pf.Material(E=1.0, nu=0.3, Gc=1.0, ell=0.3, k_ell=1e-6, regime="3d")
+    setup = pf.setup_traction3d(n=n, n_steps=steps, material=mat)
+    spec = MaterialSpec(E=1.0, nu=0.3, Gc=1.0, ell=0.3, k_ell=1e-6, model="AT1", regime="3d")
+    osetup = opb.traction3d(n=n, spec=spec, n_steps=steps)
+    cfg = pf.SolverConfig(method="oram_newton", omega=1.7, outer_atol=1e-9, elastic_solver="cg",
+                          elastic_rtol=1e-12, elastic_precond="gmg")
+    recs = pf.run_quasistatic(setup, cfg)
+    orows, _ = opb.run(osetup, oam.AMConfig(method="oram_newton", omega=1.7, outer_atol=1e-9))
+    assert max(float(np.max(o.alpha)) for o in orows) > 0.05
+    for r, o in zip(recs, orows):
+        for k in range(3):
+            assert abs(r.energy[k] - o.energy[k]) <= 1e-6 * abs(o.energy[k]) + 1e-14, (r.step, k)
+        assert np.max(np.abs(r.alpha - o.alpha)) < 1e-4
