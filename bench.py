@@ -33,6 +33,7 @@ sys.path.insert(0, ROOT)
 METRIC = "fp64 operator-apply GDOF/s & HBM GB/s vs peak; sec per load step (AM+Newton)"
 REF_N = 48          # CPU sample sizes (SENT, crossed), see DESIGN.md "CPU baseline"
 REF_N_SMALL = 32
+REF_N3, REF_N3_SMALL = 10, 6   # CPU sample cubes for config 4
 
 
 def peaks():
@@ -103,6 +104,11 @@ def sent_config(pf):
                            max_am_iterations=2000)
 
 
+def traction3d_config(pf):
+    return pf.SolverConfig(method="oram_newton", omega=1.7, outer_atol=1e-6, elastic_solver="cg",
+                           elastic_rtol=1e-8, elastic_precond="gmg", max_am_iterations=3000)
+
+
 def traction1_setup(pf):
     mat = pf.Material(E=1.0, nu=0.0, Gc=1.0, ell=0.05, k_ell=1e-6)
     return pf.setup_traction(mat, L=1.0, H=0.1, nx=200, ny=20, n_steps=20, pattern="right",
@@ -120,6 +126,11 @@ WORKLOADS = {
                 "k_ell=1e-6, notch alpha=1 on y=0.5 x<=0.5, bottom clamped, top u_y=t (60 steps to "
                 "6e-3), ORAM omega=1.8 + Newton when |Phi| < 1e-3, GMG-PCG rtol 1e-8, outer_atol "
                 "1e-6; step = one load step"),
+    "traction3d128": ("traction3d128: BASELINE config 4 -- 3D AT1 traction of the unit cube, 128^3 hex "
+                      "cells x 6 Kuhn tets (2,146,689 vertices, 6,440,067 u-dofs), E=1 nu=0.3 ell=0.03 "
+                      "k_ell=1e-6, Gc lognormal(0, 0.1) per cell (seed 0) + one Jacobi smoothing pass, "
+                      "z=0 clamped, z=1 u_z=t (30 steps to 1.5 t_c), ORAM omega=1.7 + Newton, 3D "
+                      "multigrid-PCG rtol 1e-8, outer_atol 1e-6; step = one load step"),
     "traction1": ("traction1: BASELINE config 1 -- 200x20 right-diagonal AT1 bar (E=1, nu=0, Gc=1, "
                   "ell=0.05, k=1e-6), t in linspace(0,1.5t_c,20), AM omega=1, atol 1e-6; step = one "
                   "load step"),
@@ -129,6 +140,8 @@ WORKLOADS = {
 def make_workload(pf, name):
     if name == "sent512":
         return pf.setup_sent(n=512), sent_config(pf)
+    if name == "traction3d128":
+        return pf.setup_traction3d(n=128), traction3d_config(pf)
     return traction1_setup(pf), traction1_config(pf)
 
 
@@ -144,6 +157,17 @@ def oracle_sent_steps(n, warm, timed):
     s = opb.sent(n=n)
     cfg = oam.AMConfig(method="oram_newton", omega=1.8, outer_atol=1e-6, am_switch_atol=1e-3,
                        max_am_iterations=2000)
+    _, st = opb.run(s, cfg, snapshot_stride=0, steps=list(warm))
+    t0 = time.perf_counter()
+    rows, _ = opb.run(s, cfg, snapshot_stride=0, steps=list(timed), state=st)
+    return (time.perf_counter() - t0) / len(rows)
+
+
+def oracle_traction3d_steps(n, warm, timed):
+    from oracle import am as oam
+    from oracle import problems as opb
+    s = opb.traction3d(n=n)
+    cfg = oam.AMConfig(method="oram_newton", omega=1.7, outer_atol=1e-6, max_am_iterations=3000)
     _, st = opb.run(s, cfg, snapshot_stride=0, steps=list(warm))
     t0 = time.perf_counter()
     rows, _ = opb.run(s, cfg, snapshot_stride=0, steps=list(timed), state=st)
@@ -185,6 +209,17 @@ def cpu_sample(workload, warm, timed):
                 f"vertices^{expo:.2f}")
         return value, desc, {"s_per_step_small": s_small, "s_per_step_big": s_big,
                              "n_small": REF_N_SMALL, "n_big": REF_N, "exponent": expo}
+    if workload == "traction3d128":
+        s_small = oracle_traction3d_steps(REF_N3_SMALL, warm, timed)
+        s_big = oracle_traction3d_steps(REF_N3, warm, timed)
+        v_small, v_big, v_full = ((n + 1) ** 3 for n in (REF_N3_SMALL, REF_N3, 128))
+        expo = min(max(math.log(s_big / s_small) / math.log(v_big / v_small), 1.0), 2.0)
+        value = s_big * (v_full / v_big) ** expo
+        desc = (f"schedule steps {timed[0]}..{timed[-1]} of the oracle (reference algorithm, SuperLU, "
+                f"serial) measured at {REF_N3_SMALL}^3 ({s_small:.3f} s/step) and {REF_N3}^3 "
+                f"({s_big:.3f} s/step); scaled to 128^3 with the fitted growth vertices^{expo:.2f}")
+        return value, desc, {"s_per_step_small": s_small, "s_per_step_big": s_big,
+                             "n_small": REF_N3_SMALL, "n_big": REF_N3, "exponent": expo}
     v = oracle_traction1_steps(warm, timed)
     return v, f"schedule steps {timed[0]}..{timed[-1]} of config 1 (oracle, SuperLU), full size", {}
 
@@ -310,7 +345,7 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    nsched = 60 if args.workload == "sent512" else 20
+    nsched = {"sent512": 60, "traction3d128": 30}.get(args.workload, 20)
     W = max(0, min(args.warmup, nsched - 1))
     K = max(1, min(args.steps, nsched - W))
     timed = list(range(W, W + K))
@@ -388,7 +423,7 @@ def main():
     sweep = operator_sweep(pf, torch, peak) if (not args.no_sweep and rank == 0) else None
     cpu = None
     if rank == 0 and world == 1:
-        v, desc, detail = cpu_sample(args.workload, range(W), timed[:2] if args.workload == "sent512"
+        v, desc, detail = cpu_sample(args.workload, range(W), timed[:2] if args.workload != "traction1"
                                      else timed)
         cpu = {"value": v, "unit": "s/load-step", "cores": 1, "kind": "port", "sample": desc,
                "detail": detail}
