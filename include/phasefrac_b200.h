@@ -186,6 +186,13 @@ int pf_relax_u(pf_ctx* ctx, const double* u_prev, const double* u_star, double o
 int pf_relax_alpha(pf_ctx* ctx, const double* a_prev, const double* a_star,
                    const double* alpha_lb, double omega, double* alpha_out, double* out,
                    void* stream);
+/* The AM iteration tail in one sweep (north_star part 4): pf_relax_alpha fused with the physics
+ * pass of the relaxed state (solver.py:202-219).  phys_out (HOST, 8) as pf_physics with
+ * PF_ROWS_ZERO: [E_el, E_d, E_tot, |r_u|^2, |Phi_a|^2, |Phi|, 0, 0]; relax_out (HOST, 3) as
+ * pf_relax_alpha.  2D: one relaxation-bits launch + one fused strip pass; 3D: two passes. */
+int pf_relax_alpha_physics(pf_ctx* ctx, const double* u, const double* a_prev, const double* a_star,
+                           const double* alpha_lb, double omega, double* alpha_out,
+                           double* phys_out, double* relax_out, void* stream);
 /* u[bc] = ubar (solver.py:121-123). */
 int pf_snap_bc(pf_ctx* ctx, double* u, void* stream);
 /* coupled_newton_solve (solver.py:303-330): reduced-space active-set Newton on (u, alpha)

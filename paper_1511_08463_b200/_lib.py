@@ -86,6 +86,7 @@ EXPORTS = {
     "pf_relax_u": (C.c_int, [C.c_void_p] * 3 + [C.c_double, C.c_void_p, C.c_void_p]),
     "pf_relax_alpha": (C.c_int, [C.c_void_p] * 4 + [C.c_double, C.c_void_p, C.c_void_p,
                                                      C.c_void_p]),
+    "pf_relax_alpha_physics": (C.c_int, [C.c_void_p] * 5 + [C.c_double] + [C.c_void_p] * 4),
     "pf_snap_bc": (C.c_int, [C.c_void_p] * 3),
     "pf_newton": (C.c_int, [C.c_void_p] * 6 + [C.POINTER(VIOpts), C.POINTER(VIReport),
                                                 C.c_void_p]),

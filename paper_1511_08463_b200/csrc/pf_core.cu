@@ -248,21 +248,6 @@ __global__ void k_relax_bits(long long n, const double* __restrict__ ap, const d
     if ((threadIdx.x & 31) == 0 && (lo | hi)) atomicOr(bits, ((unsigned long long)hi << 32) | lo);
 }
 
-__device__ __forceinline__ void choose_omega(double omega, unsigned long long bits, double& wb, int& kk,
-                                             bool& use_star) {
-    // first feasible k in 0..59 with (k == 0 or w_k != 1); else the unrelaxed update
-    double w = omega;
-    use_star = true;
-    wb = 1.0;
-    kk = 60;
-    if (omega == 1.0) { kk = 0; return; }
-    for (int k = 0; k < 60; ++k) {
-        if (k > 0 && w == 1.0) { kk = k; return; }
-        if (!((bits >> k) & 1ull)) { wb = w; kk = k; use_star = false; return; }
-        w = 0.5 * (1.0 + w);
-    }
-}
-
 __global__ void k_relax_apply(long long n, const double* __restrict__ ap, const double* __restrict__ as,
                               const double* __restrict__ lb, double omega, const unsigned long long* bits,
                               double* __restrict__ out, unsigned long long* dmax, double* s) {
@@ -1216,6 +1201,47 @@ int pf_relax_alpha(pf_ctx* c, const double* a_prev, const double* a_star, const 
         out[0] = c->h_scal[S_OMEGABAR];
         out[1] = dmax;
         out[2] = c->h_scal[S_AUX1];
+    }
+    return PF_OK;
+}
+// AM tail fused (north_star part 4): alpha = P[alpha_prev + w_bar (alpha* - alpha_prev)] with the
+// midpoint-backtracked w_bar (solver.py:202-216) applied while staging the physics pass, which then
+// reduces energies, |r_u|, |Phi| and |d alpha|_inf of the relaxed state in the same sweep.
+int pf_relax_alpha_physics(pf_ctx* c, const double* u, const double* a_prev, const double* a_star,
+                           const double* lb, double omega, double* a_out, double* phys_out, double* relax_out,
+                           void* s) {
+    NEED_WS(c);
+    cudaStream_t st = (cudaStream_t)s;
+    if (c->dim == 3) {  // 3D: the relaxation and the physics pass as two launches
+        PF_TRY(pf_relax_alpha(c, a_prev, a_star, lb, omega, a_out, relax_out, s));
+        return pf_physics(c, u, a_out, lb, nullptr, nullptr, nullptr, PF_ROWS_ZERO, phys_out, s);
+    }
+    const long long n = c->n_a;
+    PF_CU(c, cudaMemsetAsync(c->bits, 0, sizeof(unsigned long long) * 8, st), "memset");
+    if (omega != 1.0) {
+        k_relax_bits<<<vec_blocks(n), kVecBlock, 0, st>>>(n, a_prev, a_star, lb, omega, c->bits);
+        c->launches++;
+    }
+    PF_TRY(launch_physics_relax(c, u, a_prev, a_star, lb, omega, a_out, st));
+    PF_CU(c, cudaMemcpyAsync(c->h_scal, c->scal, sizeof(double) * S_COUNT, cudaMemcpyDeviceToHost, st), "scal");
+    PF_CU(c, cudaMemcpyAsync(c->h_scal + 200, c->bits + 1, sizeof(double), cudaMemcpyDeviceToHost, st), "d");
+    PF_CU(c, cudaStreamSynchronize(st), "sync");
+    const double* h = c->h_scal + S_PHYS0;
+    if (phys_out) {
+        phys_out[0] = h[0];
+        phys_out[1] = h[1];
+        phys_out[2] = h[0] + h[1];
+        phys_out[3] = h[2];
+        phys_out[4] = h[3];
+        phys_out[5] = std::sqrt(h[2] + h[3]);
+        phys_out[6] = phys_out[7] = 0.0;
+    }
+    if (relax_out) {
+        double dmax;
+        memcpy(&dmax, c->h_scal + 200, sizeof(double));
+        relax_out[0] = c->h_scal[S_OMEGABAR];
+        relax_out[1] = dmax;
+        relax_out[2] = c->h_scal[S_AUX1];
     }
     return PF_OK;
 }

@@ -181,6 +181,22 @@ __device__ __forceinline__ double2 bmul(const double* Dinv, long long nv, long l
                         __ldg(Dinv + 2 * nv + v) * r0 + __ldg(Dinv + 3 * nv + v) * r1);
 }
 
+// ---- over-relaxation: first feasible midpoint candidate (solver.py:202-216) ---------------------
+__device__ __forceinline__ void choose_omega(double omega, unsigned long long bits, double& wb, int& kk,
+                                             bool& use_star) {
+    // first feasible k in 0..59 with (k == 0 or w_k != 1); else the unrelaxed update
+    double w = omega;
+    use_star = true;
+    wb = 1.0;
+    kk = 60;
+    if (omega == 1.0) { kk = 0; return; }
+    for (int k = 0; k < 60; ++k) {
+        if (k > 0 && w == 1.0) { kk = k; return; }
+        if (!((bits >> k) & 1ull)) { wb = w; kk = k; use_star = false; return; }
+        w = 0.5 * (1.0 + w);
+    }
+}
+
 // ---- GMG fine-level smoother epilogues fused into the Kuu strip kernel (pf_ops2d.cu) -----------
 enum {
     EPI_NONE = 0,
@@ -315,6 +331,8 @@ void tile3(Geo3& g);
 int launch3_Kuu_on(Ctx* c, const Geo3& g, const double* alpha, const double* x, double* y, int bcmode,
                    cudaStream_t st, int kind);
 int launch3_Kuu_diag_on(Ctx* c, const Geo3& g, const double* alpha, double* dinv, cudaStream_t st, int kind);
+int launch_physics_relax(Ctx* c, const double* u, const double* a_prev, const double* a_star, const double* lb,
+                         double omega, double* a_out, cudaStream_t st);
 int launch_Kuu_smooth(Ctx* c, int epi, const double* alpha, const double* d, const GmgEpi& e, cudaStream_t st);
 int launch_Kuu_cgA(Ctx* c, const double* alpha, const double* z, const double* p_in,
                    double* p_out, double* q, cudaStream_t st);

@@ -835,15 +835,15 @@ struct OpKaaTrial {
 // Reductions -> scal[S_PHYS0 ..]: E_el, E_d, |r_u|^2, |Phi|^2.
 // vertex slots: u, alpha; cell: E, Gc, [u_c, alpha_c]
 // ================================================================================================
-template <int ROWS>
+template <int ROWS, bool RELAX = false>
 struct OpPhys {
-    static constexpr int NV = 3, NC = 3, MINB = 2;
+    static constexpr int NV = 3, NC = 3, MINB = RELAX ? 1 : 2;
     static constexpr int pd(int) { return 3; }
     static constexpr int ne(int pat) { return 2 + 3 * crossed(pat); }
-    static constexpr int sv(int) { return 3; }
-    static constexpr int sc(int pat) { return 2 + 3 * crossed(pat); }
+    static constexpr int sv(int) { return RELAX ? 5 : 3; }
+    static constexpr int sc(int pat) { return 2 + crossed(pat) * (RELAX ? 5 : 3); }
     const double* u;
-    const double* alpha;
+    const double* alpha;   // RELAX: alpha_prev
     const double* lb;
     double* ru;
     double* ra;
@@ -851,15 +851,33 @@ struct OpPhys {
     double* scal;
     RedBuf rb;
     double eel, ed, nru, nphi;
-    __device__ bool enter() const { return true; }
+    // RELAX (north_star part 4): alpha = P[alpha_prev + w_bar (alpha* - alpha_prev)] formed while
+    // staging, written at owned vertices; |alpha - alpha_prev|_inf max-reduced into bits[1]
+    const double* astar = nullptr;
+    double* aout = nullptr;
+    double omega = 1.0;
+    unsigned long long* bits = nullptr;
+    double wb = 1.0, dmax = 0.0;
+    int kk = 0;
+    bool star = true;
+    __device__ bool enter() {
+        if constexpr (RELAX) choose_omega(omega, bits[0], wb, kk, star);
+        return true;
+    }
+    __device__ __forceinline__ double relaxed(double a0, double as, double l) const {  // k_relax_apply
+        const double cand = star ? as : a0 + wb * (as - a0);
+        return fmin(fmax(cand, l), 1.0);
+    }
     __device__ void issue_v(const Geo2& g, int i, int j, const Slots& s) const {
         const long long id = vid(g, i, j);
         put2(s, 0, u, id);
         put1(s, 2, alpha, id);
+        if (RELAX) { put1(s, 3, astar, id); put1(s, 4, lb, id); }
     }
     __device__ void fix_v(const Geo2&, int, int, const Slots& s, double (&v)[NV]) const {
         const double2 uv = get2(s, 0);
-        v[0] = uv.x; v[1] = uv.y; v[2] = get1(s, 2);
+        v[0] = uv.x; v[1] = uv.y;
+        v[2] = RELAX ? relaxed(get1(s, 2), get1(s, 3), get1(s, 4)) : get1(s, 2);
     }
     template <int PAT>
     __device__ void issue_c(const Geo2& g, int ci, int j, const Slots& s) const {
@@ -870,6 +888,7 @@ struct OpPhys {
             const long long cv = ctr(g, ci, j);
             put2(s, 2, u, cv);
             put1(s, 4, alpha, cv);
+            if (RELAX) { put1(s, 5, astar, cv); put1(s, 6, lb, cv); }
         }
     }
     template <int PAT, int NE>
@@ -878,7 +897,8 @@ struct OpPhys {
         e[1] = getGc(g, s, 1);
         if constexpr (PAT == PF_CROSSED) {
             const double2 uv = get2(s, 2);
-            e[2] = uv.x; e[3] = uv.y; e[4] = get1(s, 4);
+            e[2] = uv.x; e[3] = uv.y;
+            e[4] = RELAX ? relaxed(get1(s, 4), get1(s, 5), get1(s, 6)) : get1(s, 4);
         }
     }
     __device__ __forceinline__ void vertex_out(const Geo2& g, long long id, unsigned m, double r0,
@@ -896,6 +916,10 @@ struct OpPhys {
         }
         if (ru) st2(ru, id, r0, r1);
         if (ra) ra[id] = rav;
+        if (RELAX) {
+            aout[id] = av;
+            dmax = fmax(dmax, fabs(av - __ldg(alpha + id)));
+        }
         nru += r0 * r0 + r1 * r1;
         if (lb) {
             const double ph = fbphi(av - __ldg(lb + id), fbphi(1.0 - av, -rav));
@@ -962,6 +986,17 @@ struct OpPhys {
         vertex_out(g, id, bcbits(g, i, j, id), t[0], t[1], t[2], v[2]);
     }
     __device__ void finish() {
+        if constexpr (RELAX) {
+            double dm = dmax;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) dm = fmax(dm, __shfl_xor_sync(PF_FULL, dm, o));
+            if ((threadIdx.x & 31) == 0 && dm > 0.0)
+                atomicMax(bits + 1, (unsigned long long)__double_as_longlong(dm));
+            if (blockIdx.x == 0 && threadIdx.x == 0) {
+                scal[S_OMEGABAR] = wb;
+                scal[S_AUX1] = (double)kk;
+            }
+        }
         double v[4] = {eel, ed, nru, nphi};
         double* s = scal;
         grid_reduce<4>(v, rb, 2, [s](double* tot) {
@@ -1559,6 +1594,13 @@ int launch_physics(Ctx* c, const double* u, const double* alpha, const double* l
             return run_strip(c, op, st, K_PHYS, nw);
         }
     }
+}
+int launch_physics_relax(Ctx* c, const double* u, const double* a_prev, const double* a_star, const double* lb,
+                         double omega, double* a_out, cudaStream_t st) {
+    OpPhys<PF_ROWS_ZERO, true> op{u, a_prev, lb, nullptr, nullptr, nullptr, c->scal, redbuf(c), 0, 0, 0, 0,
+                                  a_star, a_out, omega, c->bits};
+    // physics (u, alpha) + alpha_prev, alpha*, lb in, alpha out
+    return run_strip(c, op, st, K_PHYS, 0, (double)c->g.nv * (16 + 8 + 8 + 8 + 8 + 8));
 }
 int launch_load(Ctx* c, const double* alpha, double* f, const double* u_or_null, int rows,
                 cudaStream_t st) {

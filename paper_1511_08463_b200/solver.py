@@ -172,6 +172,18 @@ def relax_alpha(a_prev, a_star, alpha_lb, omega, problem: Discretization):
     return out, res[0], res[1]
 
 
+def relax_alpha_and_residual(state: State, a_prev, a_star, omega, problem: Discretization):
+    """Relaxed damage update fused with the residual/energy pass of the relaxed state
+    (solver.py:202-219; north_star part 4) -> (alpha, omega_bar, d_alpha, ||Phi||, EnergyBreakdown)."""
+    from .fem import EnergyBreakdown
+    out = torch.empty_like(a_prev)
+    ph = (C.c_double * 8)()
+    rx = (C.c_double * 3)()
+    problem.call("pf_relax_alpha_physics", _lib.ptr(state.u), _lib.ptr(a_prev), _lib.ptr(a_star),
+                 _lib.ptr(state.alpha_lb), float(omega), _lib.ptr(out), ph, rx, _stream())
+    return out, rx[0], rx[1], ph[5], EnergyBreakdown(ph[0], ph[1], ph[2])
+
+
 def relax_u(u_prev, u_star, omega, problem: Discretization):
     out = torch.empty_like(u_prev)
     problem.call("pf_relax_u", _lib.ptr(u_prev), _lib.ptr(u_star), float(omega), _lib.ptr(out),
@@ -210,11 +222,10 @@ def am_solve(state: State, problem: Discretization, config: SolverConfig,
         a_prev = state.alpha
         a_star, vrep = damage_step(state, problem, config)
         report.total_krylov_iterations += vrep.total_krylov_iterations
-        state.alpha, omega_bar, d_alpha = relax_alpha(a_prev, a_star, state.alpha_lb,
-                                                      config.omega, problem)
+        state.alpha, omega_bar, d_alpha, res, energy = relax_alpha_and_residual(
+            state, a_prev, a_star, config.omega, problem)
         report.omega_bar_min = min(report.omega_bar_min, omega_bar)
 
-        res, energy = residual_and_energy(state, problem)
         report.energy_history.append(energy)
         report.residual_history.append(res)
         if config.log_callback is not None:

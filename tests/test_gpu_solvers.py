@@ -225,3 +225,27 @@ def test_thermal_slab_config3_matches_oracle():
         for k in range(3):
             assert abs(r.energy[k] - o.energy[k]) <= 1e-6 * abs(o.energy[k]) + 1e-14, (r.step, k)
         assert np.max(np.abs(r.alpha - o.alpha)) < 1e-4
+
+
+@pytest.mark.parametrize("pattern", ["union_jack", "right", "crossed"])
+@pytest.mark.parametrize("omega", [1.0, 1.8])
+def test_fused_relax_physics_equals_separate_passes(pattern, omega):
+    """pf_relax_alpha_physics (relaxation applied while staging the physics pass) is bit-identical
+    to pf_relax_alpha followed by pf_physics."""
+    import paper_1511_08463_b200 as pf
+    from paper_1511_08463_b200 import solver as S
+    mesh = pf.StructuredMesh(37, 29, 1.0, 0.8, pattern)
+    prob = pf.Discretization(mesh, pf.Material(E=1.3, nu=0.27, Gc=0.9, ell=0.2, k_ell=1e-6))
+    g = torch.Generator(device="cuda").manual_seed(7)
+    V = mesh.n_vertices
+    lb = 0.3 * torch.rand(V, dtype=torch.float64, device="cuda", generator=g)
+    ap = lb + torch.rand(V, dtype=torch.float64, device="cuda", generator=g) * (1 - lb)
+    ast = torch.clamp(ap + 0.6 * (torch.rand(V, dtype=torch.float64, device="cuda", generator=g) - 0.3), 0, 1)
+    u = 0.1 * torch.randn(2 * V, dtype=torch.float64, device="cuda", generator=g)
+    st = pf.State(u, ap.clone(), lb)
+    a1, wb1, d1 = S.relax_alpha(ap, ast, lb, omega, prob)
+    res1, e1 = S.residual_and_energy(pf.State(u, a1, lb), prob)
+    a2, wb2, d2, res2, e2 = S.relax_alpha_and_residual(st, ap, ast, omega, prob)
+    assert torch.equal(a1, a2)
+    assert (wb1, d1) == (wb2, d2)
+    assert res1 == res2 and tuple(e1) == tuple(e2)

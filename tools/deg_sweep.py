@@ -12,8 +12,8 @@ cfg = pf.SolverConfig(method="oram_newton", omega=1.8, outer_atol=1e-6, am_switc
 st = pf.State.zeros(setup.mesh, setup.initial_alpha_lb)
 pf.run_quasistatic(setup, cfg, snapshot_stride=0, state=st, steps=list(range(10)))
 out = torch.empty_like(st.u)
-for deg in (2, 3, 4, 5):
-    for reuse in (0, 1):
+for deg in [int(x) for x in os.environ.get('DEGS', '2,3,4,5').split(',')]:
+    for reuse in (1,):
         opts = S._lin_opts(cfg, False)
         opts.cheb_degree = deg
         opts.gmg_reuse = reuse

@@ -20,7 +20,7 @@ def main():
     else:
         mesh = pf.StructuredMesh(n, n, 1.0, 1.0, pattern)
         mat = pf.Material(E=1.0, nu=0.3, Gc=1.0, ell=0.1, k_ell=1e-6)
-    prob = pf.Discretization(mesh, mat, pf.DamageModel("AT1"))
+    prob = pf.Discretization(mesh, mat, pf.DamageModel("AT1"), solvers="operators")
     V = mesh.n_vertices
     d = mesh.dim
     g = torch.Generator(device="cuda").manual_seed(1)
