@@ -107,7 +107,9 @@ typedef struct pf_vi_opts {
     int64_t inner_maxit;
     double zero_tol;        /* <= 0 -> 1e-10 (1 + |x0|_inf) as the reference */
     double fieldsplit_rtol; /* Newton only: MINRES rtol (solver.py:64) */
-    int32_t inner_cycles;   /* Newton only: V-cycles / PCG its per inner block solve */
+    int32_t inner_cycles;   /* Newton only: > 0 -> each field-split block solve is a fixed budget of
+                             * this many PCG iterations at rtol 1e-12 (fieldsplit_inner = "cg",
+                             * inner_cg linalg.py:446-456); 0 -> solved to inner_rtol */
     int32_t reserved;
 } pf_vi_opts;
 

@@ -117,25 +117,31 @@ static int eval_F(Ctx* c, const NewtonWs& w, const double* x, double* F, const d
 }
 
 // A^-1 b (GMG-PCG, hierarchy already set up for the current alpha) -> out
-static int solve_A(Ctx* c, const double* b, double* out, double rtol, long long& its, cudaStream_t st) {
+// inner block solves: to rtol, or (budget > 0) a fixed budget of `budget` PCG iterations at
+// rtol 1e-12 (fieldsplit_inner = "cg", inner_cg linalg.py:446-456)
+static int solve_A(Ctx* c, const double* b, double* out, double rtol, int budget, long long& its,
+                   cudaStream_t st) {
     PcgBuffers B{c->cg_x, c->cg_r, c->cg_z, c->cg_p0, c->cg_p1, c->cg_q, c->cg_dinv, const_cast<double*>(b), c->n_u};
     // pcg_run reads |b|^2 from S_AUX0
     double bb;
     NTRY(ndot(c, c->n_u, b, b, S_AUX0, bb, st));
     pf_lin_report rep{};
-    int rc = pcg_run(c, 2, B, c->alpha_ws, nullptr, rtol, 0.0, 10 * c->n_u, 1, 2, &rep, st);
+    int rc = pcg_run(c, 2, B, c->alpha_ws, nullptr, budget > 0 ? 1e-12 : rtol, 0.0,
+                     budget > 0 ? budget : 10 * c->n_u, 1, 2, &rep, st);
     its += rep.iterations;
     if (rc != PF_OK) return set_error(c, PF_EINNER, "inner solve on block 'A' failed: " + c->err);
     NCU(c, cudaMemcpyAsync(out, c->cg_x, sizeof(double) * c->n_u, cudaMemcpyDeviceToDevice, st), "copy");
     return PF_OK;
 }
 // C^-1 b on the inactive damage block (Jacobi-PCG, kappa / act / dinv ready) -> out
-static int solve_C(Ctx* c, const double* b, double* out, double rtol, long long& its, cudaStream_t st) {
+static int solve_C(Ctx* c, const double* b, double* out, double rtol, int budget, long long& its,
+                   cudaStream_t st) {
     PcgBuffers B{c->da_x, c->da_r, c->da_z, c->da_p0, c->da_p1, c->da_q, c->da_dinv, const_cast<double*>(b), c->n_a};
     double bb;
     NTRY(ndot(c, c->n_a, b, b, S_AUX0, bb, st));
     pf_lin_report rep{};
-    int rc = pcg_run(c, 1, B, c->kappa, c->act, rtol, 0.0, 10 * c->n_a, 1, 8, &rep, st);
+    int rc = pcg_run(c, 1, B, c->kappa, c->act, budget > 0 ? 1e-12 : rtol, 0.0,
+                     budget > 0 ? budget : 10 * c->n_a, 1, 8, &rep, st);
     its += rep.iterations;
     if (rc != PF_OK) return set_error(c, PF_EINNER, "inner solve on block 'C' failed: " + c->err);
     NCU(c, cudaMemcpyAsync(out, c->da_x, sizeof(double) * c->n_a, cudaMemcpyDeviceToDevice, st), "copy");
@@ -144,17 +150,17 @@ static int solve_C(Ctx* c, const double* b, double* out, double rtol, long long&
 
 // y = P^-1 r (symmetric multiplicative field split, linalg.py:424-430)
 static int fieldsplit(Ctx* c, const NewtonWs& w, const double* r, double* y, const double* u, const double* alpha,
-                      double inner_rtol, long long& its, cudaStream_t st) {
+                      double inner_rtol, int budget, long long& its, cudaStream_t st) {
     const long long nu = w.nu, na = w.na;
     double* y1 = y;              // u part of y
     double* z = y + nu;          // alpha part of y
-    NTRY(solve_A(c, r, y1, inner_rtol, its, st));
+    NTRY(solve_A(c, r, y1, inner_rtol, budget, its, st));
     NTRY(launch_Kau(c, u, alpha, y1, w.TMP + nu, PF_BC_ELIMINATE, st));            // B^T y1
     k_nsubmask<<<nblocks(na), kNB, 0, st>>>(na, r + nu, w.TMP + nu, c->act, w.TMP + nu);
     c->launches++;
-    NTRY(solve_C(c, w.TMP + nu, z, inner_rtol, its, st));
+    NTRY(solve_C(c, w.TMP + nu, z, inner_rtol, budget, its, st));
     NTRY(launch_Kua(c, u, alpha, z, w.TMP, PF_BC_ELIMINATE, st));                   // B z
-    NTRY(solve_A(c, w.TMP, w.TMP, inner_rtol, its, st));
+    NTRY(solve_A(c, w.TMP, w.TMP, inner_rtol, budget, its, st));
     k_naxpy<<<nblocks(nu), kNB, 0, st>>>(nu, -1.0, w.TMP, y1);
     c->launches++;
     return PF_OK;
@@ -162,7 +168,7 @@ static int fieldsplit(Ctx* c, const NewtonWs& w, const double* r, double* y, con
 
 // MINRES on the masked inactive block J_NN d = rhs (x0 = 0); returns the iterations.
 static int minres(Ctx* c, NewtonWs& w, const double* u, const double* alpha, const double* rhs, double* x,
-                  double rtol, long long maxit, double inner_rtol, long long& kits, bool& converged,
+                  double rtol, long long maxit, double inner_rtol, int budget, long long& kits, bool& converged,
                   cudaStream_t st) {
     const long long n = w.n, nu = w.nu;
     auto op = [&](const double* v, double* out) {
@@ -171,7 +177,7 @@ static int minres(Ctx* c, NewtonWs& w, const double* u, const double* alpha, con
     NCU(c, cudaMemsetAsync(x, 0, sizeof(double) * n, st), "memset");
     NCU(c, cudaMemcpyAsync(w.R1, rhs, sizeof(double) * n, cudaMemcpyDeviceToDevice, st), "copy");
     double *r1 = w.R1, *r2 = w.R2, *y = w.Y, *v = w.V, *ww = w.W, *w1 = w.W1, *w2 = w.W2;
-    NTRY(fieldsplit(c, w, r1, y, u, alpha, inner_rtol, kits, st));
+    NTRY(fieldsplit(c, w, r1, y, u, alpha, inner_rtol, budget, kits, st));
     double beta1;
     NTRY(ndot(c, n, r1, y, S_AUX1, beta1, st));
     if (beta1 < 0.0) return set_error(c, PF_EBREAKDOWN, "minres: preconditioner not SPD");
@@ -199,7 +205,7 @@ static int minres(Ctx* c, NewtonWs& w, const double* u, const double* alpha, con
         r1 = r2;
         r2 = y;
         y = old_r1;
-        NTRY(fieldsplit(c, w, r2, y, u, alpha, inner_rtol, kits, st));
+        NTRY(fieldsplit(c, w, r2, y, u, alpha, inner_rtol, budget, kits, st));
         oldb = beta;
         double bb;
         NTRY(ndot(c, n, r2, y, S_AUX1, bb, st));
@@ -303,7 +309,7 @@ int newton_solve(Ctx* c, const double* u_in, const double* a_in, const double* l
         long long kits = 0;
         bool lin_ok = false;
         int rc = minres(c, w, u, alpha, w.RHS, w.D, fs_rtol, o->inner_maxit > 0 ? o->inner_maxit : 10 * n,
-                        inner_rtol, kits, lin_ok, st);
+                        inner_rtol, std::max(0, o->inner_cycles), kits, lin_ok, st);
         rep->total_krylov_iterations += kits;
         if (rc == PF_OK && lin_ok) {
             k_nscale<<<nblocks(n), kNB, 0, st>>>(n, -1.0, w.D, w.D);  // d = -d_N (zero on active)

@@ -132,7 +132,14 @@ def _snap_bc(state: State, problem: Discretization) -> None:
 
 def _lin_opts(config: SolverConfig, warm: bool) -> _lib.LinOpts:
     rtol = config.direct_rtol if config.elastic_solver == "direct" else config.elastic_rtol
-    prec = _lib.PREC.get(config.elastic_precond, 0)
+    if config.elastic_solver == "cg" and config.elastic_precond not in _lib.PREC:
+        # SSOR (two sparse triangular solves) and the stand-alone Chebyshev preconditioner have no
+        # device form (Chebyshev-Jacobi lives inside the multigrid smoother)
+        raise ValueError(f"elastic_precond {config.elastic_precond!r} is not available on the B200 path; "
+                         "use 'gmg' (multigrid) or 'jacobi'")
+    # "direct" (the reference's LU) is PCG at direct_rtol with the configured device preconditioner,
+    # multigrid when the configured one (e.g. the reference default "ssor") has no device form
+    prec = _lib.PREC.get(config.elastic_precond, _lib.PREC["gmg"])
     return _lib.LinOpts(precond=prec, warm_start=1 if warm else 0, maxit=0, rtol=rtol, atol=0.0,
                         check_every=config.check_every, gmg_levels=0, cheb_degree=2,
                         gmg_reuse=1 if config.gmg_reuse else 0)
@@ -252,9 +259,16 @@ def am_solve(state: State, problem: Discretization, config: SolverConfig,
 def coupled_newton_solve(state: State, problem: Discretization, config: SolverConfig,
                          cycle: int = 0):
     """Active-set Newton on the stacked (u, alpha) system; returns (new_state, report)."""
+    # coupled_solver="direct" (the reference's LU on the inactive Jacobian, solver.py:251-257) is
+    # MINRES + field split at direct_rtol; fieldsplit_inner="cg" is the fixed-budget inner PCG
+    # (solver.py:259-263, linalg.py:446-456), with the device preconditioners (A: multigrid or
+    # Jacobi in place of SSOR, C: Jacobi)
+    direct = config.coupled_solver == "direct"
     vic = VIConfig(abs_tol=config.outer_atol, max_iterations=config.max_newton_iterations,
-                   fieldsplit_rtol=config.fieldsplit_rtol,
-                   inner_rtol=config.newton_inner_rtol or 0.0)
+                   fieldsplit_rtol=config.direct_rtol if direct else config.fieldsplit_rtol,
+                   inner_rtol=config.newton_inner_rtol or (config.direct_rtol if direct else 0.0),
+                   inner_cycles=config.fieldsplit_cg_budget
+                   if (config.fieldsplit_inner == "cg" and not direct) else 0)
     opts = vic.to_c()
     rep = _lib.VIReport()
     out = state.copy()

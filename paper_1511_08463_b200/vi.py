@@ -29,7 +29,7 @@ class VIConfig:
     inner_rtol: float = 1e-10
     inner_maxit: int = 0
     fieldsplit_rtol: float = 1e-6
-    inner_cycles: int = 8
+    inner_cycles: int = 0
 
     def to_c(self) -> _lib.VIOpts:
         return _lib.VIOpts(abs_tol=self.abs_tol, max_iterations=self.max_iterations, precond=0,

@@ -249,3 +249,24 @@ def test_fused_relax_physics_equals_separate_passes(pattern, omega):
     assert torch.equal(a1, a2)
     assert (wb1, d1) == (wb2, d2)
     assert res1 == res2 and tuple(e1) == tuple(e2)
+
+
+@pytest.mark.parametrize("variant", ["direct", "inner_cg"])
+def test_newton_coupled_solver_variants_converge_like_fieldsplit(variant):
+    """coupled_solver='direct' (MINRES + field split at direct_rtol) and fieldsplit_inner='cg'
+    (fixed-budget inner PCG) reach the same Newton solution as the default field split."""
+    import paper_1511_08463_b200 as pf
+    from paper_1511_08463_b200 import solver as S
+    setup = pf.setup_traction(pf.Material(ell=0.1), nx=40, ny=12, n_steps=12, pattern="right")
+    base = pf.SolverConfig(method="am", elastic_solver="cg", elastic_precond="gmg", outer_atol=1e-3)
+    st = pf.State.zeros(setup.mesh)
+    pf.run_quasistatic(setup, base, snapshot_stride=0, state=st, steps=list(range(9)))
+    prob = setup.problem
+    kw = {"coupled_solver": "direct"} if variant == "direct" else {"fieldsplit_inner": "cg", "fieldsplit_cg_budget": 30}
+    ref_cfg = pf.SolverConfig(outer_atol=1e-9, elastic_solver="cg", elastic_precond="gmg")
+    var_cfg = pf.SolverConfig(outer_atol=1e-9, elastic_solver="cg", elastic_precond="gmg", **kw)
+    s1, r1 = S.coupled_newton_solve(st, prob, ref_cfg)
+    s2, r2 = S.coupled_newton_solve(st, prob, var_cfg)
+    assert r1.converged and r2.converged
+    assert rel(s1.u.cpu().numpy(), s2.u.cpu().numpy()) < 1e-6
+    assert float((s1.alpha - s2.alpha).abs().max()) < 1e-6

@@ -100,3 +100,18 @@ def test_option_structs_built_from_config():
         assert o.precond == 1 and o.warm_start == 1 and o.rtol == 1e-9 and o.gmg_reuse == int(reuse)
     o = S._lin_opts(S.SolverConfig(), False)
     assert o.rtol == S.SolverConfig().direct_rtol and o.warm_start == 0
+
+
+def test_reference_solver_choices_map_to_device_options():
+    """coupled_solver / fieldsplit_inner / elastic_precond keep the reference meaning
+    (solver.py:58-64, 251-263) on the device path, or fail loudly."""
+    from paper_1511_08463_b200 import solver as S
+    import pytest as _pt
+    with _pt.raises(ValueError, match="not available on the B200 path"):
+        S._lin_opts(S.SolverConfig(elastic_solver="cg", elastic_precond="ssor"), False)
+    with _pt.raises(ValueError, match="not available on the B200 path"):
+        S._lin_opts(S.SolverConfig(elastic_solver="cg", elastic_precond="chebyshev"), False)
+    o = S._lin_opts(S.SolverConfig(elastic_solver="direct", elastic_precond="ssor"), False)
+    assert o.precond == 1 and o.rtol == 1e-12      # reference default precond: multigrid at direct_rtol
+    o = S._lin_opts(S.SolverConfig(elastic_solver="direct"), False)
+    assert o.precond == 0                            # configured Jacobi kept
