@@ -34,6 +34,7 @@ METRIC = "fp64 operator-apply GDOF/s & HBM GB/s vs peak; sec per load step (AM+N
 REF_N = 48          # CPU sample sizes (SENT, crossed), see DESIGN.md "CPU baseline"
 REF_N_SMALL = 32
 REF_N3, REF_N3_SMALL = 10, 6   # CPU sample cubes for config 4
+REF_NT, REF_NT_SMALL = 48, 32  # CPU sample slabs (4n x n) for config 3
 
 
 def peaks():
@@ -104,6 +105,11 @@ def sent_config(pf):
                            max_am_iterations=2000)
 
 
+def thermal_config(pf):
+    return pf.SolverConfig(method="oram_newton", omega=1.5, outer_atol=1e-7, elastic_solver="cg",
+                           elastic_rtol=1e-8, elastic_precond="gmg", max_am_iterations=2000)
+
+
 def traction3d_config(pf):
     return pf.SolverConfig(method="oram_newton", omega=1.7, outer_atol=1e-6, elastic_solver="cg",
                            elastic_rtol=1e-8, elastic_precond="gmg", max_am_iterations=3000)
@@ -131,6 +137,11 @@ WORKLOADS = {
                       "k_ell=1e-6, Gc lognormal(0, 0.1) per cell (seed 0) + one Jacobi smoothing pass, "
                       "z=0 clamped, z=1 u_z=t (30 steps to 1.5 t_c), ORAM omega=1.7 + Newton, 3D "
                       "multigrid-PCG rtol 1e-8, outer_atol 1e-6; step = one load step"),
+    "thermal2048": ("thermal2048: BASELINE config 3 -- quenched slab [0,4]x[0,1], 2048x512 union-jack "
+                    "P1 (1,051,137 vertices), plane strain AT1, E=1 (+-1% seeded cell noise) nu=0.2 "
+                    "Gc=1 ell=0.01, eps0 = -dT (1 - erf(y/(2 sqrt(1e-3)))) I, dT to 3 dT_c over 40 "
+                    "steps, ORAM omega=1.5 + Newton, GMG-PCG rtol 1e-8, outer_atol 1e-7; step = one "
+                    "load step (nucleation near step 14: pass --warmup >= 14 to time cracked steps)"),
     "traction1": ("traction1: BASELINE config 1 -- 200x20 right-diagonal AT1 bar (E=1, nu=0, Gc=1, "
                   "ell=0.05, k=1e-6), t in linspace(0,1.5t_c,20), AM omega=1, atol 1e-6; step = one "
                   "load step"),
@@ -142,6 +153,8 @@ def make_workload(pf, name):
         return pf.setup_sent(n=512), sent_config(pf)
     if name == "traction3d128":
         return pf.setup_traction3d(n=128), traction3d_config(pf)
+    if name == "thermal2048":
+        return pf.setup_thermal_slab(nx=2048, ny=512), thermal_config(pf)
     return traction1_setup(pf), traction1_config(pf)
 
 
@@ -168,6 +181,17 @@ def oracle_traction3d_steps(n, warm, timed):
     from oracle import problems as opb
     s = opb.traction3d(n=n)
     cfg = oam.AMConfig(method="oram_newton", omega=1.7, outer_atol=1e-6, max_am_iterations=3000)
+    _, st = opb.run(s, cfg, snapshot_stride=0, steps=list(warm))
+    t0 = time.perf_counter()
+    rows, _ = opb.run(s, cfg, snapshot_stride=0, steps=list(timed), state=st)
+    return (time.perf_counter() - t0) / len(rows)
+
+
+def oracle_thermal_steps(ny, warm, timed):
+    from oracle import am as oam
+    from oracle import problems as opb
+    s = opb.thermal_slab(nx=4 * ny, ny=ny)
+    cfg = oam.AMConfig(method="oram_newton", omega=1.5, outer_atol=1e-7, max_am_iterations=2000)
     _, st = opb.run(s, cfg, snapshot_stride=0, steps=list(warm))
     t0 = time.perf_counter()
     rows, _ = opb.run(s, cfg, snapshot_stride=0, steps=list(timed), state=st)
@@ -220,6 +244,18 @@ def cpu_sample(workload, warm, timed):
                 f"({s_big:.3f} s/step); scaled to 128^3 with the fitted growth vertices^{expo:.2f}")
         return value, desc, {"s_per_step_small": s_small, "s_per_step_big": s_big,
                              "n_small": REF_N3_SMALL, "n_big": REF_N3, "exponent": expo}
+    if workload == "thermal2048":
+        s_small = oracle_thermal_steps(REF_NT_SMALL, warm, timed)
+        s_big = oracle_thermal_steps(REF_NT, warm, timed)
+        v_small, v_big, v_full = ((4 * n + 1) * (n + 1) for n in (REF_NT_SMALL, REF_NT, 512))
+        expo = min(max(math.log(s_big / s_small) / math.log(v_big / v_small), 1.0), 2.0)
+        value = s_big * (v_full / v_big) ** expo
+        desc = (f"schedule steps {timed[0]}..{timed[-1]} of the oracle (reference algorithm, SuperLU, "
+                f"serial) measured at {4 * REF_NT_SMALL}x{REF_NT_SMALL} ({s_small:.3f} s/step) and "
+                f"{4 * REF_NT}x{REF_NT} ({s_big:.3f} s/step); scaled to 2048x512 with the fitted growth "
+                f"vertices^{expo:.2f}")
+        return value, desc, {"s_per_step_small": s_small, "s_per_step_big": s_big,
+                             "ny_small": REF_NT_SMALL, "ny_big": REF_NT, "exponent": expo}
     v = oracle_traction1_steps(warm, timed)
     return v, f"schedule steps {timed[0]}..{timed[-1]} of config 1 (oracle, SuperLU), full size", {}
 
@@ -345,7 +381,7 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    nsched = {"sent512": 60, "traction3d128": 30}.get(args.workload, 20)
+    nsched = {"sent512": 60, "traction3d128": 30, "thermal2048": 40}.get(args.workload, 20)
     W = max(0, min(args.warmup, nsched - 1))
     K = max(1, min(args.steps, nsched - W))
     timed = list(range(W, W + K))
