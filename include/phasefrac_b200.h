@@ -144,6 +144,10 @@ int pf_set_dirichlet(pf_ctx* ctx, const int64_t* dofs, const double* vals, int64
 /* Isotropic inelastic strain eps0 = e*(1,1,0) per element, given as a HOST table
  * e[type*ny + J] for element type `type` in cell row J (2D; profile in y only, as the
  * thermal-shock setups need, cases.py:66-80).  NULL clears. */
+/* Graded (banded) meshes, banded_rect_mesh mesh.py:163-190: heights of the ny cell rows
+ * (HOST array, bottom to top; their sum is the y extent).  NULL restores uniform rows ly/ny.
+ * Columns stay uniform.  Invalidates the multigrid hierarchy. */
+int pf_set_row_heights(pf_ctx* ctx, const double* row_heights, void* stream);
 int pf_set_eps0_rows(pf_ctx* ctx, const double* table, void* stream);
 
 /* ---- operators (fem.py:162-276) -------------------------------------------- */

@@ -19,6 +19,8 @@ from __future__ import annotations
 from dataclasses import dataclass, field
 from itertools import permutations
 
+from typing import Optional
+
 import numpy as np
 
 PATTERNS = ("union_jack", "right", "crossed", "kuhn6")
@@ -57,12 +59,20 @@ class SimplexMesh:
 
 
 def grid_mesh(nx: int, ny: int, lx: float = 1.0, ly: float = 1.0,
-              pattern: str = "union_jack", ox: float = 0.0, oy: float = 0.0) -> SimplexMesh:
-    """2D structured triangulation of [ox, ox+lx] x [oy, oy+ly]."""
+              pattern: str = "union_jack", ox: float = 0.0, oy: float = 0.0,
+              ys: Optional[np.ndarray] = None) -> SimplexMesh:
+    """2D structured triangulation of [ox, ox+lx] x [oy, oy+ly]; ``ys`` (ny+1 increasing row
+    coordinates) gives graded rows (banded_rect_mesh, mesh.py:163-190)."""
     if nx < 1 or ny < 1:
         raise ValueError("grid_mesh needs nx, ny >= 1")
     xs = np.linspace(ox, ox + lx, nx + 1)
-    ys = np.linspace(oy, oy + ly, ny + 1)
+    if ys is None:
+        ys = np.linspace(oy, oy + ly, ny + 1)
+    else:
+        ys = np.asarray(ys, dtype=float)
+        if ys.shape != (ny + 1,) or np.any(np.diff(ys) <= 0):
+            raise ValueError("ys must hold ny+1 increasing row coordinates")
+        oy, ly = float(ys[0]), float(ys[-1] - ys[0])
     X, Y = np.meshgrid(xs, ys, indexing="ij")
     corners = np.column_stack([X.ravel(), Y.ravel()])
     nv = ny + 1
@@ -96,6 +106,37 @@ def grid_mesh(nx: int, ny: int, lx: float = 1.0, ly: float = 1.0,
                 "bottom": ii * nv, "top": ii * nv + ny}
     return SimplexMesh(vertices, elements.astype(np.intp), pattern, (nx, ny), (lx, ly),
                        (ox, oy), boundary)
+
+
+def graded_heights(span: float, h_fine: float, h_coarse: float, ratio: float = 1.3) -> np.ndarray:
+    """Row heights tiling ``span``: geometric growth from h_fine by ``ratio``, capped at h_coarse,
+    then shrunk uniformly to tile the span exactly (mesh.py:145-160; same operation order)."""
+    if span <= 1e-12:
+        return np.zeros(0)
+    rows = []
+    h = h_fine
+    while sum(rows) < span:  # Python's sequential sum, as the reference
+        h = min(h * ratio, h_coarse)
+        rows.append(h)
+    rows = np.asarray(rows)
+    return rows * (span / rows.sum())
+
+
+def banded_rows(L: float, H: float, h_fine: float, h_coarse: float, band_halfwidth: float):
+    """(nx, ys) of the band-refined grid on [0, L] x [-H/2, H/2] (banded_rect_mesh,
+    mesh.py:163-190): rows of h_fine within the band (+ one guard row), graded outside."""
+    nb = int(np.ceil(band_halfwidth / h_fine)) + 1
+    nx = max(1, round(L / h_fine))
+    if nb * h_fine >= H / 2:
+        ny = max(1, round(H / h_fine))
+        return nx, np.linspace(-H / 2, -H / 2 + H, ny + 1)
+    y_band = nb * h_fine
+    upper = graded_heights(H / 2 - y_band, h_fine, h_coarse)
+    y_up = y_band + np.cumsum(upper)
+    ys = np.concatenate([-y_up[::-1], np.arange(-nb, nb + 1) * h_fine, y_up])
+    ys[0] = -H / 2
+    ys[-1] = H / 2
+    return nx, ys
 
 
 def kuhn_mesh(nx: int, ny: int, nz: int, lx: float = 1.0, ly: float = 1.0,

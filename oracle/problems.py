@@ -18,7 +18,7 @@ import numpy as np
 from scipy.special import erf
 
 from .am import AMConfig, LoadState, StepStats, load_step
-from .meshgen import SimplexMesh, grid_mesh, kuhn_mesh
+from .meshgen import SimplexMesh, banded_rows, grid_mesh, kuhn_mesh
 from .p1 import EnergyParts, MaterialSpec, P1Model, merge_bcs
 
 
@@ -130,6 +130,50 @@ def thermal_slab(nx=2048, ny=512, spec: Optional[MaterialSpec] = None, n_steps=4
 
     return Setup("thermal_slab", model, sched, apply_load,
                  params={"critical_shock": dTc, "tau": tau, "E_cell": E_cell})
+
+
+def surfing_displacement(points, t, spec: MaterialSpec, K_I=None, v=1.0, L_c=0.05):
+    """Asymptotic Mode-I displacement about a tip at (L_c + v t, 0), theta in (-pi, pi] from +x,
+    plane-stress Kolosov constant (3 - nu)/(1 + nu) (cases.py:42-63)."""
+    pts = np.atleast_2d(np.asarray(points, dtype=float))
+    K = math.sqrt(spec.Gc * spec.E) if K_I is None else K_I
+    kappa = (3.0 - spec.nu) / (1.0 + spec.nu)
+    mu = spec.E / (2.0 * (1.0 + spec.nu))
+    dx = pts[:, 0] - (L_c + v * t)
+    dy = pts[:, 1]
+    r = np.hypot(dx, dy)
+    th = np.arctan2(dy, dx)
+    amp = (K / (2.0 * mu)) * np.sqrt(r / (2.0 * np.pi)) * (kappa - np.cos(th))
+    return np.stack([amp * np.cos(0.5 * th), amp * np.sin(0.5 * th)], axis=1)
+
+
+def surfing(spec: Optional[MaterialSpec] = None, L=2.0, H=1.0, h=None, h_coarse=None,
+            band_halfwidth=None, K_I=None, v=1.0, L_c=0.05, n_steps=25, t_end=1.0) -> Setup:
+    """Steady crack propagation on [0,L]x[-H/2,H/2] driven by the translated Mode-I field on the
+    whole boundary, pre-crack alpha_lb = 1 within h of {y=0, 0<=x<=L_c}, mesh refined in a band
+    around y = 0 (cases.py:110-150, banded_rect_mesh mesh.py:163-190)."""
+    spec = spec or MaterialSpec(ell=0.1)
+    h = spec.ell / 5.0 if h is None else h
+    h_coarse = 5.0 * h if h_coarse is None else h_coarse
+    band_halfwidth = 2.0 * spec.ell if band_halfwidth is None else band_halfwidth
+    nx, ys = banded_rows(L, H, h, h_coarse, band_halfwidth)
+    mesh = grid_mesh(nx, len(ys) - 1, L, H, "union_jack", 0.0, -H / 2, ys=ys)
+    model = P1Model(mesh, spec)
+    b = mesh.boundary
+    bverts = np.unique(np.concatenate([b["left"], b["right"], b["bottom"], b["top"]]))
+    bdofs = np.column_stack([2 * bverts, 2 * bverts + 1]).ravel().astype(np.intp)
+    bxy = mesh.vertices[bverts]
+
+    def apply_load(m, st, t):
+        vals = surfing_displacement(bxy, t, spec, K_I=K_I, v=v, L_c=L_c)
+        m.bc = merge_bcs((bdofs, vals.ravel()))
+
+    xy = mesh.vertices
+    near = np.clip(xy[:, 0], 0.0, L_c)
+    lb = np.where(np.hypot(xy[:, 0] - near, xy[:, 1]) <= h * (1.0 + 1e-9), 1.0, 0.0)
+    sched = np.linspace(0.0, t_end, n_steps)
+    return Setup("surfing", model, sched, apply_load, initial_alpha_lb=lb,
+                 params={"L_c": L_c, "v": v, "h": h, "ys": ys, "nx": nx})
 
 
 def lognormal_gc(n, sigma=0.1, seed=0, Gc=1.0):

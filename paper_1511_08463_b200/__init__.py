@@ -14,7 +14,8 @@ from .linalg import (BreakdownError, InnerSolverError, LinearSolveReport,  # noq
                      LinearSolverError, SingularOperatorError)
 from .model import (C_W, DamageModel, Material, critical_shock, critical_traction,  # noqa: F401
                     internal_length)
-from .mesh import (BOUNDARY_TAGS, StructuredMesh, StructuredMesh3D, boundary_dofs, rect_mesh)  # noqa: F401
+from .mesh import (BOUNDARY_TAGS, StructuredMesh, StructuredMesh3D, banded_rect_mesh,  # noqa: F401
+                   boundary_dofs, rect_mesh)
 from .vi import ActiveSetReport, VIConfig, fb_phi  # noqa: F401
 from .fem import (DeviceOperator, DirichletBC, Discretization, EnergyBreakdown,  # noqa: F401
                   State, assemble_energy, assemble_Kaa, assemble_Kua, assemble_Kuu,
@@ -23,6 +24,7 @@ from .solver import (NonlinearReport, SolverConfig, am_solve, coupled_newton_sol
                      damage_step, elastic_step, first_order_residual, oram_n_solve,
                      residual_norm, solve_load_step)
 from .cases import (ProblemSetup, StepFailureError, StepRecord, run_quasistatic,  # noqa: F401
-                    setup_sent, setup_thermal_slab, setup_traction, setup_traction3d)
+                    setup_sent, setup_surfing, setup_thermal_slab, setup_traction,
+                    setup_traction3d, surfing_displacement)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

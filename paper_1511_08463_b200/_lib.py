@@ -71,6 +71,7 @@ EXPORTS = {
     "pf_set_cell_fields": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "pf_set_dirichlet": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
     "pf_set_eps0_rows": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "pf_set_row_heights": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "pf_apply_Kuu": (C.c_int, [C.c_void_p] * 4 + [C.c_int32, C.c_void_p]),
     "pf_apply_Kaa": (C.c_int, [C.c_void_p] * 5 + [C.c_void_p]),
     "pf_kaa_coefficients": (C.c_int, [C.c_void_p] * 5),

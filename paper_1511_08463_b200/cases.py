@@ -19,7 +19,7 @@ from scipy.special import erf
 
 from .fem import (Discretization, DirichletBC, EnergyBreakdown, State, assemble_energy,
                   combine_bcs)
-from .mesh import StructuredMesh, StructuredMesh3D, boundary_dofs, rect_mesh
+from .mesh import StructuredMesh, StructuredMesh3D, banded_rect_mesh, boundary_dofs, rect_mesh
 from .model import DamageModel, Material, critical_shock, critical_traction
 from .solver import NonlinearReport, SolverConfig, solve_load_step
 
@@ -175,6 +175,53 @@ def setup_traction3d(n: int = 128, material: Optional[Material] = None, n_steps:
                                  DirichletBC(pull, np.full(pull.size, t)))
     return ProblemSetup("traction3d", mesh, problem, schedule, apply_load,
                         params={"critical_traction": tc, "Gc_cell": Gc_cell})
+
+
+def surfing_displacement(points, t: float, material: Material, K_I: Optional[float] = None,
+                         v: float = 1.0, L_c: float = 0.05) -> np.ndarray:
+    """Asymptotic Mode-I displacement about a tip at (L_c + v t, 0) (cases.py:42-63): polar
+    angle in (-pi, pi] from +x, plane-stress Kolosov constant (3 - nu)/(1 + nu), 0 at r = 0."""
+    pts = np.atleast_2d(np.asarray(points, dtype=float))
+    K = math.sqrt(material.Gc * material.E) if K_I is None else K_I
+    kappa = (3.0 - material.nu) / (1.0 + material.nu)
+    mu = material.E / (2.0 * (1.0 + material.nu))
+    dx = pts[:, 0] - (L_c + v * t)
+    dy = pts[:, 1]
+    r = np.hypot(dx, dy)
+    th = np.arctan2(dy, dx)
+    amp = (K / (2.0 * mu)) * np.sqrt(r / (2.0 * np.pi)) * (kappa - np.cos(th))
+    out = np.stack([amp * np.cos(0.5 * th), amp * np.sin(0.5 * th)], axis=1)
+    return out[0] if np.asarray(points).ndim == 1 else out
+
+
+def setup_surfing(material: Optional[Material] = None, L: float = 2.0, H: float = 1.0,
+                  h: Optional[float] = None, h_coarse: Optional[float] = None,
+                  band_halfwidth: Optional[float] = None, K_I: Optional[float] = None,
+                  v: float = 1.0, L_c: float = 0.05, n_steps: int = 25,
+                  t_end: float = 1.0) -> ProblemSetup:
+    """Boundary-driven steady crack propagation on [0, L] x [-H/2, H/2] (cases.py:110-150): the
+    translated Mode-I field on every boundary vertex, pre-crack alpha_lb = 1 within h of
+    {y = 0, 0 <= x <= L_c}, graded mesh refined in a band of half-width ~2 ell."""
+    material = material or Material(ell=0.1)
+    h = material.ell / 5.0 if h is None else h
+    h_coarse = 5.0 * h if h_coarse is None else h_coarse
+    band_halfwidth = 2.0 * material.ell if band_halfwidth is None else band_halfwidth
+    mesh = banded_rect_mesh(L, H, h, h_coarse, band_halfwidth)
+    problem = Discretization(mesh, material)
+    bverts = mesh.all_boundary_vertices()
+    bdofs = np.column_stack([2 * bverts, 2 * bverts + 1]).ravel()
+    bxy = mesh.vertices[bverts]
+
+    def apply_load(problem: Discretization, state: State, t: float) -> None:
+        vals = surfing_displacement(bxy, t, material, K_I=K_I, v=v, L_c=L_c)
+        problem.bc = DirichletBC(bdofs, vals.ravel())
+
+    xy = mesh.vertices
+    near = np.clip(xy[:, 0], 0.0, L_c)
+    lb = np.where(np.hypot(xy[:, 0] - near, xy[:, 1]) <= h * (1.0 + 1e-9), 1.0, 0.0)
+    schedule = np.linspace(0.0, t_end, n_steps)
+    return ProblemSetup("surfing", mesh, problem, schedule, apply_load, initial_alpha_lb=lb,
+                        params={"L_c": L_c, "v": v, "h": h})
 
 
 # -- quasi-static driver (cases.py:241-306) ---------------------------------------------------------

@@ -784,6 +784,7 @@ static void geometry_2d(Ctx* c) {
     g.E_cell = nullptr;
     g.Gc_cell = nullptr;
     g.eps0 = nullptr;
+    g.rowgeo = nullptr;
     g.has_bc = 0;
     g.nwj = (g.nvy + kLanesOut - 1) / kLanesOut;
     const long long rows = g.nx + 1;
@@ -863,6 +864,7 @@ static void plan_workspace(Ctx* c) {
     add((void**)&c->bcmask, c->n_a);
     add((void**)&c->act, c->n_a);
     add((void**)&c->eps0_tab, sizeof(double) * 4 * (c->d.ny + 1));
+    add((void**)&c->rowgeo_buf, sizeof(double) * 2 * (c->d.ny + 1));
     add((void**)&c->partials, sizeof(double) * kMaxRed * kMaxBlocksRed);
     add((void**)&c->scal, sizeof(double) * S_COUNT);
     add((void**)&c->tickets, sizeof(unsigned) * 64);
@@ -1057,6 +1059,32 @@ int pf_set_dirichlet(pf_ctx* c, const int64_t* dofs, const double* vals, int64_t
     c->h_bcmask.swap(mask);
     if (c->g.has_bc != (n > 0)) c->geo_version++;
     c->g.has_bc = n > 0;
+    return PF_OK;
+}
+
+// graded rows (banded_rect_mesh, mesh.py:145-190): heights of the ny cell rows, host array
+int pf_set_row_heights(pf_ctx* c, const double* hy, void* stream) {
+    NEED_WS(c);
+    if (c->dim != 2) return hy ? set_error(c, PF_EINVAL, "row heights are 2D only") : PF_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    Geo2& g = c->g;
+    if (!hy) {
+        if (g.rowgeo) { g.rowgeo = nullptr; c->geo_version++; c->gmg_built = 0; }
+        return PF_OK;
+    }
+    const double frac = g.pattern == PF_CROSSED ? 0.25 : 0.5;  // element area / (hx hy)
+    std::vector<double> t(2 * (size_t)g.ny);
+    for (int j = 0; j < g.ny; ++j) {
+        if (!(hy[j] > 0.0)) return set_error(c, PF_EINVAL, "row heights must be positive");
+        t[j] = 1.0 / hy[j];
+        t[g.ny + j] = frac * g.hx * hy[j];
+    }
+    PF_CU(c, cudaMemcpyAsync(c->rowgeo_buf, t.data(), sizeof(double) * t.size(), cudaMemcpyHostToDevice, st),
+          "row heights");
+    PF_CU(c, cudaStreamSynchronize(st), "sync");
+    g.rowgeo = c->rowgeo_buf;
+    c->geo_version++;
+    c->gmg_built = 0;
     return PF_OK;
 }
 

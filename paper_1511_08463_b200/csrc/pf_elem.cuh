@@ -40,6 +40,13 @@ __device__ __forceinline__ void st2(double* p, long long v, double a, double b) 
     reinterpret_cast<double2*>(p)[v] = make_double2(a, b);
 }
 
+// per-cell-row geometry: graded meshes (banded_rect_mesh, mesh.py:163-190) carry 1/hy and the
+// element area per cell row J; uniform meshes use the descriptor constants (a uniform branch)
+__device__ __forceinline__ double ihy_at(const Geo2& g, int cj) { return g.rowgeo ? __ldg(g.rowgeo + cj) : g.ihy; }
+__device__ __forceinline__ double area_at(const Geo2& g, int cj) {
+    return g.rowgeo ? __ldg(g.rowgeo + g.ny + cj) : g.area[0];
+}
+
 // ---- element kernels ---------------------------------------------------------------------
 // On a uniform grid every P1 gradient coefficient is a small integer times 1/hx (b, x-derivative)
 // or 1/hy (c, y-derivative).  Shp<PAT, T> holds those integers per element shape, so zero terms

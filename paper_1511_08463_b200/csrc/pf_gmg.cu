@@ -45,10 +45,11 @@ __device__ __forceinline__ void ke_block(const Geo2& g, double s, double bm, dou
 
 // Gradients (b, c) of shape T's three local nodes, with the union-jack mirror sign.
 template <int PAT, int T>
-__device__ __forceinline__ void shape_grads(const Geo2& g, double hxs, double (&b)[3], double (&c)[3]) {
+__device__ __forceinline__ void shape_grads(const Geo2& g, int cj, double hxs, double (&b)[3], double (&c)[3]) {
     using S = Shp<PAT, T>;
     b[0] = S::b0 * hxs; b[1] = S::b1 * hxs; b[2] = S::b2 * hxs;
-    c[0] = S::c0 * g.ihy; c[1] = S::c1 * g.ihy; c[2] = S::c2 * g.ihy;
+    const double ihy = ihy_at(g, cj);
+    c[0] = S::c0 * ihy; c[1] = S::c1 * ihy; c[2] = S::c2 * ihy;
 }
 
 // Cell matrix on the cell's local nodes (0..3 corners, 4 centre): M[(r*5 + s)][4] blocks.
@@ -75,9 +76,9 @@ __device__ void cell_matrix(const Geo2& g, int ci, int cj, const double* alpha, 
         const int nodes[3] = {A.v, B.v, C.v};
         const double ab = (Al[A.v] + Al[B.v] + Al[C.v]) * (1.0 / 3.0);
         const double om = 1.0 - ab;
-        const double s = (om * om + g.kell) * g.area[0] * Ec;
+        const double s = (om * om + g.kell) * area_at(g, cj) * Ec;
         double b[3], c[3];
-        shape_grads<PAT, T.v>(g, hxs, b, c);
+        shape_grads<PAT, T.v>(g, cj, hxs, b, c);
         for (int m = 0; m < 3; ++m)
             for (int n = 0; n < 3; ++n) {
                 double K[4];

@@ -43,6 +43,7 @@ struct Geo2 {
     const double* E_cell;     // nullable, per cell (I*ny + J)
     const double* Gc_cell;    // nullable
     const double* eps0;       // nullable, isotropic strain per (type, J): t*ny + J
+    const double* rowgeo;     // nullable (uniform rows): graded rows, [1/hy (ny) | element area (ny)] per cell row J
     const unsigned char* bcmask;  // per corner vertex, bit c = component c constrained
     const double* ubar;       // n_u (values on constrained dofs)
     int has_bc;
@@ -262,6 +263,7 @@ struct Ctx {
     double *ubar;                                                            // n_u
     unsigned char *bcmask, *act;                                             // n_a
     double *eps0_tab;                                                        // 4*ny
+    double *rowgeo_buf;                                                      // 2*ny (graded rows)
     double *partials, *scal;
     unsigned int* tickets;
     unsigned long long* bits;                                                // 8 words

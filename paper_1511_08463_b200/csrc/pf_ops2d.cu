@@ -328,11 +328,11 @@ struct OpKuu {
         for_each_elem<PAT>(par, [&](auto T, auto, auto A, auto B, auto C) {
             const double ab = (Al[A.v] + Al[B.v] + Al[C.v]) * (1.0 / 3.0);
             const double om = 1.0 - ab;
-            const double s = (om * om + g.kell) * g.area[0] * Ec;
+            const double s = (om * om + g.kell) * area_at(g, j) * Ec;
             double e0, e1, e2, s0, s1, s2;
-            strain<PAT, T.v, A.v, B.v, C.v>(hxs, g.ihy, U1, U2, e0, e1, e2);
+            strain<PAT, T.v, A.v, B.v, C.v>(hxs, ihy_at(g, j), U1, U2, e0, e1, e2);
             unit_stress(g, e0, e1, e2, s0, s1, s2);
-            scatter_BT<PAT, T.v, A.v, B.v, C.v>(hxs, g.ihy, s * s0, s * s1, s * s2, Y1, Y2);
+            scatter_BT<PAT, T.v, A.v, B.v, C.v>(hxs, ihy_at(g, j), s * s0, s * s1, s * s2, Y1, Y2);
         });
         mirror<PAT>(par, Y1);
         mirror<PAT>(par, Y2);
@@ -434,9 +434,9 @@ struct OpKuuDiag : NoRed {
         for_each_elem<PAT>(par, [&](auto T, auto, auto A, auto B, auto C) {
             const double ab = (Al[A.v] + Al[B.v] + Al[C.v]) * (1.0 / 3.0);
             const double om = 1.0 - ab;
-            const double s = (om * om + g.kell) * g.area[0] * Ec;
+            const double s = (om * om + g.kell) * area_at(g, j) * Ec;
             using Sh = Shp<PAT, T.v>;
-            const double X2 = g.ihx * g.ihx, Y2h = g.ihy * g.ihy;
+            const double X2 = g.ihx * g.ihx, Y2h = ihy_at(g, j) * ihy_at(g, j);
             const double bb[3] = {double(Sh::b0 * Sh::b0) * X2, double(Sh::b1 * Sh::b1) * X2,
                                   double(Sh::b2 * Sh::b2) * X2};
             const double cc[3] = {double(Sh::c0 * Sh::c0) * Y2h, double(Sh::c1 * Sh::c1) * Y2h,
@@ -517,14 +517,14 @@ struct OpKappa : NoRed {
         const double kc = ec[1] / g.cw;
         for_each_elem<PAT>(par, [&](auto T, auto S, auto A, auto B, auto C) {
             double e0, e1, e2, s0, s1, s2;
-            strain<PAT, T.v, A.v, B.v, C.v>(hxs, g.ihy, U1, U2, e0, e1, e2);
+            strain<PAT, T.v, A.v, B.v, C.v>(hxs, ihy_at(g, j), U1, U2, e0, e1, e2);
             if (g.eps0) {
                 const double e = __ldg(g.eps0 + (long long)(T.v + 2 * par) * g.ny + j);
                 e0 -= e; e1 -= e;
             }
             unit_stress(g, e0, e1, e2, s0, s1, s2);
             const double q = Ec * (e0 * s0 + e1 * s1 + e2 * s2);
-            const double ar = g.area[0];
+            const double ar = area_at(g, j);
             const double kap = (q + (g.at2 ? 2.0 * kc / g.ell : 0.0)) * ar * (1.0 / 9.0);
             const double cc = ar * (1.0 / 3.0) * (-q + (g.at2 ? 0.0 : kc / g.ell));
             Y[A.v] += cc; Y[B.v] += cc; Y[C.v] += cc;
@@ -544,12 +544,12 @@ struct OpKappa : NoRed {
 // Damage Hessian element action: y_m += kappa (x_A + x_B + x_C) + delta (b_m gx + c_m gy),
 // delta = 2 (Gc/c_w) ell |T| (diffusion part, fem.py:272-273).
 template <int PAT, int T, int A, int B, int C>
-__device__ __forceinline__ void elem_kaa(const Geo2& g, double hx, double kap, double kc,
+__device__ __forceinline__ void elem_kaa(const Geo2& g, int j, double hx, double kap, double kc,
                                          const double (&X)[5], double (&Y)[5]) {
-    const double del = 2.0 * kc * g.ell * g.area[0];
+    const double del = 2.0 * kc * g.ell * area_at(g, j);
     double gx, gy;
-    grad<PAT, T, A, B, C>(hx, g.ihy, X, gx, gy);
-    grad_scatter<PAT, T, A, B, C>(hx, g.ihy, kap * ((X[A] + X[B]) + X[C]), del * gx, del * gy, Y);
+    grad<PAT, T, A, B, C>(hx, ihy_at(g, j), X, gx, gy);
+    grad_scatter<PAT, T, A, B, C>(hx, ihy_at(g, j), kap * ((X[A] + X[B]) + X[C]), del * gx, del * gy, Y);
 }
 
 template <int PAT>
@@ -649,7 +649,7 @@ struct OpKaa {
         mirror<PAT>(par, X);
         const double kc = ec[0] / g.cw;
         for_each_elem<PAT>(par, [&](auto T, auto S, auto A, auto B, auto C) {
-            elem_kaa<PAT, T.v, A.v, B.v, C.v>(g, hxs, ec[1 + S.v], kc, X, Y);
+            elem_kaa<PAT, T.v, A.v, B.v, C.v>(g, j, hxs, ec[1 + S.v], kc, X, Y);
         });
         mirror<PAT>(par, Y);
         c00[0] = Y[0]; c10[0] = Y[1]; c01[0] = Y[2]; c11[0] = Y[3];
@@ -716,9 +716,9 @@ struct OpKaaDiag : NoRed {
         const double kc = ec[0] / g.cw;
         for_each_elem<PAT>(par, [&](auto T, auto S, auto A, auto B, auto C) {
             const double kap = ec[1 + S.v];
-            const double del = 2.0 * kc * g.ell * g.area[0];
+            const double del = 2.0 * kc * g.ell * area_at(g, j);
             using Sh = Shp<PAT, T.v>;
-            const double X2 = g.ihx * g.ihx, Y2h = g.ihy * g.ihy;
+            const double X2 = g.ihx * g.ihx, Y2h = ihy_at(g, j) * ihy_at(g, j);
             Y[A.v] += kap + del * (double(Sh::b0 * Sh::b0) * X2 + double(Sh::c0 * Sh::c0) * Y2h);
             Y[B.v] += kap + del * (double(Sh::b1 * Sh::b1) * X2 + double(Sh::c1 * Sh::c1) * Y2h);
             Y[C.v] += kap + del * (double(Sh::b2 * Sh::b2) * X2 + double(Sh::c2 * Sh::c2) * Y2h);
@@ -806,7 +806,7 @@ struct OpKaaTrial {
         mirror<PAT>(par, X);
         const double kc = ec[0] / g.cw;
         for_each_elem<PAT>(par, [&](auto T, auto S, auto A, auto B, auto C) {
-            elem_kaa<PAT, T.v, A.v, B.v, C.v>(g, hxs, ec[1 + S.v], kc, X, Y);
+            elem_kaa<PAT, T.v, A.v, B.v, C.v>(g, j, hxs, ec[1 + S.v], kc, X, Y);
         });
         mirror<PAT>(par, Y);
         c00[0] = Y[0]; c10[0] = Y[1]; c01[0] = Y[2]; c11[0] = Y[3];
@@ -949,9 +949,9 @@ struct OpPhys {
             const double om = 1.0 - ab;
             const double a = om * om + g.kell, ap = -2.0 * om;
             const double w = g.at2 ? ab * ab : ab, wp = g.at2 ? 2.0 * ab : 1.0;
-            const double ar = g.area[0];
+            const double ar = area_at(g, j);
             double e0, e1, e2, s0, s1, s2;
-            strain<PAT, T.v, A.v, B.v, C.v>(hxs, g.ihy, U1, U2, e0, e1, e2);
+            strain<PAT, T.v, A.v, B.v, C.v>(hxs, ihy_at(g, j), U1, U2, e0, e1, e2);
             if (g.eps0) {
                 const double e = __ldg(g.eps0 + (long long)(T.v + 2 * par) * g.ny + j);
                 e0 -= e; e1 -= e;
@@ -959,12 +959,12 @@ struct OpPhys {
             unit_stress(g, e0, e1, e2, s0, s1, s2);
             const double q = Ec * (e0 * s0 + e1 * s1 + e2 * s2);
             const double s = a * ar * Ec;
-            scatter_BT<PAT, T.v, A.v, B.v, C.v>(hxs, g.ihy, s * s0, s * s1, s * s2, Y1, Y2);
+            scatter_BT<PAT, T.v, A.v, B.v, C.v>(hxs, ihy_at(g, j), s * s0, s * s1, s * s2, Y1, Y2);
             double gx, gy;
-            grad<PAT, T.v, A.v, B.v, C.v>(hxs, g.ihy, Al, gx, gy);
+            grad<PAT, T.v, A.v, B.v, C.v>(hxs, ihy_at(g, j), Al, gx, gy);
             const double nod = (0.5 * ap * q + kc * wp / g.ell) * ar * (1.0 / 3.0);
             const double del = 2.0 * kc * g.ell * ar;
-            grad_scatter<PAT, T.v, A.v, B.v, C.v>(hxs, g.ihy, nod, del * gx, del * gy, Ya);
+            grad_scatter<PAT, T.v, A.v, B.v, C.v>(hxs, ihy_at(g, j), nod, del * gx, del * gy, Ya);
             if (own) {
                 eel += 0.5 * ar * a * q;
                 ed += ar * kc * (w / g.ell + g.ell * (gx * gx + gy * gy));
@@ -1070,16 +1070,16 @@ struct OpRhs {
         for_each_elem<PAT>(par, [&](auto T, auto, auto A, auto B, auto C) {
             const double ab = (Al[A.v] + Al[B.v] + Al[C.v]) * (1.0 / 3.0);
             const double om = 1.0 - ab;
-            const double s = (om * om + g.kell) * g.area[0] * Ec;
+            const double s = (om * om + g.kell) * area_at(g, j) * Ec;
             double e0 = 0.0, e1 = 0.0, e2 = 0.0, s0, s1, s2;
-            if (!LOADONLY) strain<PAT, T.v, A.v, B.v, C.v>(hxs, g.ihy, U1, U2, e0, e1, e2);
+            if (!LOADONLY) strain<PAT, T.v, A.v, B.v, C.v>(hxs, ihy_at(g, j), U1, U2, e0, e1, e2);
             if (g.eps0) {
                 const double e = __ldg(g.eps0 + (long long)(T.v + 2 * par) * g.ny + j);
                 e0 -= e; e1 -= e;
             }
             unit_stress(g, e0, e1, e2, s0, s1, s2);
             // r_raw = K g - f  ->  B^T s D (Bg - eps0)
-            scatter_BT<PAT, T.v, A.v, B.v, C.v>(hxs, g.ihy, s * s0, s * s1, s * s2, Y1, Y2);
+            scatter_BT<PAT, T.v, A.v, B.v, C.v>(hxs, ihy_at(g, j), s * s0, s * s1, s * s2, Y1, Y2);
         });
         mirror<PAT>(par, Y1);
         mirror<PAT>(par, Y2);
@@ -1123,13 +1123,13 @@ __device__ __forceinline__ void coupling_vec(const Geo2& g, double hx, int et, c
     const double ab = (Al[A] + Al[B] + Al[C]) * (1.0 / 3.0);
     const double ap = -2.0 * (1.0 - ab);
     double e0, e1, e2;
-    strain<PAT, T, A, B, C>(hx, g.ihy, U1, U2, e0, e1, e2);
+    strain<PAT, T, A, B, C>(hx, ihy_at(g, j), U1, U2, e0, e1, e2);
     if (g.eps0) {
         const double e = __ldg(g.eps0 + (long long)et * g.ny + j);
         e0 -= e; e1 -= e;
     }
     unit_stress(g, e0, e1, e2, s0, s1, s2);
-    sc = ap * g.area[0] * Ec * (1.0 / 3.0);
+    sc = ap * area_at(g, j) * Ec * (1.0 / 3.0);
 }
 
 // vertex slots: u, alpha, xa; cell: E, [u, alpha, xa centre]
@@ -1185,7 +1185,7 @@ struct OpKua : NoRed {
             double sc, s0, s1, s2;
             coupling_vec<PAT, T.v, A.v, B.v, C.v>(g, hxs, T.v + 2 * par, U1, U2, Al, Ec, j, sc, s0, s1, s2);
             const double f = sc * ((X[A.v] + X[B.v]) + X[C.v]);
-            scatter_BT<PAT, T.v, A.v, B.v, C.v>(hxs, g.ihy, f * s0, f * s1, f * s2, Y1, Y2);
+            scatter_BT<PAT, T.v, A.v, B.v, C.v>(hxs, ihy_at(g, j), f * s0, f * s1, f * s2, Y1, Y2);
         });
         mirror<PAT>(par, Y1);
         mirror<PAT>(par, Y2);
@@ -1266,7 +1266,7 @@ struct OpKau : NoRed {
         for_each_elem<PAT>(par, [&](auto T, auto, auto A, auto B, auto C) {
             double sc, s0, s1, s2, d0, d1, d2;
             coupling_vec<PAT, T.v, A.v, B.v, C.v>(g, hxs, T.v + 2 * par, U1, U2, Al, Ec, j, sc, s0, s1, s2);
-            strain<PAT, T.v, A.v, B.v, C.v>(hxs, g.ihy, X1, X2, d0, d1, d2);  // (B x)^T sigma
+            strain<PAT, T.v, A.v, B.v, C.v>(hxs, ihy_at(g, j), X1, X2, d0, d1, d2);  // (B x)^T sigma
             const double f = sc * (d0 * s0 + d1 * s1 + d2 * s2);
             Y[A.v] += f; Y[B.v] += f; Y[C.v] += f;
         });
@@ -1368,28 +1368,28 @@ struct OpJac : NoRed {
             const double ab = (Al[A.v] + Al[B.v] + Al[C.v]) * (1.0 / 3.0);
             const double om = 1.0 - ab;
             const double a = om * om + g.kell, ap = -2.0 * om;
-            const double ar = g.area[0];
+            const double ar = area_at(g, j);
             double e0, e1, e2, s0, s1, s2, d0, d1, d2, t0, t1, t2;
-            strain<PAT, T.v, A.v, B.v, C.v>(hxs, g.ihy, U1, U2, e0, e1, e2);
+            strain<PAT, T.v, A.v, B.v, C.v>(hxs, ihy_at(g, j), U1, U2, e0, e1, e2);
             if (g.eps0) {
                 const double e = __ldg(g.eps0 + (long long)(T.v + 2 * par) * g.ny + j);
                 e0 -= e; e1 -= e;
             }
             unit_stress(g, e0, e1, e2, s0, s1, s2);          // sigma (unit E)
-            strain<PAT, T.v, A.v, B.v, C.v>(hxs, g.ihy, X1, X2, d0, d1, d2);
+            strain<PAT, T.v, A.v, B.v, C.v>(hxs, ihy_at(g, j), X1, X2, d0, d1, d2);
             unit_stress(g, d0, d1, d2, t0, t1, t2);          // D B x_u
             const double q = Ec * (e0 * s0 + e1 * s1 + e2 * s2);
             const double sxa = (Xa[A.v] + Xa[B.v]) + Xa[C.v];
             const double cpl = ap * ar * Ec * (1.0 / 3.0);
             // u rows: a|T|E B^T D B x_u + cpl * sxa * B^T sigma
             const double ka = a * ar * Ec, kb = cpl * sxa;
-            scatter_BT<PAT, T.v, A.v, B.v, C.v>(hxs, g.ihy, ka * t0 + kb * s0, ka * t1 + kb * s1,
+            scatter_BT<PAT, T.v, A.v, B.v, C.v>(hxs, ihy_at(g, j), ka * t0 + kb * s0, ka * t1 + kb * s1,
                                                 ka * t2 + kb * s2, Y1, Y2);
             // alpha rows: cpl * (B x_u)^T sigma + Kaa x_a
             const double kap = (q + (g.at2 ? 2.0 * kc / g.ell : 0.0)) * ar * (1.0 / 9.0);
             const double fa = cpl * (d0 * s0 + d1 * s1 + d2 * s2);
             double Yt[5] = {0, 0, 0, 0, 0};
-            elem_kaa<PAT, T.v, A.v, B.v, C.v>(g, hxs, kap, kc, Xa, Yt);
+            elem_kaa<PAT, T.v, A.v, B.v, C.v>(g, j, hxs, kap, kc, Xa, Yt);
             Ya[A.v] += fa + Yt[A.v];
             Ya[B.v] += fa + Yt[B.v];
             Ya[C.v] += fa + Yt[C.v];

@@ -139,6 +139,10 @@ class Discretization:
         self._E = self._field(E_cell)
         self._Gc = self._field(Gc_cell)
         _lib.raise_for(self.lib.pf_set_cell_fields(ctx, _lib.ptr(self._E), _lib.ptr(self._Gc)), ctx)
+        rows = getattr(mesh, "row_heights", None)
+        if rows is not None:  # graded rows (banded_rect_mesh)
+            hy = np.ascontiguousarray(rows, dtype=np.float64)
+            _lib.raise_for(self.lib.pf_set_row_heights(ctx, hy.ctypes.data_as(C.c_void_p), _stream()), ctx)
         self._bc: Optional[DirichletBC] = None
         self._eps0_rows: Optional[np.ndarray] = None
 

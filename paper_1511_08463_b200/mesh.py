@@ -30,6 +30,7 @@ class StructuredMesh:
     pattern: str = "union_jack"
     x0: float = 0.0
     y0: float = 0.0
+    ys: np.ndarray | None = field(default=None, repr=False)  # graded rows: ny+1 coordinates
     _vertices: np.ndarray | None = field(default=None, repr=False)
 
     def __post_init__(self):
@@ -37,6 +38,12 @@ class StructuredMesh:
             raise ValueError("StructuredMesh needs nx, ny >= 1")
         if self.pattern not in PATTERNS_2D:
             raise ValueError(f"unknown pattern {self.pattern!r}; choose from {PATTERNS_2D}")
+        if self.ys is not None:
+            ys = np.asarray(self.ys, dtype=float)
+            if ys.shape != (self.ny + 1,) or np.any(np.diff(ys) <= 0):
+                raise ValueError("ys must hold ny+1 increasing row coordinates")
+            self.ys = ys
+            self.y0, self.ly = float(ys[0]), float(ys[-1] - ys[0])
         if self.lx <= 0 or self.ly <= 0:
             raise ValueError("extents must be positive")
 
@@ -67,10 +74,18 @@ class StructuredMesh:
         return self.ly / self.ny
 
     @property
+    def row_heights(self):
+        """Cell-row heights of a graded mesh (None when rows are uniform)."""
+        return None if self.ys is None else np.diff(self.ys)
+
+    def _ys(self) -> np.ndarray:
+        return self.ys if self.ys is not None else np.linspace(self.y0, self.y0 + self.ly, self.ny + 1)
+
+    @property
     def vertices(self) -> np.ndarray:
         if self._vertices is None:
             xs = np.linspace(self.x0, self.x0 + self.lx, self.nx + 1)
-            ys = np.linspace(self.y0, self.y0 + self.ly, self.ny + 1)
+            ys = self._ys()
             X, Y = np.meshgrid(xs, ys, indexing="ij")
             v = np.column_stack([X.ravel(), Y.ravel()])
             if self.pattern == "crossed":
@@ -102,7 +117,7 @@ class StructuredMesh:
 
     def cell_row_centroid_y(self) -> np.ndarray:
         """(n_types, ny) centroid heights of each element type per cell row (for eps0 tables)."""
-        ys = np.linspace(self.y0, self.y0 + self.ly, self.ny + 1)
+        ys = self._ys()
         y0, y1 = ys[:-1], ys[1:]
         yc = 0.5 * (y0 + y1)
         if self.pattern == "union_jack":
@@ -185,6 +200,42 @@ def rect_mesh(L: float, H: float, h: float, origin_x2: float = 0.0,
     nx = max(1, round(L / h))
     ny = max(1, round(H / h))
     return StructuredMesh(nx, ny, L, H, pattern, 0.0, origin_x2)
+
+
+def _graded_heights(span: float, h_fine: float, h_coarse: float, ratio: float = 1.3) -> np.ndarray:
+    """Heights tiling ``span``, growing by ``ratio`` from h_fine and capped at h_coarse, then
+    uniformly shrunk to tile it exactly (mesh.py:145-160)."""
+    if span <= 1e-12:
+        return np.zeros(0)
+    hs = []
+    h = h_fine
+    while sum(hs) < span:
+        h = min(h * ratio, h_coarse)
+        hs.append(h)
+    hs = np.asarray(hs)
+    return hs * (span / hs.sum())
+
+
+def banded_rect_mesh(L: float, H: float, h_fine: float, h_coarse: float,
+                     band_halfwidth: float) -> StructuredMesh:
+    """Union-jack mesh of [0, L] x [-H/2, H/2] refined in a band around y = 0 (mesh.py:163-190):
+    uniform columns of ~h_fine, rows of h_fine within |y| <= band_halfwidth (+ one guard row),
+    graded (ratio <= 1.3, capped at h_coarse) towards the edges.  Uniform when the band fills H."""
+    if L <= 0 or H <= 0 or h_fine <= 0 or band_halfwidth < 0:
+        raise ValueError("banded_rect_mesh needs positive L, H, h_fine and band_halfwidth >= 0")
+    if h_coarse < h_fine:
+        raise ValueError(f"h_coarse ({h_coarse}) must be >= h_fine ({h_fine})")
+    nb = int(np.ceil(band_halfwidth / h_fine)) + 1
+    if nb * h_fine >= H / 2:
+        return rect_mesh(L, H, h_fine, origin_x2=-H / 2)
+    y_band = nb * h_fine
+    upper = _graded_heights(H / 2 - y_band, h_fine, h_coarse)
+    y_up = y_band + np.cumsum(upper)
+    ys = np.concatenate([-y_up[::-1], np.arange(-nb, nb + 1) * h_fine, y_up])
+    ys[0] = -H / 2
+    ys[-1] = H / 2
+    nx = max(1, round(L / h_fine))
+    return StructuredMesh(nx, len(ys) - 1, L, H, "union_jack", 0.0, -H / 2, ys=ys)
 
 
 def boundary_dofs(mesh: StructuredMesh, tag: str, fieldname: str) -> np.ndarray:

@@ -212,7 +212,42 @@ def gen_steps():
     return out
 
 
+def gen_surfing():
+    """Graded (banded) mesh operators and a short surfing run."""
+    out = {}
+    rng = np.random.default_rng(4242)
+    mat = model.Material(E=1.3, nu=0.27, Gc=0.9, ell=0.1, k_ell=1e-6)
+    m = mesh.banded_rect_mesh(1.0, 0.8, 0.05, 0.2, 0.1)
+    prob = fem.Discretization(m, mat)
+    st = random_state(prob, rng)
+    xu = rng.standard_normal(prob.n_udofs)
+    xa = rng.standard_normal(prob.n_vertices)
+    e = fem.assemble_energy(st, prob)
+    out["op_vertices"] = m.vertices
+    out["op_u"], out["op_alpha"], out["op_lb"] = st.u, st.alpha, st.alpha_lb
+    out["op_xu"], out["op_xa"] = xu, xa
+    out["op_energy"] = np.array([e.elastic, e.dissipated, e.total])
+    out["op_ru"] = fem.assemble_residual_u(st, prob)
+    out["op_ra"] = fem.assemble_residual_alpha(st, prob)
+    out["op_Kuu_x"] = fem.assemble_Kuu(st, prob, apply_bc=False) @ xu
+    out["op_Kaa_x"] = fem.assemble_Kaa(st, prob) @ xa
+    out["op_Kua_x"] = fem.assemble_Kua(st, prob, apply_bc=False) @ xa
+    smat = model.Material(E=1.0, nu=0.3, Gc=1.0, ell=0.2)
+    setup = cases.setup_surfing(smat, h=0.05, n_steps=12, t_end=0.9)
+    recs = cases.run_quasistatic(setup, solver.SolverConfig(method="am", omega=1.0), snapshot_stride=1)
+    out["surf_vertices"] = setup.mesh.vertices
+    out["surf_energy"] = np.array([[r.energy.elastic, r.energy.dissipated, r.energy.total] for r in recs])
+    out["surf_am"] = np.array([r.report.am_iterations for r in recs])
+    out["surf_alpha"] = np.stack([r.alpha for r in recs])
+    out["surf_loads"] = np.array([r.load for r in recs])
+    return out
+
+
 def main():
+    if len(sys.argv) > 1 and sys.argv[1] == "surfing":  # regenerate only the surfing fixture
+        np.savez_compressed(os.path.join(OUT, "ref_surfing.npz"), **gen_surfing())
+        return
+    np.savez_compressed(os.path.join(OUT, "ref_surfing.npz"), **gen_surfing())
     np.savez_compressed(os.path.join(OUT, "ref_operators.npz"), **gen_operators())
     np.savez_compressed(os.path.join(OUT, "ref_vi.npz"), **gen_vi())
     np.savez_compressed(os.path.join(OUT, "ref_krylov.npz"), **gen_krylov())

@@ -170,3 +170,45 @@ def test_quasistatic_run_matches_reference():
     assert np.allclose(E[:, 1], ST["run_energy"][:, 1], rtol=1e-10, atol=0)
     assert np.allclose(E[:, 0], ST["run_energy"][:, 0], rtol=1e-8, atol=0)
     assert np.max(np.abs(rows[-1].alpha - ST["run_alpha_final"])) < 1e-8
+
+
+# -- graded (banded) meshes and the surfing benchmark ----------------------------
+SURF = np.load(os.path.join(GOLDEN, "ref_surfing.npz"))
+
+
+def test_banded_mesh_matches_reference():
+    from oracle.meshgen import banded_rows
+    nx, ys = banded_rows(1.0, 0.8, 0.05, 0.2, 0.1)
+    m = grid_mesh(nx, len(ys) - 1, 1.0, 0.8, "union_jack", 0.0, -0.4, ys=ys)
+    assert np.array_equal(m.vertices, SURF["op_vertices"])
+    hy = np.diff(ys)
+    assert hy.max() > 2.0 * hy.min()  # really graded
+
+
+def test_banded_mesh_operators_match_reference():
+    from oracle.meshgen import banded_rows
+    nx, ys = banded_rows(1.0, 0.8, 0.05, 0.2, 0.1)
+    spec = MaterialSpec(E=1.3, nu=0.27, Gc=0.9, ell=0.1, k_ell=1e-6)
+    m = P1Model(grid_mesh(nx, len(ys) - 1, 1.0, 0.8, "union_jack", 0.0, -0.4, ys=ys), spec)
+    u, a = SURF["op_u"], SURF["op_alpha"]
+    assert rel(np.array(m.energy(u, a)), SURF["op_energy"]) < 1e-13
+    assert rel(m.residual_u(u, a, "none"), SURF["op_ru"]) < 1e-12
+    assert rel(m.residual_alpha(u, a), SURF["op_ra"]) < 1e-12
+    assert rel(m.Kuu(a, eliminate=False) @ SURF["op_xu"], SURF["op_Kuu_x"]) < 1e-12
+    assert rel(m.Kaa(u, a) @ SURF["op_xa"], SURF["op_Kaa_x"]) < 1e-12
+    assert rel(m.Kua(u, a, mask_bc=False) @ SURF["op_xa"], SURF["op_Kua_x"]) < 1e-12
+
+
+@pytest.mark.slow
+def test_surfing_run_matches_reference():
+    """12-step surfing run (AM, omega = 1, the reference defaults) through nucleation-free steady
+    propagation: energies and iteration counts equal the reference's."""
+    s = problems.surfing(MaterialSpec(E=1.0, nu=0.3, Gc=1.0, ell=0.2), h=0.05, n_steps=12, t_end=0.9)
+    assert np.array_equal(s.model.mesh.vertices, SURF["surf_vertices"])
+    rows, _ = problems.run(s, am.AMConfig(method="am", omega=1.0))
+    assert np.allclose([r.load for r in rows], SURF["surf_loads"], rtol=0, atol=0)
+    E = np.array([list(r.energy) for r in rows])
+    assert np.allclose(E, SURF["surf_energy"], rtol=1e-9, atol=0)
+    assert np.max(np.abs(np.stack([r.alpha for r in rows]) - SURF["surf_alpha"])) < 1e-7
+    its = np.array([r.stats.am_iterations for r in rows])
+    assert np.max(np.abs(its - SURF["surf_am"])) <= 1
