@@ -105,6 +105,11 @@ def sent_config(pf):
                            max_am_iterations=2000)
 
 
+def surfing_config(pf):
+    return pf.SolverConfig(method="oram_newton", omega=1.6, outer_atol=1e-7, elastic_solver="cg",
+                           elastic_rtol=1e-10, elastic_precond="gmg", max_am_iterations=3000)
+
+
 def thermal_config(pf):
     return pf.SolverConfig(method="oram_newton", omega=1.5, outer_atol=1e-7, elastic_solver="cg",
                            elastic_rtol=1e-8, elastic_precond="gmg", max_am_iterations=2000)
@@ -142,6 +147,11 @@ WORKLOADS = {
                     "Gc=1 ell=0.01, eps0 = -dT (1 - erf(y/(2 sqrt(1e-3)))) I, dT to 3 dT_c over 40 "
                     "steps, ORAM omega=1.5 + Newton, GMG-PCG rtol 1e-8, outer_atol 1e-7; step = one "
                     "load step (nucleation near step 14: pass --warmup >= 14 to time cracked steps)"),
+    "surfing": ("surfing: the reference's acceptance surfing benchmark (SURVEY 8(f) row 1) -- "
+                "[0,2]x[-0.5,0.5], band-graded union-jack mesh (h = ell/5 = 0.02 in the band, 100 "
+                "columns), plane stress AT1 E=1 nu=0.3 Gc=1 ell=0.1, translated Mode-I field on the "
+                "whole boundary (v = 1, tip from 0.05), 30 steps to t = 1.45, ORAM omega=1.6 + "
+                "Newton, GMG-PCG rtol 1e-10, outer_atol 1e-7; step = one load step"),
     "traction1": ("traction1: BASELINE config 1 -- 200x20 right-diagonal AT1 bar (E=1, nu=0, Gc=1, "
                   "ell=0.05, k=1e-6), t in linspace(0,1.5t_c,20), AM omega=1, atol 1e-6; step = one "
                   "load step"),
@@ -153,6 +163,9 @@ def make_workload(pf, name):
         return pf.setup_sent(n=512), sent_config(pf)
     if name == "traction3d128":
         return pf.setup_traction3d(n=128), traction3d_config(pf)
+    if name == "surfing":
+        return pf.setup_surfing(pf.Material(E=1.0, nu=0.3, Gc=1.0, ell=0.1), h=0.02, n_steps=30,
+                                t_end=1.45), surfing_config(pf)
     if name == "thermal2048":
         return pf.setup_thermal_slab(nx=2048, ny=512), thermal_config(pf)
     return traction1_setup(pf), traction1_config(pf)
@@ -192,6 +205,18 @@ def oracle_thermal_steps(ny, warm, timed):
     from oracle import problems as opb
     s = opb.thermal_slab(nx=4 * ny, ny=ny)
     cfg = oam.AMConfig(method="oram_newton", omega=1.5, outer_atol=1e-7, max_am_iterations=2000)
+    _, st = opb.run(s, cfg, snapshot_stride=0, steps=list(warm))
+    t0 = time.perf_counter()
+    rows, _ = opb.run(s, cfg, snapshot_stride=0, steps=list(timed), state=st)
+    return (time.perf_counter() - t0) / len(rows)
+
+
+def oracle_surfing_steps(warm, timed):
+    from oracle import am as oam
+    from oracle import problems as opb
+    from oracle.p1 import MaterialSpec
+    s = opb.surfing(MaterialSpec(E=1.0, nu=0.3, Gc=1.0, ell=0.1), h=0.02, n_steps=30, t_end=1.45)
+    cfg = oam.AMConfig(method="oram_newton", omega=1.6, outer_atol=1e-7, max_am_iterations=3000)
     _, st = opb.run(s, cfg, snapshot_stride=0, steps=list(warm))
     t0 = time.perf_counter()
     rows, _ = opb.run(s, cfg, snapshot_stride=0, steps=list(timed), state=st)
@@ -244,6 +269,10 @@ def cpu_sample(workload, warm, timed):
                 f"({s_big:.3f} s/step); scaled to 128^3 with the fitted growth vertices^{expo:.2f}")
         return value, desc, {"s_per_step_small": s_small, "s_per_step_big": s_big,
                              "n_small": REF_N3_SMALL, "n_big": REF_N3, "exponent": expo}
+    if workload == "surfing":
+        v = oracle_surfing_steps(warm, timed)
+        return v, (f"schedule steps {timed[0]}..{timed[-1]} of the oracle (reference algorithm, "
+                   f"SuperLU, serial) on the SAME surfing workload (no scaling)"), {}
     if workload == "thermal2048":
         s_small = oracle_thermal_steps(REF_NT_SMALL, warm, timed)
         s_big = oracle_thermal_steps(REF_NT, warm, timed)
@@ -381,7 +410,7 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    nsched = {"sent512": 60, "traction3d128": 30, "thermal2048": 40}.get(args.workload, 20)
+    nsched = {"sent512": 60, "traction3d128": 30, "thermal2048": 40, "surfing": 30}.get(args.workload, 20)
     W = max(0, min(args.warmup, nsched - 1))
     K = max(1, min(args.steps, nsched - W))
     timed = list(range(W, W + K))
@@ -459,8 +488,8 @@ def main():
     sweep = operator_sweep(pf, torch, peak) if (not args.no_sweep and rank == 0) else None
     cpu = None
     if rank == 0 and world == 1:
-        v, desc, detail = cpu_sample(args.workload, range(W), timed[:2] if args.workload != "traction1"
-                                     else timed)
+        v, desc, detail = cpu_sample(args.workload, range(W), timed if args.workload in ("traction1", "surfing")
+                                     else timed[:2])
         cpu = {"value": v, "unit": "s/load-step", "cores": 1, "kind": "port", "sample": desc,
                "detail": detail}
 
