@@ -760,12 +760,6 @@ static void geometry_2d(Ctx* c) {
         const double* p3 = P[L[t][2]];
         const double det = (p2[0] - p1[0]) * (p3[1] - p1[1]) - (p2[1] - p1[1]) * (p3[0] - p1[0]);
         g.area[t] = 0.5 * det;
-        g.gb[t][0] = (p2[1] - p3[1]) / det;
-        g.gb[t][1] = (p3[1] - p1[1]) / det;
-        g.gb[t][2] = (p1[1] - p2[1]) / det;
-        g.gc[t][0] = (p3[0] - p2[0]) / det;
-        g.gc[t][1] = (p1[0] - p3[0]) / det;
-        g.gc[t][2] = (p2[0] - p1[0]) / det;
     }
     const double nu = d.nu;
     if (d.regime == PF_PLANE_STRESS) {

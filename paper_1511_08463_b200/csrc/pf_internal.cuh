@@ -35,7 +35,6 @@ struct Geo2 {
     double hx, hy, ihx, ihy;
     // element types (local nodes 0=v00 1=v10 2=v01 3=v11 4=centre)
     double area[4];
-    double gb[4][3], gc[4][3];
     // unit-E stiffness (Voigt e11, e22, g12)
     double D00, D01, D11, D22;
     double E, kell, Gc, ell, cw;
