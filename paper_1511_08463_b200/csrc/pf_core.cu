@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "pf_internal.cuh"
@@ -900,6 +901,7 @@ int pf_ctx_create(const pf_desc* desc, pf_ctx** out) {
     if (desc->model != PF_AT1 && desc->model != PF_AT2) return set_error(nullptr, PF_EINVAL, "unknown model");
     pf_ctx* c = new pf_ctx();
     c->d = *desc;
+    if (getenv("PF_NO_GRAPHS")) c->use_graphs = 0;  // profiling aid: eager Krylov loops (ncu sees every launch)
     if (d3) {
         c->dim = 3;
         c->dof = 3;

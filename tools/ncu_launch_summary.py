@@ -16,7 +16,9 @@ for r in rows[hdr + 1:]:
     v = float(r[vi].replace(",", ""))
     u = r[unit_i] if unit_i is not None else "ns"
     us = v / 1e3 if u in ("ns", "nsecond") else (v if u in ("us", "usecond") else v * 1e3)
-    name = r[ki].split("(")[0][:70]
+    name = r[ki].split("(")[0][:56]
+    if "Grid Size" in h:
+        name += " g" + r[h.index("Grid Size")].replace(" ", "")
     agg[name][0] += 1
     agg[name][1] += us
 tot = sum(a[1] for a in agg.values())
