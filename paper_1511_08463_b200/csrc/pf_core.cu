@@ -901,7 +901,11 @@ int pf_ctx_create(const pf_desc* desc, pf_ctx** out) {
     if (desc->model != PF_AT1 && desc->model != PF_AT2) return set_error(nullptr, PF_EINVAL, "unknown model");
     pf_ctx* c = new pf_ctx();
     c->d = *desc;
-    if (getenv("PF_NO_GRAPHS")) c->use_graphs = 0;  // profiling aid: eager Krylov loops (ncu sees every launch)
+    // profiling / timing aids: eager Krylov loops (ncu sees every launch); the launch-per-phase
+    // V-cycle; V-cycles without the coarse correction (fine smoothing only)
+    if (getenv("PF_NO_GRAPHS")) c->use_graphs = 0;
+    if (getenv("PF_GMG_LEGACY")) c->gmg_coarse = 0;
+    if (getenv("PF_GMG_SKIP_COARSE")) c->gmg_coarse = 2;
     if (d3) {
         c->dim = 3;
         c->dof = 3;
@@ -978,6 +982,7 @@ int pf_bind_workspace(pf_ctx* c, void* p, int64_t bytes) {
         cudaMemset(c->ubar, 0, sizeof(double) * c->n_u) != cudaSuccess ||
         cudaMemset(c->cg_p0, 0, sizeof(double) * c->n_u) != cudaSuccess ||
         cudaMemset(c->da_p0, 0, sizeof(double) * c->n_a) != cudaSuccess ||
+        (c->gmg_bar && cudaMemset(c->gmg_bar, 0, 2 * sizeof(unsigned int)) != cudaSuccess) ||
         cudaDeviceSynchronize() != cudaSuccess)
         return set_error(c, PF_ECUDA, "workspace initialisation failed");
     c->g.bcmask = c->bcmask;

@@ -16,7 +16,10 @@
 // a = k_ell) are seen by the coarse operators because they are Galerkin products.
 // Stencil layout: A[(k*4 + e)*nv + v], k = (di+1)*3 + (dj+1) neighbour, e = 2r + c block entry.
 #include <algorithm>
+#include <type_traits>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "pf_elem.cuh"
@@ -403,27 +406,43 @@ __global__ void k_coarse_inverse(LevelDev L, double* Ainv) {
 }
 
 // V-cycle vectors are streamed through L2 (ld.global.cg); operators/Dinv via the read-only path.
+// SH = true: the same functions on shared-memory copies (the single-CTA coarse tail), plain loads.
+template <bool SH = false>
 __device__ __forceinline__ double2 ldv(const double* p, long long v) {
-    return __ldcg(reinterpret_cast<const double2*>(p) + v);
+    if constexpr (SH) return reinterpret_cast<const double2*>(p)[v];
+    else return __ldcg(reinterpret_cast<const double2*>(p) + v);
 }
+template <bool SH = false>
 __device__ __forceinline__ void stv(double* p, long long v, double2 x) {
     reinterpret_cast<double2*>(p)[v] = x;
 }
+template <bool SH = false>
+__device__ __forceinline__ double ldr(const double* p) {  // operator data, constant during a cycle
+    if constexpr (SH) return *p;
+    else return __ldg(p);
+}
+template <bool SH = false>
+__device__ __forceinline__ double2 bmulT(const double* Dinv, long long nv, long long v, double r0, double r1) {
+    return make_double2(ldr<SH>(Dinv + v) * r0 + ldr<SH>(Dinv + nv + v) * r1,
+                        ldr<SH>(Dinv + 2 * nv + v) * r0 + ldr<SH>(Dinv + 3 * nv + v) * r1);
+}
 
 // res = D^-1 src ; d = res / theta ; x (=|+=) d
+template <bool SH = false>
 __device__ __forceinline__ void v_cheb0(long long nv, const double* Dinv, const double* src, double* res, double* d,
                                         double* x, int accumulate, const Cheb& c, long long v) {
-    const double2 s = ldv(src, v);
-    const double2 r = bmul(Dinv, nv, v, s.x, s.y);
-    const double2 dd = make_double2(r.x / c.theta, r.y / c.theta);
-    stv(res, v, r);
-    stv(d, v, dd);
+    const double2 s = ldv<SH>(src, v);
+    const double2 r = bmulT<SH>(Dinv, nv, v, s.x, s.y);
+    const double it = c.itheta;
+    const double2 dd = make_double2(r.x * it, r.y * it);
+    stv<SH>(res, v, r);
+    stv<SH>(d, v, dd);
     double2 xo = dd;
     if (accumulate) {
-        const double2 xv = ldv(x, v);
+        const double2 xv = ldv<SH>(x, v);
         xo = make_double2(xv.x + dd.x, xv.y + dd.y);
     }
-    stv(x, v, xo);
+    stv<SH>(x, v, xo);
 }
 __global__ void k_cheb0(long long nv, const double* Dinv, const double* src, double* res, double* d, double* x,
                         int accumulate, const double* lam, double ratio, const double* live) {
@@ -434,49 +453,73 @@ __global__ void k_cheb0(long long nv, const double* Dinv, const double* src, dou
         v_cheb0(nv, Dinv, src, res, d, x, accumulate, c, v);
 }
 
-// 9-point 2x2-block stencil apply (A y)_v with y_w = val(w)
-template <class F>
-__device__ __forceinline__ double2 st_apply_f(const LevelDev& L, long long v, F val) {
+// Sum over the G consecutive lanes that share a vertex (G = 1: no-op).
+template <int G>
+__device__ __forceinline__ double gsum(double x) {
+    if constexpr (G > 1) {
+        const unsigned lane = threadIdx.x & 31u;
+        const unsigned m = ((1u << G) - 1u) << (lane & ~(unsigned)(G - 1));
+#pragma unroll
+        for (int o = 1; o < G; o <<= 1) x += __shfl_xor_sync(m, x, o);
+    }
+    return x;
+}
+
+// 9-point 2x2-block stencil apply (A y)_v with y_w = val(w).  Branch-free: an out-of-grid
+// neighbour has a zero stencil block, so its address is clamped to v and the (finite) value it
+// brings is multiplied by zero -- every load of the row issues at once (latency-bound levels).
+// G > 1: G lanes share the vertex, lane q takes neighbours q, q+G, ... and the partial sums are
+// combined by shuffles (every lane returns the full row).
+template <bool SH = false, int G = 1, class F>
+__device__ __forceinline__ double2 st_apply_f(const LevelDev& L, long long v, F val, int q = 0) {
     const int nvy = L.ny + 1;
-    const int i = (int)(v / nvy), j = (int)(v % nvy);
+    const int vi = (int)v;
+    const int i = vi / nvy, j = vi - (vi / nvy) * nvy;
     double y0 = 0.0, y1 = 0.0;
 #pragma unroll
-    for (int k = 0; k < 9; ++k) {
+    for (int t = 0; t < (9 + G - 1) / G; ++t) {
+        const int k = (G == 1) ? t : q + t * G;
+        if (G > 1 && k >= 9) break;
         const int ni = i + k / 3 - 1, nj = j + k % 3 - 1;
-        if (ni < 0 || nj < 0 || ni > L.nx || nj > L.ny) continue;
-        const long long w = (long long)ni * nvy + nj;
+        const bool in = ni >= 0 && nj >= 0 && ni <= L.nx && nj <= L.ny;
+        const long long w = in ? (long long)ni * nvy + nj : v;
         const double2 dv = val(w);
-        y0 += __ldg(L.A + (size_t)(k * 4 + 0) * L.nv + v) * dv.x + __ldg(L.A + (size_t)(k * 4 + 1) * L.nv + v) * dv.y;
-        y1 += __ldg(L.A + (size_t)(k * 4 + 2) * L.nv + v) * dv.x + __ldg(L.A + (size_t)(k * 4 + 3) * L.nv + v) * dv.y;
+        y0 += ldr<SH>(L.A + (size_t)(k * 4 + 0) * L.nv + v) * dv.x + ldr<SH>(L.A + (size_t)(k * 4 + 1) * L.nv + v) * dv.y;
+        y1 += ldr<SH>(L.A + (size_t)(k * 4 + 2) * L.nv + v) * dv.x + ldr<SH>(L.A + (size_t)(k * 4 + 3) * L.nv + v) * dv.y;
     }
-    return make_double2(y0, y1);
+    return make_double2(gsum<G>(y0), gsum<G>(y1));
 }
-__device__ __forceinline__ double2 st_apply(const LevelDev& L, const double* d, long long v) {
-    return st_apply_f(L, v, [&](long long w) { return ldv(d, w); });
+template <bool SH = false, int G = 1>
+__device__ __forceinline__ double2 st_apply(const LevelDev& L, const double* d, long long v, int q = 0) {
+    return st_apply_f<SH, G>(L, v, [&](long long w) { return ldv<SH>(d, w); }, q);
 }
 
 // One Chebyshev step k >= 1 (linalg.py:366-376): w = A d (stencil, or precomputed Ad when
 // Ad != null); res -= D^-1 w; d' = rho_k rho_{k-1} d + (2 rho_k / delta) res; x (+= d) += d'.
 // `addd` folds a deferred cheb0 update (x += d) of the post-smoother into this pass.
+// (G, q: lanes per vertex and this lane's rank; lane 0 of the group stores.)
+template <bool SH = false, int G = 1>
 __device__ __forceinline__ void v_cheb_step(const LevelDev& L, const double* Ad, const double* d, double* dnext,
-                                            double* res, double* x, double a, double b, int addd, long long v) {
-    const double2 w = Ad ? ldv(Ad, v) : st_apply(L, d, v);
-    const double2 dw = bmul(L.Dinv, L.nv, v, w.x, w.y);
-    double2 r = ldv(res, v);
+                                            double* res, double* x, double a, double b, int addd, long long v,
+                                            int q = 0) {
+    const double2 w = Ad ? ldv<SH>(Ad, v) : st_apply<SH, G>(L, d, v, q);
+    if (G > 1 && q != 0) return;
+    const double2 dw = bmulT<SH>(L.Dinv, L.nv, v, w.x, w.y);
+    double2 r = ldv<SH>(res, v);
     r.x -= dw.x;
     r.y -= dw.y;
-    const double2 dv = ldv(d, v);
+    const double2 dv = ldv<SH>(d, v);
     const double2 dn = make_double2(a * dv.x + b * r.x, a * dv.y + b * r.y);
-    stv(res, v, r);
-    stv(dnext, v, dn);
-    double2 xv = ldv(x, v);
+    stv<SH>(res, v, r);
+    stv<SH>(dnext, v, dn);
+    double2 xv = ldv<SH>(x, v);
     if (addd) {
         xv.x += dv.x;
         xv.y += dv.y;
     }
     xv.x += dn.x;
     xv.y += dn.y;
-    stv(x, v, xv);
+    stv<SH>(x, v, xv);
 }
 __global__ void k_cheb_step(LevelDev L, const double* Ad, const double* d, double* dnext, double* res, double* x,
                             int k, int addd, const double* lam, double ratio, const double* live) {
@@ -491,29 +534,37 @@ __global__ void k_cheb_step(LevelDev L, const double* Ad, const double* d, doubl
 
 // Pre-smoother from x = 0, cheb0 fused into step 1: d0 = D^-1 b / theta is recomputed at the
 // stencil neighbours, so one pass gives res, d0, d1 and x = d0 + d1 (x = d0 when deg == 1).
+template <bool SH = false, int G = 1>
 __device__ __forceinline__ void v_pre_first(const LevelDev& L, const double* bvec, double* res, double* d0,
                                             double* d1, double* x, const Cheb& c, double a, double b, int deg,
-                                            long long v) {
-    const double2 s = ldv(bvec, v);
-    const double2 r0 = bmul(L.Dinv, L.nv, v, s.x, s.y);
-    const double2 dd = make_double2(r0.x / c.theta, r0.y / c.theta);
-    stv(d0, v, dd);
+                                            long long v, int q = 0) {
+    const double it = c.itheta;
     if (deg <= 1) {
-        stv(res, v, r0);
-        stv(x, v, dd);
+        if (G > 1 && q != 0) return;
+        const double2 s = ldv<SH>(bvec, v);
+        const double2 r0 = bmulT<SH>(L.Dinv, L.nv, v, s.x, s.y);
+        const double2 dd = make_double2(r0.x * it, r0.y * it);
+        stv<SH>(d0, v, dd);
+        stv<SH>(res, v, r0);
+        stv<SH>(x, v, dd);
         return;
     }
-    const double2 w = st_apply_f(L, v, [&](long long q) {
-        const double2 sq = ldv(bvec, q);
-        const double2 rq = bmul(L.Dinv, L.nv, q, sq.x, sq.y);
-        return make_double2(rq.x / c.theta, rq.y / c.theta);
-    });
-    const double2 dw = bmul(L.Dinv, L.nv, v, w.x, w.y);
+    const double2 w = st_apply_f<SH, G>(L, v, [&](long long u) {
+        const double2 sq = ldv<SH>(bvec, u);
+        const double2 rq = bmulT<SH>(L.Dinv, L.nv, u, sq.x, sq.y);
+        return make_double2(rq.x * it, rq.y * it);
+    }, q);
+    if (G > 1 && q != 0) return;
+    const double2 s = ldv<SH>(bvec, v);
+    const double2 r0 = bmulT<SH>(L.Dinv, L.nv, v, s.x, s.y);
+    const double2 dd = make_double2(r0.x * it, r0.y * it);
+    stv<SH>(d0, v, dd);
+    const double2 dw = bmulT<SH>(L.Dinv, L.nv, v, w.x, w.y);
     const double2 r = make_double2(r0.x - dw.x, r0.y - dw.y);
     const double2 dn = make_double2(a * dd.x + b * r.x, a * dd.y + b * r.y);
-    stv(res, v, r);
-    stv(d1, v, dn);
-    stv(x, v, make_double2(dd.x + dn.x, dd.y + dn.y));
+    stv<SH>(res, v, r);
+    stv<SH>(d1, v, dn);
+    stv<SH>(x, v, make_double2(dd.x + dn.x, dd.y + dn.y));
 }
 __global__ void k_pre_first(LevelDev L, const double* bvec, double* res, double* d0, double* d1, double* x, int deg,
                             const double* lam, double ratio, const double* live) {
@@ -527,11 +578,13 @@ __global__ void k_pre_first(LevelDev L, const double* bvec, double* res, double*
 }
 
 // r = b - A x (stencil) or r = b - Ax (precomputed)
+template <bool SH = false, int G = 1>
 __device__ __forceinline__ void v_resid(const LevelDev& L, const double* Ax, const double* x, const double* b,
-                                        double* r, long long v) {
-    const double2 w = Ax ? ldv(Ax, v) : st_apply(L, x, v);
-    const double2 bv = ldv(b, v);
-    stv(r, v, make_double2(bv.x - w.x, bv.y - w.y));
+                                        double* r, long long v, int q = 0) {
+    const double2 w = Ax ? ldv<SH>(Ax, v) : st_apply<SH, G>(L, x, v, q);
+    if (G > 1 && q != 0) return;
+    const double2 bv = ldv<SH>(b, v);
+    stv<SH>(r, v, make_double2(bv.x - w.x, bv.y - w.y));
 }
 __global__ void k_resid(LevelDev L, const double* Ax, const double* x, const double* b, double* r, const double* live) {
     if (!gmg_live(live)) return;
@@ -542,14 +595,17 @@ __global__ void k_resid(LevelDev L, const double* Ax, const double* x, const dou
 
 // Post-smoother entry with cheb0 fused into the residual: res = D^-1 (b - A x), d0 = res/theta.
 // x is NOT updated here (neighbours still read it); the following step adds d0 (addd).
+template <bool SH = false, int G = 1>
 __device__ __forceinline__ void v_post_first(const LevelDev& L, const double* x, const double* b, double* res,
-                                             double* d0, const Cheb& c, long long v) {
-    const double2 w = st_apply(L, x, v);
-    const double2 bv = ldv(b, v);
+                                             double* d0, const Cheb& c, long long v, int q = 0) {
+    const double2 w = st_apply<SH, G>(L, x, v, q);
+    if (G > 1 && q != 0) return;
+    const double2 bv = ldv<SH>(b, v);
     const double2 s = make_double2(bv.x - w.x, bv.y - w.y);
-    const double2 r = bmul(L.Dinv, L.nv, v, s.x, s.y);
-    stv(res, v, r);
-    stv(d0, v, make_double2(r.x / c.theta, r.y / c.theta));
+    const double2 r = bmulT<SH>(L.Dinv, L.nv, v, s.x, s.y);
+    stv<SH>(res, v, r);
+    const double it = c.itheta;
+    stv<SH>(d0, v, make_double2(r.x * it, r.y * it));
 }
 __global__ void k_post_first(LevelDev L, const double* x, const double* b, double* res, double* d0,
                              const double* lam, double ratio, const double* live) {
@@ -571,36 +627,44 @@ __global__ void k_add(long long nv, const double* d, double* x, const double* li
     }
 }
 
-// 2:1 restriction b_c = P^T r_f (with masks), one thread per coarse vertex
-__device__ __forceinline__ void v_restrict(const LevelDev& F, const LevelDev& Cd, const unsigned char* maskc,
-                                           const double* r, double* bc, long long v) {
+// Weight of fine index f (0..nf) on coarse index C under the 2:1 ceil-rule interpolation (p1d).
+__device__ __forceinline__ double w1d(int f, int nf, int C) {
+    if (f < 0 || f > nf) return 0.0;
+    if ((f & 1) == 0) return (f >> 1) == C ? 1.0 : 0.0;
+    if (f == nf) return ((f + 1) >> 1) == C ? 1.0 : 0.0;
+    return (((f - 1) >> 1) == C || ((f + 1) >> 1) == C) ? 0.5 : 0.0;
+}
+// 2:1 restriction b_c = P^T r_f (with masks), one thread per coarse vertex; fv(f) = fine value.
+// The 3x3 fine neighbourhood is gathered unconditionally (clamped addresses, zero weights).
+template <bool SH = false, class FV>
+__device__ __forceinline__ void v_restrict_f(const LevelDev& F, const LevelDev& Cd, const unsigned char* maskc,
+                                             FV fv, double* bc, long long v) {
     const int nvyf = F.ny + 1, nvyc = Cd.ny + 1;
-    const int I = (int)(v / nvyc), J = (int)(v % nvyc);
+    const int vi = (int)v;
+    const int I = vi / nvyc, J = vi - (vi / nvyc) * nvyc;
     const unsigned mC = maskc[v];
     double s0 = 0.0, s1 = 0.0;
-    for (int fi = 2 * I - 1; fi <= 2 * I + 1; ++fi) {
-        if (fi < 0 || fi > F.nx) continue;
-        int cx[2]; double wx[2];
-        const int nxw = p1d(fi, F.nx, cx, wx);
-        double wfx = 0.0;
-        for (int a = 0; a < nxw; ++a) if (cx[a] == I) wfx = wx[a];
-        if (wfx == 0.0) continue;
-        for (int fj = 2 * J - 1; fj <= 2 * J + 1; ++fj) {
-            if (fj < 0 || fj > F.ny) continue;
-            int cy[2]; double wy[2];
-            const int nyw = p1d(fj, F.ny, cy, wy);
-            double wfy = 0.0;
-            for (int b = 0; b < nyw; ++b) if (cy[b] == J) wfy = wy[b];
-            if (wfy == 0.0) continue;
-            const long long f = (long long)fi * nvyf + fj;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const int fi = 2 * I - 1 + a;
+        const double wfx = w1d(fi, F.nx, I);
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+            const int fj = 2 * J - 1 + b;
+            const double w = wfx * w1d(fj, F.ny, J);
+            const long long f = (long long)min(max(fi, 0), F.nx) * nvyf + min(max(fj, 0), F.ny);
             const unsigned mf = F.mask ? F.mask[f] : 0u;
-            const double2 rv = ldv(r, f);
-            const double w = wfx * wfy;
-            if (!(mf & 1u)) s0 += w * rv.x;
-            if (!(mf & 2u)) s1 += w * rv.y;
+            const double2 rv = fv(f);
+            if (w != 0.0 && !(mf & 1u)) s0 += w * rv.x;
+            if (w != 0.0 && !(mf & 2u)) s1 += w * rv.y;
         }
     }
-    stv(bc, v, make_double2((mC & 1u) ? 0.0 : s0, (mC & 2u) ? 0.0 : s1));
+    stv<SH>(bc, v, make_double2((mC & 1u) ? 0.0 : s0, (mC & 2u) ? 0.0 : s1));
+}
+template <bool SH = false>
+__device__ __forceinline__ void v_restrict(const LevelDev& F, const LevelDev& Cd, const unsigned char* maskc,
+                                           const double* r, double* bc, long long v) {
+    v_restrict_f<SH>(F, Cd, maskc, [&](long long f) { return ldv<SH>(r, f); }, bc, v);
 }
 __global__ void k_restrict(LevelDev F, LevelDev Cd, const unsigned char* maskc, const double* r, double* bc,
                            const double* live) {
@@ -611,27 +675,39 @@ __global__ void k_restrict(LevelDev F, LevelDev Cd, const unsigned char* maskc, 
 }
 
 // 2:1 prolongation x_f += P x_c (with masks), one thread per fine vertex
-__device__ __forceinline__ void v_prolong(const LevelDev& F, const LevelDev& Cd, const unsigned char* maskc,
-                                          const double* xc, double* xf, long long v) {
+template <bool SH = false>
+__device__ __forceinline__ double2 pval(const LevelDev& F, const LevelDev& Cd, const unsigned char* maskc,
+                                        const double* xc, long long v) {  // (P x_c) at fine vertex v
     const int nvyf = F.ny + 1, nvyc = Cd.ny + 1;
-    const int fi = (int)(v / nvyf), fj = (int)(v % nvyf);
-    const unsigned mf = F.mask ? F.mask[v] : 0u;
+    const int vi = (int)v;
+    const int fi = vi / nvyf, fj = vi - (vi / nvyf) * nvyf;
     int cx[2], cy[2]; double wx[2], wy[2];
     const int nxw = p1d(fi, F.nx, cx, wx), nyw = p1d(fj, F.ny, cy, wy);
+    if (nxw == 1) { cx[1] = cx[0]; wx[1] = 0.0; }
+    if (nyw == 1) { cy[1] = cy[0]; wy[1] = 0.0; }
     double s0 = 0.0, s1 = 0.0;
-    for (int a = 0; a < nxw; ++a)
-        for (int b = 0; b < nyw; ++b) {
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
             const long long c = (long long)cx[a] * nvyc + cy[b];
             const unsigned mC = maskc[c];
-            const double2 xv = ldv(xc, c);
+            const double2 xv = ldv<SH>(xc, c);
             const double w = wx[a] * wy[b];
-            if (!(mC & 1u)) s0 += w * xv.x;
-            if (!(mC & 2u)) s1 += w * xv.y;
+            if (w != 0.0 && !(mC & 1u)) s0 += w * xv.x;
+            if (w != 0.0 && !(mC & 2u)) s1 += w * xv.y;
         }
-    double2 o = ldv(xf, v);
-    if (!(mf & 1u)) o.x += s0;
-    if (!(mf & 2u)) o.y += s1;
-    stv(xf, v, o);
+    return make_double2(s0, s1);
+}
+template <bool SH = false>
+__device__ __forceinline__ void v_prolong(const LevelDev& F, const LevelDev& Cd, const unsigned char* maskc,
+                                          const double* xc, double* xf, long long v) {
+    const unsigned mf = F.mask ? F.mask[v] : 0u;
+    const double2 s = pval<SH>(F, Cd, maskc, xc, v);
+    double2 o = ldv<SH>(xf, v);
+    if (!(mf & 1u)) o.x += s.x;
+    if (!(mf & 2u)) o.y += s.y;
+    stv<SH>(xf, v, o);
 }
 __global__ void k_prolong(LevelDev F, LevelDev Cd, const unsigned char* maskc, const double* xc, double* xf,
                           const double* live) {
@@ -775,6 +851,325 @@ __global__ void k_expand_centres(const Geo2 g, const unsigned char* mask0, const
     }
 }
 
+// ---- the coarse part of the V-cycle in one persistent launch -------------------------------------
+// Both level-0 transfers and levels 1..nl-1 run in one cooperative kernel: levels 1..lc-1 as
+// grid-wide phases separated by a software grid barrier, levels lc..nl-1 (the tail) on CTA 0 with
+// operators, masks, the dense coarse inverse and all vectors staged in shared memory (operators
+// are prefetched by cp.async at kernel entry, behind the grid phases).  The per-vertex functions,
+// and their order, are those of the launch-per-phase cycle, so the result is bitwise identical;
+// what goes away is ~30 dependent launches per V-cycle and the L2 round trips of the tail.
+constexpr int kMaxLev = 16;  // = the S_GMG0 lambda slots
+constexpr int kTailSmemMax = 200 * 1024;
+constexpr int kMaxDeg = 8;
+struct CCoef {  // per-level Chebyshev coefficients, computed once per launch into shared memory
+    Cheb c;
+    double a[kMaxDeg], b[kMaxDeg];
+};
+struct CLev {
+    LevelDev L;
+    double *x, *b, *r, *d0, *d1, *res;
+};
+struct TOff {  // byte offsets of a tail level's arrays in shared memory (-1: not staged)
+    int A, Dinv, mask, x, b, r, d0, d1, res;
+};
+struct CoarseArgs {
+    Geo2 g;
+    LevelDev L0;                  // level-0 corner view (mask: as the level-0 transfers use it)
+    const unsigned char* mask0;   // level-0 Dirichlet mask for the crossed collapse/expand (or null)
+    const double* r0;             // level-0 residual (restricted)
+    double* z0;                   // level-0 correction (+= P x1)
+    int crossed, nl, lc, deg, ncoarse, ainv_off, coef_off;
+    double ratio;
+    const double* ainv;
+    unsigned int* bar;
+    int skip;                     // timing aid (PF_GMG_SKIP_COARSE): return at entry
+    unsigned long long* trace;    // timing aid (PF_GMG_TRACE): %globaltimer per phase, CTA 0
+    CLev lev[kMaxLev];
+    TOff toff[kMaxLev];
+};
+
+// software grid barrier (all CTAs co-resident: cooperative launch).  One arrival word: CTA 0 adds
+// 2^31 - (nb - 1), the others 1, so the top bit flips exactly when the last CTA arrives.
+__device__ __forceinline__ void grid_sync(unsigned int* bar) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned int inc = blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1) : 1u;
+        __threadfence();
+        const unsigned int old = atomicAdd(bar, inc);
+        unsigned int cur;
+        do {
+            asm volatile("ld.acquire.gpu.u32 %0, [%1];\n" : "=r"(cur) : "l"(bar) : "memory");
+        } while (((old ^ cur) & 0x80000000u) == 0);
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ void cp16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+                 "l"(src));
+}
+__device__ __forceinline__ void stage16(unsigned char* dst, const void* src, long long bytes) {
+    const long long n16 = (bytes + 15) / 16;
+    for (long long i = threadIdx.x; i < n16; i += kTB) cp16(dst + 16 * i, (const unsigned char*)src + 16 * i);
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define TR()                                                                        \
+    do {                                                                            \
+        if (A.trace && blockIdx.x == 0 && threadIdx.x == 0) A.trace[ntr++] = gtimer(); \
+    } while (0)
+
+__global__ void __launch_bounds__(kTB, 1) k_gmg_coarse(const __grid_constant__ CoarseArgs A, const double* lam,
+                                                       const double* live) {
+    if (!gmg_live(live) || A.skip) return;  // uniform: the flags are not written during the launch
+    extern __shared__ __align__(16) unsigned char sm[];
+    const long long tid = blockIdx.x * (long long)kTB + threadIdx.x;
+    const long long nth = (long long)gridDim.x * kTB;
+    const int deg = A.deg;
+    const int t0 = threadIdx.x;
+    // stencil phases: 4 lanes per vertex when the level is small enough (shorter dependent chains)
+    using G1 = std::integral_constant<int, 1>;
+    using G4 = std::integral_constant<int, 4>;
+    auto grid_each = [&](long long nv, auto fn) {
+        if (4 * nv <= nth)
+            for (long long e = tid; e < 4 * nv; e += nth) fn(G4{}, e >> 2, (int)(e & 3));
+        else
+            for (long long v = tid; v < nv; v += nth) fn(G1{}, v, 0);
+    };
+    auto cta_each = [&](long long nv, auto fn) {
+        for (long long e = t0; e < 4 * nv; e += kTB) fn(G4{}, e >> 2, (int)(e & 3));
+    };
+    int ntr = 0;
+    TR();
+    CCoef* coef = reinterpret_cast<CCoef*>(sm + A.coef_off);
+    if (t0 < A.nl) {  // Chebyshev coefficients of every level (read by the phases after the first barrier)
+        CCoef& q = coef[t0];
+        q.c = cheb_of(lam + t0, A.ratio);
+        for (int k = 1; k < deg && k < kMaxDeg; ++k) cheb_ab(q.c, k, q.a[k], q.b[k]);
+    }
+    if (blockIdx.x == 0) {  // tail operators, masks and the dense inverse: constant during the cycle
+        for (int l = A.lc; l < A.nl; ++l) {
+            const CLev& V = A.lev[l];
+            const TOff& o = A.toff[l];
+            if (o.A >= 0) stage16(sm + o.A, V.L.A, 288LL * V.L.nv);
+            if (o.Dinv >= 0) stage16(sm + o.Dinv, V.L.Dinv, 32LL * V.L.nv);
+            stage16(sm + o.mask, V.L.mask, V.L.nv);
+        }
+        if (A.ainv_off >= 0) stage16(sm + A.ainv_off, A.ainv, 8LL * A.ncoarse * A.ncoarse);
+        asm volatile("cp.async.commit_group;\n" ::);
+    }
+    // level 0 -> 1 restriction (crossed: centres collapsed onto the corners on the fly)
+    {
+        const CLev& C = A.lev[1];
+        if (A.crossed) {
+            const Geo2& g = A.g;
+            auto collapse = [&](long long v) -> double2 {
+                const int i = (int)(v / g.nvy), j = (int)(v % g.nvy);
+                const unsigned m = vmask(A.mask0, v);
+                const double2 rv = ldv(A.r0, v);
+                double s0 = (m & 1u) ? 0.0 : rv.x, s1 = (m & 2u) ? 0.0 : rv.y;
+                for (int ci = i - 1; ci <= i; ++ci)
+                    for (int cj = j - 1; cj <= j; ++cj) {
+                        if (ci < 0 || cj < 0 || ci >= g.nx || cj >= g.ny) continue;
+                        const double2 rc = ldv(A.r0, g.nc + (long long)ci * g.ny + cj);
+                        s0 += 0.25 * rc.x;
+                        s1 += 0.25 * rc.y;
+                    }
+                return make_double2(s0, s1);
+            };
+            for (long long v = tid; v < C.L.nv; v += nth) v_restrict_f(A.L0, C.L, C.L.mask, collapse, C.b, v);
+        } else {
+            for (long long v = tid; v < C.L.nv; v += nth) v_restrict(A.L0, C.L, C.L.mask, A.r0, C.b, v);
+        }
+    }
+    grid_sync(A.bar);
+        TR();
+    // descend through the grid-wide levels
+    for (int l = 1; l < A.lc; ++l) {
+        const CLev& V = A.lev[l];
+        const Cheb c = coef[l].c;
+        double a = 0.0, b = 0.0;
+        if (deg > 1) { a = coef[l].a[1]; b = coef[l].b[1]; }
+        grid_each(V.L.nv, [&](auto g, long long v, int q) { v_pre_first<false, decltype(g)::value>(V.L, V.b, V.res, V.d0, V.d1, V.x, c, a, b, deg, v, q); });
+        grid_sync(A.bar);
+        TR();
+        double* d = V.d0;
+        double* dn = V.d1;
+        if (deg > 1) { double* t = d; d = dn; dn = t; }
+        for (int k = 2; k < deg; ++k) {
+            a = coef[l].a[k]; b = coef[l].b[k];
+            grid_each(V.L.nv, [&](auto g, long long v, int q) { v_cheb_step<false, decltype(g)::value>(V.L, nullptr, d, dn, V.res, V.x, a, b, 0, v, q); });
+            grid_sync(A.bar);
+        TR();
+            double* t = d; d = dn; dn = t;
+        }
+        grid_each(V.L.nv, [&](auto g, long long v, int q) { v_resid<false, decltype(g)::value>(V.L, nullptr, V.x, V.b, V.r, v, q); });
+        grid_sync(A.bar);
+        TR();
+        const CLev& C = A.lev[l + 1];
+        for (long long v = tid; v < C.L.nv; v += nth) v_restrict(V.L, C.L, C.L.mask, V.r, C.b, v);
+        grid_sync(A.bar);
+        TR();
+    }
+    // tail on CTA 0, in shared memory
+    if (blockIdx.x == 0) {
+        asm volatile("cp.async.wait_group 0;\n" ::);
+        auto view = [&](int l) {
+            const TOff& o = A.toff[l];
+            CLev T = A.lev[l];
+            T.L.A = o.A >= 0 ? (const double*)(sm + o.A) : nullptr;
+            T.L.Dinv = o.Dinv >= 0 ? (const double*)(sm + o.Dinv) : nullptr;
+            T.L.mask = sm + o.mask;
+            T.x = (double*)(sm + o.x);
+            T.b = (double*)(sm + o.b);
+            T.r = o.r >= 0 ? (double*)(sm + o.r) : nullptr;
+            T.d0 = o.d0 >= 0 ? (double*)(sm + o.d0) : nullptr;
+            T.d1 = o.d1 >= 0 ? (double*)(sm + o.d1) : nullptr;
+            T.res = o.res >= 0 ? (double*)(sm + o.res) : nullptr;
+            return T;
+        };
+        {
+            const CLev T = view(A.lc);
+            for (long long v = t0; v < T.L.nv; v += kTB) stv<true>(T.b, v, ldv(A.lev[A.lc].b, v));
+        }
+        __syncthreads();
+        TR();
+        for (int l = A.lc; l < A.nl - 1; ++l) {
+            const CLev V = view(l);
+            const Cheb c = coef[l].c;
+            double a = 0.0, b = 0.0;
+            if (deg > 1) { a = coef[l].a[1]; b = coef[l].b[1]; }
+            cta_each(V.L.nv, [&](auto g, long long v, int q) { v_pre_first<true, decltype(g)::value>(V.L, V.b, V.res, V.d0, V.d1, V.x, c, a, b, deg, v, q); });
+            __syncthreads();
+            double* d = V.d1;
+            double* dn = V.d0;
+            for (int k = 2; k < deg; ++k) {
+                a = coef[l].a[k]; b = coef[l].b[k];
+                cta_each(V.L.nv, [&](auto g, long long v, int q) { v_cheb_step<true, decltype(g)::value>(V.L, nullptr, d, dn, V.res, V.x, a, b, 0, v, q); });
+                __syncthreads();
+                double* tmp = d; d = dn; dn = tmp;
+            }
+            cta_each(V.L.nv, [&](auto g, long long v, int q) { v_resid<true, decltype(g)::value>(V.L, nullptr, V.x, V.b, V.r, v, q); });
+            __syncthreads();
+            const CLev C = view(l + 1);
+            for (long long v = t0; v < C.L.nv; v += kTB) v_restrict<true>(V.L, C.L, C.L.mask, V.r, C.b, v);
+            __syncthreads();
+        }
+        {   // coarsest: x = Ainv b, one warp per row
+            const CLev C = view(A.nl - 1);
+            const double* ainv = A.ainv_off >= 0 ? (const double*)(sm + A.ainv_off) : A.ainv;
+            const int n = A.ncoarse, lane = t0 & 31;
+            for (int r = t0 >> 5; r < n; r += kTB / 32) {
+                double s = 0.0;
+                for (int q = lane; q < n; q += 32)
+                    s += (A.ainv_off >= 0 ? ainv[(size_t)r * n + q] : __ldg(ainv + (size_t)r * n + q)) * C.b[q];
+                s = warp_sum(s);
+                if (lane == 0) C.x[r] = s;
+            }
+            __syncthreads();
+        }
+        for (int l = A.nl - 2; l >= A.lc; --l) {
+            const CLev V = view(l);
+            const CLev C = view(l + 1);
+            const Cheb c = coef[l].c;
+            for (long long v = t0; v < V.L.nv; v += kTB) v_prolong<true>(V.L, C.L, C.L.mask, C.x, V.x, v);
+            __syncthreads();
+            cta_each(V.L.nv, [&](auto g, long long v, int q) { v_post_first<true, decltype(g)::value>(V.L, V.x, V.b, V.res, V.d0, c, v, q); });
+            __syncthreads();
+            if (deg <= 1) {
+                for (long long v = t0; v < V.L.nv; v += kTB) {
+                    const double2 dv = ldv<true>(V.d0, v);
+                    double2 xv = ldv<true>(V.x, v);
+                    xv.x += dv.x;
+                    xv.y += dv.y;
+                    stv<true>(V.x, v, xv);
+                }
+                __syncthreads();
+            }
+            double* d = V.d0;
+            double* dn = V.d1;
+            for (int k = 1; k < deg; ++k) {
+                double a, b;
+                a = coef[l].a[k]; b = coef[l].b[k];
+                cta_each(V.L.nv, [&](auto g, long long v, int q) { v_cheb_step<true, decltype(g)::value>(V.L, nullptr, d, dn, V.res, V.x, a, b, k == 1, v, q); });
+                __syncthreads();
+                double* tmp = d; d = dn; dn = tmp;
+            }
+        }
+        {
+            const CLev T = view(A.lc);
+            for (long long v = t0; v < T.L.nv; v += kTB) stv(A.lev[A.lc].x, v, ldv<true>(T.x, v));
+        }
+    }
+    grid_sync(A.bar);
+        TR();
+    // ascend through the grid-wide levels
+    for (int l = A.lc - 1; l >= 1; --l) {
+        const CLev& V = A.lev[l];
+        const CLev& C = A.lev[l + 1];
+        const Cheb c = coef[l].c;
+        for (long long v = tid; v < V.L.nv; v += nth) v_prolong(V.L, C.L, C.L.mask, C.x, V.x, v);
+        grid_sync(A.bar);
+        TR();
+        grid_each(V.L.nv, [&](auto g, long long v, int q) { v_post_first<false, decltype(g)::value>(V.L, V.x, V.b, V.res, V.d0, c, v, q); });
+        grid_sync(A.bar);
+        TR();
+        if (deg <= 1) {
+            for (long long v = tid; v < V.L.nv; v += nth) {
+                const double2 dv = ldv(V.d0, v);
+                double2 xv = ldv(V.x, v);
+                xv.x += dv.x;
+                xv.y += dv.y;
+                stv(V.x, v, xv);
+            }
+            grid_sync(A.bar);
+        TR();
+        }
+        double* d = V.d0;
+        double* dn = V.d1;
+        for (int k = 1; k < deg; ++k) {
+            double a, b;
+            a = coef[l].a[k]; b = coef[l].b[k];
+            grid_each(V.L.nv, [&](auto g, long long v, int q) { v_cheb_step<false, decltype(g)::value>(V.L, nullptr, d, dn, V.res, V.x, a, b, k == 1, v, q); });
+            grid_sync(A.bar);
+        TR();
+            double* tmp = d; d = dn; dn = tmp;
+        }
+    }
+    // level 1 -> 0 prolongation (crossed: centres take the mean of their corners' corrections)
+    {
+        const CLev& C = A.lev[1];
+        if (A.crossed) {
+            const Geo2& g = A.g;
+            for (long long v = tid; v < g.nv; v += nth) {
+                double2 o = ldv(A.z0, v);
+                if (v < g.nc) {
+                    const unsigned m = vmask(A.mask0, v);
+                    const double2 a = pval(A.L0, C.L, C.L.mask, C.x, v);
+                    if (!(m & 1u)) o.x += a.x;
+                    if (!(m & 2u)) o.y += a.y;
+                } else {
+                    const long long cell = v - g.nc;
+                    const long long v00 = (cell / g.ny) * g.nvy + cell % g.ny;
+                    const long long cs[4] = {v00, v00 + g.nvy, v00 + 1, v00 + g.nvy + 1};
+                    for (int q = 0; q < 4; ++q) {
+                        const double2 a = pval(A.L0, C.L, C.L.mask, C.x, cs[q]);
+                        o.x += 0.25 * a.x;
+                        o.y += 0.25 * a.y;
+                    }
+                }
+                stv(A.z0, v, o);
+            }
+        } else {
+            for (long long v = tid; v < A.L0.nv; v += nth) v_prolong(A.L0, C.L, C.L.mask, C.x, A.z0, v);
+        }
+    }
+}
+
 // z_f = 0 helper + level-0 vector ops
 __global__ void k_fill0(long long n, double* x) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
@@ -818,6 +1213,7 @@ size_t gmg_bytes(const Ctx* c) {
     }
     const long long nco = 2 * c->glev.back().nv;
     tot += 2 * al(sizeof(double) * nco * nco);
+    tot += al(2 * sizeof(unsigned int));  // grid barrier
     return tot + 4096;
 }
 
@@ -842,6 +1238,7 @@ void gmg_bind(Ctx* c, char* base) {
     const long long nco = 2 * c->glev.back().nv;
     c->gmg_dense = (double*)take(sizeof(double) * nco * nco);
     c->gmg_ainv = (double*)take(sizeof(double) * nco * nco);
+    c->gmg_bar = (unsigned int*)take(2 * sizeof(unsigned int));
 }
 
 static LevelDev ldev(const Ctx* c, int l) {
@@ -963,6 +1360,191 @@ static int launch_tail(Ctx* c, int lc, cudaStream_t st, const double* live) {
     return PF_OK;
 }
 
+// Level-0 pre-smoother from z = 0 with the matrix-free fine operator (fused epilogues); leaves the
+// fine residual r - A z in L0.r.
+static int fine_pre(Ctx* c, const double* b, double* x, cudaStream_t st, const double* live, bool cheb0_done) {
+    GLevel& L = c->glev[0];
+    const long long nv = L.nv;
+    const int deg = std::max(1, c->gmg_degree);
+    double* d = L.d0;
+    double* dn = L.d1;
+    if (!cheb0_done)
+        GKB(c, K_GMG, 96.0 * nv, (k_cheb0<<<gblocks(nv), kGB, 0, st>>>(nv, L.Dinv, b, L.res, L.d0, x, 0, c->scal + S_GMG0, c->gmg_ratio, live)));
+    for (int k = 1; k < deg; ++k) {
+        GmgEpi e = epi0(c, live);
+        e.dnext = dn;
+        e.xs = x;
+        e.k = k;
+        PF_TRY_GMG(launch_Kuu_smooth(c, EPI_CHEB, c->alpha_ws, d, e, st));
+        std::swap(d, dn);
+    }
+    GmgEpi e = epi0(c, live);
+    e.bvec = b;
+    e.rout = L.r;
+    return launch_Kuu_smooth(c, EPI_RESID, c->alpha_ws, x, e, st);
+}
+
+// Level-0 post-smoother: res = D^-1 (b - A x), d0 = res/theta ; steps (x += d0 on step 1); the PCG
+// r.z rides on the last step when rz_first >= 0.
+static int fine_post(Ctx* c, const double* b, double* x, cudaStream_t st, const double* live, int rz_first,
+                     bool* rz_done) {
+    GLevel& L = c->glev[0];
+    const long long nv = L.nv;
+    const int deg = std::max(1, c->gmg_degree);
+    double* d = L.d0;
+    double* dn = L.d1;
+    GmgEpi e = epi0(c, live);
+    e.bvec = b;
+    e.dnext = L.d0;
+    PF_TRY_GMG(launch_Kuu_smooth(c, EPI_RESID_CHEB0, c->alpha_ws, x, e, st));
+    if (deg <= 1) GKB(c, K_GMG, 48.0 * nv, (k_add<<<gblocks(nv), kGB, 0, st>>>(nv, L.d0, x, live)));
+    for (int k = 1; k < deg; ++k) {
+        GmgEpi es = epi0(c, live);
+        es.dnext = dn;
+        es.xs = x;
+        es.k = k;
+        if (k == deg - 1 && rz_first >= 0) {
+            es.rcg = b;
+            es.rz_first = rz_first;
+            if (rz_done) *rz_done = true;
+        }
+        PF_TRY_GMG(launch_Kuu_smooth(c, k == 1 ? EPI_CHEB_ADDD : EPI_CHEB, c->alpha_ws, d, es, st));
+        std::swap(d, dn);
+    }
+    return PF_OK;
+}
+
+#define GCU(c, x, where) PF_TRY_GMG(check_cuda((c), (x), (where)))
+
+// Tail of the persistent coarse cycle: the first tail level lc and the shared-memory layout.
+static int coarse_plan(const Ctx* c, CoarseArgs& a) {
+    const int nl = (int)c->glev.size();
+    auto a16 = [](long long b) { return (int)((b + 15) & ~15LL); };
+    auto level_bytes = [&](int l) -> long long {
+        const long long nv = c->glev[l].nv;
+        long long b = a16(nv);                        // mask
+        if (l < nl - 1) b += 288 * nv + 32 * nv + 6 * 16 * nv;  // A, Dinv, x b r d0 d1 res
+        else b += 2 * 16 * nv;                        // x b
+        return b;
+    };
+    const long long n = 2 * c->glev[nl - 1].nv;
+    const long long ainv_b = 8 * n * n;
+    long long tot = level_bytes(nl - 1) + (long long)sizeof(CCoef) * nl + 16;
+    const bool ainv_sm = ainv_b <= 64 * 1024;
+    if (ainv_sm) tot += ainv_b;
+    int lc = nl - 1;
+    while (lc > 1 && lc - 1 < kMaxLev && tot + level_bytes(lc - 1) <= kTailSmemMax) tot += level_bytes(--lc);
+    if (tot > kTailSmemMax || nl > kMaxLev) return -1;
+    a.lc = lc;
+    int off = 0;
+    auto take = [&](long long b) { const int o = off; off += a16(b); return o; };
+    for (int l = 0; l < kMaxLev; ++l) a.toff[l] = TOff{-1, -1, -1, -1, -1, -1, -1, -1, -1};
+    for (int l = lc; l < nl; ++l) {
+        const long long nv = c->glev[l].nv;
+        TOff& o = a.toff[l];
+        if (l < nl - 1) {
+            o.A = take(288 * nv);
+            o.Dinv = take(32 * nv);
+        }
+        o.mask = take(nv);
+        o.x = take(16 * nv);
+        o.b = take(16 * nv);
+        if (l < nl - 1) {
+            o.r = take(16 * nv);
+            o.d0 = take(16 * nv);
+            o.d1 = take(16 * nv);
+            o.res = take(16 * nv);
+        }
+    }
+    a.ainv_off = ainv_sm ? take(ainv_b) : -1;
+    a.coef_off = take((long long)sizeof(CCoef) * nl);
+    return off;
+}
+
+static int launch_coarse(Ctx* c, const double* r0, double* z0, cudaStream_t st, const double* live) {
+    const Geo2& g = c->g;
+    const int nl = (int)c->glev.size();
+    CoarseArgs a;
+    memset(&a, 0, sizeof(a));
+    const int smem = coarse_plan(c, a);
+    if (smem < 0) return set_error(c, PF_EINVAL, "gmg: coarse tail does not fit in shared memory");
+    a.g = g;
+    a.crossed = g.pattern == PF_CROSSED;
+    a.mask0 = g.has_bc ? c->glev[0].mask : nullptr;
+    a.L0 = ldev(c, 0);
+    a.L0.mask = a.crossed ? nullptr : a.mask0;  // crossed: the collapse/expand apply the fine mask
+    a.r0 = r0;
+    a.z0 = z0;
+    a.nl = nl;
+    a.deg = std::max(1, c->gmg_degree);
+    a.ratio = c->gmg_ratio;
+    a.ainv = c->gmg_ainv;
+    a.ncoarse = (int)(2 * c->glev[nl - 1].nv);
+    a.bar = c->gmg_bar;
+    a.skip = c->gmg_coarse == 2;
+    static unsigned long long* trace = nullptr;
+    static int ntrace_calls = 0;
+    if (getenv("PF_GMG_TRACE") && !trace) cudaMalloc(&trace, 128 * sizeof(unsigned long long));
+    a.trace = trace;
+    for (int l = 1; l < nl; ++l) {
+        GLevel& L = c->glev[l];
+        a.lev[l].L = ldev(c, l);
+        a.lev[l].x = L.x; a.lev[l].b = L.b; a.lev[l].r = L.r;
+        a.lev[l].d0 = L.d0; a.lev[l].d1 = L.d1; a.lev[l].res = L.res;
+    }
+    static int smem_attr = -1;
+    if (smem > smem_attr) {
+        GCU(c, cudaFuncSetAttribute(k_gmg_coarse, cudaFuncAttributeMaxDynamicSharedMemorySize, kTailSmemMax),
+              "coarse smem attribute");
+        smem_attr = kTailSmemMax;
+    }
+    static int nb_cache = 0, nb_smem = -1;
+    if (nb_smem != smem) {
+        int dev = 0, nsm = 0, per = 0;
+        GCU(c, cudaGetDevice(&dev), "device");
+        GCU(c, cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev), "sm count");
+        GCU(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_gmg_coarse, kTB, smem), "occupancy");
+        if (per < 1) return set_error(c, PF_ECUDA, "gmg: coarse-cycle kernel cannot be resident");
+        nb_cache = nsm * per;
+        nb_smem = smem;
+    }
+    // algorithmic bytes: those of the per-phase launches it replaces
+    const int deg = a.deg;
+    const GLevel& L1 = c->glev[1];
+    double bytes = a.crossed ? 48.0 * g.nc + 16.0 * g.nc + 17.0 * L1.nv + 32.0 * g.nc + 17.0 * L1.nv + 48.0 * g.nv
+                             : 16.0 * g.nc + 17.0 * L1.nv + 32.0 * g.nc + 17.0 * L1.nv;
+    for (int l = 1; l < nl; ++l) {
+        const double nv = (double)c->glev[l].nv;
+        if (l == nl - 1) { bytes += 8.0 * a.ncoarse * a.ncoarse + 32.0 * a.ncoarse; break; }
+        const double nvc = (double)c->glev[l + 1].nv;
+        bytes += (deg > 1 ? 416.0 : 96.0) * nv + 416.0 * std::max(0, deg - 2) * nv + 336.0 * nv + 16.0 * nv + 17.0 * nvc;
+        bytes += 32.0 * nv + 17.0 * nvc + 400.0 * nv + (deg <= 1 ? 48.0 : 416.0 * (deg - 1)) * nv;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(nb_cache);
+    cfg.blockDim = dim3(kTB);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    const double* lam = c->scal + S_GMG0;
+    cudaError_t le = cudaSuccess;
+    if (trace) cudaMemsetAsync(trace, 0, 128 * sizeof(unsigned long long), st);
+    GKB(c, K_GMG, bytes, (le = cudaLaunchKernelEx(&cfg, k_gmg_coarse, a, lam, live)));
+    if (trace && ++ntrace_calls % 8 == 5) {  // eager mode only (PF_NO_GRAPHS): print one cycle's phases
+        unsigned long long h[128];
+        cudaMemcpyAsync(h, trace, sizeof h, cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        fprintf(stderr, "coarse cycle nb=%d lc=%d nl=%d smem=%d phases(us):", nb_cache, a.lc, nl, smem);
+        for (int q = 1; q < 128 && h[q]; ++q) fprintf(stderr, " %.2f", 1e-3 * (double)(h[q] - h[q - 1]));
+        fprintf(stderr, "\n");
+    }
+    return check_cuda(c, le, "coarse-cycle launch");
+}
+
 // z = M r : one V-cycle, level 0 vectors are the PCG r (input) and z (output).
 // cheb0_done: the caller already wrote the level-0 cheb0 (res = D^-1 r, d0 = z = res / theta;
 // k_cg_update_gmg).  rz_first >= 0: fuse the PCG r . z into the last fine smoother step
@@ -975,6 +1557,12 @@ int gmg_vcycle(Ctx* c, const double* r_in, double* z_out, cudaStream_t st, const
     const int deg = std::max(1, c->gmg_degree);
     const double ratio = c->gmg_ratio;
     double* lam = c->scal + S_GMG0;
+    if (c->gmg_coarse && nl <= kMaxLev && deg < kMaxDeg) {  // fine smoothing + one persistent launch for everything coarser
+        PF_TRY_GMG(fine_pre(c, r_in, z_out, st, live, cheb0_done));
+        PF_TRY_GMG(launch_coarse(c, c->glev[0].r, z_out, st, live));
+        PF_TRY_GMG(fine_post(c, r_in, z_out, st, live, rz_first, rz_done));
+        return check_cuda(c, cudaGetLastError(), "gmg vcycle");
+    }
     const int lc = tail_level(c);  // per-level kernels down to level lc, then the one-CTA tail
     // descend through the per-level kernels
     for (int l = 0; l < lc; ++l) {
@@ -986,21 +1574,8 @@ int gmg_vcycle(Ctx* c, const double* r_in, double* z_out, cudaStream_t st, const
         Ld.nv = nv;
         double* d = L.d0;
         double* dn = L.d1;
-        if (l == 0) {  // pre-smooth from x = 0 with the matrix-free fine operator (fused epilogues)
-            if (!cheb0_done)
-                GKB(c, K_GMG, 96.0 * nv, (k_cheb0<<<gblocks(nv), kGB, 0, st>>>(nv, L.Dinv, b, L.res, L.d0, x, 0, lam + l, ratio, live)));
-            for (int k = 1; k < deg; ++k) {
-                GmgEpi e = epi0(c, live);
-                e.dnext = dn;
-                e.xs = x;
-                e.k = k;
-                PF_TRY_GMG(launch_Kuu_smooth(c, EPI_CHEB, c->alpha_ws, d, e, st));
-                std::swap(d, dn);
-            }
-            GmgEpi e = epi0(c, live);
-            e.bvec = b;
-            e.rout = L.r;
-            PF_TRY_GMG(launch_Kuu_smooth(c, EPI_RESID, c->alpha_ws, x, e, st));
+        if (l == 0) {
+            PF_TRY_GMG(fine_pre(c, b, x, st, live, cheb0_done));
         } else {
             GKB(c, K_GMG, (deg > 1 ? 416.0 : 96.0) * nv, (k_pre_first<<<gblocks(nv), kGB, 0, st>>>(Ld, b, L.res, L.d0, L.d1, x, deg, lam + l, ratio, live)));
             if (deg > 1) std::swap(d, dn);
@@ -1058,25 +1633,8 @@ int gmg_vcycle(Ctx* c, const double* r_in, double* z_out, cudaStream_t st, const
         }
         double* d = L.d0;
         double* dn = L.d1;
-        if (l == 0) {  // post-smooth: res = D^-1 (b - A x), d0 = res/theta ; steps (x += d0 on step 1)
-            GmgEpi e = epi0(c, live);
-            e.bvec = b;
-            e.dnext = L.d0;
-            PF_TRY_GMG(launch_Kuu_smooth(c, EPI_RESID_CHEB0, c->alpha_ws, x, e, st));
-            if (deg <= 1) GKB(c, K_GMG, 48.0 * nv, (k_add<<<gblocks(nv), kGB, 0, st>>>(nv, L.d0, x, live)));
-            for (int k = 1; k < deg; ++k) {
-                GmgEpi es = epi0(c, live);
-                es.dnext = dn;
-                es.xs = x;
-                es.k = k;
-                if (k == deg - 1 && rz_first >= 0) {
-                    es.rcg = r_in;
-                    es.rz_first = rz_first;
-                    if (rz_done) *rz_done = true;
-                }
-                PF_TRY_GMG(launch_Kuu_smooth(c, k == 1 ? EPI_CHEB_ADDD : EPI_CHEB, c->alpha_ws, d, es, st));
-                std::swap(d, dn);
-            }
+        if (l == 0) {
+            PF_TRY_GMG(fine_post(c, b, x, st, live, rz_first, rz_done));
         } else {  // residual + cheb0 in one pass; the x += d0 rides on step 1
             GKB(c, K_GMG, 400.0 * nv, (k_post_first<<<gblocks(nv), kGB, 0, st>>>(Ld, x, b, L.res, L.d0, lam + l, ratio, live)));
             if (deg <= 1) GKB(c, K_GMG, 48.0 * nv, (k_add<<<gblocks(nv), kGB, 0, st>>>(nv, L.d0, x, live)));

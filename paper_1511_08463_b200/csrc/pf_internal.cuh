@@ -155,7 +155,7 @@ struct Prof {
 // Shared by the GMG level kernels (pf_gmg.cu) and the fused fine-level strip epilogues (pf_ops2d.cu)
 // so both evaluate the same expressions.
 struct Cheb {
-    double theta, delta, sigma;
+    double theta, delta, sigma, itheta;
 };
 __device__ __forceinline__ Cheb cheb_of(const double* lam, double ratio) {
     const double hi = *lam, lo = hi * ratio;
@@ -163,6 +163,7 @@ __device__ __forceinline__ Cheb cheb_of(const double* lam, double ratio) {
     c.theta = 0.5 * (hi + lo);
     c.delta = 0.5 * (hi - lo);
     c.sigma = c.theta / c.delta;
+    c.itheta = 1.0 / c.theta;
     return c;
 }
 __device__ __forceinline__ double cheb_rho(const Cheb& c, int k) {  // rho_k, rho_0 = 1/sigma
@@ -283,6 +284,8 @@ struct Ctx {
     char* gmg_base = nullptr;
     double* gmg_dense = nullptr;
     double* gmg_ainv = nullptr;
+    unsigned int* gmg_bar = nullptr;   // grid barrier of the persistent coarse-cycle kernel (2 words)
+    int gmg_coarse = 1;             // persistent coarse cycle (0: one launch per phase, PF_GMG_LEGACY)
     int gmg_degree = 2;
     int gmg_built = 0;              // hierarchy valid for reuse (pf_lin_opts.gmg_reuse)
     long long gmg_its0 = -1;        // iterations of the first elastic solve on it (-1: none yet)

@@ -270,3 +270,32 @@ def test_newton_coupled_solver_variants_converge_like_fieldsplit(variant):
     assert r1.converged and r2.converged
     assert rel(s1.u.cpu().numpy(), s2.u.cpu().numpy()) < 1e-6
     assert float((s1.alpha - s2.alpha).abs().max()) < 1e-6
+
+
+@pytest.mark.parametrize("pattern", ["union_jack", "right", "crossed"])
+@pytest.mark.parametrize("shape", [(64, 64), (57, 33), (200, 20), (3, 2), (300, 70)])
+def test_persistent_coarse_cycle_matches_the_per_phase_cycle(pattern, shape, monkeypatch):
+    """The one-launch coarse V-cycle (grid-barrier phases + shared-memory tail) runs the same
+    per-vertex arithmetic in the same order as one launch per phase: the same iterates up to
+    summation order (lanes sharing a vertex) and FMA contraction: both are converged solves
+    of the same system (rtol 1e-10) with the same iteration count."""
+    import paper_1511_08463_b200 as pf
+    nx, ny = shape
+    out = {}
+    for legacy in (False, True):
+        if legacy:
+            monkeypatch.setenv("PF_GMG_LEGACY", "1")
+        else:
+            monkeypatch.delenv("PF_GMG_LEGACY", raising=False)
+        prob, om, rng = make_pair(pattern, "plane_strain", "AT2", nx, ny, lx=1.0, ly=ny / nx,
+                                  hetero=True, eps0=False)
+        v = om.mesh.vertices
+        a = np.where(np.abs(v[:, 0] - 0.5) < 1.5 / nx, 1.0, rng.uniform(0, 0.2, om.nv))
+        st = pf.State(dev(rng.standard_normal(om.nu_dofs)), dev(a), dev(np.zeros(om.nv)))
+        cfg = pf.SolverConfig(elastic_solver="cg", elastic_rtol=1e-10, elastic_precond="gmg",
+                              warm_start=True)
+        out[legacy] = pf.elastic_step(st, prob, cfg)
+    (u0, k0), (u1, k1) = out[False], out[True]
+    d = float((u0 - u1).abs().max()) / float(u1.abs().max())
+    assert abs(k0 - k1) <= 1, (k0, k1, d)
+    assert d < 1e-8, d
