@@ -9,7 +9,8 @@
 //             corners); other patterns -> 2:1 coarsening;
 //   level l : 9-point 2x2-block stencils, Galerkin A_{l+1} = P^T A_l P with bilinear P and a
 //             ceil rule for odd cell counts (the last odd fine vertex is injected);
-//   coarsest: dense inverse (n <= 2*kCoarseMaxV dofs), applied as one matvec.
+//   coarsest: dense inverse (n <= 2*kCoarseMaxV dofs, from a banded Cholesky factor), applied as
+//             one matvec spread over the whole grid.
 // Dirichlet dofs: the fine operator is the eliminated one (fem.py:282-294); P has zero rows on
 // constrained fine dofs and zero columns on coarse dofs injected from constrained fine dofs, so
 // coarse corrections never touch them and every level stays SPD.  Coefficient jumps (cracks,
@@ -26,7 +27,10 @@
 
 namespace pf {
 
-constexpr int kCoarseMaxV = 64;   // coarsest level: at most this many vertices (dense inverse)
+constexpr int kCoarseMaxV = 300;  // coarsest level: at most this many vertices (dense inverse)
+constexpr int kBandSmem = 200 * 1024;  // banded factor of the coarsest operator, in shared memory
+// half-bandwidth (in dofs) of a level's operator: vertex neighbours differ by <= nvy + 1
+__host__ __device__ __forceinline__ int band_of(int ny) { return 2 * (ny + 1) + 3; }
 constexpr int kGB = 256;          // block size of the GMG kernels
 
 __device__ __forceinline__ bool gmg_live(const double* s) {
@@ -356,53 +360,75 @@ __global__ void k_rap(LevelDev F, LevelDev Cd, double* Ac, double* Dinvc, unsign
     }
 }
 
-// Dense coarsest operator -> Cholesky -> explicit inverse, all in shared memory (single block;
-// n <= 2*kCoarseMaxV).  Once per setup.
-__global__ void k_coarse_inverse(LevelDev L, double* Ainv) {
-    extern __shared__ double Ms[];  // n*n factor
-    const int n = (int)(2 * L.nv);
-    const int nvy = L.ny + 1;
-    for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) Ms[idx] = 0.0;
+// Coarsest operator -> banded Cholesky -> explicit inverse (once per setup).  Dofs are ordered
+// 2v + c with v row-major, so A is banded with half-bandwidth bw = band_of(ny); the factor is kept
+// as B[i * (bw + 1) + (j - i + bw)] = L[i][j], j in [i - bw, i], in shared memory (one CTA).
+__global__ void k_coarse_chol_band(LevelDev L, int bw, double* Lband) {
+    extern __shared__ double B[];
+    const int n = (int)(2 * L.nv), W = bw + 1, nvy = L.ny + 1;
+    const int t = threadIdx.x, nt = blockDim.x;
+    for (int idx = t; idx < n * W; idx += nt) B[idx] = 0.0;
     __syncthreads();
-    for (int v = threadIdx.x; v < (int)L.nv; v += blockDim.x) {
+    for (int v = t; v < (int)L.nv; v += nt) {
         const int i = v / nvy, j = v % nvy;
         for (int k = 0; k < 9; ++k) {
             const int ni = i + k / 3 - 1, nj = j + k % 3 - 1;
             if (ni < 0 || nj < 0 || ni > L.nx || nj > L.ny) continue;
             const int w = ni * nvy + nj;
             for (int r = 0; r < 2; ++r)
-                for (int c = 0; c < 2; ++c)
-                    Ms[(2 * v + r) * n + 2 * w + c] = L.A[(size_t)(k * 4 + 2 * r + c) * L.nv + v];
+                for (int cc = 0; cc < 2; ++cc) {
+                    const int row = 2 * v + r, col = 2 * w + cc;
+                    if (col <= row && row - col <= bw) B[row * W + col - row + bw] = L.A[(size_t)(k * 4 + 2 * r + cc) * L.nv + v];
+                }
         }
     }
     __syncthreads();
-    for (int k = 0; k < n; ++k) {  // right-looking Cholesky, lower triangle
-        if (threadIdx.x == 0) Ms[k * n + k] = sqrt(Ms[k * n + k]);
+    for (int k = 0; k < n; ++k) {  // right-looking, inside the band
+        const int last = min(n - 1, k + bw), m = last - k;
+        if (t == 0) B[k * W + bw] = sqrt(B[k * W + bw]);
         __syncthreads();
-        const double piv = Ms[k * n + k];
-        for (int i = k + 1 + threadIdx.x; i < n; i += blockDim.x) Ms[i * n + k] /= piv;
+        const double piv = B[k * W + bw];
+        for (int i = k + 1 + t; i <= last; i += nt) B[i * W + k - i + bw] /= piv;
         __syncthreads();
-        const int m = n - k - 1;
-        for (int idx = threadIdx.x; idx < m * m; idx += blockDim.x) {
-            const int i = k + 1 + idx / m, j = k + 1 + idx % m;
-            if (j <= i) Ms[i * n + j] -= Ms[i * n + k] * Ms[j * n + k];
+        for (int p = t; p < m * m; p += nt) {
+            const int ii = k + 1 + p / m, jj = k + 1 + p % m;
+            if (jj <= ii) B[ii * W + jj - ii + bw] -= B[ii * W + k - ii + bw] * B[jj * W + k - jj + bw];
         }
         __syncthreads();
     }
-    // inverse columns: L L^T x = e_c (one column per thread; results to global)
-    for (int c = threadIdx.x; c < n; c += blockDim.x) {
-        double* x = Ainv + (size_t)c * n;
-        for (int i = 0; i < n; ++i) {
-            double s = (i == c) ? 1.0 : 0.0;
-            for (int k = 0; k < i; ++k) s -= Ms[i * n + k] * x[k];
-            x[i] = s / Ms[i * n + i];
-        }
-        for (int i = n - 1; i >= 0; --i) {
-            double s = x[i];
-            for (int k = i + 1; k < n; ++k) s -= Ms[k * n + i] * x[k];
-            x[i] = s / Ms[i * n + i];
-        }
+    for (int idx = t; idx < n * W; idx += nt) Lband[idx] = B[idx];
+}
+
+// Columns of A^-1 = L^-T L^-1 from the band factor, one warp per column: L y = e_c (rows c..n-1),
+// L^T x = y; x is row/column c of the symmetric inverse.
+__global__ void k_coarse_inv_band(const double* Lband, int n, int bw, int wpb, double* Ainv) {
+    extern __shared__ double sh[];
+    const int W = bw + 1;
+    double* B = sh;
+    double* Y = sh + (size_t)n * W;
+    for (int idx = threadIdx.x; idx < n * W; idx += blockDim.x) B[idx] = Lband[idx];
+    __syncthreads();
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int c = blockIdx.x * wpb + w;
+    if (w >= wpb || c >= n) return;
+    double* y = Y + (size_t)w * n;
+    for (int i = lane; i < n; i += 32) y[i] = 0.0;
+    __syncwarp();
+    for (int i = c; i < n; ++i) {
+        double s = 0.0;
+        for (int j = max(c, i - bw) + lane; j < i; j += 32) s += B[i * W + j - i + bw] * y[j];
+        s = warp_sum(s);
+        if (lane == 0) y[i] = ((i == c ? 1.0 : 0.0) - s) / B[i * W + bw];
+        __syncwarp();
     }
+    for (int i = n - 1; i >= 0; --i) {
+        double s = 0.0;
+        for (int j = i + 1 + lane; j <= min(n - 1, i + bw); j += 32) s += B[j * W + i - j + bw] * y[j];
+        s = warp_sum(s);
+        if (lane == 0) y[i] = (y[i] - s) / B[i * W + bw];
+        __syncwarp();
+    }
+    for (int i = lane; i < n; i += 32) Ainv[(size_t)c * n + i] = y[i];
 }
 
 // V-cycle vectors are streamed through L2 (ld.global.cg); operators/Dinv via the read-only path.
@@ -852,14 +878,15 @@ __global__ void k_expand_centres(const Geo2 g, const unsigned char* mask0, const
 }
 
 // ---- the coarse part of the V-cycle in one persistent launch -------------------------------------
-// Both level-0 transfers and levels 1..nl-1 run in one cooperative kernel: levels 1..lc-1 as
-// grid-wide phases separated by a software grid barrier, levels lc..nl-1 (the tail) on CTA 0 with
-// operators, masks, the dense coarse inverse and all vectors staged in shared memory (operators
-// are prefetched by cp.async at kernel entry, behind the grid phases).  The per-vertex functions,
-// and their order, are those of the launch-per-phase cycle, so the result is bitwise identical;
-// what goes away is ~30 dependent launches per V-cycle and the L2 round trips of the tail.
+// Both level-0 transfers, the smoothing of levels 1..nl-2 and the dense solve on the coarsest level
+// run in one cooperative kernel: grid-wide phases separated by a software grid barrier.  Every
+// phase is latency-bound (levels of 66k vertices and fewer), so the per-vertex functions are
+// branch-free with all loads of a row issued at once, small levels give each vertex 4 lanes
+// (shuffle-reduced stencil rows), the Chebyshev coefficients are computed once per launch into
+// shared memory, and the coarsest solve is one matvec with the explicit inverse (<= 600 dofs,
+// one warp per row).  The arithmetic is that of the launch-per-phase cycle (PF_GMG_LEGACY) up to
+// summation order; what goes away is ~30 dependent launches per V-cycle.
 constexpr int kMaxLev = 16;  // = the S_GMG0 lambda slots
-constexpr int kTailSmemMax = 200 * 1024;
 constexpr int kMaxDeg = 8;
 struct CCoef {  // per-level Chebyshev coefficients, computed once per launch into shared memory
     Cheb c;
@@ -869,23 +896,19 @@ struct CLev {
     LevelDev L;
     double *x, *b, *r, *d0, *d1, *res;
 };
-struct TOff {  // byte offsets of a tail level's arrays in shared memory (-1: not staged)
-    int A, Dinv, mask, x, b, r, d0, d1, res;
-};
 struct CoarseArgs {
     Geo2 g;
     LevelDev L0;                  // level-0 corner view (mask: as the level-0 transfers use it)
     const unsigned char* mask0;   // level-0 Dirichlet mask for the crossed collapse/expand (or null)
     const double* r0;             // level-0 residual (restricted)
     double* z0;                   // level-0 correction (+= P x1)
-    int crossed, nl, lc, deg, ncoarse, ainv_off, coef_off;
+    int crossed, nl, lc, deg, ncoarse, coef_off;  // lc: coarsest level (= nl - 1)
     double ratio;
     const double* ainv;
     unsigned int* bar;
     int skip;                     // timing aid (PF_GMG_SKIP_COARSE): return at entry
     unsigned long long* trace;    // timing aid (PF_GMG_TRACE): %globaltimer per phase, CTA 0
     CLev lev[kMaxLev];
-    TOff toff[kMaxLev];
 };
 
 // software grid barrier (all CTAs co-resident: cooperative launch).  One arrival word: CTA 0 adds
@@ -902,15 +925,6 @@ __device__ __forceinline__ void grid_sync(unsigned int* bar) {
         } while (((old ^ cur) & 0x80000000u) == 0);
     }
     __syncthreads();
-}
-
-__device__ __forceinline__ void cp16(void* dst, const void* src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
-                 "l"(src));
-}
-__device__ __forceinline__ void stage16(unsigned char* dst, const void* src, long long bytes) {
-    const long long n16 = (bytes + 15) / 16;
-    for (long long i = threadIdx.x; i < n16; i += kTB) cp16(dst + 16 * i, (const unsigned char*)src + 16 * i);
 }
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -951,17 +965,6 @@ __global__ void __launch_bounds__(kTB, 1) k_gmg_coarse(const __grid_constant__ C
         q.c = cheb_of(lam + t0, A.ratio);
         for (int k = 1; k < deg && k < kMaxDeg; ++k) cheb_ab(q.c, k, q.a[k], q.b[k]);
     }
-    if (blockIdx.x == 0) {  // tail operators, masks and the dense inverse: constant during the cycle
-        for (int l = A.lc; l < A.nl; ++l) {
-            const CLev& V = A.lev[l];
-            const TOff& o = A.toff[l];
-            if (o.A >= 0) stage16(sm + o.A, V.L.A, 288LL * V.L.nv);
-            if (o.Dinv >= 0) stage16(sm + o.Dinv, V.L.Dinv, 32LL * V.L.nv);
-            stage16(sm + o.mask, V.L.mask, V.L.nv);
-        }
-        if (A.ainv_off >= 0) stage16(sm + A.ainv_off, A.ainv, 8LL * A.ncoarse * A.ncoarse);
-        asm volatile("cp.async.commit_group;\n" ::);
-    }
     // level 0 -> 1 restriction (crossed: centres collapsed onto the corners on the fly)
     {
         const CLev& C = A.lev[1];
@@ -989,7 +992,7 @@ __global__ void __launch_bounds__(kTB, 1) k_gmg_coarse(const __grid_constant__ C
     grid_sync(A.bar);
         TR();
     // descend through the grid-wide levels
-    for (int l = 1; l < A.lc; ++l) {
+    for (int l = 1; l < A.nl - 1; ++l) {
         const CLev& V = A.lev[l];
         const Cheb c = coef[l].c;
         double a = 0.0, b = 0.0;
@@ -1015,100 +1018,21 @@ __global__ void __launch_bounds__(kTB, 1) k_gmg_coarse(const __grid_constant__ C
         grid_sync(A.bar);
         TR();
     }
-    // tail on CTA 0, in shared memory
-    if (blockIdx.x == 0) {
-        asm volatile("cp.async.wait_group 0;\n" ::);
-        auto view = [&](int l) {
-            const TOff& o = A.toff[l];
-            CLev T = A.lev[l];
-            T.L.A = o.A >= 0 ? (const double*)(sm + o.A) : nullptr;
-            T.L.Dinv = o.Dinv >= 0 ? (const double*)(sm + o.Dinv) : nullptr;
-            T.L.mask = sm + o.mask;
-            T.x = (double*)(sm + o.x);
-            T.b = (double*)(sm + o.b);
-            T.r = o.r >= 0 ? (double*)(sm + o.r) : nullptr;
-            T.d0 = o.d0 >= 0 ? (double*)(sm + o.d0) : nullptr;
-            T.d1 = o.d1 >= 0 ? (double*)(sm + o.d1) : nullptr;
-            T.res = o.res >= 0 ? (double*)(sm + o.res) : nullptr;
-            return T;
-        };
-        {
-            const CLev T = view(A.lc);
-            for (long long v = t0; v < T.L.nv; v += kTB) stv<true>(T.b, v, ldv(A.lev[A.lc].b, v));
-        }
-        __syncthreads();
-        TR();
-        for (int l = A.lc; l < A.nl - 1; ++l) {
-            const CLev V = view(l);
-            const Cheb c = coef[l].c;
-            double a = 0.0, b = 0.0;
-            if (deg > 1) { a = coef[l].a[1]; b = coef[l].b[1]; }
-            cta_each(V.L.nv, [&](auto g, long long v, int q) { v_pre_first<true, decltype(g)::value>(V.L, V.b, V.res, V.d0, V.d1, V.x, c, a, b, deg, v, q); });
-            __syncthreads();
-            double* d = V.d1;
-            double* dn = V.d0;
-            for (int k = 2; k < deg; ++k) {
-                a = coef[l].a[k]; b = coef[l].b[k];
-                cta_each(V.L.nv, [&](auto g, long long v, int q) { v_cheb_step<true, decltype(g)::value>(V.L, nullptr, d, dn, V.res, V.x, a, b, 0, v, q); });
-                __syncthreads();
-                double* tmp = d; d = dn; dn = tmp;
-            }
-            cta_each(V.L.nv, [&](auto g, long long v, int q) { v_resid<true, decltype(g)::value>(V.L, nullptr, V.x, V.b, V.r, v, q); });
-            __syncthreads();
-            const CLev C = view(l + 1);
-            for (long long v = t0; v < C.L.nv; v += kTB) v_restrict<true>(V.L, C.L, C.L.mask, V.r, C.b, v);
-            __syncthreads();
-        }
-        {   // coarsest: x = Ainv b, one warp per row
-            const CLev C = view(A.nl - 1);
-            const double* ainv = A.ainv_off >= 0 ? (const double*)(sm + A.ainv_off) : A.ainv;
-            const int n = A.ncoarse, lane = t0 & 31;
-            for (int r = t0 >> 5; r < n; r += kTB / 32) {
-                double s = 0.0;
-                for (int q = lane; q < n; q += 32)
-                    s += (A.ainv_off >= 0 ? ainv[(size_t)r * n + q] : __ldg(ainv + (size_t)r * n + q)) * C.b[q];
-                s = warp_sum(s);
-                if (lane == 0) C.x[r] = s;
-            }
-            __syncthreads();
-        }
-        for (int l = A.nl - 2; l >= A.lc; --l) {
-            const CLev V = view(l);
-            const CLev C = view(l + 1);
-            const Cheb c = coef[l].c;
-            for (long long v = t0; v < V.L.nv; v += kTB) v_prolong<true>(V.L, C.L, C.L.mask, C.x, V.x, v);
-            __syncthreads();
-            cta_each(V.L.nv, [&](auto g, long long v, int q) { v_post_first<true, decltype(g)::value>(V.L, V.x, V.b, V.res, V.d0, c, v, q); });
-            __syncthreads();
-            if (deg <= 1) {
-                for (long long v = t0; v < V.L.nv; v += kTB) {
-                    const double2 dv = ldv<true>(V.d0, v);
-                    double2 xv = ldv<true>(V.x, v);
-                    xv.x += dv.x;
-                    xv.y += dv.y;
-                    stv<true>(V.x, v, xv);
-                }
-                __syncthreads();
-            }
-            double* d = V.d0;
-            double* dn = V.d1;
-            for (int k = 1; k < deg; ++k) {
-                double a, b;
-                a = coef[l].a[k]; b = coef[l].b[k];
-                cta_each(V.L.nv, [&](auto g, long long v, int q) { v_cheb_step<true, decltype(g)::value>(V.L, nullptr, d, dn, V.res, V.x, a, b, k == 1, v, q); });
-                __syncthreads();
-                double* tmp = d; d = dn; dn = tmp;
-            }
-        }
-        {
-            const CLev T = view(A.lc);
-            for (long long v = t0; v < T.L.nv; v += kTB) stv(A.lev[A.lc].x, v, ldv<true>(T.x, v));
+    // coarsest level: x = Ainv b, one warp per row across the grid
+    {
+        const CLev& C = A.lev[A.nl - 1];
+        const int n = A.ncoarse, lane = t0 & 31;
+        for (long long r = tid >> 5; r < n; r += nth >> 5) {
+            double sum = 0.0;
+            for (int q = lane; q < n; q += 32) sum += __ldg(A.ainv + (size_t)r * n + q) * __ldcg(C.b + q);
+            sum = warp_sum(sum);
+            if (lane == 0) C.x[r] = sum;
         }
     }
     grid_sync(A.bar);
         TR();
     // ascend through the grid-wide levels
-    for (int l = A.lc - 1; l >= 1; --l) {
+    for (int l = A.nl - 2; l >= 1; --l) {
         const CLev& V = A.lev[l];
         const CLev& C = A.lev[l + 1];
         const Cheb c = coef[l].c;
@@ -1197,7 +1121,9 @@ void gmg_plan(Ctx* c) {
         GLevel L;
         L.nx = nx; L.ny = ny; L.nv = (long long)(nx + 1) * (ny + 1);
         c->glev.push_back(L);
-    } while (c->glev.back().nv > kCoarseMaxV && (nx > 1 || ny > 1));
+    } while ((c->glev.back().nv > kCoarseMaxV ||
+              8LL * 2 * c->glev.back().nv * (band_of(c->glev.back().ny) + 1) > kBandSmem) &&
+             (nx > 1 || ny > 1));
 }
 
 size_t gmg_bytes(const Ctx* c) {
@@ -1302,15 +1228,21 @@ int gmg_setup(Ctx* c, cudaStream_t st) {
                                                       c->glev[l + 1].mask, lam + l + 1)));
     }
     {
-        const int n = (int)(2 * c->glev[nl - 1].nv);
-        const int smem = (int)sizeof(double) * n * n;
+        const GLevel& Lc = c->glev[nl - 1];
+        const int n = (int)(2 * Lc.nv), bw = band_of(Lc.ny), W = bw + 1;
+        const int smem = (int)sizeof(double) * n * W;
+        int wpb = 8;
+        while (wpb > 1 && smem + (int)sizeof(double) * wpb * n > 225 * 1024) --wpb;
+        const int smem2 = smem + (int)sizeof(double) * wpb * n;
         static bool attr = false;
         if (!attr) {
-            cudaFuncSetAttribute(k_coarse_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)sizeof(double) * 4 * kCoarseMaxV * kCoarseMaxV);
+            cudaFuncSetAttribute(k_coarse_chol_band, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024);
+            cudaFuncSetAttribute(k_coarse_inv_band, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024);
             attr = true;
         }
-        GKB(c, K_GMGSET, 2.0 * 8.0 * n * n, (k_coarse_inverse<<<1, 512, smem, st>>>(ldev(c, nl - 1), c->gmg_ainv)));
+        GKB(c, K_GMGSET, 2.0 * 8.0 * n * W, (k_coarse_chol_band<<<1, 1024, smem, st>>>(ldev(c, nl - 1), bw, c->gmg_dense)));
+        GKB(c, K_GMGSET, 8.0 * n * W + 8.0 * n * n, (k_coarse_inv_band<<<(n + wpb - 1) / wpb, 32 * wpb, smem2, st>>>(
+                                                      c->gmg_dense, n, bw, wpb, c->gmg_ainv)));
     }
     return check_cuda(c, cudaGetLastError(), "gmg setup");
 }
@@ -1416,49 +1348,13 @@ static int fine_post(Ctx* c, const double* b, double* x, cudaStream_t st, const 
 
 #define GCU(c, x, where) PF_TRY_GMG(check_cuda((c), (x), (where)))
 
-// Tail of the persistent coarse cycle: the first tail level lc and the shared-memory layout.
+// Shared memory of the persistent coarse cycle: the per-level Chebyshev coefficient table.
 static int coarse_plan(const Ctx* c, CoarseArgs& a) {
     const int nl = (int)c->glev.size();
-    auto a16 = [](long long b) { return (int)((b + 15) & ~15LL); };
-    auto level_bytes = [&](int l) -> long long {
-        const long long nv = c->glev[l].nv;
-        long long b = a16(nv);                        // mask
-        if (l < nl - 1) b += 288 * nv + 32 * nv + 6 * 16 * nv;  // A, Dinv, x b r d0 d1 res
-        else b += 2 * 16 * nv;                        // x b
-        return b;
-    };
-    const long long n = 2 * c->glev[nl - 1].nv;
-    const long long ainv_b = 8 * n * n;
-    long long tot = level_bytes(nl - 1) + (long long)sizeof(CCoef) * nl + 16;
-    const bool ainv_sm = ainv_b <= 64 * 1024;
-    if (ainv_sm) tot += ainv_b;
-    int lc = nl - 1;
-    while (lc > 1 && lc - 1 < kMaxLev && tot + level_bytes(lc - 1) <= kTailSmemMax) tot += level_bytes(--lc);
-    if (tot > kTailSmemMax || nl > kMaxLev) return -1;
-    a.lc = lc;
-    int off = 0;
-    auto take = [&](long long b) { const int o = off; off += a16(b); return o; };
-    for (int l = 0; l < kMaxLev; ++l) a.toff[l] = TOff{-1, -1, -1, -1, -1, -1, -1, -1, -1};
-    for (int l = lc; l < nl; ++l) {
-        const long long nv = c->glev[l].nv;
-        TOff& o = a.toff[l];
-        if (l < nl - 1) {
-            o.A = take(288 * nv);
-            o.Dinv = take(32 * nv);
-        }
-        o.mask = take(nv);
-        o.x = take(16 * nv);
-        o.b = take(16 * nv);
-        if (l < nl - 1) {
-            o.r = take(16 * nv);
-            o.d0 = take(16 * nv);
-            o.d1 = take(16 * nv);
-            o.res = take(16 * nv);
-        }
-    }
-    a.ainv_off = ainv_sm ? take(ainv_b) : -1;
-    a.coef_off = take((long long)sizeof(CCoef) * nl);
-    return off;
+    if (nl > kMaxLev) return -1;
+    a.lc = nl - 1;
+    a.coef_off = 0;
+    return (int)sizeof(CCoef) * nl;
 }
 
 static int launch_coarse(Ctx* c, const double* r0, double* z0, cudaStream_t st, const double* live) {
@@ -1491,12 +1387,6 @@ static int launch_coarse(Ctx* c, const double* r0, double* z0, cudaStream_t st, 
         a.lev[l].L = ldev(c, l);
         a.lev[l].x = L.x; a.lev[l].b = L.b; a.lev[l].r = L.r;
         a.lev[l].d0 = L.d0; a.lev[l].d1 = L.d1; a.lev[l].res = L.res;
-    }
-    static int smem_attr = -1;
-    if (smem > smem_attr) {
-        GCU(c, cudaFuncSetAttribute(k_gmg_coarse, cudaFuncAttributeMaxDynamicSharedMemorySize, kTailSmemMax),
-              "coarse smem attribute");
-        smem_attr = kTailSmemMax;
     }
     static int nb_cache = 0, nb_smem = -1;
     if (nb_smem != smem) {
