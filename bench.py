@@ -102,22 +102,26 @@ class ClockSampler:
 def sent_config(pf):
     return pf.SolverConfig(method="oram_newton", omega=1.8, outer_atol=1e-6, am_switch_atol=1e-3,
                            elastic_solver="cg", elastic_rtol=1e-8, elastic_precond="gmg",
-                           max_am_iterations=2000)
+                           max_am_iterations=2000,
+                           fieldsplit_inner="mg")
 
 
 def surfing_config(pf):
     return pf.SolverConfig(method="oram_newton", omega=1.6, outer_atol=1e-7, elastic_solver="cg",
-                           elastic_rtol=1e-10, elastic_precond="gmg", max_am_iterations=3000)
+                           elastic_rtol=1e-10, elastic_precond="gmg", max_am_iterations=3000,
+                           fieldsplit_inner="mg")
 
 
 def thermal_config(pf):
     return pf.SolverConfig(method="oram_newton", omega=1.5, outer_atol=1e-7, elastic_solver="cg",
-                           elastic_rtol=1e-8, elastic_precond="gmg", max_am_iterations=2000)
+                           elastic_rtol=1e-8, elastic_precond="gmg", max_am_iterations=2000,
+                           fieldsplit_inner="mg")
 
 
 def traction3d_config(pf):
     return pf.SolverConfig(method="oram_newton", omega=1.7, outer_atol=1e-6, elastic_solver="cg",
-                           elastic_rtol=1e-8, elastic_precond="gmg", max_am_iterations=3000)
+                           elastic_rtol=1e-8, elastic_precond="gmg", max_am_iterations=3000,
+                           fieldsplit_inner="mg")
 
 
 def traction1_setup(pf):

@@ -109,8 +109,12 @@ typedef struct pf_vi_opts {
     double fieldsplit_rtol; /* Newton only: MINRES rtol (solver.py:64) */
     int32_t inner_cycles;   /* Newton only: > 0 -> each field-split block solve is a fixed budget of
                              * this many PCG iterations at rtol 1e-12 (fieldsplit_inner = "cg",
-                             * inner_cg linalg.py:446-456); 0 -> solved to inner_rtol */
-    int32_t reserved;
+                             * inner_cg linalg.py:446-456); 0 -> solved to inner_rtol.
+                             * inner_mode 1: the Chebyshev degree of the C block (<= 0 -> 12) */
+    int32_t inner_mode;     /* Newton only: 0 -> block solves as above; 1 -> fixed linear SPD block
+                             * preconditioners: A^-1 ~ one multigrid V-cycle, C^-1 ~ Chebyshev-Jacobi
+                             * on [lmax/30, 1.1 lmax] (lmax by 30 power iterations, as the
+                             * reference ChebyshevPreconditioner linalg.py:331-378) */
 } pf_vi_opts;
 
 typedef struct pf_vi_report {

@@ -50,7 +50,7 @@ class VIOpts(C.Structure):
                 ("ls_backtrack", C.c_double), ("ls_min_step", C.c_double), ("armijo", C.c_double),
                 ("inner_rtol", C.c_double), ("inner_maxit", C.c_int64), ("zero_tol", C.c_double),
                 ("fieldsplit_rtol", C.c_double), ("inner_cycles", C.c_int32),
-                ("reserved", C.c_int32)]
+                ("inner_mode", C.c_int32)]
 
 
 class VIReport(C.Structure):

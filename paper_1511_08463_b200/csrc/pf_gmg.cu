@@ -937,25 +937,26 @@ __device__ __forceinline__ unsigned long long gtimer() {
         if (A.trace && blockIdx.x == 0 && threadIdx.x == 0) A.trace[ntr++] = gtimer(); \
     } while (0)
 
-__global__ void __launch_bounds__(kTB, 1) k_gmg_coarse(const __grid_constant__ CoarseArgs A, const double* lam,
+constexpr int kCB = 512;  // threads per CTA of the persistent coarse cycle (one CTA per SM; 1024 measured slower)
+__global__ void __launch_bounds__(kCB, 1) k_gmg_coarse(const __grid_constant__ CoarseArgs A, const double* lam,
                                                        const double* live) {
     if (!gmg_live(live) || A.skip) return;  // uniform: the flags are not written during the launch
     extern __shared__ __align__(16) unsigned char sm[];
-    const long long tid = blockIdx.x * (long long)kTB + threadIdx.x;
-    const long long nth = (long long)gridDim.x * kTB;
+    const long long tid = blockIdx.x * (long long)kCB + threadIdx.x;
+    const long long nth = (long long)gridDim.x * kCB;
     const int deg = A.deg;
     const int t0 = threadIdx.x;
-    // stencil phases: 4 lanes per vertex when the level is small enough (shorter dependent chains)
+    // stencil phases: 4 (or 2) lanes per vertex when the level is small enough (shorter chains)
     using G1 = std::integral_constant<int, 1>;
+    using G2 = std::integral_constant<int, 2>;
     using G4 = std::integral_constant<int, 4>;
     auto grid_each = [&](long long nv, auto fn) {
         if (4 * nv <= nth)
             for (long long e = tid; e < 4 * nv; e += nth) fn(G4{}, e >> 2, (int)(e & 3));
+        else if (2 * nv <= nth)
+            for (long long e = tid; e < 2 * nv; e += nth) fn(G2{}, e >> 1, (int)(e & 1));
         else
             for (long long v = tid; v < nv; v += nth) fn(G1{}, v, 0);
-    };
-    auto cta_each = [&](long long nv, auto fn) {
-        for (long long e = t0; e < 4 * nv; e += kTB) fn(G4{}, e >> 2, (int)(e & 3));
     };
     int ntr = 0;
     TR();
@@ -1393,7 +1394,7 @@ static int launch_coarse(Ctx* c, const double* r0, double* z0, cudaStream_t st, 
         int dev = 0, nsm = 0, per = 0;
         GCU(c, cudaGetDevice(&dev), "device");
         GCU(c, cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev), "sm count");
-        GCU(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_gmg_coarse, kTB, smem), "occupancy");
+        GCU(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_gmg_coarse, kCB, smem), "occupancy");
         if (per < 1) return set_error(c, PF_ECUDA, "gmg: coarse-cycle kernel cannot be resident");
         nb_cache = nsm * per;
         nb_smem = smem;
@@ -1412,7 +1413,7 @@ static int launch_coarse(Ctx* c, const double* r0, double* z0, cudaStream_t st, 
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(nb_cache);
-    cfg.blockDim = dim3(kTB);
+    cfg.blockDim = dim3(kCB);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute at[1];

@@ -80,6 +80,52 @@ __global__ void k_ngrad(long long nu, long long na, const double* pphi_a, const 
         g[i] = 2.0 * ((i >= nu ? pphi_a[i - nu] : 0.0) + Jw[i]);
 }
 
+// ---- fixed linear block preconditioners (inner_mode 1) ----
+// y2 = D^-1 y (masked rows of dinv are 1), reduce |y2|^2 into s[slot]
+__global__ void k_ndinv_dot(long long n, const double* dinv, const double* y, double* y2, double* s, int slot,
+                            RedBuf rb) {
+    double acc[1] = {0.0};
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const double v = dinv[i] * y[i];
+        y2[i] = v;
+        acc[0] += v * v;
+    }
+    grid_reduce<1>(acc, rb, 8, [=](double* t) { s[slot] = t[0]; });
+}
+// x = y / sqrt(s[slot])
+__global__ void k_nnormalize(long long n, const double* y, double* x, const double* s, int slot) {
+    const double inv = s[slot] > 0.0 ? 1.0 / sqrt(s[slot]) : 0.0;  // empty inactive block: x = 0
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        x[i] = y[i] * inv;
+}
+// power-iteration start: 1 on inactive rows, 0 on active rows
+__global__ void k_nones(long long n, const unsigned char* act, double* x) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        x[i] = act[i] ? 0.0 : 1.0;
+}
+// Chebyshev on D^-1 C: r = b ; d = D^-1 r / theta ; x = d
+__global__ void k_ncheb0(long long n, const double* dinv, const double* b, double* r, double* d, double* x,
+                         double ith) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const double ri = b[i];
+        const double di = dinv[i] * ri * ith;
+        r[i] = ri;
+        d[i] = di;
+        x[i] = di;
+    }
+}
+// r -= C d ; d = a d + b D^-1 r ; x += d
+__global__ void k_nchebk(long long n, const double* dinv, const double* Cd, double* r, double* d, double* x,
+                         double a, double b) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const double ri = r[i] - Cd[i];
+        const double di = a * d[i] + b * dinv[i] * ri;
+        r[i] = ri;
+        d[i] = di;
+        x[i] += di;
+    }
+}
+
 static int nblocks(long long n) { return (int)std::max(1LL, std::min((n + kNB - 1) / kNB, 148LL * 8)); }
 
 #define NTRY(x)                        \
@@ -148,12 +194,78 @@ static int solve_C(Ctx* c, const double* b, double* out, double rtol, int budget
     return PF_OK;
 }
 
+// lambda_max of D^-1 C on the inactive damage block: 30 power iterations from a deterministic start
+// vector (ChebyshevPreconditioner, linalg.py:347-358), normalised on the device (no host polls).
+static int lambda_C(Ctx* c, double& lmax, cudaStream_t st) {
+    const long long n = c->n_a;
+    const int nb = nblocks(n);
+    const RedBuf rb{c->partials, c->tickets, c->scal};
+    double *x = c->da_x, *y = c->da_q, *y2 = c->da_z;
+    k_nones<<<nb, kNB, 0, st>>>(n, c->act, x);
+    c->launches++;
+    for (int it = 0; it < 30; ++it) {
+        NTRY(launch_Kaa(c, c->kappa, x, y, c->act, st));
+        k_ndinv_dot<<<nb, kNB, 0, st>>>(n, c->da_dinv, y, y2, c->scal, S_AUX1, rb);
+        k_nnormalize<<<nb, kNB, 0, st>>>(n, y2, x, c->scal, S_AUX1);
+        c->launches += 2;
+    }
+    NTRY(read_scal(c, st, S_AUX1, 1));
+    lmax = std::sqrt(c->h_scal[S_AUX1]);  // |D^-1 C x| for the unit iterate x
+    if (!std::isfinite(lmax)) return set_error(c, PF_EINNER, "field split: damage-block spectrum estimate failed");
+    if (lmax == 0.0) lmax = 1.0;  // no inactive damage rows: C^-1 acts on zero vectors only
+    return PF_OK;
+}
+// x = p(D^-1 C) b: `deg` Chebyshev steps on [lmax/30, 1.1 lmax] from x = 0 (a fixed SPD operator)
+static int cheb_C(Ctx* c, const double* b, double* x, double lmax, int deg, long long& its, cudaStream_t st) {
+    const long long n = c->n_a;
+    const int nb = nblocks(n);
+    const double hi = 1.1 * lmax, lo = hi / 30.0;
+    const double theta = 0.5 * (hi + lo), delta = 0.5 * (hi - lo), sigma = theta / delta;
+    double *r = c->da_r, *d = c->da_p0, *Cd = c->da_q;
+    k_ncheb0<<<nb, kNB, 0, st>>>(n, c->da_dinv, b, r, d, x, 1.0 / theta);
+    c->launches++;
+    double rho = 1.0 / sigma;
+    for (int k = 1; k < deg; ++k) {
+        const double rn = 1.0 / (2.0 * sigma - rho);
+        NTRY(launch_Kaa(c, c->kappa, d, Cd, c->act, st));
+        k_nchebk<<<nb, kNB, 0, st>>>(n, c->da_dinv, Cd, r, d, x, rn * rho, 2.0 * rn / delta);
+        c->launches++;
+        rho = rn;
+    }
+    its += deg;
+    return PF_OK;
+}
+// x = one multigrid V-cycle applied to b (hierarchy of the current alpha; a fixed SPD operator)
+static int vcycle_A(Ctx* c, const double* b, double* x, long long& its, cudaStream_t st) {
+    if (c->dim == 3) NTRY(gmg3_vcycle(c, b, x, st, nullptr));
+    else NTRY(gmg_vcycle(c, b, x, st, nullptr, false, -1, nullptr));
+    its += 1;
+    return PF_OK;
+}
+
 // y = P^-1 r (symmetric multiplicative field split, linalg.py:424-430)
+struct InnerMg {  // inner_mode 1
+    bool on = false;
+    int deg = 12;
+    double lmax = 0.0;
+};
 static int fieldsplit(Ctx* c, const NewtonWs& w, const double* r, double* y, const double* u, const double* alpha,
-                      double inner_rtol, int budget, long long& its, cudaStream_t st) {
+                      double inner_rtol, int budget, long long& its, cudaStream_t st, const InnerMg& mg) {
     const long long nu = w.nu, na = w.na;
     double* y1 = y;              // u part of y
     double* z = y + nu;          // alpha part of y
+    if (mg.on) {
+        NTRY(vcycle_A(c, r, y1, its, st));
+        NTRY(launch_Kau(c, u, alpha, y1, w.TMP + nu, PF_BC_ELIMINATE, st));            // B^T y1
+        k_nsubmask<<<nblocks(na), kNB, 0, st>>>(na, r + nu, w.TMP + nu, c->act, w.TMP + nu);
+        c->launches++;
+        NTRY(cheb_C(c, w.TMP + nu, z, mg.lmax, mg.deg, its, st));
+        NTRY(launch_Kua(c, u, alpha, z, w.TMP, PF_BC_ELIMINATE, st));                   // B z
+        NTRY(vcycle_A(c, w.TMP, w.G, its, st));
+        k_naxpy<<<nblocks(nu), kNB, 0, st>>>(nu, -1.0, w.G, y1);
+        c->launches++;
+        return PF_OK;
+    }
     NTRY(solve_A(c, r, y1, inner_rtol, budget, its, st));
     NTRY(launch_Kau(c, u, alpha, y1, w.TMP + nu, PF_BC_ELIMINATE, st));            // B^T y1
     k_nsubmask<<<nblocks(na), kNB, 0, st>>>(na, r + nu, w.TMP + nu, c->act, w.TMP + nu);
@@ -169,7 +281,7 @@ static int fieldsplit(Ctx* c, const NewtonWs& w, const double* r, double* y, con
 // MINRES on the masked inactive block J_NN d = rhs (x0 = 0); returns the iterations.
 static int minres(Ctx* c, NewtonWs& w, const double* u, const double* alpha, const double* rhs, double* x,
                   double rtol, long long maxit, double inner_rtol, int budget, long long& kits, bool& converged,
-                  cudaStream_t st) {
+                  cudaStream_t st, const InnerMg& mg) {
     const long long n = w.n, nu = w.nu;
     auto op = [&](const double* v, double* out) {
         return launch_jac(c, u, alpha, v, v + nu, out, out + nu, c->act, st);
@@ -177,7 +289,7 @@ static int minres(Ctx* c, NewtonWs& w, const double* u, const double* alpha, con
     NCU(c, cudaMemsetAsync(x, 0, sizeof(double) * n, st), "memset");
     NCU(c, cudaMemcpyAsync(w.R1, rhs, sizeof(double) * n, cudaMemcpyDeviceToDevice, st), "copy");
     double *r1 = w.R1, *r2 = w.R2, *y = w.Y, *v = w.V, *ww = w.W, *w1 = w.W1, *w2 = w.W2;
-    NTRY(fieldsplit(c, w, r1, y, u, alpha, inner_rtol, budget, kits, st));
+    NTRY(fieldsplit(c, w, r1, y, u, alpha, inner_rtol, budget, kits, st, mg));
     double beta1;
     NTRY(ndot(c, n, r1, y, S_AUX1, beta1, st));
     if (beta1 < 0.0) return set_error(c, PF_EBREAKDOWN, "minres: preconditioner not SPD");
@@ -205,7 +317,7 @@ static int minres(Ctx* c, NewtonWs& w, const double* u, const double* alpha, con
         r1 = r2;
         r2 = y;
         y = old_r1;
-        NTRY(fieldsplit(c, w, r2, y, u, alpha, inner_rtol, budget, kits, st));
+        NTRY(fieldsplit(c, w, r2, y, u, alpha, inner_rtol, budget, kits, st, mg));
         oldb = beta;
         double bb;
         NTRY(ndot(c, n, r2, y, S_AUX1, bb, st));
@@ -305,11 +417,17 @@ int newton_solve(Ctx* c, const double* u_in, const double* a_in, const double* l
         c->gmg_its0 = -1;
         NTRY(launch_kappa(c, u, alpha, c->kappa, c->vi_c, st));
         NTRY(launch_Kaa_diag(c, c->kappa, c->da_dinv, c->act, st));
+        InnerMg mg;
+        if (o->inner_mode == 1) {
+            mg.on = true;
+            mg.deg = o->inner_cycles > 0 ? o->inner_cycles : 12;
+            NTRY(lambda_C(c, mg.lmax, st));
+        }
         bool ok = false;
         long long kits = 0;
         bool lin_ok = false;
         int rc = minres(c, w, u, alpha, w.RHS, w.D, fs_rtol, o->inner_maxit > 0 ? o->inner_maxit : 10 * n,
-                        inner_rtol, std::max(0, o->inner_cycles), kits, lin_ok, st);
+                        inner_rtol, mg.on ? 0 : std::max(0, o->inner_cycles), kits, lin_ok, st, mg);
         rep->total_krylov_iterations += kits;
         if (rc == PF_OK && lin_ok) {
             k_nscale<<<nblocks(n), kNB, 0, st>>>(n, -1.0, w.D, w.D);  // d = -d_N (zero on active)

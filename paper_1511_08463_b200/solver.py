@@ -32,7 +32,7 @@ _METHODS = ("am", "oram_newton", "newton_only")
 _ELASTIC = ("direct", "cg")
 _PRECONDS = ("jacobi", "gmg")
 _COUPLED = ("direct", "fieldsplit")
-_INNER = ("direct", "cg")
+_INNER = ("direct", "cg", "mg")
 
 
 @dataclass
@@ -58,6 +58,7 @@ class SolverConfig:
     coupled_solver: str = "fieldsplit"
     fieldsplit_inner: str = "direct"
     fieldsplit_cg_budget: int = 5
+    fieldsplit_cheb_degree: int = 12  # fieldsplit_inner="mg": Chebyshev degree of the C block
     fieldsplit_rtol: float = 1e-6
     damage_atol_factor: float = 0.1
     max_vi_iterations: int = 200
@@ -263,12 +264,17 @@ def coupled_newton_solve(state: State, problem: Discretization, config: SolverCo
     # MINRES + field split at direct_rtol; fieldsplit_inner="cg" is the fixed-budget inner PCG
     # (solver.py:259-263, linalg.py:446-456), with the device preconditioners (A: multigrid or
     # Jacobi in place of SSOR, C: Jacobi)
+    # fieldsplit_inner="mg" (device only) makes both blocks fixed linear SPD preconditioners: one
+    # multigrid V-cycle for A and a Chebyshev-Jacobi polynomial for C -- MINRES takes a few more
+    # iterations, each far cheaper than solving the blocks to a tolerance
     direct = config.coupled_solver == "direct"
+    mg = config.fieldsplit_inner == "mg" and not direct
     vic = VIConfig(abs_tol=config.outer_atol, max_iterations=config.max_newton_iterations,
                    fieldsplit_rtol=config.direct_rtol if direct else config.fieldsplit_rtol,
                    inner_rtol=config.newton_inner_rtol or (config.direct_rtol if direct else 0.0),
-                   inner_cycles=config.fieldsplit_cg_budget
-                   if (config.fieldsplit_inner == "cg" and not direct) else 0)
+                   inner_cycles=(config.fieldsplit_cheb_degree if mg else config.fieldsplit_cg_budget)
+                   if (config.fieldsplit_inner in ("cg", "mg") and not direct) else 0,
+                   inner_mode=1 if mg else 0)
     opts = vic.to_c()
     rep = _lib.VIReport()
     out = state.copy()

@@ -30,6 +30,7 @@ class VIConfig:
     inner_maxit: int = 0
     fieldsplit_rtol: float = 1e-6
     inner_cycles: int = 0
+    inner_mode: int = 0
 
     def to_c(self) -> _lib.VIOpts:
         return _lib.VIOpts(abs_tol=self.abs_tol, max_iterations=self.max_iterations, precond=0,
@@ -37,7 +38,8 @@ class VIConfig:
                            armijo=self.armijo, inner_rtol=self.inner_rtol,
                            inner_maxit=self.inner_maxit,
                            zero_tol=-1.0 if self.zero_tol is None else self.zero_tol,
-                           fieldsplit_rtol=self.fieldsplit_rtol, inner_cycles=self.inner_cycles)
+                           fieldsplit_rtol=self.fieldsplit_rtol, inner_cycles=self.inner_cycles,
+                           inner_mode=self.inner_mode)
 
 
 @dataclass

@@ -137,8 +137,10 @@ def test_gmg3_elastic_step_matches_oracle(shape):
     assert kg < kj, (kg, kj)
 
 
-def test_traction3d_config4_shape_gmg_matches_oracle():
-    """Config-4 physics through the 3D multigrid path (elastic half-steps and Newton's A block)."""
+@pytest.mark.parametrize("inner", ["direct", "mg"])
+def test_traction3d_config4_shape_gmg_matches_oracle(inner):
+    """Config-4 physics through the 3D multigrid path (elastic half-steps and Newton's A block;
+    inner="mg": the A block preconditioned by one 3D V-cycle, C by Chebyshev-Jacobi)."""
     import paper_1511_08463_b200 as pf
     from oracle import problems as opb
     n, steps = 8, 6
@@ -147,7 +149,7 @@ def test_traction3d_config4_shape_gmg_matches_oracle():
     spec = MaterialSpec(E=1.0, nu=0.3, Gc=1.0, ell=0.3, k_ell=1e-6, model="AT1", regime="3d")
     osetup = opb.traction3d(n=n, spec=spec, n_steps=steps)
     cfg = pf.SolverConfig(method="oram_newton", omega=1.7, outer_atol=1e-9, elastic_solver="cg",
-                          elastic_rtol=1e-12, elastic_precond="gmg")
+                          elastic_rtol=1e-12, elastic_precond="gmg", fieldsplit_inner=inner)
     recs = pf.run_quasistatic(setup, cfg)
     orows, _ = opb.run(osetup, oam.AMConfig(method="oram_newton", omega=1.7, outer_atol=1e-9))
     assert max(float(np.max(o.alpha)) for o in orows) > 0.05

@@ -251,10 +251,11 @@ def test_fused_relax_physics_equals_separate_passes(pattern, omega):
     assert res1 == res2 and tuple(e1) == tuple(e2)
 
 
-@pytest.mark.parametrize("variant", ["direct", "inner_cg"])
+@pytest.mark.parametrize("variant", ["direct", "inner_cg", "inner_mg"])
 def test_newton_coupled_solver_variants_converge_like_fieldsplit(variant):
-    """coupled_solver='direct' (MINRES + field split at direct_rtol) and fieldsplit_inner='cg'
-    (fixed-budget inner PCG) reach the same Newton solution as the default field split."""
+    """coupled_solver='direct' (MINRES + field split at direct_rtol), fieldsplit_inner='cg'
+    (fixed-budget inner PCG) and fieldsplit_inner='mg' (one V-cycle for A, Chebyshev-Jacobi for
+    C: fixed SPD block preconditioners) reach the same Newton solution as the default field split."""
     import paper_1511_08463_b200 as pf
     from paper_1511_08463_b200 import solver as S
     setup = pf.setup_traction(pf.Material(ell=0.1), nx=40, ny=12, n_steps=12, pattern="right")
@@ -262,7 +263,9 @@ def test_newton_coupled_solver_variants_converge_like_fieldsplit(variant):
     st = pf.State.zeros(setup.mesh)
     pf.run_quasistatic(setup, base, snapshot_stride=0, state=st, steps=list(range(9)))
     prob = setup.problem
-    kw = {"coupled_solver": "direct"} if variant == "direct" else {"fieldsplit_inner": "cg", "fieldsplit_cg_budget": 30}
+    kw = {"direct": {"coupled_solver": "direct"},
+          "inner_cg": {"fieldsplit_inner": "cg", "fieldsplit_cg_budget": 30},
+          "inner_mg": {"fieldsplit_inner": "mg"}}[variant]
     ref_cfg = pf.SolverConfig(outer_atol=1e-9, elastic_solver="cg", elastic_precond="gmg")
     var_cfg = pf.SolverConfig(outer_atol=1e-9, elastic_solver="cg", elastic_precond="gmg", **kw)
     s1, r1 = S.coupled_newton_solve(st, prob, ref_cfg)
