@@ -388,6 +388,34 @@ __global__ void k_loop_cond(cudaGraphConditionalHandle h, const double* s) {
     if (threadIdx.x == 0) cudaGraphSetConditional(h, (s[S_DONE] == 0.0 && s[S_FAIL] == 0.0) ? 1u : 0u);
 }
 
+// report + error mapping once the Krylov loop stopped (scalars already read back)
+static int pcg_finish(Ctx* c, const PcgBuffers& B, pf_lin_report* rep, cudaStream_t st) {
+    rep->iterations = (long long)c->h_scal[S_ITER];
+    rep->final_residual_norm = c->h_scal[S_RNORM];
+    rep->b_norm = c->h_scal[S_BNORM];
+    rep->converged = (c->h_scal[S_FAIL] == 0.0) && (c->h_scal[S_RNORM] <= c->h_scal[S_TARGET] ||
+                                                    c->h_scal[S_DONE] == 2.0);
+    rep->status = PF_OK;
+    if (c->h_scal[S_DONE] == 2.0) {
+        PF_CU(c, cudaMemsetAsync(B.x, 0, sizeof(double) * B.n, st), "memset");
+        rep->iterations = 0;
+        rep->final_residual_norm = 0.0;
+    }
+    if (c->h_scal[S_FAIL] != 0.0) {
+        char msg[160];
+        if (c->h_scal[S_FAIL] == 1.0)
+            snprintf(msg, sizeof msg, "cg: p'Ap = %.3e <= 0 at iteration %lld (operator not positive definite)",
+                     c->h_scal[S_PAP], (long long)c->h_scal[S_ITER] + 1);
+        else
+            snprintf(msg, sizeof msg, "cg: preconditioner not SPD at iteration %lld",
+                     (long long)c->h_scal[S_ITER]);
+        rep->status = PF_EBREAKDOWN;
+        return set_error(c, PF_EBREAKDOWN, msg);
+    }
+    return PF_OK;
+}
+
+
 int pcg_run(Ctx* c, int kind, const PcgBuffers& B, const double* coef, const unsigned char* act,
                    double rtol, double atol, long long maxit, int zero_x0, int check_every,
                    pf_lin_report* rep, cudaStream_t st) {
@@ -468,6 +496,15 @@ int pcg_run(Ctx* c, int kind, const PcgBuffers& B, const double* coef, const uns
     // failed -- no host polling, at most one no-op iteration after convergence.  Kernels read
     // every scalar from device memory, so the body is replayed unchanged.  Disabled while
     // per-kernel profiling is on (eager launches bracketed by events, host-polled batches).
+    if (kind == 1 && c->dim == 2 && c->pcg_persistent && c->h_scal[S_DONE] == 0.0 && c->h_scal[S_FAIL] == 0.0) {
+        // damage block: every iteration inside one cooperative launch (no host polls, no graph)
+        const int rc = launch_pcg_kaa(c, B, coef, act, st);
+        if (rc == PF_OK) {
+            PF_TRY(read_scal(c, st, 0, 24));
+            return pcg_finish(c, B, rep, st);
+        }
+        if (rc != PF_EINVAL) return rc;
+    }
     const bool graphs = c->use_graphs && !c->prof.on;
     const long long key = c->geo_version * 16 + (gmg ? c->gmg_degree : 0);
     // the captured body bakes in these pointers: re-capture when any of them changes
@@ -536,29 +573,7 @@ int pcg_run(Ctx* c, int kind, const PcgBuffers& B, const double* coef, const uns
             if (!gmg) batch = std::min(batch * 2, 64);
         }
     }
-    rep->iterations = (long long)c->h_scal[S_ITER];
-    rep->final_residual_norm = c->h_scal[S_RNORM];
-    rep->b_norm = c->h_scal[S_BNORM];
-    rep->converged = (c->h_scal[S_FAIL] == 0.0) && (c->h_scal[S_RNORM] <= c->h_scal[S_TARGET] ||
-                                                    c->h_scal[S_DONE] == 2.0);
-    rep->status = PF_OK;
-    if (c->h_scal[S_DONE] == 2.0) {
-        PF_CU(c, cudaMemsetAsync(B.x, 0, sizeof(double) * B.n, st), "memset");
-        rep->iterations = 0;
-        rep->final_residual_norm = 0.0;
-    }
-    if (c->h_scal[S_FAIL] != 0.0) {
-        char msg[160];
-        if (c->h_scal[S_FAIL] == 1.0)
-            snprintf(msg, sizeof msg, "cg: p'Ap = %.3e <= 0 at iteration %lld (operator not positive definite)",
-                     c->h_scal[S_PAP], (long long)c->h_scal[S_ITER] + 1);
-        else
-            snprintf(msg, sizeof msg, "cg: preconditioner not SPD at iteration %lld",
-                     (long long)c->h_scal[S_ITER]);
-        rep->status = PF_EBREAKDOWN;
-        return set_error(c, PF_EBREAKDOWN, msg);
-    }
-    return PF_OK;
+    return pcg_finish(c, B, rep, st);
 }
 
 int elastic_solve(Ctx* c, const double* alpha, const double* u0, double* u_out, const pf_lin_opts* o,
@@ -906,6 +921,7 @@ int pf_ctx_create(const pf_desc* desc, pf_ctx** out) {
     if (getenv("PF_NO_GRAPHS")) c->use_graphs = 0;
     if (getenv("PF_GMG_LEGACY")) c->gmg_coarse = 0;
     if (getenv("PF_GMG_SKIP_COARSE")) c->gmg_coarse = 2;
+    if (getenv("PF_PCG_GRAPH")) c->pcg_persistent = 0;
     if (d3) {
         c->dim = 3;
         c->dof = 3;

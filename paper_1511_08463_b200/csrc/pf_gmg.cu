@@ -911,22 +911,6 @@ struct CoarseArgs {
     CLev lev[kMaxLev];
 };
 
-// software grid barrier (all CTAs co-resident: cooperative launch).  One arrival word: CTA 0 adds
-// 2^31 - (nb - 1), the others 1, so the top bit flips exactly when the last CTA arrives.
-__device__ __forceinline__ void grid_sync(unsigned int* bar) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const unsigned int inc = blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1) : 1u;
-        __threadfence();
-        const unsigned int old = atomicAdd(bar, inc);
-        unsigned int cur;
-        do {
-            asm volatile("ld.acquire.gpu.u32 %0, [%1];\n" : "=r"(cur) : "l"(bar) : "memory");
-        } while (((old ^ cur) & 0x80000000u) == 0);
-    }
-    __syncthreads();
-}
-
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));

@@ -79,6 +79,22 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
+// software grid barrier (all CTAs co-resident: cooperative launch).  One arrival word: CTA 0 adds
+// 2^31 - (nb - 1), the others 1, so the top bit flips exactly when the last CTA arrives.
+__device__ __forceinline__ void grid_sync(unsigned int* bar) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned int inc = blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1) : 1u;
+        __threadfence();
+        const unsigned int old = atomicAdd(bar, inc);
+        unsigned int cur;
+        do {
+            asm volatile("ld.acquire.gpu.u32 %0, [%1];\n" : "=r"(cur) : "l"(bar) : "memory");
+        } while (((old ^ cur) & 0x80000000u) == 0);
+    }
+    __syncthreads();
+}
+
 // Block-reduce NV values, store per-block partials, and let the last block sum them in a
 // fixed order; `fin(vals)` runs on thread 0 of the last block with the grid totals.
 template <int NV, class Fin>
@@ -285,6 +301,7 @@ struct Ctx {
     double* gmg_dense = nullptr;
     double* gmg_ainv = nullptr;
     unsigned int* gmg_bar = nullptr;   // grid barrier of the persistent coarse-cycle kernel (2 words)
+    int pcg_persistent = 1;         // damage PCG in one cooperative launch (PF_PCG_GRAPH=1: graph loop)
     int gmg_coarse = 1;             // persistent coarse cycle (0: one launch per phase, PF_GMG_LEGACY)
     int gmg_degree = 2;
     int gmg_built = 0;              // hierarchy valid for reuse (pf_lin_opts.gmg_reuse)
@@ -390,6 +407,8 @@ struct PcgBuffers {
     double *x, *r, *z, *p0, *p1, *q, *dinv, *b;
     long long n;
 };
+// the whole Kaa Jacobi-PCG loop in one cooperative launch (2D); PF_EINVAL: not resident -> graph loop
+int launch_pcg_kaa(Ctx* c, const PcgBuffers& B, const double* kappa, const unsigned char* act, cudaStream_t st);
 // kind: 0 = Kuu Jacobi (coef = alpha), 1 = Kaa masked by act (coef = kappa), 2 = Kuu GMG
 int pcg_run(Ctx* c, int kind, const PcgBuffers& B, const double* coef, const unsigned char* act,
             double rtol, double atol, long long maxit, int zero_x0, int check_every,

@@ -73,17 +73,15 @@ __device__ __forceinline__ unsigned getb(const Slots& s, int q, long long v) {
 }
 
 // ---- the strip engine ----------------------------------------------------------------------
+// One pass of the engine for global warp index gw (= one strip of vertex rows x 30 columns).
 template <class Op, int PAT>
-__global__ void __launch_bounds__(kBlock, Op::MINB) k_strip2d(const Geo2 g, Op op) {
+__device__ __forceinline__ void strip_pass(const Geo2& g, Op& op, unsigned char* smem, int gw) {
     constexpr int NV = Op::NV, NC = Op::NC, PD = Op::pd(PAT);
     constexpr int NE = Op::ne(PAT) > 0 ? Op::ne(PAT) : 1;
     constexpr int SV = Op::sv(PAT), SC = Op::sc(PAT) > 0 ? Op::sc(PAT) : 0;
     constexpr int STAGE = (SV + SC) * 256;
-    extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31;
-    const int gw = blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5);
     const int wj = gw % g.nwj, wi = gw / g.nwj;
-    if (!op.enter()) return;  // device-side early exit (solver converged): uniform
     if (wi < g.nstrips) {
         unsigned char* wbase = smem + (threadIdx.x >> 5) * (PD * STAGE);
         const int j = wj * kLanesOut - 1 + lane;
@@ -159,6 +157,13 @@ __global__ void __launch_bounds__(kBlock, Op::MINB) k_strip2d(const Geo2 g, Op o
         }
         cp_wait<0>();
     }
+}
+
+template <class Op, int PAT>
+__global__ void __launch_bounds__(kBlock, Op::MINB) k_strip2d(const Geo2 g, Op op) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    if (!op.enter()) return;  // device-side early exit (solver converged): uniform
+    strip_pass<Op, PAT>(g, op, smem, blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5));
     op.finish();
 }
 
@@ -585,6 +590,8 @@ struct OpKaa {
     double* scal;
     RedBuf rb;
     double acc;
+    double breg = 0.0;  // persistent PCG (k_pcg_kaa): beta held in a register instead of scal[S_BETA]
+    int use_breg = 0;
     __device__ bool enter() const {
         if (!FUSED) return true;
         return scal[S_DONE] == 0.0 && scal[S_FAIL] == 0.0;
@@ -592,7 +599,7 @@ struct OpKaa {
     __device__ __forceinline__ double xval(long long v) const {
         double z = __ldg(x + v);
         if (FUSED) {
-            const double b = scal[S_ITER] > 0.0 ? scal[S_BETA] : 0.0;
+            const double b = use_breg ? breg : (scal[S_ITER] > 0.0 ? scal[S_BETA] : 0.0);
             z = z + b * __ldg(pin + v);
         }
         return z;
@@ -607,7 +614,7 @@ struct OpKaa {
     __device__ __forceinline__ double staged(const Slots& s, long long v, bool& a) const {
         double z = get1(s, 0);
         if (FUSED) {
-            const double b = scal[S_ITER] > 0.0 ? scal[S_BETA] : 0.0;
+            const double b = use_breg ? breg : (scal[S_ITER] > 0.0 ? scal[S_BETA] : 0.0);
             z = z + b * get1(s, 1);
         }
         a = MASKED ? (getb(s, FUSED ? 2 : 1, v) != 0u) : false;
@@ -1556,6 +1563,159 @@ int launch_Kaa_cgA(Ctx* c, const double* kappa, const double* z, const double* p
     OpKaa<true, false> op{kappa, z, p_in, p_out, q, nullptr, c->scal, redbuf(c), 0.0};
     return run_strip(c, op, st, K_KAA_CG);
 }
+// ---- persistent damage PCG ----------------------------------------------------------------------
+// The whole Jacobi-PCG loop on the (masked) damage block in one cooperative launch
+// (linalg.py:106-152 as restated by pcg_run, kind 1): per iteration one strip pass (p = z + beta p,
+// q = Kaa p, p.q) and one vector pass (x += gamma p, r -= gamma q, z = D^-1 r, r.r, r.z), separated
+// by grid barriers; every CTA sums the per-CTA partials in the same fixed order, so all CTAs take
+// the same scalar decisions and the result is deterministic.  The strips are "virtual blocks"
+// distributed over the resident CTAs.  Replaces 2 dependent launches per iteration (each
+// latency-bound on a 4-17 MB problem) and the per-pair graph overhead.
+__device__ __forceinline__ void block_partials(const double* v, int nv, double* partials, int row0) {
+    __shared__ double sm[4][kBlock / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int k = 0; k < nv; ++k) {
+        const double t = warp_sum(v[k]);
+        if (lane == 0) sm[k][warp] = t;
+    }
+    __syncthreads();
+    if (warp == 0)
+        for (int k = 0; k < nv; ++k) {
+            double t = lane < kBlock / 32 ? sm[k][lane] : 0.0;
+            t = warp_sum(t);
+            if (lane == 0) partials[(size_t)(row0 + k) * kMaxBlocksRed + blockIdx.x] = t;
+        }
+}
+// after a grid barrier: the grid total of partial row `row` (fixed order; identical in every CTA)
+__device__ __forceinline__ double grid_total(const double* partials, int row) {
+    __shared__ double tot;
+    if (threadIdx.x < 32) {
+        double t = 0.0;
+        for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) t += __ldcg(partials + (size_t)row * kMaxBlocksRed + b);
+        t = warp_sum(t);
+        if (threadIdx.x == 0) tot = t;
+    }
+    __syncthreads();
+    const double r = tot;
+    __syncthreads();
+    return r;
+}
+
+template <bool MASKED, int PAT>
+__global__ void __launch_bounds__(kBlock, 2) k_pcg_kaa(const Geo2 g, OpKaa<true, MASKED> op, int nvb, long long n,
+                                                        double* x, double* r, double* z, double* p0, double* p1,
+                                                        double* q, const double* dinv, double* s, double* partials,
+                                                        unsigned int* bar) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    if (!(s[S_DONE] == 0.0 && s[S_FAIL] == 0.0)) return;  // uniform
+    const double target = s[S_TARGET], maxit = s[S_MAXIT];
+    double rz = s[S_RZ], beta = s[S_BETA], rn = s[S_RNORM], pap = 0.0, gm = 0.0;
+    long long it = (long long)s[S_ITER];
+    double done = 0.0, fail = 0.0;
+    const long long tid = blockIdx.x * (long long)kBlock + threadIdx.x, nth = (long long)gridDim.x * kBlock;
+    for (;;) {
+        double* pin = (it & 1) ? p1 : p0;
+        double* pout = (it & 1) ? p0 : p1;
+        op.x = z;
+        op.pin = pin;
+        op.pout = pout;
+        op.y = q;
+        op.acc = 0.0;
+        op.use_breg = 1;
+        op.breg = it > 0 ? beta : 0.0;
+        for (int vb = blockIdx.x; vb < nvb; vb += gridDim.x)
+            strip_pass<OpKaa<true, MASKED>, PAT>(g, op, smem, vb * (kBlock / 32) + (threadIdx.x >> 5));
+        block_partials(&op.acc, 1, partials, 0);
+        grid_sync(bar);
+        pap = grid_total(partials, 0);
+        if (!(pap > 0.0)) { fail = 1.0; break; }
+        gm = rz / pap;
+        double acc[2] = {0.0, 0.0};
+        for (long long i = tid; i < n; i += nth) {
+            const double xi = __ldcg(x + i) + gm * __ldcg(pout + i);
+            const double ri = __ldcg(r + i) - gm * __ldcg(q + i);
+            const double zi = dinv[i] * ri;
+            x[i] = xi;
+            r[i] = ri;
+            z[i] = zi;
+            acc[0] += ri * ri;
+            acc[1] += ri * zi;
+        }
+        block_partials(acc, 2, partials, 1);
+        grid_sync(bar);
+        const double rr = grid_total(partials, 1), rzn = grid_total(partials, 2);
+        ++it;
+        rn = sqrt(rr);
+        if (rn <= target) { done = 1.0; break; }
+        if (!(rzn > 0.0)) { fail = 2.0; break; }
+        beta = rzn / rz;
+        rz = rzn;
+        if ((double)it >= maxit) { done = 3.0; break; }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        s[S_ITER] = (double)it;
+        s[S_RNORM] = rn;
+        s[S_PAP] = pap;
+        s[S_GAMMA] = gm;
+        s[S_RZ] = rz;
+        s[S_BETA] = beta;
+        s[S_DONE] = done;
+        s[S_FAIL] = fail;
+    }
+}
+
+template <bool MASKED, int PAT>
+static int launch_pcg_kaa_pat(Ctx* c, const PcgBuffers& B, const double* kappa, const unsigned char* act,
+                              cudaStream_t st) {
+    using Op = OpKaa<true, MASKED>;
+    constexpr int smem = strip_smem<Op, PAT>();
+    static int per = -1;
+    if (per < 0) {
+        cudaError_t e = cudaFuncSetAttribute(k_pcg_kaa<MASKED, PAT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return check_cuda(c, e, "persistent pcg attribute");
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_pcg_kaa<MASKED, PAT>, kBlock, smem);
+        if (e != cudaSuccess) return check_cuda(c, e, "persistent pcg occupancy");
+    }
+    int dev = 0, nsm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const Geo2& g = c->g;
+    const int nvb = strip_blocks(g);
+    const int nb = std::min(nvb, nsm * std::max(per, 1));
+    if (per < 1 || nb > kMaxBlocksRed) return PF_EINVAL;  // caller falls back to the graph loop
+    Op op{kappa, B.z, B.p0, B.p1, B.q, act, c->scal, redbuf(c), 0.0};
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(nb);
+    cfg.blockDim = dim3(kBlock);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    const int ps = prof_begin(c, st);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_pcg_kaa<MASKED, PAT>, g, op, nvb, B.n, B.x, B.r, B.z, B.p0, B.p1, B.q,
+                                       (const double*)B.dinv, c->scal, c->partials, c->tickets + 62);
+    prof_end(c, st, ps, K_KAA_CG, 0.0);
+    c->launches++;
+    return check_cuda(c, e, "persistent pcg launch");
+}
+int launch_pcg_kaa(Ctx* c, const PcgBuffers& B, const double* kappa, const unsigned char* act, cudaStream_t st) {
+    if (c->dim != 2) return PF_EINVAL;
+    switch (c->g.pattern) {
+        case PF_UNION_JACK:
+            return act ? launch_pcg_kaa_pat<true, PF_UNION_JACK>(c, B, kappa, act, st)
+                       : launch_pcg_kaa_pat<false, PF_UNION_JACK>(c, B, kappa, act, st);
+        case PF_RIGHT:
+            return act ? launch_pcg_kaa_pat<true, PF_RIGHT>(c, B, kappa, act, st)
+                       : launch_pcg_kaa_pat<false, PF_RIGHT>(c, B, kappa, act, st);
+        default:
+            return act ? launch_pcg_kaa_pat<true, PF_CROSSED>(c, B, kappa, act, st)
+                       : launch_pcg_kaa_pat<false, PF_CROSSED>(c, B, kappa, act, st);
+    }
+}
+
 int launch_Kaa_diag(Ctx* c, const double* kappa, double* dinv, const unsigned char* act,
                     cudaStream_t st) {
     if (c->dim == 3) return launch3_Kaa_diag(c, kappa, dinv, act, st);

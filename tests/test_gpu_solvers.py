@@ -302,3 +302,27 @@ def test_persistent_coarse_cycle_matches_the_per_phase_cycle(pattern, shape, mon
     d = float((u0 - u1).abs().max()) / float(u1.abs().max())
     assert abs(k0 - k1) <= 1, (k0, k1, d)
     assert d < 1e-8, d
+
+
+@pytest.mark.parametrize("pattern", ["union_jack", "right", "crossed"])
+@pytest.mark.parametrize("shape", [(20, 11), (257, 65), (3, 2)])
+def test_persistent_damage_pcg_matches_graph_loop(pattern, shape, monkeypatch):
+    """The damage PCG in one cooperative launch (grid barriers, in-kernel reductions) and the
+    graph-replayed two-kernel iteration solve the same masked box QP: same rsls history."""
+    import paper_1511_08463_b200 as pf
+    nx, ny = shape
+    out = {}
+    for graph in (False, True):
+        if graph:
+            monkeypatch.setenv("PF_PCG_GRAPH", "1")
+        else:
+            monkeypatch.delenv("PF_PCG_GRAPH", raising=False)
+        prob, om, rng = make_pair(pattern, "plane_strain", "AT2", nx, ny, hetero=True, eps0=True)
+        u, a, lb = random_fields(om, rng, u_scale=0.4)
+        st = pf.State(dev(u), dev(a), dev(lb))
+        out[graph] = pf.damage_step(st, prob, pf.SolverConfig(outer_atol=1e-9))
+    (a0, r0), (a1, r1) = out[False], out[True]
+    assert r0.converged and r1.converged
+    assert r0.iterations == r1.iterations
+    assert abs(r0.total_krylov_iterations - r1.total_krylov_iterations) <= r0.iterations
+    assert float((a0 - a1).abs().max()) < 1e-9
