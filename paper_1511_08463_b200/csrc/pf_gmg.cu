@@ -662,35 +662,36 @@ __device__ __forceinline__ double w1d(int f, int nf, int C) {
 }
 // 2:1 restriction b_c = P^T r_f (with masks), one thread per coarse vertex; fv(f) = fine value.
 // The 3x3 fine neighbourhood is gathered unconditionally (clamped addresses, zero weights).
-template <bool SH = false, class FV>
+// G > 1: G lanes share the coarse vertex (fine points t = q, q + G, ...), lane 0 stores.
+template <bool SH = false, int G = 1, class FV>
 __device__ __forceinline__ void v_restrict_f(const LevelDev& F, const LevelDev& Cd, const unsigned char* maskc,
-                                             FV fv, double* bc, long long v) {
+                                             FV fv, double* bc, long long v, int q = 0) {
     const int nvyf = F.ny + 1, nvyc = Cd.ny + 1;
     const int vi = (int)v;
     const int I = vi / nvyc, J = vi - (vi / nvyc) * nvyc;
-    const unsigned mC = maskc[v];
     double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        const int fi = 2 * I - 1 + a;
-        const double wfx = w1d(fi, F.nx, I);
-#pragma unroll
-        for (int b = 0; b < 3; ++b) {
-            const int fj = 2 * J - 1 + b;
-            const double w = wfx * w1d(fj, F.ny, J);
-            const long long f = (long long)min(max(fi, 0), F.nx) * nvyf + min(max(fj, 0), F.ny);
-            const unsigned mf = F.mask ? F.mask[f] : 0u;
-            const double2 rv = fv(f);
-            if (w != 0.0 && !(mf & 1u)) s0 += w * rv.x;
-            if (w != 0.0 && !(mf & 2u)) s1 += w * rv.y;
-        }
+    for (int u = 0; u < (9 + G - 1) / G; ++u) {
+        const int t = (G == 1) ? u : q + u * G;
+        if (G > 1 && t >= 9) break;
+        const int fi = 2 * I - 1 + t / 3, fj = 2 * J - 1 + t % 3;
+        const double w = w1d(fi, F.nx, I) * w1d(fj, F.ny, J);
+        const long long f = (long long)min(max(fi, 0), F.nx) * nvyf + min(max(fj, 0), F.ny);
+        const unsigned mf = F.mask ? F.mask[f] : 0u;
+        const double2 rv = fv(f);
+        if (w != 0.0 && !(mf & 1u)) s0 += w * rv.x;
+        if (w != 0.0 && !(mf & 2u)) s1 += w * rv.y;
     }
+    s0 = gsum<G>(s0);
+    s1 = gsum<G>(s1);
+    if (G > 1 && q != 0) return;
+    const unsigned mC = maskc[v];
     stv<SH>(bc, v, make_double2((mC & 1u) ? 0.0 : s0, (mC & 2u) ? 0.0 : s1));
 }
-template <bool SH = false>
+template <bool SH = false, int G = 1>
 __device__ __forceinline__ void v_restrict(const LevelDev& F, const LevelDev& Cd, const unsigned char* maskc,
-                                           const double* r, double* bc, long long v) {
-    v_restrict_f<SH>(F, Cd, maskc, [&](long long f) { return ldv<SH>(r, f); }, bc, v);
+                                           const double* r, double* bc, long long v, int q = 0) {
+    v_restrict_f<SH, G>(F, Cd, maskc, [&](long long f) { return ldv<SH>(r, f); }, bc, v, q);
 }
 __global__ void k_restrict(LevelDev F, LevelDev Cd, const unsigned char* maskc, const double* r, double* bc,
                            const double* live) {
@@ -937,7 +938,7 @@ __global__ void __launch_bounds__(kCB, 1) k_gmg_coarse(const __grid_constant__ C
     auto grid_each = [&](long long nv, auto fn) {
         if (4 * nv <= nth)
             for (long long e = tid; e < 4 * nv; e += nth) fn(G4{}, e >> 2, (int)(e & 3));
-        else if (2 * nv <= nth)
+        else if (2 * nv <= nth)  // (2 lanes in 2 rounds measured slower than 1 lane in 1 round)
             for (long long e = tid; e < 2 * nv; e += nth) fn(G2{}, e >> 1, (int)(e & 1));
         else
             for (long long v = tid; v < nv; v += nth) fn(G1{}, v, 0);
@@ -969,9 +970,9 @@ __global__ void __launch_bounds__(kCB, 1) k_gmg_coarse(const __grid_constant__ C
                     }
                 return make_double2(s0, s1);
             };
-            for (long long v = tid; v < C.L.nv; v += nth) v_restrict_f(A.L0, C.L, C.L.mask, collapse, C.b, v);
+            grid_each(C.L.nv, [&](auto g, long long v, int q) { v_restrict_f<false, decltype(g)::value>(A.L0, C.L, C.L.mask, collapse, C.b, v, q); });
         } else {
-            for (long long v = tid; v < C.L.nv; v += nth) v_restrict(A.L0, C.L, C.L.mask, A.r0, C.b, v);
+            grid_each(C.L.nv, [&](auto g, long long v, int q) { v_restrict<false, decltype(g)::value>(A.L0, C.L, C.L.mask, A.r0, C.b, v, q); });
         }
     }
     grid_sync(A.bar);
@@ -999,7 +1000,7 @@ __global__ void __launch_bounds__(kCB, 1) k_gmg_coarse(const __grid_constant__ C
         grid_sync(A.bar);
         TR();
         const CLev& C = A.lev[l + 1];
-        for (long long v = tid; v < C.L.nv; v += nth) v_restrict(V.L, C.L, C.L.mask, V.r, C.b, v);
+        grid_each(C.L.nv, [&](auto g, long long v, int q) { v_restrict<false, decltype(g)::value>(V.L, C.L, C.L.mask, V.r, C.b, v, q); });
         grid_sync(A.bar);
         TR();
     }
