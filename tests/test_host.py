@@ -115,3 +115,45 @@ def test_reference_solver_choices_map_to_device_options():
     assert o.precond == 1 and o.rtol == 1e-12      # reference default precond: multigrid at direct_rtol
     o = S._lin_opts(S.SolverConfig(elastic_solver="direct"), False)
     assert o.precond == 0                            # configured Jacobi kept
+
+
+def test_fieldsplit_inner_choices_map_onto_the_c_options():
+    """fieldsplit_inner: 'direct' (blocks solved to a tolerance), 'cg' (fixed PCG budget, the
+    reference inner_cg) and 'mg' (device: one V-cycle for A, Chebyshev-Jacobi for C) map onto
+    pf_vi_opts.inner_mode / inner_cycles; anything else is rejected like the reference."""
+    from paper_1511_08463_b200 import solver as S
+    from paper_1511_08463_b200.vi import VIConfig
+    with pytest.raises(ValueError):
+        SolverConfig(fieldsplit_inner="amg")
+    captured = {}
+
+    class Stop(Exception):
+        pass
+
+    class FakeProblem:
+        def call(self, name, *args):
+            captured["opts"] = args[5]._obj
+            raise Stop
+
+    class FakeState:
+        u = alpha = alpha_lb = None
+
+        def copy(self):
+            return self
+
+    orig, orig_stream = S._lib.ptr, S._stream
+    S._lib.ptr = lambda t: 0
+    S._stream = lambda: None
+    try:
+        for inner, mode, cycles in [("direct", 0, 0), ("cg", 0, 5), ("mg", 1, 12)]:
+            with pytest.raises(Stop):
+                S.coupled_newton_solve(FakeState(), FakeProblem(), SolverConfig(fieldsplit_inner=inner))
+            o = captured["opts"]
+            assert (o.inner_mode, o.inner_cycles) == (mode, cycles), inner
+        with pytest.raises(Stop):
+            S.coupled_newton_solve(FakeState(), FakeProblem(),
+                                   SolverConfig(fieldsplit_inner="mg", fieldsplit_cheb_degree=7))
+        assert captured["opts"].inner_cycles == 7
+    finally:
+        S._lib.ptr, S._stream = orig, orig_stream
+    assert VIConfig(inner_mode=1).to_c().inner_mode == 1
