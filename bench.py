@@ -121,7 +121,7 @@ def thermal_config(pf):
 def traction3d_config(pf):
     return pf.SolverConfig(method="oram_newton", omega=1.7, outer_atol=1e-6, elastic_solver="cg",
                            elastic_rtol=1e-8, elastic_precond="gmg", max_am_iterations=3000,
-                           fieldsplit_inner="direct")  # 3D: "mg" stalls at step 5 of this run (under study)
+                           fieldsplit_inner="mg")
 
 
 def traction1_setup(pf):

@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "pf_internal.cuh"
@@ -21,6 +22,11 @@
 namespace pf {
 
 constexpr int kNB = 256;
+// Chebyshev interval top for the C block: power iteration approaches lambda_max from below, and a
+// Chebyshev polynomial preconditioner turns indefinite for eigenvalues much above the interval
+// (degree 12: ~5% above already flips its sign) -- so a wider margin than the reference's 1.1
+// (measured: 1.1 stalled 3D Newton on config 4).
+constexpr double kChebSafety = 1.5;
 
 __global__ void k_ndot(long long n, const double* a, const double* b, double* s, int slot, RedBuf rb) {
     double acc[1] = {0.0};
@@ -219,7 +225,7 @@ static int lambda_C(Ctx* c, double& lmax, cudaStream_t st) {
 static int cheb_C(Ctx* c, const double* b, double* x, double lmax, int deg, long long& its, cudaStream_t st) {
     const long long n = c->n_a;
     const int nb = nblocks(n);
-    const double hi = 1.1 * lmax, lo = hi / 30.0;
+    const double hi = kChebSafety * lmax, lo = hi / 30.0;
     const double theta = 0.5 * (hi + lo), delta = 0.5 * (hi - lo), sigma = theta / delta;
     double *r = c->da_r, *d = c->da_p0, *Cd = c->da_q;
     k_ncheb0<<<nb, kNB, 0, st>>>(n, c->da_dinv, b, r, d, x, 1.0 / theta);
@@ -344,6 +350,8 @@ static int minres(Ctx* c, NewtonWs& w, const double* u, const double* alpha, con
     // keep the rotated buffer roles in the workspace struct consistent for the next call
     converged = phibar <= target;
     kits += it;
+    if (getenv("PF_NEWTON_TRACE"))
+        fprintf(stderr, "  minres: its=%lld beta1=%.3e phibar=%.3e target=%.3e\n", it, beta1, phibar, target);
     return PF_OK;
 }
 
@@ -391,6 +399,7 @@ int newton_solve(Ctx* c, const double* u_in, const double* a_in, const double* l
             double mt;
             NTRY(eval_F(c, w, w.TX, w.TF, lb, mt, st));
             const double bound = newton ? (1.0 - 2.0 * o->armijo * mu) * merit : merit - slope * mu;
+            if (getenv("PF_NEWTON_TRACE")) fprintf(stderr, "  ls: mu=%.3e merit=%.6e bound=%.6e\n", mu, mt, bound);
             if (mt <= bound) {
                 ok = true;
                 merit = mt;
