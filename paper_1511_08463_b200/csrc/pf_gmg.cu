@@ -923,14 +923,23 @@ __device__ __forceinline__ unsigned long long gtimer() {
     } while (0)
 
 constexpr int kCB = 512;  // threads per CTA of the persistent coarse cycle (one CTA per SM; 1024 measured slower)
-__global__ void __launch_bounds__(kCB, 1) k_gmg_coarse(const __grid_constant__ CoarseArgs A, const double* lam,
-                                                       const double* live) {
-    if (!gmg_live(live) || A.skip) return;  // uniform: the flags are not written during the launch
-    extern __shared__ __align__(16) unsigned char sm[];
-    const long long tid = blockIdx.x * (long long)kCB + threadIdx.x;
-    const long long nth = (long long)gridDim.x * kCB;
+// Chebyshev coefficients of every level into shared memory (threads t < nl; read by the phases
+// after the first barrier)
+__device__ __forceinline__ void coarse_coef(const CoarseArgs& A, const double* lam, CCoef* coef) {
+    const int t0 = threadIdx.x;
+    if (t0 < A.nl) {
+        CCoef& q = coef[t0];
+        q.c = cheb_of(lam + t0, A.ratio);
+        for (int k = 1; k < A.deg && k < kMaxDeg; ++k) cheb_ab(q.c, k, q.a[k], q.b[k]);
+    }
+}
+
+// The coarse part of one V-cycle as grid-wide phases (global thread index tid of nth); ends with
+// the level-0 prolongation into A.z0 (the caller synchronises before reading it).
+__device__ __forceinline__ void coarse_body(const CoarseArgs& A, const CCoef* coef, long long tid, long long nth) {
     const int deg = A.deg;
     const int t0 = threadIdx.x;
+    (void)t0;
     // stencil phases: 4 (or 2) lanes per vertex when the level is small enough (shorter chains)
     using G1 = std::integral_constant<int, 1>;
     using G2 = std::integral_constant<int, 2>;
@@ -945,12 +954,6 @@ __global__ void __launch_bounds__(kCB, 1) k_gmg_coarse(const __grid_constant__ C
     };
     int ntr = 0;
     TR();
-    CCoef* coef = reinterpret_cast<CCoef*>(sm + A.coef_off);
-    if (t0 < A.nl) {  // Chebyshev coefficients of every level (read by the phases after the first barrier)
-        CCoef& q = coef[t0];
-        q.c = cheb_of(lam + t0, A.ratio);
-        for (int k = 1; k < deg && k < kMaxDeg; ++k) cheb_ab(q.c, k, q.a[k], q.b[k]);
-    }
     // level 0 -> 1 restriction (crossed: centres collapsed onto the corners on the fly)
     {
         const CLev& C = A.lev[1];
@@ -1078,6 +1081,15 @@ __global__ void __launch_bounds__(kCB, 1) k_gmg_coarse(const __grid_constant__ C
             for (long long v = tid; v < A.L0.nv; v += nth) v_prolong(A.L0, C.L, C.L.mask, C.x, A.z0, v);
         }
     }
+}
+
+__global__ void __launch_bounds__(kCB, 1) k_gmg_coarse(const __grid_constant__ CoarseArgs A, const double* lam,
+                                                       const double* live) {
+    if (!gmg_live(live) || A.skip) return;  // uniform: the flags are not written during the launch
+    extern __shared__ __align__(16) unsigned char sm[];
+    CCoef* coef = reinterpret_cast<CCoef*>(sm + A.coef_off);
+    coarse_coef(A, lam, coef);
+    coarse_body(A, coef, blockIdx.x * (long long)kCB + threadIdx.x, (long long)gridDim.x * kCB);
 }
 
 // z_f = 0 helper + level-0 vector ops
@@ -1343,13 +1355,14 @@ static int coarse_plan(const Ctx* c, CoarseArgs& a) {
     return (int)sizeof(CCoef) * nl;
 }
 
-static int launch_coarse(Ctx* c, const double* r0, double* z0, cudaStream_t st, const double* live) {
+// Arguments of the coarse cycle for fine residual r0 and correction z0; returns the shared memory
+// bytes (coefficient table) or -1 when the hierarchy does not fit the persistent cycle.
+static int make_coarse_args(Ctx* c, const double* r0, double* z0, CoarseArgs& a) {
     const Geo2& g = c->g;
     const int nl = (int)c->glev.size();
-    CoarseArgs a;
     memset(&a, 0, sizeof(a));
     const int smem = coarse_plan(c, a);
-    if (smem < 0) return set_error(c, PF_EINVAL, "gmg: coarse tail does not fit in shared memory");
+    if (smem < 0) return -1;
     a.g = g;
     a.crossed = g.pattern == PF_CROSSED;
     a.mask0 = g.has_bc ? c->glev[0].mask : nullptr;
@@ -1364,16 +1377,25 @@ static int launch_coarse(Ctx* c, const double* r0, double* z0, cudaStream_t st, 
     a.ncoarse = (int)(2 * c->glev[nl - 1].nv);
     a.bar = c->gmg_bar;
     a.skip = c->gmg_coarse == 2;
-    static unsigned long long* trace = nullptr;
-    static int ntrace_calls = 0;
-    if (getenv("PF_GMG_TRACE") && !trace) cudaMalloc(&trace, 128 * sizeof(unsigned long long));
-    a.trace = trace;
     for (int l = 1; l < nl; ++l) {
         GLevel& L = c->glev[l];
         a.lev[l].L = ldev(c, l);
         a.lev[l].x = L.x; a.lev[l].b = L.b; a.lev[l].r = L.r;
         a.lev[l].d0 = L.d0; a.lev[l].d1 = L.d1; a.lev[l].res = L.res;
     }
+    return smem;
+}
+
+static int launch_coarse(Ctx* c, const double* r0, double* z0, cudaStream_t st, const double* live) {
+    const Geo2& g = c->g;
+    const int nl = (int)c->glev.size();
+    CoarseArgs a;
+    const int smem = make_coarse_args(c, r0, z0, a);
+    if (smem < 0) return set_error(c, PF_EINVAL, "gmg: hierarchy too deep for the persistent coarse cycle");
+    static unsigned long long* trace = nullptr;
+    static int ntrace_calls = 0;
+    if (getenv("PF_GMG_TRACE") && !trace) cudaMalloc(&trace, 128 * sizeof(unsigned long long));
+    a.trace = trace;
     static int nb_cache = 0, nb_smem = -1;
     if (nb_smem != smem) {
         int dev = 0, nsm = 0, per = 0;

@@ -220,6 +220,8 @@ struct OpKuu {
     double acc;
     GmgEpi e{};
     double ca = 0.0, cb = 0.0, th = 1.0;
+    double breg = 0.0;  // persistent PCG (k_pcg_gmg2d): beta held in a register instead of scal[S_BETA]
+    int use_breg = 0;
 
     __device__ bool enter() {
         if constexpr (EPI != EPI_NONE) {
@@ -266,7 +268,7 @@ struct OpKuu {
             st2(e.dnext, id, rr.x / th, rr.y / th);
         }
     }
-    __device__ __forceinline__ double beta() const { return scal[S_ITER] > 0.0 ? scal[S_BETA] : 0.0; }
+    __device__ __forceinline__ double beta() const { return use_breg ? breg : (scal[S_ITER] > 0.0 ? scal[S_BETA] : 0.0); }
     __device__ __forceinline__ double2 xval(long long v) const {  // direct (boundary rows only)
         double2 z = ld2(x, v);
         if (FUSED) {
