@@ -13,7 +13,7 @@ base = dict(method="oram_newton", omega=1.8, outer_atol=1e-6, am_switch_atol=1e-
             elastic_rtol=1e-8, elastic_precond="gmg", max_am_iterations=2000, fieldsplit_inner="mg")
 st = pf.State.zeros(setup.mesh, setup.initial_alpha_lb)
 pf.run_quasistatic(setup, pf.SolverConfig(**base), snapshot_stride=0, state=st, steps=list(range(k)))
-for guess in ("relaxed", "previous", "relaxed", "previous"):
+for guess in sys.argv[2:] or ("relaxed", "previous"):
     cfg = pf.SolverConfig(**base, elastic_guess=guess)
     s = st.copy()
     torch.cuda.synchronize(); t0 = time.perf_counter()
