@@ -87,7 +87,7 @@ class SolverConfig:
             raise ValueError(f"unknown elastic_precond {self.elastic_precond!r}")
         if self.coupled_solver not in _COUPLED:
             raise ValueError(f"unknown coupled_solver {self.coupled_solver!r}")
-        if self.elastic_guess not in ("previous", "relaxed") and not self.elastic_guess.startswith("extrap"):
+        if self.elastic_guess not in ("previous", "relaxed"):
             raise ValueError(f"unknown elastic_guess {self.elastic_guess!r}")
         if self.fieldsplit_inner not in _INNER:
             raise ValueError(f"unknown fieldsplit_inner {self.fieldsplit_inner!r}")
@@ -229,17 +229,13 @@ def am_solve(state: State, problem: Discretization, config: SolverConfig,
     report.energy_history.append(e0)
     report.residual_history.append(phi0)
     d_prev = None
-    u_guess = u_last = None
+    u_guess = None
     while report.am_iterations < config.max_am_iterations:
         report.am_iterations += 1
         u_prev = state.u
         u_star, kit = elastic_step(state, problem, config, u0=u_guess)
-        if config.elastic_guess == "previous":
+        if config.elastic_guess == "previous":  # (linear extrapolation of u* measured no better)
             u_guess = u_star
-        elif config.elastic_guess.startswith("extrap"):  # experimental: u* + theta (u* - u*_prev)
-            theta = float(config.elastic_guess[6:] or 1.0)
-            u_guess = u_star if u_last is None else u_star + theta * (u_star - u_last)
-        u_last = u_star
         report.total_krylov_iterations += kit
         state.u = relax_u(u_prev, u_star, config.omega, problem)
 
