@@ -421,9 +421,15 @@ int newton_solve(Ctx* c, const double* u_in, const double* a_in, const double* l
         NCU(c, cudaMemcpyAsync(w.RHS, w.FX, sizeof(double) * nu, cudaMemcpyDeviceToDevice, st), "copy");
         // Jacobian-dependent setup: GMG hierarchy of Kuu(alpha), kappa(u) and masked diag(Kaa)
         NCU(c, cudaMemcpyAsync(c->alpha_ws, alpha, sizeof(double) * na, cudaMemcpyDeviceToDevice, st), "copy");
-        NTRY(c->dim == 3 ? gmg3_setup(c, st) : gmg_setup(c, st));
-        c->gmg_built = 1;  // an elastic solve that follows may keep it (gmg_reuse)
-        c->gmg_its0 = -1;
+        // inner_mode 1 (the V-cycle is only a preconditioner): the first Newton iteration keeps the
+        // hierarchy of the last AM elastic solve (alpha one damage update older; damage only grows,
+        // so the old smoother bounds stay above the spectrum) -- one setup (~2.5 ms) saved per phase
+        const bool keep = o->inner_mode == 1 && it == 1 && c->gmg_built;
+        if (!keep) {
+            NTRY(c->dim == 3 ? gmg3_setup(c, st) : gmg_setup(c, st));
+            c->gmg_built = 1;  // an elastic solve that follows may keep it (gmg_reuse)
+            c->gmg_its0 = -1;
+        }
         NTRY(launch_kappa(c, u, alpha, c->kappa, c->vi_c, st));
         NTRY(launch_Kaa_diag(c, c->kappa, c->da_dinv, c->act, st));
         InnerMg mg;
