@@ -498,7 +498,7 @@ int pcg_run(Ctx* c, int kind, const PcgBuffers& B, const double* coef, const uns
     // per-kernel profiling is on (eager launches bracketed by events, host-polled batches).
     if (kind == 1 && c->dim == 2 && c->pcg_persistent && c->h_scal[S_DONE] == 0.0 && c->h_scal[S_FAIL] == 0.0) {
         // damage block: every iteration inside one cooperative launch (no host polls, no graph)
-        const int rc = launch_pcg_kaa(c, B, coef, act, st);
+        const int rc = c->pcg_single ? launch_pcg_kaa1(c, B, coef, act, st) : launch_pcg_kaa(c, B, coef, act, st);
         if (rc == PF_OK) {
             PF_TRY(read_scal(c, st, 0, 24));
             return pcg_finish(c, B, rep, st);
@@ -867,6 +867,7 @@ static void plan_workspace(Ctx* c) {
                         &c->u_ws, &c->ubar};
     for (auto p : uvecs) add((void**)p, U);
     double** avecs[] = {&c->da_x, &c->da_r, &c->da_z, &c->da_p0, &c->da_p1, &c->da_q, &c->da_dinv,
+                        &c->cg1_s0, &c->cg1_s1,
                         &c->vi_x, &c->vi_F, &c->vi_c, &c->vi_d, &c->vi_tx, &c->vi_tF, &c->vi_g, &c->vi_w,
                         &c->alpha_ws};
     for (auto p : avecs) add((void**)p, A);
@@ -922,6 +923,7 @@ int pf_ctx_create(const pf_desc* desc, pf_ctx** out) {
     if (getenv("PF_GMG_LEGACY")) c->gmg_coarse = 0;
     if (getenv("PF_GMG_SKIP_COARSE")) c->gmg_coarse = 2;
     if (getenv("PF_PCG_GRAPH")) c->pcg_persistent = 0;
+    if (getenv("PF_PCG_SINGLE")) c->pcg_single = 1;
     if (d3) {
         c->dim = 3;
         c->dof = 3;

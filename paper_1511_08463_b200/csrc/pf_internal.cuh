@@ -273,6 +273,7 @@ struct Ctx {
     // named buffers (device)
     double *cg_x, *cg_r, *cg_z, *cg_p0, *cg_p1, *cg_q, *cg_dinv, *cg_b;     // n_u
     double *da_x, *da_r, *da_z, *da_p0, *da_p1, *da_q, *da_dinv;             // n_a (damage CG)
+    double *cg1_s0, *cg1_s1;                                                 // n_a (single-reduction CG)
     double *vi_x, *vi_F, *vi_c, *vi_d, *vi_tx, *vi_tF, *vi_g, *vi_w;          // n_a
     double *kappa;                                                           // n_el
     double *alpha_ws, *u_ws;                                                 // n_a, n_u
@@ -302,6 +303,7 @@ struct Ctx {
     double* gmg_ainv = nullptr;
     unsigned int* gmg_bar = nullptr;   // grid barrier of the persistent coarse-cycle kernel (2 words)
     int pcg_persistent = 1;         // damage PCG in one cooperative launch (PF_PCG_GRAPH=1: graph loop)
+    int pcg_single = 0;             // ... in the single-reduction form (PF_PCG_SINGLE=1; measured slower)
     int gmg_coarse = 1;             // persistent coarse cycle (0: one launch per phase, PF_GMG_LEGACY)
     int gmg_degree = 2;
     int gmg_built = 0;              // hierarchy valid for reuse (pf_lin_opts.gmg_reuse)
@@ -407,7 +409,9 @@ struct PcgBuffers {
     double *x, *r, *z, *p0, *p1, *q, *dinv, *b;
     long long n;
 };
-// the whole Kaa Jacobi-PCG loop in one cooperative launch (2D); PF_EINVAL: not resident -> graph loop
+// the whole Kaa Jacobi-PCG loop in one cooperative launch (2D): two-phase standard PCG (kaa) or the
+// single-reduction Chronopoulos-Gear form (kaa1); PF_EINVAL: not resident -> graph loop
+int launch_pcg_kaa1(Ctx* c, const PcgBuffers& B, const double* kappa, const unsigned char* act, cudaStream_t st);
 int launch_pcg_kaa(Ctx* c, const PcgBuffers& B, const double* kappa, const unsigned char* act, cudaStream_t st);
 // kind: 0 = Kuu Jacobi (coef = alpha), 1 = Kaa masked by act (coef = kappa), 2 = Kuu GMG
 int pcg_run(Ctx* c, int kind, const PcgBuffers& B, const double* coef, const unsigned char* act,

@@ -1666,6 +1666,241 @@ __global__ void __launch_bounds__(kBlock, 2) k_pcg_kaa(const Geo2 g, OpKaa<true,
     }
 }
 
+// ---- single-reduction damage PCG (Chronopoulos-Gear) ---------------------------------------------
+// The same Krylov space as linalg.py:106-152 with the recurrences rearranged so that one strip
+// pass per iteration does everything: with u = M r, w = A u, s = A p and the scalars
+// alpha_i, beta_i known at the start of iteration i,
+//   s_i = w_i + beta_i s_{i-1} ; r_{i+1} = r_i - alpha_i s_i ; u_{i+1} = M r_{i+1} (pointwise,
+//   recomputed at every stencil point from staged r_i, w_i, s_{i-1}, dinv) ; w_{i+1} = A u_{i+1}
+//   (the stencil) ; p_i = u_i + beta_i p_{i-1} ; x_{i+1} = x_i + alpha_i p_i (own vertex)
+// and one grid reduction gives gamma = r.u, delta = w.u and |r|^2 for
+//   beta_{i+1} = gamma_{i+1} / gamma_i ; alpha_{i+1} = gamma_{i+1} / (delta_{i+1} - beta_{i+1} gamma_{i+1} / alpha_i).
+// r, w and s are double-buffered by iteration parity (neighbours read the old ones).
+// vertex slots: r, w, s_prev, dinv, [act word]; cell: Gc, kappa x npc, [centre: the same]
+template <bool MASKED>
+struct OpKaaCG1 {
+    static constexpr int NV = 1, NC = 1, MINB = 2;
+    static constexpr int VS = 4 + (MASKED ? 1 : 0);
+    static constexpr int pd(int pat) { return pat == PF_CROSSED ? 4 : 6; }
+    static constexpr int ne(int pat) { return 1 + npc_of(pat) + 2 * crossed(pat); }
+    static constexpr int sv(int) { return VS; }
+    static constexpr int sc(int pat) { return 1 + npc_of(pat) + crossed(pat) * VS; }
+    const double* kappa;
+    const double *r, *w, *sp;   // r_i, w_i, s_{i-1}
+    double *rn, *wn, *sn;       // r_{i+1}, w_{i+1}, s_i
+    double *p, *x;              // in place
+    const double* dinv;
+    const unsigned char* act;
+    double al, be;              // alpha_i, beta_i (be = 0: s_{-1}, p_{-1} unused)
+    int init;                   // 1: the start-up pass w_0 = A u_0 only (u_0 = M r_0)
+    double acc[3];              // gamma, delta, |r|^2 (own vertices)
+    __device__ bool enter() const { return true; }
+    __device__ void finish() {}
+    __device__ __forceinline__ double unext(double ri, double wi, double si, double di) const {
+        if (init) return di * ri;
+        const double s = be != 0.0 ? wi + be * si : wi;
+        return di * (ri - al * s);
+    }
+    __device__ __forceinline__ void stage_vertex(const Slots& s, long long v) const {
+        put1(s, 0, r, v);
+        put1(s, 1, w, v);
+        put1(s, 2, sp, v);
+        put1(s, 3, dinv, v);
+        if (MASKED) putb(s, 4, act, v);
+    }
+    __device__ __forceinline__ double staged(const Slots& s, long long v, bool& a) const {
+        a = MASKED ? (getb(s, 4, v) != 0u) : false;
+        return a ? 0.0 : unext(get1(s, 0), get1(s, 1), get1(s, 2), get1(s, 3));
+    }
+    __device__ void issue_v(const Geo2& g, int i, int j, const Slots& s) const { stage_vertex(s, vid(g, i, j)); }
+    __device__ void fix_v(const Geo2& g, int i, int j, const Slots& s, double (&v)[NV]) const {
+        bool a;
+        v[0] = staged(s, vid(g, i, j), a);
+    }
+    template <int PAT>
+    __device__ void issue_c(const Geo2& g, int ci, int j, const Slots& s) const {
+        const long long cell = cid(g, ci, j);
+        putGc(g, s, 0, cell);
+        put_kappa<PAT>(g, kappa, cell, s, 1);
+        if constexpr (PAT == PF_CROSSED) stage_vertex(s.at(1 + npc_of(PAT)), ctr(g, ci, j));
+    }
+    template <int PAT, int NE>
+    __device__ void fix_c(const Geo2& g, int ci, int j, const Slots& s, double (&e)[NE]) const {
+        e[0] = getGc(g, s, 0);
+        get_kappa<PAT>(s, 1, 1, e);
+        if constexpr (PAT == PF_CROSSED) {
+            bool a;
+            e[5] = staged(s.at(1 + npc_of(PAT)), ctr(g, ci, j), a);
+            e[6] = a ? 1.0 : 0.0;
+        }
+    }
+    // own vertex: finish the pointwise recurrences (y = (A u_{i+1})_id, u = u_{i+1}(id))
+    __device__ __forceinline__ void own(long long id, double y, double u, bool a) {
+        if (a) y = 0.0;  // masked operator: identity rows act on u = 0
+        wn[id] = y;
+        if (init) {
+            acc[0] += __ldcg(r + id) * u;
+            acc[1] += y * u;
+            return;
+        }
+        const double ri = __ldcg(r + id), wi = __ldcg(w + id);
+        const double s = be != 0.0 ? wi + be * __ldcg(sp + id) : wi;
+        const double r1 = ri - al * s;
+        const double ui = a ? 0.0 : __ldg(dinv + id) * ri;  // u_i = M r_i
+        const double pi = be != 0.0 ? ui + be * __ldcg(p + id) : ui;
+        sn[id] = s;
+        rn[id] = r1;
+        p[id] = pi;
+        x[id] = __ldcg(x + id) + al * pi;
+        acc[0] += r1 * u;
+        acc[1] += y * u;
+        acc[2] += r1 * r1;
+    }
+    template <int PAT, int NE>
+    __device__ void cell(const Geo2& g, int ci, int j, const double (&vc)[NV], const double (&vn)[NV],
+                         const double (&rc)[NV], const double (&rn_)[NV], const double (&ec)[NE],
+                         double (&c00)[NC], double (&c10)[NC], double (&c01)[NC], double (&c11)[NC],
+                         bool own_) {
+        double X[5] = {vc[0], vn[0], rc[0], rn_[0], 0.0};
+        if constexpr (PAT == PF_CROSSED) X[4] = ec[5];
+        double Y[5] = {0, 0, 0, 0, 0};
+        const int par = (PAT == PF_UNION_JACK) ? ((ci + j) & 1) : 0;
+        const double hxs = par ? -g.ihx : g.ihx;
+        mirror<PAT>(par, X);
+        const double kc = ec[0] / g.cw;
+        for_each_elem<PAT>(par, [&](auto T, auto S, auto A, auto B, auto C) {
+            elem_kaa<PAT, T.v, A.v, B.v, C.v>(g, j, hxs, ec[1 + S.v], kc, X, Y);
+        });
+        mirror<PAT>(par, Y);
+        c00[0] = Y[0]; c10[0] = Y[1]; c01[0] = Y[2]; c11[0] = Y[3];
+        if constexpr (PAT == PF_CROSSED) {
+            if (own_) own(ctr(g, ci, j), Y[4], ec[5], ec[6] != 0.0);
+        }
+    }
+    __device__ void out(const Geo2& g, int i, int j, const double (&t)[NC], const double (&v)[NV]) {
+        const long long id = vid(g, i, j);
+        own(id, t[0], v[0], MASKED && act[id] != 0);
+    }
+};
+
+template <bool MASKED, int PAT>
+__global__ void __launch_bounds__(kBlock, 2) k_pcg_kaa1(const Geo2 g, OpKaaCG1<MASKED> op0, int nvb, double* rb0,
+                                                         double* rb1, double* wb0, double* wb1, double* sb0,
+                                                         double* sb1, double* s, double* partials,
+                                                         unsigned int* bar) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    if (!(s[S_DONE] == 0.0 && s[S_FAIL] == 0.0)) return;  // uniform
+    const double target = s[S_TARGET], maxit = s[S_MAXIT];
+    long long it = (long long)s[S_ITER];
+    double rn = s[S_RNORM], done = 0.0, fail = 0.0;
+    double* rb[2] = {rb0, rb1};
+    double* wb[2] = {wb0, wb1};
+    double* sb[2] = {sb0, sb1};
+    auto pass = [&](int init, long long i, double al, double be) {
+        OpKaaCG1<MASKED> op = op0;
+        op.init = init;
+        op.al = al;
+        op.be = be;
+        op.r = rb[i & 1];
+        op.w = wb[i & 1];
+        op.rn = rb[(i + 1) & 1];
+        op.wn = wb[init ? (i & 1) : ((i + 1) & 1)];
+        op.sp = sb[(i + 1) & 1];
+        op.sn = sb[i & 1];
+        op.acc[0] = op.acc[1] = op.acc[2] = 0.0;
+        for (int vb = blockIdx.x; vb < nvb; vb += gridDim.x)
+            strip_pass<OpKaaCG1<MASKED>, PAT>(g, op, smem, vb * (kBlock / 32) + (threadIdx.x >> 5));
+        block_partials(op.acc, 3, partials, 0);
+        grid_sync(bar);
+    };
+    // start-up: w_0 = A u_0 (u_0 = M r_0 from k_cg_init), gamma_0 = r.u (= S_RZ), delta_0 = w.u
+    pass(1, 0, 0.0, 0.0);
+    double gam = grid_total(partials, 0), del = grid_total(partials, 1);
+    double al = gam / del, be = 0.0;
+    if (!(gam > 0.0)) fail = 2.0;
+    else if (!(del > 0.0)) fail = 1.0;
+    for (long long i = 0; fail == 0.0; ++i) {
+        pass(0, i, al, be);
+        const double gn = grid_total(partials, 0), dn = grid_total(partials, 1);
+        rn = sqrt(grid_total(partials, 2));
+        ++it;
+        if (rn <= target) { done = 1.0; break; }
+        if (!(gn > 0.0)) { fail = 2.0; break; }
+        be = gn / gam;
+        const double den = dn - be * gn / al;
+        if (!(den > 0.0)) { fail = 1.0; break; }
+        al = gn / den;
+        gam = gn;
+        if ((double)it >= maxit) { done = 3.0; break; }
+    }
+    // the solution lives in x; r of the last iteration in rb[it & 1]
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        s[S_ITER] = (double)it;
+        s[S_RNORM] = rn;
+        s[S_RZ] = gam;
+        s[S_DONE] = done;
+        s[S_FAIL] = fail;
+    }
+}
+
+template <bool MASKED, int PAT>
+static int launch_pcg_kaa1_pat(Ctx* c, const PcgBuffers& B, const double* kappa, const unsigned char* act,
+                               cudaStream_t st) {
+    using Op = OpKaaCG1<MASKED>;
+    constexpr int smem = strip_smem<Op, PAT>();
+    static int per = -1;
+    if (per < 0) {
+        cudaError_t e = cudaFuncSetAttribute(k_pcg_kaa1<MASKED, PAT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return check_cuda(c, e, "persistent pcg attribute");
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_pcg_kaa1<MASKED, PAT>, kBlock, smem);
+        if (e != cudaSuccess) return check_cuda(c, e, "persistent pcg occupancy");
+    }
+    int dev = 0, nsm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const Geo2& g = c->g;
+    const int nvb = strip_blocks(g);
+    const int nb = std::min(nvb, nsm * std::max(per, 1));
+    if (per < 1 || nb > kMaxBlocksRed) return PF_EINVAL;
+    // buffers: r_0 = B.r and u_0 = B.z from k_cg_init; x = B.x (zero start); p, s, w work vectors
+    Op op{};
+    op.kappa = kappa;
+    op.dinv = B.dinv;
+    op.act = act;
+    op.p = B.p0;
+    op.x = B.x;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(nb);
+    cfg.blockDim = dim3(kBlock);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    const int ps = prof_begin(c, st);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_pcg_kaa1<MASKED, PAT>, g, op, nvb, B.r, B.z, B.q, B.p1, c->cg1_s0,
+                                       c->cg1_s1, c->scal, c->partials, c->tickets + 62);
+    prof_end(c, st, ps, K_KAA_CG, 0.0);
+    c->launches++;
+    return check_cuda(c, e, "persistent pcg launch");
+}
+int launch_pcg_kaa1(Ctx* c, const PcgBuffers& B, const double* kappa, const unsigned char* act, cudaStream_t st) {
+    if (c->dim != 2) return PF_EINVAL;
+    switch (c->g.pattern) {
+        case PF_UNION_JACK:
+            return act ? launch_pcg_kaa1_pat<true, PF_UNION_JACK>(c, B, kappa, act, st)
+                       : launch_pcg_kaa1_pat<false, PF_UNION_JACK>(c, B, kappa, act, st);
+        case PF_RIGHT:
+            return act ? launch_pcg_kaa1_pat<true, PF_RIGHT>(c, B, kappa, act, st)
+                       : launch_pcg_kaa1_pat<false, PF_RIGHT>(c, B, kappa, act, st);
+        default:
+            return act ? launch_pcg_kaa1_pat<true, PF_CROSSED>(c, B, kappa, act, st)
+                       : launch_pcg_kaa1_pat<false, PF_CROSSED>(c, B, kappa, act, st);
+    }
+}
+
 template <bool MASKED, int PAT>
 static int launch_pcg_kaa_pat(Ctx* c, const PcgBuffers& B, const double* kappa, const unsigned char* act,
                               cudaStream_t st) {

@@ -306,17 +306,22 @@ def test_persistent_coarse_cycle_matches_the_per_phase_cycle(pattern, shape, mon
 
 @pytest.mark.parametrize("pattern", ["union_jack", "right", "crossed"])
 @pytest.mark.parametrize("shape", [(20, 11), (257, 65), (3, 2)])
-def test_persistent_damage_pcg_matches_graph_loop(pattern, shape, monkeypatch):
-    """The damage PCG in one cooperative launch (grid barriers, in-kernel reductions) and the
+@pytest.mark.parametrize("variant", ["single", "twophase"])
+def test_persistent_damage_pcg_matches_graph_loop(pattern, shape, variant, monkeypatch):
+    """The damage PCG in one cooperative launch (grid barriers, in-kernel reductions; the
+    single-reduction Chronopoulos-Gear form or the two-phase standard form) and the
     graph-replayed two-kernel iteration solve the same masked box QP: same rsls history."""
     import paper_1511_08463_b200 as pf
     nx, ny = shape
     out = {}
     for graph in (False, True):
+        monkeypatch.delenv("PF_PCG_SINGLE", raising=False)
         if graph:
             monkeypatch.setenv("PF_PCG_GRAPH", "1")
         else:
             monkeypatch.delenv("PF_PCG_GRAPH", raising=False)
+            if variant == "single":
+                monkeypatch.setenv("PF_PCG_SINGLE", "1")
         prob, om, rng = make_pair(pattern, "plane_strain", "AT2", nx, ny, hetero=True, eps0=True)
         u, a, lb = random_fields(om, rng, u_scale=0.4)
         st = pf.State(dev(u), dev(a), dev(lb))
