@@ -290,6 +290,11 @@ __global__ void k_clip_max(long long n, const double* __restrict__ x0, const dou
 }
 
 // activity classification (vi.py:127-141) + masked right-hand side rhs = F on N, 0 on A.
+// zeta = zero_tol, or 1e-10 (1 + |x0|_inf) as vi.py:198-201 (|x0|_inf from k_clip_max)
+__global__ void k_set_zeta(const unsigned long long* xmax, double* s, double zero_tol) {
+    s[S_ZETA] = zero_tol > 0.0 ? zero_tol : 1e-10 * (1.0 + __longlong_as_double((long long)*xmax));
+}
+
 __global__ void k_classify(long long n, const double* __restrict__ x, const double* __restrict__ F,
                            const double* __restrict__ lb, unsigned char* __restrict__ act,
                            double* __restrict__ rhs, double* s, RedBuf rb) {
@@ -446,7 +451,11 @@ int pcg_run(Ctx* c, int kind, const PcgBuffers& B, const double* coef, const uns
             c->launches++;
         }
     }
-    PF_TRY(read_scal(c, st, 0, 24));
+    // No host poll here: the persistent and graph loops below check the done/fail flags on the
+    // device (the start-up may already have converged); only the eager loop needs them now.
+    const bool graphs = c->use_graphs && !c->prof.on;
+    const bool persistent = kind == 1 && c->dim == 2 && c->pcg_persistent;
+    if (!graphs && !persistent) PF_TRY(read_scal(c, st, 0, 24));
     // one Krylov iteration k (ping-pong search-direction buffers by parity)
     auto issue_iter = [&](long long k, cudaStream_t s) -> int {
         double* pin = (k & 1) ? B.p1 : B.p0;
@@ -496,7 +505,7 @@ int pcg_run(Ctx* c, int kind, const PcgBuffers& B, const double* coef, const uns
     // failed -- no host polling, at most one no-op iteration after convergence.  Kernels read
     // every scalar from device memory, so the body is replayed unchanged.  Disabled while
     // per-kernel profiling is on (eager launches bracketed by events, host-polled batches).
-    if (kind == 1 && c->dim == 2 && c->pcg_persistent && c->h_scal[S_DONE] == 0.0 && c->h_scal[S_FAIL] == 0.0) {
+    if (persistent) {
         // damage block: every iteration inside one cooperative launch (no host polls, no graph)
         const int rc = c->pcg_single ? launch_pcg_kaa1(c, B, coef, act, st) : launch_pcg_kaa(c, B, coef, act, st);
         if (rc == PF_OK) {
@@ -505,7 +514,7 @@ int pcg_run(Ctx* c, int kind, const PcgBuffers& B, const double* coef, const uns
         }
         if (rc != PF_EINVAL) return rc;
     }
-    const bool graphs = c->use_graphs && !c->prof.on;
+    if (persistent && !graphs) PF_TRY(read_scal(c, st, 0, 24));  // fallback to the eager loop
     const long long key = c->geo_version * 16 + (gmg ? c->gmg_degree : 0);
     // the captured body bakes in these pointers: re-capture when any of them changes
     const void* body_ptrs[Ctx::kGraphPtrs] = {B.x, B.r, B.z, B.p0, B.p1, B.q, B.dinv, coef, act};
@@ -555,14 +564,11 @@ int pcg_run(Ctx* c, int kind, const PcgBuffers& B, const double* coef, const uns
     }
     long long k = 0;
     int batch = std::max(2, check_every + (check_every & 1));
-    if (graphs) {
-        if (c->h_scal[S_DONE] == 0.0 && c->h_scal[S_FAIL] == 0.0) {
-            const double it0 = c->h_scal[S_ITER];
-            PF_CU(c, cudaGraphLaunch(c->graph_exec[kind], st), "graph launch");
-            PF_TRY(read_scal(c, st, 0, 24));
-            const long long pairs = ((long long)(c->h_scal[S_ITER] - it0) + 2) / 2;
-            c->launches += pairs * c->graph_nodes[kind];
-        }
+    if (graphs) {  // a solve that converged at start-up runs one no-op pair (device-side flags)
+        PF_CU(c, cudaGraphLaunch(c->graph_exec[kind], st), "graph launch");
+        PF_TRY(read_scal(c, st, 0, 24));
+        const long long pairs = ((long long)c->h_scal[S_ITER] + 2) / 2;
+        c->launches += pairs * c->graph_nodes[kind];
     } else {
         while (c->h_scal[S_DONE] == 0.0 && c->h_scal[S_FAIL] == 0.0) {
             for (int t = 0; t < batch; ++t, ++k) PF_TRY(issue_iter(k, st));
@@ -643,14 +649,8 @@ int damage_solve(Ctx* c, const double* u, const double* lb, const double* a_in, 
     // x = clip(a_in), zeta
     PF_CU(c, cudaMemsetAsync(c->bits, 0, sizeof(unsigned long long) * 8, st), "memset bits");
     k_clip_max<<<vb, kVecBlock, 0, st>>>(n, a_in, lb, c->vi_x, c->bits + 1);
-    c->launches++;
-    PF_CU(c, cudaMemcpyAsync(c->h_scal + 100, c->bits + 1, sizeof(double), cudaMemcpyDeviceToHost, st),
-          "xmax");
-    PF_CU(c, cudaStreamSynchronize(st), "sync");
-    double xmax;
-    memcpy(&xmax, c->h_scal + 100, sizeof(double));
-    const double zeta = o->zero_tol > 0.0 ? o->zero_tol : 1e-10 * (1.0 + xmax);
-    PF_TRY(set_scal(c, st, S_ZETA, zeta));
+    k_set_zeta<<<1, 1, 0, st>>>(c->bits + 1, c->scal, o->zero_tol);  // no host round trip
+    c->launches += 2;
     double *x = c->vi_x, *F = c->vi_F, *tx = c->vi_tx, *tF = c->vi_tF;
     PF_TRY(launch_Kaa_trial(c, c->kappa, c->vi_c, x, nullptr, lb, tx, F, nullptr, S_MERIT, st));
     PF_TRY(read_scal(c, st, 0, 24));
@@ -730,8 +730,7 @@ int damage_solve(Ctx* c, const double* u, const double* lb, const double* a_in, 
     rep->final_residual_norm = std::sqrt(merit);
     rep->converged = rep->final_residual_norm <= o->abs_tol;
     PF_CU(c, cudaMemcpyAsync(a_out, x, sizeof(double) * n, cudaMemcpyDeviceToDevice, st), "alpha out");
-    PF_CU(c, cudaStreamSynchronize(st), "sync");
-    return PF_OK;
+    return PF_OK;  // stream-ordered: the caller's next kernels see a_out
 }
 
 }  // namespace pf
