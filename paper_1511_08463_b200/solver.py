@@ -74,6 +74,7 @@ class SolverConfig:
     elastic_guess: str = "previous"
     check_every: int = 8
     gmg_reuse: bool = True   # keep the GMG hierarchy across solves while it stays effective
+    gmg_degree: int = 2      # Chebyshev smoothing degree per multigrid level
     newton_inner_rtol: Optional[float] = None  # field-split block solves; None -> fieldsplit_rtol
 
     def __post_init__(self):
@@ -148,7 +149,7 @@ def _lin_opts(config: SolverConfig, warm: bool) -> _lib.LinOpts:
     # multigrid when the configured one (e.g. the reference default "ssor") has no device form
     prec = _lib.PREC.get(config.elastic_precond, _lib.PREC["gmg"])
     return _lib.LinOpts(precond=prec, warm_start=1 if warm else 0, maxit=0, rtol=rtol, atol=0.0,
-                        check_every=config.check_every, gmg_levels=0, cheb_degree=2,
+                        check_every=config.check_every, gmg_levels=0, cheb_degree=config.gmg_degree,
                         gmg_reuse=1 if config.gmg_reuse else 0)
 
 
