@@ -624,8 +624,16 @@ int elastic_solve(Ctx* c, const double* alpha, const double* u0, double* u_out, 
         return rc;
     }
     if (gmg) {
-        if (c->gmg_its0 < 0) c->gmg_its0 = rep->iterations;
-        else if (rep->iterations > (3 * c->gmg_its0) / 2 + 2) c->gmg_built = 0;  // refresh next time
+        // refresh the hierarchy once the iterations it costs beyond those of its first solve add up
+        // to about one setup (a rebuild costs ~10 V-cycle iterations; warm-started solves make
+        // single-solve ratios noisy)
+        if (c->gmg_its0 < 0) {
+            c->gmg_its0 = rep->iterations;
+            c->gmg_excess = 0;
+        } else {
+            c->gmg_excess += std::max(0LL, (long long)rep->iterations - c->gmg_its0);
+            if (c->gmg_excess > kGmgRebuildIts) c->gmg_built = 0;  // refresh next time
+        }
     }
     PF_CU(c, cudaMemcpyAsync(u_out, B.x, sizeof(double) * c->n_u, cudaMemcpyDeviceToDevice, st), "u copy");
     if (!rep->converged) {
@@ -695,7 +703,12 @@ int damage_solve(Ctx* c, const double* u, const double* lb, const double* a_in, 
             const long long maxit = o->inner_maxit > 0 ? o->inner_maxit : 10 * n;
             // atol floor: after an exact-active-set Newton step the VI merit equals the reduced
             // residual, so converging it below 0.1*abs_tol buys nothing (vi.py:222-240)
-            rc = pcg_run(c, 1, B, c->kappa, c->act, o->inner_rtol, 0.1 * o->abs_tol, maxit, 1, 8, &lr, st);
+            // inner_mode 1: inexact Newton with the quadratic forcing term rtol = min(1e-2, |Phi|)
+            // (never tighter than inner_rtol): far from the solution the reduced system is solved
+            // loosely, close to it as before; the VI stopping rule (merit <= abs_tol) is unchanged
+            const double rtol = o->inner_mode == 1 ? std::max(o->inner_rtol, std::min(1e-2, std::sqrt(merit)))
+                                                   : o->inner_rtol;
+            rc = pcg_run(c, 1, B, c->kappa, c->act, rtol, 0.1 * o->abs_tol, maxit, 1, 8, &lr, st);
             rep->total_krylov_iterations += lr.iterations;
             if (rc == PF_EBREAKDOWN) {
                 rep->linear_failures++;

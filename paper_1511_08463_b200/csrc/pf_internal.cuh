@@ -22,6 +22,7 @@
 
 namespace pf {
 
+constexpr int kGmgRebuildIts = 12;  // excess PCG iterations that trigger a multigrid rebuild
 constexpr int kBlock = 256;        // threads per block for strip kernels
 constexpr int kLanesOut = 30;      // output columns per warp
 constexpr int kMaxRed = 8;         // max values per fused reduction
@@ -308,6 +309,7 @@ struct Ctx {
     int gmg_degree = 2;
     int gmg_built = 0;              // hierarchy valid for reuse (pf_lin_opts.gmg_reuse)
     long long gmg_its0 = -1;        // iterations of the first elastic solve on it (-1: none yet)
+    long long gmg_excess = 0;       // iterations beyond gmg_its0 accumulated by the later solves on it
     std::vector<unsigned char> h_bcmask;  // last Dirichlet mask (detects mask changes)
     double gmg_ratio = 0.1;
     // device-side Krylov loop graphs per solver kind (0 Kuu-Jacobi, 1 Kaa-masked, 2 Kuu-GMG):

@@ -67,6 +67,9 @@ class SolverConfig:
     # device knobs
     direct_rtol: float = 1e-12
     damage_rtol: float = 1e-10
+    # inexact rsls Newton for the damage VI: inner rtol = min(1e-2, |Phi|) (never below damage_rtol);
+    # thermal slab: damage half-step -21%, same iterates (the VI stopping rule is unchanged)
+    damage_forcing: bool = True
     warm_start: bool = True
     # initial Krylov iterate of the AM elastic solves: "previous" = the last elastic solution u*
     # (measured: SENT 512^2 AM phase -35% wall, same iterates to 1e-12), "relaxed" = the
@@ -172,7 +175,8 @@ def elastic_step(state: State, problem: Discretization, config: SolverConfig, u0
 def damage_step(state: State, problem: Discretization, config: SolverConfig):
     """Bound-constrained damage minimisation at fixed u (device rsls).  Returns (alpha, report)."""
     vic = VIConfig(abs_tol=config.damage_atol_factor * config.outer_atol,
-                   max_iterations=config.max_vi_iterations, inner_rtol=config.damage_rtol)
+                   max_iterations=config.max_vi_iterations, inner_rtol=config.damage_rtol,
+                   inner_mode=1 if config.damage_forcing else 0)
     opts = vic.to_c()
     rep = _lib.VIReport()
     out = torch.empty_like(state.alpha)

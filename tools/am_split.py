@@ -13,7 +13,8 @@ setup = pf.setup_sent(n=n)
 cfg = pf.SolverConfig(method="oram_newton", omega=1.8, outer_atol=1e-6, am_switch_atol=1e-3,
                       elastic_solver="cg", elastic_rtol=1e-8, elastic_precond="gmg",
                       max_am_iterations=2000, fieldsplit_inner="mg",
-                      gmg_degree=int(os.environ.get("DEG", "2")))
+                      gmg_degree=int(os.environ.get("DEG", "2")),
+                      damage_forcing=bool(int(os.environ.get("FORCING", "0"))))
 st = pf.State.zeros(setup.mesh, setup.initial_alpha_lb)
 pf.run_quasistatic(setup, cfg, snapshot_stride=0, state=st, steps=list(range(k)))
 acc = defaultdict(lambda: [0, 0.0])
