@@ -111,10 +111,12 @@ typedef struct pf_vi_opts {
                              * this many PCG iterations at rtol 1e-12 (fieldsplit_inner = "cg",
                              * inner_cg linalg.py:446-456); 0 -> solved to inner_rtol.
                              * inner_mode 1: the Chebyshev degree of the C block (<= 0 -> 12) */
-    int32_t inner_mode;     /* Newton only: 0 -> block solves as above; 1 -> fixed linear SPD block
+    int32_t inner_mode;     /* Newton: 0 -> block solves as above; 1 -> fixed linear SPD block
                              * preconditioners: A^-1 ~ one multigrid V-cycle, C^-1 ~ Chebyshev-Jacobi
-                             * on [lmax/30, 1.1 lmax] (lmax by 30 power iterations, as the
-                             * reference ChebyshevPreconditioner linalg.py:331-378) */
+                             * on [lmax/30, 1.5 lmax] (lmax by 30 power iterations, the reference
+                             * ChebyshevPreconditioner recipe linalg.py:331-378), symmetric
+                             * multiplicative split; 2 -> the same blocks, block-diagonal split.
+                             * Damage solve: 1 -> inexact rsls Newton, inner rtol = min(1e-2, |Phi|). */
 } pf_vi_opts;
 
 typedef struct pf_vi_report {

@@ -250,8 +250,9 @@ static int vcycle_A(Ctx* c, const double* b, double* x, long long& its, cudaStre
 }
 
 // y = P^-1 r (symmetric multiplicative field split, linalg.py:424-430)
-struct InnerMg {  // inner_mode 1
+struct InnerMg {  // inner_mode 1 (multiplicative) / 2 (additive)
     bool on = false;
+    bool additive = false;
     int deg = 12;
     double lmax = 0.0;
 };
@@ -260,6 +261,13 @@ static int fieldsplit(Ctx* c, const NewtonWs& w, const double* r, double* y, con
     const long long nu = w.nu, na = w.na;
     double* y1 = y;              // u part of y
     double* z = y + nu;          // alpha part of y
+    if (mg.on && mg.additive) {  // block-diagonal field split: P^-1 = diag(V-cycle, Chebyshev)
+        NTRY(vcycle_A(c, r, y1, its, st));
+        k_nsubmask<<<nblocks(na), kNB, 0, st>>>(na, r + nu, nullptr, c->act, w.TMP + nu);
+        c->launches++;
+        NTRY(cheb_C(c, w.TMP + nu, z, mg.lmax, mg.deg, its, st));
+        return PF_OK;
+    }
     if (mg.on) {
         NTRY(vcycle_A(c, r, y1, its, st));
         NTRY(launch_Kau(c, u, alpha, y1, w.TMP + nu, PF_BC_ELIMINATE, st));            // B^T y1
@@ -424,7 +432,7 @@ int newton_solve(Ctx* c, const double* u_in, const double* a_in, const double* l
         // inner_mode 1 (the V-cycle is only a preconditioner): the first Newton iteration keeps the
         // hierarchy of the last AM elastic solve (alpha one damage update older; damage only grows,
         // so the old smoother bounds stay above the spectrum) -- one setup (~2.5 ms) saved per phase
-        const bool keep = o->inner_mode == 1 && it == 1 && c->gmg_built;
+        const bool keep = (o->inner_mode == 1 || o->inner_mode == 2) && it == 1 && c->gmg_built;
         if (!keep) {
             NTRY(c->dim == 3 ? gmg3_setup(c, st) : gmg_setup(c, st));
             c->gmg_built = 1;  // an elastic solve that follows may keep it (gmg_reuse)
@@ -433,8 +441,9 @@ int newton_solve(Ctx* c, const double* u_in, const double* a_in, const double* l
         NTRY(launch_kappa(c, u, alpha, c->kappa, c->vi_c, st));
         NTRY(launch_Kaa_diag(c, c->kappa, c->da_dinv, c->act, st));
         InnerMg mg;
-        if (o->inner_mode == 1) {
+        if (o->inner_mode == 1 || o->inner_mode == 2) {
             mg.on = true;
+            mg.additive = o->inner_mode == 2;
             mg.deg = o->inner_cycles > 0 ? o->inner_cycles : 12;
             NTRY(lambda_C(c, mg.lmax, st));
         }

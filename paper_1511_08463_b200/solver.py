@@ -59,6 +59,9 @@ class SolverConfig:
     fieldsplit_inner: str = "direct"
     fieldsplit_cg_budget: int = 5
     fieldsplit_cheb_degree: int = 12  # fieldsplit_inner="mg": Chebyshev degree of the C block
+    # fieldsplit_inner="mg": block-diagonal instead of the reference's symmetric multiplicative
+    # split (measured on SENT 512^2: 19 vs 18 MINRES iterations at half the cost each)
+    fieldsplit_additive: bool = True
     fieldsplit_rtol: float = 1e-6
     damage_atol_factor: float = 0.1
     max_vi_iterations: int = 200
@@ -291,7 +294,7 @@ def coupled_newton_solve(state: State, problem: Discretization, config: SolverCo
                    inner_rtol=config.newton_inner_rtol or (config.direct_rtol if direct else 0.0),
                    inner_cycles=(config.fieldsplit_cheb_degree if mg else config.fieldsplit_cg_budget)
                    if (config.fieldsplit_inner in ("cg", "mg") and not direct) else 0,
-                   inner_mode=1 if mg else 0)
+                   inner_mode=(2 if config.fieldsplit_additive else 1) if mg else 0)
     opts = vic.to_c()
     rep = _lib.VIReport()
     out = state.copy()

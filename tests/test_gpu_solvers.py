@@ -251,7 +251,7 @@ def test_fused_relax_physics_equals_separate_passes(pattern, omega):
     assert res1 == res2 and tuple(e1) == tuple(e2)
 
 
-@pytest.mark.parametrize("variant", ["direct", "inner_cg", "inner_mg"])
+@pytest.mark.parametrize("variant", ["direct", "inner_cg", "inner_mg", "inner_mg_mult"])
 def test_newton_coupled_solver_variants_converge_like_fieldsplit(variant):
     """coupled_solver='direct' (MINRES + field split at direct_rtol), fieldsplit_inner='cg'
     (fixed-budget inner PCG) and fieldsplit_inner='mg' (one V-cycle for A, Chebyshev-Jacobi for
@@ -265,7 +265,8 @@ def test_newton_coupled_solver_variants_converge_like_fieldsplit(variant):
     prob = setup.problem
     kw = {"direct": {"coupled_solver": "direct"},
           "inner_cg": {"fieldsplit_inner": "cg", "fieldsplit_cg_budget": 30},
-          "inner_mg": {"fieldsplit_inner": "mg"}}[variant]
+          "inner_mg": {"fieldsplit_inner": "mg"},
+          "inner_mg_mult": {"fieldsplit_inner": "mg", "fieldsplit_additive": False}}[variant]
     ref_cfg = pf.SolverConfig(outer_atol=1e-9, elastic_solver="cg", elastic_precond="gmg")
     var_cfg = pf.SolverConfig(outer_atol=1e-9, elastic_solver="cg", elastic_precond="gmg", **kw)
     s1, r1 = S.coupled_newton_solve(st, prob, ref_cfg)

@@ -145,7 +145,7 @@ def test_fieldsplit_inner_choices_map_onto_the_c_options():
     S._lib.ptr = lambda t: 0
     S._stream = lambda: None
     try:
-        for inner, mode, cycles in [("direct", 0, 0), ("cg", 0, 5), ("mg", 1, 12)]:
+        for inner, mode, cycles in [("direct", 0, 0), ("cg", 0, 5), ("mg", 2, 12)]:
             with pytest.raises(Stop):
                 S.coupled_newton_solve(FakeState(), FakeProblem(), SolverConfig(fieldsplit_inner=inner))
             o = captured["opts"]
@@ -154,6 +154,10 @@ def test_fieldsplit_inner_choices_map_onto_the_c_options():
             S.coupled_newton_solve(FakeState(), FakeProblem(),
                                    SolverConfig(fieldsplit_inner="mg", fieldsplit_cheb_degree=7))
         assert captured["opts"].inner_cycles == 7
+        with pytest.raises(Stop):
+            S.coupled_newton_solve(FakeState(), FakeProblem(),
+                                   SolverConfig(fieldsplit_inner="mg", fieldsplit_additive=False))
+        assert captured["opts"].inner_mode == 1
     finally:
         S._lib.ptr, S._stream = orig, orig_stream
     assert VIConfig(inner_mode=1).to_c().inner_mode == 1
