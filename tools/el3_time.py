@@ -14,7 +14,8 @@ st = pf.State.zeros(setup.mesh)
 t = float(setup.schedule[4])
 setup.apply_load(prob, st, t)
 st.u[prob._bc_dofs_dev] = prob._bc_vals_dev
-cfg = pf.SolverConfig(elastic_solver="cg", elastic_rtol=1e-8, elastic_precond="gmg", warm_start=False)
+cfg = pf.SolverConfig(elastic_solver="cg", elastic_rtol=1e-8, elastic_precond="gmg", warm_start=False,
+                      gmg_degree=int(os.environ.get("DEG", "2")))
 S.elastic_step(st, prob, cfg)
 torch.cuda.synchronize(); t0 = time.perf_counter()
 for _ in range(reps):
