@@ -432,7 +432,9 @@ int newton_solve(Ctx* c, const double* u_in, const double* a_in, const double* l
         // inner_mode 1 (the V-cycle is only a preconditioner): the first Newton iteration keeps the
         // hierarchy of the last AM elastic solve (alpha one damage update older; damage only grows,
         // so the old smoother bounds stay above the spectrum) -- one setup (~2.5 ms) saved per phase
-        const bool keep = (o->inner_mode == 1 || o->inner_mode == 2) && it == 1 && c->gmg_built;
+        // 2D only: the 3D re-discretised hierarchy with a stale alpha preconditioned config-4 Newton
+        // badly (~160 instead of ~20 MINRES iterations, measured)
+        const bool keep = c->dim == 2 && (o->inner_mode == 1 || o->inner_mode == 2) && it == 1 && c->gmg_built;
         if (!keep) {
             NTRY(c->dim == 3 ? gmg3_setup(c, st) : gmg_setup(c, st));
             c->gmg_built = 1;  // an elastic solve that follows may keep it (gmg_reuse)

@@ -13,7 +13,9 @@ inner = sys.argv[3] if len(sys.argv) > 3 else "direct"
 setup = pf.setup_traction3d(n=n)
 cfg = pf.SolverConfig(method="oram_newton", omega=1.7, outer_atol=1e-6, elastic_solver="cg",
                       elastic_rtol=1e-8, elastic_precond="gmg", max_am_iterations=3000,
-                      fieldsplit_inner=inner)
+                      fieldsplit_inner=inner,
+                      fieldsplit_additive=bool(int(os.environ.get("ADDITIVE", "1"))),
+                      damage_forcing=bool(int(os.environ.get("FORCING", "1"))))
 st = pf.State.zeros(setup.mesh)
 pf.run_quasistatic(setup, cfg, snapshot_stride=0, state=st, steps=list(range(k)))
 acc = defaultdict(lambda: [0, 0.0])
@@ -35,7 +37,7 @@ try:
 except Exception as e:  # noqa: BLE001
     print("FAILED:", e)
 torch.cuda.synchronize(); tot = time.perf_counter() - t0
-print(f"inner={inner} 2 load steps ({k},{k+1}): {1e3*tot:.1f} ms")
+print(f"inner={inner} add={cfg.fieldsplit_additive} forcing={cfg.damage_forcing} 2 load steps ({k},{k+1}): {1e3*tot:.1f} ms")
 for name, (c, t) in acc.items():
     print(f"  {name:22s} calls={c:4d} total={1e3*t:8.1f} ms  per call={1e3*t/max(c,1):7.3f} ms")
 for row in log:
