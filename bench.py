@@ -121,7 +121,8 @@ def thermal_config(pf):
 def traction3d_config(pf):
     return pf.SolverConfig(method="oram_newton", omega=1.7, outer_atol=1e-6, elastic_solver="cg",
                            elastic_rtol=1e-8, elastic_precond="gmg", max_am_iterations=3000,
-                           fieldsplit_inner="mg")
+                           fieldsplit_inner="mg",
+                           fieldsplit_cheb_degree=6)  # 3D: 104 vs 121 ms per Newton (degree 12)
 
 
 def traction1_setup(pf):

@@ -15,7 +15,8 @@ cfg = pf.SolverConfig(method="oram_newton", omega=1.7, outer_atol=1e-6, elastic_
                       elastic_rtol=1e-8, elastic_precond="gmg", max_am_iterations=3000,
                       fieldsplit_inner=inner,
                       fieldsplit_additive=bool(int(os.environ.get("ADDITIVE", "1"))),
-                      damage_forcing=bool(int(os.environ.get("FORCING", "1"))))
+                      damage_forcing=bool(int(os.environ.get("FORCING", "1"))),
+                      fieldsplit_cheb_degree=int(os.environ.get("CDEG", "12")))
 st = pf.State.zeros(setup.mesh)
 pf.run_quasistatic(setup, cfg, snapshot_stride=0, state=st, steps=list(range(k)))
 acc = defaultdict(lambda: [0, 0.0])
