@@ -1574,8 +1574,8 @@ int launch_Kaa_cgA(Ctx* c, const double* kappa, const double* z, const double* p
 // distributed over the resident CTAs.  Replaces 2 dependent launches per iteration (each
 // latency-bound on a 4-17 MB problem) and the per-pair graph overhead.
 __device__ __forceinline__ void block_partials(const double* v, int nv, double* partials, int row0) {
-    __shared__ double sm[4][kBlock / 32];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __shared__ double sm[4][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     for (int k = 0; k < nv; ++k) {
         const double t = warp_sum(v[k]);
         if (lane == 0) sm[k][warp] = t;
@@ -1583,7 +1583,7 @@ __device__ __forceinline__ void block_partials(const double* v, int nv, double* 
     __syncthreads();
     if (warp == 0)
         for (int k = 0; k < nv; ++k) {
-            double t = lane < kBlock / 32 ? sm[k][lane] : 0.0;
+            double t = lane < nw ? sm[k][lane] : 0.0;
             t = warp_sum(t);
             if (lane == 0) partials[(size_t)(row0 + k) * kMaxBlocksRed + blockIdx.x] = t;
         }
@@ -1603,8 +1603,27 @@ __device__ __forceinline__ double grid_total(const double* partials, int row) {
     return r;
 }
 
-template <bool MASKED, int PAT>
-__global__ void __launch_bounds__(kBlock, 2) k_pcg_kaa(const Geo2 g, OpKaa<true, MASKED> op, int nvb, long long n,
+// the totals of partial rows `row` and `row + 1` in one pass
+__device__ __forceinline__ double2 grid_total2(const double* partials, int row) {
+    __shared__ double2 tot2;
+    if (threadIdx.x < 32) {
+        double a = 0.0, b = 0.0;
+        for (int k = threadIdx.x; k < (int)gridDim.x; k += 32) {
+            a += __ldcg(partials + (size_t)row * kMaxBlocksRed + k);
+            b += __ldcg(partials + (size_t)(row + 1) * kMaxBlocksRed + k);
+        }
+        a = warp_sum(a);
+        b = warp_sum(b);
+        if (threadIdx.x == 0) tot2 = make_double2(a, b);
+    }
+    __syncthreads();
+    const double2 r = tot2;
+    __syncthreads();
+    return r;
+}
+
+template <bool MASKED, int PAT, int NT>
+__global__ void __launch_bounds__(NT, 512 / NT) k_pcg_kaa(const Geo2 g, OpKaa<true, MASKED> op, int nvb, long long n,
                                                         double* x, double* r, double* z, double* p0, double* p1,
                                                         double* q, const double* dinv, double* s, double* partials,
                                                         unsigned int* bar) {
@@ -1614,7 +1633,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_pcg_kaa(const Geo2 g, OpKaa<true,
     double rz = s[S_RZ], beta = s[S_BETA], rn = s[S_RNORM], pap = 0.0, gm = 0.0;
     long long it = (long long)s[S_ITER];
     double done = 0.0, fail = 0.0;
-    const long long tid = blockIdx.x * (long long)kBlock + threadIdx.x, nth = (long long)gridDim.x * kBlock;
+    const long long tid = blockIdx.x * (long long)NT + threadIdx.x, nth = (long long)gridDim.x * NT;
     for (;;) {
         double* pin = (it & 1) ? p1 : p0;
         double* pout = (it & 1) ? p0 : p1;
@@ -1626,7 +1645,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_pcg_kaa(const Geo2 g, OpKaa<true,
         op.use_breg = 1;
         op.breg = it > 0 ? beta : 0.0;
         for (int vb = blockIdx.x; vb < nvb; vb += gridDim.x)
-            strip_pass<OpKaa<true, MASKED>, PAT>(g, op, smem, vb * (kBlock / 32) + (threadIdx.x >> 5));
+            strip_pass<OpKaa<true, MASKED>, PAT>(g, op, smem, vb * (NT / 32) + (threadIdx.x >> 5));
         block_partials(&op.acc, 1, partials, 0);
         grid_sync(bar);
         pap = grid_total(partials, 0);
@@ -1645,7 +1664,8 @@ __global__ void __launch_bounds__(kBlock, 2) k_pcg_kaa(const Geo2 g, OpKaa<true,
         }
         block_partials(acc, 2, partials, 1);
         grid_sync(bar);
-        const double rr = grid_total(partials, 1), rzn = grid_total(partials, 2);
+        const double2 t2 = grid_total2(partials, 1);
+        const double rr = t2.x, rzn = t2.y;
         ++it;
         rn = sqrt(rr);
         if (rn <= target) { done = 1.0; break; }
@@ -1901,29 +1921,30 @@ int launch_pcg_kaa1(Ctx* c, const PcgBuffers& B, const double* kappa, const unsi
     }
 }
 
-template <bool MASKED, int PAT>
+template <bool MASKED, int PAT, int NT>
 static int launch_pcg_kaa_pat(Ctx* c, const PcgBuffers& B, const double* kappa, const unsigned char* act,
                               cudaStream_t st) {
     using Op = OpKaa<true, MASKED>;
-    constexpr int smem = strip_smem<Op, PAT>();
+    constexpr int smem = strip_smem<Op, PAT>() * (NT / kBlock);  // strip rings of NT/32 warps
     static int per = -1;
     if (per < 0) {
-        cudaError_t e = cudaFuncSetAttribute(k_pcg_kaa<MASKED, PAT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaError_t e = cudaFuncSetAttribute(k_pcg_kaa<MASKED, PAT, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return check_cuda(c, e, "persistent pcg attribute");
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_pcg_kaa<MASKED, PAT>, kBlock, smem);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_pcg_kaa<MASKED, PAT, NT>, NT, smem);
         if (e != cudaSuccess) return check_cuda(c, e, "persistent pcg occupancy");
     }
     int dev = 0, nsm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     const Geo2& g = c->g;
-    const int nvb = strip_blocks(g);
+    const long long warps = (long long)g.nwj * g.nstrips;
+    const int nvb = (int)((warps + NT / 32 - 1) / (NT / 32));
     const int nb = std::min(nvb, nsm * std::max(per, 1));
     if (per < 1 || nb > kMaxBlocksRed) return PF_EINVAL;  // caller falls back to the graph loop
     Op op{kappa, B.z, B.p0, B.p1, B.q, act, c->scal, redbuf(c), 0.0};
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(nb);
-    cfg.blockDim = dim3(kBlock);
+    cfg.blockDim = dim3(NT);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute at[1];
@@ -1932,24 +1953,31 @@ static int launch_pcg_kaa_pat(Ctx* c, const PcgBuffers& B, const double* kappa, 
     cfg.attrs = at;
     cfg.numAttrs = 1;
     const int ps = prof_begin(c, st);
-    cudaError_t e = cudaLaunchKernelEx(&cfg, k_pcg_kaa<MASKED, PAT>, g, op, nvb, B.n, B.x, B.r, B.z, B.p0, B.p1, B.q,
-                                       (const double*)B.dinv, c->scal, c->partials, c->tickets + 62);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_pcg_kaa<MASKED, PAT, NT>, g, op, nvb, B.n, B.x, B.r, B.z, B.p0, B.p1,
+                                       B.q, (const double*)B.dinv, c->scal, c->partials, c->tickets + 62);
     prof_end(c, st, ps, K_KAA_CG, 0.0);
     c->launches++;
     return check_cuda(c, e, "persistent pcg launch");
+}
+template <bool MASKED, int PAT>
+static int launch_pcg_kaa_nt(Ctx* c, const PcgBuffers& B, const double* kappa, const unsigned char* act,
+                             cudaStream_t st) {
+    static const bool wide = getenv("PF_PCG_NT256") == nullptr;
+    return wide ? launch_pcg_kaa_pat<MASKED, PAT, 512>(c, B, kappa, act, st)
+                : launch_pcg_kaa_pat<MASKED, PAT, 256>(c, B, kappa, act, st);
 }
 int launch_pcg_kaa(Ctx* c, const PcgBuffers& B, const double* kappa, const unsigned char* act, cudaStream_t st) {
     if (c->dim != 2) return PF_EINVAL;
     switch (c->g.pattern) {
         case PF_UNION_JACK:
-            return act ? launch_pcg_kaa_pat<true, PF_UNION_JACK>(c, B, kappa, act, st)
-                       : launch_pcg_kaa_pat<false, PF_UNION_JACK>(c, B, kappa, act, st);
+            return act ? launch_pcg_kaa_nt<true, PF_UNION_JACK>(c, B, kappa, act, st)
+                       : launch_pcg_kaa_nt<false, PF_UNION_JACK>(c, B, kappa, act, st);
         case PF_RIGHT:
-            return act ? launch_pcg_kaa_pat<true, PF_RIGHT>(c, B, kappa, act, st)
-                       : launch_pcg_kaa_pat<false, PF_RIGHT>(c, B, kappa, act, st);
+            return act ? launch_pcg_kaa_nt<true, PF_RIGHT>(c, B, kappa, act, st)
+                       : launch_pcg_kaa_nt<false, PF_RIGHT>(c, B, kappa, act, st);
         default:
-            return act ? launch_pcg_kaa_pat<true, PF_CROSSED>(c, B, kappa, act, st)
-                       : launch_pcg_kaa_pat<false, PF_CROSSED>(c, B, kappa, act, st);
+            return act ? launch_pcg_kaa_nt<true, PF_CROSSED>(c, B, kappa, act, st)
+                       : launch_pcg_kaa_nt<false, PF_CROSSED>(c, B, kappa, act, st);
     }
 }
 
