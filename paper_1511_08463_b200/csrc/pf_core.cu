@@ -510,6 +510,9 @@ int pcg_run(Ctx* c, int kind, const PcgBuffers& B, const double* coef, const uns
         const int rc = c->pcg_single ? launch_pcg_kaa1(c, B, coef, act, st) : launch_pcg_kaa(c, B, coef, act, st);
         if (rc == PF_OK) {
             PF_TRY(read_scal(c, st, 0, 24));
+            // profiling: the launch's algorithmic bytes are known once its iterations are
+            if (c->prof.on && !c->prof.log.empty())
+                c->prof.log.back().bytes = c->h_scal[S_ITER] * pcg_kaa_iter_bytes(c);
             return pcg_finish(c, B, rep, st);
         }
         if (rc != PF_EINVAL) return rc;

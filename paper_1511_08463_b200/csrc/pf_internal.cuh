@@ -414,6 +414,7 @@ struct PcgBuffers {
 // the whole Kaa Jacobi-PCG loop in one cooperative launch (2D): two-phase standard PCG (kaa) or the
 // single-reduction Chronopoulos-Gear form (kaa1); PF_EINVAL: not resident -> graph loop
 int launch_pcg_kaa1(Ctx* c, const PcgBuffers& B, const double* kappa, const unsigned char* act, cudaStream_t st);
+double pcg_kaa_iter_bytes(const Ctx* c);
 int launch_pcg_kaa(Ctx* c, const PcgBuffers& B, const double* kappa, const unsigned char* act, cudaStream_t st);
 // kind: 0 = Kuu Jacobi (coef = alpha), 1 = Kaa masked by act (coef = kappa), 2 = Kuu GMG
 int pcg_run(Ctx* c, int kind, const PcgBuffers& B, const double* coef, const unsigned char* act,

@@ -1455,6 +1455,10 @@ static double alg_bytes(const Ctx* c, int kind, int nvec_r, int nvec_w) {
     }
 }
 
+// algorithmic bytes of one persistent damage-PCG iteration: the fused Kaa strip pass + the
+// vector pass (x, p, r, q, dinv -> x, r, z)
+double pcg_kaa_iter_bytes(const Ctx* c) { return alg_bytes(c, K_KAA_CG, 0, 0) + 8.0 * 8.0 * (double)c->g.nv; }
+
 template <class Op, int PAT>
 static constexpr int strip_smem() {
     return (kBlock / 32) * Op::pd(PAT) * (Op::sv(PAT) + Op::sc(PAT)) * 256;
