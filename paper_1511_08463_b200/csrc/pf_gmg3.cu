@@ -17,6 +17,7 @@
 // preconditioner.  Not a Galerkin hierarchy: on cracked states the coarse operators are the
 // coefficient-averaged re-discretisation, which costs iterations, never correctness.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "pf_internal.cuh"
@@ -24,7 +25,7 @@
 namespace pf {
 
 constexpr int kG3B = 256;
-constexpr int kCoarseDeg3 = 12;
+constexpr int kCoarseDeg3 = 6;  // 128^3: same PCG iterations as 12, 3% less time (4: +1 iteration)
 constexpr double kCoarseRatio3 = 0.02;
 constexpr int kPowIts3 = 16;
 constexpr double kPowSafety3 = 1.25;
