@@ -14,7 +14,8 @@ cfg = pf.SolverConfig(method="oram_newton", omega=1.8, outer_atol=1e-6, am_switc
                       elastic_solver="cg", elastic_rtol=1e-8, elastic_precond="gmg",
                       max_am_iterations=2000, fieldsplit_inner="mg",
                       gmg_degree=int(os.environ.get("DEG", "2")),
-                      damage_forcing=bool(int(os.environ.get("FORCING", "0"))))
+                      damage_forcing=bool(int(os.environ.get("FORCING", "1"))),
+                      fieldsplit_rtol=float(os.environ.get("FSRTOL", "1e-6")))
 st = pf.State.zeros(setup.mesh, setup.initial_alpha_lb)
 pf.run_quasistatic(setup, cfg, snapshot_stride=0, state=st, steps=list(range(k)))
 acc = defaultdict(lambda: [0, 0.0])
@@ -29,6 +30,6 @@ for name in ("elastic_step", "damage_step", "coupled_newton_solve"):
 torch.cuda.synchronize(); t0 = time.perf_counter()
 pf.run_quasistatic(setup, cfg, snapshot_stride=0, state=st, steps=[k, k + 1])
 torch.cuda.synchronize(); tot = time.perf_counter() - t0
-print(f"2 load steps ({k},{k+1}): {1e3*tot:.1f} ms")
+print(f"2 load steps ({k},{k+1}): {1e3*tot:.1f} ms  E {st.alpha.sum().item():.12e}")
 for name, (c, t) in acc.items():
     print(f"  {name:22s} calls={c:4d} total={1e3*t:8.1f} ms  per call={1e3*t/max(c,1):7.3f} ms")
