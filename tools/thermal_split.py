@@ -10,7 +10,7 @@ import bench
 
 k0 = int(sys.argv[1]) if len(sys.argv) > 1 else 16
 setup, cfg = pf.setup_thermal_slab(nx=2048, ny=512), bench.thermal_config(pf)
-cfg.damage_forcing = bool(int(os.environ.get("FORCING", "0")))
+cfg.damage_forcing = bool(int(os.environ.get("FORCING", "1")))
 st = pf.State.zeros(setup.mesh, setup.initial_alpha_lb)
 pf.run_quasistatic(setup, cfg, snapshot_stride=0, state=st, steps=list(range(k0)))
 acc = defaultdict(lambda: [0, 0.0])
