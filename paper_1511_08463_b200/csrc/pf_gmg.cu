@@ -432,7 +432,8 @@ __global__ void k_coarse_inv_band(const double* Lband, int n, int bw, int wpb, d
 }
 
 // V-cycle vectors are streamed through L2 (ld.global.cg); operators/Dinv via the read-only path.
-// SH = true: the same functions on shared-memory copies (the single-CTA coarse tail), plain loads.
+// SH = true: the same functions on generic/shared-memory operands (plain loads); no current kernel
+// instantiates it (the shared-memory tail was replaced by the grid-wide dense coarsest solve).
 template <bool SH = false>
 __device__ __forceinline__ double2 ldv(const double* p, long long v) {
     if constexpr (SH) return reinterpret_cast<const double2*>(p)[v];
