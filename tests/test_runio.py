@@ -170,3 +170,15 @@ def test_omega_sweep_summary(tmp_path):
         assert abs(int(r["total_am_iters"]) - int(o["total_am_iters"])) <= max(3, 0.15 * int(o["total_am_iters"]))
     assert float(rows[0]["reduction"]) == 0.0
     assert (tmp_path / "omega_1.5" / "energies.csv").exists()
+
+
+@pytest.mark.gpu
+def test_sweep_rows_in_spawned_gpu_workers(tmp_path):
+    """--threads 2: rows run in spawned worker processes pinned to GPUs (replicas)."""
+    assert runio.main(["sweep", os.path.join(CLI, "omega_sweep.ini"), "--threads", "2",
+                       "--output-dir", str(tmp_path)]) == 0
+    head, rows = csv_rows(tmp_path / "summary.csv")
+    assert [r["status"] for r in rows] == ["ok", "ok"]
+    _, ref = csv_rows(os.path.join(CLI, "ref_omega_sweep_summary.csv"))
+    for r, o in zip(rows, ref):
+        assert abs(int(r["total_am_iters"]) - int(o["total_am_iters"])) <= max(3, 0.15 * int(o["total_am_iters"]))
