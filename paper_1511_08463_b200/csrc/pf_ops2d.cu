@@ -321,6 +321,50 @@ struct OpKuu {
                          const double (&rc)[NV], const double (&rn)[NV], const double (&ec)[NE],
                          double (&c00)[NC], double (&c10)[NC], double (&c01)[NC], double (&c11)[NC],
                          bool own) {
+        if constexpr (PAT == PF_UNION_JACK) {
+            // Edge form: every union-jack triangle is a right triangle with one cell edge along x
+            // and one along y, so both diagonal orientations use the same four edge differences;
+            // the parity only decides which vertical edge pairs with which triangle (4 selects on
+            // the inputs, 4 on the outputs, instead of mirroring 15 inputs and 10 outputs).
+            const bool odd = ((ci + j) & 1) != 0;
+            const double ihx = g.ihx, ihy = ihy_at(g, j);
+            const double sc = area_at(g, j) * ec[0];
+            // corners: 00 = vc (ci, j), 10 = vn (ci+1, j), 01 = rc (ci, j+1), 11 = rn (ci+1, j+1)
+            const double bx1 = vn[0] - vc[0], bx2 = vn[1] - vc[1];  // bottom edge (x)
+            const double tx1 = rn[0] - rc[0], tx2 = rn[1] - rc[1];  // top edge (x)
+            const double ly1 = rc[0] - vc[0], ly2 = rc[1] - vc[1];  // left edge (y)
+            const double ry1 = rn[0] - vn[0], ry2 = rn[1] - vn[1];  // right edge (y)
+            // triangle on the bottom edge: even (00,10,11) -> right edge ; odd (00,10,01) -> left
+            // triangle on the top edge:    even (00,11,01) -> left edge  ; odd (10,11,01) -> right
+            const double by1 = odd ? ly1 : ry1, by2 = odd ? ly2 : ry2;
+            const double ty1 = odd ? ry1 : ly1, ty2 = odd ? ry2 : ly2;
+            const double ab = (vc[2] + vn[2] + (odd ? rc[2] : rn[2])) * (1.0 / 3.0);
+            const double at = ((odd ? vn[2] : vc[2]) + rn[2] + rc[2]) * (1.0 / 3.0);
+            double fbx1, fbx2, fby1, fby2, ftx1, ftx2, fty1, fty2;  // edge fluxes (x / y), 2 comps
+            {
+                const double om = 1.0 - ab;
+                const double k = (om * om + g.kell) * sc;
+                double s0, s1, s2;
+                unit_stress(g, bx1 * ihx, by2 * ihy, by1 * ihy + bx2 * ihx, s0, s1, s2);
+                fbx1 = k * ihx * s0; fbx2 = k * ihx * s2;
+                fby1 = k * ihy * s2; fby2 = k * ihy * s1;
+            }
+            {
+                const double om = 1.0 - at;
+                const double k = (om * om + g.kell) * sc;
+                double s0, s1, s2;
+                unit_stress(g, tx1 * ihx, ty2 * ihy, ty1 * ihy + tx2 * ihx, s0, s1, s2);
+                ftx1 = k * ihx * s0; ftx2 = k * ihx * s2;
+                fty1 = k * ihy * s2; fty2 = k * ihy * s1;
+            }
+            const double fr1 = odd ? fty1 : fby1, fr2 = odd ? fty2 : fby2;  // right edge
+            const double fl1 = odd ? fby1 : fty1, fl2 = odd ? fby2 : fty2;  // left edge
+            c00[0] = -fbx1 - fl1; c00[1] = -fbx2 - fl2;
+            c10[0] = fbx1 - fr1;  c10[1] = fbx2 - fr2;
+            c01[0] = -ftx1 + fl1; c01[1] = -ftx2 + fl2;
+            c11[0] = ftx1 + fr1;  c11[1] = ftx2 + fr2;
+            return;
+        }
         double U1[5] = {vc[0], vn[0], rc[0], rn[0], 0.0};
         double U2[5] = {vc[1], vn[1], rc[1], rn[1], 0.0};
         double Al[5] = {vc[2], vn[2], rc[2], rn[2], 0.0};
