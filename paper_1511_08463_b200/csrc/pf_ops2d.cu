@@ -694,6 +694,25 @@ struct OpKaa {
                          const double (&rc)[NV], const double (&rn)[NV], const double (&ec)[NE],
                          double (&c00)[NC], double (&c10)[NC], double (&c01)[NC], double (&c11)[NC],
                          bool own) {
+        if constexpr (PAT == PF_UNION_JACK) {
+            // edge form (see OpKuu::cell): slot 0 is the triangle on the bottom cell edge, slot 1
+            // the one on the top edge, in both diagonal orientations
+            const bool odd = ((ci + j) & 1) != 0;
+            const double ihx = g.ihx, ihy = ihy_at(g, j);
+            const double del = 2.0 * (ec[0] / g.cw) * g.ell * area_at(g, j);
+            const double x00 = vc[0], x10 = vn[0], x01 = rc[0], x11 = rn[0];
+            const double bx = x10 - x00, tx = x11 - x01, ly = x01 - x00, ry = x11 - x10;
+            const double bb = ec[1] * ((x00 + x10) + (odd ? x01 : x11));  // reaction, bottom triangle
+            const double bt = ec[2] * (((odd ? x10 : x00) + x11) + x01);   // reaction, top triangle
+            const double fbx = del * bx * ihx * ihx, ftx = del * tx * ihx * ihx;
+            const double fby = del * (odd ? ly : ry) * ihy * ihy, fty = del * (odd ? ry : ly) * ihy * ihy;
+            const double fr = odd ? fty : fby, fl = odd ? fby : fty;
+            c00[0] = bb + (odd ? 0.0 : bt) - fbx - fl;
+            c10[0] = bb + (odd ? bt : 0.0) + fbx - fr;
+            c01[0] = bt + (odd ? bb : 0.0) - ftx + fl;
+            c11[0] = bt + (odd ? 0.0 : bb) + ftx + fr;
+            return;
+        }
         double X[5] = {vc[0], vn[0], rc[0], rn[0], 0.0};
         if constexpr (PAT == PF_CROSSED) X[4] = ec[6] != 0.0 ? 0.0 : ec[5];
         double Y[5] = {0, 0, 0, 0, 0};
