@@ -321,12 +321,12 @@ struct OpKuu {
                          const double (&rc)[NV], const double (&rn)[NV], const double (&ec)[NE],
                          double (&c00)[NC], double (&c10)[NC], double (&c01)[NC], double (&c11)[NC],
                          bool own) {
-        if constexpr (PAT == PF_UNION_JACK) {
+        if constexpr (PAT == PF_UNION_JACK || PAT == PF_RIGHT) {
             // Edge form: every union-jack triangle is a right triangle with one cell edge along x
             // and one along y, so both diagonal orientations use the same four edge differences;
             // the parity only decides which vertical edge pairs with which triangle (4 selects on
             // the inputs, 4 on the outputs, instead of mirroring 15 inputs and 10 outputs).
-            const bool odd = ((ci + j) & 1) != 0;
+            const bool odd = PAT == PF_UNION_JACK && ((ci + j) & 1) != 0;  // right: always the even split
             const double ihx = g.ihx, ihy = ihy_at(g, j);
             const double sc = area_at(g, j) * ec[0];
             // corners: 00 = vc (ci, j), 10 = vn (ci+1, j), 01 = rc (ci, j+1), 11 = rn (ci+1, j+1)
@@ -694,10 +694,10 @@ struct OpKaa {
                          const double (&rc)[NV], const double (&rn)[NV], const double (&ec)[NE],
                          double (&c00)[NC], double (&c10)[NC], double (&c01)[NC], double (&c11)[NC],
                          bool own) {
-        if constexpr (PAT == PF_UNION_JACK) {
+        if constexpr (PAT == PF_UNION_JACK || PAT == PF_RIGHT) {
             // edge form (see OpKuu::cell): slot 0 is the triangle on the bottom cell edge, slot 1
             // the one on the top edge, in both diagonal orientations
-            const bool odd = ((ci + j) & 1) != 0;
+            const bool odd = PAT == PF_UNION_JACK && ((ci + j) & 1) != 0;  // right: always the even split
             const double ihx = g.ihx, ihy = ihy_at(g, j);
             const double del = 2.0 * (ec[0] / g.cw) * g.ell * area_at(g, j);
             const double x00 = vc[0], x10 = vn[0], x01 = rc[0], x11 = rn[0];
