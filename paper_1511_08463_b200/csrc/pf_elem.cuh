@@ -42,9 +42,12 @@ __device__ __forceinline__ void st2(double* p, long long v, double a, double b) 
 
 // per-cell-row geometry: graded meshes (banded_rect_mesh, mesh.py:163-190) carry 1/hy and the
 // element area per cell row J; uniform meshes use the descriptor constants (a uniform branch)
-__device__ __forceinline__ double ihy_at(const Geo2& g, int cj) { return g.rowgeo ? __ldg(g.rowgeo + cj) : g.ihy; }
+// Plain (non-volatile) loads on purpose: __ldg is volatile inline asm, so every call site issued
+// its own predicated load even on uniform meshes (rowgeo == null; ncu: 13 LDG + 30 LEA per vertex
+// in the crossed Kuu apply); plain loads let the compiler hoist and share them per cell.
+__device__ __forceinline__ double ihy_at(const Geo2& g, int cj) { return g.rowgeo ? g.rowgeo[cj] : g.ihy; }
 __device__ __forceinline__ double area_at(const Geo2& g, int cj) {
-    return g.rowgeo ? __ldg(g.rowgeo + g.ny + cj) : g.area[0];
+    return g.rowgeo ? g.rowgeo[g.ny + cj] : g.area[0];
 }
 
 // ---- element kernels ---------------------------------------------------------------------
