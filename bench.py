@@ -55,6 +55,7 @@ class ClockSampler:
         self.dev = dev_index
         self.proc = None
         self.lines = []
+        self.first = threading.Event()
 
     def start(self):
         try:
@@ -64,12 +65,16 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi's start-up (NVML init) stays outside the timed region
+            self.first.wait(10.0)
         except Exception:  # noqa: BLE001
             self.proc = None
 
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
+            self.first.set()
+        self.first.set()
 
     def stop(self):
         if self.proc is None:

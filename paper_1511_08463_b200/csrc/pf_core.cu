@@ -454,7 +454,7 @@ int pcg_run(Ctx* c, int kind, const PcgBuffers& B, const double* coef, const uns
     // No host poll here: the persistent and graph loops below check the done/fail flags on the
     // device (the start-up may already have converged); only the eager loop needs them now.
     const bool graphs = c->use_graphs && !c->prof.on;
-    const bool persistent = kind == 1 && c->dim == 2 && c->pcg_persistent;
+    const bool persistent = kind == 1 && c->pcg_persistent;
     if (!graphs && !persistent) PF_TRY(read_scal(c, st, 0, 24));
     // one Krylov iteration k (ping-pong search-direction buffers by parity)
     auto issue_iter = [&](long long k, cudaStream_t s) -> int {
@@ -839,14 +839,16 @@ static void geometry_3d(Ctx* c) {
     tile3(g);
 }
 
-// 3D strip tiling: blocks of 14 j-pencils x 30 k-lanes, strips of S vertex rows sized for ~4
-// blocks per SM across the 148 SMs
-void pf::tile3(Geo3& g) {
-    g.nbj = (g.nvy + 13) / 14;
+// 3D strip tiling: blocks of outj (6) j-pencils x 30 k-lanes, strips of S vertex rows sized for
+// ~4 blocks per SM across the 148 SMs
+void pf::tile3(Geo3& g, int outj) {
+    g.nbj = (g.nvy + outj - 1) / outj;
     g.nbk = (g.nvz + 29) / 30;
     const long long per = (long long)g.nbj * g.nbk;
     long long S = ((g.nx + 1) * per + 148LL * 4 - 1) / (148LL * 4);
     S = std::max(4LL, std::min(64LL, S));
+    // large grids: longer strips keep the block count within the reduction buffer
+    while (per * ((g.nx + 1 + S - 1) / S) > kMaxBlocksRed && S < g.nx + 1) S *= 2;
     g.S = (int)S;
     g.nstrips = (int)((g.nx + 1 + S - 1) / S);
 }

@@ -375,14 +375,34 @@ int gmg3_setup(Ctx* c, cudaStream_t st) {
     return check_cuda(c, cudaGetLastError(), "3D multigrid setup");
 }
 
+// fused smoother steps (launch3_Kuu_sm); PF_GMG3_UNFUSED=1 keeps one vector pass per step
+static bool fused3(int deg) {
+    static const bool off = getenv("PF_GMG3_UNFUSED") != nullptr;
+    return deg >= 2 && !off;
+}
+static Sm3Args sm_args(G3Level& L, int l, const double* xin, const double* b, double* res, double* dnext, double* xs,
+                       int k, int pending, double ratio, const double* live, Ctx* c) {
+    return Sm3Args{L.alpha, xin, b, L.dinv, res, dnext, xs, live, c->scal + S_GMG0 + l, ratio, k, pending};
+}
+
 // Chebyshev-Jacobi of degree deg on level l from x = 0 (pre-smoother / coarsest solve)
 static int smooth_from_zero(Ctx* c, int l, const double* b, double* x, int deg, double ratio, cudaStream_t st,
                             const double* live) {
     G3Level& L = c->g3lev[l];
     const long long n = 3 * L.g.nv;
     const double* lam = c->scal + S_GMG0 + l;
-    G3K(c, 40.0 * n, (k3_cheb0<<<gb3(n), kG3B, 0, st>>>(n, L.dinv, b, L.res, L.d0, x, 0, lam, ratio, live)));
     double *d = L.d0, *dn = L.d1;
+    if (fused3(deg)) {
+        // step 1 forms d0 = D b / theta inside the apply; x = d0 + dn
+        PF_TRY_GMG(launch3_Kuu_sm(c, L.g, E3_CHEB_B, sm_args(L, l, nullptr, b, L.res, dn, x, 1, 0, ratio, live, c), st, K_GMG));
+        std::swap(d, dn);
+        for (int k = 2; k < deg; ++k) {
+            PF_TRY_GMG(launch3_Kuu_sm(c, L.g, E3_CHEB, sm_args(L, l, d, b, L.res, dn, x, k, 0, ratio, live, c), st, K_GMG));
+            std::swap(d, dn);
+        }
+        return PF_OK;
+    }
+    G3K(c, 40.0 * n, (k3_cheb0<<<gb3(n), kG3B, 0, st>>>(n, L.dinv, b, L.res, L.d0, x, 0, lam, ratio, live)));
     for (int k = 1; k < deg; ++k) {
         PF_TRY_GMG(launch3_Kuu_on(c, L.g, L.alpha, d, L.w, PF_BC_ELIMINATE, st, K_GMG));
         G3K(c, 64.0 * n, (k3_cheb_step<<<gb3(n), kG3B, 0, st>>>(n, L.w, d, dn, L.res, x, L.dinv, k, lam, ratio, live)));
@@ -396,14 +416,19 @@ int gmg3_vcycle(Ctx* c, const double* r_in, double* z_out, cudaStream_t st, cons
     const int nl = (int)Ls.size();
     const int deg = std::max(1, c->gmg_degree);
     const double ratio = c->gmg_ratio;
+    const bool fz = fused3(deg);
     for (int l = 0; l < nl - 1; ++l) {
         G3Level& L = Ls[l];
         const long long n = 3 * L.g.nv;
         const double* b = l == 0 ? r_in : L.b;
         double* x = l == 0 ? z_out : L.x;
         PF_TRY_GMG(smooth_from_zero(c, l, b, x, deg, ratio, st, live));
-        PF_TRY_GMG(launch3_Kuu_on(c, L.g, L.alpha, x, L.w, PF_BC_ELIMINATE, st, K_GMG));
-        G3K(c, 24.0 * n, (k3_resid<<<gb3(n), kG3B, 0, st>>>(n, L.w, b, L.r, live)));
+        if (fz) {
+            PF_TRY_GMG(launch3_Kuu_sm(c, L.g, E3_RESID, sm_args(L, l, x, b, L.r, nullptr, nullptr, 0, 0, ratio, live, c), st, K_GMG));
+        } else {
+            PF_TRY_GMG(launch3_Kuu_on(c, L.g, L.alpha, x, L.w, PF_BC_ELIMINATE, st, K_GMG));
+            G3K(c, 24.0 * n, (k3_resid<<<gb3(n), kG3B, 0, st>>>(n, L.w, b, L.r, live)));
+        }
         G3Level& C = Ls[l + 1];
         G3K(c, 24.0 * n + 24.0 * 3 * C.g.nv, (k3_restrict<<<gb3(C.g.nv), kG3B, 0, st>>>(L.g, C.g, L.mask, C.mask, L.r, C.b, live)));
     }
@@ -420,9 +445,18 @@ int gmg3_vcycle(Ctx* c, const double* r_in, double* z_out, cudaStream_t st, cons
         double* x = l == 0 ? z_out : L.x;
         const double* lam = c->scal + S_GMG0 + l;
         G3K(c, 48.0 * n + 24.0 * C.g.nv, (k3_prolong<<<gb3(L.g.nv), kG3B, 0, st>>>(L.g, C.g, L.mask, C.mask, C.x, x, live)));
+        double *d = L.d0, *dn = L.d1;
+        if (fz) {
+            // x += d0 is deferred into the first Chebyshev step (the apply reads x)
+            PF_TRY_GMG(launch3_Kuu_sm(c, L.g, E3_RESID_CHEB0, sm_args(L, l, x, b, L.res, d, nullptr, 0, 0, ratio, live, c), st, K_GMG));
+            for (int k = 1; k < deg; ++k) {
+                PF_TRY_GMG(launch3_Kuu_sm(c, L.g, E3_CHEB, sm_args(L, l, d, b, L.res, dn, x, k, k == 1, ratio, live, c), st, K_GMG));
+                std::swap(d, dn);
+            }
+            continue;
+        }
         PF_TRY_GMG(launch3_Kuu_on(c, L.g, L.alpha, x, L.w, PF_BC_ELIMINATE, st, K_GMG));
         G3K(c, 64.0 * n, (k3_resid_cheb0<<<gb3(n), kG3B, 0, st>>>(n, L.w, b, L.dinv, L.res, L.d0, x, lam, ratio, live)));
-        double *d = L.d0, *dn = L.d1;
         for (int k = 1; k < deg; ++k) {
             PF_TRY_GMG(launch3_Kuu_on(c, L.g, L.alpha, d, L.w, PF_BC_ELIMINATE, st, K_GMG));
             G3K(c, 64.0 * n, (k3_cheb_step<<<gb3(n), kG3B, 0, st>>>(n, L.w, d, dn, L.res, x, L.dinv, k, lam, ratio, live)));

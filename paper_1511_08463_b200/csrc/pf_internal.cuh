@@ -352,9 +352,25 @@ struct CgScal {  // pointers into the scalar block used by fused CG kernels
 // y = K p_out and pAp reduced into scal (CG step A).
 int launch_Kuu(Ctx* c, const double* alpha, const double* x, double* y, int bcmode,
                cudaStream_t st);
-void tile3(Geo3& g);
+void tile3(Geo3& g, int outj = 6);  // outj = output pencils per block (warps - 2)
 int launch3_Kuu_on(Ctx* c, const Geo3& g, const double* alpha, const double* x, double* y, int bcmode,
                    cudaStream_t st, int kind);
+// Kuu apply with a fused multigrid-smoother epilogue (pf_ops3d.cu, Op3KuuSm)
+enum { E3_CHEB = 1, E3_CHEB_B = 2, E3_RESID = 3, E3_RESID_CHEB0 = 4 };
+struct Sm3Args {
+    const double* alpha;
+    const double* xin;
+    const double* b;
+    const double* dinv;
+    double* res;
+    double* dnext;
+    double* xs;
+    const double* live;
+    const double* lam;
+    double ratio;
+    int k, pending;
+};
+int launch3_Kuu_sm(Ctx* c, const Geo3& g, int epi, const Sm3Args& a, cudaStream_t st, int kind);
 int launch3_Kuu_diag_on(Ctx* c, const Geo3& g, const double* alpha, double* dinv, cudaStream_t st, int kind);
 int launch_physics_relax(Ctx* c, const double* u, const double* a_prev, const double* a_star, const double* lb,
                          double omega, double* a_out, cudaStream_t st);
@@ -407,6 +423,56 @@ int launch3_jac(Ctx* c, const double* u, const double* alpha, const double* xu, 
                 double* ya, const unsigned char* act, int mode, int bcmode, cudaStream_t st);
 
 // ---- vector kernels + solvers (pf_core.cu) ---------------------------------------------
+// ---- persistent-kernel reductions (fixed order: every CTA computes identical totals) -----------
+__device__ __forceinline__ void block_partials(const double* v, int nv, double* partials, int row0) {
+    __shared__ double sm[4][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int k = 0; k < nv; ++k) {
+        const double t = warp_sum(v[k]);
+        if (lane == 0) sm[k][warp] = t;
+    }
+    __syncthreads();
+    if (warp == 0)
+        for (int k = 0; k < nv; ++k) {
+            double t = lane < nw ? sm[k][lane] : 0.0;
+            t = warp_sum(t);
+            if (lane == 0) partials[(size_t)(row0 + k) * kMaxBlocksRed + blockIdx.x] = t;
+        }
+}
+// after a grid barrier: the grid total of partial row `row` (fixed order; identical in every CTA)
+__device__ __forceinline__ double grid_total(const double* partials, int row) {
+    __shared__ double tot;
+    if (threadIdx.x < 32) {
+        double t = 0.0;
+        for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) t += __ldcg(partials + (size_t)row * kMaxBlocksRed + b);
+        t = warp_sum(t);
+        if (threadIdx.x == 0) tot = t;
+    }
+    __syncthreads();
+    const double r = tot;
+    __syncthreads();
+    return r;
+}
+
+// the totals of partial rows `row` and `row + 1` in one pass
+__device__ __forceinline__ double2 grid_total2(const double* partials, int row) {
+    __shared__ double2 tot2;
+    if (threadIdx.x < 32) {
+        double a = 0.0, b = 0.0;
+        for (int k = threadIdx.x; k < (int)gridDim.x; k += 32) {
+            a += __ldcg(partials + (size_t)row * kMaxBlocksRed + k);
+            b += __ldcg(partials + (size_t)(row + 1) * kMaxBlocksRed + k);
+        }
+        a = warp_sum(a);
+        b = warp_sum(b);
+        if (threadIdx.x == 0) tot2 = make_double2(a, b);
+    }
+    __syncthreads();
+    const double2 r = tot2;
+    __syncthreads();
+    return r;
+}
+
 struct PcgBuffers {
     double *x, *r, *z, *p0, *p1, *q, *dinv, *b;
     long long n;
@@ -416,6 +482,7 @@ struct PcgBuffers {
 int launch_pcg_kaa1(Ctx* c, const PcgBuffers& B, const double* kappa, const unsigned char* act, cudaStream_t st);
 double pcg_kaa_iter_bytes(const Ctx* c);
 int launch_pcg_kaa(Ctx* c, const PcgBuffers& B, const double* kappa, const unsigned char* act, cudaStream_t st);
+int launch3_pcg_kaa(Ctx* c, const PcgBuffers& B, const double* kappa, const unsigned char* act, cudaStream_t st);
 // kind: 0 = Kuu Jacobi (coef = alpha), 1 = Kaa masked by act (coef = kappa), 2 = Kuu GMG
 int pcg_run(Ctx* c, int kind, const PcgBuffers& B, const double* coef, const unsigned char* act,
             double rtol, double atol, long long maxit, int zero_x0, int check_every,

@@ -1520,7 +1520,10 @@ static double alg_bytes(const Ctx* c, int kind, int nvec_r, int nvec_w) {
 
 // algorithmic bytes of one persistent damage-PCG iteration: the fused Kaa strip pass + the
 // vector pass (x, p, r, q, dinv -> x, r, z)
-double pcg_kaa_iter_bytes(const Ctx* c) { return alg_bytes(c, K_KAA_CG, 0, 0) + 8.0 * 8.0 * (double)c->g.nv; }
+double pcg_kaa_iter_bytes(const Ctx* c) {
+    if (c->dim == 3) return 33.0 * c->g3.nv + 8.0 * c->n_el + 8.0 * 8.0 * (double)c->g3.nv;
+    return alg_bytes(c, K_KAA_CG, 0, 0) + 8.0 * 8.0 * (double)c->g.nv;
+}
 
 template <class Op, int PAT>
 static constexpr int strip_smem() {
@@ -1640,55 +1643,6 @@ int launch_Kaa_cgA(Ctx* c, const double* kappa, const double* z, const double* p
 // the same scalar decisions and the result is deterministic.  The strips are "virtual blocks"
 // distributed over the resident CTAs.  Replaces 2 dependent launches per iteration (each
 // latency-bound on a 4-17 MB problem) and the per-pair graph overhead.
-__device__ __forceinline__ void block_partials(const double* v, int nv, double* partials, int row0) {
-    __shared__ double sm[4][32];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (int k = 0; k < nv; ++k) {
-        const double t = warp_sum(v[k]);
-        if (lane == 0) sm[k][warp] = t;
-    }
-    __syncthreads();
-    if (warp == 0)
-        for (int k = 0; k < nv; ++k) {
-            double t = lane < nw ? sm[k][lane] : 0.0;
-            t = warp_sum(t);
-            if (lane == 0) partials[(size_t)(row0 + k) * kMaxBlocksRed + blockIdx.x] = t;
-        }
-}
-// after a grid barrier: the grid total of partial row `row` (fixed order; identical in every CTA)
-__device__ __forceinline__ double grid_total(const double* partials, int row) {
-    __shared__ double tot;
-    if (threadIdx.x < 32) {
-        double t = 0.0;
-        for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) t += __ldcg(partials + (size_t)row * kMaxBlocksRed + b);
-        t = warp_sum(t);
-        if (threadIdx.x == 0) tot = t;
-    }
-    __syncthreads();
-    const double r = tot;
-    __syncthreads();
-    return r;
-}
-
-// the totals of partial rows `row` and `row + 1` in one pass
-__device__ __forceinline__ double2 grid_total2(const double* partials, int row) {
-    __shared__ double2 tot2;
-    if (threadIdx.x < 32) {
-        double a = 0.0, b = 0.0;
-        for (int k = threadIdx.x; k < (int)gridDim.x; k += 32) {
-            a += __ldcg(partials + (size_t)row * kMaxBlocksRed + k);
-            b += __ldcg(partials + (size_t)(row + 1) * kMaxBlocksRed + k);
-        }
-        a = warp_sum(a);
-        b = warp_sum(b);
-        if (threadIdx.x == 0) tot2 = make_double2(a, b);
-    }
-    __syncthreads();
-    const double2 r = tot2;
-    __syncthreads();
-    return r;
-}
-
 template <bool MASKED, int PAT, int NT>
 __global__ void __launch_bounds__(NT, 512 / NT) k_pcg_kaa(const Geo2 g, OpKaa<true, MASKED> op, int nvb, long long n,
                                                         double* x, double* r, double* z, double* p0, double* p1,
@@ -2034,7 +1988,7 @@ static int launch_pcg_kaa_nt(Ctx* c, const PcgBuffers& B, const double* kappa, c
                 : launch_pcg_kaa_pat<MASKED, PAT, 256>(c, B, kappa, act, st);
 }
 int launch_pcg_kaa(Ctx* c, const PcgBuffers& B, const double* kappa, const unsigned char* act, cudaStream_t st) {
-    if (c->dim != 2) return PF_EINVAL;
+    if (c->dim == 3) return launch3_pcg_kaa(c, B, kappa, act, st);
     switch (c->g.pattern) {
         case PF_UNION_JACK:
             return act ? launch_pcg_kaa_nt<true, PF_UNION_JACK>(c, B, kappa, act, st)

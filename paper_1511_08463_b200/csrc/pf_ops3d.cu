@@ -16,13 +16,27 @@
 //     (barrier B), to i+1 are carried in registers.
 // Every input is read once from HBM, every output written once, no atomics (deterministic).
 // Reference formulas: fem.py:149-276 (dim-generic restatement in oracle/p1.py).
+#include <type_traits>
+
 #include "pf_internal.cuh"
 
 namespace pf {
 
-constexpr int kW3 = 16;       // warps per block
-constexpr int kOutJ3 = kW3 - 2;  // output pencils per block
-constexpr int kBlock3 = kW3 * 32;
+// Block tiling: by default 8-warp blocks, two resident per SM (128 registers).  The two blocks'
+// barriers are independent, so one block's fp64 phase overlaps the other's shuffle/barrier phase:
+// against one 16-warp block per SM, Kuu 128^3 0.143 -> 0.133 ms, 256^3 0.91 -> 0.82 ms; Kaa
+// 128^3 0.076 -> 0.066 ms.  Register-heavy ops (Op::MINB = 1) get one 8-warp block and 255
+// registers instead of spilling.  PF_K3W=16 / 8 switches the Kuu / Kaa applies for A/B runs.
+constexpr int kW3 = 8;
+
+template <class Op, class = void> struct WarpsOf { static constexpr int v = kW3; };
+template <class Op> struct WarpsOf<Op, std::void_t<decltype(Op::W3)>> { static constexpr int v = Op::W3; };
+template <class Op, class = void> struct MinBlocksOf { static constexpr int v = 2; };
+template <class Op> struct MinBlocksOf<Op, std::void_t<decltype(Op::MINB)>> { static constexpr int v = Op::MINB; };
+// an operator re-tiled: W warps per block, MB resident blocks per SM
+template <class Base, int W, int MB> struct Tiled3 : Base {
+    static constexpr int W3 = W, MINB = MB;
+};
 
 template <int N> struct IC3 { static constexpr int v = N; };
 
@@ -221,17 +235,18 @@ __device__ __forceinline__ unsigned bc3(const Geo3& g, int i, int j, int k, long
 }
 
 // ---- the 3D strip engine ----------------------------------------------------------------------
-template <class Op>
-__global__ void __launch_bounds__(kBlock3, 1) k_strip3d(const Geo3 g, Op op) {
+// one tile (j-block bj, k-block bk, strip bs) of the engine; `tile` plays the role of the block index
+// (k_strip3d: one tile per CTA; the persistent damage PCG: tiles distributed over resident CTAs)
+template <class Op, int kW3>
+__device__ __forceinline__ void strip3_tile(const Geo3& g, Op& op, unsigned char* smem, int tile) {
+    constexpr int kOutJ3 = kW3 - 2;  // output pencils per block
     constexpr int NV = Op::NV, NC = Op::NC, PD = Op::PD, NE = Op::NE, SV = Op::SV, SC = Op::SC;
     constexpr int STAGE = (SV + SC) * 256;
-    extern __shared__ __align__(16) unsigned char smem[];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double* vx = reinterpret_cast<double*>(smem + kW3 * PD * STAGE);   // [kW3][NV][32]
     double* cx = vx + kW3 * NV * 32;                                     // [kW3][2][NC][32]
-    if (!op.enter()) return;
-    const int bk = blockIdx.x % g.nbk;
-    const int rest = blockIdx.x / g.nbk;
+    const int bk = tile % g.nbk;
+    const int rest = tile / g.nbk;
     const int bj = rest % g.nbj;
     const int bs = rest / g.nbj;
     const int j = bj * kOutJ3 - 1 + w, k = bk * 30 - 1 + lane;
@@ -338,7 +353,19 @@ __global__ void __launch_bounds__(kBlock3, 1) k_strip3d(const Geo3 g, Op op) {
         }
     }
     cp_wait3<0>();
+}
+
+template <class Op, int kW3, int kMinB>
+__global__ void __launch_bounds__(kW3 * 32, kMinB) k_strip3d(const Geo3 g, Op op) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    if (!op.enter()) return;
+    strip3_tile<Op, kW3>(g, op, smem, blockIdx.x);
     op.finish();
+}
+
+template <class Op, int kW3>
+static constexpr int strip3_smem() {
+    return kW3 * Op::PD * (Op::SV + Op::SC) * 256 + kW3 * Op::NV * 32 * 8 + kW3 * 2 * Op::NC * 32 * 8;
 }
 
 struct NoRed3 {
@@ -416,6 +443,84 @@ struct Op3Kuu {
             if (!(tot[0] > 0.0)) s[S_FAIL] = 1.0;
             else s[S_GAMMA] = s[S_RZ] / tot[0];
         });
+    }
+};
+
+// Kuu with a multigrid-smoother epilogue: pf_gmg3.cu's pointwise Chebyshev / residual steps run
+// in the apply's output stage instead of as separate vector passes.  The 3D apply is fp64- and
+// latency-bound (~0.15 of HBM), so the epilogue's vector bytes ride along almost for free; the
+// V-cycle saves the w = K d round trip and one launch per step.  w below is the apply's output
+// (identity rows for eliminated dofs), p its input at the vertex.
+//   E3_CHEB        r = res - D w ; dn = a p + b r ; res = r ; dnext = dn ; x += [p +] dn
+//   E3_CHEB_B      first step from x = 0: the input p = (D b)/theta is formed on the fly (the
+//                  separate k3_cheb0 pass disappears) ; r = D b - D w ; x = p + dn
+//   E3_RESID       res = b - w
+//   E3_RESID_CHEB0 r = D (b - w) ; res = r ; dnext = r/theta (x += dnext is deferred to the next
+//                  E3_CHEB step, "pending": the input x cannot be written while it is read)
+template <int EPI, bool ISO>
+struct Op3KuuSm : Op3Kuu<false, ISO> {
+    using Base = Op3Kuu<false, ISO>;
+    static constexpr int SV = EPI == E3_CHEB_B ? 7 : 4;
+    const double* b;
+    const double* dinv;
+    double* res;
+    double* dnext;
+    double* xs;
+    const double* live;
+    const double* lam;
+    double ratio;
+    int k;
+    int pending;
+    double th, ca, cb;
+    __device__ bool enter() {
+        if (live && !(live[S_DONE] == 0.0 && live[S_FAIL] == 0.0)) return false;
+        const Cheb c = cheb_of(lam, ratio);
+        th = c.theta;
+        ca = cb = 0.0;
+        if (EPI == E3_CHEB || EPI == E3_CHEB_B) cheb_ab(c, k, ca, cb);
+        return true;
+    }
+    __device__ void issue_v(const Geo3& g, int i, int j, int k_, const S3& s) const {
+        if (EPI != E3_CHEB_B) { Base::issue_v(g, i, j, k_, s); return; }
+        const long long v = vid3(g, i, j, k_);
+        put3_3(s, 0, b, v);
+        put3_3(s, 3, dinv, v);
+        put1_3(s, 6, this->alpha, v);
+    }
+    __device__ void fix_v(const Geo3& g, int i, int j, int k_, const S3& s, double (&v)[4]) const {
+        if (EPI != E3_CHEB_B) { Base::fix_v(g, i, j, k_, s, v); return; }
+        const unsigned m = this->bcmode ? bc3(g, i, j, k_, vid3(g, i, j, k_)) : 0u;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) v[c] = ((m >> c) & 1u) ? 0.0 : (get1_3(s, 3 + c) * get1_3(s, c)) / th;
+        v[3] = get1_3(s, 6);
+    }
+    __device__ void out(const Geo3& g, int i, int j, int k_, const double (&t)[3], const double (&v)[4]) {
+        const long long id = vid3(g, i, j, k_);
+        const unsigned m = this->bcmode ? bc3(g, i, j, k_, id) : 0u;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const long long q = 3 * id + c;
+            double w = t[c], p = v[c];
+            if ((m >> c) & 1u) {
+                p = EPI == E3_CHEB_B ? (__ldg(dinv + q) * __ldg(b + q)) / th : __ldg(this->x + q);
+                w = p;
+            }
+            if (EPI == E3_RESID) {
+                res[q] = __ldg(b + q) - w;
+            } else if (EPI == E3_RESID_CHEB0) {
+                const double r = __ldg(dinv + q) * (__ldg(b + q) - w);
+                res[q] = r;
+                dnext[q] = r / th;
+            } else {
+                const double dq = __ldg(dinv + q);
+                const double r = (EPI == E3_CHEB_B ? dq * __ldg(b + q) : res[q]) - dq * w;
+                const double dn = ca * p + cb * r;
+                res[q] = r;
+                dnext[q] = dn;
+                if (EPI == E3_CHEB_B) xs[q] = p + dn;
+                else xs[q] = pending ? (xs[q] + p) + dn : xs[q] + dn;
+            }
+        }
     }
 };
 
@@ -526,8 +631,13 @@ struct Op3Kaa {
     double* scal;
     RedBuf rb;
     double acc;
+    double breg = 0.0;  // persistent PCG (k_pcg_kaa3): beta held in a register instead of scal[S_BETA]
+    int use_breg = 0;
     __device__ bool enter() const { return !FUSED || (scal[S_DONE] == 0.0 && scal[S_FAIL] == 0.0); }
-    __device__ __forceinline__ double bval() const { return scal[S_ITER] > 0.0 ? scal[S_BETA] : 0.0; }
+    __device__ __forceinline__ double bval() const {
+        if (use_breg) return breg;
+        return scal[S_ITER] > 0.0 ? scal[S_BETA] : 0.0;
+    }
     __device__ void issue_v(const Geo3& g, int i, int j, int k, const S3& s) const {
         const long long v = vid3(g, i, j, k);
         put1_3(s, 0, x, v);
@@ -676,7 +786,7 @@ struct Op3KaaTrial {
 // ================================================================================================
 template <int ROWS>
 struct Op3Phys {
-    static constexpr int NV = 4, NC = 4, PD = 2, NE = 2, SV = 4, SC = 2;
+    static constexpr int NV = 4, NC = 4, PD = 2, NE = 2, SV = 4, SC = 2, MINB = 1;
     const double* u;
     const double* alpha;
     const double* lb;
@@ -818,7 +928,7 @@ struct Op3Rhs {
 // Coupled Jacobian apply [[Kuu_bc, Kua_bc], [Kau_bc, Kaa]] (optionally masked by act), also used
 // for Kua (xu = 0) / Kau (xa = 0) alone.  vertex: u, alpha, xu, xa, [act] ; cell: E, Gc
 struct Op3Jac : NoRed3 {
-    static constexpr int NV = 8, NC = 4, PD = 2, NE = 2, SV = 9, SC = 2;
+    static constexpr int NV = 8, NC = 4, PD = 2, NE = 2, SV = 9, SC = 2, MINB = 1;
     const double* u;
     const double* alpha;
     const double* xu;
@@ -914,20 +1024,22 @@ struct Op3Jac : NoRed3 {
 
 // ---- launch plumbing -----------------------------------------------------------------------------
 template <class Op>
-static int run3g(Ctx* c, const Geo3& g, Op op, cudaStream_t st, int kind, double bytes) {
-    constexpr int smem = kW3 * Op::PD * (Op::SV + Op::SC) * 256 + kW3 * Op::NV * 32 * 8 +
-                         kW3 * 2 * Op::NC * 32 * 8;
+static int run3g(Ctx* c, const Geo3& g0, Op op, cudaStream_t st, int kind, double bytes) {
+    constexpr int kW3 = WarpsOf<Op>::v;
+    Geo3 g = g0;
+    if (kW3 != 8) tile3(g, kW3 - 2);  // Geo3's own tiling is for 8 warps
+    constexpr int smem = strip3_smem<Op, kW3>();
     static_assert(smem <= 227 * 1024, "3D stage ring exceeds shared memory");
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_strip3d<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaError_t e = cudaFuncSetAttribute(k_strip3d<Op, kW3, MinBlocksOf<Op>::v>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return check_cuda(c, e, "3D kernel attribute");
         attr = true;
     }
     const long long nb = (long long)g.nbj * g.nbk * g.nstrips;
     if (nb > kMaxBlocksRed) return set_error(c, PF_EINVAL, "3D grid too large for the reduction buffer");
     const int ps = prof_begin(c, st);
-    k_strip3d<Op><<<(int)nb, kBlock3, smem, st>>>(g, op);
+    k_strip3d<Op, kW3, MinBlocksOf<Op>::v><<<(int)nb, kW3 * 32, smem, st>>>(g, op);
     prof_end(c, st, ps, kind, bytes);
     c->launches++;
     return check_cuda(c, cudaGetLastError(), "3D strip kernel launch");
@@ -935,6 +1047,15 @@ static int run3g(Ctx* c, const Geo3& g, Op op, cudaStream_t st, int kind, double
 template <class Op>
 static int run3(Ctx* c, Op op, cudaStream_t st, int kind, double bytes) {
     return run3g(c, c->g3, op, st, kind, bytes);
+}
+// A/B switch for the tiling of the Kuu / Kaa applies: PF_K3W=16 (one 16-warp block per SM) or 8
+// (two 8-warp blocks per SM)
+template <class Op>
+static int run3w(Ctx* c, const Geo3& g, Op op, cudaStream_t st, int kind, double bytes) {
+    static const int w = getenv("PF_K3W") ? atoi(getenv("PF_K3W")) : 0;
+    if (w == 16) return run3g(c, g, Tiled3<Op, 16, 1>{op}, st, kind, bytes);
+    if (w == 8) return run3g(c, g, Tiled3<Op, 8, 2>{op}, st, kind, bytes);
+    return run3g(c, g, op, st, kind, bytes);
 }
 static RedBuf rb3(Ctx* c) { return RedBuf{c->partials, c->tickets, c->scal}; }
 
@@ -944,10 +1065,28 @@ int launch3_Kuu_on(Ctx* c, const Geo3& g, const double* alpha, const double* x, 
                    cudaStream_t st, int kind) {
     if (iso3(g)) {
         Op3Kuu<false, true> op{alpha, x, nullptr, nullptr, y, bcmode, c->scal, rb3(c), 0.0};
-        return run3g(c, g, op, st, kind, 56.0 * g.nv);
+        return run3w(c, g, op, st, kind, 56.0 * g.nv);
     }
     Op3Kuu<false, false> op{alpha, x, nullptr, nullptr, y, bcmode, c->scal, rb3(c), 0.0};
     return run3g(c, g, op, st, kind, 56.0 * g.nv);
+}
+template <int EPI, bool ISO>
+static int run3_sm(Ctx* c, const Geo3& g, const Sm3Args& a, cudaStream_t st, int kind) {
+    Op3KuuSm<EPI, ISO> op{{a.alpha, a.xin, nullptr, nullptr, nullptr, PF_BC_ELIMINATE, c->scal, rb3(c), 0.0},
+                          a.b, a.dinv, a.res, a.dnext, a.xs, a.live, a.lam, a.ratio, a.k, a.pending,
+                          0.0, 0.0, 0.0};
+    const double vec = EPI == E3_RESID ? 48.0 : (EPI == E3_RESID_CHEB0 ? 96.0 : (EPI == E3_CHEB ? 144.0 : 144.0));
+    return run3g(c, g, op, st, kind, (EPI == E3_CHEB_B ? 56.0 + 24.0 : 56.0 - 24.0) * g.nv + vec * g.nv);
+}
+int launch3_Kuu_sm(Ctx* c, const Geo3& g, int epi, const Sm3Args& a, cudaStream_t st, int kind) {
+    const bool iso = iso3(g);
+    switch (epi) {
+        case E3_CHEB: return iso ? run3_sm<E3_CHEB, true>(c, g, a, st, kind) : run3_sm<E3_CHEB, false>(c, g, a, st, kind);
+        case E3_CHEB_B: return iso ? run3_sm<E3_CHEB_B, true>(c, g, a, st, kind) : run3_sm<E3_CHEB_B, false>(c, g, a, st, kind);
+        case E3_RESID: return iso ? run3_sm<E3_RESID, true>(c, g, a, st, kind) : run3_sm<E3_RESID, false>(c, g, a, st, kind);
+        default: return iso ? run3_sm<E3_RESID_CHEB0, true>(c, g, a, st, kind)
+                            : run3_sm<E3_RESID_CHEB0, false>(c, g, a, st, kind);
+    }
 }
 int launch3_Kuu_diag_on(Ctx* c, const Geo3& g, const double* alpha, double* dinv, cudaStream_t st, int kind) {
     Op3KuuDiag op;
@@ -983,21 +1122,133 @@ int launch3_Kaa(Ctx* c, const double* kappa, const double* x, double* y, const u
     const double bytes = 16.0 * c->g3.nv + 8.0 * c->n_el;
     if (act) {
         Op3Kaa<false, true> op{kappa, x, nullptr, nullptr, y, act, c->scal, rb3(c), 0.0};
-        return run3(c, op, st, K_KAA, bytes);
+        return run3w(c, c->g3, op, st, K_KAA, bytes);
     }
     Op3Kaa<false, false> op{kappa, x, nullptr, nullptr, y, nullptr, c->scal, rb3(c), 0.0};
-    return run3(c, op, st, K_KAA, bytes);
+    return run3w(c, c->g3, op, st, K_KAA, bytes);
 }
 int launch3_Kaa_cgA(Ctx* c, const double* kappa, const double* z, const double* p_in, double* p_out, double* q,
                     const unsigned char* act, cudaStream_t st) {
     const double bytes = 33.0 * c->g3.nv + 8.0 * c->n_el;
     if (act) {
         Op3Kaa<true, true> op{kappa, z, p_in, p_out, q, act, c->scal, rb3(c), 0.0};
-        return run3(c, op, st, K_KAA_CG, bytes);
+        return run3w(c, c->g3, op, st, K_KAA_CG, bytes);
     }
     Op3Kaa<true, false> op{kappa, z, p_in, p_out, q, nullptr, c->scal, rb3(c), 0.0};
-    return run3(c, op, st, K_KAA_CG, bytes);
+    return run3w(c, c->g3, op, st, K_KAA_CG, bytes);
 }
+// The whole masked Jacobi-PCG loop on the 3D damage block in one cooperative launch, as the 2D
+// k_pcg_kaa (pf_ops2d.cu): per iteration one strip pass over all tiles (p = z + beta p, q = Kaa p,
+// p.q) and one vector pass (x += gamma p, r -= gamma q, z = D^-1 r, r.r, r.z), separated by grid
+// barriers; the scalar decisions come from fixed-order sums, identical in every CTA.  Replaces two
+// launches per iteration (plus the graph's loop node) on a latency-bound 2-17 MB problem.
+template <bool MASKED>
+__global__ void __launch_bounds__(kW3 * 32, 2) k_pcg_kaa3(const Geo3 g, Op3Kaa<true, MASKED> op, int ntile, long long n,
+                                                         double* x, double* r, double* z, double* p0, double* p1,
+                                                         double* q, const double* dinv, double* s, double* partials,
+                                                         unsigned int* bar) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    if (!(s[S_DONE] == 0.0 && s[S_FAIL] == 0.0)) return;  // uniform
+    const double target = s[S_TARGET], maxit = s[S_MAXIT];
+    double rz = s[S_RZ], beta = s[S_BETA], rn = s[S_RNORM], pap = 0.0, gm = 0.0;
+    long long it = (long long)s[S_ITER];
+    double done = 0.0, fail = 0.0;
+    const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x, nth = (long long)gridDim.x * blockDim.x;
+    for (;;) {
+        double* pin = (it & 1) ? p1 : p0;
+        double* pout = (it & 1) ? p0 : p1;
+        op.x = z;
+        op.pin = pin;
+        op.pout = pout;
+        op.y = q;
+        op.acc = 0.0;
+        op.use_breg = 1;
+        op.breg = it > 0 ? beta : 0.0;
+        for (int t = blockIdx.x; t < ntile; t += gridDim.x) {
+            __syncthreads();  // the previous tile's readers of the exchange buffers are done
+            strip3_tile<Op3Kaa<true, MASKED>, kW3>(g, op, smem, t);
+        }
+        block_partials(&op.acc, 1, partials, 0);
+        grid_sync(bar);
+        pap = grid_total(partials, 0);
+        if (!(pap > 0.0)) { fail = 1.0; break; }
+        gm = rz / pap;
+        double acc[2] = {0.0, 0.0};
+        for (long long i = tid; i < n; i += nth) {
+            const double xi = __ldcg(x + i) + gm * __ldcg(pout + i);
+            const double ri = __ldcg(r + i) - gm * __ldcg(q + i);
+            const double zi = dinv[i] * ri;
+            x[i] = xi;
+            r[i] = ri;
+            z[i] = zi;
+            acc[0] += ri * ri;
+            acc[1] += ri * zi;
+        }
+        block_partials(acc, 2, partials, 1);
+        grid_sync(bar);
+        const double2 t2 = grid_total2(partials, 1);
+        const double rr = t2.x, rzn = t2.y;
+        ++it;
+        rn = sqrt(rr);
+        if (rn <= target) { done = 1.0; break; }
+        if (!(rzn > 0.0)) { fail = 2.0; break; }
+        beta = rzn / rz;
+        rz = rzn;
+        if ((double)it >= maxit) { done = 3.0; break; }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        s[S_ITER] = (double)it;
+        s[S_RNORM] = rn;
+        s[S_PAP] = pap;
+        s[S_GAMMA] = gm;
+        s[S_RZ] = rz;
+        s[S_BETA] = beta;
+        s[S_DONE] = done;
+        s[S_FAIL] = fail;
+    }
+}
+
+template <bool MASKED>
+static int launch3_pcg_kaa_m(Ctx* c, const PcgBuffers& B, const double* kappa, const unsigned char* act,
+                             cudaStream_t st) {
+    using Op = Op3Kaa<true, MASKED>;
+    constexpr int smem = strip3_smem<Op, kW3>();
+    static int per = -1;
+    if (per < 0) {
+        cudaError_t e = cudaFuncSetAttribute(k_pcg_kaa3<MASKED>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return check_cuda(c, e, "persistent 3D pcg attribute");
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_pcg_kaa3<MASKED>, kW3 * 32, smem);
+        if (e != cudaSuccess) return check_cuda(c, e, "persistent 3D pcg occupancy");
+    }
+    int dev = 0, nsm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const Geo3& g = c->g3;
+    const int ntile = g.nbj * g.nbk * g.nstrips;
+    const int nb = std::min(ntile, nsm * std::max(per, 1));
+    if (per < 1 || nb > kMaxBlocksRed) return PF_EINVAL;  // caller falls back to the graph loop
+    Op op{kappa, B.z, B.p0, B.p1, B.q, act, c->scal, rb3(c), 0.0};
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(nb);
+    cfg.blockDim = dim3(kW3 * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    const int ps = prof_begin(c, st);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_pcg_kaa3<MASKED>, g, op, ntile, B.n, B.x, B.r, B.z, B.p0, B.p1, B.q,
+                                       (const double*)B.dinv, c->scal, c->partials, c->tickets + 62);
+    prof_end(c, st, ps, K_KAA_CG, 0.0);
+    c->launches++;
+    return check_cuda(c, e, "persistent 3D pcg launch");
+}
+int launch3_pcg_kaa(Ctx* c, const PcgBuffers& B, const double* kappa, const unsigned char* act, cudaStream_t st) {
+    return act ? launch3_pcg_kaa_m<true>(c, B, kappa, act, st) : launch3_pcg_kaa_m<false>(c, B, kappa, act, st);
+}
+
 int launch3_Kaa_diag(Ctx* c, const double* kappa, double* dinv, const unsigned char* act, cudaStream_t st) {
     if (act) {
         Op3KaaDiag<true> op;

@@ -157,3 +157,69 @@ def test_traction3d_config4_shape_gmg_matches_oracle(inner):
         for k in range(3):
             assert abs(r.energy[k] - o.energy[k]) <= 1e-6 * abs(o.energy[k]) + 1e-14, (r.step, k)
         assert np.max(np.abs(r.alpha - o.alpha)) < 1e-4
+
+
+_FUSED_SNIPPET = r"""
+import sys, numpy as np
+sys.path.insert(0, "tests")
+from test_gpu_ops3d import make3, dev, host
+import paper_1511_08463_b200 as pf
+prob, om, rng = make3(19, 13, 22, model="AT1")
+nv = om.nv
+lb = rng.uniform(0, 0.3, nv)
+a = lb + rng.uniform(0, 1, nv) * (1 - lb)
+a[rng.uniform(size=nv) < 0.05] = 1.0
+u = 0.3 * rng.standard_normal(3 * nv)
+st = pf.State(dev(u), dev(a), dev(lb))
+ug, kg = pf.elastic_step(st, prob, pf.SolverConfig(elastic_solver="cg", elastic_rtol=1e-12,
+                                                   elastic_precond="gmg", gmg_reuse=False))
+np.save(sys.argv[1], host(ug))
+print(kg)
+"""
+
+
+@pytest.mark.parametrize("degree", [2, 3])
+def test_gmg3_fused_smoother_matches_separate_passes(tmp_path, degree):
+    """The 3D V-cycle with the smoother steps fused into the Kuu apply (Op3KuuSm) against the same
+    cycle with one vector pass per step (PF_GMG3_UNFUSED=1): same PCG iterations, same solution."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    snippet = _FUSED_SNIPPET.replace('elastic_precond="gmg"', f'elastic_precond="gmg", gmg_degree={degree}')
+    out = {}
+    for tag, extra in (("fused", {}), ("split", {"PF_GMG3_UNFUSED": "1"})):
+        env = dict(os.environ, **extra)
+        f = tmp_path / f"{tag}.npy"
+        r = subprocess.run([sys.executable, "-c", snippet, str(f)], cwd=root, env=env, capture_output=True,
+                           text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        out[tag] = (int(r.stdout.split()[-1]), np.load(f))
+    assert abs(out["fused"][0] - out["split"][0]) <= 1, (out["fused"][0], out["split"][0])
+    assert rel(out["fused"][1], out["split"][1]) < 1e-10
+
+
+@pytest.mark.parametrize("model", ["AT1", "AT2"])
+def test_persistent_damage_pcg_3d_matches_graph_loop(monkeypatch, model):
+    """The 3D damage Jacobi-PCG in one cooperative launch (k_pcg_kaa3, tiles distributed over the
+    resident CTAs) against the graph-replayed two-launch loop (PF_PCG_GRAPH=1): same VI iterations,
+    Krylov counts within one per VI iteration, same damage field."""
+    import paper_1511_08463_b200 as pf
+    out = {}
+    for graph in (False, True):
+        if graph:
+            monkeypatch.setenv("PF_PCG_GRAPH", "1")
+        else:
+            monkeypatch.delenv("PF_PCG_GRAPH", raising=False)
+        prob, om, rng = make3(23, 9, 31, model=model)
+        nv = om.nv
+        lb = rng.uniform(0, 0.3, nv)
+        a = lb + rng.uniform(0, 1, nv) * (1 - lb)
+        u = 0.5 * rng.standard_normal(3 * nv)
+        st = pf.State(dev(u), dev(a), dev(lb))
+        out[graph] = pf.damage_step(st, prob, pf.SolverConfig(outer_atol=1e-9))
+    (a0, r0), (a1, r1) = out[False], out[True]
+    assert r0.converged and r1.converged
+    assert r0.iterations == r1.iterations
+    assert abs(r0.total_krylov_iterations - r1.total_krylov_iterations) <= r0.iterations
+    assert float((a0 - a1).abs().max()) < 1e-9

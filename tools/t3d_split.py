@@ -16,7 +16,8 @@ cfg = pf.SolverConfig(method="oram_newton", omega=1.7, outer_atol=1e-6, elastic_
                       fieldsplit_inner=inner,
                       fieldsplit_additive=bool(int(os.environ.get("ADDITIVE", "1"))),
                       damage_forcing=bool(int(os.environ.get("FORCING", "1"))),
-                      fieldsplit_cheb_degree=int(os.environ.get("CDEG", "12")))
+                      fieldsplit_cheb_degree=int(os.environ.get("CDEG", "6")),
+                      gmg_degree=int(os.environ.get("DEG", "2")))
 st = pf.State.zeros(setup.mesh)
 pf.run_quasistatic(setup, cfg, snapshot_stride=0, state=st, steps=list(range(k)))
 acc = defaultdict(lambda: [0, 0.0])
@@ -38,7 +39,7 @@ try:
 except Exception as e:  # noqa: BLE001
     print("FAILED:", e)
 torch.cuda.synchronize(); tot = time.perf_counter() - t0
-print(f"inner={inner} add={cfg.fieldsplit_additive} forcing={cfg.damage_forcing} 2 load steps ({k},{k+1}): {1e3*tot:.1f} ms")
+print(f"deg={cfg.gmg_degree} inner={inner} add={cfg.fieldsplit_additive} forcing={cfg.damage_forcing} 2 load steps ({k},{k+1}): {1e3*tot:.1f} ms")
 for name, (c, t) in acc.items():
     print(f"  {name:22s} calls={c:4d} total={1e3*t:8.1f} ms  per call={1e3*t/max(c,1):7.3f} ms")
 for row in log:
