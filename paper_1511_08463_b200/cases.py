@@ -245,6 +245,21 @@ class StepFailureError(RuntimeError):
         self.step, self.load, self.records, self.state, self.report = step, load, records, state, report
 
 
+def _to_host(problem, t) -> np.ndarray:
+    """Device field -> fresh host array through a pinned staging buffer kept on the problem
+    (a pageable .cpu() of a 128^3 snapshot ran at ~2.5 GB/s: 27 ms of a 0.2 s load step)."""
+    if not t.is_cuda:
+        return t.numpy().copy()
+    n = t.numel()
+    buf = getattr(problem, "_pinned_stage", None)
+    if buf is None or buf.numel() < n:
+        buf = torch.empty(n, dtype=t.dtype, pin_memory=True)
+        problem._pinned_stage = buf
+    v = buf[:n]
+    v.copy_(t.reshape(-1))
+    return v.numpy().copy().reshape(tuple(t.shape))
+
+
 def run_quasistatic(setup: ProblemSetup, config: SolverConfig, snapshot_stride: int = 1,
                     state: Optional[State] = None, steps=None) -> list:
     """March a state through the loading schedule (cases.py:268-306).
@@ -273,8 +288,8 @@ def run_quasistatic(setup: ProblemSetup, config: SolverConfig, snapshot_stride: 
         energy = assemble_energy(state, problem)
         snap = snapshot_stride > 0 and (k % snapshot_stride == 0 or k == n - 1)
         records.append(StepRecord(step=k, load=t, energy=energy, report=report,
-                                  u=state.u.cpu().numpy() if snap else None,
-                                  alpha=state.alpha.cpu().numpy() if snap else None))
+                                  u=_to_host(problem, state.u) if snap else None,
+                                  alpha=_to_host(problem, state.alpha) if snap else None))
         if not report.converged:
             raise StepFailureError(k, t, records, state, report)
     return records

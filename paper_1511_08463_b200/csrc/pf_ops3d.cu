@@ -191,6 +191,80 @@ __device__ __forceinline__ void kuu_hex(const Geo3& g, const double (&U)[3][8], 
     kuu_pair<2, 0, 1, ISO>(g, U, Al, s07, ve, Y);
 }
 
+// Edge-flux form of the same action (used by Op3Kuu).  Every Kuhn path edge is a cube edge: tet
+// (A,B,C) walks axis A at corner 0, axis B at corner bit(A), axis C at corner 7 - bit(C).  So the
+// 12 cube-edge differences are formed once per hex (36 subtractions instead of 45), each tet adds
+// its three axis fluxes to its path edges (the A edge is shared by the pair (A,B,C), (A,C,B); the C
+// edge by (A,B,C), (B,A,C)), and each node force is the difference of the fluxes of its three
+// edges (66 adds instead of 108).  Y is assigned, not accumulated.
+template <bool ISO>
+__device__ __forceinline__ void kuu_hex_e(const Geo3& g, const double (&U)[3][8], const double (&Al)[8], double Ec,
+                                          double (&Y)[3][8]) {
+    double D[3][8][3], F[3][8][3];  // [axis][low corner][component]; corners with the axis bit set unused
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+        const int b = ax == 0 ? 4 : (ax == 1 ? 2 : 1);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            if (q & b) continue;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                D[ax][q][c] = U[c][q | b] - U[c][q];
+                if (!ISO) D[ax][q][c] *= ihof(g, ax);
+            }
+        }
+    }
+    const double s07 = Al[0] + Al[7];
+    const double ve = ISO ? g.vol * Ec * (g.ihx * g.ihx) : g.vol * Ec;
+    for_each_tet([&](auto, auto A_, auto B_, auto C_) {
+        constexpr int A = decltype(A_)::v, B = decltype(B_)::v, C = decltype(C_)::v;
+        constexpr int q1 = Bit<A>::v, q2 = Bit<A>::v | Bit<B>::v;
+        const double (&D1)[3] = D[A][0];
+        const double (&D2)[3] = D[B][q1];
+        const double (&D3)[3] = D[C][q2];
+        const double ab = (s07 + (Al[q1] + Al[q2])) * 0.25;
+        const double om = 1.0 - ab;
+        const double sk = (om * om + g.kell) * ve;
+        const double eaa = D1[A], ebb = D2[B], ecc = D3[C];
+        const double gab = D1[B] + D2[A], gac = D1[C] + D3[A], gbc = D2[C] + D3[B];
+        const double lt = (sk * g.lam) * (eaa + ebb + ecc);
+        const double m2 = sk * (2.0 * g.mu), m1 = sk * g.mu;
+        const double saa = lt + m2 * eaa, sbb = lt + m2 * ebb, scc = lt + m2 * ecc;
+        const double sab = m1 * gab, sac = m1 * gac, sbc = m1 * gbc;
+        double f1[3], f2[3], f3[3];
+        f1[A] = saa; f1[B] = sab; f1[C] = sac;
+        f2[A] = sab; f2[B] = sbb; f2[C] = sbc;
+        f3[A] = sac; f3[B] = sbc; f3[C] = scc;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            if (B < C) F[A][0][c] = f1[c]; else F[A][0][c] += f1[c];
+            F[B][q1][c] = f2[c];
+            if (A < B) F[C][q2][c] = f3[c]; else F[C][q2][c] += f3[c];
+        }
+    });
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+        const int b = ax == 0 ? 4 : (ax == 1 ? 2 : 1);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            if (q & b) continue;
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+                if (!ISO) F[ax][q][c] *= ihof(g, ax);
+        }
+    }
+    // node q: + flux of each edge ending at q, - flux of each edge starting at q
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const double t0 = (q & 4) ? F[0][q ^ 4][c] : -F[0][q][c];
+            const double t1 = (q & 2) ? F[1][q ^ 2][c] : -F[1][q][c];
+            const double t2 = (q & 1) ? F[2][q ^ 1][c] : -F[2][q][c];
+            Y[c][q] = (t0 + t1) + t2;
+        }
+}
+
 // ---- staging helpers (same conventions as 2D: slot q of lane l at q*256 + 8l) ------------------
 __device__ __forceinline__ unsigned smem_addr3(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void cp8(void* dst, const void* src) {
@@ -416,7 +490,7 @@ struct Op3Kuu {
     __device__ void cell(const Geo3& g, int, int, int, const double (&X)[NV][8], const double (&ec)[NE],
                          double (&Y)[NC][8], bool) {
         const double (&U)[3][8] = *reinterpret_cast<const double(*)[3][8]>(&X[0][0]);
-        kuu_hex<ISO>(g, U, X[3], ec[0], Y);
+        kuu_hex_e<ISO>(g, U, X[3], ec[0], Y);
     }
     __device__ __forceinline__ double xval(const Geo3&, long long v, int c) const {
         double z = __ldg(x + 3 * v + c);
