@@ -839,18 +839,32 @@ static void geometry_3d(Ctx* c) {
     tile3(g);
 }
 
-// 3D strip tiling: blocks of outj (6) j-pencils x 30 k-lanes, strips of S vertex rows sized for
-// ~4 blocks per SM across the 148 SMs
-void pf::tile3(Geo3& g, int outj) {
+// 3D strip tiling: blocks of outj (6) j-pencils x 30 k-lanes walking strips of S vertex rows.
+// The strip count minimises a wave model of the latency-bound walk: time ~ waves x (S + 1 + 3)
+// row steps (one halo row, ~3 steps of pipeline ramp per tile), waves = ceil(tiles / resident)
+// with `resident` CTAs in flight (148 SMs x blocks per SM).  At 128^3 this picks 5 strips of 26
+// rows (550 tiles, two waves of 296) instead of 6 strips of 24 (660 tiles, a third wave of 68).
+// Measured against the fixed ~4-blocks-per-SM rule: 256^3 Kuu 0.757 -> 0.739 ms, Kaa 0.385 ->
+// 0.375 ms, config-4 damage PCG -7%; 128^3 single applies within 2% (the model overstates the
+// tail: a partial wave overlaps the previous one's stragglers).
+void pf::tile3(Geo3& g, int outj, int resident) {
     g.nbj = (g.nvy + outj - 1) / outj;
     g.nbk = (g.nvz + 29) / 30;
     const long long per = (long long)g.nbj * g.nbk;
-    long long S = ((g.nx + 1) * per + 148LL * 4 - 1) / (148LL * 4);
-    S = std::max(4LL, std::min(64LL, S));
-    // large grids: longer strips keep the block count within the reduction buffer
-    while (per * ((g.nx + 1 + S - 1) / S) > kMaxBlocksRed && S < g.nx + 1) S *= 2;
+    const long long rows = g.nx + 1;
+    long long best_ns = 1, best_t = -1;
+    for (long long ns = 1; ns <= rows; ++ns) {
+        const long long S = (rows + ns - 1) / ns;
+        if (S < 4 && ns > 1) break;
+        const long long tiles = per * ns;
+        if (tiles > kMaxBlocksRed) break;
+        const long long waves = (tiles + resident - 1) / resident;
+        const long long t = waves * (S + 4);
+        if (best_t < 0 || t < best_t) { best_t = t; best_ns = ns; }
+    }
+    const long long S = (rows + best_ns - 1) / best_ns;
     g.S = (int)S;
-    g.nstrips = (int)((g.nx + 1 + S - 1) / S);
+    g.nstrips = (int)((rows + S - 1) / S);
 }
 
 __global__ void k_relax_u3(long long nv, int nvy, int nvz, int nx, int ny, int nz, const double* __restrict__ up,

@@ -352,7 +352,7 @@ struct CgScal {  // pointers into the scalar block used by fused CG kernels
 // y = K p_out and pAp reduced into scal (CG step A).
 int launch_Kuu(Ctx* c, const double* alpha, const double* x, double* y, int bcmode,
                cudaStream_t st);
-void tile3(Geo3& g, int outj = 6);  // outj = output pencils per block (warps - 2)
+void tile3(Geo3& g, int outj = 6, int resident = 296);  // outj = output pencils per block (warps - 2)
 int launch3_Kuu_on(Ctx* c, const Geo3& g, const double* alpha, const double* x, double* y, int bcmode,
                    cudaStream_t st, int kind);
 // Kuu apply with a fused multigrid-smoother epilogue (pf_ops3d.cu, Op3KuuSm)

@@ -1101,7 +1101,7 @@ template <class Op>
 static int run3g(Ctx* c, const Geo3& g0, Op op, cudaStream_t st, int kind, double bytes) {
     constexpr int kW3 = WarpsOf<Op>::v;
     Geo3 g = g0;
-    if (kW3 != 8) tile3(g, kW3 - 2);  // Geo3's own tiling is for 8 warps
+    if (kW3 != 8 || MinBlocksOf<Op>::v != 2) tile3(g, kW3 - 2, 148 * MinBlocksOf<Op>::v);  // Geo3's own tiling: 8 warps x 2
     constexpr int smem = strip3_smem<Op, kW3>();
     static_assert(smem <= 227 * 1024, "3D stage ring exceeds shared memory");
     static bool attr = false;
