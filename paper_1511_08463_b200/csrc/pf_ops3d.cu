@@ -310,15 +310,20 @@ __device__ __forceinline__ unsigned bc3(const Geo3& g, int i, int j, int k, long
 
 // ---- the 3D strip engine ----------------------------------------------------------------------
 // one tile (j-block bj, k-block bk, strip bs) of the engine; `tile` plays the role of the block index
-// (k_strip3d: one tile per CTA; the persistent damage PCG: tiles distributed over resident CTAs)
+// (k_strip3d: one tile per CTA; the persistent damage PCG: tiles distributed over resident CTAs).
+// One block barrier per row step: step ci computes cell row ci from the vertex rows ci / ci+1 it
+// already holds, then fixes vertex row ci+2 (and cell row ci+1) from the stage ring and publishes
+// both its j-carry contributions and row ci+2 in one double-buffered exchange.  (The first form
+// published row ci+1 and the contributions behind two barriers per step; barrier stalls were
+// the largest stall reason of the 256^3 Kuu apply.)
 template <class Op, int kW3>
 __device__ __forceinline__ void strip3_tile(const Geo3& g, Op& op, unsigned char* smem, int tile) {
     constexpr int kOutJ3 = kW3 - 2;  // output pencils per block
     constexpr int NV = Op::NV, NC = Op::NC, PD = Op::PD, NE = Op::NE, SV = Op::SV, SC = Op::SC;
     constexpr int STAGE = (SV + SC) * 256;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    double* vx = reinterpret_cast<double*>(smem + kW3 * PD * STAGE);   // [kW3][NV][32]
-    double* cx = vx + kW3 * NV * 32;                                     // [kW3][2][NC][32]
+    double* vx = reinterpret_cast<double*>(smem + kW3 * PD * STAGE);   // [2][kW3][NV][32]
+    double* cx = vx + 2 * kW3 * NV * 32;                                 // [2][kW3][2][NC][32]
     const int bk = tile % g.nbk;
     const int rest = tile / g.nbk;
     const int bj = rest % g.nbj;
@@ -331,7 +336,7 @@ __device__ __forceinline__ void strip3_tile(const Geo3& g, Op& op, unsigned char
     const int i1 = min(i0 + g.S, g.nx + 1);
     const int vlast = min(i1, g.nx), clast = min(i1 - 1, g.nx - 1);
     unsigned char* wbase = smem + w * (PD * STAGE);
-    double vc[NV], rc[NV], carry[NC];
+    double vc[NV], rc[NV], vn[NV], rn[NV], ec[NE], carry[NC];
 #pragma unroll
     for (int q = 0; q < NC; ++q) carry[q] = 0.0;
     int ci = i0 - 1;
@@ -341,6 +346,9 @@ __device__ __forceinline__ void strip3_tile(const Geo3& g, Op& op, unsigned char
         if (cr >= 0 && cr <= clast && cv) op.issue_c(g, cr, j, k, s.at(SV));
         cp_commit3();
     };
+    auto xv = [&](int b, int ww, int q) -> double* { return vx + ((b * kW3 + ww) * NV + q) * 32 + lane; };
+    auto xc = [&](int b, int ww, int h, int q) -> double* { return cx + (((b * kW3 + ww) * 2 + h) * NC + q) * 32 + lane; };
+    // row ci (synchronously through stage 0), then the ring of rows ci+1 .. ci+PD
 #pragma unroll
     for (int q = 0; q < NV; ++q) vc[q] = 0.0;
     if (ci >= 0 && vv) {
@@ -350,35 +358,39 @@ __device__ __forceinline__ void strip3_tile(const Geo3& g, Op& op, unsigned char
         cp_wait3<0>();
         op.fix_v(g, ci, j, k, s0, vc);
     }
-    // j+1 neighbour at row ci through shared memory
 #pragma unroll
-    for (int q = 0; q < NV; ++q) vx[(w * NV + q) * 32 + lane] = vc[q];
+    for (int q = 0; q < NV; ++q) *xv(0, w, q) = vc[q];
     __syncthreads();
 #pragma unroll
-    for (int q = 0; q < NV; ++q) rc[q] = (w + 1 < kW3) ? vx[((w + 1) * NV + q) * 32 + lane] : 0.0;
-    __syncthreads();  // every warp has its initial neighbour values before vx is overwritten
+    for (int q = 0; q < NV; ++q) rc[q] = (w + 1 < kW3) ? *xv(0, w + 1, q) : 0.0;
+    __syncthreads();  // every warp read row ci before stage 0 / buffer 0 are reused
 #pragma unroll
     for (int u = 0; u < PD; ++u) issue(u, ci + 1 + u, ci + u);
+    // row ci+1 and cell row ci from stage 0 (buffer 1)
+    {
+        cp_wait3<PD - 1>();
+        const S3 s{wbase, lane};
+#pragma unroll
+        for (int q = 0; q < NV; ++q) vn[q] = 0.0;
+#pragma unroll
+        for (int q = 0; q < NE; ++q) ec[q] = 0.0;
+        if (ci + 1 <= vlast && vv) op.fix_v(g, ci + 1, j, k, s, vn);
+        if (ci >= 0 && ci < g.nx && cv) op.fix_c(g, ci, j, k, s.at(SV), ec);
+#pragma unroll
+        for (int q = 0; q < NV; ++q) *xv(1, w, q) = vn[q];
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < NV; ++q) rn[q] = (w + 1 < kW3) ? *xv(1, w + 1, q) : 0.0;
+        issue(0, ci + 1 + PD, ci + PD);
+    }
+    int buf = 0;
     while (ci < i1) {
 #pragma unroll
         for (int u = 0; u < PD; ++u) {
             if (ci < i1) {
-                cp_wait3<PD - 1>();
-                const S3 s{wbase + u * STAGE, lane};
-                double vn[NV], rn[NV], ec[NE];
-#pragma unroll
-                for (int q = 0; q < NV; ++q) vn[q] = 0.0;
-#pragma unroll
-                for (int q = 0; q < NE; ++q) ec[q] = 0.0;
+                constexpr int one = 1;
+                const int us = (u + one) % PD;  // the stage holding vertex row ci+2 / cell row ci+1
                 const bool cell_ok = ci >= 0 && ci < g.nx && cv;
-                if (ci + 1 <= vlast && vv) op.fix_v(g, ci + 1, j, k, s, vn);
-                if (cell_ok) op.fix_c(g, ci, j, k, s.at(SV), ec);
-                // vx / cx readers of the previous step finished before its barrier B
-#pragma unroll
-                for (int q = 0; q < NV; ++q) vx[(w * NV + q) * 32 + lane] = vn[q];
-                __syncthreads();  // barrier A
-#pragma unroll
-                for (int q = 0; q < NV; ++q) rn[q] = (w + 1 < kW3) ? vx[((w + 1) * NV + q) * 32 + lane] : 0.0;
                 // corners: q = 4 di + 2 dj + dk
                 double X[NV][8];
 #pragma unroll
@@ -404,24 +416,43 @@ __device__ __forceinline__ void strip3_tile(const Geo3& g, Op& op, unsigned char
                     T10[q] = Y[q][4] + __shfl_up_sync(PF_FULL, Y[q][5], 1);
                     T11[q] = Y[q][6] + __shfl_up_sync(PF_FULL, Y[q][7], 1);
                 }
+                // next rows from the ring
+                cp_wait3<PD - 1>();
+                const S3 s{wbase + us * STAGE, lane};
+                double vnn[NV], ecn[NE];
+#pragma unroll
+                for (int q = 0; q < NV; ++q) vnn[q] = 0.0;
+#pragma unroll
+                for (int q = 0; q < NE; ++q) ecn[q] = 0.0;
+                if (ci + 2 <= vlast && vv) op.fix_v(g, ci + 2, j, k, s, vnn);
+                if (ci + 1 >= 0 && ci + 1 <= clast && cv) op.fix_c(g, ci + 1, j, k, s.at(SV), ecn);
+                // one exchange: j-carry contributions of row ci and vertex row ci+2
 #pragma unroll
                 for (int q = 0; q < NC; ++q) {
-                    cx[((w * 2 + 0) * NC + q) * 32 + lane] = T01[q];
-                    cx[((w * 2 + 1) * NC + q) * 32 + lane] = T11[q];
+                    *xc(buf, w, 0, q) = T01[q];
+                    *xc(buf, w, 1, q) = T11[q];
                 }
-                __syncthreads();  // barrier B
+#pragma unroll
+                for (int q = 0; q < NV; ++q) *xv(buf, w, q) = vnn[q];
+                __syncthreads();
                 double tot[NC];
 #pragma unroll
                 for (int q = 0; q < NC; ++q) {
-                    const double l01 = w > 0 ? cx[(((w - 1) * 2 + 0) * NC + q) * 32 + lane] : 0.0;
-                    const double l11 = w > 0 ? cx[(((w - 1) * 2 + 1) * NC + q) * 32 + lane] : 0.0;
+                    const double l01 = w > 0 ? *xc(buf, w - 1, 0, q) : 0.0;
+                    const double l11 = w > 0 ? *xc(buf, w - 1, 1, q) : 0.0;
                     tot[q] = carry[q] + T00[q] + l01;
                     carry[q] = T10[q] + l11;
                 }
+                double rnn[NV];
+#pragma unroll
+                for (int q = 0; q < NV; ++q) rnn[q] = (w + 1 < kW3) ? *xv(buf, w + 1, q) : 0.0;
                 if (ci >= i0 && ov) op.out(g, ci, j, k, tot, vc);
 #pragma unroll
-                for (int q = 0; q < NV; ++q) { vc[q] = vn[q]; rc[q] = rn[q]; }
-                issue(u, ci + 1 + PD, ci + PD);
+                for (int q = 0; q < NV; ++q) { vc[q] = vn[q]; rc[q] = rn[q]; vn[q] = vnn[q]; rn[q] = rnn[q]; }
+#pragma unroll
+                for (int q = 0; q < NE; ++q) ec[q] = ecn[q];
+                issue(us, ci + 2 + PD, ci + 1 + PD);
+                buf ^= 1;
                 ++ci;
             }
         }
@@ -439,7 +470,7 @@ __global__ void __launch_bounds__(kW3 * 32, kMinB) k_strip3d(const Geo3 g, Op op
 
 template <class Op, int kW3>
 static constexpr int strip3_smem() {
-    return kW3 * Op::PD * (Op::SV + Op::SC) * 256 + kW3 * Op::NV * 32 * 8 + kW3 * 2 * Op::NC * 32 * 8;
+    return kW3 * Op::PD * (Op::SV + Op::SC) * 256 + 2 * (kW3 * Op::NV * 32 * 8 + kW3 * 2 * Op::NC * 32 * 8);
 }
 
 struct NoRed3 {
