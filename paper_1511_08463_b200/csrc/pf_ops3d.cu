@@ -923,27 +923,97 @@ struct Op3Phys {
                          double (&Y)[NC][8], bool own) {
         const double (&U)[3][8] = *reinterpret_cast<const double(*)[3][8]>(&X[0][0]);
         double (&YU)[3][8] = *reinterpret_cast<double(*)[3][8]>(&Y[0][0]);
+        // edge-flux form (see kuu_hex_e): the 12 cube-edge differences of u and alpha are formed
+        // once per hex; each tet adds its axis fluxes to its three path edges and its nodal source
+        // to its four nodes; node forces are edge-flux differences.  Y is assigned.
+        const double (&Al)[8] = X[3];
         const double Ec = ec[0], kc = ec[1] / g.cw;
-        for_each_tet([&](auto, auto A, auto B, auto C) {
-            const double ab = tet_abar<A.v, B.v, C.v>(X[3]);
+        const double del = 2.0 * kc * g.ell * g.vol;
+        double D[3][8][3], Da[3][8], F[3][8][3], Fa[3][8];
+#pragma unroll
+        for (int ax = 0; ax < 3; ++ax) {
+            const int b = ax == 0 ? 4 : (ax == 1 ? 2 : 1);
+            const double ih = ihof(g, ax);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                if (q & b) continue;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) D[ax][q][c] = (U[c][q | b] - U[c][q]) * ih;
+                Da[ax][q] = (Al[q | b] - Al[q]) * ih;
+            }
+        }
+        double n_all = 0.0, n_q1[3], n_q2[3];  // nodal sources: nodes 0 and 7 / single-bit / two-bit
+        for_each_tet([&](auto, auto A_, auto B_, auto C_) {
+            constexpr int A = decltype(A_)::v, B = decltype(B_)::v, C = decltype(C_)::v;
+            constexpr int q1 = Bit<A>::v, q2 = Bit<A>::v | Bit<B>::v;
+            const double ab = ((Al[0] + Al[q1]) + (Al[q2] + Al[7])) * 0.25;
             const double om = 1.0 - ab;
             const double a = om * om + g.kell, ap = -2.0 * om;
             const double w = g.at2 ? ab * ab : ab, wp = g.at2 ? 2.0 * ab : 1.0;
-            double G[3][3], e[6], sg[6], gr[3];
-            tet_grad<A.v, B.v, C.v>(g, U, G);
-            voigt(G, e);
-            stress3(g, e, sg);
-            const double q = Ec * (e[0] * sg[0] + e[1] * sg[1] + e[2] * sg[2] + e[3] * sg[3] + e[4] * sg[4] +
-                                   e[5] * sg[5]);
-            tet_scatter<A.v, B.v, C.v>(g, a * g.vol * Ec, sg, YU);
-            tet_sgrad<A.v, B.v, C.v>(g, X[3], gr);
+            const double (&D1)[3] = D[A][0];
+            const double (&D2)[3] = D[B][q1];
+            const double (&D3)[3] = D[C][q2];
+            const double eaa = D1[A], ebb = D2[B], ecc = D3[C];
+            const double gab = D1[B] + D2[A], gac = D1[C] + D3[A], gbc = D2[C] + D3[B];
+            const double lt = g.lam * (eaa + ebb + ecc);
+            const double saa = lt + 2.0 * g.mu * eaa, sbb = lt + 2.0 * g.mu * ebb, scc = lt + 2.0 * g.mu * ecc;
+            const double sab = g.mu * gab, sac = g.mu * gac, sbc = g.mu * gbc;
+            const double q = Ec * (eaa * saa + ebb * sbb + ecc * scc + gab * sab + gac * sac + gbc * sbc);
+            const double kk = a * g.vol * Ec;
+            double f1[3], f2[3], f3[3];
+            f1[A] = kk * saa; f1[B] = kk * sab; f1[C] = kk * sac;
+            f2[A] = kk * sab; f2[B] = kk * sbb; f2[C] = kk * sbc;
+            f3[A] = kk * sac; f3[B] = kk * sbc; f3[C] = kk * scc;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                if (B < C) F[A][0][c] = f1[c]; else F[A][0][c] += f1[c];
+                F[B][q1][c] = f2[c];
+                if (A < B) F[C][q2][c] = f3[c]; else F[C][q2][c] += f3[c];
+            }
+            const double ga = Da[A][0], gb = Da[B][q1], gc = Da[C][q2];
+            if (B < C) Fa[A][0] = del * ga; else Fa[A][0] += del * ga;
+            Fa[B][q1] = del * gb;
+            if (A < B) Fa[C][q2] = del * gc; else Fa[C][q2] += del * gc;
             const double nod = (0.5 * ap * q + kc * wp / g.ell) * g.vol * 0.25;
-            tet_sscatter<A.v, B.v, C.v>(g, nod, 2.0 * kc * g.ell * g.vol, gr, Y[3]);
+            if (A == 0 && B == 1) n_all = nod; else n_all += nod;
+            if (B < C) n_q1[A] = nod; else n_q1[A] += nod;
+            if (A < B) n_q2[C] = nod; else n_q2[C] += nod;
             if (own) {
                 eel += 0.5 * g.vol * a * q;
-                ed += g.vol * kc * (w / g.ell + g.ell * (gr[0] * gr[0] + gr[1] * gr[1] + gr[2] * gr[2]));
+                ed += g.vol * kc * (w / g.ell + g.ell * (ga * ga + gb * gb + gc * gc));
             }
         });
+#pragma unroll
+        for (int ax = 0; ax < 3; ++ax) {
+            const int b = ax == 0 ? 4 : (ax == 1 ? 2 : 1);
+            const double ih = ihof(g, ax);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                if (q & b) continue;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) F[ax][q][c] *= ih;
+                Fa[ax][q] *= ih;
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const double t0 = (q & 4) ? F[0][q ^ 4][c] : -F[0][q][c];
+                const double t1 = (q & 2) ? F[1][q ^ 2][c] : -F[1][q][c];
+                const double t2 = (q & 1) ? F[2][q ^ 1][c] : -F[2][q][c];
+                YU[c][q] = (t0 + t1) + t2;
+            }
+            const double t0 = (q & 4) ? Fa[0][q ^ 4] : -Fa[0][q];
+            const double t1 = (q & 2) ? Fa[1][q ^ 2] : -Fa[1][q];
+            const double t2 = (q & 1) ? Fa[2][q ^ 1] : -Fa[2][q];
+            // nodal source: nodes 0 and 7 in all six tets; node bit(A) in the two tets with first
+            // axis A; node 7 - bit(C) in the two tets with last axis C
+            const int nb = __popc(q);
+            const double src = (nb == 0 || nb == 3) ? n_all
+                             : (nb == 1 ? n_q1[q == 4 ? 0 : (q == 2 ? 1 : 2)] : n_q2[q == 3 ? 0 : (q == 5 ? 1 : 2)]);
+            Y[3][q] = src + ((t0 + t1) + t2);
+        }
     }
     __device__ void out(const Geo3& g, int i, int j, int k, const double (&t)[NC], const double (&v)[NV]) {
         const long long id = vid3(g, i, j, k);
