@@ -467,13 +467,6 @@ def main():
         dist.barrier()
     sampler = ClockSampler(local)
     sampler.start()
-    # ~0.3 s of device work after the sampler's start-up, so the first timed step does not pay
-    # for an idle-clocked GPU (config 4's first timed step measured 0.16-0.25 s for the same work)
-    t_busy = time.perf_counter()
-    while time.perf_counter() - t_busy < 0.3:
-        for _ in range(20):
-            flush.add_(1.0)
-        torch.cuda.synchronize()
     l0 = prob.launches()
     step_s, recs, _, _, _ = run_steps(pf, torch, setup, cfg, state, timed, flush)
     launches = prob.launches() - l0
