@@ -379,6 +379,61 @@ def operator_sweep(pf, torch, peak, reps=10):
     return res
 
 
+UMESH_SWEEP = ((2, 1024), (2, 2048), (2, 4096), (3, 64), (3, 128))
+
+
+def umesh_sweep(pf, torch, peak, reps=10):
+    """Element-list (jittered) meshes: pf_umesh Kuu / Kaa applies on the
+    reference's jittered union-jack rect_mesh (jitter 0.25, mesh.py:134-141) and on jittered
+    Kuhn boxes; same inputs and L2 flush as the structured sweep.  Algorithmic bytes = the
+    compulsory footprint of one apply: per vertex x, y, alpha (Kuu) or u, x, y (Kaa) + the vertex
+    CSR row pointer; per element its record (64 B 2D / 128 B 3D) + int4 connectivity; per
+    (vertex, element) incidence one 4 B entry."""
+    res = []
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device="cuda")
+    for dim, n in UMESH_SWEEP:
+        if dim == 2:
+            mesh = pf.jittered_rect_mesh(1.0, 1.0, 1.0 / n, jitter=0.25, seed=n)
+            mat = pf.Material(E=1.0, nu=0.3, Gc=1.0, ell=0.1, k_ell=1e-6)
+        else:
+            mesh = pf.jittered_box_mesh(n, n, n, jitter=0.25, seed=n)
+            mat = pf.Material(E=1.0, nu=0.3, Gc=1.0, ell=0.1, k_ell=1e-6, regime="3d")
+        ops = pf.UnstructuredOperators(mesh, mat, "AT1")
+        V, T = mesh.n_vertices, mesh.n_elements
+        del mesh
+        g = torch.Generator(device="cuda").manual_seed(n + dim)
+        alpha = torch.rand(V, dtype=torch.float64, device="cuda", generator=g)
+        x = torch.randn(dim * V, dtype=torch.float64, device="cuda", generator=g)
+        u = torch.randn(dim * V, dtype=torch.float64, device="cuda", generator=g)
+        xa = torch.randn(V, dtype=torch.float64, device="cuda", generator=g)
+        y = torch.empty_like(x)
+        ya = torch.empty_like(xa)
+        table = T * ((64 if dim == 2 else 128) + 16) + 4.0 * (V + 1) + 4.0 * (dim + 1) * T
+        for name, fn, nbytes, dofs in (
+                ("Kuu", lambda: ops.apply_Kuu(alpha, x, out=y), (16.0 * dim + 8.0) * V + table, dim * V),
+                ("Kaa", lambda: ops.apply_Kaa(u, alpha, xa, out=ya), (8.0 * dim + 16.0) * V + table, V)):
+            fn()
+            times = []
+            for _ in range(reps):
+                flush.add_(1.0)
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record()
+                fn()
+                e1.record()
+                torch.cuda.synchronize()
+                times.append(e0.elapsed_time(e1) * 1e-3)
+            t = sorted(times)[len(times) // 2]
+            res.append({"op": name, "mesh": f"{n}^{dim} jittered {'union_jack' if dim == 2 else 'kuhn6'}",
+                        "dofs": dofs, "elements": T, "median_s": t, "GDOF_s": round(dofs / t / 1e9, 3),
+                        "GB_s": round(nbytes / t / 1e9, 1), "frac": round(nbytes / t / 1e9 / peak, 3),
+                        "bytes_per_dof": round(nbytes / dofs, 2), "l2": "flushed"})
+        del ops, alpha, x, u, xa, y, ya
+        gc.collect()
+        torch.cuda.empty_cache()
+    return res
+
+
 def run_steps(pf, torch, setup, cfg, state, steps, flush, host_io=False):
     """Run schedule steps; returns (seconds per step list, records, h2d, d2h bytes)."""
     times, recs = [], []
@@ -496,6 +551,7 @@ def main():
         prob.call("pf_profile", 0)
 
     sweep = operator_sweep(pf, torch, peak) if (not args.no_sweep and rank == 0) else None
+    usweep = umesh_sweep(pf, torch, peak) if (not args.no_sweep and rank == 0) else None
     cpu = None
     if rank == 0 and world == 1:
         v, desc, detail = cpu_sample(args.workload, range(W), timed if args.workload in ("traction1", "surfing")
@@ -521,7 +577,8 @@ def main():
                                        "GB_s": round(v["bytes"] / max(v["ms"], 1e-9) / 1e6, 1)}
                                    for k, v in prof.items()},
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
-                "clocks": clocks, "operator_sweep": sweep}
+                "clocks": clocks, "operator_sweep": sweep,
+                "operator_sweep_unstructured": usweep}
         print(json.dumps(line))
     if dist:
         dist.barrier()

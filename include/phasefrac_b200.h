@@ -223,6 +223,48 @@ int64_t pf_launch_count(const pf_ctx* ctx);
 int pf_profile(pf_ctx* ctx, int32_t enable);
 int pf_profile_read(pf_ctx* ctx, double* out, int32_t nkinds);
 
+/* ---- Element-list (unstructured / jittered) P1 meshes -------------------
+ * The reference builds its thermal-shock mesh by jittering the interior vertices of a
+ * structured triangulation (mesh.py:112-142, cases.py:195-234); geometry is then no longer
+ * implicit.  pf_umesh holds an arbitrary positively oriented triangle (dim 2) or tetrahedron
+ * (dim 3) mesh as element lists and applies the same centroid-quadrature operators as the
+ * structured context (fem.py:221-276 assemble_* matvecs).  Vertex numbering is the caller's; u
+ * is interleaved per vertex.  Mesh arrays in the descriptor are HOST arrays, read only during
+ * pf_umesh_create (which validates orientation: PF_EINVAL "mesh contains non-CCW or degenerate
+ * triangles", as Discretization construction raises, fem.py:107-123). */
+typedef struct pf_umesh_desc {
+    int32_t dim;               /* 2 or 3 */
+    int32_t regime;            /* PF_PLANE_STRESS | PF_PLANE_STRAIN (dim 2) | PF_3D (dim 3) */
+    int32_t model;             /* PF_AT1 | PF_AT2 */
+    int32_t reserved;
+    int64_t n_vertices, n_elements;
+    const double* vertices;    /* host (n_vertices, dim) */
+    const int64_t* elements;   /* host (n_elements, dim+1) */
+    const double* E_elem;      /* host (n_elements) or NULL -> E */
+    const double* Gc_elem;     /* host (n_elements) or NULL -> Gc */
+    double E, nu, Gc, ell, k_ell;
+} pf_umesh_desc;
+
+typedef struct pf_umesh pf_umesh;
+
+int pf_umesh_create(const pf_umesh_desc* desc, pf_umesh** out);
+void pf_umesh_destroy(pf_umesh* m);
+const char* pf_umesh_last_error(const pf_umesh* m);  /* m may be NULL (creation errors) */
+int64_t pf_umesh_workspace_bytes(const pf_umesh* m);
+/* Uploads the element records and vertex->element lists into the (256 B aligned, caller-owned)
+ * device workspace; synchronises the stream. */
+int pf_umesh_bind_workspace(pf_umesh* m, void* dev_ptr, int64_t bytes, void* stream);
+/* Dirichlet dofs (host, interleaved dof indices) for PF_BC_ELIMINATE applies (fem.py:297-310). */
+int pf_umesh_set_dirichlet(pf_umesh* m, const int64_t* dofs, int64_t n, void* stream);
+/* y = Kuu(alpha) x (assemble_Kuu(...).matvec, fem.py:233-244); PF_BC_ELIMINATE: Dirichlet
+ * rows/cols replaced by the identity. */
+int pf_umesh_apply_Kuu(pf_umesh* m, const double* alpha, const double* x, double* y, int32_t bc_mode,
+                       void* stream);
+/* y = Kaa(u, alpha) x (assemble_Kaa(...).matvec, fem.py:266-282). */
+int pf_umesh_apply_Kaa(pf_umesh* m, const double* u, const double* alpha, const double* x, double* y,
+                       void* stream);
+int64_t pf_umesh_launch_count(const pf_umesh* m);
+
 #ifdef __cplusplus
 }
 #endif

@@ -186,3 +186,32 @@ def kuhn_mesh(nx: int, ny: int, nz: int, lx: float = 1.0, ly: float = 1.0,
 def kuhn_paths():
     """The 6 axis orders (x=0, y=1, z=2) defining the Kuhn tetrahedra, in storage order."""
     return list(permutations((0, 1, 2)))
+
+
+def jitter_interior(mesh: SimplexMesh, jitter: float, seed: int = 0) -> SimplexMesh:
+    """Move every interior vertex by a seeded uniform offset of up to ``jitter`` cell sizes per
+    axis (the reference's rect_mesh jitter, mesh.py:127-141: ``default_rng(seed).uniform(-j, j,
+    (n_interior, d)) * h`` on the strictly interior vertices in index order).  Connectivity is
+    unchanged; a non-positive element raises as the reference's _validate_orientation
+    (mesh.py:66-75).  Applies in 3D too (the reference's jitter is 2D only)."""
+    if not 0.0 <= jitter <= 0.4:
+        raise ValueError(f"jitter must lie in [0, 0.4]; got {jitter}")
+    v = mesh.vertices.copy()
+    lo = np.asarray(mesh.origin, float)
+    hi = lo + np.asarray(mesh.extent, float)
+    h = np.asarray(mesh.extent, float) / np.asarray(mesh.shape, float)
+    interior = np.all((v > lo) & (v < hi), axis=1)
+    if jitter > 0.0:
+        rng = np.random.default_rng(seed)
+        v[interior] += rng.uniform(-jitter, jitter, size=(int(interior.sum()), v.shape[1])) * h
+    out = SimplexMesh(v, mesh.elements.copy(), mesh.pattern, mesh.shape, mesh.extent, mesh.origin,
+                      dict(mesh.boundary))
+    P = v[out.elements]
+    if out.dim == 2:
+        det = ((P[:, 1, 0] - P[:, 0, 0]) * (P[:, 2, 1] - P[:, 0, 1])
+               - (P[:, 1, 1] - P[:, 0, 1]) * (P[:, 2, 0] - P[:, 0, 0]))
+    else:
+        det = np.einsum("ti,ti->t", np.cross(P[:, 1] - P[:, 0], P[:, 2] - P[:, 0]), P[:, 3] - P[:, 0])
+    if np.any(det <= 0):
+        raise ValueError(f"mesh has {int(np.sum(det <= 0))} non-CCW/degenerate elements")
+    return out

@@ -26,5 +26,7 @@ from .solver import (NonlinearReport, SolverConfig, am_solve, coupled_newton_sol
 from .cases import (ProblemSetup, StepFailureError, StepRecord, run_quasistatic,  # noqa: F401
                     setup_sent, setup_surfing, setup_thermal_slab, setup_traction,
                     setup_traction3d, surfing_displacement)
+from .umesh import (UnstructuredMesh, UnstructuredOperators, jittered_box_mesh,  # noqa: F401
+                    jittered_rect_mesh)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -94,6 +94,16 @@ EXPORTS = {
     "pf_launch_count": (C.c_int64, [C.c_void_p]),
     "pf_profile": (C.c_int, [C.c_void_p, C.c_int32]),
     "pf_profile_read": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
+    # element-list meshes (umesh.py)
+    "pf_umesh_create": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
+    "pf_umesh_destroy": (None, [C.c_void_p]),
+    "pf_umesh_last_error": (C.c_char_p, [C.c_void_p]),
+    "pf_umesh_workspace_bytes": (C.c_int64, [C.c_void_p]),
+    "pf_umesh_bind_workspace": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
+    "pf_umesh_set_dirichlet": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
+    "pf_umesh_apply_Kuu": (C.c_int, [C.c_void_p] * 4 + [C.c_int32, C.c_void_p]),
+    "pf_umesh_apply_Kaa": (C.c_int, [C.c_void_p] * 5 + [C.c_void_p]),
+    "pf_umesh_launch_count": (C.c_int64, [C.c_void_p]),
 }
 KERNEL_KINDS = ["Kuu", "Kuu_cg", "Kuu_diag", "kappa", "Kaa", "Kaa_cg", "Kaa_diag", "Kaa_trial",
                 "physics", "rhs", "Kua", "Kau", "jacobian", "cg_vec", "vec", "gmg_cycle", "gmg_setup"]

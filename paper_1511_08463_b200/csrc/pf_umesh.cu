@@ -1,0 +1,549 @@
+// pf_umesh.cu -- element-list (unstructured / jittered) P1 operator applies, 2D triangles and
+// 3D tetrahedra (first step).
+//
+// The structured engines (pf_ops2d.cu, pf_ops3d.cu) keep the geometry implicit.  A mesh whose
+// vertices move (the reference's jittered rect_mesh, mesh.py:134-141, used by the thermal-shock
+// case, cases.py:195-234) or whose connectivity is arbitrary needs element lists.  This file
+// applies the same centroid-quadrature P1 operators (fem.py:221-276; oracle/p1.py Kuu, Kaa) on
+// such a mesh:
+//
+//   Kuu x   = sum_e A(ab_e) |T_e| E_e  B_e^T D1 B_e x_e                          (bc: eliminate)
+//   Kaa x   = sum_e [ (A''(ab) q_e/2 + Gc_e w''(ab)/(c_w ell)) |T_e|/npe^2 11^T
+//                     + 2 Gc_e ell/c_w |T_e| G_e^T G_e ] x_e,   q_e = E_e eps(u)^T D1 eps(u)
+//
+// Design (B200, fp64, HBM-bound):
+//  * one thread per VERTEX gathers over its incident elements (vertex->element CSR built on the
+//    host, element index ascending): no atomics, bitwise-reproducible sums, every row written
+//    once with one coalesced store;
+//  * per element one 64 B (2D) / 128 B (3D) record {gradients, |T| E_e, |T| Gc_e}, precomputed
+//    at bind time in fp64 (the vertex coordinates are not needed on the device afterwards);
+//  * connectivity as int4 (16 B), vertex-sorted mesh => the three/four gathers of an element
+//    by its vertices' threads hit L2; compulsory HBM traffic per vertex is the roofline
+//    (x, y, alpha, (u), element records, connectivity, CSR).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/phasefrac_b200.h"
+
+struct pf_umesh {
+    int dim = 2, regime = 0, model = 0;
+    int64_t nv = 0, nt = 0, nadj = 0;
+    double E = 1, nu = 0.3, Gc = 1, ell = 0.1, k_ell = 1e-6;
+    std::string err;
+    // host staging until bind
+    std::vector<double> h_rec;
+    std::vector<int32_t> h_conn, h_rowptr, h_adj;
+    // device (inside the bound workspace)
+    double* rec = nullptr;
+    int32_t* conn = nullptr;
+    int32_t* rowptr = nullptr;
+    int32_t* adj = nullptr;
+    uint8_t* vmask = nullptr;  // per vertex: bit c = Dirichlet on component c
+    bool bound = false, has_bc = false;
+    int64_t launches = 0;
+};
+
+namespace {
+
+thread_local std::string g_create_err;  // creation errors have no mesh object to carry them
+
+constexpr int REC2 = 8, REC3 = 16;  // doubles per element record
+
+inline int64_t align256(int64_t b) { return (b + 255) & ~int64_t(255); }
+
+struct UParams {
+    double d11, d12, d33;  // 2D unit stiffness
+    double lam, mu;        // 3D unit stiffness
+    double k_ell, inv_cw, ell, inv_ell;
+    int at2;
+};
+
+UParams make_params(const pf_umesh* m) {
+    UParams p{};
+    const double nu = m->nu;
+    if (m->regime == PF_PLANE_STRESS) {
+        const double s = 1.0 / (1.0 - nu * nu);
+        p.d11 = s; p.d12 = s * nu; p.d33 = s * 0.5 * (1.0 - nu);
+    } else {
+        const double s = 1.0 / ((1.0 + nu) * (1.0 - 2.0 * nu));
+        p.d11 = s * (1.0 - nu); p.d12 = s * nu; p.d33 = s * 0.5 * (1.0 - 2.0 * nu);
+    }
+    p.lam = nu / ((1.0 + nu) * (1.0 - 2.0 * nu));
+    p.mu = 1.0 / (2.0 * (1.0 + nu));
+    p.k_ell = m->k_ell;
+    p.inv_cw = m->model == PF_AT1 ? 3.0 / 8.0 : 0.5;
+    p.ell = m->ell;
+    p.inv_ell = 1.0 / m->ell;
+    p.at2 = m->model == PF_AT2;
+    return p;
+}
+
+// ---- 2D ------------------------------------------------------------------------------------
+struct Rec2 { double gx[3], gy[3], volE, volGc; };
+
+__device__ __forceinline__ Rec2 load_rec2(const double* __restrict__ rec, int e) {
+    const double2* r = reinterpret_cast<const double2*>(rec + (size_t)e * REC2);
+    double2 a = __ldg(r), b = __ldg(r + 1), c = __ldg(r + 2), d = __ldg(r + 3);
+    Rec2 o;
+    o.gx[0] = a.x; o.gx[1] = a.y; o.gx[2] = b.x;
+    o.gy[0] = b.y; o.gy[1] = c.x; o.gy[2] = c.y;
+    o.volE = d.x; o.volGc = d.y;
+    return o;
+}
+
+__device__ __forceinline__ void strain2(const Rec2& r, const double2 (&x)[3], double (&eps)[3]) {
+    eps[0] = r.gx[0] * x[0].x + r.gx[1] * x[1].x + r.gx[2] * x[2].x;
+    eps[1] = r.gy[0] * x[0].y + r.gy[1] * x[1].y + r.gy[2] * x[2].y;
+    eps[2] = r.gy[0] * x[0].x + r.gy[1] * x[1].x + r.gy[2] * x[2].x
+           + r.gx[0] * x[0].y + r.gx[1] * x[1].y + r.gx[2] * x[2].y;
+}
+
+__global__ void __launch_bounds__(256) k_umesh_Kuu2(
+    const double* __restrict__ rec, const int4* __restrict__ conn, const int32_t* __restrict__ rowptr,
+    const int32_t* __restrict__ adj, const uint8_t* __restrict__ vmask, const double* __restrict__ alpha,
+    const double2* __restrict__ x, double2* __restrict__ y, int64_t nv, UParams p) {
+    const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= nv) return;
+    const uint8_t mv = vmask ? vmask[v] : 0;
+    double y0 = 0.0, y1 = 0.0;
+    const int k0 = rowptr[v], k1 = rowptr[v + 1];
+    for (int k = k0; k < k1; ++k) {
+        const int ent = __ldg(adj + k);
+        const int e = ent >> 2, li = ent & 3;
+        const int4 c = __ldg(conn + e);
+        const int vs[3] = {c.x, c.y, c.z};
+        const Rec2 r = load_rec2(rec, e);
+        double2 xe[3];
+        double ab = 0.0;
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            xe[j] = __ldg(x + vs[j]);
+            ab += __ldg(alpha + vs[j]);
+            if (vmask) {
+                const uint8_t mj = __ldg(vmask + vs[j]);
+                if (mj & 1) xe[j].x = 0.0;
+                if (mj & 2) xe[j].y = 0.0;
+            }
+        }
+        ab *= (1.0 / 3.0);
+        const double om = 1.0 - ab;
+        const double w = (om * om + p.k_ell) * r.volE;
+        double eps[3];
+        strain2(r, xe, eps);
+        const double s0 = w * (p.d11 * eps[0] + p.d12 * eps[1]);
+        const double s1 = w * (p.d12 * eps[0] + p.d11 * eps[1]);
+        const double s2 = w * (p.d33 * eps[2]);
+        const double gxi = li == 0 ? r.gx[0] : (li == 1 ? r.gx[1] : r.gx[2]);
+        const double gyi = li == 0 ? r.gy[0] : (li == 1 ? r.gy[1] : r.gy[2]);
+        y0 += gxi * s0 + gyi * s2;
+        y1 += gyi * s1 + gxi * s2;
+    }
+    if (mv) {
+        const double2 xv = x[v];
+        if (mv & 1) y0 = xv.x;
+        if (mv & 2) y1 = xv.y;
+    }
+    y[v] = make_double2(y0, y1);
+}
+
+__global__ void __launch_bounds__(256) k_umesh_Kaa2(
+    const double* __restrict__ rec, const int4* __restrict__ conn, const int32_t* __restrict__ rowptr,
+    const int32_t* __restrict__ adj, const double2* __restrict__ u,
+    const double* __restrict__ x, double* __restrict__ y, int64_t nv, UParams p) {
+    const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= nv) return;
+    double acc = 0.0;
+    const int k0 = rowptr[v], k1 = rowptr[v + 1];
+    for (int k = k0; k < k1; ++k) {
+        const int ent = __ldg(adj + k);
+        const int e = ent >> 2, li = ent & 3;
+        const int4 c = __ldg(conn + e);
+        const int vs[3] = {c.x, c.y, c.z};
+        const Rec2 r = load_rec2(rec, e);
+        double2 ue[3];
+        double sx = 0.0, gxa = 0.0, gya = 0.0;  // A''(ab) = 2 and w''(ab) are constants
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            ue[j] = __ldg(u + vs[j]);
+            const double xj = __ldg(x + vs[j]);
+            sx += xj;
+            gxa += r.gx[j] * xj;
+            gya += r.gy[j] * xj;
+        }
+        double eps[3];
+        strain2(r, ue, eps);
+        const double q = eps[0] * (p.d11 * eps[0] + p.d12 * eps[1])
+                       + eps[1] * (p.d12 * eps[0] + p.d11 * eps[1]) + p.d33 * eps[2] * eps[2];
+        const double wpp = p.at2 ? 2.0 : 0.0;
+        const double kc = r.volGc * p.inv_cw;  // |T| Gc_e / c_w
+        const double react = (q * r.volE + kc * wpp * p.inv_ell) * (1.0 / 9.0);  // A''/2 = 1
+        const double gxi = li == 0 ? r.gx[0] : (li == 1 ? r.gx[1] : r.gx[2]);
+        const double gyi = li == 0 ? r.gy[0] : (li == 1 ? r.gy[1] : r.gy[2]);
+        acc += react * sx + 2.0 * kc * p.ell * (gxi * gxa + gyi * gya);
+    }
+    y[v] = acc;
+}
+
+// ---- 3D ------------------------------------------------------------------------------------
+struct Rec3 { double g[3][4]; double volE, volGc; };
+
+__device__ __forceinline__ Rec3 load_rec3(const double* __restrict__ rec, int e) {
+    const double2* r = reinterpret_cast<const double2*>(rec + (size_t)e * REC3);
+    Rec3 o;
+    double t[14];
+#pragma unroll
+    for (int i = 0; i < 7; ++i) {
+        const double2 a = __ldg(r + i);
+        t[2 * i] = a.x;
+        t[2 * i + 1] = a.y;
+    }
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) o.g[d][j] = t[4 * d + j];
+    o.volE = t[12];
+    o.volGc = t[13];
+    return o;
+}
+
+// Voigt (e11, e22, e33, g23, g13, g12), engineering shears (oracle/p1.py voigt_B)
+__device__ __forceinline__ void strain3(const Rec3& r, const double (&x)[4][3], double (&eps)[6]) {
+#pragma unroll
+    for (int i = 0; i < 6; ++i) eps[i] = 0.0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const double gx = r.g[0][j], gy = r.g[1][j], gz = r.g[2][j];
+        eps[0] += gx * x[j][0];
+        eps[1] += gy * x[j][1];
+        eps[2] += gz * x[j][2];
+        eps[3] += gz * x[j][1] + gy * x[j][2];
+        eps[4] += gz * x[j][0] + gx * x[j][2];
+        eps[5] += gy * x[j][0] + gx * x[j][1];
+    }
+}
+
+__device__ __forceinline__ void stress3(const UParams& p, const double (&e)[6], double (&s)[6]) {
+    const double tr = p.lam * (e[0] + e[1] + e[2]);
+    s[0] = tr + 2.0 * p.mu * e[0];
+    s[1] = tr + 2.0 * p.mu * e[1];
+    s[2] = tr + 2.0 * p.mu * e[2];
+    s[3] = p.mu * e[3];
+    s[4] = p.mu * e[4];
+    s[5] = p.mu * e[5];
+}
+
+__device__ __forceinline__ double pick4(const double (&a)[4], int i) {
+    return i == 0 ? a[0] : (i == 1 ? a[1] : (i == 2 ? a[2] : a[3]));
+}
+
+__global__ void __launch_bounds__(256) k_umesh_Kuu3(
+    const double* __restrict__ rec, const int4* __restrict__ conn, const int32_t* __restrict__ rowptr,
+    const int32_t* __restrict__ adj, const uint8_t* __restrict__ vmask, const double* __restrict__ alpha,
+    const double* __restrict__ x, double* __restrict__ y, int64_t nv, UParams p) {
+    const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= nv) return;
+    double y0 = 0.0, y1 = 0.0, y2 = 0.0;
+    const int k0 = rowptr[v], k1 = rowptr[v + 1];
+    for (int k = k0; k < k1; ++k) {
+        const int ent = __ldg(adj + k);
+        const int e = ent >> 2, li = ent & 3;
+        const int4 c = __ldg(conn + e);
+        const int vs[4] = {c.x, c.y, c.z, c.w};
+        const Rec3 r = load_rec3(rec, e);
+        double xe[4][3];
+        double ab = 0.0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint8_t mj = vmask ? __ldg(vmask + vs[j]) : 0;
+#pragma unroll
+            for (int d = 0; d < 3; ++d) xe[j][d] = (mj >> d) & 1 ? 0.0 : __ldg(x + 3 * (int64_t)vs[j] + d);
+            ab += __ldg(alpha + vs[j]);
+        }
+        ab *= 0.25;
+        const double om = 1.0 - ab;
+        const double w = (om * om + p.k_ell) * r.volE;
+        double eps[6], s[6];
+        strain3(r, xe, eps);
+        stress3(p, eps, s);
+        const double gx = pick4(r.g[0], li), gy = pick4(r.g[1], li), gz = pick4(r.g[2], li);
+        y0 += w * (gx * s[0] + gz * s[4] + gy * s[5]);
+        y1 += w * (gy * s[1] + gz * s[3] + gx * s[5]);
+        y2 += w * (gz * s[2] + gy * s[3] + gx * s[4]);
+    }
+    const uint8_t mv = vmask ? vmask[v] : 0;
+    if (mv & 1) y0 = x[3 * v];
+    if (mv & 2) y1 = x[3 * v + 1];
+    if (mv & 4) y2 = x[3 * v + 2];
+    y[3 * v] = y0;
+    y[3 * v + 1] = y1;
+    y[3 * v + 2] = y2;
+}
+
+__global__ void __launch_bounds__(256) k_umesh_Kaa3(
+    const double* __restrict__ rec, const int4* __restrict__ conn, const int32_t* __restrict__ rowptr,
+    const int32_t* __restrict__ adj, const double* __restrict__ u,
+    const double* __restrict__ x, double* __restrict__ y, int64_t nv, UParams p) {
+    const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= nv) return;
+    double acc = 0.0;
+    const int k0 = rowptr[v], k1 = rowptr[v + 1];
+    for (int k = k0; k < k1; ++k) {
+        const int ent = __ldg(adj + k);
+        const int e = ent >> 2, li = ent & 3;
+        const int4 c = __ldg(conn + e);
+        const int vs[4] = {c.x, c.y, c.z, c.w};
+        const Rec3 r = load_rec3(rec, e);
+        double ue[4][3];
+        double sx = 0.0, ga[3] = {0.0, 0.0, 0.0};  // A'' = 2 and w'' are constants
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+#pragma unroll
+            for (int d = 0; d < 3; ++d) ue[j][d] = __ldg(u + 3 * (int64_t)vs[j] + d);
+            const double xj = __ldg(x + vs[j]);
+            sx += xj;
+#pragma unroll
+            for (int d = 0; d < 3; ++d) ga[d] += r.g[d][j] * xj;
+        }
+        double eps[6], s[6];
+        strain3(r, ue, eps);
+        stress3(p, eps, s);
+        double q = 0.0;
+#pragma unroll
+        for (int i = 0; i < 6; ++i) q += eps[i] * s[i];
+        const double wpp = p.at2 ? 2.0 : 0.0;
+        const double kc = r.volGc * p.inv_cw;
+        const double react = (q * r.volE + kc * wpp * p.inv_ell) * (1.0 / 16.0);
+        const double gi0 = pick4(r.g[0], li), gi1 = pick4(r.g[1], li), gi2 = pick4(r.g[2], li);
+        acc += react * sx + 2.0 * kc * p.ell * (gi0 * ga[0] + gi1 * ga[1] + gi2 * ga[2]);
+    }
+    y[v] = acc;
+}
+
+int fail(pf_umesh* m, int code, const std::string& msg) {
+    if (m) m->err = msg;
+    return code;
+}
+
+int cuda_fail(pf_umesh* m, cudaError_t e) {
+    return fail(m, PF_ECUDA, std::string("CUDA: ") + cudaGetErrorString(e));
+}
+
+// element geometry: |T| and the P1 basis gradients (fem.py:107-123; oracle/p1.py
+// simplex_gradients).  Returns false on a non-positive orientation.
+bool geom2(const double* P, const int64_t* el, double* out, double E, double Gc) {
+    const double* p1 = P + 2 * el[0];
+    const double* p2 = P + 2 * el[1];
+    const double* p3 = P + 2 * el[2];
+    const double det = (p2[0] - p1[0]) * (p3[1] - p1[1]) - (p2[1] - p1[1]) * (p3[0] - p1[0]);
+    if (!(det > 0.0)) return false;
+    out[0] = (p2[1] - p3[1]) / det;
+    out[1] = (p3[1] - p1[1]) / det;
+    out[2] = (p1[1] - p2[1]) / det;
+    out[3] = (p3[0] - p2[0]) / det;
+    out[4] = (p1[0] - p3[0]) / det;
+    out[5] = (p2[0] - p1[0]) / det;
+    out[6] = 0.5 * det * E;
+    out[7] = 0.5 * det * Gc;
+    return true;
+}
+
+bool geom3(const double* P, const int64_t* el, double* out, double E, double Gc) {
+    const double* p0 = P + 3 * el[0];
+    double J[3][3];  // columns p_{c+1} - p0
+    for (int c = 0; c < 3; ++c)
+        for (int r = 0; r < 3; ++r) J[r][c] = P[3 * el[c + 1] + r] - p0[r];
+    const double det = J[0][0] * (J[1][1] * J[2][2] - J[1][2] * J[2][1])
+                     - J[0][1] * (J[1][0] * J[2][2] - J[1][2] * J[2][0])
+                     + J[0][2] * (J[1][0] * J[2][1] - J[1][1] * J[2][0]);
+    if (!(det > 0.0)) return false;
+    // inv(J) by cofactors; row r of inv(J) = grad lambda_{r+1}
+    double inv[3][3];
+    inv[0][0] = (J[1][1] * J[2][2] - J[1][2] * J[2][1]) / det;
+    inv[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) / det;
+    inv[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) / det;
+    inv[1][0] = (J[1][2] * J[2][0] - J[1][0] * J[2][2]) / det;
+    inv[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) / det;
+    inv[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) / det;
+    inv[2][0] = (J[1][0] * J[2][1] - J[1][1] * J[2][0]) / det;
+    inv[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) / det;
+    inv[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) / det;
+    for (int d = 0; d < 3; ++d) {
+        double s = 0.0;
+        for (int j = 1; j < 4; ++j) {
+            out[4 * d + j] = inv[j - 1][d];
+            s += inv[j - 1][d];
+        }
+        out[4 * d] = -s;
+    }
+    out[12] = det / 6.0 * E;
+    out[13] = det / 6.0 * Gc;
+    out[14] = out[15] = 0.0;
+    return true;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pf_umesh_create(const pf_umesh_desc* d, pf_umesh** out) {
+    if (!out) return PF_EINVAL;
+    *out = nullptr;
+    auto bad = [](const std::string& msg) { g_create_err = msg; return PF_EINVAL; };
+    if (!d) return bad("pf_umesh_create: NULL descriptor");
+    if (d->dim != 2 && d->dim != 3) return bad("pf_umesh_create: dim must be 2 or 3");
+    if ((d->dim == 3) != (d->regime == PF_3D) || d->regime < 0 || d->regime > 2)
+        return bad("pf_umesh_create: regime does not match dim");
+    if (d->model != PF_AT1 && d->model != PF_AT2) return bad("pf_umesh_create: model must be AT1 or AT2");
+    if (d->n_vertices < 1 || d->n_elements < 1 || !d->vertices || !d->elements)
+        return bad("pf_umesh_create: empty mesh");
+    if (d->n_vertices >= (int64_t(1) << 31) / 3 || d->n_elements >= (int64_t(1) << 29))
+        return bad("pf_umesh_create: mesh too large for 32-bit element lists");
+    if (!(d->E > 0) || !(d->Gc > 0) || !(d->ell > 0) || !(d->nu > -1.0 && d->nu < 0.5))
+        return bad("pf_umesh_create: invalid material");
+    const int dim = d->dim, npe = dim + 1, R = dim == 2 ? REC2 : REC3;
+    const int64_t nv = d->n_vertices, nt = d->n_elements;
+    auto* m = new pf_umesh();
+    m->dim = dim; m->regime = d->regime; m->model = d->model;
+    m->nv = nv; m->nt = nt;
+    m->E = d->E; m->nu = d->nu; m->Gc = d->Gc; m->ell = d->ell; m->k_ell = d->k_ell;
+    m->h_rec.assign((size_t)nt * R, 0.0);
+    m->h_conn.assign((size_t)nt * 4, 0);
+    m->h_rowptr.assign((size_t)nv + 1, 0);
+    for (int64_t e = 0; e < nt; ++e) {
+        const int64_t* el = d->elements + e * npe;
+        for (int j = 0; j < npe; ++j) {
+            if (el[j] < 0 || el[j] >= nv) {
+                delete m;
+                return bad("pf_umesh_create: element vertex index out of range");
+            }
+            m->h_conn[4 * e + j] = (int32_t)el[j];
+            m->h_rowptr[el[j] + 1]++;
+        }
+        const double Ee = d->E_elem ? d->E_elem[e] : d->E;
+        const double Ge = d->Gc_elem ? d->Gc_elem[e] : d->Gc;
+        const bool ok = dim == 2 ? geom2(d->vertices, el, &m->h_rec[e * R], Ee, Ge)
+                                 : geom3(d->vertices, el, &m->h_rec[e * R], Ee, Ge);
+        if (!ok) {
+            delete m;
+            return bad(dim == 2 ? "mesh contains non-CCW or degenerate triangles"
+                                : "mesh contains inverted or degenerate tetrahedra");
+        }
+    }
+    for (int64_t v = 0; v < nv; ++v) m->h_rowptr[v + 1] += m->h_rowptr[v];
+    m->nadj = m->h_rowptr[nv];
+    m->h_adj.assign((size_t)m->nadj, 0);
+    std::vector<int32_t> fill(m->h_rowptr.begin(), m->h_rowptr.end() - 1);
+    for (int64_t e = 0; e < nt; ++e)  // element index ascending within each vertex row
+        for (int j = 0; j < npe; ++j) m->h_adj[fill[m->h_conn[4 * e + j]]++] = (int32_t)((e << 2) | j);
+    *out = m;
+    return PF_OK;
+}
+
+void pf_umesh_destroy(pf_umesh* m) { delete m; }
+
+const char* pf_umesh_last_error(const pf_umesh* m) { return m ? m->err.c_str() : g_create_err.c_str(); }
+
+int64_t pf_umesh_workspace_bytes(const pf_umesh* m) {
+    if (!m) return -1;
+    const int R = m->dim == 2 ? REC2 : REC3;
+    return align256(m->nt * R * 8) + align256(m->nt * 16) + align256((m->nv + 1) * 4)
+         + align256(m->nadj * 4) + align256(m->nv);
+}
+
+int pf_umesh_bind_workspace(pf_umesh* m, void* dev, int64_t bytes, void* stream) {
+    if (!m) return PF_EINVAL;
+    if (m->bound) return fail(m, PF_EINVAL, "pf_umesh_bind_workspace: already bound");
+    if (!dev || bytes < pf_umesh_workspace_bytes(m))
+        return fail(m, PF_ENOWS, "pf_umesh_bind_workspace: workspace too small");
+    if (reinterpret_cast<uintptr_t>(dev) % 256)
+        return fail(m, PF_EINVAL, "pf_umesh_bind_workspace: workspace must be 256-byte aligned");
+    const int R = m->dim == 2 ? REC2 : REC3;
+    char* p = static_cast<char*>(dev);
+    m->rec = reinterpret_cast<double*>(p); p += align256(m->nt * R * 8);
+    m->conn = reinterpret_cast<int32_t*>(p); p += align256(m->nt * 16);
+    m->rowptr = reinterpret_cast<int32_t*>(p); p += align256((m->nv + 1) * 4);
+    m->adj = reinterpret_cast<int32_t*>(p); p += align256(m->nadj * 4);
+    m->vmask = reinterpret_cast<uint8_t*>(p);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaError_t e = cudaMemcpyAsync(m->rec, m->h_rec.data(), m->nt * R * 8, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(m->conn, m->h_conn.data(), m->nt * 16, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(m->rowptr, m->h_rowptr.data(), (m->nv + 1) * 4, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(m->adj, m->h_adj.data(), m->nadj * 4, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(m->vmask, 0, m->nv, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(m, e);
+    std::vector<double>().swap(m->h_rec);
+    std::vector<int32_t>().swap(m->h_conn);
+    std::vector<int32_t>().swap(m->h_rowptr);
+    std::vector<int32_t>().swap(m->h_adj);
+    m->bound = true;
+    return PF_OK;
+}
+
+int pf_umesh_set_dirichlet(pf_umesh* m, const int64_t* dofs, int64_t n, void* stream) {
+    if (!m) return PF_EINVAL;
+    if (!m->bound) return fail(m, PF_ENOWS, "pf_umesh_set_dirichlet: no workspace bound");
+    if (n < 0 || (n > 0 && !dofs)) return fail(m, PF_EINVAL, "pf_umesh_set_dirichlet: bad dof list");
+    std::vector<uint8_t> mask((size_t)m->nv, 0);
+    for (int64_t i = 0; i < n; ++i) {
+        if (dofs[i] < 0 || dofs[i] >= m->dim * m->nv)
+            return fail(m, PF_EINVAL, "pf_umesh_set_dirichlet: dof out of range");
+        mask[dofs[i] / m->dim] |= uint8_t(1u << (dofs[i] % m->dim));
+    }
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaError_t e = cudaMemcpyAsync(m->vmask, mask.data(), m->nv, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // host staging dies with this call
+    if (e != cudaSuccess) return cuda_fail(m, e);
+    m->has_bc = n > 0;
+    return PF_OK;
+}
+
+int pf_umesh_apply_Kuu(pf_umesh* m, const double* alpha, const double* x, double* y, int32_t bc_mode,
+                       void* stream) {
+    if (!m) return PF_EINVAL;
+    if (!m->bound) return fail(m, PF_ENOWS, "pf_umesh_apply_Kuu: no workspace bound");
+    if (!alpha || !x || !y || x == y) return fail(m, PF_EINVAL, "pf_umesh_apply_Kuu: bad pointers");
+    const UParams p = make_params(m);
+    const uint8_t* mask = (bc_mode == PF_BC_ELIMINATE && m->has_bc) ? m->vmask : nullptr;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const unsigned grid = (unsigned)((m->nv + 255) / 256);
+    if (m->dim == 2)
+        k_umesh_Kuu2<<<grid, 256, 0, s>>>(m->rec, reinterpret_cast<const int4*>(m->conn), m->rowptr, m->adj,
+                                          mask, alpha, reinterpret_cast<const double2*>(x),
+                                          reinterpret_cast<double2*>(y), m->nv, p);
+    else
+        k_umesh_Kuu3<<<grid, 256, 0, s>>>(m->rec, reinterpret_cast<const int4*>(m->conn), m->rowptr, m->adj,
+                                          mask, alpha, x, y, m->nv, p);
+    m->launches++;
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? PF_OK : cuda_fail(m, e);
+}
+
+int pf_umesh_apply_Kaa(pf_umesh* m, const double* u, const double* alpha, const double* x, double* y,
+                       void* stream) {
+    if (!m) return PF_EINVAL;
+    if (!m->bound) return fail(m, PF_ENOWS, "pf_umesh_apply_Kaa: no workspace bound");
+    if (!u || !alpha || !x || !y || x == y) return fail(m, PF_EINVAL, "pf_umesh_apply_Kaa: bad pointers");
+    const UParams p = make_params(m);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const unsigned grid = (unsigned)((m->nv + 255) / 256);
+    if (m->dim == 2)
+        k_umesh_Kaa2<<<grid, 256, 0, s>>>(m->rec, reinterpret_cast<const int4*>(m->conn), m->rowptr, m->adj,
+                                          reinterpret_cast<const double2*>(u), x, y, m->nv, p);
+    else
+        k_umesh_Kaa3<<<grid, 256, 0, s>>>(m->rec, reinterpret_cast<const int4*>(m->conn), m->rowptr, m->adj,
+                                          u, x, y, m->nv, p);
+    m->launches++;
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? PF_OK : cuda_fail(m, e);
+}
+
+int64_t pf_umesh_launch_count(const pf_umesh* m) { return m ? m->launches : -1; }
+
+}  // extern "C"

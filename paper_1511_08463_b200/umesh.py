@@ -1,0 +1,231 @@
+"""Element-list (unstructured / jittered) P1 meshes on the device (first step).
+
+The structured path (``fem.Discretization``) keeps geometry implicit.  The reference's
+thermal-shock case builds its mesh by jittering the interior vertices of a union-jack grid
+(``rect_mesh(..., jitter, seed)``, mesh.py:112-142; cases.py:195-234), after which every
+element has its own shape.  ``UnstructuredOperators`` holds such a mesh (or any positively
+oriented triangle / tetrahedron mesh) as element lists in a PyTorch-owned device workspace and
+applies the reference's Hessian blocks through the C ABI (``pf_umesh_*``,
+include/phasefrac_b200.h):
+
+* ``apply_Kuu(alpha, x)``  = ``assemble_Kuu(state, problem, apply_bc) @ x``  (fem.py:233-244)
+* ``apply_Kaa(u, alpha, x)`` = ``assemble_Kaa(state, problem) @ x``           (fem.py:266-282)
+
+No CPU fallback: without the CUDA library every call raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from itertools import permutations
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from .model import DamageModel, Material
+
+_REGIME = {"plane_stress": 0, "plane_strain": 1, "3d": 2}
+
+
+@dataclass
+class UnstructuredMesh:
+    """Vertices (V, d) and positively oriented elements (T, d+1); boundary tag -> vertex ids."""
+    vertices: np.ndarray
+    elements: np.ndarray
+    boundary: dict = field(default_factory=dict)
+
+    def __post_init__(self):
+        self.vertices = np.ascontiguousarray(self.vertices, dtype=np.float64)
+        self.elements = np.ascontiguousarray(self.elements, dtype=np.int64)
+        d = self.vertices.shape[1]
+        if d not in (2, 3) or self.elements.ndim != 2 or self.elements.shape[1] != d + 1:
+            raise ValueError("UnstructuredMesh needs (V, 2) + (T, 3) or (V, 3) + (T, 4) arrays")
+
+    @property
+    def dim(self) -> int:
+        return self.vertices.shape[1]
+
+    @property
+    def n_vertices(self) -> int:
+        return self.vertices.shape[0]
+
+    @property
+    def n_elements(self) -> int:
+        return self.elements.shape[0]
+
+
+def _jitter(v, lo, hi, h, jitter, seed):
+    """mesh.py:134-141: seeded uniform offsets of up to ``jitter`` cell sizes on the strictly
+    interior vertices, in vertex-index order."""
+    if not 0.0 <= jitter <= 0.4:
+        raise ValueError(f"jitter must lie in [0, 0.4]; got {jitter}")
+    if jitter > 0.0:
+        interior = np.all((v > lo) & (v < hi), axis=1)
+        rng = np.random.default_rng(seed)
+        v[interior] += rng.uniform(-jitter, jitter, size=(int(interior.sum()), v.shape[1])) * h
+    return v
+
+
+def jittered_rect_mesh(L: float, H: float, h: float, jitter: float = 0.0, seed: int = 0,
+                       origin_x2: float = 0.0) -> UnstructuredMesh:
+    """The reference's ``rect_mesh(L, H, h, origin_x2, jitter, seed)`` (mesh.py:112-142): a
+    union-jack grid (vertex (i, j) = i*(ny+1)+j, triangles as ``_grid`` mesh.py:88-99) whose
+    interior vertices are jittered."""
+    if L <= 0 or H <= 0 or h <= 0:
+        raise ValueError(f"rect_mesh needs positive L, H, h; got L={L}, H={H}, h={h}")
+    nx, ny = max(1, round(L / h)), max(1, round(H / h))
+    xs = np.linspace(0.0, L, nx + 1)
+    ys = np.linspace(origin_x2, origin_x2 + H, ny + 1)
+    X, Y = np.meshgrid(xs, ys, indexing="ij")
+    v = np.column_stack([X.ravel(), Y.ravel()])
+    I, J = (a.ravel() for a in np.meshgrid(np.arange(nx), np.arange(ny), indexing="ij"))
+    v00, v10, v11, v01 = I * (ny + 1) + J, (I + 1) * (ny + 1) + J, (I + 1) * (ny + 1) + J + 1, I * (ny + 1) + J + 1
+    even = ((I + J) % 2 == 0)[:, None]
+    t1 = np.where(even, np.column_stack([v00, v10, v11]), np.column_stack([v00, v10, v01]))
+    t2 = np.where(even, np.column_stack([v00, v11, v01]), np.column_stack([v10, v11, v01]))
+    v = _jitter(v, np.array([xs[0], ys[0]]), np.array([xs[-1], ys[-1]]), np.array([L / nx, H / ny]),
+                jitter, seed)
+    jj, ii = np.arange(ny + 1), np.arange(nx + 1)
+    bnd = {"left": jj, "right": nx * (ny + 1) + jj, "bottom": ii * (ny + 1), "top": ii * (ny + 1) + ny}
+    return UnstructuredMesh(v, np.vstack([t1, t2]), bnd)
+
+
+def jittered_box_mesh(nx: int, ny: int, nz: int, lx: float = 1.0, ly: float = 1.0, lz: float = 1.0,
+                      jitter: float = 0.0, seed: int = 0) -> UnstructuredMesh:
+    """Hex grid split into 6 Kuhn tetrahedra (the structured 3D layout, vertex (i, j, k) =
+    (i*(ny+1)+j)*(nz+1)+k) with the rect_mesh jitter applied to its interior vertices."""
+    xs, ys, zs = (np.linspace(0.0, l, n + 1) for l, n in ((lx, nx), (ly, ny), (lz, nz)))
+    X, Y, Z = np.meshgrid(xs, ys, zs, indexing="ij")
+    v = np.column_stack([X.ravel(), Y.ravel(), Z.ravel()])
+    I, J, K = (a.ravel() for a in np.meshgrid(np.arange(nx), np.arange(ny), np.arange(nz), indexing="ij"))
+
+    def vid(i, j, k):
+        return (i * (ny + 1) + j) * (nz + 1) + k
+
+    blocks = []
+    for perm in permutations((0, 1, 2)):
+        cur, path = [0, 0, 0], [(0, 0, 0)]
+        for ax in perm:
+            cur[ax] = 1
+            path.append(tuple(cur))
+        blocks.append(np.column_stack([vid(I + p[0], J + p[1], K + p[2]) for p in path]))
+    el = np.vstack(blocks)
+    p = v[el]
+    neg = np.einsum("ti,ti->t", np.cross(p[:, 1] - p[:, 0], p[:, 2] - p[:, 0]), p[:, 3] - p[:, 0]) < 0
+    el[neg] = el[neg][:, [0, 2, 1, 3]]
+    v = _jitter(v, np.zeros(3), np.array([lx, ly, lz]), np.array([lx / nx, ly / ny, lz / nz]), jitter, seed)
+    return UnstructuredMesh(v, el)
+
+
+class _UDesc(C.Structure):
+    _fields_ = [("dim", C.c_int32), ("regime", C.c_int32), ("model", C.c_int32), ("reserved", C.c_int32),
+                ("n_vertices", C.c_int64), ("n_elements", C.c_int64),
+                ("vertices", C.c_void_p), ("elements", C.c_void_p), ("E_elem", C.c_void_p),
+                ("Gc_elem", C.c_void_p), ("E", C.c_double), ("nu", C.c_double), ("Gc", C.c_double),
+                ("ell", C.c_double), ("k_ell", C.c_double)]
+
+
+def _raise(code, handle):
+    if code == _lib.PF_OK:
+        return
+    msg = _lib.load().pf_umesh_last_error(handle).decode(errors="replace") or f"status {code}"
+    if code in (_lib.PF_EINVAL, _lib.PF_ENOWS):
+        raise ValueError(msg)
+    raise RuntimeError(f"CUDA failure in libphasefrac_b200: {msg}")
+
+
+class UnstructuredOperators:
+    """Matrix-free Kuu / Kaa on an element-list mesh (the structured ``Discretization``'s
+    operators, fem.py:233-282, for meshes whose geometry is not implicit).
+
+    ``E_elem`` / ``Gc_elem``: optional per-element absolute values (override the scalars)."""
+
+    def __init__(self, mesh: UnstructuredMesh, material: Material,
+                 damage_model: DamageModel | str = "AT1", E_elem=None, Gc_elem=None, device=None):
+        import torch
+
+        if not torch.cuda.is_available():
+            raise RuntimeError("UnstructuredOperators needs a CUDA device (no CPU fallback)")
+        dm = damage_model if isinstance(damage_model, DamageModel) else DamageModel(damage_model)
+        if (mesh.dim == 3) != (material.regime == "3d"):
+            raise ValueError(f"regime {material.regime!r} does not match a {mesh.dim}D mesh")
+        self.mesh, self.material, self.damage_model = mesh, material, dm
+        dev = torch.device(device or "cuda")
+        self.device = dev if dev.index is not None else torch.device("cuda", torch.cuda.current_device())
+        lib = _lib.load()
+        Ee = None if E_elem is None else np.ascontiguousarray(E_elem, dtype=np.float64)
+        Ge = None if Gc_elem is None else np.ascontiguousarray(Gc_elem, dtype=np.float64)
+        for a in (Ee, Ge):
+            if a is not None and a.shape != (mesh.n_elements,):
+                raise ValueError("per-element fields need one value per element")
+        d = _UDesc(mesh.dim, _REGIME[material.regime], 0 if dm.kind == "AT1" else 1, 0,
+                   mesh.n_vertices, mesh.n_elements, mesh.vertices.ctypes.data, mesh.elements.ctypes.data,
+                   None if Ee is None else Ee.ctypes.data, None if Ge is None else Ge.ctypes.data,
+                   material.E, material.nu, material.Gc, material.ell, material.k_ell)
+        h = C.c_void_p()
+        _raise(lib.pf_umesh_create(C.byref(d), C.byref(h)), None)
+        self._h = h
+        nbytes = lib.pf_umesh_workspace_bytes(h)
+        with torch.cuda.device(self.device):
+            self._ws = torch.empty(nbytes + 256, dtype=torch.uint8, device=self.device)
+            base = self._ws.data_ptr()
+            self._check(lib.pf_umesh_bind_workspace(h, C.c_void_p((base + 255) & ~255), nbytes, self._stream()))
+        self.workspace_bytes = int(nbytes)
+
+    # ---- plumbing ---------------------------------------------------------------------------
+    @staticmethod
+    def _stream():
+        import torch
+        return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+    def _check(self, code):
+        _raise(code, self._h)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and _lib._lib is not None:
+            _lib._lib.pf_umesh_destroy(h)
+            self._h = None
+
+    @property
+    def n_vertices(self) -> int:
+        return self.mesh.n_vertices
+
+    @property
+    def n_udofs(self) -> int:
+        return self.mesh.dim * self.mesh.n_vertices
+
+    @property
+    def launches(self) -> int:
+        return int(_lib.load().pf_umesh_launch_count(self._h))
+
+    def _vec(self, t, n, name):
+        import torch
+        if t.device != self.device or t.dtype != torch.float64 or t.numel() != n:
+            raise ValueError(f"{name} must be a float64 tensor of {n} entries on {self.device}")
+        return _lib.ptr(t)
+
+    # ---- API ----------------------------------------------------------------------------------
+    def set_dirichlet(self, dofs) -> None:
+        """Dirichlet dofs (interleaved indices) for ``apply_Kuu(..., apply_bc=True)``."""
+        d = np.ascontiguousarray(np.unique(np.asarray(dofs, dtype=np.int64)))
+        self._check(_lib.load().pf_umesh_set_dirichlet(self._h, d.ctypes.data if d.size else None, d.size,
+                                                        self._stream()))
+
+    def apply_Kuu(self, alpha, x, out=None, apply_bc: bool = False):
+        import torch
+        out = torch.empty_like(x) if out is None else out
+        self._check(_lib.load().pf_umesh_apply_Kuu(
+            self._h, self._vec(alpha, self.n_vertices, "alpha"), self._vec(x, self.n_udofs, "x"),
+            self._vec(out, self.n_udofs, "out"), 1 if apply_bc else 0, self._stream()))
+        return out
+
+    def apply_Kaa(self, u, alpha, x, out=None):
+        import torch
+        out = torch.empty_like(x) if out is None else out
+        self._check(_lib.load().pf_umesh_apply_Kaa(
+            self._h, self._vec(u, self.n_udofs, "u"), self._vec(alpha, self.n_vertices, "alpha"),
+            self._vec(x, self.n_vertices, "x"), self._vec(out, self.n_vertices, "out"), self._stream()))
+        return out

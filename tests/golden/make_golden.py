@@ -243,10 +243,43 @@ def gen_surfing():
     return out
 
 
+def gen_jitter():
+    """Hessian-block products on the reference's JITTERED rect meshes (mesh.py:134-141), the
+    mesh family of its thermal-shock case (cases.py:195-234): pins the element-list path."""
+    out = {}
+    rng = np.random.default_rng(4321)
+    for tag, (L, H, h, jit, seed) in {"jit": (2.0, 1.0, 0.125, 0.25, 0),
+                                      "jit3": (1.0, 0.5, 0.0625, 0.3, 7)}.items():
+        mat = model.Material(E=1.7, nu=0.3, Gc=1.3, ell=0.1, k_ell=1e-6)
+        m = mesh.rect_mesh(L, H, h, jitter=jit, seed=seed)
+        prob = fem.Discretization(m, mat)
+        st = random_state(prob, rng)
+        xu = rng.standard_normal(prob.n_udofs)
+        xa = rng.standard_normal(prob.n_vertices)
+        left = mesh.boundary_dofs(m, "left", "displacement_x1")
+        bottom = mesh.boundary_dofs(m, "bottom", "displacement_x2")
+        prob.bc = fem.combine_bcs(fem.DirichletBC(left, np.zeros(left.size)),
+                                  fem.DirichletBC(bottom, np.zeros(bottom.size)))
+        out.update({
+            f"{tag}_params": np.array([L, H, h, jit, seed, mat.E, mat.nu, mat.Gc, mat.ell, mat.k_ell]),
+            f"{tag}_vertices": m.vertices, f"{tag}_triangles": m.triangles,
+            f"{tag}_u": st.u, f"{tag}_alpha": st.alpha, f"{tag}_xu": xu, f"{tag}_xa": xa,
+            f"{tag}_bc_dofs": prob.bc.dofs,
+            f"{tag}_Kuu_raw_x": fem.assemble_Kuu(st, prob, apply_bc=False) @ xu,
+            f"{tag}_Kuu_bc_x": fem.assemble_Kuu(st, prob, apply_bc=True) @ xu,
+            f"{tag}_Kaa_x": fem.assemble_Kaa(st, prob) @ xa,
+        })
+    return out
+
+
 def main():
     if len(sys.argv) > 1 and sys.argv[1] == "surfing":  # regenerate only the surfing fixture
         np.savez_compressed(os.path.join(OUT, "ref_surfing.npz"), **gen_surfing())
         return
+    if len(sys.argv) > 1 and sys.argv[1] == "jitter":  # regenerate only the jittered-mesh fixture
+        np.savez_compressed(os.path.join(OUT, "ref_jitter.npz"), **gen_jitter())
+        return
+    np.savez_compressed(os.path.join(OUT, "ref_jitter.npz"), **gen_jitter())
     np.savez_compressed(os.path.join(OUT, "ref_surfing.npz"), **gen_surfing())
     np.savez_compressed(os.path.join(OUT, "ref_operators.npz"), **gen_operators())
     np.savez_compressed(os.path.join(OUT, "ref_vi.npz"), **gen_vi())

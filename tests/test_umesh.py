@@ -1,0 +1,199 @@
+"""Element-list (jittered / unstructured) P1 path -- SURVEY 8(f) row 4, first step.
+
+CPU: the oracle's jitter (oracle/meshgen.jitter_interior) and the package's mesh generator
+reproduce the REFERENCE's jittered rect_mesh bit for bit (tests/golden/ref_jitter.npz, made by
+running the reference, make_golden.py gen_jitter); the oracle's assembled Kuu / Kaa products on
+those meshes match the reference's; the C ABI validates meshes without a device.
+GPU: pf_umesh_apply_Kuu / _Kaa against the reference goldens and the oracle's assembled CSR
+(relative max error <= 1e-12), 2D and 3D, AT1/AT2, plane stress/strain, per-element fields,
+Dirichlet elimination, bitwise reproducibility.
+"""
+
+import ctypes as C
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+from oracle.meshgen import grid_mesh, jitter_interior, kuhn_mesh
+from oracle.p1 import MaterialSpec, P1Model, eliminate_rows_cols
+
+TOL = 1e-12
+
+
+def golden():
+    return np.load(os.path.join(GOLDEN, "ref_jitter.npz"))
+
+
+def rel(a, b):
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300))
+
+
+def oracle_model(d, tag):
+    L, H, h, jit, seed, E, nu, Gc, ell, k_ell = d[f"{tag}_params"]
+    m = jitter_interior(grid_mesh(round(L / h), round(H / h), L, H), jit, int(seed))
+    spec = MaterialSpec(E=E, nu=nu, Gc=Gc, ell=ell, k_ell=k_ell, model="AT1", regime="plane_stress")
+    return m, P1Model(m, spec)
+
+
+# ---- CPU -------------------------------------------------------------------------------------
+@pytest.mark.parametrize("tag", ["jit", "jit3"])
+def test_oracle_jitter_is_the_reference_mesh(tag):
+    d = golden()
+    m, _ = oracle_model(d, tag)
+    assert np.array_equal(m.vertices, d[f"{tag}_vertices"])
+    assert np.array_equal(m.elements, d[f"{tag}_triangles"])
+
+
+@pytest.mark.parametrize("tag", ["jit", "jit3"])
+def test_package_jittered_rect_mesh_is_the_reference_mesh(tag):
+    import paper_1511_08463_b200 as pf
+    d = golden()
+    L, H, h, jit, seed = d[f"{tag}_params"][:5]
+    m = pf.jittered_rect_mesh(L, H, h, jitter=jit, seed=int(seed))
+    assert np.array_equal(m.vertices, d[f"{tag}_vertices"])
+    assert np.array_equal(m.elements, d[f"{tag}_triangles"])
+
+
+@pytest.mark.parametrize("tag", ["jit", "jit3"])
+def test_oracle_operators_match_reference_on_jittered_mesh(tag):
+    d = golden()
+    _, om = oracle_model(d, tag)
+    u, a, xu, xa = d[f"{tag}_u"], d[f"{tag}_alpha"], d[f"{tag}_xu"], d[f"{tag}_xa"]
+    assert rel(om.Kuu(a, eliminate=False) @ xu, d[f"{tag}_Kuu_raw_x"]) < TOL
+    K = eliminate_rows_cols(om.Kuu(a, eliminate=False), d[f"{tag}_bc_dofs"])
+    assert rel(K @ xu, d[f"{tag}_Kuu_bc_x"]) < TOL
+    assert rel(om.Kaa(u, a) @ xa, d[f"{tag}_Kaa_x"]) < TOL
+
+
+def test_package_box_mesh_matches_oracle_kuhn():
+    import paper_1511_08463_b200 as pf
+    m = pf.jittered_box_mesh(3, 4, 5, 1.0, 2.0, 1.5, jitter=0.2, seed=5)
+    o = jitter_interior(kuhn_mesh(3, 4, 5, 1.0, 2.0, 1.5), 0.2, 5)
+    assert np.array_equal(m.vertices, o.vertices)
+    assert np.array_equal(m.elements, o.elements)
+
+
+def test_jitter_range_rejected():
+    import paper_1511_08463_b200 as pf
+    with pytest.raises(ValueError, match="jitter"):
+        pf.jittered_rect_mesh(1.0, 1.0, 0.25, jitter=0.5)
+
+
+def _desc(mesh, **kw):
+    from paper_1511_08463_b200.umesh import _UDesc
+    v, el = mesh.vertices, mesh.elements
+    args = dict(dim=mesh.dim, regime=0 if mesh.dim == 2 else 2, model=0, reserved=0,
+                n_vertices=v.shape[0], n_elements=el.shape[0], vertices=v.ctypes.data,
+                elements=el.ctypes.data, E_elem=None, Gc_elem=None, E=1.0, nu=0.3, Gc=1.0,
+                ell=0.1, k_ell=1e-6)
+    args.update(kw)
+    return _UDesc(**args)
+
+
+def test_capi_create_validates_without_device():
+    import paper_1511_08463_b200 as pf
+    from paper_1511_08463_b200 import _lib
+    lib = _lib.load()
+    mesh = pf.jittered_rect_mesh(1.0, 0.5, 0.125, jitter=0.2, seed=1)
+    h = C.c_void_p()
+    assert lib.pf_umesh_create(C.byref(_desc(mesh)), C.byref(h)) == _lib.PF_OK
+    nv, nt = mesh.n_vertices, mesh.n_elements
+    adj = 3 * nt
+    expect = sum((b + 255) // 256 * 256 for b in (nt * 64, nt * 16, (nv + 1) * 4, adj * 4, nv))
+    assert lib.pf_umesh_workspace_bytes(h) == expect
+    lib.pf_umesh_destroy(h)
+    # an inverted triangle, an out-of-range index, a regime/dim mismatch
+    bad = pf.UnstructuredMesh(mesh.vertices, mesh.elements[:, [0, 2, 1]])
+    h = C.c_void_p()
+    assert lib.pf_umesh_create(C.byref(_desc(bad)), C.byref(h)) == _lib.PF_EINVAL
+    assert b"non-CCW" in lib.pf_umesh_last_error(None)
+    oob = pf.UnstructuredMesh(mesh.vertices, np.where(mesh.elements == 3, nv + 7, mesh.elements))
+    assert lib.pf_umesh_create(C.byref(_desc(oob)), C.byref(h)) == _lib.PF_EINVAL
+    assert b"out of range" in lib.pf_umesh_last_error(None)
+    assert lib.pf_umesh_create(C.byref(_desc(mesh, regime=2)), C.byref(h)) == _lib.PF_EINVAL
+    box = pf.jittered_box_mesh(2, 2, 2)
+    flipped = pf.UnstructuredMesh(box.vertices, box.elements[:, [0, 2, 1, 3]])
+    assert lib.pf_umesh_create(C.byref(_desc(flipped)), C.byref(h)) == _lib.PF_EINVAL
+    assert b"inverted" in lib.pf_umesh_last_error(None)
+
+
+# ---- GPU -------------------------------------------------------------------------------------
+def _dev(a):
+    import torch
+    return torch.as_tensor(np.ascontiguousarray(a), dtype=torch.float64, device="cuda")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("tag", ["jit", "jit3"])
+def test_gpu_umesh_matches_reference_goldens(tag):
+    import paper_1511_08463_b200 as pf
+    d = golden()
+    L, H, h, jit, seed, E, nu, Gc, ell, k_ell = d[f"{tag}_params"]
+    mesh = pf.jittered_rect_mesh(L, H, h, jitter=jit, seed=int(seed))
+    ops = pf.UnstructuredOperators(mesh, pf.Material(E=E, nu=nu, Gc=Gc, ell=ell, k_ell=k_ell), "AT1")
+    u, a, xu, xa = (_dev(d[f"{tag}_{k}"]) for k in ("u", "alpha", "xu", "xa"))
+    assert rel(ops.apply_Kuu(a, xu).cpu().numpy(), d[f"{tag}_Kuu_raw_x"]) < TOL
+    assert rel(ops.apply_Kaa(u, a, xa).cpu().numpy(), d[f"{tag}_Kaa_x"]) < TOL
+    ops.set_dirichlet(d[f"{tag}_bc_dofs"])
+    assert rel(ops.apply_Kuu(a, xu, apply_bc=True).cpu().numpy(), d[f"{tag}_Kuu_bc_x"]) < TOL
+    assert ops.launches == 3
+
+
+CASES = [
+    # dim, regime, model, shape, jitter, hetero
+    (2, "plane_strain", "AT2", (40, 23), 0.3, True),
+    (2, "plane_stress", "AT1", (1, 1), 0.0, False),
+    (2, "plane_strain", "AT1", (64, 64), 0.25, False),
+    (3, "3d", "AT1", (5, 4, 6), 0.2, True),
+    (3, "3d", "AT2", (9, 9, 9), 0.25, False),
+    (3, "3d", "AT1", (1, 1, 1), 0.0, False),
+]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", CASES, ids=lambda c: f"{c[0]}d-{c[1]}-{c[2]}-{'x'.join(map(str, c[3]))}")
+def test_gpu_umesh_parity_vs_oracle(case):
+    import torch
+    import paper_1511_08463_b200 as pf
+    dim, regime, model, shape, jit, hetero = case
+    om_mesh = (jitter_interior(grid_mesh(*shape, 2.0, 1.0), jit, 11) if dim == 2
+               else jitter_interior(kuhn_mesh(*shape), jit, 11))
+    rng = np.random.default_rng(sum(shape) + dim)
+    T, V = om_mesh.n_elements, om_mesh.n_vertices
+    Ee = rng.uniform(0.5, 1.5, T) if hetero else None
+    Ge = rng.uniform(0.5, 1.5, T) if hetero else None
+    spec = MaterialSpec(E=1.3, nu=0.3, Gc=0.9, ell=0.07, k_ell=1e-6, model=model, regime=regime)
+    om = P1Model(om_mesh, spec, Ee, Ge)
+    mesh = pf.UnstructuredMesh(om_mesh.vertices, om_mesh.elements)
+    ops = pf.UnstructuredOperators(mesh, pf.Material(E=1.3, nu=0.3, Gc=0.9, ell=0.07, k_ell=1e-6,
+                                                     regime=regime), model, Ee, Ge)
+    a = rng.uniform(0, 1, V)
+    u = rng.standard_normal(dim * V)
+    xu = rng.standard_normal(dim * V)
+    xa = rng.standard_normal(V)
+    y = ops.apply_Kuu(_dev(a), _dev(xu))
+    assert rel(y.cpu().numpy(), om.Kuu(a, eliminate=False) @ xu) < TOL
+    assert rel(ops.apply_Kaa(_dev(u), _dev(a), _dev(xa)).cpu().numpy(), om.Kaa(u, a) @ xa) < TOL
+    bc = np.unique(np.concatenate([dim * om_mesh.boundary[next(iter(om_mesh.boundary))] + c
+                                   for c in range(dim)]))
+    ops.set_dirichlet(bc)
+    yb = ops.apply_Kuu(_dev(a), _dev(xu), apply_bc=True).cpu().numpy()
+    assert rel(yb, eliminate_rows_cols(om.Kuu(a, eliminate=False), bc) @ xu) < TOL
+    # fixed-order gathers: bitwise reproducible
+    y2 = ops.apply_Kuu(_dev(a), _dev(xu))
+    assert torch.equal(y, y2)
+
+
+@pytest.mark.gpu
+def test_gpu_umesh_rejects_bad_arguments():
+    import torch
+    import paper_1511_08463_b200 as pf
+    ops = pf.UnstructuredOperators(pf.jittered_rect_mesh(1.0, 1.0, 0.25, 0.2), pf.Material())
+    with pytest.raises(ValueError, match="float64"):
+        ops.apply_Kuu(torch.zeros(ops.n_vertices, device="cuda"), torch.zeros(ops.n_udofs, device="cuda"))
+    with pytest.raises(ValueError, match="dof out of range"):
+        ops.set_dirichlet([ops.n_udofs])
+    with pytest.raises(ValueError, match="does not match"):
+        pf.UnstructuredOperators(pf.jittered_box_mesh(2, 2, 2), pf.Material())
