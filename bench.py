@@ -385,7 +385,7 @@ UMESH_SWEEP = ((2, 1024), (2, 2048), (2, 4096), (3, 64), (3, 128))
 def umesh_sweep(pf, torch, peak, reps=10):
     """Element-list (jittered) meshes: pf_umesh Kuu / Kaa applies on the
     reference's jittered union-jack rect_mesh (jitter 0.25, mesh.py:134-141) and on jittered
-    Kuhn boxes; same inputs and L2 flush as the structured sweep.  Algorithmic bytes = the
+    Kuhn boxes (jitter 0.1: Kuhn tets invert sooner); same inputs and L2 flush as the structured sweep.  Algorithmic bytes = the
     compulsory footprint of one apply: per vertex x, y, alpha (Kuu) or u, x, y (Kaa) + the vertex
     CSR row pointer; per element its record (64 B 2D / 128 B 3D) + int4 connectivity; per
     (vertex, element) incidence one 4 B entry."""
@@ -396,7 +396,7 @@ def umesh_sweep(pf, torch, peak, reps=10):
             mesh = pf.jittered_rect_mesh(1.0, 1.0, 1.0 / n, jitter=0.25, seed=n)
             mat = pf.Material(E=1.0, nu=0.3, Gc=1.0, ell=0.1, k_ell=1e-6)
         else:
-            mesh = pf.jittered_box_mesh(n, n, n, jitter=0.25, seed=n)
+            mesh = pf.jittered_box_mesh(n, n, n, jitter=0.1, seed=n)
             mat = pf.Material(E=1.0, nu=0.3, Gc=1.0, ell=0.1, k_ell=1e-6, regime="3d")
         ops = pf.UnstructuredOperators(mesh, mat, "AT1")
         V, T = mesh.n_vertices, mesh.n_elements

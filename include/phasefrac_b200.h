@@ -263,6 +263,13 @@ int pf_umesh_apply_Kuu(pf_umesh* m, const double* alpha, const double* x, double
 /* y = Kaa(u, alpha) x (assemble_Kaa(...).matvec, fem.py:266-282). */
 int pf_umesh_apply_Kaa(pf_umesh* m, const double* u, const double* alpha, const double* x, double* y,
                        void* stream);
+/* Solve Kuu(alpha) x = b with Dirichlet rows/cols eliminated (pf_umesh_set_dirichlet) by Jacobi
+ * PCG from x0 = 0 (cg_solve linalg.py:106-152: stop when ||r|| <= max(rtol ||b||, atol), polled
+ * every check_every iterations; maxit <= 0 -> 10 n).  opts->precond must be PF_PREC_JACOBI.
+ * Non-convergence is rep->converged = 0; p^T A p <= 0 is PF_EBREAKDOWN.  Fixed-order reductions:
+ * bitwise-reproducible iterates. */
+int pf_umesh_elastic_solve(pf_umesh* m, const double* alpha, const double* b, double* x,
+                           const pf_lin_opts* opts, pf_lin_report* rep, void* stream);
 int64_t pf_umesh_launch_count(const pf_umesh* m);
 
 #ifdef __cplusplus

@@ -44,6 +44,9 @@ struct pf_umesh {
     int32_t* rowptr = nullptr;
     int32_t* adj = nullptr;
     uint8_t* vmask = nullptr;  // per vertex: bit c = Dirichlet on component c
+    // Jacobi-PCG work vectors (d*nv each) + per-block partials + scalars
+    double *r = nullptr, *z = nullptr, *p = nullptr, *q = nullptr, *dinv = nullptr, *part = nullptr,
+           *scal = nullptr;
     bool bound = false, has_bc = false;
     int64_t launches = 0;
 };
@@ -103,12 +106,33 @@ __device__ __forceinline__ void strain2(const Rec2& r, const double2 (&x)[3], do
            + r.gx[0] * x[0].y + r.gx[1] * x[1].y + r.gx[2] * x[2].y;
 }
 
+// Fixed-order block sum of one value per thread (256 threads) -> part[blockIdx.x].
+__device__ __forceinline__ void block_partial(double v, double* __restrict__ part) {
+    __shared__ double sh[8];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) t += sh[w];
+        part[blockIdx.x] = t;
+    }
+    __syncthreads();  // sh is reused by the next call in the same kernel
+}
+
+template <bool DOT>
 __global__ void __launch_bounds__(256) k_umesh_Kuu2(
     const double* __restrict__ rec, const int4* __restrict__ conn, const int32_t* __restrict__ rowptr,
     const int32_t* __restrict__ adj, const uint8_t* __restrict__ vmask, const double* __restrict__ alpha,
-    const double2* __restrict__ x, double2* __restrict__ y, int64_t nv, UParams p) {
+    const double2* __restrict__ x, double2* __restrict__ y, int64_t nv, UParams p,
+    double* __restrict__ part) {
     const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (v >= nv) return;
+    if (v >= nv) {
+        if (DOT) block_partial(0.0, part);
+        return;
+    }
     const uint8_t mv = vmask ? vmask[v] : 0;
     double y0 = 0.0, y1 = 0.0;
     const int k0 = rowptr[v], k1 = rowptr[v + 1];
@@ -149,6 +173,10 @@ __global__ void __launch_bounds__(256) k_umesh_Kuu2(
         if (mv & 2) y1 = xv.y;
     }
     y[v] = make_double2(y0, y1);
+    if (DOT) {
+        const double2 xv = x[v];
+        block_partial(xv.x * y0 + xv.y * y1, part);
+    }
 }
 
 __global__ void __launch_bounds__(256) k_umesh_Kaa2(
@@ -241,12 +269,16 @@ __device__ __forceinline__ double pick4(const double (&a)[4], int i) {
     return i == 0 ? a[0] : (i == 1 ? a[1] : (i == 2 ? a[2] : a[3]));
 }
 
+template <bool DOT>
 __global__ void __launch_bounds__(256) k_umesh_Kuu3(
     const double* __restrict__ rec, const int4* __restrict__ conn, const int32_t* __restrict__ rowptr,
     const int32_t* __restrict__ adj, const uint8_t* __restrict__ vmask, const double* __restrict__ alpha,
-    const double* __restrict__ x, double* __restrict__ y, int64_t nv, UParams p) {
+    const double* __restrict__ x, double* __restrict__ y, int64_t nv, UParams p, double* __restrict__ part) {
     const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (v >= nv) return;
+    if (v >= nv) {
+        if (DOT) block_partial(0.0, part);
+        return;
+    }
     double y0 = 0.0, y1 = 0.0, y2 = 0.0;
     const int k0 = rowptr[v], k1 = rowptr[v + 1];
     for (int k = k0; k < k1; ++k) {
@@ -282,6 +314,7 @@ __global__ void __launch_bounds__(256) k_umesh_Kuu3(
     y[3 * v] = y0;
     y[3 * v + 1] = y1;
     y[3 * v + 2] = y2;
+    if (DOT) block_partial(x[3 * v] * y0 + x[3 * v + 1] * y1 + x[3 * v + 2] * y2, part);
 }
 
 __global__ void __launch_bounds__(256) k_umesh_Kaa3(
@@ -322,6 +355,107 @@ __global__ void __launch_bounds__(256) k_umesh_Kaa3(
         acc += react * sx + 2.0 * kc * p.ell * (gi0 * ga[0] + gi1 * ga[1] + gi2 * ga[2]);
     }
     y[v] = acc;
+}
+
+// ---- Jacobi PCG (cg_solve, linalg.py:106-152) ---------------------------------------------
+// Diagonal of the eliminated Kuu (Dirichlet dofs -> 1), inverted.
+__global__ void __launch_bounds__(256) k_umesh_dinv(
+    const double* __restrict__ rec, const int4* __restrict__ conn, const int32_t* __restrict__ rowptr,
+    const int32_t* __restrict__ adj, const uint8_t* __restrict__ vmask, const double* __restrict__ alpha,
+    double* __restrict__ dinv, int64_t nv, int dim, UParams p) {
+    const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= nv) return;
+    double dg[3] = {0.0, 0.0, 0.0};
+    const int npe = dim + 1;
+    for (int k = rowptr[v]; k < rowptr[v + 1]; ++k) {
+        const int ent = __ldg(adj + k);
+        const int e = ent >> 2, li = ent & 3;
+        const int4 c = __ldg(conn + e);
+        const double ab = (__ldg(alpha + c.x) + __ldg(alpha + c.y) + __ldg(alpha + c.z)
+                           + (dim == 3 ? __ldg(alpha + c.w) : 0.0)) / npe;
+        const double om = 1.0 - ab;
+        if (dim == 2) {
+            const Rec2 r = load_rec2(rec, e);
+            const double w = (om * om + p.k_ell) * r.volE;
+            const double gx = r.gx[li], gy = r.gy[li];
+            dg[0] += w * (p.d11 * gx * gx + p.d33 * gy * gy);
+            dg[1] += w * (p.d11 * gy * gy + p.d33 * gx * gx);
+        } else {
+            const Rec3 r = load_rec3(rec, e);
+            const double w = (om * om + p.k_ell) * r.volE;
+            const double g[3] = {r.g[0][li], r.g[1][li], r.g[2][li]};
+            const double gg = g[0] * g[0] + g[1] * g[1] + g[2] * g[2];
+#pragma unroll
+            for (int d = 0; d < 3; ++d) dg[d] += w * ((p.lam + p.mu) * g[d] * g[d] + p.mu * gg);
+        }
+    }
+    const uint8_t mv = vmask[v];
+    for (int d = 0; d < dim; ++d) dinv[dim * v + d] = (mv >> d) & 1 ? 1.0 : 1.0 / dg[d];
+}
+
+// x = 0, r = b, z = Dinv r, p = z; partials of r.z and r.r
+__global__ void __launch_bounds__(256) k_umesh_pcg_init(
+    const double* __restrict__ b, double* __restrict__ x, double* __restrict__ r, double* __restrict__ z,
+    double* __restrict__ pv, const double* __restrict__ dinv, double* __restrict__ part, int64_t n, int nb) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    double rz = 0.0, rr = 0.0;
+    if (i < n) {
+        const double ri = b[i], zi = dinv[i] * ri;
+        x[i] = 0.0; r[i] = ri; z[i] = zi; pv[i] = zi;
+        rz = ri * zi; rr = ri * ri;
+    }
+    block_partial(rz, part);
+    block_partial(rr, part + nb);
+}
+
+// one block: fixed-order sums of the partial arrays -> scal[o0], scal[o1]
+__global__ void __launch_bounds__(1024) k_umesh_reduce(const double* __restrict__ part, int nb, int npart,
+                                                       double* __restrict__ scal, int o0, int o1) {
+    __shared__ double sh[32];
+    for (int a = 0; a < npart; ++a) {
+        double t = 0.0;
+        for (int i = threadIdx.x; i < nb; i += 1024) t += part[a * nb + i];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
+        if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = t;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double u = 0.0;
+            for (int w = 0; w < 32; ++w) u += sh[w];
+            scal[a == 0 ? o0 : o1] = u;
+        }
+        __syncthreads();
+    }
+}
+
+// scal layout: [0,1] r.z ring, [2] p.q, [3] r.r, [4] breakdown flag
+// x += a p, r -= a q, z = Dinv r (a = rz_k / pq); partials of the new r.z and r.r
+__global__ void __launch_bounds__(256) k_umesh_pcg_update(
+    double* __restrict__ x, double* __restrict__ r, double* __restrict__ z, const double* __restrict__ pv,
+    const double* __restrict__ q, const double* __restrict__ dinv, double* __restrict__ scal,
+    double* __restrict__ part, int64_t n, int nb, int slot) {
+    const double pq = scal[2];
+    const double a = pq > 0.0 ? scal[slot] / pq : 0.0;
+    if (!(pq > 0.0) && blockIdx.x == 0 && threadIdx.x == 0) scal[4] = 1.0;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    double rz = 0.0, rr = 0.0;
+    if (i < n) {
+        x[i] += a * pv[i];
+        const double ri = r[i] - a * q[i], zi = dinv[i] * ri;
+        r[i] = ri; z[i] = zi;
+        rz = ri * zi; rr = ri * ri;
+    }
+    block_partial(rz, part);
+    block_partial(rr, part + nb);
+}
+
+// p = z + (rz_{k+1} / rz_k) p
+__global__ void __launch_bounds__(256) k_umesh_pcg_dir(double* __restrict__ pv, const double* __restrict__ z,
+                                                       const double* __restrict__ scal, int64_t n, int slot) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const double rzo = scal[slot], rzn = scal[slot ^ 1];
+    const double beta = rzo != 0.0 ? rzn / rzo : 0.0;
+    if (i < n) pv[i] = z[i] + beta * pv[i];
 }
 
 int fail(pf_umesh* m, int code, const std::string& msg) {
@@ -451,8 +585,9 @@ const char* pf_umesh_last_error(const pf_umesh* m) { return m ? m->err.c_str() :
 int64_t pf_umesh_workspace_bytes(const pf_umesh* m) {
     if (!m) return -1;
     const int R = m->dim == 2 ? REC2 : REC3;
+    const int64_t n = m->dim * m->nv, nb = (n + 255) / 256;
     return align256(m->nt * R * 8) + align256(m->nt * 16) + align256((m->nv + 1) * 4)
-         + align256(m->nadj * 4) + align256(m->nv);
+         + align256(m->nadj * 4) + align256(m->nv) + 5 * align256(n * 8) + align256(2 * nb * 8) + 256;
 }
 
 int pf_umesh_bind_workspace(pf_umesh* m, void* dev, int64_t bytes, void* stream) {
@@ -468,7 +603,14 @@ int pf_umesh_bind_workspace(pf_umesh* m, void* dev, int64_t bytes, void* stream)
     m->conn = reinterpret_cast<int32_t*>(p); p += align256(m->nt * 16);
     m->rowptr = reinterpret_cast<int32_t*>(p); p += align256((m->nv + 1) * 4);
     m->adj = reinterpret_cast<int32_t*>(p); p += align256(m->nadj * 4);
-    m->vmask = reinterpret_cast<uint8_t*>(p);
+    m->vmask = reinterpret_cast<uint8_t*>(p); p += align256(m->nv);
+    {
+        const int64_t n = m->dim * m->nv, nb = (n + 255) / 256;
+        double** vecs[5] = {&m->r, &m->z, &m->p, &m->q, &m->dinv};
+        for (auto v : vecs) { *v = reinterpret_cast<double*>(p); p += align256(n * 8); }
+        m->part = reinterpret_cast<double*>(p); p += align256(2 * nb * 8);
+        m->scal = reinterpret_cast<double*>(p);
+    }
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     cudaError_t e = cudaMemcpyAsync(m->rec, m->h_rec.data(), m->nt * R * 8, cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess) e = cudaMemcpyAsync(m->conn, m->h_conn.data(), m->nt * 16, cudaMemcpyHostToDevice, s);
@@ -514,12 +656,12 @@ int pf_umesh_apply_Kuu(pf_umesh* m, const double* alpha, const double* x, double
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const unsigned grid = (unsigned)((m->nv + 255) / 256);
     if (m->dim == 2)
-        k_umesh_Kuu2<<<grid, 256, 0, s>>>(m->rec, reinterpret_cast<const int4*>(m->conn), m->rowptr, m->adj,
-                                          mask, alpha, reinterpret_cast<const double2*>(x),
-                                          reinterpret_cast<double2*>(y), m->nv, p);
+        k_umesh_Kuu2<false><<<grid, 256, 0, s>>>(m->rec, reinterpret_cast<const int4*>(m->conn), m->rowptr,
+                                                 m->adj, mask, alpha, reinterpret_cast<const double2*>(x),
+                                                 reinterpret_cast<double2*>(y), m->nv, p, nullptr);
     else
-        k_umesh_Kuu3<<<grid, 256, 0, s>>>(m->rec, reinterpret_cast<const int4*>(m->conn), m->rowptr, m->adj,
-                                          mask, alpha, x, y, m->nv, p);
+        k_umesh_Kuu3<false><<<grid, 256, 0, s>>>(m->rec, reinterpret_cast<const int4*>(m->conn), m->rowptr,
+                                                 m->adj, mask, alpha, x, y, m->nv, p, nullptr);
     m->launches++;
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? PF_OK : cuda_fail(m, e);
@@ -542,6 +684,73 @@ int pf_umesh_apply_Kaa(pf_umesh* m, const double* u, const double* alpha, const 
     m->launches++;
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? PF_OK : cuda_fail(m, e);
+}
+
+int pf_umesh_elastic_solve(pf_umesh* m, const double* alpha, const double* b, double* x, const pf_lin_opts* o,
+                           pf_lin_report* rep, void* stream) {
+    if (!m) return PF_EINVAL;
+    if (!m->bound) return fail(m, PF_ENOWS, "pf_umesh_elastic_solve: no workspace bound");
+    if (!alpha || !b || !x || !o || x == b) return fail(m, PF_EINVAL, "pf_umesh_elastic_solve: bad pointers");
+    if (o->precond != PF_PREC_JACOBI)
+        return fail(m, PF_EINVAL, "pf_umesh_elastic_solve: element-list meshes take precond = jacobi");
+    const UParams p = make_params(m);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int64_t n = m->dim * m->nv;
+    const int nb = (int)((n + 255) / 256);
+    const unsigned gv = (unsigned)((m->nv + 255) / 256);
+    const int64_t maxit = o->maxit > 0 ? o->maxit : 10 * n;
+    const int every = o->check_every > 0 ? o->check_every : 10;
+    const int4* conn = reinterpret_cast<const int4*>(m->conn);
+    double h[5];
+    auto poll = [&]() -> cudaError_t {
+        cudaError_t e = cudaMemcpyAsync(h, m->scal, sizeof h, cudaMemcpyDeviceToHost, s);
+        return e == cudaSuccess ? cudaStreamSynchronize(s) : e;
+    };
+    if (!rep) return fail(m, PF_EINVAL, "pf_umesh_elastic_solve: NULL report");
+    cudaMemsetAsync(m->scal, 0, 8 * sizeof(double), s);
+    k_umesh_dinv<<<gv, 256, 0, s>>>(m->rec, conn, m->rowptr, m->adj, m->vmask, alpha, m->dinv, m->nv, m->dim, p);
+    k_umesh_pcg_init<<<nb, 256, 0, s>>>(b, x, m->r, m->z, m->p, m->dinv, m->part, n, nb);
+    k_umesh_reduce<<<1, 1024, 0, s>>>(m->part, nb, 2, m->scal, 0, 3);
+    m->launches += 3;
+    cudaError_t e = poll();
+    if (e != cudaSuccess) return cuda_fail(m, e);
+    const double bnorm = std::sqrt(h[3]);
+    const double tol = std::max(o->rtol * bnorm, o->atol);
+    rep->b_norm = bnorm;
+    rep->iterations = 0;
+    rep->final_residual_norm = bnorm;
+    rep->converged = bnorm <= tol;
+    rep->status = PF_OK;
+    // the partial arrays of the Kuu apply (one per vertex block) reuse part[0..gv)
+    int64_t it = 0;
+    while (!rep->converged && it < maxit) {
+        const int slot = (int)(it & 1);
+        if (m->dim == 2)
+            k_umesh_Kuu2<true><<<gv, 256, 0, s>>>(m->rec, conn, m->rowptr, m->adj, m->vmask, alpha,
+                                                  reinterpret_cast<const double2*>(m->p),
+                                                  reinterpret_cast<double2*>(m->q), m->nv, p, m->part);
+        else
+            k_umesh_Kuu3<true><<<gv, 256, 0, s>>>(m->rec, conn, m->rowptr, m->adj, m->vmask, alpha, m->p, m->q,
+                                                  m->nv, p, m->part);
+        k_umesh_reduce<<<1, 1024, 0, s>>>(m->part, (int)gv, 1, m->scal, 2, 2);
+        k_umesh_pcg_update<<<nb, 256, 0, s>>>(x, m->r, m->z, m->p, m->q, m->dinv, m->scal, m->part, n, nb, slot);
+        k_umesh_reduce<<<1, 1024, 0, s>>>(m->part, nb, 2, m->scal, slot ^ 1, 3);
+        k_umesh_pcg_dir<<<nb, 256, 0, s>>>(m->p, m->z, m->scal, n, slot);
+        m->launches += 5;
+        ++it;
+        if (it % every == 0 || it == maxit) {
+            if ((e = poll()) != cudaSuccess) return cuda_fail(m, e);
+            rep->iterations = it;
+            rep->final_residual_norm = std::sqrt(h[3]);
+            if (h[4] != 0.0) {
+                rep->status = PF_EBREAKDOWN;
+                return fail(m, PF_EBREAKDOWN, "CG breakdown: p^T A p <= 0 (operator not SPD)");
+            }
+            rep->converged = rep->final_residual_norm <= tol;
+        }
+    }
+    if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(m, e);
+    return PF_OK;
 }
 
 int64_t pf_umesh_launch_count(const pf_umesh* m) { return m ? m->launches : -1; }

@@ -24,6 +24,7 @@ from typing import Optional
 import numpy as np
 
 from . import _lib
+from .linalg import BreakdownError, LinearSolveReport, LinearSolverError
 from .model import DamageModel, Material
 
 _REGIME = {"plane_stress": 0, "plane_strain": 1, "3d": 2}
@@ -131,6 +132,8 @@ def _raise(code, handle):
     if code == _lib.PF_OK:
         return
     msg = _lib.load().pf_umesh_last_error(handle).decode(errors="replace") or f"status {code}"
+    if code == _lib.PF_EBREAKDOWN:
+        raise BreakdownError(msg)
     if code in (_lib.PF_EINVAL, _lib.PF_ENOWS):
         raise ValueError(msg)
     raise RuntimeError(f"CUDA failure in libphasefrac_b200: {msg}")
@@ -229,3 +232,23 @@ class UnstructuredOperators:
             self._h, self._vec(u, self.n_udofs, "u"), self._vec(alpha, self.n_vertices, "alpha"),
             self._vec(x, self.n_vertices, "x"), self._vec(out, self.n_vertices, "out"), self._stream()))
         return out
+
+    def elastic_solve(self, alpha, b, out=None, rtol: float = 1e-8, atol: float = 0.0, maxit: int = 0,
+                      check_every: int = 10, raise_on_failure: bool = True):
+        """x with Kuu(alpha) x = b, Dirichlet rows/cols eliminated, by device Jacobi PCG from
+        x0 = 0 (cg_solve, linalg.py:106-152).  Returns (x, LinearSolveReport); non-convergence
+        raises LinearSolverError "elastic CG stalled" as solver.py:139-141 unless
+        raise_on_failure is False."""
+        import torch
+        out = torch.empty_like(b) if out is None else out
+        o = _lib.LinOpts(precond=_lib.PREC["jacobi"], warm_start=0, maxit=int(maxit), rtol=float(rtol),
+                         atol=float(atol), check_every=int(check_every))
+        rep = _lib.LinReport()
+        self._check(_lib.load().pf_umesh_elastic_solve(
+            self._h, self._vec(alpha, self.n_vertices, "alpha"), self._vec(b, self.n_udofs, "b"),
+            self._vec(out, self.n_udofs, "out"), C.byref(o), C.byref(rep), self._stream()))
+        report = LinearSolveReport(int(rep.iterations), float(rep.final_residual_norm), bool(rep.converged))
+        if raise_on_failure and not rep.converged:
+            raise LinearSolverError(f"elastic CG stalled after {rep.iterations} iterations "
+                                    f"(|r| = {rep.final_residual_norm:.3e})")
+        return out, report
