@@ -270,6 +270,12 @@ int pf_umesh_apply_Kaa(pf_umesh* m, const double* u, const double* alpha, const 
  * bitwise-reproducible iterates. */
 int pf_umesh_elastic_solve(pf_umesh* m, const double* alpha, const double* b, double* x,
                            const pf_lin_opts* opts, pf_lin_report* rep, void* stream);
+/* Energy parts and gradients at (u, alpha) (assemble_energy / assemble_residual_u(apply_bc=False) /
+ * assemble_residual_alpha, fem.py:162-218): r_u (device, d*V, raw rows) and r_alpha (device, V)
+ * may be NULL; energy (HOST, 3: elastic, surface, total) may be NULL, else the stream is
+ * synchronised.  No inelastic strain on this path. */
+int pf_umesh_physics(pf_umesh* m, const double* u, const double* alpha, double* r_u, double* r_alpha,
+                     double* energy, void* stream);
 int64_t pf_umesh_launch_count(const pf_umesh* m);
 
 #ifdef __cplusplus

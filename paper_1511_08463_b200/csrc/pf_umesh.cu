@@ -458,6 +458,160 @@ __global__ void __launch_bounds__(256) k_umesh_pcg_dir(double* __restrict__ pv, 
     if (i < n) pv[i] = z[i] + beta * pv[i];
 }
 
+// ---- physics: energy parts and gradients (fem.py:162-218; oracle/p1.py energy, residual_*) ----
+__device__ __forceinline__ void ab_terms(const UParams& p, double ab, double& A, double& Ap, double& w,
+                                         double& wp) {
+    const double om = 1.0 - ab;
+    A = om * om + p.k_ell;
+    Ap = -2.0 * om;
+    w = p.at2 ? ab * ab : ab;
+    wp = p.at2 ? 2.0 * ab : 1.0;
+}
+
+// per element: elastic 1/2 A q |T| E, surface |T| Gc/c_w (w/ell + ell |grad alpha|^2)
+__global__ void __launch_bounds__(256) k_umesh_energy(
+    const double* __restrict__ rec, const int4* __restrict__ conn, const double* __restrict__ u,
+    const double* __restrict__ alpha, double* __restrict__ part, int64_t nt, int nbe, int dim, UParams p) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    double el = 0.0, ds = 0.0;
+    if (e < nt) {
+        const int4 c = __ldg(conn + e);
+        const int vs[4] = {c.x, c.y, c.z, c.w};
+        double A, Ap, w, wp, q, volE, volGc, gg = 0.0;
+        if (dim == 2) {
+            const Rec2 r = load_rec2(rec, (int)e);
+            double2 ue[3];
+            double ab = 0.0, ga[2] = {0.0, 0.0};
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                ue[j] = __ldg(reinterpret_cast<const double2*>(u) + vs[j]);
+                const double aj = __ldg(alpha + vs[j]);
+                ab += aj; ga[0] += r.gx[j] * aj; ga[1] += r.gy[j] * aj;
+            }
+            ab_terms(p, ab * (1.0 / 3.0), A, Ap, w, wp);
+            double eps[3];
+            strain2(r, ue, eps);
+            q = eps[0] * (p.d11 * eps[0] + p.d12 * eps[1]) + eps[1] * (p.d12 * eps[0] + p.d11 * eps[1])
+              + p.d33 * eps[2] * eps[2];
+            gg = ga[0] * ga[0] + ga[1] * ga[1];
+            volE = r.volE; volGc = r.volGc;
+        } else {
+            const Rec3 r = load_rec3(rec, (int)e);
+            double ue[4][3];
+            double ab = 0.0, ga[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+#pragma unroll
+                for (int d = 0; d < 3; ++d) ue[j][d] = __ldg(u + 3 * (int64_t)vs[j] + d);
+                const double aj = __ldg(alpha + vs[j]);
+                ab += aj;
+#pragma unroll
+                for (int d = 0; d < 3; ++d) ga[d] += r.g[d][j] * aj;
+            }
+            ab_terms(p, ab * 0.25, A, Ap, w, wp);
+            double eps[6], sg[6];
+            strain3(r, ue, eps);
+            stress3(p, eps, sg);
+            q = 0.0;
+#pragma unroll
+            for (int i = 0; i < 6; ++i) q += eps[i] * sg[i];
+            gg = ga[0] * ga[0] + ga[1] * ga[1] + ga[2] * ga[2];
+            volE = r.volE; volGc = r.volGc;
+        }
+        el = 0.5 * A * q * volE;
+        ds = volGc * p.inv_cw * (w * p.inv_ell + p.ell * gg);
+    }
+    block_partial(el, part);
+    block_partial(ds, part + nbe);
+}
+
+// per vertex: r_u = dE/du (raw rows) and r_alpha = dE/dalpha
+template <int D>
+__global__ void __launch_bounds__(256) k_umesh_grad(
+    const double* __restrict__ rec, const int4* __restrict__ conn, const int32_t* __restrict__ rowptr,
+    const int32_t* __restrict__ adj, const double* __restrict__ u, const double* __restrict__ alpha,
+    double* __restrict__ ru, double* __restrict__ ra, int64_t nv, UParams p) {
+    const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= nv) return;
+    constexpr int NPE = D + 1;
+    double yu[D] = {}, ya = 0.0;
+    for (int k = rowptr[v]; k < rowptr[v + 1]; ++k) {
+        const int ent = __ldg(adj + k);
+        const int e = ent >> 2, li = ent & 3;
+        const int4 c = __ldg(conn + e);
+        const int vs[4] = {c.x, c.y, c.z, c.w};
+        double g[3][4], volE, volGc;
+        if (D == 2) {
+            const Rec2 r = load_rec2(rec, e);
+#pragma unroll
+            for (int j = 0; j < 3; ++j) { g[0][j] = r.gx[j]; g[1][j] = r.gy[j]; g[2][j] = 0.0; }
+            g[0][3] = g[1][3] = g[2][3] = 0.0;
+            volE = r.volE; volGc = r.volGc;
+        } else {
+            const Rec3 r = load_rec3(rec, e);
+#pragma unroll
+            for (int d = 0; d < 3; ++d)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) g[d][j] = r.g[d][j];
+            volE = r.volE; volGc = r.volGc;
+        }
+        double ue[4][3] = {}, ab = 0.0, ga[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+        for (int j = 0; j < NPE; ++j) {
+#pragma unroll
+            for (int d = 0; d < D; ++d) ue[j][d] = __ldg(u + D * (int64_t)vs[j] + d);
+            const double aj = __ldg(alpha + vs[j]);
+            ab += aj;
+#pragma unroll
+            for (int d = 0; d < D; ++d) ga[d] += g[d][j] * aj;
+        }
+        double A, Ap, w, wp;
+        ab_terms(p, ab / NPE, A, Ap, w, wp);
+        double gi[3];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) gi[d] = li == 0 ? g[d][0] : (li == 1 ? g[d][1] : (li == 2 ? g[d][2] : g[d][3]));
+        double q;
+        if (D == 2) {
+            double e0 = 0.0, e1 = 0.0, e2 = 0.0;
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                e0 += g[0][j] * ue[j][0];
+                e1 += g[1][j] * ue[j][1];
+                e2 += g[1][j] * ue[j][0] + g[0][j] * ue[j][1];
+            }
+            const double s0 = p.d11 * e0 + p.d12 * e1, s1 = p.d12 * e0 + p.d11 * e1, s2 = p.d33 * e2;
+            q = e0 * s0 + e1 * s1 + e2 * s2;
+            const double wA = A * volE;
+            yu[0] += wA * (gi[0] * s0 + gi[1] * s2);
+            yu[1] += wA * (gi[1] * s1 + gi[0] * s2);
+        } else {
+            Rec3 r;
+#pragma unroll
+            for (int d = 0; d < 3; ++d)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) r.g[d][j] = g[d][j];
+            double eps[6], sg[6];
+            strain3(r, ue, eps);
+            stress3(p, eps, sg);
+            q = 0.0;
+#pragma unroll
+            for (int i = 0; i < 6; ++i) q += eps[i] * sg[i];
+            const double wA = A * volE;
+            yu[0] += wA * (gi[0] * sg[0] + gi[2] * sg[4] + gi[1] * sg[5]);
+            yu[1 % D] += wA * (gi[1] * sg[1] + gi[2] * sg[3] + gi[0] * sg[5]);
+            yu[2 % D] += wA * (gi[2] * sg[2] + gi[1] * sg[3] + gi[0] * sg[4]);
+        }
+        const double kc = volGc * p.inv_cw;
+        ya += (0.5 * Ap * q * volE + kc * wp * p.inv_ell) / NPE
+            + 2.0 * kc * p.ell * (gi[0] * ga[0] + gi[1] * ga[1] + gi[2] * ga[2]);
+    }
+    if (ru) {
+#pragma unroll
+        for (int d = 0; d < D; ++d) ru[D * v + d] = yu[d];
+    }
+    if (ra) ra[v] = ya;
+}
+
 int fail(pf_umesh* m, int code, const std::string& msg) {
     if (m) m->err = msg;
     return code;
@@ -585,7 +739,7 @@ const char* pf_umesh_last_error(const pf_umesh* m) { return m ? m->err.c_str() :
 int64_t pf_umesh_workspace_bytes(const pf_umesh* m) {
     if (!m) return -1;
     const int R = m->dim == 2 ? REC2 : REC3;
-    const int64_t n = m->dim * m->nv, nb = (n + 255) / 256;
+    const int64_t n = m->dim * m->nv, nb = std::max((n + 255) / 256, (m->nt + 255) / 256);
     return align256(m->nt * R * 8) + align256(m->nt * 16) + align256((m->nv + 1) * 4)
          + align256(m->nadj * 4) + align256(m->nv) + 5 * align256(n * 8) + align256(2 * nb * 8) + 256;
 }
@@ -605,7 +759,7 @@ int pf_umesh_bind_workspace(pf_umesh* m, void* dev, int64_t bytes, void* stream)
     m->adj = reinterpret_cast<int32_t*>(p); p += align256(m->nadj * 4);
     m->vmask = reinterpret_cast<uint8_t*>(p); p += align256(m->nv);
     {
-        const int64_t n = m->dim * m->nv, nb = (n + 255) / 256;
+        const int64_t n = m->dim * m->nv, nb = std::max((n + 255) / 256, (m->nt + 255) / 256);
         double** vecs[5] = {&m->r, &m->z, &m->p, &m->q, &m->dinv};
         for (auto v : vecs) { *v = reinterpret_cast<double*>(p); p += align256(n * 8); }
         m->part = reinterpret_cast<double*>(p); p += align256(2 * nb * 8);
@@ -751,6 +905,39 @@ int pf_umesh_elastic_solve(pf_umesh* m, const double* alpha, const double* b, do
     }
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(m, e);
     return PF_OK;
+}
+
+int pf_umesh_physics(pf_umesh* m, const double* u, const double* alpha, double* r_u, double* r_alpha,
+                     double* energy, void* stream) {
+    if (!m) return PF_EINVAL;
+    if (!m->bound) return fail(m, PF_ENOWS, "pf_umesh_physics: no workspace bound");
+    if (!u || !alpha) return fail(m, PF_EINVAL, "pf_umesh_physics: bad pointers");
+    const UParams p = make_params(m);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int4* conn = reinterpret_cast<const int4*>(m->conn);
+    const unsigned gv = (unsigned)((m->nv + 255) / 256);
+    if (r_u || r_alpha) {
+        if (m->dim == 2)
+            k_umesh_grad<2><<<gv, 256, 0, s>>>(m->rec, conn, m->rowptr, m->adj, u, alpha, r_u, r_alpha, m->nv, p);
+        else
+            k_umesh_grad<3><<<gv, 256, 0, s>>>(m->rec, conn, m->rowptr, m->adj, u, alpha, r_u, r_alpha, m->nv, p);
+        m->launches++;
+    }
+    if (energy) {
+        const int nbe = (int)((m->nt + 255) / 256);
+        k_umesh_energy<<<nbe, 256, 0, s>>>(m->rec, conn, u, alpha, m->part, m->nt, nbe, m->dim, p);
+        k_umesh_reduce<<<1, 1024, 0, s>>>(m->part, nbe, 2, m->scal, 5, 6);
+        m->launches += 2;
+        double h[2];
+        cudaError_t e = cudaMemcpyAsync(h, m->scal + 5, sizeof h, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) return cuda_fail(m, e);
+        energy[0] = h[0];
+        energy[1] = h[1];
+        energy[2] = h[0] + h[1];
+    }
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? PF_OK : cuda_fail(m, e);
 }
 
 int64_t pf_umesh_launch_count(const pf_umesh* m) { return m ? m->launches : -1; }

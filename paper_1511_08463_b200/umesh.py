@@ -252,3 +252,16 @@ class UnstructuredOperators:
             raise LinearSolverError(f"elastic CG stalled after {rep.iterations} iterations "
                                     f"(|r| = {rep.final_residual_norm:.3e})")
         return out, report
+
+    def physics(self, u, alpha, want_residuals: bool = True):
+        """(EnergyBreakdown-like (elastic, surface, total), r_u raw, r_alpha) at (u, alpha):
+        assemble_energy / assemble_residual_u(apply_bc=False) / assemble_residual_alpha
+        (fem.py:162-218) on the element-list mesh."""
+        import torch
+        ru = torch.empty_like(u) if want_residuals else None
+        ra = torch.empty_like(alpha) if want_residuals else None
+        en = (C.c_double * 3)()
+        self._check(_lib.load().pf_umesh_physics(
+            self._h, self._vec(u, self.n_udofs, "u"), self._vec(alpha, self.n_vertices, "alpha"),
+            None if ru is None else _lib.ptr(ru), None if ra is None else _lib.ptr(ra), en, self._stream()))
+        return (float(en[0]), float(en[1]), float(en[2])), ru, ra

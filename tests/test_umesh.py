@@ -102,7 +102,7 @@ def test_capi_create_validates_without_device():
     nv, nt = mesh.n_vertices, mesh.n_elements
     adj = 3 * nt
     n = 2 * nv
-    nb = (n + 255) // 256
+    nb = max((n + 255) // 256, (nt + 255) // 256)
     expect = sum((b + 255) // 256 * 256 for b in (nt * 64, nt * 16, (nv + 1) * 4, adj * 4, nv,
                                                   n * 8, n * 8, n * 8, n * 8, n * 8, 2 * nb * 8)) + 256
     assert lib.pf_umesh_workspace_bytes(h) == expect
@@ -236,3 +236,31 @@ def test_gpu_umesh_jacobi_pcg_solves_eliminated_system(dim):
     assert rep2.iterations == rep.iterations and torch.equal(x, x2)
     with pytest.raises(LinearSolverError, match="stalled"):
         ops.elastic_solve(_dev(a), _dev(b), rtol=1e-11, maxit=5, check_every=5)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", CASES, ids=lambda c: f"{c[0]}d-{c[1]}-{c[2]}-{'x'.join(map(str, c[3]))}")
+def test_gpu_umesh_physics_vs_oracle(case):
+    """Energy parts (1e-12 relative) and the raw gradients r_u, r_alpha on element-list meshes."""
+    import paper_1511_08463_b200 as pf
+    dim, regime, model, shape, jit, hetero = case
+    om_mesh = (jitter_interior(grid_mesh(*shape, 2.0, 1.0), jit, 5) if dim == 2
+               else jitter_interior(kuhn_mesh(*shape), jit, 5))
+    rng = np.random.default_rng(3 * sum(shape) + dim)
+    T, V = om_mesh.n_elements, om_mesh.n_vertices
+    Ee = rng.uniform(0.5, 1.5, T) if hetero else None
+    Ge = rng.uniform(0.5, 1.5, T) if hetero else None
+    spec = MaterialSpec(E=1.3, nu=0.3, Gc=0.9, ell=0.07, k_ell=1e-6, model=model, regime=regime)
+    om = P1Model(om_mesh, spec, Ee, Ge)
+    ops = pf.UnstructuredOperators(pf.UnstructuredMesh(om_mesh.vertices, om_mesh.elements),
+                                   pf.Material(E=1.3, nu=0.3, Gc=0.9, ell=0.07, k_ell=1e-6, regime=regime),
+                                   model, Ee, Ge)
+    a = rng.uniform(0, 1, V)
+    u = 0.1 * rng.standard_normal(dim * V)
+    (el, ds, tot), ru, ra = ops.physics(_dev(u), _dev(a))
+    ref = om.energy(u, a)
+    assert abs(el - ref[0]) <= 1e-12 * abs(ref[0])
+    assert abs(ds - ref[1]) <= 1e-12 * abs(ref[1])
+    assert abs(tot - ref[2]) <= 1e-12 * abs(ref[2])
+    assert rel(ru.cpu().numpy(), om.residual_u(u, a, bc_rows="none")) < TOL
+    assert rel(ra.cpu().numpy(), om.residual_alpha(u, a)) < TOL
