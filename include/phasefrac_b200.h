@@ -276,6 +276,14 @@ int pf_umesh_elastic_solve(pf_umesh* m, const double* alpha, const double* b, do
  * synchronised.  No inelastic strain on this path. */
 int pf_umesh_physics(pf_umesh* m, const double* u, const double* alpha, double* r_u, double* r_alpha,
                      double* energy, void* stream);
+/* Damage half-step on the element-list mesh (damage_half_step, am.py / solver.py:160-191): alpha_out =
+ * the rsls solution (vi.py:187-264) of the box QP min 1/2 a^T Kaa(u) a + c^T a, alpha_lb <= a <= 1, at
+ * fixed u, started from clip(alpha_in) (alpha_out may alias alpha_in).  Reduced-space active set:
+ * each iteration solves K_II d_I = -g_I by Jacobi PCG (opts->inner_rtol / inner_maxit), then a
+ * projected Armijo backtracking step on 1/2 |Phi_FB|^2.  rep->status = PF_ESTALL when max_iterations
+ * end unconverged (the call still returns PF_OK). */
+int pf_umesh_damage_solve(pf_umesh* m, const double* u, const double* alpha_lb, const double* alpha_in,
+                          double* alpha_out, const pf_vi_opts* opts, pf_vi_report* rep, void* stream);
 int64_t pf_umesh_launch_count(const pf_umesh* m);
 
 #ifdef __cplusplus

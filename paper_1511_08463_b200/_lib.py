@@ -106,6 +106,8 @@ EXPORTS = {
     "pf_umesh_elastic_solve": (C.c_int, [C.c_void_p] * 4 + [C.POINTER(LinOpts), C.POINTER(LinReport),
                                                              C.c_void_p]),
     "pf_umesh_physics": (C.c_int, [C.c_void_p] * 6 + [C.c_void_p]),
+    "pf_umesh_damage_solve": (C.c_int, [C.c_void_p] * 5 + [C.POINTER(VIOpts), C.POINTER(VIReport),
+                                                         C.c_void_p]),
     "pf_umesh_launch_count": (C.c_int64, [C.c_void_p]),
 }
 KERNEL_KINDS = ["Kuu", "Kuu_cg", "Kuu_diag", "kappa", "Kaa", "Kaa_cg", "Kaa_diag", "Kaa_trial",

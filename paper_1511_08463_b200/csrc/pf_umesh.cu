@@ -179,12 +179,35 @@ __global__ void __launch_bounds__(256) k_umesh_Kuu2(
     }
 }
 
+// MODE: KAA_APPLY y = Kaa x; KAA_PCG y = Kaa x on rows with dinv != 0 (the inactive set of the
+// damage VI; x is zero on the active rows) else 0, plus block partials of x.y; KAA_DIAG y = diag(Kaa)
+// (x unused).
+enum { KAA_APPLY = 0, KAA_PCG = 1, KAA_DIAG = 2 };
+
+template <int MODE>
+__device__ __forceinline__ void kaa_store(int64_t v, double acc, const double* __restrict__ x,
+                                          double* __restrict__ y, const double* __restrict__ dinv,
+                                          double* __restrict__ part) {
+    if (MODE == KAA_PCG) {
+        if (dinv[v] == 0.0) acc = 0.0;
+        y[v] = acc;
+        block_partial(x[v] * acc, part);
+    } else {
+        y[v] = acc;
+    }
+}
+
+template <int MODE>
 __global__ void __launch_bounds__(256) k_umesh_Kaa2(
     const double* __restrict__ rec, const int4* __restrict__ conn, const int32_t* __restrict__ rowptr,
     const int32_t* __restrict__ adj, const double2* __restrict__ u,
-    const double* __restrict__ x, double* __restrict__ y, int64_t nv, UParams p) {
+    const double* __restrict__ x, double* __restrict__ y, int64_t nv, UParams p,
+    const double* __restrict__ dinv = nullptr, double* __restrict__ part = nullptr) {
     const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (v >= nv) return;
+    if (v >= nv) {
+        if (MODE == KAA_PCG) block_partial(0.0, part);
+        return;
+    }
     double acc = 0.0;
     const int k0 = rowptr[v], k1 = rowptr[v + 1];
     for (int k = k0; k < k1; ++k) {
@@ -198,7 +221,7 @@ __global__ void __launch_bounds__(256) k_umesh_Kaa2(
 #pragma unroll
         for (int j = 0; j < 3; ++j) {
             ue[j] = __ldg(u + vs[j]);
-            const double xj = __ldg(x + vs[j]);
+            const double xj = MODE == KAA_DIAG ? (j == li ? 1.0 : 0.0) : __ldg(x + vs[j]);
             sx += xj;
             gxa += r.gx[j] * xj;
             gya += r.gy[j] * xj;
@@ -214,7 +237,7 @@ __global__ void __launch_bounds__(256) k_umesh_Kaa2(
         const double gyi = li == 0 ? r.gy[0] : (li == 1 ? r.gy[1] : r.gy[2]);
         acc += react * sx + 2.0 * kc * p.ell * (gxi * gxa + gyi * gya);
     }
-    y[v] = acc;
+    kaa_store<MODE>(v, acc, x, y, dinv, part);
 }
 
 // ---- 3D ------------------------------------------------------------------------------------
@@ -317,12 +340,17 @@ __global__ void __launch_bounds__(256) k_umesh_Kuu3(
     if (DOT) block_partial(x[3 * v] * y0 + x[3 * v + 1] * y1 + x[3 * v + 2] * y2, part);
 }
 
+template <int MODE>
 __global__ void __launch_bounds__(256) k_umesh_Kaa3(
     const double* __restrict__ rec, const int4* __restrict__ conn, const int32_t* __restrict__ rowptr,
     const int32_t* __restrict__ adj, const double* __restrict__ u,
-    const double* __restrict__ x, double* __restrict__ y, int64_t nv, UParams p) {
+    const double* __restrict__ x, double* __restrict__ y, int64_t nv, UParams p,
+    const double* __restrict__ dinv = nullptr, double* __restrict__ part = nullptr) {
     const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (v >= nv) return;
+    if (v >= nv) {
+        if (MODE == KAA_PCG) block_partial(0.0, part);
+        return;
+    }
     double acc = 0.0;
     const int k0 = rowptr[v], k1 = rowptr[v + 1];
     for (int k = k0; k < k1; ++k) {
@@ -337,7 +365,7 @@ __global__ void __launch_bounds__(256) k_umesh_Kaa3(
         for (int j = 0; j < 4; ++j) {
 #pragma unroll
             for (int d = 0; d < 3; ++d) ue[j][d] = __ldg(u + 3 * (int64_t)vs[j] + d);
-            const double xj = __ldg(x + vs[j]);
+            const double xj = MODE == KAA_DIAG ? (j == li ? 1.0 : 0.0) : __ldg(x + vs[j]);
             sx += xj;
 #pragma unroll
             for (int d = 0; d < 3; ++d) ga[d] += r.g[d][j] * xj;
@@ -354,7 +382,7 @@ __global__ void __launch_bounds__(256) k_umesh_Kaa3(
         const double gi0 = pick4(r.g[0], li), gi1 = pick4(r.g[1], li), gi2 = pick4(r.g[2], li);
         acc += react * sx + 2.0 * kc * p.ell * (gi0 * ga[0] + gi1 * ga[1] + gi2 * ga[2]);
     }
-    y[v] = acc;
+    kaa_store<MODE>(v, acc, x, y, dinv, part);
 }
 
 // ---- Jacobi PCG (cg_solve, linalg.py:106-152) ---------------------------------------------
@@ -612,6 +640,41 @@ __global__ void __launch_bounds__(256) k_umesh_grad(
     if (ra) ra[v] = ya;
 }
 
+// ---- damage box QP (damage_half_step: rsls on Kaa(u) a + c, vi.py:187-264; oracle/mcp.py rsls) ----
+__device__ __forceinline__ double fbf(double a, double b) { return hypot(a, b) - a - b; }
+
+// Phi(a) for lb <= a <= 1 (fb_box, vi.py:95-115), its square into block partials, the reduced-space
+// active set (active_sets, zeta) as dinv = 0, dinv = 1/diag on the inactive rows and the Newton
+// right-hand side rhs = -g on the inactive rows.
+__global__ void __launch_bounds__(256) k_umesh_vi_prep(
+    const double* __restrict__ a, const double* __restrict__ g, const double* __restrict__ lb,
+    const double* __restrict__ diag, double* __restrict__ dinv, double* __restrict__ rhs,
+    double* __restrict__ part, int64_t nv, double zeta) {
+    const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    double ph2 = 0.0;
+    if (v < nv) {
+        const double av = a[v], gv = g[v], lo = lb[v];
+        const double ph = fbf(av - lo, fbf(1.0 - av, -gv));
+        ph2 = ph * ph;
+        const bool la = (av - lo <= zeta) && (gv > 0.0);
+        const bool ua = !la && (1.0 - av <= zeta) && (gv < 0.0);
+        const bool act = la || ua;
+        dinv[v] = act ? 0.0 : 1.0 / diag[v];
+        rhs[v] = act ? 0.0 : -gv;
+    }
+    block_partial(ph2, part);
+}
+
+// out = clip(a + t d, lb, 1) (d may be NULL: a projection of a onto the box)
+__global__ void __launch_bounds__(256) k_umesh_vi_cand(
+    const double* __restrict__ a, const double* __restrict__ d, const double* __restrict__ lb, double t,
+    double* __restrict__ out, int64_t nv) {
+    const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= nv) return;
+    const double c = a[v] + (d ? t * d[v] : 0.0);
+    out[v] = fmin(fmax(c, lb[v]), 1.0);
+}
+
 int fail(pf_umesh* m, int code, const std::string& msg) {
     if (m) m->err = msg;
     return code;
@@ -830,10 +893,10 @@ int pf_umesh_apply_Kaa(pf_umesh* m, const double* u, const double* alpha, const 
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const unsigned grid = (unsigned)((m->nv + 255) / 256);
     if (m->dim == 2)
-        k_umesh_Kaa2<<<grid, 256, 0, s>>>(m->rec, reinterpret_cast<const int4*>(m->conn), m->rowptr, m->adj,
+        k_umesh_Kaa2<KAA_APPLY><<<grid, 256, 0, s>>>(m->rec, reinterpret_cast<const int4*>(m->conn), m->rowptr, m->adj,
                                           reinterpret_cast<const double2*>(u), x, y, m->nv, p);
     else
-        k_umesh_Kaa3<<<grid, 256, 0, s>>>(m->rec, reinterpret_cast<const int4*>(m->conn), m->rowptr, m->adj,
+        k_umesh_Kaa3<KAA_APPLY><<<grid, 256, 0, s>>>(m->rec, reinterpret_cast<const int4*>(m->conn), m->rowptr, m->adj,
                                           u, x, y, m->nv, p);
     m->launches++;
     const cudaError_t e = cudaGetLastError();
@@ -938,6 +1001,132 @@ int pf_umesh_physics(pf_umesh* m, const double* u, const double* alpha, double* 
     }
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? PF_OK : cuda_fail(m, e);
+}
+
+int pf_umesh_damage_solve(pf_umesh* m, const double* u, const double* alpha_lb, const double* alpha_in,
+                          double* alpha_out, const pf_vi_opts* o, pf_vi_report* rep, void* stream) {
+    if (!m) return PF_EINVAL;
+    if (!m->bound) return fail(m, PF_ENOWS, "pf_umesh_damage_solve: no workspace bound");
+    if (!u || !alpha_lb || !alpha_in || !alpha_out || !o || !rep)
+        return fail(m, PF_EINVAL, "pf_umesh_damage_solve: bad pointers");
+    if (alpha_out == alpha_lb) return fail(m, PF_EINVAL, "pf_umesh_damage_solve: alpha_out aliases alpha_lb");
+    const UParams p = make_params(m);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int64_t nv = m->nv;
+    const int nb = (int)((nv + 255) / 256);
+    const unsigned gv = (unsigned)nb;
+    const int4* conn = reinterpret_cast<const int4*>(m->conn);
+    // scratch: every workspace vector holds dim*nv >= 2 nv doubles
+    double *r = m->r, *g = m->r + nv, *z = m->z, *d = m->z + nv, *pv = m->p, *cand = m->p + nv;
+    double *q = m->q, *dinv = m->dinv, *diag = m->dinv + nv;
+    double* a = alpha_out;
+    double h[8];
+    auto poll = [&]() -> cudaError_t {
+        cudaError_t e = cudaMemcpyAsync(h, m->scal, sizeof h, cudaMemcpyDeviceToHost, s);
+        return e == cudaSuccess ? cudaStreamSynchronize(s) : e;
+    };
+    auto grad = [&](const double* x) {
+        if (m->dim == 2)
+            k_umesh_grad<2><<<gv, 256, 0, s>>>(m->rec, conn, m->rowptr, m->adj, u, x, nullptr, g, nv, p);
+        else
+            k_umesh_grad<3><<<gv, 256, 0, s>>>(m->rec, conn, m->rowptr, m->adj, u, x, nullptr, g, nv, p);
+    };
+    *rep = pf_vi_report{};
+    cudaMemsetAsync(m->scal, 0, 8 * sizeof(double), s);
+    // zeta from the initial iterate (rsls: 1e-10 (1 + |x0|_inf)); the box keeps |a| <= 1
+    double zeta = o->zero_tol;
+    k_umesh_vi_cand<<<gv, 256, 0, s>>>(alpha_in, nullptr, alpha_lb, 0.0, a, nv);
+    if (m->dim == 2)
+        k_umesh_Kaa2<KAA_DIAG><<<gv, 256, 0, s>>>(m->rec, conn, m->rowptr, m->adj,
+                                                  reinterpret_cast<const double2*>(u), nullptr, diag, nv, p);
+    else
+        k_umesh_Kaa3<KAA_DIAG><<<gv, 256, 0, s>>>(m->rec, conn, m->rowptr, m->adj, u, nullptr, diag, nv, p);
+    grad(a);
+    m->launches += 3;
+    if (!(zeta > 0.0)) {
+        std::vector<double> a0(nv);
+        cudaError_t e = cudaMemcpyAsync(a0.data(), alpha_in, nv * 8, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) return cuda_fail(m, e);
+        double mx = 0.0;
+        for (double x : a0) mx = std::max(mx, std::fabs(x));
+        zeta = 1e-10 * (1.0 + mx);
+    }
+    k_umesh_vi_prep<<<gv, 256, 0, s>>>(a, g, alpha_lb, diag, dinv, q, m->part, nv, zeta);
+    k_umesh_reduce<<<1, 1024, 0, s>>>(m->part, nb, 1, m->scal, 7, 7);
+    m->launches += 2;
+    cudaError_t e = poll();
+    if (e != cudaSuccess) return cuda_fail(m, e);
+    double merit = h[7];
+    const int maxit = o->max_iterations > 0 ? o->max_iterations : 100;
+    const double bt = o->ls_backtrack > 0.0 && o->ls_backtrack < 1.0 ? o->ls_backtrack : 0.5;
+    const double tmin = o->ls_min_step > 0.0 ? o->ls_min_step : 1e-10;
+    const double irtol = o->inner_rtol > 0.0 ? o->inner_rtol : 1e-10;
+    const int64_t imaxit = o->inner_maxit > 0 ? o->inner_maxit : 10 * nv;
+    auto record = [&]() {
+        if (rep->n_history < 64) rep->history[rep->n_history++] = std::sqrt(merit);
+    };
+    record();
+    int it = 0;
+    while (true) {
+        rep->final_residual_norm = std::sqrt(merit);
+        if (std::sqrt(merit) <= o->abs_tol) { rep->converged = 1; break; }
+        if (it >= maxit) break;
+        // reduced Newton system K_II d_I = -g_I by Jacobi PCG (rhs in q, d = 0 on the active rows)
+        cudaMemsetAsync(m->scal, 0, 5 * sizeof(double), s);
+        k_umesh_pcg_init<<<nb, 256, 0, s>>>(q, d, r, z, pv, dinv, m->part, nv, nb);
+        k_umesh_reduce<<<1, 1024, 0, s>>>(m->part, nb, 2, m->scal, 0, 3);
+        m->launches += 2;
+        if ((e = poll()) != cudaSuccess) return cuda_fail(m, e);
+        const double tol = irtol * std::sqrt(h[3]);
+        double rn = std::sqrt(h[3]);
+        int64_t k = 0;
+        while (rn > tol && k < imaxit) {
+            const int slot = (int)(k & 1);
+            if (m->dim == 2)
+                k_umesh_Kaa2<KAA_PCG><<<gv, 256, 0, s>>>(m->rec, conn, m->rowptr, m->adj,
+                                                         reinterpret_cast<const double2*>(u), pv, q, nv, p,
+                                                         dinv, m->part);
+            else
+                k_umesh_Kaa3<KAA_PCG><<<gv, 256, 0, s>>>(m->rec, conn, m->rowptr, m->adj, u, pv, q, nv, p,
+                                                         dinv, m->part);
+            k_umesh_reduce<<<1, 1024, 0, s>>>(m->part, nb, 1, m->scal, 2, 2);
+            k_umesh_pcg_update<<<nb, 256, 0, s>>>(d, r, z, pv, q, dinv, m->scal, m->part, nv, nb, slot);
+            k_umesh_reduce<<<1, 1024, 0, s>>>(m->part, nb, 2, m->scal, slot ^ 1, 3);
+            k_umesh_pcg_dir<<<nb, 256, 0, s>>>(pv, z, m->scal, nv, slot);
+            m->launches += 5;
+            ++k;
+            if (k % 10 == 0 || k == imaxit) {
+                if ((e = poll()) != cudaSuccess) return cuda_fail(m, e);
+                if (h[4] != 0.0) break;
+                rn = std::sqrt(h[3]);
+            }
+        }
+        rep->total_krylov_iterations += k;
+        if (rn > tol) rep->linear_failures++;
+        // projected step with Armijo backtracking on the merit 1/2 |Phi|^2
+        double t = 1.0, mnew = merit;
+        while (true) {
+            k_umesh_vi_cand<<<gv, 256, 0, s>>>(a, d, alpha_lb, t, cand, nv);
+            grad(cand);
+            k_umesh_vi_prep<<<gv, 256, 0, s>>>(cand, g, alpha_lb, diag, dinv, q, m->part, nv, zeta);
+            k_umesh_reduce<<<1, 1024, 0, s>>>(m->part, nb, 1, m->scal, 7, 7);
+            m->launches += 4;
+            if ((e = poll()) != cudaSuccess) return cuda_fail(m, e);
+            mnew = h[7];
+            if (mnew <= (1.0 - 2.0 * o->armijo * t) * merit || t * bt < tmin) break;
+            t *= bt;
+        }
+        if ((e = cudaMemcpyAsync(a, cand, nv * 8, cudaMemcpyDeviceToDevice, s)) != cudaSuccess)
+            return cuda_fail(m, e);
+        merit = mnew;
+        ++it;
+        rep->iterations = it;
+        record();
+    }
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(m, e);
+    rep->status = rep->converged ? PF_OK : PF_ESTALL;
+    return PF_OK;
 }
 
 int64_t pf_umesh_launch_count(const pf_umesh* m) { return m ? m->launches : -1; }

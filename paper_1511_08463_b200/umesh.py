@@ -10,6 +10,8 @@ include/phasefrac_b200.h):
 
 * ``apply_Kuu(alpha, x)``  = ``assemble_Kuu(state, problem, apply_bc) @ x``  (fem.py:233-244)
 * ``apply_Kaa(u, alpha, x)`` = ``assemble_Kaa(state, problem) @ x``           (fem.py:266-282)
+* ``elastic_solve`` / ``physics`` / ``damage_solve``: the elastic CG, energies and gradients, and
+  the damage box QP (damage_step, solver.py:160-191) on the same mesh
 
 No CPU fallback: without the CUDA library every call raises.
 """
@@ -265,3 +267,24 @@ class UnstructuredOperators:
             self._h, self._vec(u, self.n_udofs, "u"), self._vec(alpha, self.n_vertices, "alpha"),
             None if ru is None else _lib.ptr(ru), None if ra is None else _lib.ptr(ra), en, self._stream()))
         return (float(en[0]), float(en[1]), float(en[2])), ru, ra
+
+    def damage_solve(self, u, alpha_lb, alpha, out=None, config=None, raise_on_failure: bool = True):
+        """alpha_out = rsls solution of the damage box QP at fixed u (damage_step, solver.py:160-191;
+        rsls vi.py:187-264): min E(u, a) over alpha_lb <= a <= 1 from clip(alpha).  Reduced-space
+        active set with a device Jacobi-PCG inner solve.  Returns (alpha_out, ActiveSetReport);
+        non-convergence raises VISolverError-like RuntimeError unless raise_on_failure is False."""
+        import torch
+        from .vi import ActiveSetReport, VIConfig
+        cfg = config or VIConfig()
+        out = torch.empty_like(alpha) if out is None else out
+        o = cfg.to_c()
+        rep = _lib.VIReport()
+        self._check(_lib.load().pf_umesh_damage_solve(
+            self._h, self._vec(u, self.n_udofs, "u"), self._vec(alpha_lb, self.n_vertices, "alpha_lb"),
+            self._vec(alpha, self.n_vertices, "alpha"), self._vec(out, self.n_vertices, "out"),
+            C.byref(o), C.byref(rep), self._stream()))
+        report = ActiveSetReport.from_c(rep)
+        if raise_on_failure and not report.converged:
+            raise RuntimeError(f"damage VI did not converge in {report.iterations} iterations "
+                               f"(|Phi| = {report.final_residual_norm:.3e})")
+        return out, report

@@ -264,3 +264,45 @@ def test_gpu_umesh_physics_vs_oracle(case):
     assert abs(tot - ref[2]) <= 1e-12 * abs(ref[2])
     assert rel(ru.cpu().numpy(), om.residual_u(u, a, bc_rows="none")) < TOL
     assert rel(ra.cpu().numpy(), om.residual_alpha(u, a)) < TOL
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dim,model", [(2, "AT1"), (2, "AT2"), (3, "AT1"), (3, "AT2")])
+def test_gpu_umesh_damage_solve_vs_oracle_rsls(dim, model):
+    """Damage box QP at fixed u (damage_half_step: rsls on Kaa(u) a + c over [alpha_lb, 1]) on a
+    jittered mesh: the device reduced-space solve and the oracle's rsls reach the same unique
+    minimiser; the device result is FB-stationary and bitwise reproducible."""
+    import torch
+    import paper_1511_08463_b200 as pf
+    from oracle.mcp import RSLSConfig, fb_box, rsls
+    from paper_1511_08463_b200.vi import VIConfig
+    regime = "plane_strain" if dim == 2 else "3d"
+    om_mesh = (jitter_interior(grid_mesh(40, 20, 2.0, 1.0), 0.25, 9) if dim == 2
+               else jitter_interior(kuhn_mesh(7, 6, 8), 0.1, 9))
+    V = om_mesh.n_vertices
+    rng = np.random.default_rng(11 * dim + (model == "AT2"))
+    spec = MaterialSpec(E=1.0, nu=0.3, Gc=1.0, ell=0.1, k_ell=1e-6, model=model, regime=regime)
+    om = P1Model(om_mesh, spec)
+    x = om_mesh.vertices
+    u = np.zeros(dim * V)
+    u[0::dim] = 0.6 * x[:, 0] * (1.0 + 0.5 * np.sin(3.0 * x[:, 1]))
+    u += 0.02 * rng.standard_normal(dim * V)
+    lb = np.where(rng.uniform(size=V) < 0.3, rng.uniform(0.0, 0.6, V), 0.0)
+    a0 = lb.copy()
+    K = om.Kaa(u, a0)
+    c = om.residual_alpha(u, a0) - K @ a0
+    ref, st = rsls(lambda a: K @ a + c, lambda a: K, lb, np.ones(V), a0, RSLSConfig(abs_tol=1e-10),
+                   jac_matvec=lambda J: (lambda v: J.T @ v))
+    ops = pf.UnstructuredOperators(pf.UnstructuredMesh(om_mesh.vertices, om_mesh.elements),
+                                   pf.Material(E=1.0, nu=0.3, Gc=1.0, ell=0.1, k_ell=1e-6, regime=regime),
+                                   model)
+    cfg = VIConfig(abs_tol=1e-10, inner_rtol=1e-12)
+    ad, rep = ops.damage_solve(_dev(u), _dev(lb), _dev(a0), config=cfg)
+    assert rep.converged and rep.iterations >= 1 and rep.total_krylov_iterations > 0
+    ah = ad.cpu().numpy()
+    assert np.all(ah >= lb) and np.all(ah <= 1.0)
+    assert np.linalg.norm(fb_box(ah, K @ ah + c, lb, np.ones(V))) <= 1e-9
+    assert np.max(np.abs(ah - ref)) < 1e-8
+    assert 0 < np.count_nonzero(ah > lb + 1e-12) < V  # the bound is active on part of the mesh
+    ad2, rep2 = ops.damage_solve(_dev(u), _dev(lb), _dev(a0), config=cfg)
+    assert rep2.iterations == rep.iterations and torch.equal(ad, ad2)
