@@ -288,3 +288,67 @@ class UnstructuredOperators:
             raise RuntimeError(f"damage VI did not converge in {report.iterations} iterations "
                                f"(|Phi| = {report.final_residual_norm:.3e})")
         return out, report
+
+    def am_load_step(self, u, alpha, alpha_lb, bc_dofs, bc_values, omega: float = 1.0,
+                     outer_atol: float = 1e-7, max_am_iterations: int = 1000,
+                     elastic_rtol: float = 1e-10, damage_atol_factor: float = 0.1,
+                     max_vi_iterations: int = 200):
+        """One load step of alternate minimisation on the element-list mesh (am_loop with an
+        absolute target, solver.py:129-241; oracle/am.py am_loop): elastic half-step (device PCG on
+        the Dirichlet-lifted Kuu), over-relaxed update u0 + omega (u* - u0), damage half-step
+        (``damage_solve``), relaxed damage with midpoint backtracking (relax_damage,
+        solver.py:202-215), until |(r_u with Dirichlet rows zero, Phi_FB(alpha, r_alpha))| <=
+        outer_atol.  Updates u and alpha in place; returns a dict of step statistics.  No body
+        force / inelastic strain on this path."""
+        import torch
+        from .vi import VIConfig
+        dofs = torch.as_tensor(np.asarray(bc_dofs, dtype=np.int64), device=u.device)
+        vals = torch.as_tensor(np.asarray(bc_values, dtype=np.float64), device=u.device)
+        self.set_dirichlet(np.asarray(bc_dofs, dtype=np.int64))
+        g = torch.zeros_like(u)
+        g[dofs] = vals
+        u[dofs] = vals
+        one = torch.ones_like(alpha)
+        vcfg = VIConfig(abs_tol=damage_atol_factor * outer_atol, max_iterations=max_vi_iterations)
+
+        def residual():
+            en, ru, ra = self.physics(u, alpha)
+            ru[dofs] = 0.0
+            x = alpha - alpha_lb
+            y = one - alpha
+            inner = torch.hypot(y, ra) - y + ra          # fb(hi - x, -F)
+            phi = torch.hypot(x, inner) - x - inner      # fb(x - lo, inner)
+            return float(torch.sqrt(torch.sum(ru * ru) + torch.sum(phi * phi))), en
+
+        res, en = residual()
+        stats = {"converged": res <= outer_atol, "am_iterations": 0, "krylov_iterations": 0,
+                 "omega_bar_min": omega, "residual_history": [res], "energy_history": [en]}
+        while not stats["converged"] and stats["am_iterations"] < max_am_iterations:
+            stats["am_iterations"] += 1
+            b = -self.apply_Kuu(alpha, g)
+            b[dofs] = vals
+            us, lrep = self.elastic_solve(alpha, b, rtol=elastic_rtol)
+            stats["krylov_iterations"] += lrep.iterations
+            u.add_(omega * (us - u))
+            u[dofs] = vals
+            a0 = alpha.clone()
+            a_star, vrep = self.damage_solve(u, alpha_lb, alpha, config=vcfg)
+            stats["krylov_iterations"] += vrep.total_krylov_iterations
+            wb, cand, k = omega, a_star, 0
+            if wb != 1.0:
+                cand = a0 + wb * (a_star - a0)
+                while bool(torch.any(cand < alpha_lb)) or bool(torch.any(cand > 1.0)):
+                    wb = 0.5 * (1.0 + wb)
+                    k += 1
+                    if k >= 60 or wb == 1.0:
+                        wb, cand = 1.0, a_star
+                        break
+                    cand = a0 + wb * (a_star - a0)
+            alpha.copy_(torch.minimum(torch.maximum(cand, alpha_lb), one))
+            stats["omega_bar_min"] = min(stats["omega_bar_min"], wb)
+            res, en = residual()
+            stats["residual_history"].append(res)
+            stats["energy_history"].append(en)
+            stats["converged"] = res <= outer_atol
+        stats["final_residual_norm"] = stats["residual_history"][-1]
+        return stats

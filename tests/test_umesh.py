@@ -306,3 +306,55 @@ def test_gpu_umesh_damage_solve_vs_oracle_rsls(dim, model):
     assert 0 < np.count_nonzero(ah > lb + 1e-12) < V  # the bound is active on part of the mesh
     ad2, rep2 = ops.damage_solve(_dev(u), _dev(lb), _dev(a0), config=cfg)
     assert rep2.iterations == rep.iterations and torch.equal(ad, ad2)
+
+
+def _am_case(model):
+    from oracle.p1 import MaterialSpec, P1Model
+    mesh = jitter_interior(grid_mesh(24, 12, 2.0, 1.0), 0.2, 4)
+    V = mesh.n_vertices
+    Gc, t = (0.05, 0.1) if model == "AT2" else (0.01, 0.45)
+    spec = MaterialSpec(E=1.0, nu=0.3, Gc=Gc, ell=0.15, k_ell=1e-6, model=model, regime="plane_strain")
+    left, right = mesh.boundary["left"], mesh.boundary["right"]
+    dofs = np.concatenate([2 * left, 2 * left + 1, 2 * right])
+    vals = np.concatenate([np.zeros(2 * left.size), np.full(right.size, t)])
+    order = np.argsort(dofs)
+    m = P1Model(mesh, spec)
+    m.bc = (dofs[order], vals[order])
+    lb = np.zeros(V)
+    return mesh, spec, m, dofs[order], vals[order], lb
+
+
+@pytest.mark.parametrize("model", ["AT1", "AT2"])
+def test_oracle_am_case_damages(model):
+    """The AM parity case loads past the damage threshold (oracle only, CPU)."""
+    from oracle.am import AMConfig, LoadState, am_loop
+    mesh, spec, m, dofs, vals, lb = _am_case(model)
+    st = LoadState.zeros(m, lb)
+    rep = am_loop(st, m, AMConfig(elastic_solver="direct", outer_atol=1e-7, max_am_iterations=400))
+    assert rep.converged and st.alpha.max() > 1e-3
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("model", ["AT1", "AT2"])
+def test_gpu_umesh_am_load_step_vs_oracle(model):
+    """One AM load step on a jittered mesh (elastic PCG + damage box QP on the element-list
+    path) against the oracle's am_loop with direct elastic solves: same fixed point."""
+    import torch
+    import paper_1511_08463_b200 as pf
+    from oracle.am import AMConfig, LoadState, am_loop
+    mesh, spec, m, dofs, vals, lb = _am_case(model)
+    st = LoadState.zeros(m, lb)
+    rep = am_loop(st, m, AMConfig(elastic_solver="direct", outer_atol=1e-7, max_am_iterations=400))
+    assert rep.converged
+    ops = pf.UnstructuredOperators(pf.UnstructuredMesh(mesh.vertices, mesh.elements),
+                                   pf.Material(E=1.0, nu=0.3, Gc=spec.Gc, ell=0.15, k_ell=1e-6,
+                                               regime="plane_strain"), model)
+    u = torch.zeros(2 * mesh.n_vertices, dtype=torch.float64, device="cuda")
+    a = torch.zeros(mesh.n_vertices, dtype=torch.float64, device="cuda")
+    stats = ops.am_load_step(u, a, _dev(lb), dofs, vals, outer_atol=1e-7, max_am_iterations=400)
+    assert stats["converged"] and stats["final_residual_norm"] <= 1e-7
+    assert abs(stats["am_iterations"] - rep.am_iterations) <= 2
+    assert np.max(np.abs(a.cpu().numpy() - st.alpha)) < 1e-5
+    assert rel(u.cpu().numpy(), st.u) < 1e-5
+    ref_en = m.energy(st.u, st.alpha)
+    assert abs(stats["energy_history"][-1][2] - ref_en[2]) <= 1e-6 * abs(ref_en[2])
