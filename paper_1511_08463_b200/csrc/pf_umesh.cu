@@ -128,11 +128,11 @@ __global__ void __launch_bounds__(256) k_umesh_Kuu2(
     const int32_t* __restrict__ adj, const uint8_t* __restrict__ vmask, const double* __restrict__ alpha,
     const double2* __restrict__ x, double2* __restrict__ y, int64_t nv, UParams p,
     double* __restrict__ part) {
-    const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (v >= nv) {
-        if (DOT) block_partial(0.0, part);
-        return;
-    }
+    // no early exit: every lane reaches the block reduction's full-mask shuffles (a lane past nv
+    // recomputes the last vertex and writes nothing)
+    const int64_t v0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool live = v0 < nv;
+    const int64_t v = live ? v0 : nv - 1;
     const uint8_t mv = vmask ? vmask[v] : 0;
     double y0 = 0.0, y1 = 0.0;
     const int k0 = rowptr[v], k1 = rowptr[v + 1];
@@ -172,10 +172,10 @@ __global__ void __launch_bounds__(256) k_umesh_Kuu2(
         if (mv & 1) y0 = xv.x;
         if (mv & 2) y1 = xv.y;
     }
-    y[v] = make_double2(y0, y1);
+    if (live) y[v] = make_double2(y0, y1);
     if (DOT) {
         const double2 xv = x[v];
-        block_partial(xv.x * y0 + xv.y * y1, part);
+        block_partial(live ? xv.x * y0 + xv.y * y1 : 0.0, part);
     }
 }
 
@@ -185,14 +185,14 @@ __global__ void __launch_bounds__(256) k_umesh_Kuu2(
 enum { KAA_APPLY = 0, KAA_PCG = 1, KAA_DIAG = 2 };
 
 template <int MODE>
-__device__ __forceinline__ void kaa_store(int64_t v, double acc, const double* __restrict__ x,
+__device__ __forceinline__ void kaa_store(bool live, int64_t v, double acc, const double* __restrict__ x,
                                           double* __restrict__ y, const double* __restrict__ dinv,
                                           double* __restrict__ part) {
     if (MODE == KAA_PCG) {
         if (dinv[v] == 0.0) acc = 0.0;
-        y[v] = acc;
-        block_partial(x[v] * acc, part);
-    } else {
+        if (live) y[v] = acc;
+        block_partial(live ? x[v] * acc : 0.0, part);
+    } else if (live) {
         y[v] = acc;
     }
 }
@@ -203,11 +203,11 @@ __global__ void __launch_bounds__(256) k_umesh_Kaa2(
     const int32_t* __restrict__ adj, const double2* __restrict__ u,
     const double* __restrict__ x, double* __restrict__ y, int64_t nv, UParams p,
     const double* __restrict__ dinv = nullptr, double* __restrict__ part = nullptr) {
-    const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (v >= nv) {
-        if (MODE == KAA_PCG) block_partial(0.0, part);
-        return;
-    }
+    // no early exit: every lane reaches the block reduction's full-mask shuffles (a lane past nv
+    // recomputes the last vertex and writes nothing)
+    const int64_t v0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool live = v0 < nv;
+    const int64_t v = live ? v0 : nv - 1;
     double acc = 0.0;
     const int k0 = rowptr[v], k1 = rowptr[v + 1];
     for (int k = k0; k < k1; ++k) {
@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(256) k_umesh_Kaa2(
         const double gyi = li == 0 ? r.gy[0] : (li == 1 ? r.gy[1] : r.gy[2]);
         acc += react * sx + 2.0 * kc * p.ell * (gxi * gxa + gyi * gya);
     }
-    kaa_store<MODE>(v, acc, x, y, dinv, part);
+    kaa_store<MODE>(live, v, acc, x, y, dinv, part);
 }
 
 // ---- 3D ------------------------------------------------------------------------------------
@@ -297,11 +297,11 @@ __global__ void __launch_bounds__(256) k_umesh_Kuu3(
     const double* __restrict__ rec, const int4* __restrict__ conn, const int32_t* __restrict__ rowptr,
     const int32_t* __restrict__ adj, const uint8_t* __restrict__ vmask, const double* __restrict__ alpha,
     const double* __restrict__ x, double* __restrict__ y, int64_t nv, UParams p, double* __restrict__ part) {
-    const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (v >= nv) {
-        if (DOT) block_partial(0.0, part);
-        return;
-    }
+    // no early exit: every lane reaches the block reduction's full-mask shuffles (a lane past nv
+    // recomputes the last vertex and writes nothing)
+    const int64_t v0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool live = v0 < nv;
+    const int64_t v = live ? v0 : nv - 1;
     double y0 = 0.0, y1 = 0.0, y2 = 0.0;
     const int k0 = rowptr[v], k1 = rowptr[v + 1];
     for (int k = k0; k < k1; ++k) {
@@ -334,10 +334,12 @@ __global__ void __launch_bounds__(256) k_umesh_Kuu3(
     if (mv & 1) y0 = x[3 * v];
     if (mv & 2) y1 = x[3 * v + 1];
     if (mv & 4) y2 = x[3 * v + 2];
-    y[3 * v] = y0;
-    y[3 * v + 1] = y1;
-    y[3 * v + 2] = y2;
-    if (DOT) block_partial(x[3 * v] * y0 + x[3 * v + 1] * y1 + x[3 * v + 2] * y2, part);
+    if (live) {
+        y[3 * v] = y0;
+        y[3 * v + 1] = y1;
+        y[3 * v + 2] = y2;
+    }
+    if (DOT) block_partial(live ? x[3 * v] * y0 + x[3 * v + 1] * y1 + x[3 * v + 2] * y2 : 0.0, part);
 }
 
 template <int MODE>
@@ -346,11 +348,11 @@ __global__ void __launch_bounds__(256) k_umesh_Kaa3(
     const int32_t* __restrict__ adj, const double* __restrict__ u,
     const double* __restrict__ x, double* __restrict__ y, int64_t nv, UParams p,
     const double* __restrict__ dinv = nullptr, double* __restrict__ part = nullptr) {
-    const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (v >= nv) {
-        if (MODE == KAA_PCG) block_partial(0.0, part);
-        return;
-    }
+    // no early exit: every lane reaches the block reduction's full-mask shuffles (a lane past nv
+    // recomputes the last vertex and writes nothing)
+    const int64_t v0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool live = v0 < nv;
+    const int64_t v = live ? v0 : nv - 1;
     double acc = 0.0;
     const int k0 = rowptr[v], k1 = rowptr[v + 1];
     for (int k = k0; k < k1; ++k) {
@@ -382,7 +384,7 @@ __global__ void __launch_bounds__(256) k_umesh_Kaa3(
         const double gi0 = pick4(r.g[0], li), gi1 = pick4(r.g[1], li), gi2 = pick4(r.g[2], li);
         acc += react * sx + 2.0 * kc * p.ell * (gi0 * ga[0] + gi1 * ga[1] + gi2 * ga[2]);
     }
-    kaa_store<MODE>(v, acc, x, y, dinv, part);
+    kaa_store<MODE>(live, v, acc, x, y, dinv, part);
 }
 
 // ---- Jacobi PCG (cg_solve, linalg.py:106-152) ---------------------------------------------
