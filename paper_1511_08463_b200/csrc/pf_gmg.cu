@@ -1233,11 +1233,12 @@ int gmg_setup(Ctx* c, cudaStream_t st) {
         int wpb = 8;
         while (wpb > 1 && smem + (int)sizeof(double) * wpb * n > 225 * 1024) --wpb;
         const int smem2 = smem + (int)sizeof(double) * wpb * n;
-        static bool attr = false;
-        if (!attr) {
+        static std::atomic<bool> attr[kMaxDev];
+        const int dv = cur_dev();
+        if (!attr[dv].load()) {
             cudaFuncSetAttribute(k_coarse_chol_band, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024);
             cudaFuncSetAttribute(k_coarse_inv_band, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024);
-            attr = true;
+            attr[dv] = true;
         }
         GKB(c, K_GMGSET, 2.0 * 8.0 * n * W, (k_coarse_chol_band<<<1, 1024, smem, st>>>(ldev(c, nl - 1), bw, c->gmg_dense)));
         GKB(c, K_GMGSET, 8.0 * n * W + 8.0 * n * n, (k_coarse_inv_band<<<(n + wpb - 1) / wpb, 32 * wpb, smem2, st>>>(
@@ -1397,8 +1398,12 @@ static int launch_coarse(Ctx* c, const double* r0, double* z0, cudaStream_t st, 
     static int ntrace_calls = 0;
     if (getenv("PF_GMG_TRACE") && !trace) cudaMalloc(&trace, 128 * sizeof(unsigned long long));
     a.trace = trace;
-    static int nb_cache = 0, nb_smem = -1;
-    if (nb_smem != smem) {
+    static int nb_cache_d[kMaxDev], nb_smem_d[kMaxDev];
+    static std::atomic<bool> nb_ok[kMaxDev];
+    const int dvc = cur_dev();
+    int& nb_cache = nb_cache_d[dvc];
+    int& nb_smem = nb_smem_d[dvc];
+    if (!nb_ok[dvc].load() || nb_smem != smem) {
         int dev = 0, nsm = 0, per = 0;
         GCU(c, cudaGetDevice(&dev), "device");
         GCU(c, cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev), "sm count");
@@ -1406,6 +1411,7 @@ static int launch_coarse(Ctx* c, const double* r0, double* z0, cudaStream_t st, 
         if (per < 1) return set_error(c, PF_ECUDA, "gmg: coarse-cycle kernel cannot be resident");
         nb_cache = nsm * per;
         nb_smem = smem;
+        nb_ok[dvc] = true;
     }
     // algorithmic bytes: those of the per-phase launches it replaces
     const int deg = a.deg;

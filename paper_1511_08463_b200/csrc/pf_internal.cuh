@@ -12,6 +12,8 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+
+#include <atomic>
 #include <string>
 #include <utility>
 #include <vector>
@@ -21,6 +23,15 @@
 #define PF_FULL 0xffffffffu
 
 namespace pf {
+
+// Per-device one-time launch setup (the >48 KB shared-memory opt-in and occupancy queries are
+// properties of a device context): slot of the current device in a static per-kernel table.
+constexpr int kMaxDev = 64;
+inline int cur_dev() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d & (kMaxDev - 1);
+}
 
 constexpr int kGmgRebuildIts = 12;  // excess PCG iterations that trigger a multigrid rebuild
 constexpr int kBlock = 256;        // threads per block for strip kernels

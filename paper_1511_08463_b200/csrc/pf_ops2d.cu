@@ -1534,11 +1534,12 @@ template <class Op, int PAT>
 static cudaError_t launch_pat(const Geo2& g, const Op& op, int nb, cudaStream_t st) {
     constexpr int smem = strip_smem<Op, PAT>();
     static_assert(smem <= 227 * 1024, "strip stage ring exceeds shared memory");
-    static bool attr = false;  // one-time opt-in above 48 KB per instantiation
-    if (!attr) {
+    static std::atomic<bool> attr[kMaxDev];  // one-time opt-in above 48 KB per instantiation and device
+    const int dv = cur_dev();
+    if (!attr[dv].load()) {
         cudaError_t e = cudaFuncSetAttribute(k_strip2d<Op, PAT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
-        attr = true;
+        attr[dv] = true;
     }
     k_strip2d<Op, PAT><<<nb, kBlock, smem, st>>>(g, op);
     return cudaSuccess;
@@ -1889,12 +1890,15 @@ static int launch_pcg_kaa1_pat(Ctx* c, const PcgBuffers& B, const double* kappa,
                                cudaStream_t st) {
     using Op = OpKaaCG1<MASKED>;
     constexpr int smem = strip_smem<Op, PAT>();
-    static int per = -1;
-    if (per < 0) {
+    static std::atomic<int> per_dev[kMaxDev];
+    const int dvp = cur_dev();
+    int per = per_dev[dvp].load();
+    if (per <= 0) {
         cudaError_t e = cudaFuncSetAttribute(k_pcg_kaa1<MASKED, PAT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return check_cuda(c, e, "persistent pcg attribute");
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_pcg_kaa1<MASKED, PAT>, kBlock, smem);
         if (e != cudaSuccess) return check_cuda(c, e, "persistent pcg occupancy");
+        per_dev[dvp] = per;
     }
     int dev = 0, nsm = 0;
     cudaGetDevice(&dev);
@@ -1947,12 +1951,15 @@ static int launch_pcg_kaa_pat(Ctx* c, const PcgBuffers& B, const double* kappa, 
                               cudaStream_t st) {
     using Op = OpKaa<true, MASKED>;
     constexpr int smem = strip_smem<Op, PAT>() * (NT / kBlock);  // strip rings of NT/32 warps
-    static int per = -1;
-    if (per < 0) {
+    static std::atomic<int> per_dev[kMaxDev];
+    const int dvp = cur_dev();
+    int per = per_dev[dvp].load();
+    if (per <= 0) {
         cudaError_t e = cudaFuncSetAttribute(k_pcg_kaa<MASKED, PAT, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return check_cuda(c, e, "persistent pcg attribute");
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_pcg_kaa<MASKED, PAT, NT>, NT, smem);
         if (e != cudaSuccess) return check_cuda(c, e, "persistent pcg occupancy");
+        per_dev[dvp] = per;
     }
     int dev = 0, nsm = 0;
     cudaGetDevice(&dev);

@@ -1205,11 +1205,12 @@ static int run3g(Ctx* c, const Geo3& g0, Op op, cudaStream_t st, int kind, doubl
     if (kW3 != 8 || MinBlocksOf<Op>::v != 2) tile3(g, kW3 - 2, 148 * MinBlocksOf<Op>::v);  // Geo3's own tiling: 8 warps x 2
     constexpr int smem = strip3_smem<Op, kW3>();
     static_assert(smem <= 227 * 1024, "3D stage ring exceeds shared memory");
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<bool> attr[kMaxDev];
+    const int dv = cur_dev();
+    if (!attr[dv].load()) {
         cudaError_t e = cudaFuncSetAttribute(k_strip3d<Op, kW3, MinBlocksOf<Op>::v>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return check_cuda(c, e, "3D kernel attribute");
-        attr = true;
+        attr[dv] = true;
     }
     const long long nb = (long long)g.nbj * g.nbk * g.nstrips;
     if (nb > kMaxBlocksRed) return set_error(c, PF_EINVAL, "3D grid too large for the reduction buffer");
@@ -1388,12 +1389,15 @@ static int launch3_pcg_kaa_m(Ctx* c, const PcgBuffers& B, const double* kappa, c
                              cudaStream_t st) {
     using Op = Op3Kaa<true, MASKED>;
     constexpr int smem = strip3_smem<Op, kW3>();
-    static int per = -1;
-    if (per < 0) {
+    static std::atomic<int> per_dev[kMaxDev];
+    const int dvp = cur_dev();
+    int per = per_dev[dvp].load();
+    if (per <= 0) {
         cudaError_t e = cudaFuncSetAttribute(k_pcg_kaa3<MASKED>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return check_cuda(c, e, "persistent 3D pcg attribute");
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_pcg_kaa3<MASKED>, kW3 * 32, smem);
         if (e != cudaSuccess) return check_cuda(c, e, "persistent 3D pcg occupancy");
+        per_dev[dvp] = per;
     }
     int dev = 0, nsm = 0;
     cudaGetDevice(&dev);

@@ -466,7 +466,9 @@ __global__ void __launch_bounds__(256) k_umesh_pcg_update(
     double* __restrict__ part, int64_t n, int nb, int slot) {
     const double pq = scal[2];
     const double a = pq > 0.0 ? scal[slot] / pq : 0.0;
-    if (!(pq > 0.0) && blockIdx.x == 0 && threadIdx.x == 0) scal[4] = 1.0;
+    // breakdown only for a nonzero residual: r = 0 exactly (a converged solve that is still being
+    // iterated between host polls) gives p = 0 and p.q = 0 legitimately
+    if (!(pq > 0.0) && scal[slot] != 0.0 && blockIdx.x == 0 && threadIdx.x == 0) scal[4] = 1.0;
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     double rz = 0.0, rr = 0.0;
     if (i < n) {
@@ -675,6 +677,45 @@ __global__ void __launch_bounds__(256) k_umesh_vi_cand(
     if (v >= nv) return;
     const double c = a[v] + (d ? t * d[v] : 0.0);
     out[v] = fmin(fmax(c, lb[v]), 1.0);
+}
+
+// Merit-gradient ingredients on the box [lb, 1] (vi.py:144-178, the structured k_merit_parts):
+// pphi = p * phi and w = q * phi; the gradient of |Phi|^2 is 2 (pphi + Kaa w) (Kaa symmetric).
+__device__ __forceinline__ void fb_part_u(double a, double b, double& pa, double& pb) {
+    const double rho = hypot(a, b);
+    if (rho > 0.0) { pa = a / rho - 1.0; pb = b / rho - 1.0; }
+    else { pa = 0.70710678118654752440 - 1.0; pb = pa; }
+}
+__global__ void __launch_bounds__(256) k_umesh_merit_parts(
+    const double* __restrict__ a, const double* __restrict__ g, const double* __restrict__ lb,
+    double* __restrict__ pphi, double* __restrict__ w, int64_t nv) {
+    const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= nv) return;
+    const double xv = a[v], Fv = g[v], sl = 1.0 - xv, lo = lb[v];
+    const double inner = fbf(sl, -Fv);
+    double pao, pbo, pai, pbi;
+    fb_part_u(xv - lo, inner, pao, pbo);
+    fb_part_u(sl, -Fv, pai, pbi);
+    const double ph = fbf(xv - lo, inner);
+    pphi[v] = (pao - pbo * pai) * ph;
+    w[v] = -pbo * pbi * ph;
+}
+__global__ void __launch_bounds__(256) k_scale_u(double* __restrict__ x, double a, int64_t n) {
+    const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v < n) x[v] *= a;
+}
+// gm = 2 (pphi + kw) (in place into kw) and block partials of |gm|^2
+__global__ void __launch_bounds__(256) k_umesh_grad_finish(const double* __restrict__ pphi,
+                                                           double* __restrict__ kw, double* __restrict__ part,
+                                                           int64_t nv) {
+    const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    double g2 = 0.0;
+    if (v < nv) {
+        const double gv = 2.0 * (pphi[v] + kw[v]);
+        kw[v] = gv;
+        g2 = gv * gv;
+    }
+    block_partial(g2, part);
 }
 
 int fail(pf_umesh* m, int code, const std::string& msg) {
@@ -1074,6 +1115,8 @@ int pf_umesh_damage_solve(pf_umesh* m, const double* u, const double* alpha_lb, 
         rep->final_residual_norm = std::sqrt(merit);
         if (std::sqrt(merit) <= o->abs_tol) { rep->converged = 1; break; }
         if (it >= maxit) break;
+        ++it;
+        rep->iterations = it;  // counted at the start of the iteration, as vi.py:219
         // reduced Newton system K_II d_I = -g_I by Jacobi PCG (rhs in q, d = 0 on the active rows)
         cudaMemsetAsync(m->scal, 0, 5 * sizeof(double), s);
         k_umesh_pcg_init<<<nb, 256, 0, s>>>(q, d, r, z, pv, dinv, m->part, nv, nb);
@@ -1106,26 +1149,60 @@ int pf_umesh_damage_solve(pf_umesh* m, const double* u, const double* alpha_lb, 
         }
         rep->total_krylov_iterations += k;
         if (rn > tol) rep->linear_failures++;
-        // projected step with Armijo backtracking on the merit 1/2 |Phi|^2
-        double t = 1.0, mnew = merit;
-        while (true) {
-            k_umesh_vi_cand<<<gv, 256, 0, s>>>(a, d, alpha_lb, t, cand, nv);
-            grad(cand);
-            k_umesh_vi_prep<<<gv, 256, 0, s>>>(cand, g, alpha_lb, diag, dinv, q, m->part, nv, zeta);
-            k_umesh_reduce<<<1, 1024, 0, s>>>(m->part, nb, 1, m->scal, 7, 7);
-            m->launches += 4;
+        // projected Newton step with Armijo backtracking on |Phi|^2 (vi.py:207-240); on failure a
+        // steepest-descent step on the merit (vi.py:241-252); no descent along either: stall
+        // (vi.py:253-254) -- a trial that fails its test is never accepted
+        auto line_search = [&](const double* dir, double slope, bool newton, bool& ok) -> cudaError_t {
+            ok = false;
+            for (double t = 1.0; t >= tmin; t *= bt) {
+                k_umesh_vi_cand<<<gv, 256, 0, s>>>(a, dir, alpha_lb, t, cand, nv);
+                grad(cand);
+                k_umesh_vi_prep<<<gv, 256, 0, s>>>(cand, g, alpha_lb, diag, dinv, q, m->part, nv, zeta);
+                k_umesh_reduce<<<1, 1024, 0, s>>>(m->part, nb, 1, m->scal, 7, 7);
+                m->launches += 4;
+                cudaError_t le = poll();
+                if (le != cudaSuccess) return le;
+                const double mt = h[7];
+                const double bound = newton ? (1.0 - 2.0 * o->armijo * t) * merit : merit - slope * t;
+                if (mt <= bound) {
+                    ok = true;
+                    merit = mt;
+                    return cudaMemcpyAsync(a, cand, nv * 8, cudaMemcpyDeviceToDevice, s);
+                }
+            }
+            return cudaSuccess;
+        };
+        bool ok = false;
+        if ((e = line_search(d, 0.0, true, ok)) != cudaSuccess) return cuda_fail(m, e);
+        if (!ok) {
+            grad(a);  // g at the current iterate (the trials overwrote it)
+            k_umesh_merit_parts<<<gv, 256, 0, s>>>(a, g, alpha_lb, z, r, nv);
+            if (m->dim == 2)
+                k_umesh_Kaa2<KAA_APPLY><<<gv, 256, 0, s>>>(m->rec, conn, m->rowptr, m->adj,
+                                                           reinterpret_cast<const double2*>(u), r, pv, nv, p);
+            else
+                k_umesh_Kaa3<KAA_APPLY><<<gv, 256, 0, s>>>(m->rec, conn, m->rowptr, m->adj, u, r, pv, nv, p);
+            k_umesh_grad_finish<<<gv, 256, 0, s>>>(z, pv, m->part, nv);
+            k_umesh_reduce<<<1, 1024, 0, s>>>(m->part, nb, 1, m->scal, 6, 6);
+            m->launches += 5;
             if ((e = poll()) != cudaSuccess) return cuda_fail(m, e);
-            mnew = h[7];
-            if (mnew <= (1.0 - 2.0 * o->armijo * t) * merit || t * bt < tmin) break;
-            t *= bt;
+            const double gn = std::sqrt(h[6]);
+            if (gn > 0.0) {
+                const double sc = 1.0 / std::max(1.0, gn);
+                k_scale_u<<<gv, 256, 0, s>>>(pv, -sc, nv);
+                m->launches++;
+                if ((e = line_search(pv, o->armijo * sc * gn * gn, false, ok)) != cudaSuccess) return cuda_fail(m, e);
+                rep->steepest_descent_steps++;
+            }
+            if (!ok) {  // the prep buffers (dinv, rhs) must describe the current iterate again
+                k_umesh_vi_prep<<<gv, 256, 0, s>>>(a, g, alpha_lb, diag, dinv, q, m->part, nv, zeta);
+                m->launches++;
+            }
         }
-        if ((e = cudaMemcpyAsync(a, cand, nv * 8, cudaMemcpyDeviceToDevice, s)) != cudaSuccess)
-            return cuda_fail(m, e);
-        merit = mnew;
-        ++it;
-        rep->iterations = it;
+        if (!ok) break;
         record();
     }
+    rep->final_residual_norm = std::sqrt(merit);
     if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(m, e);
     rep->status = rep->converged ? PF_OK : PF_ESTALL;
     return PF_OK;

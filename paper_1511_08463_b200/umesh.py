@@ -321,9 +321,11 @@ class UnstructuredOperators:
             return float(torch.sqrt(torch.sum(ru * ru) + torch.sum(phi * phi))), en
 
         res, en = residual()
-        stats = {"converged": res <= outer_atol, "am_iterations": 0, "krylov_iterations": 0,
-                 "omega_bar_min": omega, "residual_history": [res], "energy_history": [en]}
-        while not stats["converged"] and stats["am_iterations"] < max_am_iterations:
+        stats = {"converged": False, "am_iterations": 0, "krylov_iterations": 0,
+                 "omega_bar_min": omega, "residual_history": [res], "energy_history": [en],
+                 "vi_unconverged": 0, "vi_steepest_descent_steps": 0}
+        # at least one AM iteration, as the reference loop (solver.py:186-241; oracle am_loop)
+        while stats["am_iterations"] < max_am_iterations:
             stats["am_iterations"] += 1
             b = -self.apply_Kuu(alpha, g)
             b[dofs] = vals
@@ -332,8 +334,12 @@ class UnstructuredOperators:
             u.add_(omega * (us - u))
             u[dofs] = vals
             a0 = alpha.clone()
-            a_star, vrep = self.damage_solve(u, alpha_lb, alpha, config=vcfg)
+            # an unconverged damage VI returns its iterate and the AM loop carries on, as the
+            # reference damage_step (solver.py:145-160)
+            a_star, vrep = self.damage_solve(u, alpha_lb, alpha, config=vcfg, raise_on_failure=False)
             stats["krylov_iterations"] += vrep.total_krylov_iterations
+            stats["vi_unconverged"] += 0 if vrep.converged else 1
+            stats["vi_steepest_descent_steps"] += vrep.steepest_descent_steps
             wb, cand, k = omega, a_star, 0
             if wb != 1.0:
                 cand = a0 + wb * (a_star - a0)
@@ -350,5 +356,7 @@ class UnstructuredOperators:
             stats["residual_history"].append(res)
             stats["energy_history"].append(en)
             stats["converged"] = res <= outer_atol
+            if stats["converged"]:
+                break
         stats["final_residual_norm"] = stats["residual_history"][-1]
         return stats

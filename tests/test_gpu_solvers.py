@@ -332,3 +332,40 @@ def test_persistent_damage_pcg_matches_graph_loop(pattern, shape, variant, monke
     assert r0.iterations == r1.iterations
     assert abs(r0.total_krylov_iterations - r1.total_krylov_iterations) <= r0.iterations
     assert float((a0 - a1).abs().max()) < 1e-9
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_damage_steepest_descent_fallback_matches_oracle_rsls(seed):
+    """rsls' merit-gradient fallback (vi.py:241-256): with armijo = 0.6 the Newton bound
+    (1 - 2 armijo mu) merit is negative for every tried step (ls_min_step = 0.6 leaves mu = 1 only),
+    so each iteration takes a steepest-descent step on |Phi|^2 until that fails too (stagnation
+    break) or the iteration budget ends.  Device and oracle take the same steps."""
+    import ctypes as C
+    import paper_1511_08463_b200 as pf
+    from paper_1511_08463_b200 import _lib
+    from paper_1511_08463_b200.fem import _stream
+    from paper_1511_08463_b200.vi import ActiveSetReport, VIConfig
+    from oracle.mcp import RSLSConfig, rsls
+    prob, om, _ = make_pair("union_jack", "plane_stress", "AT1", 20, 11)
+    rng = np.random.default_rng(seed)
+    V = om.nv
+    lb = rng.uniform(0.0, 0.3, V)
+    a0 = lb + rng.uniform(0, 1, V) * (1 - lb)
+    u = rng.standard_normal(om.nu_dofs) * 0.4
+    K = om.Kaa(u, a0)
+    c = om.residual_alpha(u, a0) - K @ a0
+    xo, so = rsls(lambda a: K @ a + c, lambda a: K, lb, np.ones(V), a0,
+                  RSLSConfig(abs_tol=1e-10, ls_min_step=0.6, armijo=0.6, max_iterations=8),
+                  jac_matvec=lambda J: (lambda v: J.T @ v))
+    assert so.steepest_descent_steps >= 7 and not so.converged
+    vic = VIConfig(abs_tol=1e-10, ls_min_step=0.6, armijo=0.6, max_iterations=8, inner_rtol=1e-13)
+    rep = _lib.VIReport()
+    out = torch.empty(V, dtype=torch.float64, device="cuda")
+    ud, lbd, ad = dev(u), dev(lb), dev(a0)
+    prob.call("pf_damage_solve", _lib.ptr(ud), _lib.ptr(lbd), _lib.ptr(ad), _lib.ptr(out),
+              C.byref(vic.to_c()), C.byref(rep), _stream())
+    r = ActiveSetReport.from_c(rep)
+    assert (r.iterations, r.steepest_descent_steps, r.converged) == \
+        (so.iterations, so.steepest_descent_steps, so.converged)
+    assert abs(r.final_residual_norm - so.final_residual_norm) <= 1e-9 * so.final_residual_norm
+    assert np.max(np.abs(host(out) - xo)) < 1e-10

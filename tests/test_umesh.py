@@ -358,3 +358,38 @@ def test_gpu_umesh_am_load_step_vs_oracle(model):
     assert rel(u.cpu().numpy(), st.u) < 1e-5
     ref_en = m.energy(st.u, st.alpha)
     assert abs(stats["energy_history"][-1][2] - ref_en[2]) <= 1e-6 * abs(ref_en[2])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", [0, 1])
+def test_gpu_umesh_damage_steepest_descent_fallback(seed):
+    """Element-list damage VI: the merit-gradient fallback and the stagnation break of rsls
+    (vi.py:241-256), forced by armijo = 0.6 with ls_min_step = 0.6 (every Newton trial fails):
+    same iterations, steepest-descent steps and iterate as the oracle; a trial that fails its
+    Armijo test is never accepted (the merit never increases)."""
+    import paper_1511_08463_b200 as pf
+    from oracle.mcp import RSLSConfig, rsls
+    from paper_1511_08463_b200.vi import VIConfig
+    om_mesh = jitter_interior(grid_mesh(20, 11, 1.3, 0.9), 0.2, 3)
+    V = om_mesh.n_vertices
+    spec = MaterialSpec(E=1.7, nu=0.27, Gc=1.3, ell=0.1, k_ell=1e-6, model="AT1", regime="plane_stress")
+    om = P1Model(om_mesh, spec)
+    rng = np.random.default_rng(seed)
+    lb = rng.uniform(0.0, 0.3, V)
+    a0 = lb + rng.uniform(0, 1, V) * (1 - lb)
+    u = rng.standard_normal(2 * V) * 0.4
+    K = om.Kaa(u, a0)
+    c = om.residual_alpha(u, a0) - K @ a0
+    xo, so = rsls(lambda a: K @ a + c, lambda a: K, lb, np.ones(V), a0,
+                  RSLSConfig(abs_tol=1e-10, ls_min_step=0.6, armijo=0.6, max_iterations=8),
+                  jac_matvec=lambda J: (lambda v: J.T @ v))
+    assert so.steepest_descent_steps >= 1
+    ops = pf.UnstructuredOperators(pf.UnstructuredMesh(om_mesh.vertices, om_mesh.elements),
+                                   pf.Material(E=1.7, nu=0.27, Gc=1.3, ell=0.1, k_ell=1e-6), "AT1")
+    cfg = VIConfig(abs_tol=1e-10, ls_min_step=0.6, armijo=0.6, max_iterations=8, inner_rtol=1e-13)
+    ad, rep = ops.damage_solve(_dev(u), _dev(lb), _dev(a0), config=cfg, raise_on_failure=False)
+    assert (rep.iterations, rep.steepest_descent_steps, rep.converged) == \
+        (so.iterations, so.steepest_descent_steps, so.converged)
+    assert np.max(np.abs(ad.cpu().numpy() - xo)) < 1e-10
+    h = rep.residual_history
+    assert all(h[k + 1] <= h[k] for k in range(len(h) - 1))
