@@ -987,6 +987,8 @@ void pf_ctx_destroy(pf_ctx* c) {
     for (auto e : c->prof.ev) cudaEventDestroy(e);
     for (auto& ge : c->graph_exec)
         if (ge) cudaGraphExecDestroy(ge);
+    for (auto& ge : c->mr_exec)
+        if (ge) cudaGraphExecDestroy(ge);
     if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
     if (c->h_scal) cudaFreeHost(c->h_scal);
     delete c;

@@ -333,6 +333,12 @@ struct Ctx {
     long long graph_key[3] = {-1, -1, -1};
     const void* graph_ptrs[3][kGraphPtrs] = {};
     long long geo_version = 0;   // bumped whenever Geo2 fields baked into kernels change
+    // device-resident MINRES of the Newton phase (pf_newton.cu): one graph per Newton-iterate
+    // buffer (the line search ping-pongs two), keyed on the pointers and sizes it bakes in
+    static constexpr int kMrKey = 12;
+    cudaGraphExec_t mr_exec[2] = {nullptr, nullptr};
+    long long mr_nodes[2] = {0, 0};
+    long long mr_key[2][kMrKey] = {};
 };
 
 #define PF_TRY_GMG(x)                   \

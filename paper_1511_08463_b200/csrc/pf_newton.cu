@@ -132,6 +132,146 @@ __global__ void k_nchebk(long long n, const double* dinv, const double* Cd, doub
     }
 }
 
+// ---- device-resident MINRES (fixed block preconditioners, inner_mode 1/2) --------------------
+// The Paige-Saunders recurrence of linalg.py:155-219 with every scalar in device memory and every
+// vector in a fixed buffer (the host loop rotates buffer pointers; here the rotation is data
+// movement fused into the vector passes), so one iteration is a fixed sequence of launches that a
+// CUDA graph replays under a WHILE node: no host round trip per iteration.
+constexpr int S_MR = 80;  // MINRES state slots
+enum {
+    MR_BETA = 0, MR_OLDB, MR_DBAR, MR_EPS, MR_PHIBAR, MR_CS, MR_SN, MR_TARGET, MR_IT, MR_MAXIT, MR_DONE,
+    MR_FAIL, MR_ALFA, MR_BB, MR_OLDEPS, MR_DELTA, MR_GAM, MR_PHI
+};
+constexpr int S_CHEB = 100;  // Chebyshev table of the C block: [0] = 1/theta, [2k-1], [2k] = a_k, b_k
+constexpr int kMaxChebDeg = 14;
+
+__global__ void k_mr_start(double* s, double rtol, double maxit) {
+    double* m = s + S_MR;
+    const double bb = m[MR_BB];
+    const double b1 = bb > 0.0 ? sqrt(bb) : 0.0;
+    m[MR_BETA] = b1; m[MR_OLDB] = 0.0; m[MR_DBAR] = 0.0; m[MR_EPS] = 0.0; m[MR_PHIBAR] = b1;
+    m[MR_CS] = -1.0; m[MR_SN] = 0.0; m[MR_TARGET] = rtol * b1; m[MR_IT] = 0.0; m[MR_MAXIT] = maxit;
+    m[MR_FAIL] = bb < 0.0 ? 1.0 : 0.0;
+    m[MR_DONE] = (bb <= 0.0) ? 1.0 : 0.0;
+}
+// v = y / beta
+__global__ void k_mr_v(long long n, const double* __restrict__ y, double* __restrict__ v, const double* s) {
+    const double ib = 1.0 / s[S_MR + MR_BETA];
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        v[i] = y[i] * ib;
+}
+// t -= (beta / oldb) r1 (not on the first iteration) ; alfa = v . t
+__global__ void k_mr_a(long long n, double* __restrict__ t, const double* __restrict__ r1, const double* __restrict__ v,
+                       double* s, RedBuf rb) {
+    const double* m = s + S_MR;
+    const double f = m[MR_IT] >= 1.0 ? m[MR_BETA] / m[MR_OLDB] : 0.0;
+    double acc[1] = {0.0};
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const double ti = t[i] - f * r1[i];
+        t[i] = ti;
+        acc[0] += v[i] * ti;
+    }
+    grid_reduce<1>(acc, rb, 8, [=](double* tt) { s[S_MR + MR_ALFA] = tt[0]; });
+}
+// r1 <- r2 ; r2 <- t - (alfa / beta) r2
+__global__ void k_mr_b(long long n, const double* __restrict__ t, double* __restrict__ r1, double* __restrict__ r2,
+                       const double* s) {
+    const double f = s[S_MR + MR_ALFA] / s[S_MR + MR_BETA];
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const double a = r2[i];
+        r1[i] = a;
+        r2[i] = t[i] - f * a;
+    }
+}
+// bb = r2 . y
+__global__ void k_mr_dot(long long n, const double* __restrict__ a, const double* __restrict__ b, double* s,
+                         RedBuf rb) {
+    double acc[1] = {0.0};
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        acc[0] += a[i] * b[i];
+    grid_reduce<1>(acc, rb, 8, [=](double* tt) { s[S_MR + MR_BB] = tt[0]; });
+}
+// the Givens rotation of one iteration (the host loop's scalar block, minres above)
+__global__ void k_mr_rot(double* s) {
+    double* m = s + S_MR;
+    const double bb = m[MR_BB];
+    if (bb < 0.0) { m[MR_FAIL] = 1.0; m[MR_DONE] = 1.0; return; }
+    const double alfa = m[MR_ALFA];
+    m[MR_OLDB] = m[MR_BETA];
+    const double beta = sqrt(bb);
+    m[MR_BETA] = beta;
+    const double cs = m[MR_CS], sn = m[MR_SN], dbar = m[MR_DBAR];
+    m[MR_OLDEPS] = m[MR_EPS];
+    m[MR_DELTA] = cs * dbar + sn * alfa;
+    const double gbar = sn * dbar - cs * alfa;
+    m[MR_EPS] = sn * beta;
+    m[MR_DBAR] = -cs * beta;
+    const double gam = fmax(hypot(gbar, beta), 2.220446049250313e-16);
+    m[MR_GAM] = gam;
+    const double csn = gbar / gam, snn = beta / gam;
+    m[MR_CS] = csn;
+    m[MR_SN] = snn;
+    m[MR_PHI] = csn * m[MR_PHIBAR];
+    m[MR_PHIBAR] = snn * m[MR_PHIBAR];
+    m[MR_IT] += 1.0;
+    m[MR_DONE] = (m[MR_PHIBAR] <= m[MR_TARGET] || m[MR_IT] >= m[MR_MAXIT]) ? 1.0 : 0.0;
+}
+// (w1, w2) <- (w2, w) ; w = (v - oldeps w1 - delta w2) / gam ; x += phi w   [wa = w2, wb = w]
+__global__ void k_mr_w(long long n, const double* __restrict__ v, double* __restrict__ wa, double* __restrict__ wb,
+                       double* __restrict__ x, const double* s) {
+    const double* m = s + S_MR;
+    if (m[MR_FAIL] != 0.0) return;
+    const double oe = m[MR_OLDEPS], de = m[MR_DELTA], ig = 1.0 / m[MR_GAM], ph = m[MR_PHI];
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const double a = wa[i], b = wb[i];
+        const double w = (v[i] - oe * a - de * b) * ig;
+        wa[i] = b;
+        wb[i] = w;
+        x[i] += ph * w;
+    }
+}
+__global__ void k_mr_cond(cudaGraphConditionalHandle h, const double* s) {
+    if (threadIdx.x == 0) cudaGraphSetConditional(h, s[S_MR + MR_DONE] == 0.0 ? 1u : 0u);
+}
+// Chebyshev coefficients of the C block on the device (from |D^-1 C x|^2 in S_AUX1, lambda_C)
+__global__ void k_cheb_table(double* s, int deg, double safety) {
+    double lmax = sqrt(s[S_AUX1]);
+    if (!(lmax > 0.0) || !isfinite(lmax)) lmax = 1.0;
+    const double hi = safety * lmax, lo = hi / 30.0;
+    const double theta = 0.5 * (hi + lo), delta = 0.5 * (hi - lo), sigma = theta / delta;
+    double* t = s + S_CHEB;
+    t[0] = 1.0 / theta;
+    double rho = 1.0 / sigma;
+    for (int k = 1; k < deg; ++k) {
+        const double rn = 1.0 / (2.0 * sigma - rho);
+        t[2 * k - 1] = rn * rho;
+        t[2 * k] = 2.0 * rn / delta;
+        rho = rn;
+    }
+}
+__global__ void k_ncheb0_d(long long n, const double* dinv, const double* b, double* r, double* d, double* x,
+                           const double* s) {
+    const double ith = s[S_CHEB];
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const double ri = b[i];
+        const double di = dinv[i] * ri * ith;
+        r[i] = ri;
+        d[i] = di;
+        x[i] = di;
+    }
+}
+__global__ void k_nchebk_d(long long n, const double* dinv, const double* Cd, double* r, double* d, double* x,
+                           const double* s, int k) {
+    const double a = s[S_CHEB + 2 * k - 1], b = s[S_CHEB + 2 * k];
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const double ri = r[i] - Cd[i];
+        const double di = a * d[i] + b * dinv[i] * ri;
+        r[i] = ri;
+        d[i] = di;
+        x[i] += di;
+    }
+}
+
 static int nblocks(long long n) { return (int)std::max(1LL, std::min((n + kNB - 1) / kNB, 148LL * 8)); }
 
 #define NTRY(x)                        \
@@ -241,6 +381,21 @@ static int cheb_C(Ctx* c, const double* b, double* x, double lmax, int deg, long
     its += deg;
     return PF_OK;
 }
+// the same polynomial with its coefficients read from the device table (graph-capturable)
+static int cheb_C_dev(Ctx* c, const double* b, double* x, int deg, long long& its, cudaStream_t st) {
+    const long long n = c->n_a;
+    const int nb = nblocks(n);
+    double *r = c->da_r, *d = c->da_p0, *Cd = c->da_q;
+    k_ncheb0_d<<<nb, kNB, 0, st>>>(n, c->da_dinv, b, r, d, x, c->scal);
+    c->launches++;
+    for (int k = 1; k < deg; ++k) {
+        NTRY(launch_Kaa(c, c->kappa, d, Cd, c->act, st));
+        k_nchebk_d<<<nb, kNB, 0, st>>>(n, c->da_dinv, Cd, r, d, x, c->scal, k);
+        c->launches++;
+    }
+    its += deg;
+    return PF_OK;
+}
 // x = one multigrid V-cycle applied to b (hierarchy of the current alpha; a fixed SPD operator)
 static int vcycle_A(Ctx* c, const double* b, double* x, long long& its, cudaStream_t st) {
     if (c->dim == 3) NTRY(gmg3_vcycle(c, b, x, st, nullptr));
@@ -253,6 +408,7 @@ static int vcycle_A(Ctx* c, const double* b, double* x, long long& its, cudaStre
 struct InnerMg {  // inner_mode 1 (multiplicative) / 2 (additive)
     bool on = false;
     bool additive = false;
+    bool dev = false;  // Chebyshev coefficients from the device table (k_cheb_table)
     int deg = 12;
     double lmax = 0.0;
 };
@@ -265,7 +421,7 @@ static int fieldsplit(Ctx* c, const NewtonWs& w, const double* r, double* y, con
         NTRY(vcycle_A(c, r, y1, its, st));
         k_nsubmask<<<nblocks(na), kNB, 0, st>>>(na, r + nu, nullptr, c->act, w.TMP + nu);
         c->launches++;
-        NTRY(cheb_C(c, w.TMP + nu, z, mg.lmax, mg.deg, its, st));
+        NTRY(mg.dev ? cheb_C_dev(c, w.TMP + nu, z, mg.deg, its, st) : cheb_C(c, w.TMP + nu, z, mg.lmax, mg.deg, its, st));
         return PF_OK;
     }
     if (mg.on) {
@@ -273,7 +429,7 @@ static int fieldsplit(Ctx* c, const NewtonWs& w, const double* r, double* y, con
         NTRY(launch_Kau(c, u, alpha, y1, w.TMP + nu, PF_BC_ELIMINATE, st));            // B^T y1
         k_nsubmask<<<nblocks(na), kNB, 0, st>>>(na, r + nu, w.TMP + nu, c->act, w.TMP + nu);
         c->launches++;
-        NTRY(cheb_C(c, w.TMP + nu, z, mg.lmax, mg.deg, its, st));
+        NTRY(mg.dev ? cheb_C_dev(c, w.TMP + nu, z, mg.deg, its, st) : cheb_C(c, w.TMP + nu, z, mg.lmax, mg.deg, its, st));
         NTRY(launch_Kua(c, u, alpha, z, w.TMP, PF_BC_ELIMINATE, st));                   // B z
         NTRY(vcycle_A(c, w.TMP, w.G, its, st));
         k_naxpy<<<nblocks(nu), kNB, 0, st>>>(nu, -1.0, w.G, y1);
@@ -363,6 +519,106 @@ static int minres(Ctx* c, NewtonWs& w, const double* u, const double* alpha, con
     return PF_OK;
 }
 
+// MINRES with the state on the device (fixed block preconditioners only): one eager start-up
+// (r1 = rhs, y = M r1, beta1) and then a WHILE-node graph over one iteration; one host read at the
+// end.  Same recurrence, buffers and counting as minres() above.
+static int minres_dev(Ctx* c, NewtonWs& w, const double* u, const double* alpha, const double* rhs, double* x,
+                      double rtol, long long maxit, long long& kits, bool& converged, cudaStream_t st,
+                      const InnerMg& mg) {
+    const long long n = w.n, nu = w.nu;
+    const RedBuf rb{c->partials, c->tickets, c->scal};
+    const int nb = nblocks(n);
+    double *R1 = w.R1, *R2 = w.R2, *Y = w.Y, *V = w.V, *T = w.W, *Wa = w.W1, *Wb = w.W2;
+    NCU(c, cudaMemsetAsync(x, 0, sizeof(double) * n, st), "memset");
+    NCU(c, cudaMemsetAsync(Wa, 0, sizeof(double) * n, st), "memset");
+    NCU(c, cudaMemsetAsync(Wb, 0, sizeof(double) * n, st), "memset");
+    NCU(c, cudaMemcpyAsync(R1, rhs, sizeof(double) * n, cudaMemcpyDeviceToDevice, st), "copy");
+    NCU(c, cudaMemcpyAsync(R2, rhs, sizeof(double) * n, cudaMemcpyDeviceToDevice, st), "copy");
+    long long fs_its = 0;
+    NTRY(fieldsplit(c, w, R1, Y, u, alpha, 0.0, 0, fs_its, st, mg));
+    k_mr_dot<<<nb, kNB, 0, st>>>(n, R1, Y, c->scal, rb);
+    k_mr_start<<<1, 1, 0, st>>>(c->scal, rtol, (double)maxit);
+    c->launches += 2;
+    kits += fs_its;
+    long long key[Ctx::kMrKey] = {(long long)(uintptr_t)u, (long long)(uintptr_t)alpha, (long long)(uintptr_t)x,
+                                 (long long)(uintptr_t)R1, c->geo_version, (long long)c->glev.size(),
+                                 c->gmg_degree, mg.deg, mg.additive ? 1 : 0, n, nu, c->dim};
+    int slot = -1;
+    for (int q = 0; q < 2; ++q)
+        if (c->mr_exec[q] && memcmp(c->mr_key[q], key, sizeof key) == 0) slot = q;
+    if (slot < 0) {  // capture one iteration under a WHILE node (replace the older slot)
+        // the slot last used with this iterate buffer (stale after a geometry change), else the other
+        const long long up = (long long)(uintptr_t)u;
+        slot = c->mr_key[0][0] == up ? 0 : (c->mr_key[1][0] == up ? 1 : (c->mr_exec[0] ? 1 : 0));
+        if (c->mr_exec[slot]) { cudaGraphExecDestroy(c->mr_exec[slot]); c->mr_exec[slot] = nullptr; }
+        if (!c->cap_stream) NCU(c, cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking), "stream");
+        NCU(c, cudaStreamSynchronize(st), "sync");
+        const long long l0 = c->launches;
+        cudaGraph_t graph = nullptr;
+        NCU(c, cudaGraphCreate(&graph, 0), "graph create");
+        cudaGraphConditionalHandle h;
+        cudaGraphNodeParams np = {};
+        cudaGraphNode_t node;
+        cudaError_t ce = cudaGraphConditionalHandleCreate(&h, graph, 1, cudaGraphCondAssignDefault);
+        if (ce == cudaSuccess) {
+            np.type = cudaGraphNodeTypeConditional;
+            np.conditional.handle = h;
+            np.conditional.type = cudaGraphCondTypeWhile;
+            np.conditional.size = 1;
+            ce = cudaGraphAddNode(&node, graph, nullptr, 0, &np);
+        }
+        if (ce != cudaSuccess) {
+            cudaGraphDestroy(graph);
+            return check_cuda(c, ce, "minres conditional node");
+        }
+        cudaStream_t s = c->cap_stream;
+        NCU(c, cudaStreamBeginCaptureToGraph(s, np.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                             cudaStreamCaptureModeThreadLocal), "begin capture");
+        long long dummy = 0;
+        int rc = PF_OK;
+        k_mr_v<<<nb, kNB, 0, s>>>(n, Y, V, c->scal);
+        rc = launch_jac(c, u, alpha, V, V + nu, T, T + nu, c->act, s);
+        if (rc == PF_OK) {
+            k_mr_a<<<nb, kNB, 0, s>>>(n, T, R1, V, c->scal, rb);
+            k_mr_b<<<nb, kNB, 0, s>>>(n, T, R1, R2, c->scal);
+            rc = fieldsplit(c, w, R2, Y, u, alpha, 0.0, 0, dummy, s, mg);
+        }
+        if (rc == PF_OK) {
+            k_mr_dot<<<nb, kNB, 0, s>>>(n, R2, Y, c->scal, rb);
+            k_mr_rot<<<1, 1, 0, s>>>(c->scal);
+            k_mr_w<<<nb, kNB, 0, s>>>(n, V, Wa, Wb, x, c->scal);
+            k_mr_cond<<<1, 32, 0, s>>>(h, c->scal);
+            c->launches += 8;
+        }
+        cudaGraph_t captured = nullptr;
+        ce = cudaStreamEndCapture(s, &captured);
+        if (rc != PF_OK) { cudaGraphDestroy(graph); return rc; }
+        if (ce != cudaSuccess) { cudaGraphDestroy(graph); return check_cuda(c, ce, "minres end capture"); }
+        ce = cudaGraphInstantiate(&c->mr_exec[slot], graph, 0);
+        cudaGraphDestroy(graph);
+        NCU(c, ce, "minres graph instantiate");
+        c->mr_nodes[slot] = c->launches - l0;
+        c->launches = l0;
+        memcpy(c->mr_key[slot], key, sizeof key);
+    }
+    NTRY(read_scal(c, st, S_MR, 18));
+    const double* m = c->h_scal + S_MR;
+    if (m[MR_FAIL] != 0.0) return set_error(c, PF_EBREAKDOWN, "minres: preconditioner not SPD");
+    if (m[MR_DONE] == 0.0) {
+        NCU(c, cudaGraphLaunch(c->mr_exec[slot], st), "minres graph launch");
+        NTRY(read_scal(c, st, S_MR, 18));
+    }
+    if (m[MR_FAIL] != 0.0) return set_error(c, PF_EBREAKDOWN, "minres: preconditioner not SPD");
+    const long long it = (long long)m[MR_IT];
+    c->launches += it * c->mr_nodes[slot];
+    kits += it + it * (long long)(mg.deg + 1);
+    converged = m[MR_PHIBAR] <= m[MR_TARGET];
+    if (getenv("PF_NEWTON_TRACE"))
+        fprintf(stderr, "  minres(dev): its=%lld beta1=%.3e phibar=%.3e target=%.3e\n", it,
+                m[MR_TARGET] / rtol, m[MR_PHIBAR], m[MR_TARGET]);
+    return PF_OK;
+}
+
 int newton_solve(Ctx* c, const double* u_in, const double* a_in, const double* lb, double* u_out, double* a_out,
                  const pf_vi_opts* o, pf_vi_report* rep, cudaStream_t st) {
     memset(rep, 0, sizeof(*rep));
@@ -448,12 +704,20 @@ int newton_solve(Ctx* c, const double* u_in, const double* a_in, const double* l
             mg.additive = o->inner_mode == 2;
             mg.deg = o->inner_cycles > 0 ? o->inner_cycles : 12;
             NTRY(lambda_C(c, mg.lmax, st));
+            // device-resident MINRES (graph) unless profiling (eager, bracketed launches) or disabled
+            mg.dev = c->use_graphs && !c->prof.on && !getenv("PF_NEWTON_HOST_MINRES") && mg.deg <= kMaxChebDeg;
+            if (mg.dev) {
+                k_cheb_table<<<1, 1, 0, st>>>(c->scal, mg.deg, kChebSafety);
+                c->launches++;
+            }
         }
         bool ok = false;
         long long kits = 0;
         bool lin_ok = false;
-        int rc = minres(c, w, u, alpha, w.RHS, w.D, fs_rtol, o->inner_maxit > 0 ? o->inner_maxit : 10 * n,
-                        inner_rtol, mg.on ? 0 : std::max(0, o->inner_cycles), kits, lin_ok, st, mg);
+        const long long mr_maxit = o->inner_maxit > 0 ? o->inner_maxit : 10 * n;
+        int rc = mg.dev ? minres_dev(c, w, u, alpha, w.RHS, w.D, fs_rtol, mr_maxit, kits, lin_ok, st, mg)
+                        : minres(c, w, u, alpha, w.RHS, w.D, fs_rtol, mr_maxit, inner_rtol,
+                                 mg.on ? 0 : std::max(0, o->inner_cycles), kits, lin_ok, st, mg);
         rep->total_krylov_iterations += kits;
         if (rc == PF_OK && lin_ok) {
             k_nscale<<<nblocks(n), kNB, 0, st>>>(n, -1.0, w.D, w.D);  // d = -d_N (zero on active)

@@ -369,3 +369,32 @@ def test_damage_steepest_descent_fallback_matches_oracle_rsls(seed):
         (so.iterations, so.steepest_descent_steps, so.converged)
     assert abs(r.final_residual_norm - so.final_residual_norm) <= 1e-9 * so.final_residual_norm
     assert np.max(np.abs(host(out) - xo)) < 1e-10
+
+
+@pytest.mark.parametrize("additive", [True, False])
+@pytest.mark.parametrize("dim", [2, 3])
+def test_device_minres_matches_host_minres(additive, dim, monkeypatch):
+    """The device-resident MINRES of the multigrid field split (one graph-replayed iteration, every
+    scalar on the device) follows the host-driven Paige-Saunders loop (linalg.py:155-219): same
+    Newton and MINRES iteration counts, same Newton iterate to round-off."""
+    import paper_1511_08463_b200 as pf
+    from paper_1511_08463_b200 import solver as S
+    if dim == 2:
+        setup = pf.setup_traction(pf.Material(ell=0.1), nx=40, ny=12, n_steps=12, pattern="right")
+        nsteps = 9
+    else:
+        setup = pf.setup_traction3d(n=6, n_steps=6)
+        nsteps = 5
+    base = pf.SolverConfig(method="am", elastic_solver="cg", elastic_precond="gmg", outer_atol=1e-3)
+    st = pf.State.zeros(setup.mesh)
+    pf.run_quasistatic(setup, base, snapshot_stride=0, state=st, steps=list(range(nsteps)))
+    cfg = pf.SolverConfig(outer_atol=1e-9, elastic_solver="cg", elastic_precond="gmg",
+                          fieldsplit_inner="mg", fieldsplit_additive=additive)
+    s1, r1 = S.coupled_newton_solve(st, setup.problem, cfg)
+    monkeypatch.setenv("PF_NEWTON_HOST_MINRES", "1")
+    s2, r2 = S.coupled_newton_solve(st, setup.problem, cfg)
+    assert r1.converged and r2.converged
+    assert r1.iterations == r2.iterations
+    assert abs(r1.total_krylov_iterations - r2.total_krylov_iterations) <= 2 * (cfg.fieldsplit_cheb_degree + 2)
+    assert rel(s1.u.cpu().numpy(), s2.u.cpu().numpy()) < 1e-9
+    assert float((s1.alpha - s2.alpha).abs().max()) < 1e-9
