@@ -103,10 +103,13 @@ class ClockSampler:
 
 # ---- workloads -----------------------------------------------------------------------------------
 def sent_config(pf):
+    # C-block Chebyshev degree 6: driver window (steps 5..24) 0.251 -> 0.236 s/step against degree
+    # 12, degree 8 0.240 (gpurun_out sw_deg*, profiles/r02d_*): cheaper MINRES iterations win over
+    # the few extra ones in the stalled Newton phase of the nucleation step
     return pf.SolverConfig(method="oram_newton", omega=1.8, outer_atol=1e-6, am_switch_atol=1e-3,
                            elastic_solver="cg", elastic_rtol=1e-8, elastic_precond="gmg",
                            max_am_iterations=2000,
-                           fieldsplit_inner="mg")
+                           fieldsplit_inner="mg", fieldsplit_cheb_degree=6)
 
 
 def surfing_config(pf):

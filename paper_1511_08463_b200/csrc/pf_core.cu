@@ -989,6 +989,9 @@ void pf_ctx_destroy(pf_ctx* c) {
         if (ge) cudaGraphExecDestroy(ge);
     for (auto& ge : c->mr_exec)
         if (ge) cudaGraphExecDestroy(ge);
+    if (c->side_stream) cudaStreamDestroy(c->side_stream);
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->ev_join) cudaEventDestroy(c->ev_join);
     if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
     if (c->h_scal) cudaFreeHost(c->h_scal);
     delete c;

@@ -336,6 +336,8 @@ struct Ctx {
     // device-resident MINRES of the Newton phase (pf_newton.cu): one graph per Newton-iterate
     // buffer (the line search ping-pongs two), keyed on the pointers and sizes it bakes in
     static constexpr int kMrKey = 12;
+    cudaStream_t side_stream = nullptr;  // the C block of the block-diagonal split, beside the V-cycle
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     cudaGraphExec_t mr_exec[2] = {nullptr, nullptr};
     long long mr_nodes[2] = {0, 0};
     long long mr_key[2][kMrKey] = {};

@@ -417,6 +417,26 @@ static int fieldsplit(Ctx* c, const NewtonWs& w, const double* r, double* y, con
     const long long nu = w.nu, na = w.na;
     double* y1 = y;              // u part of y
     double* z = y + nu;          // alpha part of y
+    if (mg.on && mg.additive && mg.dev && !getenv("PF_NEWTON_NO_FORK")) {
+        // block-diagonal split, the two blocks concurrently: the Chebyshev polynomial of the C block
+        // runs on a side stream beside the V-cycle (whose coarse levels are latency-bound and leave
+        // most of the machine idle); fork/join by events, also inside the graph capture
+        if (!c->side_stream) {
+            NCU(c, cudaStreamCreateWithFlags(&c->side_stream, cudaStreamNonBlocking), "side stream");
+            NCU(c, cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming), "event");
+            NCU(c, cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming), "event");
+        }
+        cudaStream_t sd = c->side_stream;
+        NCU(c, cudaEventRecord(c->ev_fork, st), "fork");
+        NCU(c, cudaStreamWaitEvent(sd, c->ev_fork, 0), "fork wait");
+        k_nsubmask<<<nblocks(na), kNB, 0, sd>>>(na, r + nu, nullptr, c->act, w.TMP + nu);
+        c->launches++;
+        NTRY(cheb_C_dev(c, w.TMP + nu, z, mg.deg, its, sd));
+        NCU(c, cudaEventRecord(c->ev_join, sd), "join");
+        NTRY(vcycle_A(c, r, y1, its, st));
+        NCU(c, cudaStreamWaitEvent(st, c->ev_join, 0), "join wait");
+        return PF_OK;
+    }
     if (mg.on && mg.additive) {  // block-diagonal field split: P^-1 = diag(V-cycle, Chebyshev)
         NTRY(vcycle_A(c, r, y1, its, st));
         k_nsubmask<<<nblocks(na), kNB, 0, st>>>(na, r + nu, nullptr, c->act, w.TMP + nu);
@@ -543,6 +563,36 @@ static int minres_dev(Ctx* c, NewtonWs& w, const double* u, const double* alpha,
     long long key[Ctx::kMrKey] = {(long long)(uintptr_t)u, (long long)(uintptr_t)alpha, (long long)(uintptr_t)x,
                                  (long long)(uintptr_t)R1, c->geo_version, (long long)c->glev.size(),
                                  c->gmg_degree, mg.deg, mg.additive ? 1 : 0, n, nu, c->dim};
+    // one iteration (k_mr_cond ends the graph body; the eager debug loop polls instead)
+    auto issue = [&](cudaStream_t s, const cudaGraphConditionalHandle* h) -> int {
+        long long dummy = 0;
+        k_mr_v<<<nb, kNB, 0, s>>>(n, Y, V, c->scal);
+        NTRY(launch_jac(c, u, alpha, V, V + nu, T, T + nu, c->act, s));
+        k_mr_a<<<nb, kNB, 0, s>>>(n, T, R1, V, c->scal, rb);
+        k_mr_b<<<nb, kNB, 0, s>>>(n, T, R1, R2, c->scal);
+        NTRY(fieldsplit(c, w, R2, Y, u, alpha, 0.0, 0, dummy, s, mg));
+        k_mr_dot<<<nb, kNB, 0, s>>>(n, R2, Y, c->scal, rb);
+        k_mr_rot<<<1, 1, 0, s>>>(c->scal);
+        k_mr_w<<<nb, kNB, 0, s>>>(n, V, Wa, Wb, x, c->scal);
+        if (h) k_mr_cond<<<1, 32, 0, s>>>(*h, c->scal);
+        c->launches += h ? 8 : 7;
+        return PF_OK;
+    };
+    if (getenv("PF_MR_EAGER")) {  // debugging aid: the same launches, host-polled
+        NTRY(read_scal(c, st, S_MR, 18));
+        while (c->h_scal[S_MR + MR_DONE] == 0.0) {
+            NTRY(issue(st, nullptr));
+            NTRY(read_scal(c, st, S_MR, 18));
+        }
+        const double* m = c->h_scal + S_MR;
+        if (m[MR_FAIL] != 0.0) return set_error(c, PF_EBREAKDOWN, "minres: preconditioner not SPD");
+        const long long it = (long long)m[MR_IT];
+        kits += it + it * fs_its;
+        converged = m[MR_PHIBAR] <= m[MR_TARGET];
+        if (getenv("PF_NEWTON_TRACE"))
+            fprintf(stderr, "  minres(eager dev): its=%lld phibar=%.3e target=%.3e\n", it, m[MR_PHIBAR], m[MR_TARGET]);
+        return PF_OK;
+    }
     int slot = -1;
     for (int q = 0; q < 2; ++q)
         if (c->mr_exec[q] && memcmp(c->mr_key[q], key, sizeof key) == 0) slot = q;
@@ -574,22 +624,7 @@ static int minres_dev(Ctx* c, NewtonWs& w, const double* u, const double* alpha,
         cudaStream_t s = c->cap_stream;
         NCU(c, cudaStreamBeginCaptureToGraph(s, np.conditional.phGraph_out[0], nullptr, nullptr, 0,
                                              cudaStreamCaptureModeThreadLocal), "begin capture");
-        long long dummy = 0;
-        int rc = PF_OK;
-        k_mr_v<<<nb, kNB, 0, s>>>(n, Y, V, c->scal);
-        rc = launch_jac(c, u, alpha, V, V + nu, T, T + nu, c->act, s);
-        if (rc == PF_OK) {
-            k_mr_a<<<nb, kNB, 0, s>>>(n, T, R1, V, c->scal, rb);
-            k_mr_b<<<nb, kNB, 0, s>>>(n, T, R1, R2, c->scal);
-            rc = fieldsplit(c, w, R2, Y, u, alpha, 0.0, 0, dummy, s, mg);
-        }
-        if (rc == PF_OK) {
-            k_mr_dot<<<nb, kNB, 0, s>>>(n, R2, Y, c->scal, rb);
-            k_mr_rot<<<1, 1, 0, s>>>(c->scal);
-            k_mr_w<<<nb, kNB, 0, s>>>(n, V, Wa, Wb, x, c->scal);
-            k_mr_cond<<<1, 32, 0, s>>>(h, c->scal);
-            c->launches += 8;
-        }
+        const int rc = issue(s, &h);
         cudaGraph_t captured = nullptr;
         ce = cudaStreamEndCapture(s, &captured);
         if (rc != PF_OK) { cudaGraphDestroy(graph); return rc; }
@@ -611,7 +646,7 @@ static int minres_dev(Ctx* c, NewtonWs& w, const double* u, const double* alpha,
     if (m[MR_FAIL] != 0.0) return set_error(c, PF_EBREAKDOWN, "minres: preconditioner not SPD");
     const long long it = (long long)m[MR_IT];
     c->launches += it * c->mr_nodes[slot];
-    kits += it + it * (long long)(mg.deg + 1);
+    kits += it + it * fs_its;  // fs_its: the count of one field-split application (start-up call)
     converged = m[MR_PHIBAR] <= m[MR_TARGET];
     if (getenv("PF_NEWTON_TRACE"))
         fprintf(stderr, "  minres(dev): its=%lld beta1=%.3e phibar=%.3e target=%.3e\n", it,
@@ -690,7 +725,8 @@ int newton_solve(Ctx* c, const double* u_in, const double* a_in, const double* l
         // so the old smoother bounds stay above the spectrum) -- one setup (~2.5 ms) saved per phase
         // 2D only: the 3D re-discretised hierarchy with a stale alpha preconditioned config-4 Newton
         // badly (~160 instead of ~20 MINRES iterations, measured)
-        const bool keep = c->dim == 2 && (o->inner_mode == 1 || o->inner_mode == 2) && it == 1 && c->gmg_built;
+        const bool keep = c->dim == 2 && (o->inner_mode == 1 || o->inner_mode == 2) && it == 1 && c->gmg_built &&
+                          !getenv("PF_NEWTON_NO_KEEP");  // (tests: calls independent of the prior hierarchy)
         if (!keep) {
             NTRY(c->dim == 3 ? gmg3_setup(c, st) : gmg_setup(c, st));
             c->gmg_built = 1;  // an elastic solve that follows may keep it (gmg_reuse)
@@ -715,9 +751,21 @@ int newton_solve(Ctx* c, const double* u_in, const double* a_in, const double* l
         long long kits = 0;
         bool lin_ok = false;
         const long long mr_maxit = o->inner_maxit > 0 ? o->inner_maxit : 10 * n;
-        int rc = mg.dev ? minres_dev(c, w, u, alpha, w.RHS, w.D, fs_rtol, mr_maxit, kits, lin_ok, st, mg)
-                        : minres(c, w, u, alpha, w.RHS, w.D, fs_rtol, mr_maxit, inner_rtol,
-                                 mg.on ? 0 : std::max(0, o->inner_cycles), kits, lin_ok, st, mg);
+        auto run_minres = [&]() {
+            return mg.dev ? minres_dev(c, w, u, alpha, w.RHS, w.D, fs_rtol, mr_maxit, kits, lin_ok, st, mg)
+                          : minres(c, w, u, alpha, w.RHS, w.D, fs_rtol, mr_maxit, inner_rtol,
+                                   mg.on ? 0 : std::max(0, o->inner_cycles), kits, lin_ok, st, mg);
+        };
+        int rc = run_minres();
+        if (rc == PF_EBREAKDOWN && keep) {
+            // the kept AM hierarchy gave an indefinite V-cycle: rebuild it for this iterate and retry
+            // (as the elastic PCG does on breakdown) instead of spending the iteration on a
+            // steepest-descent step
+            NTRY(gmg_setup(c, st));
+            c->gmg_built = 1;
+            c->gmg_its0 = -1;
+            rc = run_minres();
+        }
         rep->total_krylov_iterations += kits;
         if (rc == PF_OK && lin_ok) {
             k_nscale<<<nblocks(n), kNB, 0, st>>>(n, -1.0, w.D, w.D);  // d = -d_N (zero on active)

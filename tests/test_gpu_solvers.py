@@ -390,7 +390,14 @@ def test_device_minres_matches_host_minres(additive, dim, monkeypatch):
     pf.run_quasistatic(setup, base, snapshot_stride=0, state=st, steps=list(range(nsteps)))
     cfg = pf.SolverConfig(outer_atol=1e-9, elastic_solver="cg", elastic_precond="gmg",
                           fieldsplit_inner="mg", fieldsplit_additive=additive)
+    # every Newton iteration builds its own hierarchy, so the calls do not depend on each other
+    monkeypatch.setenv("PF_NEWTON_NO_KEEP", "1")
     s1, r1 = S.coupled_newton_solve(st, setup.problem, cfg)
+    # the block-diagonal split runs its two blocks on two streams: the same arithmetic, bitwise
+    monkeypatch.setenv("PF_NEWTON_NO_FORK", "1")
+    s0, r0 = S.coupled_newton_solve(st, setup.problem, cfg)
+    assert torch.equal(s0.u, s1.u) and torch.equal(s0.alpha, s1.alpha)
+    assert r0.total_krylov_iterations == r1.total_krylov_iterations
     monkeypatch.setenv("PF_NEWTON_HOST_MINRES", "1")
     s2, r2 = S.coupled_newton_solve(st, setup.problem, cfg)
     assert r1.converged and r2.converged

@@ -29,12 +29,15 @@ ap.add_argument("--steps", type=int, default=60)
 ap.add_argument("--save", default="")
 ap.add_argument("--out", default="gpurun_out/sent_window.json")
 ap.add_argument("--no-split", action="store_true")
+ap.add_argument("--cheb-deg", type=int, default=0, help="override fieldsplit_cheb_degree")
 args = ap.parse_args()
 save = {int(s) for s in args.save.split(",") if s}
 os.makedirs("gpurun_out", exist_ok=True)
 
 setup = pf.setup_sent(n=args.n)
 cfg = bench.sent_config(pf)
+if args.cheb_deg:
+    cfg.fieldsplit_cheb_degree = args.cheb_deg
 flush = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device="cuda")
 
 

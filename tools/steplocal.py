@@ -96,7 +96,7 @@ def run_oracle():
              energy=np.array([r.energy.elastic, r.energy.dissipated, r.energy.total]), load=r.load,
              am=r.stats.am_iterations, newton=r.stats.newton_iterations,
              attempts=r.stats.newton_attempts, wall=wall, residual=r.stats.final_residual_norm,
-             hist=np.array(hist))
+             hist=np.array(hist), lu=os.environ.get("ORACLE_LU_PERMC", "COLAMD"))
     print(f"oracle step {args.step}: {wall:.1f} s AM={r.stats.am_iterations} "
           f"N={r.stats.newton_iterations}/{r.stats.newton_attempts} E={tuple(r.energy)}")
 
@@ -117,7 +117,7 @@ def compare():
                       "wall_s": float(a["wall"]), "residual": float(a["residual"])},
            "oracle": {"am": int(b["am"]), "newton": int(b["newton"]), "attempts": int(b["attempts"]),
                       "wall_s": float(b["wall"]), "residual": float(b["residual"]),
-                      "lu_ordering": os.environ.get("ORACLE_LU_PERMC", "COLAMD")}}
+                      "lu_ordering": str(b["lu"]) if "lu" in b.files else "MMD_AT_PLUS_A"}}
     out["pass"] = bool(rel.max() <= 1e-6 and out["alpha_max_abs_diff"] <= 1e-4)
     print(json.dumps(out, indent=1))
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
