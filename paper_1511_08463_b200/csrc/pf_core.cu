@@ -912,7 +912,7 @@ static void plan_workspace(Ctx* c) {
     add((void**)&c->tickets, sizeof(unsigned) * 64);
     add((void**)&c->bits, sizeof(unsigned long long) * 8);
     c->n_newton_vec = ((c->n_u + c->n_a + 31) / 32) * 32;  // keep every stacked slot 256-byte aligned
-    if (!(c->d.skip & PF_SKIP_NEWTON)) add((void**)&c->newton, sizeof(double) * c->n_newton_vec * 16);
+    if (!(c->d.skip & PF_SKIP_NEWTON)) add((void**)&c->newton, sizeof(double) * c->n_newton_vec * 17);
     if (c->dim == 2 && !(c->d.skip & PF_SKIP_GMG)) {
         gmg_plan(c);
         add((void**)&c->gmg_base, gmg_bytes(c));

@@ -140,19 +140,57 @@ __global__ void k_nchebk(long long n, const double* dinv, const double* Cd, doub
 constexpr int S_MR = 80;  // MINRES state slots
 enum {
     MR_BETA = 0, MR_OLDB, MR_DBAR, MR_EPS, MR_PHIBAR, MR_CS, MR_SN, MR_TARGET, MR_IT, MR_MAXIT, MR_DONE,
-    MR_FAIL, MR_ALFA, MR_BB, MR_OLDEPS, MR_DELTA, MR_GAM, MR_PHI
+    MR_FAIL, MR_ALFA, MR_BB, MR_OLDEPS, MR_DELTA, MR_GAM, MR_PHI, MR_TB, MR_TT
 };
 constexpr int S_CHEB = 100;  // Chebyshev table of the C block: [0] = 1/theta, [2k-1], [2k] = a_k, b_k
 constexpr int kMaxChebDeg = 14;
 
-__global__ void k_mr_start(double* s, double rtol, double maxit) {
+// warm != 0: the target was set from |b|_M (k_mr_target) and the start-up residual is b - J x0
+__global__ void k_mr_start(double* s, double rtol, double maxit, int warm) {
     double* m = s + S_MR;
     const double bb = m[MR_BB];
     const double b1 = bb > 0.0 ? sqrt(bb) : 0.0;
     m[MR_BETA] = b1; m[MR_OLDB] = 0.0; m[MR_DBAR] = 0.0; m[MR_EPS] = 0.0; m[MR_PHIBAR] = b1;
-    m[MR_CS] = -1.0; m[MR_SN] = 0.0; m[MR_TARGET] = rtol * b1; m[MR_IT] = 0.0; m[MR_MAXIT] = maxit;
+    m[MR_CS] = -1.0; m[MR_SN] = 0.0; m[MR_IT] = 0.0; m[MR_MAXIT] = maxit;
+    if (!warm) m[MR_TARGET] = rtol * b1;
     m[MR_FAIL] = bb < 0.0 ? 1.0 : 0.0;
-    m[MR_DONE] = (bb <= 0.0) ? 1.0 : 0.0;
+    m[MR_DONE] = (bb <= 0.0 || b1 <= m[MR_TARGET]) ? 1.0 : 0.0;
+}
+__global__ void k_mr_target(double* s, double rtol) {
+    const double bb = s[S_MR + MR_BB];
+    s[S_MR + MR_TARGET] = rtol * (bb > 0.0 ? sqrt(bb) : 0.0);
+}
+// x0 = previous solution with the currently active damage rows zeroed; r = b - t (t = J x0)
+__global__ void k_mr_x0(long long nu, long long na, const double* __restrict__ dp, const unsigned char* __restrict__ act,
+                        double* __restrict__ x) {
+    const long long n = nu + na;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        x[i] = (i >= nu && act[i - nu]) ? 0.0 : dp[i];
+}
+// t.b and t.t for the least-squares scale of the warm start
+__global__ void k_mr_dot2(long long n, const double* __restrict__ t, const double* __restrict__ b, double* s, RedBuf rb) {
+    double acc[2] = {0.0, 0.0};
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const double ti = t[i];
+        acc[0] += ti * b[i];
+        acc[1] += ti * ti;
+    }
+    grid_reduce<2>(acc, rb, 8, [=](double* tt) { s[S_MR + MR_TB] = tt[0]; s[S_MR + MR_TT] = tt[1]; });
+}
+// x0 = g x ; r1 = r2 = b - g t with g = (t.b)/(t.t) (the best multiple of the previous solution)
+__global__ void k_mr_r0(long long n, const double* __restrict__ b, const double* __restrict__ t, double* __restrict__ x,
+                        double* __restrict__ r1, double* __restrict__ r2, const double* s) {
+    double g = 1.0;  // s == null: x0 as given
+    if (s) {
+        const double tt = s[S_MR + MR_TT];
+        g = tt > 0.0 ? s[S_MR + MR_TB] / tt : 0.0;
+    }
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const double v = b[i] - g * t[i];
+        x[i] *= g;
+        r1[i] = v;
+        r2[i] = v;
+    }
 }
 // v = y / beta
 __global__ void k_mr_v(long long n, const double* __restrict__ y, double* __restrict__ v, const double* s) {
@@ -288,6 +326,8 @@ static int nblocks(long long n) { return (int)std::max(1LL, std::min((n + kNB - 
 struct NewtonWs {
     long long nu, na, n;
     double *X, *TX, *FX, *TF, *D, *RHS, *R1, *R2, *Y, *V, *W, *W1, *W2, *TMP, *PP, *G;
+    double* DP;        // the previous Newton iteration's MINRES solution (warm start)
+    bool dp_valid = false;
 };
 
 static int ndot(Ctx* c, long long n, const double* a, const double* b, int slot, double& out, cudaStream_t st) {
@@ -549,17 +589,46 @@ static int minres_dev(Ctx* c, NewtonWs& w, const double* u, const double* alpha,
     const RedBuf rb{c->partials, c->tickets, c->scal};
     const int nb = nblocks(n);
     double *R1 = w.R1, *R2 = w.R2, *Y = w.Y, *V = w.V, *T = w.W, *Wa = w.W1, *Wb = w.W2;
-    NCU(c, cudaMemsetAsync(x, 0, sizeof(double) * n, st), "memset");
     NCU(c, cudaMemsetAsync(Wa, 0, sizeof(double) * n, st), "memset");
     NCU(c, cudaMemsetAsync(Wb, 0, sizeof(double) * n, st), "memset");
-    NCU(c, cudaMemcpyAsync(R1, rhs, sizeof(double) * n, cudaMemcpyDeviceToDevice, st), "copy");
-    NCU(c, cudaMemcpyAsync(R2, rhs, sizeof(double) * n, cudaMemcpyDeviceToDevice, st), "copy");
     long long fs_its = 0;
-    NTRY(fieldsplit(c, w, R1, Y, u, alpha, 0.0, 0, fs_its, st, mg));
-    k_mr_dot<<<nb, kNB, 0, st>>>(n, R1, Y, c->scal, rb);
-    k_mr_start<<<1, 1, 0, st>>>(c->scal, rtol, (double)maxit);
+    // warm start (x0 = the previous Newton iteration's solution, active rows zeroed): in a stalled
+    // Newton phase consecutive systems barely change.  The stopping target stays rtol |b|_M, the
+    // cold start's, so the accepted direction meets the same residual bound; only the iteration
+    // count changes.
+    bool warm = w.dp_valid && !getenv("PF_MINRES_COLD");
+    NTRY(fieldsplit(c, w, rhs, Y, u, alpha, 0.0, 0, fs_its, st, mg));  // y = M b (cold start-up, |b|_M)
+    k_mr_dot<<<nb, kNB, 0, st>>>(n, rhs, Y, c->scal, rb);
+    k_mr_target<<<1, 1, 0, st>>>(c->scal, rtol);
     c->launches += 2;
     kits += fs_its;
+    const long long fs_one = std::max(1LL, fs_its);  // the count of one field-split application
+    if (warm) {
+        k_mr_x0<<<nb, kNB, 0, st>>>(nu, n - nu, w.DP, c->act, x);
+        NTRY(launch_jac(c, u, alpha, x, x + nu, T, T + nu, c->act, st));
+        // x0 = the previous solution itself (a least-squares multiple of it was measured worse:
+        // SENT 512^2 stalled Newton phase 0.88 s with x0 = d_prev, 1.05 s with the 2-norm-optimal scale)
+        k_mr_r0<<<nb, kNB, 0, st>>>(n, rhs, T, x, R1, R2, nullptr);
+        NTRY(fieldsplit(c, w, R1, V, u, alpha, 0.0, 0, fs_its, st, mg));  // M r0 (V is free here)
+        kits += fs_one;
+        k_mr_dot<<<nb, kNB, 0, st>>>(n, R1, V, c->scal, rb);
+        c->launches += 4;
+        NTRY(read_scal(c, st, S_MR, 20));
+        const double bb_r = c->h_scal[S_MR + MR_BB], tgt = c->h_scal[S_MR + MR_TARGET];
+        // keep the warm start only when it is closer than the cold one: |b - J x0|_M < |b|_M
+        warm = bb_r >= 0.0 && rtol > 0.0 && std::sqrt(bb_r) < tgt / rtol;
+        if (warm) NCU(c, cudaMemcpyAsync(Y, V, sizeof(double) * n, cudaMemcpyDeviceToDevice, st), "copy");
+    }
+    if (!warm) {  // cold: x = 0, r1 = r2 = b, y = M b (computed above), restore |b|_M^2
+        NCU(c, cudaMemsetAsync(x, 0, sizeof(double) * n, st), "memset");
+        NCU(c, cudaMemcpyAsync(R1, rhs, sizeof(double) * n, cudaMemcpyDeviceToDevice, st), "copy");
+        NCU(c, cudaMemcpyAsync(R2, rhs, sizeof(double) * n, cudaMemcpyDeviceToDevice, st), "copy");
+        k_mr_dot<<<nb, kNB, 0, st>>>(n, rhs, Y, c->scal, rb);
+        c->launches++;
+    }
+    k_mr_start<<<1, 1, 0, st>>>(c->scal, rtol, (double)maxit, 1);
+    c->launches++;
+    fs_its = fs_one;
     long long key[Ctx::kMrKey] = {(long long)(uintptr_t)u, (long long)(uintptr_t)alpha, (long long)(uintptr_t)x,
                                  (long long)(uintptr_t)R1, c->geo_version, (long long)c->glev.size(),
                                  c->gmg_degree, mg.deg, mg.additive ? 1 : 0, n, nu, c->dim};
@@ -664,6 +733,7 @@ int newton_solve(Ctx* c, const double* u_in, const double* a_in, const double* l
     double** slots[] = {&w.X, &w.TX, &w.FX, &w.TF, &w.D, &w.RHS, &w.R1, &w.R2, &w.Y, &w.V, &w.W, &w.W1, &w.W2,
                         &w.TMP, &w.PP, &w.G};
     for (int k = 0; k < 16; ++k) *slots[k] = c->newton + (size_t)k * c->n_newton_vec;
+    w.DP = c->newton + (size_t)16 * c->n_newton_vec;
     const long long nu = w.nu, na = w.na, n = w.n;
     NCU(c, cudaMemcpyAsync(w.X, u_in, sizeof(double) * nu, cudaMemcpyDeviceToDevice, st), "copy");
     NCU(c, cudaMemcpyAsync(w.X + nu, a_in, sizeof(double) * na, cudaMemcpyDeviceToDevice, st), "copy");
@@ -767,6 +837,10 @@ int newton_solve(Ctx* c, const double* u_in, const double* a_in, const double* l
             rc = run_minres();
         }
         rep->total_krylov_iterations += kits;
+        if (rc == PF_OK && lin_ok && mg.dev) {  // the next iteration's MINRES starts from it
+            NCU(c, cudaMemcpyAsync(w.DP, w.D, sizeof(double) * n, cudaMemcpyDeviceToDevice, st), "copy");
+            w.dp_valid = true;
+        }
         if (rc == PF_OK && lin_ok) {
             k_nscale<<<nblocks(n), kNB, 0, st>>>(n, -1.0, w.D, w.D);  // d = -d_N (zero on active)
             c->launches++;

@@ -398,6 +398,10 @@ def test_device_minres_matches_host_minres(additive, dim, monkeypatch):
     s0, r0 = S.coupled_newton_solve(st, setup.problem, cfg)
     assert torch.equal(s0.u, s1.u) and torch.equal(s0.alpha, s1.alpha)
     assert r0.total_krylov_iterations == r1.total_krylov_iterations
+    # the host loop starts every MINRES from zero: compare with the device loop started cold too
+    # (the warm start changes the iteration counts, not the accepted tolerance)
+    monkeypatch.setenv("PF_MINRES_COLD", "1")
+    s1, r1 = S.coupled_newton_solve(st, setup.problem, cfg)
     monkeypatch.setenv("PF_NEWTON_HOST_MINRES", "1")
     s2, r2 = S.coupled_newton_solve(st, setup.problem, cfg)
     assert r1.converged and r2.converged
@@ -405,3 +409,23 @@ def test_device_minres_matches_host_minres(additive, dim, monkeypatch):
     assert abs(r1.total_krylov_iterations - r2.total_krylov_iterations) <= 2 * (cfg.fieldsplit_cheb_degree + 2)
     assert rel(s1.u.cpu().numpy(), s2.u.cpu().numpy()) < 1e-9
     assert float((s1.alpha - s2.alpha).abs().max()) < 1e-9
+
+
+def test_minres_warm_start_meets_the_same_tolerance(monkeypatch):
+    """The device MINRES restarts each Newton iteration from the best multiple of the previous
+    solution when that is closer than zero (the stopping target stays rtol |b|_M): the Newton
+    solution is the cold-start one to the Newton tolerance, the iteration count is unchanged."""
+    import paper_1511_08463_b200 as pf
+    from paper_1511_08463_b200 import solver as S
+    setup = pf.setup_traction(pf.Material(ell=0.1), nx=40, ny=12, n_steps=12, pattern="right")
+    base = pf.SolverConfig(method="am", elastic_solver="cg", elastic_precond="gmg", outer_atol=1e-3)
+    st = pf.State.zeros(setup.mesh)
+    pf.run_quasistatic(setup, base, snapshot_stride=0, state=st, steps=list(range(9)))
+    cfg = pf.SolverConfig(outer_atol=1e-9, elastic_solver="cg", elastic_precond="gmg", fieldsplit_inner="mg")
+    monkeypatch.setenv("PF_NEWTON_NO_KEEP", "1")
+    s1, r1 = S.coupled_newton_solve(st, setup.problem, cfg)
+    monkeypatch.setenv("PF_MINRES_COLD", "1")
+    s2, r2 = S.coupled_newton_solve(st, setup.problem, cfg)
+    assert r1.converged and r2.converged and r1.iterations == r2.iterations
+    assert rel(s1.u.cpu().numpy(), s2.u.cpu().numpy()) < 1e-8
+    assert float((s1.alpha - s2.alpha).abs().max()) < 1e-8

@@ -38,12 +38,9 @@ rep = S.am_solve(st, setup.problem, cfg, rtol=cfg.am_rtol, cycle=0)
 print(f"AM to hand-off: {rep.am_iterations} its, residual {rep.final_residual_norm:.3e}", flush=True)
 VARIANTS = {
     "default": {},
+    "cold_minres": {"PF_MINRES_COLD": "1"},
     "host_minres": {"PF_NEWTON_HOST_MINRES": "1"},
-    "cheb_deg4": {"__deg": 4},
-    "cheb_deg6": {"__deg": 6},
-    "cheb_deg8": {"__deg": 8},
-    "multiplicative": {"__mult": 1},
-    "mult_deg6": {"__mult": 1, "__deg": 6},
+    "cheb_deg12": {"__deg": 12},
 }
 for name, env in VARIANTS.items():
     c = bench.sent_config(pf)
