@@ -953,6 +953,9 @@ int pf_ctx_create(const pf_desc* desc, pf_ctx** out) {
     if (getenv("PF_NO_GRAPHS")) c->use_graphs = 0;
     if (getenv("PF_GMG_LEGACY")) c->gmg_coarse = 0;
     if (getenv("PF_GMG_SKIP_COARSE")) c->gmg_coarse = 2;
+    // measured slower on SENT 512^2 (16-CTA cluster phases are latency-bound on fewer SMs: coarse
+    // cycle 125 -> 160 us), so the cluster tail is opt-in (PF_GMG_CLUSTER=1)
+    c->gmg_cluster = getenv("PF_GMG_CLUSTER") ? 1 : 0;
     if (getenv("PF_PCG_GRAPH")) c->pcg_persistent = 0;
     if (getenv("PF_PCG_SINGLE")) c->pcg_single = 1;
     if (d3) {

@@ -918,9 +918,9 @@ __device__ __forceinline__ unsigned long long gtimer() {
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
 }
-#define TR()                                                                        \
-    do {                                                                            \
-        if (A.trace && blockIdx.x == 0 && threadIdx.x == 0) A.trace[ntr++] = gtimer(); \
+#define TR()                                                                               \
+    do {                                                                                   \
+        if (A.trace && blockIdx.x == 0 && threadIdx.x == 0) A.trace[tro + ntr++] = gtimer(); \
     } while (0)
 
 constexpr int kCB = 512;  // threads per CTA of the persistent coarse cycle (one CTA per SM; 1024 measured slower)
@@ -935,9 +935,30 @@ __device__ __forceinline__ void coarse_coef(const CoarseArgs& A, const double* l
     }
 }
 
-// The coarse part of one V-cycle as grid-wide phases (global thread index tid of nth); ends with
-// the level-0 prolongation into A.z0 (the caller synchronises before reading it).
-__device__ __forceinline__ void coarse_body(const CoarseArgs& A, const CCoef* coef, long long tid, long long nth) {
+// Barriers between the phases: the software grid barrier of the persistent cooperative launch, or
+// the hardware cluster barrier (barrier.cluster, release/acquire at cluster scope: ~0.2 us against
+// ~1.5-2 us for the grid barrier) when the phases run inside one thread-block cluster.
+struct GridBar {
+    unsigned int* bar;
+    __device__ __forceinline__ void operator()() const { grid_sync(bar); }
+};
+struct ClusterBar {
+    __device__ __forceinline__ void operator()() const {
+        asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+        asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+    }
+};
+// Which phases a launch runs: the whole coarse cycle (one grid launch), or split at level lt into
+// the grid-wide top (restriction from level 0 down to lt; prolongation from lt back to level 0)
+// and the cluster part (levels lt..nl-1 and back up to lt, small and latency-bound).
+enum { CP_ALL = 0, CP_DOWN = 1, CP_CLUSTER = 2, CP_UP = 3 };
+
+// The coarse part of one V-cycle as phases over threads tid of nth separated by sync(); the full
+// cycle (CP_ALL) ends with the level-0 prolongation into A.z0 (the caller synchronises before
+// reading it).
+template <class SYNC>
+__device__ __forceinline__ void coarse_body(const CoarseArgs& A, const CCoef* coef, long long tid, long long nth,
+                                            int part, int lt, SYNC sync) {
     const int deg = A.deg;
     const int t0 = threadIdx.x;
     (void)t0;
@@ -954,9 +975,10 @@ __device__ __forceinline__ void coarse_body(const CoarseArgs& A, const CCoef* co
             for (long long v = tid; v < nv; v += nth) fn(G1{}, v, 0);
     };
     int ntr = 0;
+    const int tro = part == CP_ALL ? 0 : 40 * (part - 1);  // trace slots per launch of a split cycle
     TR();
     // level 0 -> 1 restriction (crossed: centres collapsed onto the corners on the fly)
-    {
+    if (part == CP_ALL || part == CP_DOWN) {
         const CLev& C = A.lev[1];
         if (A.crossed) {
             const Geo2& g = A.g;
@@ -978,17 +1000,19 @@ __device__ __forceinline__ void coarse_body(const CoarseArgs& A, const CCoef* co
         } else {
             grid_each(C.L.nv, [&](auto g, long long v, int q) { v_restrict<false, decltype(g)::value>(A.L0, C.L, C.L.mask, A.r0, C.b, v, q); });
         }
-    }
-    grid_sync(A.bar);
+        sync();
         TR();
-    // descend through the grid-wide levels
-    for (int l = 1; l < A.nl - 1; ++l) {
+    }
+    // descend: pre-smooth, residual, restriction of levels [d0, d1)
+    const int d0 = part == CP_CLUSTER ? lt : 1;
+    const int d1 = part == CP_DOWN ? lt : (part == CP_UP ? 0 : A.nl - 1);
+    for (int l = d0; l < d1; ++l) {
         const CLev& V = A.lev[l];
         const Cheb c = coef[l].c;
         double a = 0.0, b = 0.0;
         if (deg > 1) { a = coef[l].a[1]; b = coef[l].b[1]; }
         grid_each(V.L.nv, [&](auto g, long long v, int q) { v_pre_first<false, decltype(g)::value>(V.L, V.b, V.res, V.d0, V.d1, V.x, c, a, b, deg, v, q); });
-        grid_sync(A.bar);
+        sync();
         TR();
         double* d = V.d0;
         double* dn = V.d1;
@@ -996,20 +1020,20 @@ __device__ __forceinline__ void coarse_body(const CoarseArgs& A, const CCoef* co
         for (int k = 2; k < deg; ++k) {
             a = coef[l].a[k]; b = coef[l].b[k];
             grid_each(V.L.nv, [&](auto g, long long v, int q) { v_cheb_step<false, decltype(g)::value>(V.L, nullptr, d, dn, V.res, V.x, a, b, 0, v, q); });
-            grid_sync(A.bar);
-        TR();
+            sync();
+            TR();
             double* t = d; d = dn; dn = t;
         }
         grid_each(V.L.nv, [&](auto g, long long v, int q) { v_resid<false, decltype(g)::value>(V.L, nullptr, V.x, V.b, V.r, v, q); });
-        grid_sync(A.bar);
+        sync();
         TR();
         const CLev& C = A.lev[l + 1];
         grid_each(C.L.nv, [&](auto g, long long v, int q) { v_restrict<false, decltype(g)::value>(V.L, C.L, C.L.mask, V.r, C.b, v, q); });
-        grid_sync(A.bar);
+        sync();
         TR();
     }
-    // coarsest level: x = Ainv b, one warp per row across the grid
-    {
+    // coarsest level: x = Ainv b, one warp per row across the threads
+    if (part == CP_ALL || part == CP_CLUSTER) {
         const CLev& C = A.lev[A.nl - 1];
         const int n = A.ncoarse, lane = t0 & 31;
         for (long long r = tid >> 5; r < n; r += nth >> 5) {
@@ -1018,19 +1042,21 @@ __device__ __forceinline__ void coarse_body(const CoarseArgs& A, const CCoef* co
             sum = warp_sum(sum);
             if (lane == 0) C.x[r] = sum;
         }
-    }
-    grid_sync(A.bar);
+        sync();
         TR();
-    // ascend through the grid-wide levels
-    for (int l = A.nl - 2; l >= 1; --l) {
+    }
+    // ascend: prolongation from l + 1, post-smoothing of levels (u0, u1] from the top down
+    const int u1 = part == CP_UP ? lt - 1 : (part == CP_DOWN ? 0 : A.nl - 2);
+    const int u0 = part == CP_CLUSTER ? lt : 1;
+    for (int l = u1; l >= u0; --l) {
         const CLev& V = A.lev[l];
         const CLev& C = A.lev[l + 1];
         const Cheb c = coef[l].c;
         for (long long v = tid; v < V.L.nv; v += nth) v_prolong(V.L, C.L, C.L.mask, C.x, V.x, v);
-        grid_sync(A.bar);
+        sync();
         TR();
         grid_each(V.L.nv, [&](auto g, long long v, int q) { v_post_first<false, decltype(g)::value>(V.L, V.x, V.b, V.res, V.d0, c, v, q); });
-        grid_sync(A.bar);
+        sync();
         TR();
         if (deg <= 1) {
             for (long long v = tid; v < V.L.nv; v += nth) {
@@ -1040,8 +1066,8 @@ __device__ __forceinline__ void coarse_body(const CoarseArgs& A, const CCoef* co
                 xv.y += dv.y;
                 stv(V.x, v, xv);
             }
-            grid_sync(A.bar);
-        TR();
+            sync();
+            TR();
         }
         double* d = V.d0;
         double* dn = V.d1;
@@ -1049,13 +1075,13 @@ __device__ __forceinline__ void coarse_body(const CoarseArgs& A, const CCoef* co
             double a, b;
             a = coef[l].a[k]; b = coef[l].b[k];
             grid_each(V.L.nv, [&](auto g, long long v, int q) { v_cheb_step<false, decltype(g)::value>(V.L, nullptr, d, dn, V.res, V.x, a, b, k == 1, v, q); });
-            grid_sync(A.bar);
-        TR();
+            sync();
+            TR();
             double* tmp = d; d = dn; dn = tmp;
         }
     }
     // level 1 -> 0 prolongation (crossed: centres take the mean of their corners' corrections)
-    {
+    if (part == CP_ALL || part == CP_UP) {
         const CLev& C = A.lev[1];
         if (A.crossed) {
             const Geo2& g = A.g;
@@ -1085,12 +1111,25 @@ __device__ __forceinline__ void coarse_body(const CoarseArgs& A, const CCoef* co
 }
 
 __global__ void __launch_bounds__(kCB, 1) k_gmg_coarse(const __grid_constant__ CoarseArgs A, const double* lam,
-                                                       const double* live) {
+                                                       const double* live, int part, int lt) {
     if (!gmg_live(live) || A.skip) return;  // uniform: the flags are not written during the launch
     extern __shared__ __align__(16) unsigned char sm[];
     CCoef* coef = reinterpret_cast<CCoef*>(sm + A.coef_off);
     coarse_coef(A, lam, coef);
-    coarse_body(A, coef, blockIdx.x * (long long)kCB + threadIdx.x, (long long)gridDim.x * kCB);
+    __syncthreads();
+    coarse_body(A, coef, blockIdx.x * (long long)kCB + threadIdx.x, (long long)gridDim.x * kCB, part, lt,
+                GridBar{A.bar});
+}
+// levels lt..nl-1 of the coarse cycle in ONE thread-block cluster (grid = the cluster)
+__global__ void __launch_bounds__(kCB, 1) k_gmg_ctail(const __grid_constant__ CoarseArgs A, const double* lam,
+                                                      const double* live, int lt) {
+    if (!gmg_live(live) || A.skip) return;
+    extern __shared__ __align__(16) unsigned char sm[];
+    CCoef* coef = reinterpret_cast<CCoef*>(sm + A.coef_off);
+    coarse_coef(A, lam, coef);
+    __syncthreads();
+    coarse_body(A, coef, blockIdx.x * (long long)kCB + threadIdx.x, (long long)gridDim.x * kCB, CP_CLUSTER, lt,
+                ClusterBar{});
 }
 
 // z_f = 0 helper + level-0 vector ops
@@ -1388,6 +1427,29 @@ static int make_coarse_args(Ctx* c, const double* r0, double* z0, CoarseArgs& a)
     return smem;
 }
 
+// The small coarse levels (<= kClusterMaxV vertices) run inside one thread-block cluster of
+// kClusterCTAs CTAs (cluster barriers instead of grid barriers); the levels above stay grid-wide.
+constexpr long long kClusterMaxV = 20000;
+static int cluster_level(const Ctx* c) {
+    const int nl = (int)c->glev.size();
+    int lt = nl - 1;
+    while (lt > 1 && c->glev[lt - 1].nv <= kClusterMaxV) --lt;
+    return lt;
+}
+// algorithmic bytes of the per-phase launches the persistent phases of levels [la, lb) replace
+static double coarse_level_bytes(const Ctx* c, int la, int lb, int deg, int ncoarse) {
+    const int nl = (int)c->glev.size();
+    double bytes = 0.0;
+    for (int l = std::max(1, la); l < lb && l < nl; ++l) {
+        const double nv = (double)c->glev[l].nv;
+        if (l == nl - 1) { bytes += 8.0 * ncoarse * ncoarse + 32.0 * ncoarse; break; }
+        const double nvc = (double)c->glev[l + 1].nv;
+        bytes += (deg > 1 ? 416.0 : 96.0) * nv + 416.0 * std::max(0, deg - 2) * nv + 336.0 * nv + 16.0 * nv + 17.0 * nvc;
+        bytes += 32.0 * nv + 17.0 * nvc + 400.0 * nv + (deg <= 1 ? 48.0 : 416.0 * (deg - 1)) * nv;
+    }
+    return bytes;
+}
+
 static int launch_coarse(Ctx* c, const double* r0, double* z0, cudaStream_t st, const double* live) {
     const Geo2& g = c->g;
     const int nl = (int)c->glev.size();
@@ -1398,11 +1460,12 @@ static int launch_coarse(Ctx* c, const double* r0, double* z0, cudaStream_t st, 
     static int ntrace_calls = 0;
     if (getenv("PF_GMG_TRACE") && !trace) cudaMalloc(&trace, 128 * sizeof(unsigned long long));
     a.trace = trace;
-    static int nb_cache_d[kMaxDev], nb_smem_d[kMaxDev];
+    static int nb_cache_d[kMaxDev], nb_smem_d[kMaxDev], ncl_d[kMaxDev];
     static std::atomic<bool> nb_ok[kMaxDev];
     const int dvc = cur_dev();
     int& nb_cache = nb_cache_d[dvc];
     int& nb_smem = nb_smem_d[dvc];
+    int& ncl = ncl_d[dvc];  // CTAs of the cluster part (0: no cluster launch possible)
     if (!nb_ok[dvc].load() || nb_smem != smem) {
         int dev = 0, nsm = 0, per = 0;
         GCU(c, cudaGetDevice(&dev), "device");
@@ -1411,20 +1474,35 @@ static int launch_coarse(Ctx* c, const double* r0, double* z0, cudaStream_t st, 
         if (per < 1) return set_error(c, PF_ECUDA, "gmg: coarse-cycle kernel cannot be resident");
         nb_cache = nsm * per;
         nb_smem = smem;
+        // the largest cluster (16 non-portable, else 8) this kernel can be launched with
+        ncl = 0;
+        cudaFuncSetAttribute(k_gmg_ctail, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        for (int cs : {16, 8}) {
+            cudaLaunchConfig_t q = {};
+            q.gridDim = dim3(cs);
+            q.blockDim = dim3(kCB);
+            q.dynamicSmemBytes = smem;
+            cudaLaunchAttribute qa[1];
+            qa[0].id = cudaLaunchAttributeClusterDimension;
+            qa[0].val.clusterDim.x = cs; qa[0].val.clusterDim.y = 1; qa[0].val.clusterDim.z = 1;
+            q.attrs = qa;
+            q.numAttrs = 1;
+            int nclusters = 0;
+            if (cudaOccupancyMaxActiveClusters(&nclusters, k_gmg_ctail, &q) == cudaSuccess && nclusters >= 1) {
+                ncl = cs;
+                break;
+            }
+            cudaGetLastError();
+        }
         nb_ok[dvc] = true;
     }
-    // algorithmic bytes: those of the per-phase launches it replaces
     const int deg = a.deg;
     const GLevel& L1 = c->glev[1];
-    double bytes = a.crossed ? 48.0 * g.nc + 16.0 * g.nc + 17.0 * L1.nv + 32.0 * g.nc + 17.0 * L1.nv + 48.0 * g.nv
-                             : 16.0 * g.nc + 17.0 * L1.nv + 32.0 * g.nc + 17.0 * L1.nv;
-    for (int l = 1; l < nl; ++l) {
-        const double nv = (double)c->glev[l].nv;
-        if (l == nl - 1) { bytes += 8.0 * a.ncoarse * a.ncoarse + 32.0 * a.ncoarse; break; }
-        const double nvc = (double)c->glev[l + 1].nv;
-        bytes += (deg > 1 ? 416.0 : 96.0) * nv + 416.0 * std::max(0, deg - 2) * nv + 336.0 * nv + 16.0 * nv + 17.0 * nvc;
-        bytes += 32.0 * nv + 17.0 * nvc + 400.0 * nv + (deg <= 1 ? 48.0 : 416.0 * (deg - 1)) * nv;
-    }
+    const double top = a.crossed ? 48.0 * g.nc + 16.0 * g.nc + 17.0 * L1.nv + 32.0 * g.nc + 17.0 * L1.nv + 48.0 * g.nv
+                                 : 16.0 * g.nc + 17.0 * L1.nv + 32.0 * g.nc + 17.0 * L1.nv;
+    const double* lam = c->scal + S_GMG0;
+    cudaError_t le = cudaSuccess;
+    if (trace) cudaMemsetAsync(trace, 0, 128 * sizeof(unsigned long long), st);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(nb_cache);
     cfg.blockDim = dim3(kCB);
@@ -1435,16 +1513,40 @@ static int launch_coarse(Ctx* c, const double* r0, double* z0, cudaStream_t st, 
     at[0].val.cooperative = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    const double* lam = c->scal + S_GMG0;
-    cudaError_t le = cudaSuccess;
-    if (trace) cudaMemsetAsync(trace, 0, 128 * sizeof(unsigned long long), st);
-    GKB(c, K_GMG, bytes, (le = cudaLaunchKernelEx(&cfg, k_gmg_coarse, a, lam, live)));
+    const int lt = cluster_level(c);
+    const bool split = ncl > 0 && c->gmg_cluster && lt < nl;
+    if (!split) {
+        const double bytes = top + coarse_level_bytes(c, 1, nl, deg, a.ncoarse);
+        GKB(c, K_GMG, bytes, (le = cudaLaunchKernelEx(&cfg, k_gmg_coarse, a, lam, live, (int)CP_ALL, lt)));
+    } else {
+        const double b_top = coarse_level_bytes(c, 1, lt, deg, a.ncoarse);
+        GKB(c, K_GMG, 0.5 * (top + b_top), (le = cudaLaunchKernelEx(&cfg, k_gmg_coarse, a, lam, live, (int)CP_DOWN, lt)));
+        if (le == cudaSuccess) {
+            cudaLaunchConfig_t q = {};
+            q.gridDim = dim3(ncl);
+            q.blockDim = dim3(kCB);
+            q.dynamicSmemBytes = smem;
+            q.stream = st;
+            cudaLaunchAttribute qa[1];
+            qa[0].id = cudaLaunchAttributeClusterDimension;
+            qa[0].val.clusterDim.x = ncl; qa[0].val.clusterDim.y = 1; qa[0].val.clusterDim.z = 1;
+            q.attrs = qa;
+            q.numAttrs = 1;
+            GKB(c, K_GMG, coarse_level_bytes(c, lt, nl, deg, a.ncoarse), (le = cudaLaunchKernelEx(&q, k_gmg_ctail, a, lam, live, lt)));
+        }
+        if (le == cudaSuccess)
+            GKB(c, K_GMG, 0.5 * (top + b_top), (le = cudaLaunchKernelEx(&cfg, k_gmg_coarse, a, lam, live, (int)CP_UP, lt)));
+    }
     if (trace && ++ntrace_calls % 8 == 5) {  // eager mode only (PF_NO_GRAPHS): print one cycle's phases
         unsigned long long h[128];
         cudaMemcpyAsync(h, trace, sizeof h, cudaMemcpyDeviceToHost, st);
         cudaStreamSynchronize(st);
-        fprintf(stderr, "coarse cycle nb=%d lc=%d nl=%d smem=%d phases(us):", nb_cache, a.lc, nl, smem);
-        for (int q = 1; q < 128 && h[q]; ++q) fprintf(stderr, " %.2f", 1e-3 * (double)(h[q] - h[q - 1]));
+        fprintf(stderr, "coarse cycle nb=%d cluster=%d lt=%d nl=%d smem=%d phases(us):", nb_cache, split ? ncl : 0, lt,
+                nl, smem);
+        for (int seg = 0; seg < 3; ++seg) {
+            fprintf(stderr, seg ? " |" : "");
+            for (int q = 40 * seg + 1; q < 40 * seg + 40 && h[q]; ++q) fprintf(stderr, " %.2f", 1e-3 * (double)(h[q] - h[q - 1]));
+        }
         fprintf(stderr, "\n");
     }
     return check_cuda(c, le, "coarse-cycle launch");

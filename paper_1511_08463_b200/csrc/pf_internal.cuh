@@ -317,6 +317,7 @@ struct Ctx {
     int pcg_persistent = 1;         // damage PCG in one cooperative launch (PF_PCG_GRAPH=1: graph loop)
     int pcg_single = 0;             // ... in the single-reduction form (PF_PCG_SINGLE=1; measured slower)
     int gmg_coarse = 1;             // persistent coarse cycle (0: one launch per phase, PF_GMG_LEGACY)
+    int gmg_cluster = 0;            // small coarse levels in one thread-block cluster (PF_GMG_CLUSTER=1: on)
     int gmg_degree = 2;
     int gmg_built = 0;              // hierarchy valid for reuse (pf_lin_opts.gmg_reuse)
     long long gmg_its0 = -1;        // iterations of the first elastic solve on it (-1: none yet)

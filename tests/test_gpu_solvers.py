@@ -286,11 +286,15 @@ def test_persistent_coarse_cycle_matches_the_per_phase_cycle(pattern, shape, mon
     import paper_1511_08463_b200 as pf
     nx, ny = shape
     out = {}
-    for legacy in (False, True):
-        if legacy:
+    for legacy in ("cluster", False, True):
+        # "cluster": the small levels inside one thread-block cluster (PF_GMG_CLUSTER, opt-in);
+        # False: every coarse level in the grid-wide launch (default); True: one launch per phase
+        monkeypatch.delenv("PF_GMG_LEGACY", raising=False)
+        monkeypatch.delenv("PF_GMG_CLUSTER", raising=False)
+        if legacy is True:
             monkeypatch.setenv("PF_GMG_LEGACY", "1")
-        else:
-            monkeypatch.delenv("PF_GMG_LEGACY", raising=False)
+        elif legacy == "cluster":
+            monkeypatch.setenv("PF_GMG_CLUSTER", "1")
         prob, om, rng = make_pair(pattern, "plane_strain", "AT2", nx, ny, lx=1.0, ly=ny / nx,
                                   hetero=True, eps0=False)
         v = om.mesh.vertices
@@ -299,10 +303,13 @@ def test_persistent_coarse_cycle_matches_the_per_phase_cycle(pattern, shape, mon
         cfg = pf.SolverConfig(elastic_solver="cg", elastic_rtol=1e-10, elastic_precond="gmg",
                               warm_start=True)
         out[legacy] = pf.elastic_step(st, prob, cfg)
-    (u0, k0), (u1, k1) = out[False], out[True]
+    (u0, k0), (u1, k1), (u2, k2) = out[False], out[True], out["cluster"]
     d = float((u0 - u1).abs().max()) / float(u1.abs().max())
     assert abs(k0 - k1) <= 1, (k0, k1, d)
     assert d < 1e-8, d
+    d2 = float((u2 - u1).abs().max()) / float(u1.abs().max())
+    assert abs(k2 - k1) <= 1, (k2, k1, d2)
+    assert d2 < 1e-8, d2
 
 
 @pytest.mark.parametrize("pattern", ["union_jack", "right", "crossed"])

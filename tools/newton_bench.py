@@ -23,6 +23,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--state", default="steplocal_in/sent512_state17.npz")
 ap.add_argument("--step", type=int, default=18)
+ap.add_argument("--only", default="")
 args = ap.parse_args()
 os.environ["PF_NEWTON_NO_KEEP"] = "1"
 s0 = np.load(args.state)
@@ -43,6 +44,8 @@ VARIANTS = {
     "cheb_deg12": {"__deg": 12},
 }
 for name, env in VARIANTS.items():
+    if args.only and name not in args.only.split(","):
+        continue
     c = bench.sent_config(pf)
     for k, v in env.items():
         if k == "__deg":
