@@ -215,6 +215,11 @@ int pf_newton(pf_ctx* ctx, const double* u_in, const double* alpha_in, const dou
 
 /* Counters for the bench: kernel launches issued by this context since creation. */
 int64_t pf_launch_count(const pf_ctx* ctx);
+/* Bounds-check aid (no reference counterpart).  A context created with PF_WS_GUARD=1 in the
+ * environment puts a 16 KB guard zone after every workspace buffer (and every multigrid-level
+ * buffer), filled with 0xA5 at pf_bind_workspace; *bad_bytes = how many guard bytes differ now,
+ * i.e. out-of-bounds writes past any buffer since binding (0 without guards).  Synchronises. */
+int pf_check_guards(pf_ctx* ctx, int64_t* bad_bytes, void* stream);
 /* Per-kernel-class timing: when enabled, every launch is bracketed by CUDA events on its
  * stream.  pf_profile_read syncs and returns out[3k..3k+2] = (launches, total ms,
  * algorithmic bytes) for kernel class k = 0..nkinds-1 (order: Kuu, Kuu-CG, Kuu-diag, kappa,

@@ -92,6 +92,7 @@ EXPORTS = {
     "pf_newton": (C.c_int, [C.c_void_p] * 6 + [C.POINTER(VIOpts), C.POINTER(VIReport),
                                                 C.c_void_p]),
     "pf_launch_count": (C.c_int64, [C.c_void_p]),
+    "pf_check_guards": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64), C.c_void_p]),
     "pf_profile": (C.c_int, [C.c_void_p, C.c_int32]),
     "pf_profile_read": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
     # element-list meshes (umesh.py)

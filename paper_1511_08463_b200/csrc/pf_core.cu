@@ -892,7 +892,10 @@ __global__ void k_relax_u3(long long nv, int nvy, int nvz, int nx, int ny, int n
 
 static void plan_workspace(Ctx* c) {
     c->layout.clear();
-    auto add = [&](void** p, size_t bytes) { c->layout.push_back({p, (bytes + 255) & ~size_t(255)}); };
+    auto add = [&](void** p, size_t bytes) {
+        c->layout.push_back({p, (bytes + 255) & ~size_t(255)});
+        if (c->guard) c->layout.push_back({nullptr, c->guard});  // guard zone (bounds-check aid)
+    };
     const size_t U = sizeof(double) * c->n_u, A = sizeof(double) * c->n_a;
     double** uvecs[] = {&c->cg_x, &c->cg_r, &c->cg_z, &c->cg_p0, &c->cg_p1, &c->cg_q, &c->cg_dinv, &c->cg_b,
                         &c->u_ws, &c->ubar};
@@ -957,6 +960,7 @@ int pf_ctx_create(const pf_desc* desc, pf_ctx** out) {
     // cycle 125 -> 160 us), so the cluster tail is opt-in (PF_GMG_CLUSTER=1)
     c->gmg_cluster = getenv("PF_GMG_CLUSTER") ? 1 : 0;
     if (getenv("PF_PCG_GRAPH")) c->pcg_persistent = 0;
+    if (getenv("PF_WS_GUARD")) c->guard = 16384;
     if (getenv("PF_PCG_SINGLE")) c->pcg_single = 1;
     if (d3) {
         c->dim = 3;
@@ -1023,10 +1027,15 @@ int pf_bind_workspace(pf_ctx* c, void* p, int64_t bytes) {
     if (((uintptr_t)p & 255) != 0) return set_error(c, PF_EINVAL, "workspace must be 256-byte aligned");
     char* base = (char*)p;
     size_t off = 0;
+    c->guards.clear();
     for (auto& e : c->layout) {
-        *e.first = base + off;
+        if (e.first) *e.first = base + off;
+        else c->guards.push_back({off, e.second});
         off += e.second;
     }
+    for (auto& gz : c->guards)
+        if (cudaMemset(base + gz.first, kGuardByte, gz.second) != cudaSuccess)
+            return set_error(c, PF_ECUDA, "guard fill failed");
     c->ws = base;
     c->bound = 1;
     if (c->dim == 2 && !(c->d.skip & PF_SKIP_GMG)) gmg_bind(c, c->gmg_base);
@@ -1054,6 +1063,25 @@ int pf_bind_workspace(pf_ctx* c, void* p, int64_t bytes) {
         if (!(c)) return PF_EINVAL;                                                \
         if (!(c)->bound) return set_error((c), PF_ENOWS, "workspace not bound");   \
     } while (0)
+
+int pf_check_guards(pf_ctx* c, int64_t* bad_bytes, void* stream) {
+    NEED_WS(c);
+    if (!bad_bytes) return set_error(c, PF_EINVAL, "pf_check_guards: null output");
+    cudaStream_t st = (cudaStream_t)stream;
+    int64_t bad = 0;
+    std::vector<unsigned char> h;
+    std::vector<std::pair<const char*, size_t>> zones;
+    for (auto& gz : c->guards) zones.push_back({c->ws + gz.first, gz.second});
+    for (auto& gz : c->gmg_guards) zones.push_back({gz.first, gz.second});
+    for (auto& z : zones) {
+        h.resize(z.second);
+        PF_CU(c, cudaMemcpyAsync(h.data(), z.first, z.second, cudaMemcpyDeviceToHost, st), "guard read");
+        PF_CU(c, cudaStreamSynchronize(st), "guard sync");
+        for (unsigned char b : h) bad += (b != (unsigned char)kGuardByte);
+    }
+    *bad_bytes = bad;
+    return PF_OK;
+}
 
 int pf_set_cell_fields(pf_ctx* c, const double* E_cell, const double* Gc_cell) {
     if (!c) return PF_EINVAL;

@@ -1166,7 +1166,7 @@ void gmg_plan(Ctx* c) {
 
 size_t gmg_bytes(const Ctx* c) {
     size_t tot = 0;
-    auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+    auto al = [&](size_t b) { return ((b + 255) & ~size_t(255)) + c->guard; };  // + guard zone (PF_WS_GUARD)
     for (size_t l = 0; l < c->glev.size(); ++l) {
         const GLevel& L = c->glev[l];
         const long long nvc = (l == 0) ? c->g.nc : L.nv;
@@ -1183,8 +1183,17 @@ size_t gmg_bytes(const Ctx* c) {
 
 void gmg_bind(Ctx* c, char* base) {
     size_t off = 0;
-    auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
-    auto take = [&](size_t b) { char* p = base + off; off += al(b); return p; };
+    c->gmg_guards.clear();
+    auto take = [&](size_t b) {
+        char* p = base + off;
+        off += (b + 255) & ~size_t(255);
+        if (c->guard) {
+            c->gmg_guards.push_back({base + off, c->guard});
+            cudaMemset(base + off, kGuardByte, c->guard);
+            off += c->guard;
+        }
+        return p;
+    };
     for (size_t l = 0; l < c->glev.size(); ++l) {
         GLevel& L = c->glev[l];
         const long long nvc = (l == 0) ? c->g.nc : L.nv;

@@ -27,6 +27,7 @@ namespace pf {
 // Per-device one-time launch setup (the >48 KB shared-memory opt-in and occupancy queries are
 // properties of a device context): slot of the current device in a static per-kernel table.
 constexpr int kMaxDev = 64;
+constexpr int kGuardByte = 0xA5;  // workspace guard zones (PF_WS_GUARD)
 inline int cur_dev() {
     int d = 0;
     cudaGetDevice(&d);
@@ -282,6 +283,11 @@ struct Ctx {
     size_t ws_bytes = 0;
     char* ws = nullptr;
     std::vector<std::pair<void**, size_t>> layout;
+    // bounds-check aid (PF_WS_GUARD=1 at creation): a guard zone after every workspace buffer,
+    // filled with kGuardByte at binding; pf_check_guards counts the bytes kernels overwrote
+    size_t guard = 0;
+    std::vector<std::pair<size_t, size_t>> guards;  // (offset, bytes) in the workspace
+    std::vector<std::pair<char*, size_t>> gmg_guards;  // guard zones between the hierarchy buffers
     // named buffers (device)
     double *cg_x, *cg_r, *cg_z, *cg_p0, *cg_p1, *cg_q, *cg_dinv, *cg_b;     // n_u
     double *da_x, *da_r, *da_z, *da_p0, *da_p1, *da_q, *da_dinv;             // n_a (damage CG)

@@ -10,6 +10,7 @@ are matrix-free: ``assemble_Kuu`` & co. return operator objects whose ``matvec``
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 from typing import NamedTuple, Optional
 
@@ -145,6 +146,12 @@ class Discretization:
             _lib.raise_for(self.lib.pf_set_row_heights(ctx, hy.ctypes.data_as(C.c_void_p), _stream()), ctx)
         self._bc: Optional[DirichletBC] = None
         self._eps0_rows: Optional[np.ndarray] = None
+        self._guarded = bool(os.environ.get("PF_WS_GUARD"))  # read by pf_ctx_create as well
+
+    def ws_guarded(self) -> bool:
+        """True when the context was created with workspace guard zones (PF_WS_GUARD=1, a
+        bounds-check aid; pf_check_guards counts overwritten guard bytes)."""
+        return self._guarded
 
     def _field(self, f):
         if f is None:
