@@ -759,6 +759,8 @@ int newton_solve(Ctx* c, const double* u_in, const double* a_in, const double* l
     // tighter inner solves leave the MINRES history unchanged (measured on SENT 512^2 down to
     // 1e-10) at 1.5-2x the cost
     const double inner_rtol = o->inner_rtol > 0.0 ? o->inner_rtol : fs_rtol;
+    double last_mu = 1.0;      // accepted step length of the previous iteration
+    double last_lmax = -1.0;   // C-block spectrum estimate of the previous iteration
     auto line_search = [&](const double* dir, double slope, bool newton, bool& ok) -> int {
         double mu = 1.0;
         ok = false;
@@ -772,6 +774,7 @@ int newton_solve(Ctx* c, const double* u_in, const double* a_in, const double* l
             if (mt <= bound) {
                 ok = true;
                 merit = mt;
+                last_mu = mu;
                 std::swap(w.X, w.TX);
                 std::swap(w.FX, w.TF);
                 return PF_OK;
@@ -795,8 +798,14 @@ int newton_solve(Ctx* c, const double* u_in, const double* a_in, const double* l
         // so the old smoother bounds stay above the spectrum) -- one setup (~2.5 ms) saved per phase
         // 2D only: the 3D re-discretised hierarchy with a stale alpha preconditioned config-4 Newton
         // badly (~160 instead of ~20 MINRES iterations, measured)
-        const bool keep = c->dim == 2 && (o->inner_mode == 1 || o->inner_mode == 2) && it == 1 && c->gmg_built &&
-                          !getenv("PF_NEWTON_NO_KEEP");  // (tests: calls independent of the prior hierarchy)
+        // A stalled Newton phase (the previous accepted step was at most 1/64 of its direction) barely
+        // moves the iterate: keep the hierarchy (2.5 ms of setup per iteration at 512^2) and the
+        // C-block spectrum estimate of the previous iteration; a breakdown rebuilds and retries.
+        const bool fixed_pc = o->inner_mode == 1 || o->inner_mode == 2;
+        const bool stalled = fixed_pc && it > 1 && last_mu <= 1.0 / 64.0 && !getenv("PF_NEWTON_NO_STALL_KEEP");
+        const bool keep = c->dim == 2 && fixed_pc && c->gmg_built &&
+                          ((it == 1 && !getenv("PF_NEWTON_NO_KEEP")) || stalled);  // (NO_KEEP: calls
+                                                         // independent of the prior hierarchy)
         if (!keep) {
             NTRY(c->dim == 3 ? gmg3_setup(c, st) : gmg_setup(c, st));
             c->gmg_built = 1;  // an elastic solve that follows may keep it (gmg_reuse)
@@ -809,7 +818,13 @@ int newton_solve(Ctx* c, const double* u_in, const double* a_in, const double* l
             mg.on = true;
             mg.additive = o->inner_mode == 2;
             mg.deg = o->inner_cycles > 0 ? o->inner_cycles : 12;
-            NTRY(lambda_C(c, mg.lmax, st));
+            if (stalled && keep && last_lmax > 0.0) {
+                mg.lmax = last_lmax;  // S_AUX1 still holds its |D^-1 C x|^2 unless MINRES ran on the host
+                NTRY(set_scal(c, st, S_AUX1, last_lmax * last_lmax));
+            } else {
+                NTRY(lambda_C(c, mg.lmax, st));
+            }
+            last_lmax = mg.lmax;
             // device-resident MINRES (graph) unless profiling (eager, bracketed launches) or disabled
             mg.dev = c->use_graphs && !c->prof.on && !getenv("PF_NEWTON_HOST_MINRES") && mg.deg <= kMaxChebDeg;
             if (mg.dev) {

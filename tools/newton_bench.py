@@ -39,6 +39,7 @@ rep = S.am_solve(st, setup.problem, cfg, rtol=cfg.am_rtol, cycle=0)
 print(f"AM to hand-off: {rep.am_iterations} its, residual {rep.final_residual_norm:.3e}", flush=True)
 VARIANTS = {
     "default": {},
+    "no_stall_keep": {"PF_NEWTON_NO_STALL_KEEP": "1"},
     "cold_minres": {"PF_MINRES_COLD": "1"},
     "host_minres": {"PF_NEWTON_HOST_MINRES": "1"},
     "cheb_deg12": {"__deg": 12},
