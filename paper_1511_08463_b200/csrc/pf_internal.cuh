@@ -408,6 +408,8 @@ int launch_kappa(Ctx* c, const double* u, const double* alpha, double* kappa, do
                  cudaStream_t st);
 int launch_Kaa(Ctx* c, const double* kappa, const double* x, double* y, const unsigned char* act,
                cudaStream_t st);
+int launch_Kaa_cheb(Ctx* c, const double* kappa, const double* d, const unsigned char* act, double* r,
+                    double* dnext, double* x, const double* dinv, const double* tab, int k, cudaStream_t st);
 int launch_Kaa_cgA(Ctx* c, const double* kappa, const double* z, const double* p_in,
                    double* p_out, double* q, const unsigned char* act, cudaStream_t st);
 int launch_Kaa_diag(Ctx* c, const double* kappa, double* dinv, const unsigned char* act,

@@ -288,10 +288,10 @@ __global__ void k_cheb_table(double* s, int deg, double safety) {
     }
 }
 __global__ void k_ncheb0_d(long long n, const double* dinv, const double* b, double* r, double* d, double* x,
-                           const double* s) {
+                           const double* s, const unsigned char* bmask) {
     const double ith = s[S_CHEB];
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-        const double ri = b[i];
+        const double ri = (bmask && bmask[i]) ? 0.0 : b[i];
         const double di = dinv[i] * ri * ith;
         r[i] = ri;
         d[i] = di;
@@ -421,13 +421,27 @@ static int cheb_C(Ctx* c, const double* b, double* x, double lmax, int deg, long
     its += deg;
     return PF_OK;
 }
-// the same polynomial with its coefficients read from the device table (graph-capturable)
-static int cheb_C_dev(Ctx* c, const double* b, double* x, int deg, long long& its, cudaStream_t st) {
+// the same polynomial with its coefficients read from the device table (graph-capturable); the
+// start-up applies the active mask to the raw right-hand side (bmask: rows of b to zero, or null).
+// PF_CHEB_FUSED=1 (2D): each step as one strip pass whose epilogue does the update at the owner
+// (launch_Kaa_cheb) -- measured slower beside the V-cycle on the side stream (stalled SENT Newton
+// phase 0.78 -> 0.82 s): the small separate update kernels interleave with the V-cycle phases.
+static int cheb_C_dev(Ctx* c, const double* b, double* x, int deg, long long& its, cudaStream_t st,
+                      const unsigned char* bmask = nullptr) {
     const long long n = c->n_a;
     const int nb = nblocks(n);
     double *r = c->da_r, *d = c->da_p0, *Cd = c->da_q;
-    k_ncheb0_d<<<nb, kNB, 0, st>>>(n, c->da_dinv, b, r, d, x, c->scal);
+    k_ncheb0_d<<<nb, kNB, 0, st>>>(n, c->da_dinv, b, r, d, x, c->scal, bmask);
     c->launches++;
+    if (c->dim == 2 && getenv("PF_CHEB_FUSED")) {
+        double* dn = Cd;
+        for (int k = 1; k < deg; ++k) {
+            NTRY(launch_Kaa_cheb(c, c->kappa, d, c->act, r, dn, x, c->da_dinv, c->scal + S_CHEB, k, st));
+            std::swap(d, dn);
+        }
+        its += deg;
+        return PF_OK;
+    }
     for (int k = 1; k < deg; ++k) {
         NTRY(launch_Kaa(c, c->kappa, d, Cd, c->act, st));
         k_nchebk_d<<<nb, kNB, 0, st>>>(n, c->da_dinv, Cd, r, d, x, c->scal, k);
@@ -469,9 +483,7 @@ static int fieldsplit(Ctx* c, const NewtonWs& w, const double* r, double* y, con
         cudaStream_t sd = c->side_stream;
         NCU(c, cudaEventRecord(c->ev_fork, st), "fork");
         NCU(c, cudaStreamWaitEvent(sd, c->ev_fork, 0), "fork wait");
-        k_nsubmask<<<nblocks(na), kNB, 0, sd>>>(na, r + nu, nullptr, c->act, w.TMP + nu);
-        c->launches++;
-        NTRY(cheb_C_dev(c, w.TMP + nu, z, mg.deg, its, sd));
+        NTRY(cheb_C_dev(c, r + nu, z, mg.deg, its, sd, c->act));  // (active rows of r zeroed)
         NCU(c, cudaEventRecord(c->ev_join, sd), "join");
         NTRY(vcycle_A(c, r, y1, its, st));
         NCU(c, cudaStreamWaitEvent(st, c->ev_join, 0), "join wait");

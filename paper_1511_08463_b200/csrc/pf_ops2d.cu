@@ -619,7 +619,16 @@ __device__ __forceinline__ void get_kappa(const Slots& s, int q, int off, double
 // reduced inactive-block operator J_NN of vi.py:235 embedded in full space).
 // vertex slots: x|z, [p_in], [act word]; cell: Gc, kappa x npc, [centre x|z, p_in, act word]
 // ec: [Gc, kappa x npc, (centre: x unmasked, active flag)]
-template <bool FUSED, bool MASKED>
+// CHEB: the apply feeds one Chebyshev step instead of storing y (the C block of Newton's field
+// split, pf_newton.cu cheb_C_dev): at each own vertex r -= (K d)_v ; d' = a d_v + b D^-1 r ;
+// x += d' with d' written to a second buffer (the neighbours still read d); a, b = tab[2k-1], tab[2k].
+struct KaaCheb {
+    double *r, *dnext, *xacc;
+    const double* dinv;
+    const double* tab;
+    int k;
+};
+template <bool FUSED, bool MASKED, bool CHEB = false>
 struct OpKaa {
     static constexpr int NV = 1, NC = 1, MINB = 2;
     static constexpr int VS = 1 + (FUSED ? 1 : 0) + (MASKED ? 1 : 0);  // vertex slots
@@ -638,9 +647,26 @@ struct OpKaa {
     double acc;
     double breg = 0.0;  // persistent PCG (k_pcg_kaa): beta held in a register instead of scal[S_BETA]
     int use_breg = 0;
-    __device__ bool enter() const {
+    KaaCheb ch{};
+    double ca = 0.0, cb = 0.0;
+    __device__ bool enter() {
+        if constexpr (CHEB) {
+            ca = ch.tab[2 * ch.k - 1];
+            cb = ch.tab[2 * ch.k];
+        }
         if (!FUSED) return true;
         return scal[S_DONE] == 0.0 && scal[S_FAIL] == 0.0;
+    }
+    __device__ __forceinline__ void store_y(long long id, double dv, double yy) const {
+        if constexpr (CHEB) {
+            const double ri = ch.r[id] - yy;
+            const double dn = ca * dv + cb * ch.dinv[id] * ri;
+            ch.r[id] = ri;
+            ch.dnext[id] = dn;
+            ch.xacc[id] += dn;
+        } else {
+            y[id] = yy;
+        }
     }
     __device__ __forceinline__ double xval(long long v) const {
         double z = __ldg(x + v);
@@ -730,7 +756,7 @@ struct OpKaa {
                 const long long cv = ctr(g, ci, j);
                 const double xc = ec[5];
                 const double yy = ec[6] != 0.0 ? xc : Y[4];
-                y[cv] = yy;
+                store_y(cv, xc, yy);
                 if (FUSED) { pout[cv] = xc; acc += xc * yy; }
             }
         }
@@ -739,7 +765,7 @@ struct OpKaa {
         const long long id = vid(g, i, j);
         double yy = t[0], p = v[0];
         if (is_act(id)) { p = xval(id); yy = p; }
-        y[id] = yy;
+        store_y(id, p, yy);
         if (FUSED) { pout[id] = p; acc += p * yy; }
     }
     __device__ void finish() {
@@ -1624,6 +1650,14 @@ int launch_Kaa(Ctx* c, const double* kappa, const double* x, double* y, const un
         return run_strip(c, op, st, K_KAA);
     }
     OpKaa<false, false> op{kappa, x, nullptr, nullptr, y, nullptr, c->scal, redbuf(c), 0.0};
+    return run_strip(c, op, st, K_KAA);
+}
+// one fused Chebyshev step of the masked C block (2D): K d feeds r, d' and x at the owner (KaaCheb)
+int launch_Kaa_cheb(Ctx* c, const double* kappa, const double* d, const unsigned char* act, double* r,
+                    double* dnext, double* x, const double* dinv, const double* tab, int k, cudaStream_t st) {
+    if (c->dim == 3) return set_error(c, PF_EINVAL, "launch_Kaa_cheb is 2D");
+    OpKaa<false, true, true> op{kappa, d, nullptr, nullptr, nullptr, act, c->scal, redbuf(c), 0.0};
+    op.ch = KaaCheb{r, dnext, x, dinv, tab, k};
     return run_strip(c, op, st, K_KAA);
 }
 int launch_Kaa_cgA(Ctx* c, const double* kappa, const double* z, const double* p_in, double* p_out,
