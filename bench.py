@@ -337,6 +337,26 @@ def read_profile(problem):
     return out
 
 
+def ncu_traffic(kind):
+    """DRAM bytes (read + write) per launch of a kernel class from the committed ncu --set full
+    capture (profiles/r02_ncu/summary.json, tools/ncu_r02.sh).  The multigrid-cycle class launches,
+    per V-cycle, one persistent coarse cycle and four fine smoother strips (two EPI_CHEB-like, two
+    EPI_RESID-like): its per-launch traffic is their average."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_ncu", "summary.json")) as f:
+            s = json.load(f)
+    except Exception:  # noqa: BLE001
+        return None, None
+    if kind == "gmg_cycle":
+        t = (s["k_gmg_coarse"]["dram_bytes_per_launch"] + 2 * s["OpKuuILb0ELi1E"]["dram_bytes_per_launch"]
+             + 2 * s["OpKuuILb0ELi2E"]["dram_bytes_per_launch"]) / 5.0
+        return round(t), ("profiles/r02_ncu/summary.json: ncu --set full dram__bytes_read.sum + "
+                          "dram__bytes_write.sum, mean over the class's launches per V-cycle (1 k_gmg_coarse "
+                          "+ 4 fine smoother strips); below the algorithmic bytes because the 512^2 working "
+                          "set is L2-resident")
+    return None, None
+
+
 def dominant_roofline(prof, peak, peak_kind):
     """Largest total-time kernel class that has algorithmic bytes; achieved = bytes / time."""
     cands = {k: v for k, v in prof.items() if v["bytes"] > 0 and v["ms"] > 0}
@@ -345,9 +365,10 @@ def dominant_roofline(prof, peak, peak_kind):
     name, p = max(cands.items(), key=lambda kv: kv[1]["ms"])
     gbs = p["bytes"] / (p["ms"] * 1e-3) / 1e9
     total = sum(v["ms"] for v in prof.values())
+    traffic, tsrc = ncu_traffic(name)
     return {"bound": "hbm", "kernel": name, "achieved": round(gbs, 2), "peak": peak,
             "peak_source": peak_kind, "unit": "GB/s", "frac": round(gbs / peak, 4),
-            "traffic": None, "launches": int(p["count"]),
+            "traffic": traffic, "traffic_source": tsrc, "launches": int(p["count"]),
             "avg_launch_us": round(1e3 * p["ms"] / max(p["count"], 1), 3),
             "bytes_per_launch": round(p["bytes"] / max(p["count"], 1)),
             "share_of_kernel_time": round(p["ms"] / total, 4) if total > 0 else None}
