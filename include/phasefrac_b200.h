@@ -263,6 +263,11 @@ int pf_umesh_bind_workspace(pf_umesh* m, void* dev_ptr, int64_t bytes, void* str
 int pf_umesh_set_dirichlet(pf_umesh* m, const int64_t* dofs, int64_t n, void* stream);
 /* y = Kuu(alpha) x (assemble_Kuu(...).matvec, fem.py:233-244); PF_BC_ELIMINATE: Dirichlet
  * rows/cols replaced by the identity. */
+/* Inelastic strain per element (assemble_load_u / thermal_strain, fem.py:192-199, cases.py:66-80):
+ * eps0 = DEVICE pointer to T x 3 (2D Voigt e11, e22, g12) or T x 6 (3D) doubles, caller-owned and
+ * kept alive by the caller; NULL clears.  Every strain of u (energies, residuals, the damage
+ * Hessian's elastic coupling) becomes B u - eps0; the Kuu apply is unchanged. */
+int pf_umesh_set_eps0(pf_umesh* m, const double* eps0, void* stream);
 int pf_umesh_apply_Kuu(pf_umesh* m, const double* alpha, const double* x, double* y, int32_t bc_mode,
                        void* stream);
 /* y = Kaa(u, alpha) x (assemble_Kaa(...).matvec, fem.py:266-282). */

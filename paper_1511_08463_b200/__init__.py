@@ -23,9 +23,10 @@ from .fem import (DeviceOperator, DirichletBC, Discretization, EnergyBreakdown, 
 from .solver import (NonlinearReport, SolverConfig, am_solve, coupled_newton_solve,  # noqa: F401
                      damage_step, elastic_step, first_order_residual, oram_n_solve,
                      residual_norm, solve_load_step)
-from .cases import (ProblemSetup, StepFailureError, StepRecord, run_quasistatic,  # noqa: F401
-                    setup_sent, setup_surfing, setup_thermal_slab, setup_traction,
-                    setup_traction3d, surfing_displacement)
+from .cases import (ProblemSetup, StepFailureError, StepRecord, UnstructuredSetup,  # noqa: F401
+                    run_quasistatic, run_quasistatic_unstructured, setup_sent, setup_surfing,
+                    setup_thermal_shock, setup_thermal_slab, setup_traction, setup_traction3d,
+                    surfing_displacement, thermal_strain)
 from .umesh import (UnstructuredMesh, UnstructuredOperators, jittered_box_mesh,  # noqa: F401
                     jittered_rect_mesh)
 

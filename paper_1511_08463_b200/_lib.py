@@ -102,6 +102,7 @@ EXPORTS = {
     "pf_umesh_workspace_bytes": (C.c_int64, [C.c_void_p]),
     "pf_umesh_bind_workspace": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
     "pf_umesh_set_dirichlet": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
+    "pf_umesh_set_eps0": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "pf_umesh_apply_Kuu": (C.c_int, [C.c_void_p] * 4 + [C.c_int32, C.c_void_p]),
     "pf_umesh_apply_Kaa": (C.c_int, [C.c_void_p] * 5 + [C.c_void_p]),
     "pf_umesh_elastic_solve": (C.c_int, [C.c_void_p] * 4 + [C.POINTER(LinOpts), C.POINTER(LinReport),

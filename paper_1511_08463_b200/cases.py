@@ -260,12 +260,15 @@ def _to_host(problem, t) -> np.ndarray:
     return v.numpy().copy().reshape(tuple(t.shape))
 
 
-def run_quasistatic(setup: ProblemSetup, config: SolverConfig, snapshot_stride: int = 1,
+def run_quasistatic(setup, config: SolverConfig, snapshot_stride: int = 1,
                     state: Optional[State] = None, steps=None) -> list:
     """March a state through the loading schedule (cases.py:268-306).
 
     Fields stay on the device; snapshots are copied to the host every
-    ``snapshot_stride`` steps (and on the final step)."""
+    ``snapshot_stride`` steps (and on the final step).  An ``UnstructuredSetup`` (element-list
+    mesh, e.g. the thermal-shock case) runs on the element-list path."""
+    if isinstance(setup, UnstructuredSetup):
+        return run_quasistatic_unstructured(setup, config, snapshot_stride, state, steps)
     problem = setup.problem
     state = State.zeros(setup.mesh, setup.initial_alpha_lb, device=problem.device) \
         if state is None else state
@@ -290,6 +293,117 @@ def run_quasistatic(setup: ProblemSetup, config: SolverConfig, snapshot_stride: 
         records.append(StepRecord(step=k, load=t, energy=energy, report=report,
                                   u=_to_host(problem, state.u) if snap else None,
                                   alpha=_to_host(problem, state.alpha) if snap else None))
+        if not report.converged:
+            raise StepFailureError(k, t, records, state, report)
+    return records
+
+
+# -- element-list meshes: the reference's thermal-shock case -------------------
+
+@dataclass
+class UnstructuredSetup:
+    """A benchmark on an element-list mesh (the ProblemSetup of cases.py:83-109).  ``apply_load(ops,
+    t)`` installs the inelastic strain for load value t and returns the Dirichlet data (dofs,
+    values)."""
+
+    name: str
+    mesh: object
+    ops: object
+    schedule: np.ndarray
+    apply_load: Callable
+    initial_alpha_lb: Optional[np.ndarray] = None
+    params: dict = field(default_factory=dict)
+
+    def __post_init__(self):
+        self.schedule = np.asarray(self.schedule, dtype=float)
+        if self.schedule.ndim != 1 or np.any(np.diff(self.schedule) <= 0.0):
+            raise ValueError("schedule must be a strictly increasing 1D array of load values")
+
+
+def thermal_strain(x2, tau: float, material: Material, delta_T: float) -> np.ndarray:
+    """(e, e, 0) Voigt with e = -beta dT erfc(x2 / (ell tau)) (the reference's thermal_strain,
+    cases.py:66-80)."""
+    from scipy.special import erfc
+    if tau <= 0.0:
+        raise ValueError(f"tau must be positive, got {tau}")
+    x2 = np.asarray(x2, dtype=float)
+    e = -material.beta * delta_T * erfc(x2 / (material.ell * tau))
+    out = np.zeros(x2.shape + (3,))
+    out[..., 0] = e
+    out[..., 1] = e
+    return out
+
+
+def setup_thermal_shock(material: Optional[Material] = None, L: float = 20.0, H: float = 10.0,
+                        h: Optional[float] = None, dT_factor: float = 1.0, n_steps: int = 40,
+                        tau_min: float = 0.05, tau_max: float = 3.0, jitter: float = 0.25,
+                        model: str = "AT1") -> UnstructuredSetup:
+    """Quench of [0, L] x [0, H] from its bottom surface (the reference's setup_thermal_shock,
+    cases.py:195-235) on the element-list path: the jittered union-jack rect_mesh (mesh.py:112-142,
+    seed 0), the erfc inelastic strain at the element centroids, u1 = 0 on the lateral sides,
+    u2 = 0 on the top, tau in geomspace(tau_min, tau_max, n_steps), dT = dT_factor dT_c."""
+    from .umesh import UnstructuredOperators, jittered_rect_mesh
+    material = material or Material(ell=1.0)
+    h = material.ell / 4.0 if h is None else h
+    mesh = jittered_rect_mesh(L, H, h, jitter=jitter)
+    ops = UnstructuredOperators(mesh, material, model)
+    dTc = critical_shock(material)
+    dT = dT_factor * dTc
+    b = mesh.boundary
+    dofs = np.unique(np.concatenate([2 * b["left"], 2 * b["right"], 2 * b["top"] + 1])).astype(np.int64)
+    vals = np.zeros(dofs.size)
+    depth = mesh.vertices[mesh.elements].mean(axis=1)[:, 1]
+
+    def apply_load(ops, tau):
+        ops.set_eps0(thermal_strain(depth, tau, material, dT))
+        return dofs, vals
+
+    schedule = np.geomspace(tau_min, tau_max, n_steps)
+    return UnstructuredSetup("thermal_shock", mesh, ops, schedule, apply_load,
+                             params={"delta_T": dT, "critical_shock": dTc, "h": h})
+
+
+def run_quasistatic_unstructured(setup: UnstructuredSetup, config: SolverConfig, snapshot_stride: int = 1,
+                                 state: Optional[State] = None, steps=None) -> list:
+    """run_quasistatic (cases.py:268-306) on an element-list mesh: per load step the alternate
+    minimisation of UnstructuredOperators.am_load_step (elastic Jacobi-PCG half-step, damage VI,
+    over-relaxation with the midpoint rule).  There is no Newton phase on this path: methods other
+    than "am" (= the INI's am / oram) are a ValueError."""
+    import torch
+    from .vi import ActiveSetReport  # noqa: F401  (report types shared with the structured path)
+    if config.method != "am":
+        raise ValueError(f"method {config.method!r} needs the coupled Newton step, which the element-list "
+                         "path does not have; use method 'am' (am / oram in the INI)")
+    ops, mesh = setup.ops, setup.mesh
+    d = mesh.dim
+    if state is None:
+        lb = np.zeros(mesh.n_vertices) if setup.initial_alpha_lb is None else setup.initial_alpha_lb
+        state = State(u=torch.zeros(d * mesh.n_vertices, dtype=torch.float64, device=ops.device),
+                      alpha=torch.as_tensor(lb, dtype=torch.float64, device=ops.device).clone(),
+                      alpha_lb=torch.as_tensor(lb, dtype=torch.float64, device=ops.device).clone())
+    rtol = config.direct_rtol if config.elastic_solver == "direct" else config.elastic_rtol
+    records = []
+    n = setup.schedule.shape[0]
+    for k in (range(n) if steps is None else steps):
+        t = float(setup.schedule[k])
+        state.load = t
+        state.alpha_lb = state.alpha.clone()
+        dofs, vals = setup.apply_load(ops, t)
+        st = ops.am_load_step(state.u, state.alpha, state.alpha_lb, dofs, vals, omega=config.omega,
+                              outer_atol=config.outer_atol, max_am_iterations=config.max_am_iterations,
+                              elastic_rtol=rtol, damage_atol_factor=config.damage_atol_factor,
+                              max_vi_iterations=config.max_vi_iterations, log_callback=config.log_callback)
+        en = st["energy_history"][-1]
+        energy = EnergyBreakdown(*en)
+        report = NonlinearReport(converged=bool(st["converged"]), final_residual_norm=st["final_residual_norm"],
+                                 am_iterations=st["am_iterations"], total_krylov_iterations=st["krylov_iterations"],
+                                 omega_bar_min=st["omega_bar_min"],
+                                 energy_history=[EnergyBreakdown(*e) for e in st["energy_history"]],
+                                 residual_history=list(st["residual_history"]))
+        snap = snapshot_stride > 0 and (k % snapshot_stride == 0 or k == n - 1)
+        records.append(StepRecord(step=k, load=t, energy=energy, report=report,
+                                  u=state.u.cpu().numpy() if snap else None,
+                                  alpha=state.alpha.cpu().numpy() if snap else None))
         if not report.converged:
             raise StepFailureError(k, t, records, state, report)
     return records

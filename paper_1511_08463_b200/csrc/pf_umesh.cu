@@ -47,6 +47,7 @@ struct pf_umesh {
     // Jacobi-PCG work vectors (d*nv each) + per-block partials + scalars
     double *r = nullptr, *z = nullptr, *p = nullptr, *q = nullptr, *dinv = nullptr, *part = nullptr,
            *scal = nullptr;
+    const double* eps0 = nullptr;  // caller-owned inelastic strain per element (T x 3 / T x 6), or null
     bool bound = false, has_bc = false;
     int64_t launches = 0;
 };
@@ -64,6 +65,7 @@ struct UParams {
     double lam, mu;        // 3D unit stiffness
     double k_ell, inv_cw, ell, inv_ell;
     int at2;
+    const double* eps0;  // inelastic strain (Voigt) per element or null: strains of u are B u - eps0
 };
 
 UParams make_params(const pf_umesh* m) {
@@ -83,7 +85,15 @@ UParams make_params(const pf_umesh* m) {
     p.ell = m->ell;
     p.inv_ell = 1.0 / m->ell;
     p.at2 = m->model == PF_AT2;
+    p.eps0 = m->eps0;
     return p;
+}
+// strain of u minus the element's inelastic strain (fem.py:125-131 with eps0, oracle/p1.py strain)
+template <int NVOIGT>
+__device__ __forceinline__ void sub_eps0(const UParams& p, int64_t e, double (&eps)[NVOIGT]) {
+    if (!p.eps0) return;
+#pragma unroll
+    for (int i = 0; i < NVOIGT; ++i) eps[i] -= __ldg(p.eps0 + NVOIGT * e + i);
 }
 
 // ---- 2D ------------------------------------------------------------------------------------
@@ -228,6 +238,7 @@ __global__ void __launch_bounds__(256) k_umesh_Kaa2(
         }
         double eps[3];
         strain2(r, ue, eps);
+        sub_eps0<3>(p, e, eps);
         const double q = eps[0] * (p.d11 * eps[0] + p.d12 * eps[1])
                        + eps[1] * (p.d12 * eps[0] + p.d11 * eps[1]) + p.d33 * eps[2] * eps[2];
         const double wpp = p.at2 ? 2.0 : 0.0;
@@ -374,6 +385,7 @@ __global__ void __launch_bounds__(256) k_umesh_Kaa3(
         }
         double eps[6], s[6];
         strain3(r, ue, eps);
+        sub_eps0<6>(p, e, eps);
         stress3(p, eps, s);
         double q = 0.0;
 #pragma unroll
@@ -523,6 +535,7 @@ __global__ void __launch_bounds__(256) k_umesh_energy(
             ab_terms(p, ab * (1.0 / 3.0), A, Ap, w, wp);
             double eps[3];
             strain2(r, ue, eps);
+            sub_eps0<3>(p, e, eps);
             q = eps[0] * (p.d11 * eps[0] + p.d12 * eps[1]) + eps[1] * (p.d12 * eps[0] + p.d11 * eps[1])
               + p.d33 * eps[2] * eps[2];
             gg = ga[0] * ga[0] + ga[1] * ga[1];
@@ -543,6 +556,7 @@ __global__ void __launch_bounds__(256) k_umesh_energy(
             ab_terms(p, ab * 0.25, A, Ap, w, wp);
             double eps[6], sg[6];
             strain3(r, ue, eps);
+            sub_eps0<6>(p, e, eps);
             stress3(p, eps, sg);
             q = 0.0;
 #pragma unroll
@@ -611,6 +625,11 @@ __global__ void __launch_bounds__(256) k_umesh_grad(
                 e1 += g[1][j] * ue[j][1];
                 e2 += g[1][j] * ue[j][0] + g[0][j] * ue[j][1];
             }
+            if (p.eps0) {
+                e0 -= __ldg(p.eps0 + 3 * (int64_t)e);
+                e1 -= __ldg(p.eps0 + 3 * (int64_t)e + 1);
+                e2 -= __ldg(p.eps0 + 3 * (int64_t)e + 2);
+            }
             const double s0 = p.d11 * e0 + p.d12 * e1, s1 = p.d12 * e0 + p.d11 * e1, s2 = p.d33 * e2;
             q = e0 * s0 + e1 * s1 + e2 * s2;
             const double wA = A * volE;
@@ -624,6 +643,7 @@ __global__ void __launch_bounds__(256) k_umesh_grad(
                 for (int j = 0; j < 4; ++j) r.g[d][j] = g[d][j];
             double eps[6], sg[6];
             strain3(r, ue, eps);
+            sub_eps0<6>(p, e, eps);
             stress3(p, eps, sg);
             q = 0.0;
 #pragma unroll
@@ -903,6 +923,13 @@ int pf_umesh_set_dirichlet(pf_umesh* m, const int64_t* dofs, int64_t n, void* st
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // host staging dies with this call
     if (e != cudaSuccess) return cuda_fail(m, e);
     m->has_bc = n > 0;
+    return PF_OK;
+}
+
+int pf_umesh_set_eps0(pf_umesh* m, const double* eps0, void* stream) {
+    (void)stream;
+    if (!m) return PF_EINVAL;
+    m->eps0 = eps0;  // device pointer, T x (3 | 6) Voigt per element; NULL clears
     return PF_OK;
 }
 

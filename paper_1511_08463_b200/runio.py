@@ -6,8 +6,10 @@ validation, the same artifacts (energies.csv, iterations.csv, step_NNNN.vtk, pro
 summary.csv) and exit codes (0 ok, 2 configuration, 3 non-convergence, 4 I/O).  Differences,
 all loud:
 
-* ``[case] name = thermal_shock`` uses the reference's jittered unstructured mesh
-  (mesh.py:112-142), which has no structured device form: ConfigError.
+* ``[case] name = thermal_shock`` runs on the element-list path (the reference's jittered
+  rect_mesh, mesh.py:112-142; cases.setup_thermal_shock): alternate minimisation only (methods am
+  and oram); oram_n / newton_only need the coupled Newton step, which that path does not have:
+  ConfigError.
 * ``[linear] elastic = cg`` with ``elastic_precond = ssor | chebyshev`` has no device form
   (two sparse triangular solves / a stand-alone polynomial): ConfigError.  ``elastic = direct``
   is device PCG at the parity tolerance with the multigrid preconditioner whatever the
@@ -263,9 +265,12 @@ def build_setup(cfg: RunConfig):
                               load_max_factor=cfg.load_max_factor)
     if cfg.case == "surfing":
         return setup_surfing(mat, L=cfg.L, H=cfg.H, h=cfg.h, n_steps=cfg.n_steps, t_end=cfg.t_end)
-    raise ConfigError("[case] thermal_shock runs on the reference's jittered unstructured mesh, which "
-                      "has no structured device form (the structured slab of BASELINE config 3 is "
-                      "cases.setup_thermal_slab)")
+    from .cases import setup_thermal_shock
+    if cfg.method not in ("am", "oram"):
+        raise ConfigError(f"[solver] method {cfg.method} needs the coupled Newton step, which the element-list "
+                          "path of [case] thermal_shock does not have; use method am or oram")
+    return setup_thermal_shock(mat, L=cfg.L, H=cfg.H, h=cfg.h, dT_factor=cfg.dT_factor, n_steps=cfg.n_steps,
+                               tau_min=cfg.tau_min, tau_max=cfg.tau_max)
 
 
 # ---- artifacts ---------------------------------------------------------------------------------
@@ -309,7 +314,10 @@ def write_iterations_csv(path: Path, rows: list) -> None:
 
 def triangles(mesh) -> np.ndarray:
     """(T, 3) vertex triples in the reference element order (mesh.py:95-99): every cell's first
-    triangle (I-major), then every second one; crossed: the 4 centre fans in turn."""
+    triangle (I-major), then every second one; crossed: the 4 centre fans in turn.  Element-list
+    meshes carry their triangles."""
+    if getattr(mesh, "elements", None) is not None:
+        return np.asarray(mesh.elements, dtype=np.intp)
     nx, ny = mesh.nx, mesh.ny
     I, J = (a.ravel() for a in np.meshgrid(np.arange(nx), np.arange(ny), indexing="ij"))
     v00, v10 = I * (ny + 1) + J, (I + 1) * (ny + 1) + J
@@ -346,8 +354,9 @@ def write_vtk(path: Path, mesh, alpha: np.ndarray, u: np.ndarray, title: str) ->
 
 def write_provenance(path: Path, cfg: RunConfig, setup) -> None:
     from . import __version__
+    material = setup.ops.material if hasattr(setup, "ops") else setup.problem.material
     lines = [f"paper_1511_08463_b200 {__version__} (B200 device path)",
-             f"elastic_regime = {setup.problem.material.regime}", f"case = {setup.name}"]
+             f"elastic_regime = {material.regime}", f"case = {setup.name}"]
     lines += [f"{k} = {_fmt(setup.params[k])}" for k in sorted(setup.params)
               if isinstance(setup.params[k], (int, float, str))]
     lines += ["", "--- config echo ---", echo_config(cfg)]
@@ -363,9 +372,9 @@ def _execute(cfg: RunConfig):
     rows, step = [], [-1]
     apply = setup.apply_load
 
-    def counted(problem, state, t):
+    def counted(*args):  # (problem, state, t) structured, (ops, t) element-list
         step[0] += 1
-        apply(problem, state, t)
+        return apply(*args)
 
     setup.apply_load = counted
     scfg.log_callback = lambda rec: rows.append({"step": step[0], **rec})

@@ -219,6 +219,23 @@ class UnstructuredOperators:
         self._check(_lib.load().pf_umesh_set_dirichlet(self._h, d.ctypes.data if d.size else None, d.size,
                                                         self._stream()))
 
+    def set_eps0(self, eps0) -> None:
+        """Inelastic strain per element (T x 3 Voigt in 2D, T x 6 in 3D; fem.py eps0, cases.py
+        thermal_strain) as a host array or device tensor, or None: every strain of u becomes
+        B u - eps0 (energies, residuals, the damage Hessian's coupling).  Kept on the device."""
+        import torch
+        if eps0 is None:
+            self._eps0 = None
+            self._check(_lib.load().pf_umesh_set_eps0(self._h, None, self._stream()))
+            return
+        nv = 3 if self.mesh.dim == 2 else 6
+        t = torch.as_tensor(np.asarray(eps0, dtype=np.float64) if not torch.is_tensor(eps0) else eps0,
+                            dtype=torch.float64, device=self.device).reshape(-1).contiguous()
+        if t.numel() != nv * self.mesh.n_elements:
+            raise ValueError(f"eps0 needs {nv} Voigt components per element")
+        self._eps0 = t  # the library keeps the pointer: keep the tensor alive
+        self._check(_lib.load().pf_umesh_set_eps0(self._h, _lib.ptr(t), self._stream()))
+
     def apply_Kuu(self, alpha, x, out=None, apply_bc: bool = False):
         import torch
         out = torch.empty_like(x) if out is None else out
@@ -292,7 +309,7 @@ class UnstructuredOperators:
     def am_load_step(self, u, alpha, alpha_lb, bc_dofs, bc_values, omega: float = 1.0,
                      outer_atol: float = 1e-7, max_am_iterations: int = 1000,
                      elastic_rtol: float = 1e-10, damage_atol_factor: float = 0.1,
-                     max_vi_iterations: int = 200):
+                     max_vi_iterations: int = 200, log_callback=None):
         """One load step of alternate minimisation on the element-list mesh (am_loop with an
         absolute target, solver.py:129-241; oracle/am.py am_loop): elastic half-step (device PCG on
         the Dirichlet-lifted Kuu), over-relaxed update u0 + omega (u* - u0), damage half-step
@@ -327,7 +344,10 @@ class UnstructuredOperators:
         # at least one AM iteration, as the reference loop (solver.py:186-241; oracle am_loop)
         while stats["am_iterations"] < max_am_iterations:
             stats["am_iterations"] += 1
-            b = -self.apply_Kuu(alpha, g)
+            # lifted right-hand side -r_u(g) = f - K g (f: the inelastic-strain load,
+            # assemble_load_u fem.py:192-199), Dirichlet rows = the prescribed values
+            _, b, _ = self.physics(g, alpha)
+            b.neg_()
             b[dofs] = vals
             us, lrep = self.elastic_solve(alpha, b, rtol=elastic_rtol)
             stats["krylov_iterations"] += lrep.iterations
@@ -355,6 +375,9 @@ class UnstructuredOperators:
             res, en = residual()
             stats["residual_history"].append(res)
             stats["energy_history"].append(en)
+            if log_callback is not None:  # the AM log record of solver.py:226-233
+                log_callback({"phase": "am", "cycle": 0, "iteration": stats["am_iterations"], "residual": res,
+                              "omega_bar": wb, "elastic": en[0], "dissipated": en[1], "total": en[2]})
             stats["converged"] = res <= outer_atol
             if stats["converged"]:
                 break

@@ -72,8 +72,10 @@ def test_sweep_grammar():
 def test_no_device_form_is_a_config_error():
     with pytest.raises(runio.ConfigError):
         runio.build_solver_config(runio.parse_config("[linear]\nelastic = cg\nelastic_precond = ssor\n"))
+    # thermal_shock runs on the element-list path (alternate minimisation only): Newton methods
+    # are a configuration error before any device work
     with pytest.raises(runio.ConfigError):
-        runio.build_setup(runio.parse_config("[case]\nname = thermal_shock\n"))
+        runio.build_setup(runio.parse_config("[case]\nname = thermal_shock\n[solver]\nmethod = oram_n\n"))
     s = runio.build_solver_config(runio.parse_config("[solver]\nmethod = oram_n\nomega = 1.3\n"))
     assert (s.method, s.omega) == ("oram_newton", 1.3)
 

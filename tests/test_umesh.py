@@ -393,3 +393,47 @@ def test_gpu_umesh_damage_steepest_descent_fallback(seed):
     assert np.max(np.abs(ad.cpu().numpy() - xo)) < 1e-10
     h = rep.residual_history
     assert all(h[k + 1] <= h[k] for k in range(len(h) - 1))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dim,model", [(2, "AT1"), (2, "AT2"), (3, "AT1")])
+def test_gpu_umesh_eps0_physics_vs_oracle(dim, model):
+    """Inelastic strain on the element-list path (pf_umesh_set_eps0; fem.py eps0, oracle/p1.py
+    strain = B u - eps0): energies, raw residuals and the damage Hessian's elastic coupling against
+    the oracle at 1e-12; the Kuu apply ignores eps0."""
+    import torch
+    import paper_1511_08463_b200 as pf
+    regime = "plane_stress" if dim == 2 else "3d"
+    om_mesh = (jitter_interior(grid_mesh(20, 10, 2.0, 1.0), 0.25, 5) if dim == 2
+               else jitter_interior(kuhn_mesh(5, 4, 6), 0.1, 5))
+    spec = MaterialSpec(E=1.0, nu=0.3, Gc=1.0, ell=0.2, k_ell=1e-6, model=model, regime=regime)
+    om = P1Model(om_mesh, spec)
+    rng = np.random.default_rng(17 + dim)
+    V, T, nv = om_mesh.n_vertices, om_mesh.n_elements, (3 if dim == 2 else 6)
+    om.eps0 = 0.05 * rng.standard_normal((T, nv))
+    u = 0.1 * rng.standard_normal(dim * V)
+    a = rng.uniform(0, 0.9, V)
+    x = rng.standard_normal(V)
+    ops = pf.UnstructuredOperators(pf.UnstructuredMesh(om_mesh.vertices, om_mesh.elements),
+                                   pf.Material(E=1.0, nu=0.3, Gc=1.0, ell=0.2, k_ell=1e-6, regime=regime), model)
+    ops.set_eps0(om.eps0)
+    en, ru, ra = ops.physics(_dev(u), _dev(a))
+    eo = om.energy(u, a)
+    assert abs(en[0] - eo.elastic) <= 1e-12 * abs(eo.elastic)
+    assert abs(en[1] - eo.dissipated) <= 1e-12 * abs(eo.dissipated)
+    rr = om.residual_u(u, a, bc_rows="none")
+    assert np.max(np.abs(ru.cpu().numpy() - rr)) <= 1e-12 * np.max(np.abs(rr))
+    rra = om.residual_alpha(u, a)
+    assert np.max(np.abs(ra.cpu().numpy() - rra)) <= 1e-12 * np.max(np.abs(rra))
+    ya = ops.apply_Kaa(_dev(u), _dev(a), _dev(x)).cpu().numpy()
+    yo = om.Kaa(u, a) @ x
+    assert np.max(np.abs(ya - yo)) <= 1e-12 * np.max(np.abs(yo))
+    xu = rng.standard_normal(dim * V)
+    yu = ops.apply_Kuu(_dev(a), _dev(xu)).cpu().numpy()
+    yuo = om.Kuu(a, eliminate=False) @ xu
+    assert np.max(np.abs(yu - yuo)) <= 1e-12 * np.max(np.abs(yuo))
+    ops.set_eps0(None)
+    en0, _, _ = ops.physics(_dev(u), _dev(a), want_residuals=False)
+    om.eps0 = np.zeros((T, nv))
+    assert abs(en0[0] - om.energy(u, a).elastic) <= 1e-12 * abs(en0[0])
+    del torch

@@ -30,12 +30,18 @@ ap.add_argument("--save", default="")
 ap.add_argument("--out", default="gpurun_out/sent_window.json")
 ap.add_argument("--no-split", action="store_true")
 ap.add_argument("--cheb-deg", type=int, default=0, help="override fieldsplit_cheb_degree")
+ap.add_argument("--workload", default="sent", choices=["sent", "traction3d"])
 args = ap.parse_args()
 save = {int(s) for s in args.save.split(",") if s}
 os.makedirs("gpurun_out", exist_ok=True)
 
-setup = pf.setup_sent(n=args.n)
-cfg = bench.sent_config(pf)
+if args.workload == "sent":
+    setup = pf.setup_sent(n=args.n)
+    cfg = bench.sent_config(pf)
+else:
+    setup = pf.setup_traction3d(n=args.n)
+    cfg = bench.traction3d_config(pf)
+args.steps = min(args.steps, len(setup.schedule))
 if args.cheb_deg:
     cfg.fieldsplit_cheb_degree = args.cheb_deg
 flush = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device="cuda")
@@ -65,7 +71,7 @@ def plain_pass():
               f"E=({r.energy.elastic:.6e},{r.energy.dissipated:.6e}) amax={rows[-1]['amax']:.3f}",
               flush=True)
         if k in save:
-            np.savez(f"gpurun_out/sent{args.n}_state{k}.npz", u=st.u.cpu().numpy(),
+            np.savez(f"gpurun_out/{args.workload}{args.n}_state{k}.npz", u=st.u.cpu().numpy(),
                      alpha=st.alpha.cpu().numpy(), alpha_lb=st.alpha_lb.cpu().numpy(), load=r.load,
                      E=np.array(rows[-1]["E"]), am=rep.am_iterations)
     return rows
@@ -112,7 +118,7 @@ def split_pass(rows):
 rows = plain_pass()
 if not args.no_split:
     split_pass(rows)
-win = [r["ms"] for r in rows[5:25]]
+win = [r["ms"] for r in rows[5:25]] if args.workload == "sent" else [r["ms"] for r in rows[5:]]
 summary = {"n": args.n, "steps": args.steps, "rows": rows,
            "driver_window_5_24_s_per_step": (sum(win) / len(win) / 1e3) if win else None,
            "all_steps_s_per_step": sum(r["ms"] for r in rows) / len(rows) / 1e3}

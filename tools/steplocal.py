@@ -32,6 +32,8 @@ ap.add_argument("--n", type=int, default=512)
 ap.add_argument("--atol", type=float, default=1e-9)
 ap.add_argument("--literal", action="store_true", help="config-literal tolerances instead")
 ap.add_argument("--outdir", default="gpurun_out/steplocal")
+ap.add_argument("--oracle-cg", action="store_true",
+                help="oracle elastic half-steps by Jacobi-PCG at rtol 1e-13 instead of SuperLU (3D sizes)")
 args = ap.parse_args()
 d = args.outdir
 os.makedirs(d, exist_ok=True)
@@ -80,6 +82,8 @@ def run_oracle():
         s = opb.traction3d(n=args.n)
         cfg = oam.AMConfig(method="oram_newton", omega=1.7, outer_atol=1e-6 if args.literal else args.atol,
                            max_am_iterations=3000)
+    if args.oracle_cg:
+        cfg.elastic_solver, cfg.elastic_precond, cfg.elastic_rtol = "cg", "jacobi", 1e-13
     hist = []
 
     def log(e):
