@@ -566,6 +566,7 @@ template <int EPI, bool ISO>
 struct Op3KuuSm : Op3Kuu<false, ISO> {
     using Base = Op3Kuu<false, ISO>;
     static constexpr int SV = EPI == E3_CHEB_B ? 7 : 4;
+
     const double* b;
     const double* dinv;
     double* res;
@@ -1252,7 +1253,18 @@ static int run3_sm(Ctx* c, const Geo3& g, const Sm3Args& a, cudaStream_t st, int
                           a.b, a.dinv, a.res, a.dnext, a.xs, a.live, a.lam, a.ratio, a.k, a.pending,
                           0.0, 0.0, 0.0};
     const double vec = EPI == E3_RESID ? 48.0 : (EPI == E3_RESID_CHEB0 ? 96.0 : (EPI == E3_CHEB ? 144.0 : 144.0));
-    return run3g(c, g, op, st, kind, (EPI == E3_CHEB_B ? 56.0 + 24.0 : 56.0 - 24.0) * g.nv + vec * g.nv);
+    const double bytes = (EPI == E3_CHEB_B ? 56.0 + 24.0 : 56.0 - 24.0) * g.nv + vec * g.nv;
+    // the first step from zero stages 7 vertex slots and spills 76 B at 128 registers (two 8-warp
+    // blocks per SM); PF_K3SM_MINB1=1 runs it one block per SM with 255 registers instead (A/B)
+    if constexpr (EPI == E3_CHEB_B) {
+        static const bool one = getenv("PF_K3SM_MINB1") != nullptr;
+        if (one) {
+            Tiled3<Op3KuuSm<EPI, ISO>, 8, 1> t;
+            static_cast<Op3KuuSm<EPI, ISO>&>(t) = op;
+            return run3g(c, g, t, st, kind, bytes);
+        }
+    }
+    return run3g(c, g, op, st, kind, bytes);
 }
 int launch3_Kuu_sm(Ctx* c, const Geo3& g, int epi, const Sm3Args& a, cudaStream_t st, int kind) {
     const bool iso = iso3(g);

@@ -22,6 +22,7 @@
 //    (x, y, alpha, (u), element records, connectivity, CSR).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -48,6 +49,8 @@ struct pf_umesh {
     double *r = nullptr, *z = nullptr, *p = nullptr, *q = nullptr, *dinv = nullptr, *part = nullptr,
            *scal = nullptr;
     const double* eps0 = nullptr;  // caller-owned inelastic strain per element (T x 3 / T x 6), or null
+    unsigned* bar = nullptr;       // software grid barrier of the persistent PCG
+    int pcg_blocks[4] = {0, 0, 0, 0};  // resident-block capacity per persistent-PCG variant
     bool bound = false, has_bc = false;
     int64_t launches = 0;
 };
@@ -132,17 +135,12 @@ __device__ __forceinline__ void block_partial(double v, double* __restrict__ par
     __syncthreads();  // sh is reused by the next call in the same kernel
 }
 
-template <bool DOT>
-__global__ void __launch_bounds__(256) k_umesh_Kuu2(
-    const double* __restrict__ rec, const int4* __restrict__ conn, const int32_t* __restrict__ rowptr,
-    const int32_t* __restrict__ adj, const uint8_t* __restrict__ vmask, const double* __restrict__ alpha,
-    const double2* __restrict__ x, double2* __restrict__ y, int64_t nv, UParams p,
-    double* __restrict__ part) {
-    // no early exit: every lane reaches the block reduction's full-mask shuffles (a lane past nv
-    // recomputes the last vertex and writes nothing)
-    const int64_t v0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const bool live = v0 < nv;
-    const int64_t v = live ? v0 : nv - 1;
+// one row (vertex v) of the (Dirichlet-eliminated when vmask) Kuu apply: gather over the incident
+// elements (fem.py:233-244); Dirichlet rows return x (identity)
+__device__ __forceinline__ double2 kuu2_row(const double* __restrict__ rec, const int4* __restrict__ conn,
+                                           const int32_t* __restrict__ rowptr, const int32_t* __restrict__ adj,
+                                           const uint8_t* __restrict__ vmask, const double* __restrict__ alpha,
+                                           const double2* __restrict__ x, int64_t v, const UParams& p) {
     const uint8_t mv = vmask ? vmask[v] : 0;
     double y0 = 0.0, y1 = 0.0;
     const int k0 = rowptr[v], k1 = rowptr[v + 1];
@@ -156,7 +154,7 @@ __global__ void __launch_bounds__(256) k_umesh_Kuu2(
         double ab = 0.0;
 #pragma unroll
         for (int j = 0; j < 3; ++j) {
-            xe[j] = __ldg(x + vs[j]);
+            xe[j] = __ldcg(x + vs[j]);
             ab += __ldg(alpha + vs[j]);
             if (vmask) {
                 const uint8_t mj = __ldg(vmask + vs[j]);
@@ -178,14 +176,29 @@ __global__ void __launch_bounds__(256) k_umesh_Kuu2(
         y1 += gyi * s1 + gxi * s2;
     }
     if (mv) {
-        const double2 xv = x[v];
+        const double2 xv = __ldcg(x + v);
         if (mv & 1) y0 = xv.x;
         if (mv & 2) y1 = xv.y;
     }
-    if (live) y[v] = make_double2(y0, y1);
+    return make_double2(y0, y1);
+}
+
+template <bool DOT>
+__global__ void __launch_bounds__(256) k_umesh_Kuu2(
+    const double* __restrict__ rec, const int4* __restrict__ conn, const int32_t* __restrict__ rowptr,
+    const int32_t* __restrict__ adj, const uint8_t* __restrict__ vmask, const double* __restrict__ alpha,
+    const double2* __restrict__ x, double2* __restrict__ y, int64_t nv, UParams p,
+    double* __restrict__ part) {
+    // no early exit: every lane reaches the block reduction's full-mask shuffles (a lane past nv
+    // recomputes the last vertex and writes nothing)
+    const int64_t v0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool live = v0 < nv;
+    const int64_t v = live ? v0 : nv - 1;
+    const double2 yv = kuu2_row(rec, conn, rowptr, adj, vmask, alpha, x, v, p);
+    if (live) y[v] = yv;
     if (DOT) {
         const double2 xv = x[v];
-        block_partial(live ? xv.x * y0 + xv.y * y1 : 0.0, part);
+        block_partial(live ? xv.x * yv.x + xv.y * yv.y : 0.0, part);
     }
 }
 
@@ -207,17 +220,12 @@ __device__ __forceinline__ void kaa_store(bool live, int64_t v, double acc, cons
     }
 }
 
+// one row of the Kaa apply (fem.py:266-282; KAA_DIAG: the diagonal, x unused)
 template <int MODE>
-__global__ void __launch_bounds__(256) k_umesh_Kaa2(
-    const double* __restrict__ rec, const int4* __restrict__ conn, const int32_t* __restrict__ rowptr,
-    const int32_t* __restrict__ adj, const double2* __restrict__ u,
-    const double* __restrict__ x, double* __restrict__ y, int64_t nv, UParams p,
-    const double* __restrict__ dinv = nullptr, double* __restrict__ part = nullptr) {
-    // no early exit: every lane reaches the block reduction's full-mask shuffles (a lane past nv
-    // recomputes the last vertex and writes nothing)
-    const int64_t v0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const bool live = v0 < nv;
-    const int64_t v = live ? v0 : nv - 1;
+__device__ __forceinline__ double kaa2_row(const double* __restrict__ rec, const int4* __restrict__ conn,
+                                          const int32_t* __restrict__ rowptr, const int32_t* __restrict__ adj,
+                                          const double2* __restrict__ u, const double* __restrict__ x, int64_t v,
+                                          const UParams& p) {
     double acc = 0.0;
     const int k0 = rowptr[v], k1 = rowptr[v + 1];
     for (int k = k0; k < k1; ++k) {
@@ -231,7 +239,7 @@ __global__ void __launch_bounds__(256) k_umesh_Kaa2(
 #pragma unroll
         for (int j = 0; j < 3; ++j) {
             ue[j] = __ldg(u + vs[j]);
-            const double xj = MODE == KAA_DIAG ? (j == li ? 1.0 : 0.0) : __ldg(x + vs[j]);
+            const double xj = MODE == KAA_DIAG ? (j == li ? 1.0 : 0.0) : __ldcg(x + vs[j]);
             sx += xj;
             gxa += r.gx[j] * xj;
             gya += r.gy[j] * xj;
@@ -248,6 +256,21 @@ __global__ void __launch_bounds__(256) k_umesh_Kaa2(
         const double gyi = li == 0 ? r.gy[0] : (li == 1 ? r.gy[1] : r.gy[2]);
         acc += react * sx + 2.0 * kc * p.ell * (gxi * gxa + gyi * gya);
     }
+    return acc;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256) k_umesh_Kaa2(
+    const double* __restrict__ rec, const int4* __restrict__ conn, const int32_t* __restrict__ rowptr,
+    const int32_t* __restrict__ adj, const double2* __restrict__ u,
+    const double* __restrict__ x, double* __restrict__ y, int64_t nv, UParams p,
+    const double* __restrict__ dinv = nullptr, double* __restrict__ part = nullptr) {
+    // no early exit: every lane reaches the block reduction's full-mask shuffles (a lane past nv
+    // recomputes the last vertex and writes nothing)
+    const int64_t v0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool live = v0 < nv;
+    const int64_t v = live ? v0 : nv - 1;
+    const double acc = kaa2_row<MODE>(rec, conn, rowptr, adj, u, x, v, p);
     kaa_store<MODE>(live, v, acc, x, y, dinv, part);
 }
 
@@ -303,16 +326,11 @@ __device__ __forceinline__ double pick4(const double (&a)[4], int i) {
     return i == 0 ? a[0] : (i == 1 ? a[1] : (i == 2 ? a[2] : a[3]));
 }
 
-template <bool DOT>
-__global__ void __launch_bounds__(256) k_umesh_Kuu3(
-    const double* __restrict__ rec, const int4* __restrict__ conn, const int32_t* __restrict__ rowptr,
-    const int32_t* __restrict__ adj, const uint8_t* __restrict__ vmask, const double* __restrict__ alpha,
-    const double* __restrict__ x, double* __restrict__ y, int64_t nv, UParams p, double* __restrict__ part) {
-    // no early exit: every lane reaches the block reduction's full-mask shuffles (a lane past nv
-    // recomputes the last vertex and writes nothing)
-    const int64_t v0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const bool live = v0 < nv;
-    const int64_t v = live ? v0 : nv - 1;
+__device__ __forceinline__ void kuu3_row(const double* __restrict__ rec, const int4* __restrict__ conn,
+                                         const int32_t* __restrict__ rowptr, const int32_t* __restrict__ adj,
+                                         const uint8_t* __restrict__ vmask, const double* __restrict__ alpha,
+                                         const double* __restrict__ x, int64_t v, const UParams& p,
+                                         double (&y)[3]) {
     double y0 = 0.0, y1 = 0.0, y2 = 0.0;
     const int k0 = rowptr[v], k1 = rowptr[v + 1];
     for (int k = k0; k < k1; ++k) {
@@ -327,43 +345,52 @@ __global__ void __launch_bounds__(256) k_umesh_Kuu3(
         for (int j = 0; j < 4; ++j) {
             const uint8_t mj = vmask ? __ldg(vmask + vs[j]) : 0;
 #pragma unroll
-            for (int d = 0; d < 3; ++d) xe[j][d] = (mj >> d) & 1 ? 0.0 : __ldg(x + 3 * (int64_t)vs[j] + d);
+            for (int d = 0; d < 3; ++d) xe[j][d] = (mj >> d) & 1 ? 0.0 : __ldcg(x + 3 * (int64_t)vs[j] + d);
             ab += __ldg(alpha + vs[j]);
         }
         ab *= 0.25;
         const double om = 1.0 - ab;
         const double w = (om * om + p.k_ell) * r.volE;
-        double eps[6], s[6];
+        double eps[6], st[6];
         strain3(r, xe, eps);
-        stress3(p, eps, s);
+        stress3(p, eps, st);
         const double gx = pick4(r.g[0], li), gy = pick4(r.g[1], li), gz = pick4(r.g[2], li);
-        y0 += w * (gx * s[0] + gz * s[4] + gy * s[5]);
-        y1 += w * (gy * s[1] + gz * s[3] + gx * s[5]);
-        y2 += w * (gz * s[2] + gy * s[3] + gx * s[4]);
+        y0 += w * (gx * st[0] + gz * st[4] + gy * st[5]);
+        y1 += w * (gy * st[1] + gz * st[3] + gx * st[5]);
+        y2 += w * (gz * st[2] + gy * st[3] + gx * st[4]);
     }
     const uint8_t mv = vmask ? vmask[v] : 0;
-    if (mv & 1) y0 = x[3 * v];
-    if (mv & 2) y1 = x[3 * v + 1];
-    if (mv & 4) y2 = x[3 * v + 2];
-    if (live) {
-        y[3 * v] = y0;
-        y[3 * v + 1] = y1;
-        y[3 * v + 2] = y2;
-    }
-    if (DOT) block_partial(live ? x[3 * v] * y0 + x[3 * v + 1] * y1 + x[3 * v + 2] * y2 : 0.0, part);
+    if (mv & 1) y0 = __ldcg(x + 3 * v);
+    if (mv & 2) y1 = __ldcg(x + 3 * v + 1);
+    if (mv & 4) y2 = __ldcg(x + 3 * v + 2);
+    y[0] = y0; y[1] = y1; y[2] = y2;
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(256) k_umesh_Kaa3(
+template <bool DOT>
+__global__ void __launch_bounds__(256) k_umesh_Kuu3(
     const double* __restrict__ rec, const int4* __restrict__ conn, const int32_t* __restrict__ rowptr,
-    const int32_t* __restrict__ adj, const double* __restrict__ u,
-    const double* __restrict__ x, double* __restrict__ y, int64_t nv, UParams p,
-    const double* __restrict__ dinv = nullptr, double* __restrict__ part = nullptr) {
+    const int32_t* __restrict__ adj, const uint8_t* __restrict__ vmask, const double* __restrict__ alpha,
+    const double* __restrict__ x, double* __restrict__ y, int64_t nv, UParams p, double* __restrict__ part) {
     // no early exit: every lane reaches the block reduction's full-mask shuffles (a lane past nv
     // recomputes the last vertex and writes nothing)
     const int64_t v0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const bool live = v0 < nv;
     const int64_t v = live ? v0 : nv - 1;
+    double yv[3];
+    kuu3_row(rec, conn, rowptr, adj, vmask, alpha, x, v, p, yv);
+    if (live) {
+        y[3 * v] = yv[0];
+        y[3 * v + 1] = yv[1];
+        y[3 * v + 2] = yv[2];
+    }
+    if (DOT) block_partial(live ? x[3 * v] * yv[0] + x[3 * v + 1] * yv[1] + x[3 * v + 2] * yv[2] : 0.0, part);
+}
+
+template <int MODE>
+__device__ __forceinline__ double kaa3_row(const double* __restrict__ rec, const int4* __restrict__ conn,
+                                          const int32_t* __restrict__ rowptr, const int32_t* __restrict__ adj,
+                                          const double* __restrict__ u, const double* __restrict__ x, int64_t v,
+                                          const UParams& p) {
     double acc = 0.0;
     const int k0 = rowptr[v], k1 = rowptr[v + 1];
     for (int k = k0; k < k1; ++k) {
@@ -378,24 +405,39 @@ __global__ void __launch_bounds__(256) k_umesh_Kaa3(
         for (int j = 0; j < 4; ++j) {
 #pragma unroll
             for (int d = 0; d < 3; ++d) ue[j][d] = __ldg(u + 3 * (int64_t)vs[j] + d);
-            const double xj = MODE == KAA_DIAG ? (j == li ? 1.0 : 0.0) : __ldg(x + vs[j]);
+            const double xj = MODE == KAA_DIAG ? (j == li ? 1.0 : 0.0) : __ldcg(x + vs[j]);
             sx += xj;
 #pragma unroll
             for (int d = 0; d < 3; ++d) ga[d] += r.g[d][j] * xj;
         }
-        double eps[6], s[6];
+        double eps[6], st[6];
         strain3(r, ue, eps);
         sub_eps0<6>(p, e, eps);
-        stress3(p, eps, s);
+        stress3(p, eps, st);
         double q = 0.0;
 #pragma unroll
-        for (int i = 0; i < 6; ++i) q += eps[i] * s[i];
+        for (int i = 0; i < 6; ++i) q += eps[i] * st[i];
         const double wpp = p.at2 ? 2.0 : 0.0;
         const double kc = r.volGc * p.inv_cw;
         const double react = (q * r.volE + kc * wpp * p.inv_ell) * (1.0 / 16.0);
         const double gi0 = pick4(r.g[0], li), gi1 = pick4(r.g[1], li), gi2 = pick4(r.g[2], li);
         acc += react * sx + 2.0 * kc * p.ell * (gi0 * ga[0] + gi1 * ga[1] + gi2 * ga[2]);
     }
+    return acc;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256) k_umesh_Kaa3(
+    const double* __restrict__ rec, const int4* __restrict__ conn, const int32_t* __restrict__ rowptr,
+    const int32_t* __restrict__ adj, const double* __restrict__ u,
+    const double* __restrict__ x, double* __restrict__ y, int64_t nv, UParams p,
+    const double* __restrict__ dinv = nullptr, double* __restrict__ part = nullptr) {
+    // no early exit: every lane reaches the block reduction's full-mask shuffles (a lane past nv
+    // recomputes the last vertex and writes nothing)
+    const int64_t v0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool live = v0 < nv;
+    const int64_t v = live ? v0 : nv - 1;
+    const double acc = kaa3_row<MODE>(rec, conn, rowptr, adj, u, x, v, p);
     kaa_store<MODE>(live, v, acc, x, y, dinv, part);
 }
 
@@ -699,6 +741,147 @@ __global__ void __launch_bounds__(256) k_umesh_vi_cand(
     out[v] = fmin(fmax(c, lb[v]), 1.0);
 }
 
+// ---- persistent Jacobi PCG (whole Krylov loop in one cooperative launch) -------------------------
+// The loop of pf_umesh_elastic_solve / the damage VI's inner solve (cg_solve, linalg.py:106-152)
+// with every iteration inside one launch: per iteration the apply + p.q (one vertex per thread,
+// strided), the x / r / z update + r.z, r.r, and p = z + beta p, separated by a software grid
+// barrier.  Every block sums the per-block partials in the same fixed order, so all blocks take the
+// same decisions (deterministic).  It replaces 5 launches and a host poll every few iterations; the
+// element-list path is launch-bound at the sizes of the reference's thermal-shock case.
+__device__ __forceinline__ void ugrid_sync(unsigned int* bar) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned int inc = blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1) : 1u;
+        __threadfence();
+        const unsigned int old = atomicAdd(bar, inc);
+        unsigned int cur;
+        do {
+            asm volatile("ld.acquire.gpu.u32 %0, [%1];\n" : "=r"(cur) : "l"(bar) : "memory");
+        } while (((old ^ cur) & 0x80000000u) == 0);
+    }
+    __syncthreads();
+}
+// sum of rows [0, nb) of part (and [nb, 2 nb) when two): the same fixed order in every block
+__device__ __forceinline__ double2 ugrid_total(const double* part, int nb, bool two) {
+    __shared__ double2 tot;
+    if (threadIdx.x < 32) {
+        double a = 0.0, b = 0.0;
+        for (int i = threadIdx.x; i < nb; i += 32) {
+            a += __ldcg(part + i);
+            if (two) b += __ldcg(part + nb + i);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            a += __shfl_xor_sync(0xffffffffu, a, o);
+            b += __shfl_xor_sync(0xffffffffu, b, o);
+        }
+        if (threadIdx.x == 0) tot = make_double2(a, b);
+    }
+    __syncthreads();
+    const double2 r = tot;
+    __syncthreads();
+    return r;
+}
+struct UPcg {
+    const double* rec;
+    const int4* conn;
+    const int32_t *rowptr, *adj;
+    const uint8_t* vmask;
+    const double* alpha;  // Kuu
+    const double* u;      // Kaa
+    const double* dinv;   // Jacobi (Kaa: 0 on the active rows, masked out)
+    double *x, *r, *z, *p, *q, *part, *scal;
+    unsigned* bar;
+    int64_t nv;
+    double tol2;
+    int64_t maxit;
+    UParams prm;
+};
+// OP: 0 Kuu 2D, 1 Kuu 3D, 2 masked Kaa 2D, 3 masked Kaa 3D.  Start: scal[0] = r.z, scal[3] = r.r
+// (k_umesh_pcg_init); end: scal[5] = iterations, scal[3] = r.r, scal[4] = breakdown flag.
+template <int OP>
+__global__ void __launch_bounds__(256) k_umesh_pcg_persistent(UPcg a) {
+    constexpr int D = (OP == 0) ? 2 : (OP == 1 ? 3 : 1);  // dofs per vertex
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
+    const int nb = gridDim.x;
+    double rz = a.scal[0], rr = a.scal[3], brk = 0.0;
+    int64_t it = 0;
+    while (rr > a.tol2 && it < a.maxit) {
+        double acc = 0.0;
+        for (int64_t v = tid; v < a.nv; v += nth) {
+            if constexpr (OP == 0) {
+                const double2 y = kuu2_row(a.rec, a.conn, a.rowptr, a.adj, a.vmask, a.alpha,
+                                           reinterpret_cast<const double2*>(a.p), v, a.prm);
+                reinterpret_cast<double2*>(a.q)[v] = y;
+                const double2 pv = reinterpret_cast<const double2*>(a.p)[v];
+                acc += pv.x * y.x + pv.y * y.y;
+            } else if constexpr (OP == 1) {
+                double y[3];
+                kuu3_row(a.rec, a.conn, a.rowptr, a.adj, a.vmask, a.alpha, a.p, v, a.prm, y);
+#pragma unroll
+                for (int d = 0; d < 3; ++d) {
+                    a.q[3 * v + d] = y[d];
+                    acc += a.p[3 * v + d] * y[d];
+                }
+            } else {
+                double y = OP == 2 ? kaa2_row<KAA_APPLY>(a.rec, a.conn, a.rowptr, a.adj,
+                                                         reinterpret_cast<const double2*>(a.u), a.p, v, a.prm)
+                                   : kaa3_row<KAA_APPLY>(a.rec, a.conn, a.rowptr, a.adj, a.u, a.p, v, a.prm);
+                if (a.dinv[v] == 0.0) y = 0.0;  // active row (KAA_PCG)
+                a.q[v] = y;
+                acc += a.p[v] * y;
+            }
+        }
+        block_partial(acc, a.part);
+        ugrid_sync(a.bar);
+        const double pq = ugrid_total(a.part, nb, false).x;
+        if (!(pq > 0.0)) {
+            if (rz != 0.0) brk = 1.0;
+            break;
+        }
+        const double al = rz / pq;
+        double arz = 0.0, arr = 0.0;
+        for (int64_t v = tid; v < a.nv; v += nth) {
+#pragma unroll
+            for (int d = 0; d < D; ++d) {
+                const int64_t i = D * v + d;
+                a.x[i] += al * a.p[i];
+                const double ri = a.r[i] - al * a.q[i], zi = a.dinv[i] * ri;
+                a.r[i] = ri;
+                a.z[i] = zi;
+                arz += ri * zi;
+                arr += ri * ri;
+            }
+        }
+        // r.z / r.r partials in rows [nb, 3 nb): no barrier needed against the readers of the p.q
+        // partials in [0, nb) (the workspace holds >= 2 x the vertex blocks of partials)
+        block_partial(arz, a.part + nb);
+        block_partial(arr, a.part + 2 * nb);
+        ugrid_sync(a.bar);
+        const double2 t = ugrid_total(a.part + nb, nb, true);
+        ++it;
+        rr = t.y;
+        const double rzo = rz;
+        rz = t.x;
+        if (rr <= a.tol2) break;
+        const double be = rzo != 0.0 ? rz / rzo : 0.0;
+        for (int64_t v = tid; v < a.nv; v += nth) {
+#pragma unroll
+            for (int d = 0; d < D; ++d) {
+                const int64_t i = D * v + d;
+                a.p[i] = a.z[i] + be * a.p[i];
+            }
+        }
+        ugrid_sync(a.bar);  // p complete (and the r.z / r.r partials read) before the next apply
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        a.scal[5] = (double)it;
+        a.scal[3] = rr;
+        a.scal[4] = brk;
+        a.scal[0] = rz;
+    }
+}
+
 // Merit-gradient ingredients on the box [lb, 1] (vi.py:144-178, the structured k_merit_parts):
 // pphi = p * phi and w = q * phi; the gradient of |Phi|^2 is 2 (pphi + Kaa w) (Kaa symmetric).
 __device__ __forceinline__ void fb_part_u(double a, double b, double& pa, double& pb) {
@@ -736,6 +919,37 @@ __global__ void __launch_bounds__(256) k_umesh_grad_finish(const double* __restr
         g2 = gv * gv;
     }
     block_partial(g2, part);
+}
+
+
+// launch the persistent PCG of variant OP over the vertices (cooperative: the blocks must be
+// co-resident); returns cudaErrorNotSupported when the variant cannot be made resident
+template <int OP>
+cudaError_t launch_upcg(pf_umesh* m, const UPcg& a, cudaStream_t s) {
+    int& cap = m->pcg_blocks[OP];
+    if (cap == 0) {
+        int dev = 0, nsm = 0, per = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_umesh_pcg_persistent<OP>, 256, 0);
+        if (e != cudaSuccess) return e;
+        cap = std::max(0, nsm * per);
+    }
+    if (cap <= 0) return cudaErrorNotSupported;
+    const int64_t n = (OP <= 1 ? m->dim : 1) * m->nv;
+    const int64_t nbmax = std::max((n + 255) / 256, (m->nt + 255) / 256);
+    // three rows of per-block partials (p.q | r.z | r.r) must fit the 2 * nbmax of the workspace
+    const int grid = (int)std::min<int64_t>(std::min<int64_t>(cap, (a.nv + 255) / 256), (2 * nbmax) / 3);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(std::max(grid, 1));
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k_umesh_pcg_persistent<OP>, a);
 }
 
 int fail(pf_umesh* m, int code, const std::string& msg) {
@@ -867,7 +1081,7 @@ int64_t pf_umesh_workspace_bytes(const pf_umesh* m) {
     const int R = m->dim == 2 ? REC2 : REC3;
     const int64_t n = m->dim * m->nv, nb = std::max((n + 255) / 256, (m->nt + 255) / 256);
     return align256(m->nt * R * 8) + align256(m->nt * 16) + align256((m->nv + 1) * 4)
-         + align256(m->nadj * 4) + align256(m->nv) + 5 * align256(n * 8) + align256(2 * nb * 8) + 256;
+         + align256(m->nadj * 4) + align256(m->nv) + 5 * align256(n * 8) + align256(2 * nb * 8) + 256 + 256;
 }
 
 int pf_umesh_bind_workspace(pf_umesh* m, void* dev, int64_t bytes, void* stream) {
@@ -889,7 +1103,8 @@ int pf_umesh_bind_workspace(pf_umesh* m, void* dev, int64_t bytes, void* stream)
         double** vecs[5] = {&m->r, &m->z, &m->p, &m->q, &m->dinv};
         for (auto v : vecs) { *v = reinterpret_cast<double*>(p); p += align256(n * 8); }
         m->part = reinterpret_cast<double*>(p); p += align256(2 * nb * 8);
-        m->scal = reinterpret_cast<double*>(p);
+        m->scal = reinterpret_cast<double*>(p); p += 256;
+        m->bar = reinterpret_cast<unsigned*>(p);
     }
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     cudaError_t e = cudaMemcpyAsync(m->rec, m->h_rec.data(), m->nt * R * 8, cudaMemcpyHostToDevice, s);
@@ -898,6 +1113,7 @@ int pf_umesh_bind_workspace(pf_umesh* m, void* dev, int64_t bytes, void* stream)
         e = cudaMemcpyAsync(m->rowptr, m->h_rowptr.data(), (m->nv + 1) * 4, cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess) e = cudaMemcpyAsync(m->adj, m->h_adj.data(), m->nadj * 4, cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess) e = cudaMemsetAsync(m->vmask, 0, m->nv, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(m->bar, 0, 256, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) return cuda_fail(m, e);
     std::vector<double>().swap(m->h_rec);
@@ -1010,6 +1226,27 @@ int pf_umesh_elastic_solve(pf_umesh* m, const double* alpha, const double* b, do
     rep->status = PF_OK;
     // the partial arrays of the Kuu apply (one per vertex block) reuse part[0..gv)
     int64_t it = 0;
+    if (!rep->converged && !getenv("PF_UMESH_EAGER")) {  // the whole loop in one persistent launch
+        UPcg a{m->rec, conn, m->rowptr, m->adj, m->vmask, alpha, nullptr, m->dinv, x, m->r, m->z, m->p, m->q,
+               m->part, m->scal, m->bar, m->nv, tol * tol, maxit, p};
+        e = m->dim == 2 ? launch_upcg<0>(m, a, s) : launch_upcg<1>(m, a, s);
+        if (e == cudaSuccess) {
+            m->launches++;
+            double h6[6];
+            if ((e = cudaMemcpyAsync(h6, m->scal, sizeof h6, cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
+                (e = cudaStreamSynchronize(s)) != cudaSuccess)
+                return cuda_fail(m, e);
+            rep->iterations = (int64_t)h6[5];
+            rep->final_residual_norm = std::sqrt(h6[3]);
+            if (h6[4] != 0.0) {
+                rep->status = PF_EBREAKDOWN;
+                return fail(m, PF_EBREAKDOWN, "CG breakdown: p^T A p <= 0 (operator not SPD)");
+            }
+            rep->converged = rep->final_residual_norm <= tol;
+            return PF_OK;
+        }
+        cudaGetLastError();  // not co-resident: the launch-per-kernel loop below
+    }
     while (!rep->converged && it < maxit) {
         const int slot = (int)(it & 1);
         if (m->dim == 2)
@@ -1153,7 +1390,23 @@ int pf_umesh_damage_solve(pf_umesh* m, const double* u, const double* alpha_lb, 
         const double tol = irtol * std::sqrt(h[3]);
         double rn = std::sqrt(h[3]);
         int64_t k = 0;
-        while (rn > tol && k < imaxit) {
+        bool eager = true;
+        if (rn > tol && !getenv("PF_UMESH_EAGER")) {  // the whole inner PCG in one persistent launch
+            UPcg a{m->rec, conn, m->rowptr, m->adj, nullptr, nullptr, u, dinv, d, r, z, pv, q, m->part, m->scal,
+                   m->bar, nv, tol * tol, imaxit, p};
+            e = m->dim == 2 ? launch_upcg<2>(m, a, s) : launch_upcg<3>(m, a, s);
+            if (e == cudaSuccess) {
+                eager = false;
+                m->launches++;
+                if ((e = poll()) != cudaSuccess) return cuda_fail(m, e);
+                k = (int64_t)h[5];
+                rn = std::sqrt(h[3]);
+                if (h[4] != 0.0) rn = tol * 2.0 + 1.0;  // breakdown: counted as a linear failure below
+            } else {
+                cudaGetLastError();
+            }
+        }
+        while (eager && rn > tol && k < imaxit) {
             const int slot = (int)(k & 1);
             if (m->dim == 2)
                 k_umesh_Kaa2<KAA_PCG><<<gv, 256, 0, s>>>(m->rec, conn, m->rowptr, m->adj,

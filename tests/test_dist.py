@@ -63,3 +63,63 @@ def test_replicas_gloo_world2():
     assert tmax >= t0                         # job time is the max over ranks
     assert energies[0] != energies[1]         # independent replicas (different ell)
     assert all(np.isfinite(energies))
+
+
+def _gpu_worker(rank, world, port, out):
+    """One device replica per rank (both ranks share the box's single GPU: replicas never wait on
+    each other's kernels), coordinated over gloo exactly as bench.py coordinates NCCL ranks."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import torch
+
+    import paper_1511_08463_b200 as pf
+    from oracle import am as oam
+    from oracle import problems as opb
+    from oracle.p1 import MaterialSpec
+    torch.cuda.set_device(0)
+    ell = 0.1 + 0.05 * rank  # distinct sweep rows per replica
+    setup = pf.setup_traction(pf.Material(E=1.0, nu=0.0, Gc=1.0, ell=ell, k_ell=1e-6), L=1.0, H=0.2,
+                              nx=20, ny=4, n_steps=4, pattern="union_jack")
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    dist.barrier()
+    e0.record()
+    recs = pf.run_quasistatic(setup, pf.SolverConfig(outer_atol=1e-9), snapshot_stride=0)
+    e1.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) * 1e-3], dtype=torch.float64)
+    tmax = t.clone()
+    dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    # the same row on the CPU oracle: each replica computes its own row correctly
+    os_ = opb.traction(MaterialSpec(E=1.0, nu=0.0, Gc=1.0, ell=ell, k_ell=1e-6), L=1.0, H=0.2, nx=20,
+                       ny=4, n_steps=4, pattern="union_jack")
+    orows, _ = opb.run(os_, oam.AMConfig(outer_atol=1e-9), snapshot_stride=0)
+    rel = max(abs(r.energy.total - o.energy.total) / abs(o.energy.total) for r, o in zip(recs, orows))
+    stats = torch.tensor([rel, float(len(recs)), recs[-1].energy.total], dtype=torch.float64)
+    gathered = [torch.zeros(3, dtype=torch.float64) for _ in range(world)]
+    dist.all_gather(gathered, stats)
+    if rank == 0:
+        out.put((float(tmax), float(t), [g.tolist() for g in gathered]))
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_device_replicas_world2():
+    """The replica mode of bench.py / the INI sweep with the DEVICE path in
+    every rank: each replica's run matches the oracle for its own row, the job time is the max of
+    the ranks' CUDA-event times, and the rows differ."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gpu_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    tmax, t0, g = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert tmax >= t0 > 0.0
+    for rel, n, _ in g:
+        assert n == 4.0 and rel < 1e-6
+    assert g[0][2] != g[1][2]
