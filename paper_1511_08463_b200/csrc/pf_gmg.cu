@@ -593,6 +593,36 @@ __device__ __forceinline__ void v_pre_first(const LevelDev& L, const double* bve
     stv<SH>(d1, v, dn);
     stv<SH>(x, v, make_double2(dd.x + dn.x, dd.y + dn.y));
 }
+// v_pre_first with r0 = D^-1 b precomputed by the restriction into this level (in the d0 buffer):
+// the neighbours' d0 = r0 / theta are formed from the gathered r0 instead of from b and D^-1 (~40%
+// fewer loads per vertex) -- the same arithmetic, so the same bits.  d0 is not written (neighbours
+// still read r0 there); the pre-smoother continues from d1 (deg >= 2) or x (deg 1).
+template <bool SH = false, int G = 1>
+__device__ __forceinline__ void v_pre_first_d0(const LevelDev& L, double* res, const double* rb, double* d1,
+                                               double* x, const Cheb& c, double a, double b, int deg, long long v,
+                                               int q = 0) {
+    const double it = c.itheta;
+    if (deg <= 1) {
+        if (G > 1 && q != 0) return;
+        const double2 r0 = ldv<SH>(rb, v);
+        stv<SH>(res, v, r0);
+        stv<SH>(x, v, make_double2(r0.x * it, r0.y * it));
+        return;
+    }
+    const double2 w = st_apply_f<SH, G>(L, v, [&](long long u) {
+        const double2 rq = ldv<SH>(rb, u);
+        return make_double2(rq.x * it, rq.y * it);
+    }, q);
+    if (G > 1 && q != 0) return;
+    const double2 r0 = ldv<SH>(rb, v);
+    const double2 dd = make_double2(r0.x * it, r0.y * it);
+    const double2 dw = bmulT<SH>(L.Dinv, L.nv, v, w.x, w.y);
+    const double2 r = make_double2(r0.x - dw.x, r0.y - dw.y);
+    const double2 dn = make_double2(a * dd.x + b * r.x, a * dd.y + b * r.y);
+    stv<SH>(res, v, r);
+    stv<SH>(d1, v, dn);
+    stv<SH>(x, v, make_double2(dd.x + dn.x, dd.y + dn.y));
+}
 __global__ void k_pre_first(LevelDev L, const double* bvec, double* res, double* d0, double* d1, double* x, int deg,
                             const double* lam, double ratio, const double* live) {
     if (!gmg_live(live)) return;
@@ -666,7 +696,7 @@ __device__ __forceinline__ double w1d(int f, int nf, int C) {
 // G > 1: G lanes share the coarse vertex (fine points t = q, q + G, ...), lane 0 stores.
 template <bool SH = false, int G = 1, class FV>
 __device__ __forceinline__ void v_restrict_f(const LevelDev& F, const LevelDev& Cd, const unsigned char* maskc,
-                                             FV fv, double* bc, long long v, int q = 0) {
+                                             FV fv, double* bc, long long v, int q = 0, double* d0c = nullptr) {
     const int nvyf = F.ny + 1, nvyc = Cd.ny + 1;
     const int vi = (int)v;
     const int I = vi / nvyc, J = vi - (vi / nvyc) * nvyc;
@@ -687,12 +717,17 @@ __device__ __forceinline__ void v_restrict_f(const LevelDev& F, const LevelDev& 
     s1 = gsum<G>(s1);
     if (G > 1 && q != 0) return;
     const unsigned mC = maskc[v];
-    stv<SH>(bc, v, make_double2((mC & 1u) ? 0.0 : s0, (mC & 2u) ? 0.0 : s1));
+    const double2 bv = make_double2((mC & 1u) ? 0.0 : s0, (mC & 2u) ? 0.0 : s1);
+    stv<SH>(bc, v, bv);
+    if (d0c) {  // r0 = D^-1 b of the coarse pre-smoother, once per vertex (v_pre_first_d0)
+        stv<SH>(d0c, v, bmulT<SH>(Cd.Dinv, Cd.nv, v, bv.x, bv.y));
+    }
 }
 template <bool SH = false, int G = 1>
 __device__ __forceinline__ void v_restrict(const LevelDev& F, const LevelDev& Cd, const unsigned char* maskc,
-                                           const double* r, double* bc, long long v, int q = 0) {
-    v_restrict_f<SH, G>(F, Cd, maskc, [&](long long f) { return ldv<SH>(r, f); }, bc, v, q);
+                                           const double* r, double* bc, long long v, int q = 0,
+                                           double* d0c = nullptr) {
+    v_restrict_f<SH, G>(F, Cd, maskc, [&](long long f) { return ldv<SH>(r, f); }, bc, v, q, d0c);
 }
 __global__ void k_restrict(LevelDev F, LevelDev Cd, const unsigned char* maskc, const double* r, double* bc,
                            const double* live) {
@@ -996,9 +1031,9 @@ __device__ __forceinline__ void coarse_body(const CoarseArgs& A, const CCoef* co
                     }
                 return make_double2(s0, s1);
             };
-            grid_each(C.L.nv, [&](auto g, long long v, int q) { v_restrict_f<false, decltype(g)::value>(A.L0, C.L, C.L.mask, collapse, C.b, v, q); });
+            grid_each(C.L.nv, [&](auto g, long long v, int q) { v_restrict_f<false, decltype(g)::value>(A.L0, C.L, C.L.mask, collapse, C.b, v, q, C.d0); });
         } else {
-            grid_each(C.L.nv, [&](auto g, long long v, int q) { v_restrict<false, decltype(g)::value>(A.L0, C.L, C.L.mask, A.r0, C.b, v, q); });
+            grid_each(C.L.nv, [&](auto g, long long v, int q) { v_restrict<false, decltype(g)::value>(A.L0, C.L, C.L.mask, A.r0, C.b, v, q, C.d0); });
         }
         sync();
         TR();
@@ -1011,7 +1046,7 @@ __device__ __forceinline__ void coarse_body(const CoarseArgs& A, const CCoef* co
         const Cheb c = coef[l].c;
         double a = 0.0, b = 0.0;
         if (deg > 1) { a = coef[l].a[1]; b = coef[l].b[1]; }
-        grid_each(V.L.nv, [&](auto g, long long v, int q) { v_pre_first<false, decltype(g)::value>(V.L, V.b, V.res, V.d0, V.d1, V.x, c, a, b, deg, v, q); });
+        grid_each(V.L.nv, [&](auto g, long long v, int q) { v_pre_first_d0<false, decltype(g)::value>(V.L, V.res, V.d0, V.d1, V.x, c, a, b, deg, v, q); });
         sync();
         TR();
         double* d = V.d0;
@@ -1028,7 +1063,8 @@ __device__ __forceinline__ void coarse_body(const CoarseArgs& A, const CCoef* co
         sync();
         TR();
         const CLev& C = A.lev[l + 1];
-        grid_each(C.L.nv, [&](auto g, long long v, int q) { v_restrict<false, decltype(g)::value>(V.L, C.L, C.L.mask, V.r, C.b, v, q); });
+        double* r0c = l + 1 < A.nl - 1 ? C.d0 : nullptr;  // the coarsest level has no pre-smoother
+        grid_each(C.L.nv, [&](auto g, long long v, int q) { v_restrict<false, decltype(g)::value>(V.L, C.L, C.L.mask, V.r, C.b, v, q, r0c); });
         sync();
         TR();
     }
