@@ -16,6 +16,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <ctime>
 
 #include "pf_internal.cuh"
 
@@ -795,9 +796,21 @@ int newton_solve(Ctx* c, const double* u_in, const double* a_in, const double* l
         }
         return PF_OK;
     };
+    static const bool tmg = getenv("PF_NEWTON_TIMING") != nullptr;  // (diagnostic: synchronised phases)
+    double tmark = 0.0;
+    auto tick = [&](const char* what) {
+        if (!tmg) return;
+        cudaStreamSynchronize(st);
+        timespec ts;
+        clock_gettime(CLOCK_MONOTONIC, &ts);
+        const double now = ts.tv_sec + 1e-9 * ts.tv_nsec;
+        if (what) fprintf(stderr, "  newton %-8s %8.3f ms\n", what, 1e3 * (now - tmark));
+        tmark = now;
+    };
     for (int it = 1; it <= o->max_iterations; ++it) {
         if (std::sqrt(merit) <= o->abs_tol) break;
         rep->iterations = it;
+        tick(nullptr);
         const double* u = w.X;
         const double* alpha = w.X + nu;
         // active set on the damage rows; u rows are always inactive (free bounds)
@@ -823,6 +836,7 @@ int newton_solve(Ctx* c, const double* u_in, const double* a_in, const double* l
             c->gmg_built = 1;  // an elastic solve that follows may keep it (gmg_reuse)
             c->gmg_its0 = -1;
         }
+        tick("setup");
         NTRY(launch_kappa(c, u, alpha, c->kappa, c->vi_c, st));
         NTRY(launch_Kaa_diag(c, c->kappa, c->da_dinv, c->act, st));
         InnerMg mg;
@@ -844,6 +858,7 @@ int newton_solve(Ctx* c, const double* u_in, const double* a_in, const double* l
                 c->launches++;
             }
         }
+        tick("kappa+C");
         bool ok = false;
         long long kits = 0;
         bool lin_ok = false;
@@ -864,6 +879,7 @@ int newton_solve(Ctx* c, const double* u_in, const double* a_in, const double* l
             rc = run_minres();
         }
         rep->total_krylov_iterations += kits;
+        tick("minres");
         if (rc == PF_OK && lin_ok && mg.dev) {  // the next iteration's MINRES starts from it
             NCU(c, cudaMemcpyAsync(w.DP, w.D, sizeof(double) * n, cudaMemcpyDeviceToDevice, st), "copy");
             w.dp_valid = true;
@@ -895,6 +911,7 @@ int newton_solve(Ctx* c, const double* u_in, const double* a_in, const double* l
                 rep->steepest_descent_steps++;
             }
         }
+        tick("search");
         if (!ok) break;
         push_hist(merit);
     }

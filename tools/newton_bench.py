@@ -24,11 +24,16 @@ ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--state", default="steplocal_in/sent512_state17.npz")
 ap.add_argument("--step", type=int, default=18)
 ap.add_argument("--only", default="")
+ap.add_argument("--workload", default="sent", choices=["sent", "traction3d"])
+ap.add_argument("--n", type=int, default=512)
 args = ap.parse_args()
 os.environ["PF_NEWTON_NO_KEEP"] = "1"
 s0 = np.load(args.state)
-setup = pf.setup_sent(n=512)
-cfg = bench.sent_config(pf)
+if args.workload == "sent":
+    setup, mkcfg = pf.setup_sent(n=args.n), bench.sent_config
+else:
+    setup, mkcfg = pf.setup_traction3d(n=args.n), bench.traction3d_config
+cfg = mkcfg(pf)
 st = pf.State.from_numpy(s0["u"], s0["alpha"], s0["alpha_lb"])
 t = float(setup.schedule[args.step])
 st.load = t
@@ -36,6 +41,8 @@ st.alpha_lb = st.alpha.clone()
 setup.apply_load(setup.problem, st, t)
 st.u[setup.problem._bc_dofs_dev] = setup.problem._bc_vals_dev
 rep = S.am_solve(st, setup.problem, cfg, rtol=cfg.am_rtol, cycle=0)
+if os.environ.get("PF_NEWTON_TRACE"):
+    pass
 print(f"AM to hand-off: {rep.am_iterations} its, residual {rep.final_residual_norm:.3e}", flush=True)
 VARIANTS = {
     "default": {},
@@ -43,11 +50,15 @@ VARIANTS = {
     "cold_minres": {"PF_MINRES_COLD": "1"},
     "host_minres": {"PF_NEWTON_HOST_MINRES": "1"},
     "cheb_deg12": {"__deg": 12},
+    "cheb_deg3": {"__deg": 3},
+    "cheb_deg4": {"__deg": 4},
+    "cheb_deg8": {"__deg": 8},
+    "multiplicative": {"__mult": 1},
 }
 for name, env in VARIANTS.items():
     if args.only and name not in args.only.split(","):
         continue
-    c = bench.sent_config(pf)
+    c = mkcfg(pf)
     for k, v in env.items():
         if k == "__deg":
             c.fieldsplit_cheb_degree = v

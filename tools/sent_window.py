@@ -31,6 +31,7 @@ ap.add_argument("--out", default="gpurun_out/sent_window.json")
 ap.add_argument("--no-split", action="store_true")
 ap.add_argument("--cheb-deg", type=int, default=0, help="override fieldsplit_cheb_degree")
 ap.add_argument("--workload", default="sent", choices=["sent", "traction3d"])
+ap.add_argument("--save-dir", default="gpurun_out")
 args = ap.parse_args()
 save = {int(s) for s in args.save.split(",") if s}
 os.makedirs("gpurun_out", exist_ok=True)
@@ -71,7 +72,7 @@ def plain_pass():
               f"E=({r.energy.elastic:.6e},{r.energy.dissipated:.6e}) amax={rows[-1]['amax']:.3f}",
               flush=True)
         if k in save:
-            np.savez(f"gpurun_out/{args.workload}{args.n}_state{k}.npz", u=st.u.cpu().numpy(),
+            np.savez(f"{args.save_dir}/{args.workload}{args.n}_state{k}.npz", u=st.u.cpu().numpy(),
                      alpha=st.alpha.cpu().numpy(), alpha_lb=st.alpha_lb.cpu().numpy(), load=r.load,
                      E=np.array(rows[-1]["E"]), am=rep.am_iterations)
     return rows
