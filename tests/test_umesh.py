@@ -104,7 +104,7 @@ def test_capi_create_validates_without_device():
     n = 2 * nv
     nb = max((n + 255) // 256, (nt + 255) // 256)
     expect = sum((b + 255) // 256 * 256 for b in (nt * 64, nt * 16, (nv + 1) * 4, adj * 4, nv,
-                                                  n * 8, n * 8, n * 8, n * 8, n * 8, 2 * nb * 8)) + 256
+                                                  n * 8, n * 8, n * 8, n * 8, n * 8, 2 * nb * 8)) + 256 + 256  # scalars + grid barrier
     assert lib.pf_umesh_workspace_bytes(h) == expect
     lib.pf_umesh_destroy(h)
     # an inverted triangle, an out-of-range index, a regime/dim mismatch
