@@ -116,7 +116,9 @@ typedef struct pf_vi_opts {
                              * on [lmax/30, 1.5 lmax] (lmax by 30 power iterations, the reference
                              * ChebyshevPreconditioner recipe linalg.py:331-378), symmetric
                              * multiplicative split; 2 -> the same blocks, block-diagonal split.
-                             * Damage solve: 1 -> inexact rsls Newton, inner rtol = min(1e-2, |Phi|). */
+                             * Damage solve: 1 -> inexact rsls Newton, inner rtol = min(1e-2, |Phi|).
+                             * pf_newton: | 4 -> inexact Newton, MINRES rtol per iteration
+                             * max(fieldsplit_rtol, min(1e-2, |Phi|)). */
 } pf_vi_opts;
 
 typedef struct pf_vi_report {

@@ -772,6 +772,11 @@ int newton_solve(Ctx* c, const double* u_in, const double* a_in, const double* l
     // tighter inner solves leave the MINRES history unchanged (measured on SENT 512^2 down to
     // 1e-10) at 1.5-2x the cost
     const double inner_rtol = o->inner_rtol > 0.0 ? o->inner_rtol : fs_rtol;
+    // inner_mode bit 4: inexact Newton, MINRES rtol_k = max(fieldsplit_rtol, min(1e-2, |Phi_k|)) (the
+    // quadratic forcing term, as the damage VI's inner solves): never tighter than the reference's
+    // fieldsplit_rtol, loose far from the solution and in stalled phases, where |Phi| stays large
+    const int imode = o->inner_mode & 3;
+    const bool forcing = (o->inner_mode & 4) != 0;
     double last_mu = 1.0;      // accepted step length of the previous iteration
     double last_lmax = -1.0;   // C-block spectrum estimate of the previous iteration
     auto line_search = [&](const double* dir, double slope, bool newton, bool& ok) -> int {
@@ -826,7 +831,7 @@ int newton_solve(Ctx* c, const double* u_in, const double* a_in, const double* l
         // A stalled Newton phase (the previous accepted step was at most 1/64 of its direction) barely
         // moves the iterate: keep the hierarchy (2.5 ms of setup per iteration at 512^2) and the
         // C-block spectrum estimate of the previous iteration; a breakdown rebuilds and retries.
-        const bool fixed_pc = o->inner_mode == 1 || o->inner_mode == 2;
+        const bool fixed_pc = imode == 1 || imode == 2;
         const bool stalled = fixed_pc && it > 1 && last_mu <= 1.0 / 64.0 && !getenv("PF_NEWTON_NO_STALL_KEEP");
         const bool keep = c->dim == 2 && fixed_pc && c->gmg_built &&
                           ((it == 1 && !getenv("PF_NEWTON_NO_KEEP")) || stalled);  // (NO_KEEP: calls
@@ -840,9 +845,9 @@ int newton_solve(Ctx* c, const double* u_in, const double* a_in, const double* l
         NTRY(launch_kappa(c, u, alpha, c->kappa, c->vi_c, st));
         NTRY(launch_Kaa_diag(c, c->kappa, c->da_dinv, c->act, st));
         InnerMg mg;
-        if (o->inner_mode == 1 || o->inner_mode == 2) {
+        if (imode == 1 || imode == 2) {
             mg.on = true;
-            mg.additive = o->inner_mode == 2;
+            mg.additive = imode == 2;
             mg.deg = o->inner_cycles > 0 ? o->inner_cycles : 12;
             if (stalled && keep && last_lmax > 0.0) {
                 mg.lmax = last_lmax;  // S_AUX1 still holds its |D^-1 C x|^2 unless MINRES ran on the host
@@ -863,9 +868,10 @@ int newton_solve(Ctx* c, const double* u_in, const double* a_in, const double* l
         long long kits = 0;
         bool lin_ok = false;
         const long long mr_maxit = o->inner_maxit > 0 ? o->inner_maxit : 10 * n;
+        const double rtol_it = forcing ? std::max(fs_rtol, std::min(1e-2, std::sqrt(merit))) : fs_rtol;
         auto run_minres = [&]() {
-            return mg.dev ? minres_dev(c, w, u, alpha, w.RHS, w.D, fs_rtol, mr_maxit, kits, lin_ok, st, mg)
-                          : minres(c, w, u, alpha, w.RHS, w.D, fs_rtol, mr_maxit, inner_rtol,
+            return mg.dev ? minres_dev(c, w, u, alpha, w.RHS, w.D, rtol_it, mr_maxit, kits, lin_ok, st, mg)
+                          : minres(c, w, u, alpha, w.RHS, w.D, rtol_it, mr_maxit, inner_rtol,
                                    mg.on ? 0 : std::max(0, o->inner_cycles), kits, lin_ok, st, mg);
         };
         int rc = run_minres();

@@ -82,6 +82,9 @@ class SolverConfig:
     gmg_reuse: bool = True   # keep the GMG hierarchy across solves while it stays effective
     gmg_degree: int = 2      # Chebyshev smoothing degree per multigrid level
     newton_inner_rtol: Optional[float] = None  # field-split block solves; None -> fieldsplit_rtol
+    # inexact coupled Newton: MINRES rtol = max(fieldsplit_rtol, min(1e-2, |Phi|)) per iteration (the
+    # quadratic forcing term of the damage VI); the Newton stopping rule is unchanged
+    newton_forcing: bool = True
 
     def __post_init__(self):
         if not 0.0 < self.omega < 2.0:
@@ -294,7 +297,8 @@ def coupled_newton_solve(state: State, problem: Discretization, config: SolverCo
                    inner_rtol=config.newton_inner_rtol or (config.direct_rtol if direct else 0.0),
                    inner_cycles=(config.fieldsplit_cheb_degree if mg else config.fieldsplit_cg_budget)
                    if (config.fieldsplit_inner in ("cg", "mg") and not direct) else 0,
-                   inner_mode=(2 if config.fieldsplit_additive else 1) if mg else 0)
+                   inner_mode=((2 if config.fieldsplit_additive else 1) if mg else 0)
+                   | (4 if config.newton_forcing else 0))
     opts = vic.to_c()
     rep = _lib.VIReport()
     out = state.copy()

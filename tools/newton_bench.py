@@ -54,6 +54,10 @@ VARIANTS = {
     "cheb_deg4": {"__deg": 4},
     "cheb_deg8": {"__deg": 8},
     "multiplicative": {"__mult": 1},
+    "inner_direct": {"__inner": "direct"},          # A, C blocks solved to fieldsplit_rtol
+    "coupled_direct": {"__coupled": "direct"},      # MINRES at direct_rtol (the LU stand-in)
+    "mg_rtol1e-8": {"__fsrtol": 1e-8},              # the mg split, MINRES to 1e-8
+    "no_forcing": {"__noforce": 1},                 # MINRES at fieldsplit_rtol every iteration
 }
 for name, env in VARIANTS.items():
     if args.only and name not in args.only.split(","):
@@ -64,6 +68,14 @@ for name, env in VARIANTS.items():
             c.fieldsplit_cheb_degree = v
         elif k == "__mult":
             c.fieldsplit_additive = False
+        elif k == "__inner":
+            c.fieldsplit_inner = v
+        elif k == "__coupled":
+            c.coupled_solver = v
+        elif k == "__fsrtol":
+            c.fieldsplit_rtol = v
+        elif k == "__noforce":
+            c.newton_forcing = False
         else:
             os.environ[k] = v
     ts = []
