@@ -149,7 +149,8 @@ def test_fieldsplit_inner_choices_map_onto_the_c_options():
             with pytest.raises(Stop):
                 S.coupled_newton_solve(FakeState(), FakeProblem(), SolverConfig(fieldsplit_inner=inner))
             o = captured["opts"]
-            assert (o.inner_mode, o.inner_cycles) == (mode, cycles), inner
+            assert (o.inner_mode & 3, o.inner_cycles) == (mode, cycles), inner
+            assert o.inner_mode & 4                      # newton_forcing (default): inexact Newton bit
         with pytest.raises(Stop):
             S.coupled_newton_solve(FakeState(), FakeProblem(),
                                    SolverConfig(fieldsplit_inner="mg", fieldsplit_cheb_degree=7))
@@ -157,7 +158,11 @@ def test_fieldsplit_inner_choices_map_onto_the_c_options():
         with pytest.raises(Stop):
             S.coupled_newton_solve(FakeState(), FakeProblem(),
                                    SolverConfig(fieldsplit_inner="mg", fieldsplit_additive=False))
-        assert captured["opts"].inner_mode == 1
+        assert captured["opts"].inner_mode & 3 == 1
+        with pytest.raises(Stop):
+            S.coupled_newton_solve(FakeState(), FakeProblem(),
+                                   SolverConfig(fieldsplit_inner="mg", newton_forcing=False))
+        assert captured["opts"].inner_mode == 2          # the reference's fixed fieldsplit_rtol
     finally:
         S._lib.ptr, S._stream = orig, orig_stream
     assert VIConfig(inner_mode=1).to_c().inner_mode == 1
