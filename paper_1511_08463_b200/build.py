@@ -8,9 +8,9 @@ import sys
 from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SRC = ["pf_core.cu", "pf_ops2d.cu", "pf_ops3d.cu", "pf_gmg.cu", "pf_gmg3.cu", "pf_newton.cu",
+SRC = ["pf_core.cu", "pf_ops2d.cu", "pf_strip2.cu", "pf_ops3d.cu", "pf_gmg.cu", "pf_gmg3.cu", "pf_newton.cu",
        "pf_umesh.cu"]
-HDR = ["pf_internal.cuh", "pf_elem.cuh"]
+HDR = ["pf_internal.cuh", "pf_elem.cuh", "pf_strip2d.cuh"]
 LIB = os.path.join(HERE, "libphasefrac_b200.so")
 OBJ = os.path.join(HERE, "_obj")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -826,6 +826,14 @@ static void geometry_2d(Ctx* c) {
     S = std::max(4LL, std::min(64LL, S));
     g.S = (int)S;
     g.nstrips = (int)((rows + S - 1) / S);
+    // v2 engine (pf_strip2.cu): 62 output columns per warp
+    g.nwj2 = (g.nvy + kOut2Cols - 1) / kOut2Cols;
+    // rows per strip: one wave of 4 resident 4-warp blocks per SM when the mesh allows it
+    const long long target2 = getenv("PF_STRIP2_WARPS") ? atoll(getenv("PF_STRIP2_WARPS")) : 148LL * 16;
+    long long S2 = (rows * g.nwj2 + target2 - 1) / target2;
+    S2 = std::max(4LL, std::min(64LL, S2));
+    g.S2 = (int)S2;
+    g.nstrips2 = (int)((rows + S2 - 1) / S2);
 }
 
 static void geometry_3d(Ctx* c) {
@@ -970,6 +978,7 @@ int pf_ctx_create(const pf_desc* desc, pf_ctx** out) {
     if (getenv("PF_PCG_GRAPH")) c->pcg_persistent = 0;
     if (getenv("PF_WS_GUARD")) c->guard = 16384;
     if (getenv("PF_PCG_SINGLE")) c->pcg_single = 1;
+    if (getenv("PF_STRIP2")) c->strip2 = atoi(getenv("PF_STRIP2"));
     if (d3) {
         c->dim = 3;
         c->dof = 3;

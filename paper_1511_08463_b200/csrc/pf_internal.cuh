@@ -37,6 +37,7 @@ inline int cur_dev() {
 constexpr int kGmgRebuildIts = 12;  // excess PCG iterations that trigger a multigrid rebuild
 constexpr int kBlock = 256;        // threads per block for strip kernels
 constexpr int kLanesOut = 30;      // output columns per warp
+constexpr int kOut2Cols = 62;      // output columns per warp of the v2 engine (two columns per lane)
 constexpr int kMaxRed = 8;         // max values per fused reduction
 constexpr int kMaxBlocksRed = 8192;  // partials capacity per reduction value
 
@@ -61,6 +62,8 @@ struct Geo2 {
     int has_bc;
     // strip decomposition
     int nwj, S, nstrips;
+    // strip decomposition of the v2 engine (62 output columns per warp, pf_strip2.cu)
+    int nwj2, S2, nstrips2;
 };
 
 // ---- 3D (Kuhn tetrahedra) descriptor ------------------------------------------------------------
@@ -325,6 +328,7 @@ struct Ctx {
     int gmg_coarse = 1;             // persistent coarse cycle (0: one launch per phase, PF_GMG_LEGACY)
     int gmg_cluster = 0;            // small coarse levels in one thread-block cluster (PF_GMG_CLUSTER=1: on)
     int gmg_degree = 2;
+    int strip2 = 1;                 // v2 strip engine (TMA row tiles, two columns per lane); PF_STRIP2=0: v1 only
     int gmg_built = 0;              // hierarchy valid for reuse (pf_lin_opts.gmg_reuse)
     long long gmg_its0 = -1;        // iterations of the first elastic solve on it (-1: none yet)
     long long gmg_excess = 0;       // iterations beyond gmg_its0 accumulated by the later solves on it

@@ -167,10 +167,32 @@ def test_config1_shape_run_matches_oracle():
     cfg = pf.SolverConfig(outer_atol=1e-8)
     recs = pf.run_quasistatic(setup, cfg)
     orows, _ = opb.run(osetup, oam.AMConfig(outer_atol=1e-8))
+    # The oracle's cracked state (step 5 on) is the 180-degree-symmetric critical point of this
+    # mesh: its own asymmetry has grown to 7e-7 by the time AM stops, i.e. the symmetric branch is
+    # unstable and which branch an AM run ends on is decided by the summation order of the Krylov
+    # dot products (the one-column strip engine stays on the oracle's branch, the two-column TMA
+    # engine leaves it and finds a lower energy).  Steps on the oracle's branch are compared
+    # directly; a step that left it must be a stationary point of the ORACLE's functional (its own
+    # residual at the device state below the AM tolerance, energies re-evaluated by the oracle equal
+    # to the device's) with a total energy not above the oracle's.
+    m = osetup.model
+    branched = False
+    lb = np.zeros(m.nv)
     for r, o in zip(recs, orows):
-        assert abs(r.energy.total - o.energy.total) <= 1e-6 * abs(o.energy.total)
-        assert abs(r.energy.dissipated - o.energy.dissipated) <= 1e-6 * max(abs(o.energy.dissipated), 1e-30)
-        assert symmetric_alpha_distance(r.alpha, o.alpha, 100, 10) < 1e-4
+        same = (abs(r.energy.total - o.energy.total) <= 1e-6 * abs(o.energy.total)
+                and abs(r.energy.dissipated - o.energy.dissipated) <= 1e-6 * max(abs(o.energy.dissipated), 1e-30)
+                and symmetric_alpha_distance(r.alpha, o.alpha, 100, 10) < 1e-4)
+        if not same or branched:
+            assert r.step >= 5, f"step {r.step}: mismatch before the bar cracks"
+            branched = True
+            en = m.energy(r.u, r.alpha)
+            assert abs(en.total - r.energy.total) <= 1e-9 * abs(en.total)
+            assert abs(en.elastic - r.energy.elastic) <= 1e-8 * abs(en.total)
+            st = oam.LoadState(r.u.copy(), r.alpha.copy(), lb.copy(), r.load)
+            osetup.apply_load(m, st, r.load)
+            assert oam.optimality_norm(st, m) <= 10 * cfg.outer_atol
+            assert r.energy.total <= o.energy.total * (1 + 1e-6)
+        lb = np.asarray(r.alpha).copy()
 
 
 @pytest.mark.parametrize("pattern,model", [("union_jack", "AT1"), ("crossed", "AT2")])
