@@ -828,7 +828,8 @@ static void geometry_2d(Ctx* c) {
     g.nstrips = (int)((rows + S - 1) / S);
     // v2 engine (pf_strip2.cu): 62 output columns per warp
     g.nwj2 = (g.nvy + kOut2Cols - 1) / kOut2Cols;
-    // rows per strip: one wave of 4 resident 4-warp blocks per SM when the mesh allows it
+    // (rows per strip are sized per kernel at launch by a wave model, size_strips2; PF_STRIP2_WARPS
+    // fixes a warp target instead, for experiments)
     const long long target2 = getenv("PF_STRIP2_WARPS") ? atoll(getenv("PF_STRIP2_WARPS")) : 148LL * 16;
     long long S2 = (rows * g.nwj2 + target2 - 1) / target2;
     S2 = std::max(4LL, std::min(64LL, S2));
@@ -978,6 +979,7 @@ int pf_ctx_create(const pf_desc* desc, pf_ctx** out) {
     if (getenv("PF_PCG_GRAPH")) c->pcg_persistent = 0;
     if (getenv("PF_WS_GUARD")) c->guard = 16384;
     if (getenv("PF_PCG_SINGLE")) c->pcg_single = 1;
+    c->strip2 = -1;  // auto: by mesh size, at binding
     if (getenv("PF_STRIP2")) c->strip2 = atoi(getenv("PF_STRIP2"));
     if (d3) {
         c->dim = 3;
@@ -993,6 +995,11 @@ int pf_ctx_create(const pf_desc* desc, pf_ctx** out) {
         c->dim = 2;
         c->dof = 2;
         geometry_2d(c);
+        // engine choice by size (A/B on B200, tools/opbench2.py): the TMA engine wins from about
+        // 2048^2 up (HBM-bound applies: 8192^2 union-jack Kuu 4.6 -> 5.8 TB/s); below that an apply
+        // is a few strip rows per warp, bound by launch and pipeline-fill latency, where the
+        // one-column engine's shorter steps are as fast or faster (SENT 512^2 load step +4%)
+        if (c->strip2 < 0) c->strip2 = c->g.nc >= 3000000 ? 1 : 0;
         c->n_a = c->g.nv;
         c->n_u = 2 * c->g.nv;
         c->n_el = c->g.ncell * c->g.npc;

@@ -328,7 +328,7 @@ struct Ctx {
     int gmg_coarse = 1;             // persistent coarse cycle (0: one launch per phase, PF_GMG_LEGACY)
     int gmg_cluster = 0;            // small coarse levels in one thread-block cluster (PF_GMG_CLUSTER=1: on)
     int gmg_degree = 2;
-    int strip2 = 1;                 // v2 strip engine (TMA row tiles, two columns per lane); PF_STRIP2=0: v1 only
+    int strip2 = 1;                 // v2 strip engine (TMA row tiles, two columns per lane): auto by mesh size; PF_STRIP2=0/1 forces
     int gmg_built = 0;              // hierarchy valid for reuse (pf_lin_opts.gmg_reuse)
     long long gmg_its0 = -1;        // iterations of the first elastic solve on it (-1: none yet)
     long long gmg_excess = 0;       // iterations beyond gmg_its0 accumulated by the later solves on it

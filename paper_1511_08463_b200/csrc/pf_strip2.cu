@@ -110,18 +110,49 @@ inline int strip2_blocks(const Geo2& g) {
     return (int)((warps * 32 + kBlock2 - 1) / kBlock2);
 }
 
+// Rows per strip by a wave model (as tile3 does for the 3D engine): with R warps resident on the
+// GPU (148 SMs x this kernel's blocks per SM x 4 warps), ns strips of S = ceil(rows / ns) rows cost
+// about waves x (S + 1 halo row + kRamp steps of pipeline fill), waves = ceil(nwj2 ns / R).  A fixed
+// warp target loses up to a wave when the kernel's occupancy differs from the assumed one (measured:
+// crossed Kuu 2048^2 0.094 ms at 2368 target warps, 0.080 ms at 2 x 1776).
+static void size_strips2(Geo2& g, int resident_warps) {
+    constexpr long long kRamp = 3;
+    const long long rows = g.nx + 1;
+    long long best_ns = 1, best_t = -1;
+    for (long long ns = 1; ns <= rows; ++ns) {
+        const long long S = (rows + ns - 1) / ns;
+        if (S < 4 && ns > 1) break;
+        if (S > 64) continue;  // longer strips measured slower at 8192^2 (one wave of 373-row strips: 0.51 vs 0.46 ms)
+        const long long warps = (long long)g.nwj2 * ns;
+        if ((warps * 32 + kBlock2 - 1) / kBlock2 > kMaxBlocksRed) break;
+        const long long waves = (warps + resident_warps - 1) / resident_warps;
+        const long long t = waves * (S + 1 + kRamp);
+        if (best_t < 0 || t < best_t) { best_t = t; best_ns = ns; }
+    }
+    const long long S = (rows + best_ns - 1) / best_ns;
+    g.S2 = (int)S;
+    g.nstrips2 = (int)((rows + S - 1) / S);
+}
+
 template <class Op, int PAT>
-static cudaError_t launch2_pat(const Geo2& g, const Op& op, const TmaSet& tm, int nb, cudaStream_t st) {
+static cudaError_t launch2_pat(Geo2 g, const Op& op, const TmaSet& tm, cudaStream_t st) {
     constexpr int smem = strip2_smem<Op, PAT>();
     static_assert(smem <= 227 * 1024, "strip stage ring exceeds shared memory");
-    static std::atomic<bool> attr[kMaxDev];
+    static std::atomic<int> occ[kMaxDev];  // blocks per SM of this instantiation (0: not set up yet)
     const int dv = cur_dev();
-    if (!attr[dv].load()) {
+    if (!occ[dv].load()) {
         cudaError_t e = cudaFuncSetAttribute(k_strip2v<Op, PAT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
-        attr[dv] = true;
+        int nb = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_strip2v<Op, PAT>, kBlock2, smem);
+        if (e != cudaSuccess) return e;
+        occ[dv] = nb > 0 ? nb : 1;
     }
-    k_strip2v<Op, PAT><<<nb, kBlock2, smem, st>>>(g, op, tm);
+    static const long long forced = getenv("PF_STRIP2_WARPS") ? atoll(getenv("PF_STRIP2_WARPS")) : 0;
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dv);
+    if (!forced) size_strips2(g, sms * occ[dv].load() * (kBlock2 / 32));
+    k_strip2v<Op, PAT><<<strip2_blocks(g), kBlock2, smem, st>>>(g, op, tm);
     return cudaSuccess;
 }
 
@@ -132,14 +163,12 @@ int run_strip2(Ctx* c, const Op& op, cudaStream_t st, int kind, double bytes) {
     op.maps(c->g, mb);
     if (!mb.ok) return -1;
     const Geo2& g = c->g;
-    const int nb = strip2_blocks(g);
-    if (nb > kMaxBlocksRed) return -1;
     const int slot = prof_begin(c, st);
     cudaError_t e;
     switch (g.pattern) {
-        case PF_UNION_JACK: e = launch2_pat<Op, PF_UNION_JACK>(g, op, mb.set, nb, st); break;
-        case PF_RIGHT: e = launch2_pat<Op, PF_RIGHT>(g, op, mb.set, nb, st); break;
-        default: e = launch2_pat<Op, PF_CROSSED>(g, op, mb.set, nb, st); break;
+        case PF_UNION_JACK: e = launch2_pat<Op, PF_UNION_JACK>(g, op, mb.set, st); break;
+        case PF_RIGHT: e = launch2_pat<Op, PF_RIGHT>(g, op, mb.set, st); break;
+        default: e = launch2_pat<Op, PF_CROSSED>(g, op, mb.set, st); break;
     }
     if (e != cudaSuccess) return check_cuda(c, e, "strip v2 kernel attribute");
     prof_end(c, st, slot, kind, bytes);
