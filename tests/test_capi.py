@@ -71,3 +71,19 @@ def test_no_device_fails_loudly():
     assert rc == _lib.PF_ECUDA
     with pytest.raises(RuntimeError):
         _lib.raise_for(rc, None)
+
+
+def test_library_stages_rows_with_tma():
+    """The shipped library's v2 strip kernels stage rows with the tensor memory accelerator: SASS
+    UTMALDG (cp.async.bulk.tensor loads) completing on mbarrier transactions (SYNCS.ARRIVE.TRANS64).
+    Reads the object of csrc/pf_strip2.cu when the build left it (seconds), else the whole library."""
+    import shutil
+    import subprocess
+    from paper_1511_08463_b200 import build
+    if shutil.which("cuobjdump") is None or not os.path.exists(build.LIB):
+        pytest.skip("cuobjdump or the built library is not available")
+    obj = os.path.join(build.OBJ, "pf_strip2.o")
+    target = obj if os.path.exists(obj) and os.path.getmtime(obj) <= os.path.getmtime(build.LIB) + 1 else build.LIB
+    sass = subprocess.run(["cuobjdump", "-sass", target], capture_output=True, text=True).stdout
+    assert sass.count("UTMALDG.1D") > 100
+    assert "SYNCS.ARRIVE.TRANS64" in sass and "SYNCS.PHASECHK.TRANS64.TRYWAIT" in sass
