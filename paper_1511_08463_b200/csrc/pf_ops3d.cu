@@ -321,7 +321,7 @@ __device__ __forceinline__ void strip3_tile(const Geo3& g, Op& op, unsigned char
     constexpr int kOutJ3 = kW3 - 2;  // output pencils per block
     constexpr int NV = Op::NV, NC = Op::NC, PD = Op::PD, NE = Op::NE, SV = Op::SV, SC = Op::SC;
     constexpr int STAGE = (SV + SC) * 256;
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int w = __shfl_sync(PF_FULL, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;  // warp-uniform for the compiler
     double* vx = reinterpret_cast<double*>(smem + kW3 * PD * STAGE);   // [2][kW3][NV][32]
     double* cx = vx + 2 * kW3 * NV * 32;                                 // [2][kW3][2][NC][32]
     const int bk = tile % g.nbk;
@@ -332,6 +332,10 @@ __device__ __forceinline__ void strip3_tile(const Geo3& g, Op& op, unsigned char
     const bool vv = j >= 0 && j <= g.ny && k >= 0 && k <= g.nz;
     const bool cv = j >= 0 && j < g.ny && k >= 0 && k < g.nz && w < kW3 - 1 && lane < 31;
     const bool ov = vv && w >= 1 && w <= kOutJ3 && lane >= 1 && lane <= 30;
+    // interior tile: pencils bj*kOutJ3-1 .. +kW3-1 and lanes bk*30-1 .. +31 all strictly inside the mesh
+    const bool tile_in = bj * kOutJ3 - 1 >= 1 && bj * kOutJ3 - 1 + kW3 - 1 <= g.ny - 1 &&
+                         bk * 30 - 1 >= 1 && bk * 30 - 1 + 31 <= g.nz - 1;
+    const bool ovf = w >= 1 && w <= kOutJ3 && lane >= 1 && lane <= 30;  // ov on an interior tile
     const int i0 = bs * g.S;
     const int i1 = min(i0 + g.S, g.nx + 1);
     const int vlast = min(i1, g.nx), clast = min(i1 - 1, g.nx - 1);
@@ -384,77 +388,92 @@ __device__ __forceinline__ void strip3_tile(const Geo3& g, Op& op, unsigned char
         issue(0, ci + 1 + PD, ci + PD);
     }
     int buf = 0;
+    int us = 1 % PD;  // the stage holding vertex row ci+2 / cell row ci+1
+    // One row step.  FAST: the tile is interior (every pencil and lane a valid vertex, none on the
+    // mesh boundary) and rows ci .. ci+2 are interior rows of the strip, so the validity predicates,
+    // the zero fills they guard and the Dirichlet-mask lookups (a descriptor copy with has_bc = 0)
+    // drop out at compile time; the general form keeps them.
+    Geo3 gi = g;
+    gi.has_bc = 0;
+    auto step = [&](auto fast_c) {
+        constexpr bool FAST = decltype(fast_c)::v != 0;
+        const Geo3& gg = FAST ? gi : g;
+        const bool cell_ok = FAST ? true : (ci >= 0 && ci < g.nx && cv);
+        // corners: q = 4 di + 2 dj + dk
+        double X[NV][8];
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+            X[q][0] = vc[q]; X[q][2] = rc[q]; X[q][4] = vn[q]; X[q][6] = rn[q];
+            X[q][1] = __shfl_down_sync(PF_FULL, vc[q], 1);
+            X[q][3] = __shfl_down_sync(PF_FULL, rc[q], 1);
+            X[q][5] = __shfl_down_sync(PF_FULL, vn[q], 1);
+            X[q][7] = __shfl_down_sync(PF_FULL, rn[q], 1);
+        }
+        double Y[NC][8];
+#pragma unroll
+        for (int q = 0; q < NC; ++q)
+#pragma unroll
+            for (int c = 0; c < 8; ++c) Y[q][c] = 0.0;
+        if (cell_ok) op.cell(gg, ci, j, k, X, ec, Y, FAST ? ovf : ((ci >= i0) && ov));
+        // k-combine: T_ab = Y[ab0] + shfl_up(Y[ab1])
+        double T00[NC], T01[NC], T10[NC], T11[NC];
+#pragma unroll
+        for (int q = 0; q < NC; ++q) {
+            T00[q] = Y[q][0] + __shfl_up_sync(PF_FULL, Y[q][1], 1);
+            T01[q] = Y[q][2] + __shfl_up_sync(PF_FULL, Y[q][3], 1);
+            T10[q] = Y[q][4] + __shfl_up_sync(PF_FULL, Y[q][5], 1);
+            T11[q] = Y[q][6] + __shfl_up_sync(PF_FULL, Y[q][7], 1);
+        }
+        // next rows from the ring
+        cp_wait3<PD - 1>();
+        const S3 s{wbase + us * STAGE, lane};
+        double vnn[NV], ecn[NE];
+#pragma unroll
+        for (int q = 0; q < NV; ++q) vnn[q] = 0.0;
+#pragma unroll
+        for (int q = 0; q < NE; ++q) ecn[q] = 0.0;
+        if (FAST || (ci + 2 <= vlast && vv)) op.fix_v(gg, ci + 2, j, k, s, vnn);
+        if (FAST || (ci + 1 >= 0 && ci + 1 <= clast && cv)) op.fix_c(gg, ci + 1, j, k, s.at(SV), ecn);
+        // one exchange: j-carry contributions of row ci and vertex row ci+2
+#pragma unroll
+        for (int q = 0; q < NC; ++q) {
+            *xc(buf, w, 0, q) = T01[q];
+            *xc(buf, w, 1, q) = T11[q];
+        }
+#pragma unroll
+        for (int q = 0; q < NV; ++q) *xv(buf, w, q) = vnn[q];
+        __syncthreads();
+        double tot[NC];
+#pragma unroll
+        for (int q = 0; q < NC; ++q) {
+            const double l01 = w > 0 ? *xc(buf, w - 1, 0, q) : 0.0;
+            const double l11 = w > 0 ? *xc(buf, w - 1, 1, q) : 0.0;
+            tot[q] = carry[q] + T00[q] + l01;
+            carry[q] = T10[q] + l11;
+        }
+        double rnn[NV];
+#pragma unroll
+        for (int q = 0; q < NV; ++q) rnn[q] = (w + 1 < kW3) ? *xv(buf, w + 1, q) : 0.0;
+        if (FAST ? ovf : (ci >= i0 && ov)) op.out(gg, ci, j, k, tot, vc);
+#pragma unroll
+        for (int q = 0; q < NV; ++q) { vc[q] = vn[q]; rc[q] = rn[q]; vn[q] = vnn[q]; rn[q] = rnn[q]; }
+#pragma unroll
+        for (int q = 0; q < NE; ++q) ec[q] = ecn[q];
+        issue(us, ci + 2 + PD, ci + 1 + PD);
+        us = us + 1 == PD ? 0 : us + 1;
+        buf ^= 1;
+        ++ci;
+    };
+    // fast rounds of three steps (the row registers rotate with period 3: no moves): rows ci .. ci+4
+    // interior and owned, i.e. ci >= max(i0, 1) and ci + 4 <= min(vlast, nx - 1), ci + 3 <= clast
+    const int flo = max(i0, 1), fhi = min(min(vlast, g.nx - 1) - 4, clast - 3);
     while (ci < i1) {
-#pragma unroll
-        for (int u = 0; u < PD; ++u) {
-            if (ci < i1) {
-                constexpr int one = 1;
-                const int us = (u + one) % PD;  // the stage holding vertex row ci+2 / cell row ci+1
-                const bool cell_ok = ci >= 0 && ci < g.nx && cv;
-                // corners: q = 4 di + 2 dj + dk
-                double X[NV][8];
-#pragma unroll
-                for (int q = 0; q < NV; ++q) {
-                    X[q][0] = vc[q]; X[q][2] = rc[q]; X[q][4] = vn[q]; X[q][6] = rn[q];
-                    X[q][1] = __shfl_down_sync(PF_FULL, vc[q], 1);
-                    X[q][3] = __shfl_down_sync(PF_FULL, rc[q], 1);
-                    X[q][5] = __shfl_down_sync(PF_FULL, vn[q], 1);
-                    X[q][7] = __shfl_down_sync(PF_FULL, rn[q], 1);
-                }
-                double Y[NC][8];
-#pragma unroll
-                for (int q = 0; q < NC; ++q)
-#pragma unroll
-                    for (int c = 0; c < 8; ++c) Y[q][c] = 0.0;
-                if (cell_ok) op.cell(g, ci, j, k, X, ec, Y, (ci >= i0) && ov);
-                // k-combine: T_ab = Y[ab0] + shfl_up(Y[ab1])
-                double T00[NC], T01[NC], T10[NC], T11[NC];
-#pragma unroll
-                for (int q = 0; q < NC; ++q) {
-                    T00[q] = Y[q][0] + __shfl_up_sync(PF_FULL, Y[q][1], 1);
-                    T01[q] = Y[q][2] + __shfl_up_sync(PF_FULL, Y[q][3], 1);
-                    T10[q] = Y[q][4] + __shfl_up_sync(PF_FULL, Y[q][5], 1);
-                    T11[q] = Y[q][6] + __shfl_up_sync(PF_FULL, Y[q][7], 1);
-                }
-                // next rows from the ring
-                cp_wait3<PD - 1>();
-                const S3 s{wbase + us * STAGE, lane};
-                double vnn[NV], ecn[NE];
-#pragma unroll
-                for (int q = 0; q < NV; ++q) vnn[q] = 0.0;
-#pragma unroll
-                for (int q = 0; q < NE; ++q) ecn[q] = 0.0;
-                if (ci + 2 <= vlast && vv) op.fix_v(g, ci + 2, j, k, s, vnn);
-                if (ci + 1 >= 0 && ci + 1 <= clast && cv) op.fix_c(g, ci + 1, j, k, s.at(SV), ecn);
-                // one exchange: j-carry contributions of row ci and vertex row ci+2
-#pragma unroll
-                for (int q = 0; q < NC; ++q) {
-                    *xc(buf, w, 0, q) = T01[q];
-                    *xc(buf, w, 1, q) = T11[q];
-                }
-#pragma unroll
-                for (int q = 0; q < NV; ++q) *xv(buf, w, q) = vnn[q];
-                __syncthreads();
-                double tot[NC];
-#pragma unroll
-                for (int q = 0; q < NC; ++q) {
-                    const double l01 = w > 0 ? *xc(buf, w - 1, 0, q) : 0.0;
-                    const double l11 = w > 0 ? *xc(buf, w - 1, 1, q) : 0.0;
-                    tot[q] = carry[q] + T00[q] + l01;
-                    carry[q] = T10[q] + l11;
-                }
-                double rnn[NV];
-#pragma unroll
-                for (int q = 0; q < NV; ++q) rnn[q] = (w + 1 < kW3) ? *xv(buf, w + 1, q) : 0.0;
-                if (ci >= i0 && ov) op.out(g, ci, j, k, tot, vc);
-#pragma unroll
-                for (int q = 0; q < NV; ++q) { vc[q] = vn[q]; rc[q] = rn[q]; vn[q] = vnn[q]; rn[q] = rnn[q]; }
-#pragma unroll
-                for (int q = 0; q < NE; ++q) ec[q] = ecn[q];
-                issue(us, ci + 2 + PD, ci + 1 + PD);
-                buf ^= 1;
-                ++ci;
-            }
+        if (tile_in && ci >= flo && ci <= fhi) {
+            step(IC3<1>{});
+            step(IC3<1>{});
+            step(IC3<1>{});
+        } else {
+            step(IC3<0>{});
         }
     }
     cp_wait3<0>();
