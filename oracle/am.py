@@ -189,7 +189,19 @@ def _coupled_linear(cfg: AMConfig, nu: int):
         iu = idx[idx < nu]
         ia = idx[idx >= nu] - nu
         red = kr.Block2x2(kr.sub(J.A, iu, iu), kr.sub(J.B, iu, ia), kr.sub(J.C, ia, ia))
-        P = kr.FieldSplit(red, kr.lu_solver(red.A), kr.lu_solver(red.C))
+        if cfg.fieldsplit_inner == "cg":
+            # 3D sizes where an LU of the elastic block does not fit: A^-1 by Jacobi-PCG at 1e-12
+            # (the reference's exact block solve to round-off), C^-1 still by LU
+            MA = kr.Jacobi(red.A)
+
+            def solve_A(r, A=red.A, MA=MA):
+                x, rep = kr.pcg(A, r, MA, rtol=1e-12)
+                if not rep.converged:
+                    raise kr.InnerFailure(f"field-split A block CG stalled at {rep.residual:.3e}")
+                return x
+            P = kr.FieldSplit(red, solve_A, kr.lu_solver(red.C))
+        else:
+            P = kr.FieldSplit(red, kr.lu_solver(red.A), kr.lu_solver(red.C))
         d, rep = kr.minres(red, rhs, P, rtol=cfg.fieldsplit_rtol)
         if not rep.converged:
             raise kr.SolverFailure(f"field-split MINRES stalled at {rep.residual:.3e}")

@@ -84,6 +84,7 @@ def run_oracle():
                            max_am_iterations=3000)
     if args.oracle_cg:
         cfg.elastic_solver, cfg.elastic_precond, cfg.elastic_rtol = "cg", "jacobi", 1e-13
+        cfg.fieldsplit_inner = "cg"   # the Newton field split's elastic block by PCG too (no 3D LU of Kuu)
     hist = []
 
     def log(e):
