@@ -8,7 +8,9 @@ vector passed in is a view into a NaN-filled tensor with 4096 guard elements on 
 * an out-of-bounds READ of a caller tensor pulls a NaN into the result -> caught by the finiteness
   and oracle-parity checks.
 The sizes are odd and tiny (1 x 3, 13 x 7, 3 x 4 x 5) so strip, tile and block boundaries fall
-everywhere; every kernel family on the load-step path runs: operators, physics, load, the elastic
+everywhere, plus one wide mesh (5 x 131) with interior windows of the TMA engine; the 2D cases run on
+both strip engines (the TMA engine cannot read outside a caller tensor by construction -- its tensor
+maps carry the extents and the hardware zero-fills -- so for it the checks are about writes); every kernel family on the load-step path runs: operators, physics, load, the elastic
 PCG (Jacobi and multigrid), the damage VI (persistent PCG), the relaxation, Newton (device MINRES).
 """
 
@@ -113,10 +115,12 @@ def _exercise(prob, om, rng, dim):
     assert _guard_bytes(prob) == 0, "a kernel wrote past a workspace buffer"
 
 
+@pytest.mark.parametrize("engine", ["0", "1"])  # one-column cp.async engine / two-column TMA engine
 @pytest.mark.parametrize("pattern", ["union_jack", "right", "crossed"])
-@pytest.mark.parametrize("shape", [(13, 7), (1, 3), (33, 2)])
-def test_bounds_2d(pattern, shape, monkeypatch):
+@pytest.mark.parametrize("shape", [(13, 7), (1, 3), (33, 2), (5, 131)])
+def test_bounds_2d(pattern, shape, engine, monkeypatch):
     monkeypatch.setenv("PF_WS_GUARD", "1")
+    monkeypatch.setenv("PF_STRIP2", engine)
     prob, om, rng = make_pair(pattern, "plane_strain", "AT2", shape[0], shape[1], hetero=True, eps0=True)
     assert prob.ws_guarded()
     _exercise(prob, om, rng, 2)
