@@ -317,6 +317,14 @@ __global__ void k_classify(long long n, const double* __restrict__ x, const doub
     });
 }
 
+// projected-Jacobi direction of the damage QP: d = -D^-1 F  (damage_solve, crawl mode)
+__global__ void k_pj_dir(long long n, const double* __restrict__ dinv, const double* __restrict__ F,
+                         double* __restrict__ d) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        d[i] = -dinv[i] * F[i];
+}
+
 __global__ void k_scale(long long n, double* __restrict__ x, double a) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x)
@@ -695,9 +703,41 @@ int damage_solve(Ctx* c, const double* u, const double* lb, const double* a_in, 
     double merit_prev = 0.0;  // |Phi|^2 of the previous VI iterate (0: none yet)
     static const bool ew_on = !(getenv("PF_VI_EW") && atoi(getenv("PF_VI_EW")) == 0);
     static const double ew_cap = getenv("PF_VI_EWCAP") ? atof(getenv("PF_VI_EWCAP")) : 0.1;
+    // Crawl mode.  When two consecutive active-set iterations reduce |Phi| by less than 30 % the
+    // free boundary is moving one vertex layer per Newton solve (see the forcing-term note below);
+    // from then on every iteration is preceded by a few projected-Jacobi sweeps
+    //     x <- P[x - w D^-1 (Kaa x + c)]
+    // (one vector pass and one trial strip pass each, no host round trip), which move the free
+    // boundary at a twentieth of the cost of an active-set iteration.  The QP is strictly convex, so
+    // its minimiser -- what the VI stopping rule tests -- does not depend on the path.
+    static const int pj_sweeps = getenv("PF_VI_PJ") ? atoi(getenv("PF_VI_PJ")) : 16;
+    static const double pj_w = getenv("PF_VI_PJW") ? atof(getenv("PF_VI_PJW")) : 0.7;
+    int slow = 0;
+    bool have_dinvJ = false;
     for (int it = 1; it <= o->max_iterations; ++it) {
         if (std::sqrt(merit) <= o->abs_tol) break;
         rep->iterations = it;
+        // (inexact mode only: inner_mode 0 follows the reference's iterates step by step; scratch:
+        // the single-reduction PCG's two vectors, free unless that variant is selected)
+        if (pj_sweeps > 0 && slow >= 2 && o->inner_mode == 1 && !c->pcg_single) {
+            double *dinvJ = c->cg1_s0, *dir = c->cg1_s1;
+            if (!have_dinvJ) {  // unmasked Jacobi scaling
+                PF_TRY(launch_Kaa_diag(c, c->kappa, dinvJ, nullptr, st));
+                have_dinvJ = true;
+            }
+            PF_TRY(set_scal(c, st, S_MU, pj_w));
+            for (int sw = 0; sw < pj_sweeps; ++sw) {
+                k_pj_dir<<<vb, kVecBlock, 0, st>>>(n, dinvJ, F, dir);
+                c->launches++;
+                PF_TRY(launch_Kaa_trial(c, c->kappa, c->vi_c, x, dir, lb, tx, tF, nullptr, S_TMERIT, st));
+                std::swap(x, tx);
+                std::swap(F, tF);
+            }
+            PF_TRY(read_scal(c, st, S_TMERIT, 1));
+            merit = c->h_scal[S_TMERIT];
+            if (getenv("PF_VI_TRACE")) fprintf(stderr, "  vi it=%d after %d sweeps merit=%.3e\n", it, pj_sweeps, std::sqrt(merit));
+            if (std::sqrt(merit) <= o->abs_tol) break;
+        }
         k_classify<<<vb, kVecBlock, 0, st>>>(n, x, F, lb, c->act, c->vi_d, c->scal, rb);
         c->launches++;
         PF_TRY(read_scal(c, st, S_NINACT, 1));
@@ -766,6 +806,7 @@ int damage_solve(Ctx* c, const double* u, const double* lb, const double* a_in, 
         }
         if (!ok) break;
         push_hist(merit);
+        slow = (merit_prev > 0.0 && merit > 0.49 * merit_prev) ? slow + 1 : 0;
     }
     rep->final_residual_norm = std::sqrt(merit);
     rep->converged = rep->final_residual_norm <= o->abs_tol;
