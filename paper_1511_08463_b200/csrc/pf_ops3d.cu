@@ -1274,7 +1274,11 @@ static int run3_sm(Ctx* c, const Geo3& g, const Sm3Args& a, cudaStream_t st, int
     const double vec = EPI == E3_RESID ? 48.0 : (EPI == E3_RESID_CHEB0 ? 96.0 : (EPI == E3_CHEB ? 144.0 : 144.0));
     const double bytes = (EPI == E3_CHEB_B ? 56.0 + 24.0 : 56.0 - 24.0) * g.nv + vec * g.nv;
     // the first step from zero stages 7 vertex slots and spills 76 B at 128 registers (two 8-warp
-    // blocks per SM); PF_K3SM_MINB1=1 runs it one block per SM with 255 registers instead (A/B)
+    // blocks per SM); PF_K3SM_MINB1=1 runs it one block per SM with 212 registers and no spill
+    // instead.  Measured on config 4 (128^3, steps 7-11): 0.2668 / 0.1650 / 0.2335 / 0.2287 / 0.2059 s
+    // with the spilling two-block tiling, 0.2678 / 0.1658 / 0.2344 / 0.2299 / 0.2067 s without the
+    // spill -- the spill costs nothing measurable (one of four smoother steps, L1-resident), the lost
+    // occupancy slightly more, so the default stays
     if constexpr (EPI == E3_CHEB_B) {
         static const bool one = getenv("PF_K3SM_MINB1") != nullptr;
         if (one) {
