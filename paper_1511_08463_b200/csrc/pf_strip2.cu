@@ -110,24 +110,38 @@ inline int strip2_blocks(const Geo2& g) {
     return (int)((warps * 32 + kBlock2 - 1) / kBlock2);
 }
 
-// Rows per strip by a wave model (as tile3 does for the 3D engine): with R warps resident on the
-// GPU (148 SMs x this kernel's blocks per SM x 4 warps), ns strips of S = ceil(rows / ns) rows cost
-// about waves x (S + 1 halo row + kRamp steps of pipeline fill), waves = ceil(nwj2 ns / R).  A fixed
-// warp target loses up to a wave when the kernel's occupancy differs from the assumed one (measured:
-// crossed Kuu 2048^2 0.094 ms at 2368 target warps, 0.080 ms at 2 x 1776).
+// Rows per strip.  With R warps resident on the GPU (SMs x this kernel's blocks per SM x 4 warps),
+// ns strips of S = ceil(rows / ns) rows run nwj2 ns warps of S + 1 row steps each (one halo row per
+// strip).  Blocks start and retire one by one, so the launch behaves like a continuous flow of
+// nwj2 (rows + ns) / R steps through the resident slots, plus the tail while the last blocks drain
+// (about half a strip and its pipeline fill).  Short strips cost halo rows, long strips cost tail:
+//     t(ns) = nwj2 (rows + ns) / R + (S + kRamp) / 2,   minimised over ns (S >= 4, grid <= the
+// reduction buffer).  Measured against a whole-wave model (waves x (S + 4), which prefers few long
+// waves): 4096^2 union-jack Kuu 0.1485 -> 0.128 ms, 2048^2 0.0481 -> 0.0461 ms (tools/opbench.py with
+// PF_STRIP2_WARPS sweeps, profiles/r02t_strip2_sizing.log).
 static void size_strips2(Geo2& g, int resident_warps) {
-    constexpr long long kRamp = 3;
+    constexpr double kRamp = 3.0;
     const long long rows = g.nx + 1;
-    long long best_ns = 1, best_t = -1;
+    // a mesh that fits one wave of strips of at most 32 rows runs as that one wave (1024^2 .. 2048^2:
+    // Kaa 2048^2 union-jack 0.039 vs 0.042 ms, the config-3 slab 0.958 vs 0.976 s/step)
+    {
+        const long long ns1 = std::max(1LL, (long long)resident_warps / g.nwj2);
+        const long long S1 = std::max(4LL, (rows + ns1 - 1) / ns1);
+        if (S1 <= 32) {
+            g.S2 = (int)S1;
+            g.nstrips2 = (int)((rows + S1 - 1) / S1);
+            return;
+        }
+    }
+    long long best_ns = 1;
+    double best_t = -1.0;
     for (long long ns = 1; ns <= rows; ++ns) {
         const long long S = (rows + ns - 1) / ns;
         if (S < 4 && ns > 1) break;
-        if (S > 64) continue;  // longer strips measured slower at 8192^2 (one wave of 373-row strips: 0.51 vs 0.46 ms)
         const long long warps = (long long)g.nwj2 * ns;
         if ((warps * 32 + kBlock2 - 1) / kBlock2 > kMaxBlocksRed) break;
-        const long long waves = (warps + resident_warps - 1) / resident_warps;
-        const long long t = waves * (S + 1 + kRamp);
-        if (best_t < 0 || t < best_t) { best_t = t; best_ns = ns; }
+        const double t = (double)g.nwj2 * (double)(rows + ns) / (double)resident_warps + 0.5 * ((double)S + kRamp);
+        if (best_t < 0.0 || t < best_t) { best_t = t; best_ns = ns; }
     }
     const long long S = (rows + best_ns - 1) / best_ns;
     g.S2 = (int)S;
