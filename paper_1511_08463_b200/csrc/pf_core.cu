@@ -936,7 +936,8 @@ void pf::tile3(Geo3& g, int outj, int resident) {
         const long long t = waves * (S + 4);
         if (best_t < 0 || t < best_t) { best_t = t; best_ns = ns; }
     }
-    const long long S = (rows + best_ns - 1) / best_ns;
+    long long S = (rows + best_ns - 1) / best_ns;
+    if (getenv("PF_K3_S")) S = std::max(1LL, std::min(rows, atoll(getenv("PF_K3_S"))));  // A/B sweeps
     g.S = (int)S;
     g.nstrips = (int)((rows + S - 1) / S);
 }
