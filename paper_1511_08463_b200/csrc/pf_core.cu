@@ -892,6 +892,7 @@ static void geometry_2d(Ctx* c) {
     S2 = std::max(4LL, std::min(64LL, S2));
     g.S2 = (int)S2;
     g.nstrips2 = (int)((rows + S2 - 1) / S2);
+    g.nslow2 = 0;
 }
 
 static void geometry_3d(Ctx* c) {

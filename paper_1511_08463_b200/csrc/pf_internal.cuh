@@ -64,6 +64,7 @@ struct Geo2 {
     int nwj, S, nstrips;
     // strip decomposition of the v2 engine (62 output columns per warp, pf_strip2.cu)
     int nwj2, S2, nstrips2;
+    int nslow2;   // boundary windows whose strips are split between two warps (0: none)
 };
 
 // ---- 3D (Kuhn tetrahedra) descriptor ------------------------------------------------------------

@@ -106,7 +106,7 @@ static constexpr int strip2_smem() {
 }
 
 inline int strip2_blocks(const Geo2& g) {
-    const long long warps = (long long)g.nwj2 * g.nstrips2;
+    const long long warps = (long long)(g.nwj2 + g.nslow2) * g.nstrips2;
     return (int)((warps * 32 + kBlock2 - 1) / kBlock2);
 }
 
@@ -119,13 +119,13 @@ inline int strip2_blocks(const Geo2& g) {
 // reduction buffer).  Measured against a whole-wave model (waves x (S + 4), which prefers few long
 // waves): 4096^2 union-jack Kuu 0.1485 -> 0.128 ms, 2048^2 0.0481 -> 0.0461 ms (tools/opbench.py with
 // PF_STRIP2_WARPS sweeps, profiles/r02t_strip2_sizing.log).
-static void size_strips2(Geo2& g, int resident_warps) {
+static void size_strips2(Geo2& g, int resident_warps, int nslow) {
     constexpr double kRamp = 3.0;
     const long long rows = g.nx + 1;
     // a mesh that fits one wave of strips of at most 32 rows runs as that one wave (1024^2 .. 2048^2:
     // Kaa 2048^2 union-jack 0.039 vs 0.042 ms, the config-3 slab 0.958 vs 0.976 s/step)
     {
-        const long long ns1 = std::max(1LL, (long long)resident_warps / g.nwj2);
+        const long long ns1 = std::max(1LL, (long long)resident_warps / (g.nwj2 + nslow));  // incl. the split halves
         const long long S1 = std::max(4LL, (rows + ns1 - 1) / ns1);
         if (S1 <= 32) {
             g.S2 = (int)S1;
@@ -138,7 +138,7 @@ static void size_strips2(Geo2& g, int resident_warps) {
     for (long long ns = 1; ns <= rows; ++ns) {
         const long long S = (rows + ns - 1) / ns;
         if (S < 4 && ns > 1) break;
-        const long long warps = (long long)g.nwj2 * ns;
+        const long long warps = (long long)(g.nwj2 + nslow) * ns;
         if ((warps * 32 + kBlock2 - 1) / kBlock2 > kMaxBlocksRed) break;
         const double t = (double)g.nwj2 * (double)(rows + ns) / (double)resident_warps + 0.5 * ((double)S + kRamp);
         if (best_t < 0.0 || t < best_t) { best_t = t; best_ns = ns; }
@@ -165,7 +165,17 @@ static cudaError_t launch2_pat(Geo2 g, const Op& op, const TmaSet& tm, cudaStrea
     static const long long forced = getenv("PF_STRIP2_WARPS") ? atoll(getenv("PF_STRIP2_WARPS")) : 0;
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dv);
-    if (!forced) size_strips2(g, sms * occ[dv].load() * (kBlock2 / 32));
+    // boundary windows (general row step): window 0 and every window reaching past column ny - 1;
+    // their strips are split between two warps (strip_pass2)
+    static const bool split = !(getenv("PF_STRIP2_SPLIT") && atoi(getenv("PF_STRIP2_SPLIT")) == 0);
+    int nslow = 0;
+    if (split && g.nwj2 >= 4) {
+        nslow = 1;
+        for (int wj = g.nwj2 - 1; wj > 0 && wj * kOut2 - 1 + kCols2 > g.ny; --wj) ++nslow;
+    }
+    if (!forced) size_strips2(g, sms * occ[dv].load() * (kBlock2 / 32), nslow);
+    g.nslow2 = 0;
+    if (nslow > 0 && ((long long)(g.nwj2 + nslow) * g.nstrips2 * 32 + kBlock2 - 1) / kBlock2 <= kMaxBlocksRed) g.nslow2 = nslow;
     k_strip2v<Op, PAT><<<strip2_blocks(g), kBlock2, smem, st>>>(g, op, tm);
     return cudaSuccess;
 }

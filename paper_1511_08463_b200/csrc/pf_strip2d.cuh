@@ -294,8 +294,25 @@ __device__ __forceinline__ void strip_pass2(const Geo2& g, Op& op, const TmaMap*
     constexpr int SV = Op::sv(PAT), SC = Op::sc(PAT) > 0 ? Op::sc(PAT) : 0;
     constexpr int STAGE = (SV + SC) * kPitch2;
     const int lane = threadIdx.x & 31;
-    const int wj = gw % g.nwj2, wi = gw / g.nwj2;
-    if (wi >= g.nstrips2) return;
+    // Windows that touch the mesh boundary run the general row step, about twice the instructions of
+    // the fast one, and in a one-wave launch the slowest warp is the launch time.  Each of their
+    // strips is therefore split between two warps: warps past the regular nwj2 x nstrips2 take the
+    // second halves (g.nslow2 such windows: window 0 and the last nslow2 - 1).
+    const int nreg = g.nwj2 * g.nstrips2;
+    int wj, wi, half;
+    if (gw < nreg) {
+        wj = gw % g.nwj2;
+        wi = gw / g.nwj2;
+        half = (wj == 0 || wj >= g.nwj2 - (g.nslow2 - 1)) ? 1 : 0;
+    } else {
+        const int e = gw - nreg;
+        if (g.nslow2 <= 0 || e >= g.nslow2 * g.nstrips2) return;
+        const int si = e % g.nslow2;
+        wi = e / g.nslow2;
+        wj = si == 0 ? 0 : g.nwj2 - g.nslow2 + si;
+        half = 2;
+    }
+    if (g.nslow2 <= 0) half = 0;
     constexpr int WSM = PD * STAGE + SV * kPitch2;  // the ring + the strip's first vertex row
     unsigned char* const wbase = smem + wib * WSM;
     const unsigned bar0 = smem_addr(smem + nwb * WSM) + wib * ((PD + 1) * 8);
@@ -305,8 +322,10 @@ __device__ __forceinline__ void strip_pass2(const Geo2& g, Op& op, const TmaMap*
     const bool cA = jA >= 0 && jA < g.ny, cB = jB < g.ny && lane < 31;
     const bool oA = vA && lane >= 1, oB = vB && lane < 31;
     const bool fastwin = j0 >= 1 && j0 + kCols2 <= g.ny;  // every column a valid interior vertex
-    const int i0 = wi * g.S2;
-    const int i1 = min(i0 + g.S2, g.nx + 1);
+    const int h2 = (g.S2 + 1) / 2;  // rows of a first half
+    const int i0 = wi * g.S2 + (half == 2 ? h2 : 0);
+    const int i1 = min(wi * g.S2 + (half == 1 ? h2 : g.S2), g.nx + 1);
+    if (i0 >= i1) return;
     const int vlast = min(i1, g.nx);          // last vertex row this strip reads
     const int clast = min(i1 - 1, g.nx - 1);  // last cell row this strip computes
     if (lane == 0) {
