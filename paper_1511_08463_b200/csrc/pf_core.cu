@@ -1054,12 +1054,13 @@ int pf_ctx_create(const pf_desc* desc, pf_ctx** out) {
         c->dim = 2;
         c->dof = 2;
         geometry_2d(c);
-        // engine choice by size (A/B on B200, tools/opbench2.py): the TMA engine wins from about 1M
-        // corner vertices up (1024^2 applies -5..-11 %, the config-3 slab load step 1.049 -> 1.021 s,
+        // engine choice by size (A/B on B200, tools/opbench2.py): the TMA engine wins from about 0.55M
+        // corner vertices (768^2) up (1024^2 applies -5..-11 %, the config-3 slab load step 1.049 -> 1.021 s,
         // 8192^2 union-jack Kuu 4.6 -> 5.9 TB/s); below that an apply is a few strip rows per warp,
         // bound by launch and pipeline-fill latency, where the one-column engine's shorter steps
         // are as fast or faster (SENT 512^2 load step: v2 +4 %)
-        if (c->strip2 < 0) c->strip2 = c->g.nc >= 1000000 ? 1 : 0;
+        // (768^2: isolated applies -13..-18 %; 512^2: equal in isolation, +6 % on the SENT load step)
+        if (c->strip2 < 0) c->strip2 = c->g.nc >= 550000 ? 1 : 0;
         c->n_a = c->g.nv;
         c->n_u = 2 * c->g.nv;
         c->n_el = c->g.ncell * c->g.npc;

@@ -1,5 +1,5 @@
 """The v2 2D strip engine (two vertex columns per lane, TMA row tiles; csrc/pf_strip2.cu) forced on
-(PF_STRIP2=1) at test sizes -- by default it only takes meshes of 1M vertices and more.
+(PF_STRIP2=1) at test sizes -- by default it only takes meshes of 0.55M vertices and more.
 
 Shapes are chosen so that every form of the row step runs: windows that touch the mesh boundary
 (general step), interior windows (fast step: ny >= 126 gives a window with no boundary column),
