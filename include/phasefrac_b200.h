@@ -189,6 +189,12 @@ int pf_load_u(pf_ctx* ctx, const double* alpha, double* f, void* stream);
  * (NULL or warm_start = 0 -> zero).  u_out may alias u0. */
 int pf_elastic_solve(pf_ctx* ctx, const double* alpha, const double* u0, double* u_out,
                      const pf_lin_opts* opts, pf_lin_report* rep, void* stream);
+/* The multigrid V-cycle of Kuu(alpha) as a stand-alone fixed SPD preconditioner (replaces the
+ * reference's SuperLU factor object, linalg.py:250-262, where a caller runs its own Krylov loop):
+ * prepare builds the hierarchy for alpha and the context's Dirichlet mask, apply computes z = M r
+ * (identity on eliminated rows).  Used by the element-list path on jittered structured meshes. */
+int pf_gmg_prepare(pf_ctx* ctx, const double* alpha, void* stream);
+int pf_gmg_apply(pf_ctx* ctx, const double* r, double* z, void* stream);
 /* damage_step: alpha_out = rsls solution of the box QP at fixed u (vi.py:187-264). */
 int pf_damage_solve(pf_ctx* ctx, const double* u, const double* alpha_lb, const double* alpha_in,
                     double* alpha_out, const pf_vi_opts* opts, pf_vi_report* rep, void* stream);

@@ -82,6 +82,8 @@ EXPORTS = {
     "pf_load_u": (C.c_int, [C.c_void_p] * 3 + [C.c_void_p]),
     "pf_elastic_solve": (C.c_int, [C.c_void_p] * 4 + [C.POINTER(LinOpts), C.POINTER(LinReport),
                                                        C.c_void_p]),
+    "pf_gmg_prepare": (C.c_int, [C.c_void_p] * 3),
+    "pf_gmg_apply": (C.c_int, [C.c_void_p] * 4),
     "pf_damage_solve": (C.c_int, [C.c_void_p] * 5 + [C.POINTER(VIOpts), C.POINTER(VIReport),
                                                       C.c_void_p]),
     "pf_relax_u": (C.c_int, [C.c_void_p] * 3 + [C.c_double, C.c_void_p, C.c_void_p]),

@@ -337,7 +337,7 @@ def thermal_strain(x2, tau: float, material: Material, delta_T: float) -> np.nda
 def setup_thermal_shock(material: Optional[Material] = None, L: float = 20.0, H: float = 10.0,
                         h: Optional[float] = None, dT_factor: float = 1.0, n_steps: int = 40,
                         tau_min: float = 0.05, tau_max: float = 3.0, jitter: float = 0.25,
-                        model: str = "AT1") -> UnstructuredSetup:
+                        model: str = "AT1", multigrid: bool = False) -> UnstructuredSetup:
     """Quench of [0, L] x [0, H] from its bottom surface (the reference's setup_thermal_shock,
     cases.py:195-235) on the element-list path: the jittered union-jack rect_mesh (mesh.py:112-142,
     seed 0), the erfc inelastic strain at the element centroids, u1 = 0 on the lateral sides,
@@ -359,6 +359,13 @@ def setup_thermal_shock(material: Optional[Material] = None, L: float = 20.0, H:
         return dofs, vals
 
     schedule = np.geomspace(tau_min, tau_max, n_steps)
+    if multigrid:
+        # the same grid without the jitter: its multigrid V-cycle preconditions the elastic PCG
+        # (SolverConfig.elastic_precond = "gmg")
+        nx, ny = max(1, round(L / h)), max(1, round(H / h))
+        twin = Discretization(StructuredMesh(nx, ny, L, H, "union_jack"), material, DamageModel(model))
+        twin.bc = DirichletBC(dofs, vals)
+        ops.attach_structured_twin(twin)
     return UnstructuredSetup("thermal_shock", mesh, ops, schedule, apply_load,
                              params={"delta_T": dT, "critical_shock": dTc, "h": h})
 
@@ -382,6 +389,8 @@ def run_quasistatic_unstructured(setup: UnstructuredSetup, config: SolverConfig,
                       alpha=torch.as_tensor(lb, dtype=torch.float64, device=ops.device).clone(),
                       alpha_lb=torch.as_tensor(lb, dtype=torch.float64, device=ops.device).clone())
     rtol = config.direct_rtol if config.elastic_solver == "direct" else config.elastic_rtol
+    # elastic_precond="gmg": the V-cycle of the structured twin (jittered structured meshes only)
+    precond = "gmg" if (config.elastic_precond == "gmg" and getattr(ops, "_twin", None) is not None) else "jacobi"
     records = []
     n = setup.schedule.shape[0]
     for k in (range(n) if steps is None else steps):
@@ -392,7 +401,8 @@ def run_quasistatic_unstructured(setup: UnstructuredSetup, config: SolverConfig,
         st = ops.am_load_step(state.u, state.alpha, state.alpha_lb, dofs, vals, omega=config.omega,
                               outer_atol=config.outer_atol, max_am_iterations=config.max_am_iterations,
                               elastic_rtol=rtol, damage_atol_factor=config.damage_atol_factor,
-                              max_vi_iterations=config.max_vi_iterations, log_callback=config.log_callback)
+                              max_vi_iterations=config.max_vi_iterations, log_callback=config.log_callback,
+                              elastic_precond=precond)
         en = st["energy_history"][-1]
         energy = EnergyBreakdown(*en)
         report = NonlinearReport(converged=bool(st["converged"]), final_residual_norm=st["final_residual_norm"],

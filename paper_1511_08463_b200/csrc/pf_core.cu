@@ -1335,6 +1335,29 @@ int pf_elastic_solve(pf_ctx* c, const double* alpha, const double* u0, double* u
         return set_error(c, PF_EINVAL, "context created with PF_SKIP_GMG");
     return elastic_solve(c, alpha, u0, u_out, o, rep, (cudaStream_t)s);
 }
+// The multigrid V-cycle as a stand-alone preconditioner: prepare builds the hierarchy of Kuu(alpha)
+// (with the context's Dirichlet mask), apply computes z = M r.  M is a fixed linear SPD operator, so a
+// caller's PCG on a spectrally equivalent operator -- the element-list Kuu of the same grid with
+// jittered vertices (umesh.py) -- may use it.
+int pf_gmg_prepare(pf_ctx* c, const double* alpha, void* s) {
+    NEED_WS(c);
+    if (c->d.skip & PF_SKIP_GMG) return set_error(c, PF_EINVAL, "context created with PF_SKIP_GMG");
+    if (!alpha) return set_error(c, PF_EINVAL, "null alpha");
+    cudaStream_t st = (cudaStream_t)s;
+    if (cudaMemcpyAsync(c->alpha_ws, alpha, sizeof(double) * c->n_a, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+        return set_error(c, PF_ECUDA, "alpha copy");
+    c->gmg_degree = 2;
+    const int rc = c->dim == 3 ? gmg3_setup(c, st) : gmg_setup(c, st);
+    c->gmg_built = 0;  // a later pf_elastic_solve builds its own
+    c->gmg_its0 = -1;
+    return rc;
+}
+int pf_gmg_apply(pf_ctx* c, const double* r, double* z, void* s) {
+    NEED_WS(c);
+    if (c->d.skip & PF_SKIP_GMG) return set_error(c, PF_EINVAL, "context created with PF_SKIP_GMG");
+    if (!r || !z) return set_error(c, PF_EINVAL, "null vector");
+    return c->dim == 3 ? gmg3_vcycle(c, r, z, (cudaStream_t)s, nullptr) : gmg_vcycle(c, r, z, (cudaStream_t)s, nullptr);
+}
 int pf_damage_solve(pf_ctx* c, const double* u, const double* lb, const double* a_in, double* a_out,
                     const pf_vi_opts* o, pf_vi_report* rep, void* s) {
     NEED_WS(c);

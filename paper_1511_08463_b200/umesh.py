@@ -252,14 +252,76 @@ class UnstructuredOperators:
             self._vec(x, self.n_vertices, "x"), self._vec(out, self.n_vertices, "out"), self._stream()))
         return out
 
+    def attach_structured_twin(self, twin) -> None:
+        """Use the multigrid V-cycle of a structured Discretization on the SAME grid (same vertex
+        numbering, cells and Dirichlet dofs; vertices at their un-jittered positions) as the
+        preconditioner of this mesh's elastic PCG (elastic_solve(precond="gmg")).  The reference's
+        jitter (mesh.py:134-141) moves interior vertices by a fraction of h and keeps the union-jack
+        connectivity, so the two stiffness operators are spectrally equivalent."""
+        if twin.mesh.n_vertices != self.n_vertices or twin.mesh.dim != self.mesh.dim:
+            raise ValueError("the structured twin must have the same vertices as the element-list mesh")
+        self._twin = twin
+
+    def _elastic_solve_gmg(self, alpha, b, out, rtol, atol, maxit):
+        """PCG (cg_solve, linalg.py:106-152: x0 = 0, stop at |r| <= max(rtol |b|, atol), breakdown on
+        p.Ap <= 0 or r.z <= 0) on this mesh's Kuu with z = V-cycle(structured twin) r.  Vectors and
+        scalars stay on the device; one host read of |r| per iteration."""
+        import torch
+        from .fem import _stream
+        from .linalg import BreakdownError
+        twin = self._twin
+        twin.call("pf_gmg_prepare", _lib.ptr(alpha), _stream())
+        n = self.n_udofs
+        x = out.zero_()
+        r = b.clone()
+        z, q = torch.empty_like(b), torch.empty_like(b)
+        bnorm = float(torch.linalg.vector_norm(b))
+        tol = max(rtol * bnorm, atol)
+        rn = bnorm
+        its = 0
+        maxit = int(maxit) if maxit else 10 * n
+        if rn <= tol:
+            return x, LinearSolveReport(0, rn, True)
+        twin.call("pf_gmg_apply", _lib.ptr(r), _lib.ptr(z), _stream())
+        p = z.clone()
+        rz = torch.dot(r, z)
+        while its < maxit:
+            self.apply_Kuu(alpha, p, out=q, apply_bc=True)
+            pq = torch.dot(p, q)
+            gamma = rz / pq
+            x.addcmul_(p, gamma)
+            r.addcmul_(q, gamma, value=-1.0)
+            its += 1
+            rn, pqh, rzh = (float(v) for v in torch.stack([torch.linalg.vector_norm(r), pq, rz]).tolist())
+            if not pqh > 0.0 or not rzh > 0.0:
+                raise BreakdownError(f"elastic PCG breakdown (p.Ap = {pqh:.3e}, r.z = {rzh:.3e})")
+            if rn <= tol:
+                break
+            twin.call("pf_gmg_apply", _lib.ptr(r), _lib.ptr(z), _stream())
+            rz_new = torch.dot(r, z)
+            p.mul_(rz_new / rz).add_(z)
+            rz = rz_new
+        return x, LinearSolveReport(its, rn, rn <= tol)
+
     def elastic_solve(self, alpha, b, out=None, rtol: float = 1e-8, atol: float = 0.0, maxit: int = 0,
-                      check_every: int = 10, raise_on_failure: bool = True):
+                      check_every: int = 10, raise_on_failure: bool = True, precond: str = "jacobi"):
         """x with Kuu(alpha) x = b, Dirichlet rows/cols eliminated, by device Jacobi PCG from
         x0 = 0 (cg_solve, linalg.py:106-152).  Returns (x, LinearSolveReport); non-convergence
         raises LinearSolverError "elastic CG stalled" as solver.py:139-141 unless
-        raise_on_failure is False."""
+        raise_on_failure is False.  ``precond="gmg"``: the V-cycle of an attached structured twin
+        (attach_structured_twin) instead of Jacobi."""
         import torch
         out = torch.empty_like(b) if out is None else out
+        if precond == "gmg":
+            if getattr(self, "_twin", None) is None:
+                raise ValueError("precond='gmg' needs attach_structured_twin() first")
+            x, report = self._elastic_solve_gmg(alpha, b, out, float(rtol), float(atol), maxit)
+            if raise_on_failure and not report.converged:
+                raise LinearSolverError(f"elastic CG stalled after {report.iterations} iterations "
+                                        f"(|r| = {report.final_residual_norm:.3e})")
+            return x, report
+        if precond != "jacobi":
+            raise ValueError(f"unknown preconditioner {precond!r}")
         o = _lib.LinOpts(precond=_lib.PREC["jacobi"], warm_start=0, maxit=int(maxit), rtol=float(rtol),
                          atol=float(atol), check_every=int(check_every))
         rep = _lib.LinReport()
@@ -309,7 +371,7 @@ class UnstructuredOperators:
     def am_load_step(self, u, alpha, alpha_lb, bc_dofs, bc_values, omega: float = 1.0,
                      outer_atol: float = 1e-7, max_am_iterations: int = 1000,
                      elastic_rtol: float = 1e-10, damage_atol_factor: float = 0.1,
-                     max_vi_iterations: int = 200, log_callback=None):
+                     max_vi_iterations: int = 200, log_callback=None, elastic_precond: str = "jacobi"):
         """One load step of alternate minimisation on the element-list mesh (am_loop with an
         absolute target, solver.py:129-241; oracle/am.py am_loop): elastic half-step (device PCG on
         the Dirichlet-lifted Kuu), over-relaxed update u0 + omega (u* - u0), damage half-step
@@ -349,7 +411,7 @@ class UnstructuredOperators:
             _, b, _ = self.physics(g, alpha)
             b.neg_()
             b[dofs] = vals
-            us, lrep = self.elastic_solve(alpha, b, rtol=elastic_rtol)
+            us, lrep = self.elastic_solve(alpha, b, rtol=elastic_rtol, precond=elastic_precond)
             stats["krylov_iterations"] += lrep.iterations
             u.add_(omega * (us - u))
             u[dofs] = vals

@@ -5,8 +5,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_1511_08463_b200 as pf
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 12
-setup = pf.setup_thermal_shock(n_steps=n, dT_factor=2.0)
-cfg = pf.SolverConfig(method="am", outer_atol=1e-8)
+mg = len(sys.argv) > 2 and sys.argv[2] == "gmg"   # elastic PCG preconditioned by the structured twin's V-cycle
+setup = pf.setup_thermal_shock(n_steps=n, dT_factor=2.0, multigrid=mg)
+cfg = pf.SolverConfig(method="am", outer_atol=1e-8, elastic_precond="gmg" if mg else "jacobi")
 V = setup.mesh.n_vertices
 z = torch.zeros(V, dtype=torch.float64, device="cuda")
 st = pf.State(u=torch.zeros(2 * V, dtype=torch.float64, device="cuda"), alpha=z.clone(), alpha_lb=z.clone())
