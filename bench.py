@@ -244,7 +244,7 @@ def oracle_traction1_steps(warm, timed):
 # omega = 1.8 contracts the displacement by |1 - omega| = 0.8 per iteration while the damage is
 # static, so every non-nucleating step needs the same 31 iterations to reach the 1e-3 hand-off)
 SENT512_AM = [31] * 18 + [67] + [31] * 30 + [308, 2148] + [31] * 9
-SENT512_NEWTON = [1, 2, 1, 1, 2, 2] + [1] * 12 + [63, 2] + [1] * 29 + [90, 61] + [1] * 9
+SENT512_NEWTON = [1, 2, 1, 1, 2, 2, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 23, 2, 1, 1, 1, 1, 1, 1, 1, 1, 1, 2, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 30, 21, 1, 1, 1, 1, 1, 1, 1, 1, 1]  # with Newton attempts capped at 10 (sent_config)
 
 
 def oracle_sent_am_iteration(n, step):
