@@ -973,6 +973,11 @@ __device__ __forceinline__ unsigned long long gtimer() {
         if (A.trace && blockIdx.x == 0 && threadIdx.x == 0) A.trace[tro + ntr++] = gtimer(); \
     } while (0)
 
+// Two lanes per vertex for levels of nth/4 < nv <= nth/2 vertices: off.  Every phase of the
+// persistent cycle starts on cold instructions (ncu: 12 % of its stall samples are instruction
+// fetch), and the variant was a quarter of the kernel's 15.5k SASS instructions; without it the SENT
+// 512^2 window is 0.6 % and the config-3 slab step 3.4 % faster (neither has a level in that range).
+constexpr bool kCoarseG2 = false;
 constexpr int kCB = 512;  // threads per CTA of the persistent coarse cycle (one CTA per SM; 1024 measured slower)
 // Chebyshev coefficients of every level into shared memory (threads t < nl; read by the phases
 // after the first barrier)
@@ -1019,7 +1024,7 @@ __device__ __forceinline__ void coarse_body(const CoarseArgs& A, const CCoef* co
     auto grid_each = [&](long long nv, auto fn) {
         if (4 * nv <= nth)
             for (long long e = tid; e < 4 * nv; e += nth) fn(G4{}, e >> 2, (int)(e & 3));
-        else if (2 * nv <= nth)  // (2 lanes in 2 rounds measured slower than 1 lane in 1 round)
+        else if (kCoarseG2 && 2 * nv <= nth)  // (2 lanes in 2 rounds measured slower than 1 lane in 1 round)
             for (long long e = tid; e < 2 * nv; e += nth) fn(G2{}, e >> 1, (int)(e & 1));
         else
             for (long long v = tid; v < nv; v += nth) fn(G1{}, v, 0);
