@@ -30,7 +30,7 @@ ap.add_argument("--save", default="")
 ap.add_argument("--out", default="gpurun_out/sent_window.json")
 ap.add_argument("--no-split", action="store_true")
 ap.add_argument("--cheb-deg", type=int, default=0, help="override fieldsplit_cheb_degree")
-ap.add_argument("--workload", default="sent", choices=["sent", "traction3d"])
+ap.add_argument("--workload", default="sent", choices=["sent", "traction3d", "thermal"])
 ap.add_argument("--save-dir", default="gpurun_out")
 args = ap.parse_args()
 save = {int(s) for s in args.save.split(",") if s}
@@ -39,6 +39,9 @@ os.makedirs("gpurun_out", exist_ok=True)
 if args.workload == "sent":
     setup = pf.setup_sent(n=args.n)
     cfg = bench.sent_config(pf)
+elif args.workload == "thermal":   # config 3: --n is ny, the slab is 4 n x n cells
+    setup = pf.setup_thermal_slab(nx=4 * args.n, ny=args.n)
+    cfg = bench.thermal_config(pf)
 else:
     setup = pf.setup_traction3d(n=args.n)
     cfg = bench.traction3d_config(pf)
@@ -72,7 +75,7 @@ def plain_pass():
               f"E=({r.energy.elastic:.6e},{r.energy.dissipated:.6e}) amax={rows[-1]['amax']:.3f}",
               flush=True)
         if k in save:
-            np.savez(f"{args.save_dir}/{args.workload}{args.n}_state{k}.npz", u=st.u.cpu().numpy(),
+            np.savez_compressed(f"{args.save_dir}/{args.workload}{args.n}_state{k}.npz", u=st.u.cpu().numpy(),
                      alpha=st.alpha.cpu().numpy(), alpha_lb=st.alpha_lb.cpu().numpy(), load=r.load,
                      E=np.array(rows[-1]["E"]), am=rep.am_iterations)
     return rows

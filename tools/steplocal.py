@@ -11,7 +11,8 @@ then compared (north-star bars: energies 1e-6 relative, max|d alpha| 1e-4).
 Parity settings (SURVEY 8(c) rule): outer_atol 1e-9 on both sides, device elastic PCG rtol 1e-12,
 damage VI abs_tol 0.1 outer_atol; everything else is config 2 (bench.sent_config: ORAM omega 1.8,
 Newton hand-off at |Phi| < 1e-3, multigrid field split).  The oracle solves directly (SuperLU).
-``--workload traction3d`` runs config 4 (the 3D problem at --n cells per side).
+``--workload traction3d`` runs config 4 (the 3D problem at --n cells per side), ``--workload
+thermal`` config 3 (the quenched slab, 4 n x n cells).
 """
 import argparse
 import json
@@ -27,7 +28,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("mode", choices=["device", "oracle", "compare"])
 ap.add_argument("--state", required=True)
 ap.add_argument("--step", type=int, required=True)
-ap.add_argument("--workload", default="sent", choices=["sent", "traction3d"])
+ap.add_argument("--workload", default="sent", choices=["sent", "traction3d", "thermal"])
 ap.add_argument("--n", type=int, default=512)
 ap.add_argument("--atol", type=float, default=1e-9)
 ap.add_argument("--literal", action="store_true", help="config-literal tolerances instead")
@@ -49,6 +50,8 @@ def run_device():
     import paper_1511_08463_b200 as pf
     if args.workload == "sent":
         setup, cfg = pf.setup_sent(n=args.n), bench.sent_config(pf)
+    elif args.workload == "thermal":
+        setup, cfg = pf.setup_thermal_slab(nx=4 * args.n, ny=args.n), bench.thermal_config(pf)
     else:
         setup, cfg = pf.setup_traction3d(n=args.n), bench.traction3d_config(pf)
     if not args.literal:
@@ -62,7 +65,7 @@ def run_device():
     r = pf.run_quasistatic(setup, cfg, snapshot_stride=1, state=st, steps=[args.step])[0]
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
-    np.savez(dev_path, u=r.u, alpha=r.alpha, energy=np.array(tuple(r.energy)), load=r.load,
+    np.savez_compressed(dev_path, u=r.u, alpha=r.alpha, energy=np.array(tuple(r.energy)), load=r.load,
              am=r.report.am_iterations, newton=r.report.newton_iterations,
              attempts=r.report.newton_attempts, wall=wall,
              residual=r.report.final_residual_norm,
@@ -78,6 +81,10 @@ def run_oracle():
         s = opb.sent(n=args.n)
         cfg = oam.AMConfig(method="oram_newton", omega=1.8, outer_atol=1e-6 if args.literal else args.atol,
                            am_switch_atol=1e-3, max_am_iterations=3000)
+    elif args.workload == "thermal":
+        s = opb.thermal_slab(nx=4 * args.n, ny=args.n)
+        cfg = oam.AMConfig(method="oram_newton", omega=1.5, outer_atol=1e-7 if args.literal else args.atol,
+                           max_am_iterations=2000)
     else:
         s = opb.traction3d(n=args.n)
         cfg = oam.AMConfig(method="oram_newton", omega=1.7, outer_atol=1e-6 if args.literal else args.atol,
