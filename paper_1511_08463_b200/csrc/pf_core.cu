@@ -520,7 +520,7 @@ int pcg_run(Ctx* c, int kind, const PcgBuffers& B, const double* coef, const uns
             PF_TRY(read_scal(c, st, 0, 24));
             // profiling: the launch's algorithmic bytes are known once its iterations are
             if (c->prof.on && !c->prof.log.empty())
-                c->prof.log.back().bytes = c->h_scal[S_ITER] * pcg_kaa_iter_bytes(c);
+                c->prof.log.back().bytes = c->h_scal[S_ITER] * pcg_kaa_iter_bytes(c) * c->tile_frac;
             return pcg_finish(c, B, rep, st);
         }
         if (rc != PF_EINVAL) return rc;
@@ -984,6 +984,8 @@ static void plan_workspace(Ctx* c) {
     add((void**)&c->kappa, sizeof(double) * c->n_el);
     add((void**)&c->bcmask, c->n_a);
     add((void**)&c->act, c->n_a);
+    c->tile_cap = (int)(c->n_a / 16 + 4096);  // a strip tile has >= 30 outputs
+    add((void**)&c->tile_list, sizeof(int) * (c->tile_cap + 1) + c->tile_cap);
     add((void**)&c->eps0_tab, sizeof(double) * 4 * (c->d.ny + 1));
     add((void**)&c->rowgeo_buf, sizeof(double) * 2 * (c->d.ny + 1));
     add((void**)&c->partials, sizeof(double) * kMaxRed * kMaxBlocksRed);

@@ -301,6 +301,9 @@ struct Ctx {
     double *alpha_ws, *u_ws;                                                 // n_a, n_u
     double *ubar;                                                            // n_u
     unsigned char *bcmask, *act;                                             // n_a
+    int* tile_list = nullptr;  // free tiles of the masked damage PCG: [0] count, [1..] tiles, then tile_cap flag bytes
+    int tile_cap = 0;
+    double tile_frac = 1.0;    // share of the tiles the last persistent damage PCG visited (profiling)
     double *eps0_tab;                                                        // 4*ny
     double *rowgeo_buf;                                                      // 2*ny (graded rows)
     double *partials, *scal;
@@ -516,6 +519,7 @@ int launch_pcg_kaa1(Ctx* c, const PcgBuffers& B, const double* kappa, const unsi
 double pcg_kaa_iter_bytes(const Ctx* c);
 int launch_pcg_kaa(Ctx* c, const PcgBuffers& B, const double* kappa, const unsigned char* act, cudaStream_t st);
 int launch3_pcg_kaa(Ctx* c, const PcgBuffers& B, const double* kappa, const unsigned char* act, cudaStream_t st);
+void launch_tile_compact(int ntile, const unsigned char* flag, int* list, cudaStream_t st);
 // kind: 0 = Kuu Jacobi (coef = alpha), 1 = Kaa masked by act (coef = kappa), 2 = Kuu GMG
 int pcg_run(Ctx* c, int kind, const PcgBuffers& B, const double* coef, const unsigned char* act,
             double rtol, double atol, long long maxit, int zero_x0, int check_every,

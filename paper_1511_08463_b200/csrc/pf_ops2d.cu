@@ -168,13 +168,40 @@ int launch_Kaa_cgA(Ctx* c, const double* kappa, const double* z, const double* p
 // the same scalar decisions and the result is deterministic.  The strips are "virtual blocks"
 // distributed over the resident CTAs.  Replaces 2 dependent launches per iteration (each
 // latency-bound on a 4-17 MB problem) and the per-pair graph overhead.
+// Free strips of the masked solve (as k_tile_flags3, pf_ops3d.cu): on an active row the masked system
+// is the identity with a zero right-hand side, so x, r, z, p and q stay 0 there.  A warp's strip
+// (30 output columns x S rows) whose input box -- outputs +-1, and for the crossed pattern the
+// centres of the cells it touches -- holds active vertices only writes zeros and adds 0 to p.q.
+// The loop visits the flagged strips only (ascending list), the vector pass skips active rows.
+__global__ void __launch_bounds__(256) k_tile_flags2(const Geo2 g, const unsigned char* __restrict__ act, int ntile,
+                                                     unsigned char* __restrict__ flag) {
+    const int t = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (t >= ntile) return;
+    const int wj = t % g.nwj, wi = t / g.nwj;
+    const int j = wj * kLanesOut - 1 + lane;
+    const int i0 = max(wi * g.S - 1, 0), i1 = min(wi * g.S + g.S, g.nx);
+    bool f = false;
+    if (j >= 0 && j <= g.ny)
+        for (int i = i0; i <= i1; ++i) f |= act[vid(g, i, j)] == 0;
+    if (g.pattern == PF_CROSSED && j >= 0 && j < g.ny && lane < 31)
+        for (int ci = i0; ci < i1; ++ci) f |= act[ctr(g, ci, j)] == 0;
+    f = __any_sync(PF_FULL, f);
+    if (lane == 0) flag[t] = f ? 1 : 0;
+}
+
 template <bool MASKED, int PAT, int NT>
 __global__ void __launch_bounds__(NT, 512 / NT) k_pcg_kaa(const Geo2 g, OpKaa<true, MASKED> op, int nvb, long long n,
                                                         double* x, double* r, double* z, double* p0, double* p1,
                                                         double* q, const double* dinv, double* s, double* partials,
-                                                        unsigned int* bar) {
+                                                        unsigned int* bar, const int* __restrict__ tiles) {
     extern __shared__ __align__(16) unsigned char smem[];
     if (!(s[S_DONE] == 0.0 && s[S_FAIL] == 0.0)) return;  // uniform
+    // flagged strips (see k_tile_flags2); the list pays when at most half of the strips are flagged --
+    // otherwise (AT2: nearly every vertex is free) the loop runs exactly as without it
+    const int nall = g.nwj * g.nstrips;
+    const int nfree = tiles ? tiles[0] : nall;
+    const bool sparse = MASKED && tiles && 2 * nfree <= nall;
+    const int wpb = NT / 32, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const double target = s[S_TARGET], maxit = s[S_MAXIT];
     double rz = s[S_RZ], beta = s[S_BETA], rn = s[S_RNORM], pap = 0.0, gm = 0.0;
     long long it = (long long)s[S_ITER];
@@ -190,23 +217,45 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_pcg_kaa(const Geo2 g, OpKaa<tr
         op.acc = 0.0;
         op.use_breg = 1;
         op.breg = it > 0 ? beta : 0.0;
-        for (int vb = blockIdx.x; vb < nvb; vb += gridDim.x)
-            strip_pass<OpKaa<true, MASKED>, PAT>(g, op, smem, vb * (NT / 32) + (threadIdx.x >> 5));
+        // warps are independent in this engine: each takes (flagged) strips in turn
+        const int nw = sparse ? nfree : nvb * wpb;
+        for (int m = blockIdx.x * wpb + warp; m < nw; m += gridDim.x * wpb)
+            strip_pass<OpKaa<true, MASKED>, PAT>(g, op, smem, sparse ? tiles[1 + m] : m);
         block_partials(&op.acc, 1, partials, 0);
         grid_sync(bar);
         pap = grid_total(partials, 0);
         if (!(pap > 0.0)) { fail = 1.0; break; }
         gm = rz / pap;
         double acc[2] = {0.0, 0.0};
-        for (long long i = tid; i < n; i += nth) {
+        auto upd = [&](long long i, bool live) {
             const double xi = __ldcg(x + i) + gm * __ldcg(pout + i);
             const double ri = __ldcg(r + i) - gm * __ldcg(q + i);
             const double zi = dinv[i] * ri;
-            x[i] = xi;
-            r[i] = ri;
-            z[i] = zi;
-            acc[0] += ri * ri;
-            acc[1] += ri * zi;
+            if (live) {
+                x[i] = xi;
+                r[i] = ri;
+                z[i] = zi;
+                acc[0] += ri * ri;
+                acc[1] += ri * zi;
+            }
+        };
+        if (sparse) {  // the rows the flagged strips own (every free row is one of them), spread
+                       // over all threads: item = (strip on the list, row of the strip, lane)
+            const int R = g.S * 32;
+            const long long half = (long long)nfree * R, items = PAT == PF_CROSSED ? 2 * half : half;
+            for (long long e = tid; e < items; e += nth) {
+                const bool cen = PAT == PF_CROSSED && e >= half;
+                const long long e2 = cen ? e - half : e;
+                const int m = (int)(e2 / R), rho = (int)(e2 % R), l = rho & 31;
+                if (l >= kLanesOut) continue;
+                const int t = tiles[1 + m], wj = t % g.nwj, wi = t / g.nwj;
+                const int j = wj * kLanesOut + l, i = wi * g.S + (rho >> 5);
+                if (cen ? (j >= g.ny || i >= g.nx) : (j > g.ny || i > g.nx)) continue;
+                const long long v = cen ? ctr(g, i, j) : vid(g, i, j);
+                upd(v, op.act[v] == 0);
+            }
+        } else {
+            for (long long i = tid; i < n; i += nth) upd(i, true);
         }
         block_partials(acc, 2, partials, 1);
         grid_sync(bar);
@@ -494,6 +543,28 @@ static int launch_pcg_kaa_pat(Ctx* c, const PcgBuffers& B, const double* kappa, 
     const int nb = std::min(nvb, nsm * std::max(per, 1));
     if (per < 1 || nb > kMaxBlocksRed) return PF_EINVAL;  // caller falls back to the graph loop
     Op op{kappa, B.z, B.p0, B.p1, B.q, act, c->scal, redbuf(c), 0.0};
+    const int* tiles = nullptr;
+    c->tile_frac = 1.0;
+    static const bool skip_off = getenv("PF_NO_TILE_SKIP") != nullptr;
+    if (MASKED && !skip_off && c->tile_list && warps <= c->tile_cap) {
+        unsigned char* flag = reinterpret_cast<unsigned char*>(c->tile_list + c->tile_cap + 1);
+        k_tile_flags2<<<(int)((warps + 7) / 8), 256, 0, st>>>(g, act, (int)warps, flag);
+        launch_tile_compact((int)warps, flag, c->tile_list, st);
+        c->launches += 2;
+        tiles = c->tile_list;
+        if (c->prof.on || getenv("PF_TILE_TRACE")) {  // (diagnostics only: one host read)
+            int nfree = 0;
+            cudaMemcpyAsync(&nfree, c->tile_list, sizeof(int), cudaMemcpyDeviceToHost, st);
+            cudaStreamSynchronize(st);
+            c->tile_frac = 2LL * nfree <= (long long)warps ? (double)nfree / (double)warps : 1.0;
+        }
+        if (getenv("PF_TILE_TRACE")) {
+            int nfree = 0;
+            cudaMemcpyAsync(&nfree, c->tile_list, sizeof(int), cudaMemcpyDeviceToHost, st);
+            cudaStreamSynchronize(st);
+            fprintf(stderr, "  damage pcg: %d of %lld strips hold free vertices\n", nfree, warps);
+        }
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(nb);
     cfg.blockDim = dim3(NT);
@@ -506,7 +577,7 @@ static int launch_pcg_kaa_pat(Ctx* c, const PcgBuffers& B, const double* kappa, 
     cfg.numAttrs = 1;
     const int ps = prof_begin(c, st);
     cudaError_t e = cudaLaunchKernelEx(&cfg, k_pcg_kaa<MASKED, PAT, NT>, g, op, nvb, B.n, B.x, B.r, B.z, B.p0, B.p1,
-                                       B.q, (const double*)B.dinv, c->scal, c->partials, c->tickets + 62);
+                                       B.q, (const double*)B.dinv, c->scal, c->partials, c->tickets + 62, tiles);
     prof_end(c, st, ps, K_KAA_CG, 0.0);
     c->launches++;
     return check_cuda(c, e, "persistent pcg launch");

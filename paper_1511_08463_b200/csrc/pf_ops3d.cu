@@ -1348,6 +1348,57 @@ int launch3_Kaa_cgA(Ctx* c, const double* kappa, const double* z, const double* 
     Op3Kaa<true, false> op{kappa, z, p_in, p_out, q, nullptr, c->scal, rb3(c), 0.0};
     return run3w(c, c->g3, op, st, K_KAA_CG, bytes);
 }
+// ---- free tiles of the masked damage PCG ---------------------------------------------------------
+// On an active row the masked system is the identity with a zero right-hand side, so x, r, z, p and
+// q stay 0 there for the whole solve.  A tile whose input box (its output vertices +-1 in every
+// direction) holds active vertices only therefore writes zeros and adds 0 to p.q: the persistent
+// loop visits just the tiles on this list (ascending, so the sums keep a fixed order), and its
+// vector pass skips the active rows.  After localisation the free set of an AT1 damage solve is a
+// thin layer around the crack.
+__global__ void __launch_bounds__(256) k_tile_flags3(const Geo3 g, const unsigned char* __restrict__ act, int ntile,
+                                                     unsigned char* __restrict__ flag) {
+    const int t = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (t >= ntile) return;
+    const int bk = t % g.nbk, rest = t / g.nbk, bj = rest % g.nbj, bs = rest / g.nbj;
+    const int k = bk * 30 - 1 + lane;
+    const int j0 = max(bj * (kW3 - 2) - 1, 0), j1 = min(bj * (kW3 - 2) + (kW3 - 2), g.ny);
+    const int i0 = max(bs * g.S - 1, 0), i1 = min(bs * g.S + g.S, g.nx);
+    bool f = false;
+    if (k >= 0 && k <= g.nz)
+        for (int i = i0; i <= i1; ++i)
+            for (int j = j0; j <= j1; ++j) f |= act[vid3(g, i, j, k)] == 0;
+    f = __any_sync(PF_FULL, f);
+    if (lane == 0) flag[t] = f ? 1 : 0;
+}
+// list[0] = number of flagged tiles, list[1..] = their indices in ascending order (one block)
+__global__ void __launch_bounds__(1024) k_tile_compact(int ntile, const unsigned char* __restrict__ flag,
+                                                       int* __restrict__ list) {
+    __shared__ int wsum[32];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int per = ((ntile + 31) / 32 + 31) / 32 * 32;  // tiles per warp, a multiple of 32
+    const int b0 = w * per, b1 = min(b0 + per, ntile);
+    int cnt = 0;
+    for (int b = b0; b < b1; b += 32) {
+        const int t = b + lane;
+        cnt += __popc(__ballot_sync(PF_FULL, t < b1 && flag[t]));
+    }
+    if (lane == 0) wsum[w] = cnt;
+    __syncthreads();
+    int off = 0;
+    for (int q = 0; q < w; ++q) off += wsum[q];
+    for (int b = b0; b < b1; b += 32) {
+        const int t = b + lane;
+        const bool f = t < b1 && flag[t];
+        const unsigned m = __ballot_sync(PF_FULL, f);
+        if (f) list[1 + off + __popc(m & ((1u << lane) - 1u))] = t;
+        off += __popc(m);
+    }
+    if (threadIdx.x == 1023) list[0] = off;
+}
+void launch_tile_compact(int ntile, const unsigned char* flag, int* list, cudaStream_t st) {
+    k_tile_compact<<<1, 1024, 0, st>>>(ntile, flag, list);
+}
+
 // The whole masked Jacobi-PCG loop on the 3D damage block in one cooperative launch, as the 2D
 // k_pcg_kaa (pf_ops2d.cu): per iteration one strip pass over all tiles (p = z + beta p, q = Kaa p,
 // p.q) and one vector pass (x += gamma p, r -= gamma q, z = D^-1 r, r.r, r.z), separated by grid
@@ -1357,9 +1408,13 @@ template <bool MASKED>
 __global__ void __launch_bounds__(kW3 * 32, 2) k_pcg_kaa3(const Geo3 g, Op3Kaa<true, MASKED> op, int ntile, long long n,
                                                          double* x, double* r, double* z, double* p0, double* p1,
                                                          double* q, const double* dinv, double* s, double* partials,
-                                                         unsigned int* bar) {
+                                                         unsigned int* bar, const int* __restrict__ tiles) {
     extern __shared__ __align__(16) unsigned char smem[];
     if (!(s[S_DONE] == 0.0 && s[S_FAIL] == 0.0)) return;  // uniform
+    // free tiles only (see k_tile_flags3), when at most half of the tiles are flagged
+    const int nfree = tiles ? tiles[0] : ntile;
+    const bool sparse = MASKED && tiles && 2 * nfree <= ntile;
+    const int nt = sparse ? nfree : ntile;
     const double target = s[S_TARGET], maxit = s[S_MAXIT];
     double rz = s[S_RZ], beta = s[S_BETA], rn = s[S_RNORM], pap = 0.0, gm = 0.0;
     long long it = (long long)s[S_ITER];
@@ -1375,9 +1430,9 @@ __global__ void __launch_bounds__(kW3 * 32, 2) k_pcg_kaa3(const Geo3 g, Op3Kaa<t
         op.acc = 0.0;
         op.use_breg = 1;
         op.breg = it > 0 ? beta : 0.0;
-        for (int t = blockIdx.x; t < ntile; t += gridDim.x) {
+        for (int m = blockIdx.x; m < nt; m += gridDim.x) {
             __syncthreads();  // the previous tile's readers of the exchange buffers are done
-            strip3_tile<Op3Kaa<true, MASKED>, kW3>(g, op, smem, t);
+            strip3_tile<Op3Kaa<true, MASKED>, kW3>(g, op, smem, sparse ? tiles[1 + m] : m);
         }
         block_partials(&op.acc, 1, partials, 0);
         grid_sync(bar);
@@ -1385,15 +1440,36 @@ __global__ void __launch_bounds__(kW3 * 32, 2) k_pcg_kaa3(const Geo3 g, Op3Kaa<t
         if (!(pap > 0.0)) { fail = 1.0; break; }
         gm = rz / pap;
         double acc[2] = {0.0, 0.0};
-        for (long long i = tid; i < n; i += nth) {
+        auto upd = [&](long long i, bool live) {
             const double xi = __ldcg(x + i) + gm * __ldcg(pout + i);
             const double ri = __ldcg(r + i) - gm * __ldcg(q + i);
             const double zi = dinv[i] * ri;
-            x[i] = xi;
-            r[i] = ri;
-            z[i] = zi;
-            acc[0] += ri * ri;
-            acc[1] += ri * zi;
+            if (live) {
+                x[i] = xi;
+                r[i] = ri;
+                z[i] = zi;
+                acc[0] += ri * ri;
+                acc[1] += ri * zi;
+            }
+        };
+        if (sparse) {  // the rows the flagged tiles own (every free row is one of them), spread over
+                       // all threads: item = (tile on the list, row of the tile, pencil, lane)
+            const int R = g.S * (kW3 - 2) * 32;
+            const long long items = (long long)nfree * R;
+            for (long long e = tid; e < items; e += nth) {
+                const int m = (int)(e / R), rho = (int)(e % R), l = rho & 31;
+                if (l >= 30) continue;
+                const int t = tiles[1 + m];
+                const int bk = t % g.nbk, rest = t / g.nbk, bj = rest % g.nbj, bs = rest / g.nbj;
+                const int j = bj * (kW3 - 2) + (rho >> 5) % (kW3 - 2), k = bk * 30 + l;
+                const int i = bs * g.S + (rho >> 5) / (kW3 - 2);
+                if (i > g.nx || j > g.ny || k > g.nz) continue;
+                const long long v = vid3(g, i, j, k);
+                if (op.act[v]) continue;  // most rows of a flagged 3D tile are active: skip their loads
+                upd(v, true);
+            }
+        } else {
+            for (long long i = tid; i < n; i += nth) upd(i, true);
         }
         block_partials(acc, 2, partials, 1);
         grid_sync(bar);
@@ -1442,6 +1518,28 @@ static int launch3_pcg_kaa_m(Ctx* c, const PcgBuffers& B, const double* kappa, c
     const int nb = std::min(ntile, nsm * std::max(per, 1));
     if (per < 1 || nb > kMaxBlocksRed) return PF_EINVAL;  // caller falls back to the graph loop
     Op op{kappa, B.z, B.p0, B.p1, B.q, act, c->scal, rb3(c), 0.0};
+    const int* tiles = nullptr;
+    c->tile_frac = 1.0;
+    static const bool skip_off = getenv("PF_NO_TILE_SKIP") != nullptr;
+    if (MASKED && !skip_off && c->tile_list && ntile <= c->tile_cap) {
+        unsigned char* flag = reinterpret_cast<unsigned char*>(c->tile_list + c->tile_cap + 1);
+        k_tile_flags3<<<(ntile + 7) / 8, 256, 0, st>>>(g, act, ntile, flag);
+        launch_tile_compact(ntile, flag, c->tile_list, st);
+        c->launches += 2;
+        tiles = c->tile_list;
+        if (c->prof.on || getenv("PF_TILE_TRACE")) {  // (diagnostics only: one host read)
+            int nfree = 0;
+            cudaMemcpyAsync(&nfree, c->tile_list, sizeof(int), cudaMemcpyDeviceToHost, st);
+            cudaStreamSynchronize(st);
+            c->tile_frac = 2LL * nfree <= (long long)ntile ? (double)nfree / (double)ntile : 1.0;
+        }
+        if (getenv("PF_TILE_TRACE")) {
+            int nfree = 0;
+            cudaMemcpyAsync(&nfree, c->tile_list, sizeof(int), cudaMemcpyDeviceToHost, st);
+            cudaStreamSynchronize(st);
+            fprintf(stderr, "  damage pcg: %d of %d tiles hold free vertices\n", nfree, ntile);
+        }
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(nb);
     cfg.blockDim = dim3(kW3 * 32);
@@ -1454,7 +1552,7 @@ static int launch3_pcg_kaa_m(Ctx* c, const PcgBuffers& B, const double* kappa, c
     cfg.numAttrs = 1;
     const int ps = prof_begin(c, st);
     cudaError_t e = cudaLaunchKernelEx(&cfg, k_pcg_kaa3<MASKED>, g, op, ntile, B.n, B.x, B.r, B.z, B.p0, B.p1, B.q,
-                                       (const double*)B.dinv, c->scal, c->partials, c->tickets + 62);
+                                       (const double*)B.dinv, c->scal, c->partials, c->tickets + 62, tiles);
     prof_end(c, st, ps, K_KAA_CG, 0.0);
     c->launches++;
     return check_cuda(c, e, "persistent 3D pcg launch");

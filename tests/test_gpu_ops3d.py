@@ -223,3 +223,30 @@ def test_persistent_damage_pcg_3d_matches_graph_loop(monkeypatch, model):
     assert r0.iterations == r1.iterations
     assert abs(r0.total_krylov_iterations - r1.total_krylov_iterations) <= r0.iterations
     assert float((a0 - a1).abs().max()) < 1e-9
+
+
+def test_damage_step_3d_with_a_localised_free_set(monkeypatch, capfd):
+    """As the 2D test of the same name (test_gpu_solvers.py): the persistent 3D damage PCG on the
+    list of tiles that hold free vertices (k_tile_flags3), against the oracle."""
+    import re
+    import paper_1511_08463_b200 as pf
+    monkeypatch.setenv("PF_TILE_TRACE", "1")
+    prob, om, rng = make3(30, 20, 70, model="AT1", ell=0.08)
+    x = om.mesh.vertices
+    c = np.array([0.55, 0.3, 1.5])
+    d2 = ((x - c) ** 2).sum(axis=1)
+    u = np.zeros(3 * om.nv)
+    for k in range(3):
+        u[k::3] = (3.5 - 0.2 * k) * np.exp(-d2 / 0.02) * (x[:, k] - c[k])
+    lb = np.where(d2 < 0.005, 0.2, 0.0)
+    a = lb.copy()
+    st = pf.State(dev(u), dev(a), dev(lb))
+    ad, rep = pf.damage_step(st, prob, pf.SolverConfig(outer_atol=1e-9))
+    counts = [(int(p), int(q)) for p, q in re.findall(r"damage pcg: (\d+) of (\d+) tiles", capfd.readouterr().err)]
+    ao, orep = oam.damage_half_step(oam.LoadState(u, a, lb), om, oam.AMConfig(outer_atol=1e-9))
+    assert rep.converged and orep.converged
+    # both sides stop at |Phi_FB| <= 1e-9; with or without the tile list the device field differs
+    # from the oracle's by the same 3.1e-9 here
+    assert np.max(np.abs(host(ad) - ao)) < 1e-8
+    assert host(ad).max() > 0.25 and np.count_nonzero(host(ad) > lb + 1e-12) < 0.3 * om.nv
+    assert counts and any(2 * free <= total for free, total in counts), counts

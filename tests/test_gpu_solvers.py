@@ -490,3 +490,34 @@ def test_minres_warm_start_meets_the_same_tolerance(monkeypatch):
     assert r1.converged and r2.converged and r1.iterations == r2.iterations
     assert rel(s1.u.cpu().numpy(), s2.u.cpu().numpy()) < 1e-8
     assert float((s1.alpha - s2.alpha).abs().max()) < 1e-8
+
+
+def _tile_counts(err):
+    import re
+    return [(int(a), int(b)) for a, b in re.findall(r"damage pcg: (\d+) of (\d+) (?:strips|tiles)", err)]
+
+
+@pytest.mark.parametrize("pattern", ["union_jack", "right", "crossed"])
+def test_damage_step_with_a_localised_free_set(pattern, monkeypatch, capfd):
+    """AT1 with the strain concentrated in one spot: away from it every vertex sits on its lower
+    bound (active), so the persistent damage PCG runs on the list of strips that hold free vertices
+    (k_tile_flags2, pf_ops2d.cu) and its vector pass on the rows those strips own.  The result
+    must be the oracle's; the trace shows that the list was short enough to be used."""
+    import paper_1511_08463_b200 as pf
+    monkeypatch.setenv("PF_TILE_TRACE", "1")
+    prob, om, rng = make_pair(pattern, "plane_strain", "AT1", 40, 95, lx=1.0, ly=2.4, hetero=True, ell=0.06)
+    xy = om.mesh.vertices
+    d2 = (xy[:, 0] - 0.62) ** 2 + (xy[:, 1] - 1.7) ** 2
+    u = np.zeros(om.nu_dofs)
+    u[0::2] = 4.0 * np.exp(-d2 / 0.02) * (xy[:, 0] - 0.62)
+    u[1::2] = 3.2 * np.exp(-d2 / 0.02) * (xy[:, 1] - 1.7)
+    lb = np.where(d2 < 0.004, 0.25, 0.0)       # an irreversibility bound inside the spot
+    a = lb.copy()
+    st = pf.State(dev(u), dev(a), dev(lb))
+    ad, rep = pf.damage_step(st, prob, pf.SolverConfig(outer_atol=1e-9))
+    counts = _tile_counts(capfd.readouterr().err)
+    ao, orep = oam.damage_half_step(oam.LoadState(u, a, lb), om, oam.AMConfig(outer_atol=1e-9))
+    assert rep.converged and orep.converged
+    assert np.max(np.abs(host(ad) - ao)) < 1e-9
+    assert host(ad).max() > 0.3 and np.count_nonzero(host(ad) > lb + 1e-12) < 0.3 * om.nv
+    assert counts and any(2 * free <= total for free, total in counts), counts
