@@ -772,7 +772,9 @@ int damage_solve(Ctx* c, const double* u, const double* lb, const double* a_in, 
             // 0.197 -> 0.209 s/step, so the default stays 0.1)
             static const double floor_f = getenv("PF_VI_FLOOR") ? atof(getenv("PF_VI_FLOOR")) : 0.1;
             const double afloor = (o->inner_mode == 1 ? floor_f : 0.1) * o->abs_tol;
+            c->rhs_masked = 1;  // k_classify zeroed the right-hand side on the active rows
             rc = pcg_run(c, 1, B, c->kappa, c->act, rtol, afloor, maxit, 1, 8, &lr, st);
+            c->rhs_masked = 0;
             rep->total_krylov_iterations += lr.iterations;
             if (getenv("PF_VI_TRACE"))
                 fprintf(stderr, "  vi it=%d merit=%.3e ninact=%.0f pcg its=%lld rtol=%.1e\n", it, std::sqrt(merit),

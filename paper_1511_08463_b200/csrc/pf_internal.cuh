@@ -304,6 +304,8 @@ struct Ctx {
     int* tile_list = nullptr;  // free tiles of the masked damage PCG: [0] count, [1..] tiles, then tile_cap flag bytes
     int tile_cap = 0;
     double tile_frac = 1.0;    // share of the tiles the last persistent damage PCG visited (profiling)
+    int rhs_masked = 0;        // the running masked PCG has b = 0 on its active rows (pf_damage_solve; not the
+                               // Newton field split's C block, whose identity rows carry b): the list applies
     double *eps0_tab;                                                        // 4*ny
     double *rowgeo_buf;                                                      // 2*ny (graded rows)
     double *partials, *scal;

@@ -546,7 +546,7 @@ static int launch_pcg_kaa_pat(Ctx* c, const PcgBuffers& B, const double* kappa, 
     const int* tiles = nullptr;
     c->tile_frac = 1.0;
     static const bool skip_off = getenv("PF_NO_TILE_SKIP") != nullptr;
-    if (MASKED && !skip_off && c->tile_list && warps <= c->tile_cap) {
+    if (MASKED && c->rhs_masked && !skip_off && c->tile_list && warps <= c->tile_cap) {
         unsigned char* flag = reinterpret_cast<unsigned char*>(c->tile_list + c->tile_cap + 1);
         k_tile_flags2<<<(int)((warps + 7) / 8), 256, 0, st>>>(g, act, (int)warps, flag);
         launch_tile_compact((int)warps, flag, c->tile_list, st);

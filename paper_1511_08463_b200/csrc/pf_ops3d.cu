@@ -1521,7 +1521,7 @@ static int launch3_pcg_kaa_m(Ctx* c, const PcgBuffers& B, const double* kappa, c
     const int* tiles = nullptr;
     c->tile_frac = 1.0;
     static const bool skip_off = getenv("PF_NO_TILE_SKIP") != nullptr;
-    if (MASKED && !skip_off && c->tile_list && ntile <= c->tile_cap) {
+    if (MASKED && c->rhs_masked && !skip_off && c->tile_list && ntile <= c->tile_cap) {
         unsigned char* flag = reinterpret_cast<unsigned char*>(c->tile_list + c->tile_cap + 1);
         k_tile_flags3<<<(ntile + 7) / 8, 256, 0, st>>>(g, act, ntile, flag);
         launch_tile_compact(ntile, flag, c->tile_list, st);
