@@ -521,3 +521,13 @@ def test_damage_step_with_a_localised_free_set(pattern, monkeypatch, capfd):
     assert np.max(np.abs(host(ad) - ao)) < 1e-9
     assert host(ad).max() > 0.3 and np.count_nonzero(host(ad) > lb + 1e-12) < 0.3 * om.nv
     assert counts and any(2 * free <= total for free, total in counts), counts
+
+
+def test_newton_c_block_solve_never_uses_the_free_strip_list(monkeypatch, capfd):
+    """The Newton field split's C-block solve (fieldsplit_inner="direct") shares the persistent masked
+    PCG kernel with the damage VI, but its identity rows carry a right-hand side: it must run the full
+    loop (Ctx::rhs_masked stays 0), so the trace of the list builder stays silent during Newton."""
+    monkeypatch.setenv("PF_TILE_TRACE", "1")
+    capfd.readouterr()
+    test_coupled_newton_matches_oracle("union_jack", "AT1")
+    assert not _tile_counts(capfd.readouterr().err)
