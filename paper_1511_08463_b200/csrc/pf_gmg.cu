@@ -1051,7 +1051,52 @@ __device__ __forceinline__ void coarse_body(const CoarseArgs& A, const CCoef* co
                     }
                 return make_double2(s0, s1);
             };
-            grid_each(C.L.nv, [&](auto g, long long v, int q) { v_restrict_f<false, decltype(g)::value>(A.L0, C.L, C.L.mask, collapse, C.b, v, q, C.d0); });
+            // one lane per coarse vertex (the large meshes): the 3x3 fine vertices under it touch
+            // 4x4 cells, so their 16 centres are loaded once instead of 4 per fine vertex (36);
+            // every sum is formed in collapse()'s order (an absent cell adds 0.25 * 0)
+            auto restrict1 = [&](long long v) {
+                const int nvyc = C.L.ny + 1;
+                const int I = (int)(v / nvyc), J = (int)(v % nvyc);
+                double2 cen[4][4];
+#pragma unroll
+                for (int a = 0; a < 4; ++a)
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) {
+                        const int ci = 2 * I - 2 + a, cj = 2 * J - 2 + b;
+                        const bool in = ci >= 0 && cj >= 0 && ci < g.nx && cj < g.ny;
+                        cen[a][b] = in ? ldv(A.r0, g.nc + (long long)ci * g.ny + cj) : make_double2(0.0, 0.0);
+                    }
+                double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+                for (int t = 0; t < 9; ++t) {
+                    const int pa = t / 3, pb = t % 3;
+                    const int fi = 2 * I - 1 + pa, fj = 2 * J - 1 + pb;
+                    const double w = w1d(fi, g.nx, I) * w1d(fj, g.ny, J);
+                    if (w == 0.0) continue;  // (also every out-of-range fine vertex)
+                    const long long f = (long long)fi * g.nvy + fj;
+                    const unsigned m = vmask(A.mask0, f);
+                    const double2 rv = ldv(A.r0, f);
+                    double c0 = (m & 1u) ? 0.0 : rv.x, c1 = (m & 2u) ? 0.0 : rv.y;
+#pragma unroll
+                    for (int da = 0; da < 2; ++da)
+#pragma unroll
+                        for (int db = 0; db < 2; ++db) {
+                            c0 += 0.25 * cen[pa + da][pb + db].x;
+                            c1 += 0.25 * cen[pa + da][pb + db].y;
+                        }
+                    const unsigned mf = A.L0.mask ? A.L0.mask[f] : 0u;
+                    if (!(mf & 1u)) s0 += w * c0;
+                    if (!(mf & 2u)) s1 += w * c1;
+                }
+                const unsigned mC = C.L.mask[v];
+                const double2 bv = make_double2((mC & 1u) ? 0.0 : s0, (mC & 2u) ? 0.0 : s1);
+                stv(C.b, v, bv);
+                if (C.d0) stv(C.d0, v, bmulT<false>(C.L.Dinv, C.L.nv, v, bv.x, bv.y));
+            };
+            grid_each(C.L.nv, [&](auto gg, long long v, int q) {
+                if constexpr (decltype(gg)::value == 1) restrict1(v);
+                else v_restrict_f<false, decltype(gg)::value>(A.L0, C.L, C.L.mask, collapse, C.b, v, q, C.d0);
+            });
         } else {
             grid_each(C.L.nv, [&](auto g, long long v, int q) { v_restrict<false, decltype(g)::value>(A.L0, C.L, C.L.mask, A.r0, C.b, v, q, C.d0); });
         }
