@@ -1208,6 +1208,7 @@ __device__ __forceinline__ void coarse_body(const CoarseArgs& A, const CCoef* co
         } else {
             for (long long v = tid; v < A.L0.nv; v += nth) v_prolong(A.L0, C.L, C.L.mask, C.x, A.z0, v);
         }
+        TR();  // (block 0's own share of the last phase: no barrier follows it)
     }
 }
 
