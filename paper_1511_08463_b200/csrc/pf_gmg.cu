@@ -754,11 +754,9 @@ __global__ void k_restrict(LevelDev F, LevelDev Cd, const unsigned char* maskc, 
 
 // 2:1 prolongation x_f += P x_c (with masks), one thread per fine vertex
 template <bool SH = false>
-__device__ __forceinline__ double2 pval(const LevelDev& F, const LevelDev& Cd, const unsigned char* maskc,
-                                        const double* xc, long long v) {  // (P x_c) at fine vertex v
-    const int nvyf = F.ny + 1, nvyc = Cd.ny + 1;
-    const int vi = (int)v;
-    const int fi = vi / nvyf, fj = vi - (vi / nvyf) * nvyf;
+__device__ __forceinline__ double2 pval_ij(const LevelDev& F, const LevelDev& Cd, const unsigned char* maskc,
+                                           const double* xc, int fi, int fj) {  // (P x_c) at fine vertex (fi, fj)
+    const int nvyc = Cd.ny + 1;
     int cx[2], cy[2]; double wx[2], wy[2];
     const int nxw = p1d(fi, F.nx, cx, wx), nyw = p1d(fj, F.ny, cy, wy);
     if (nxw == 1) { cx[1] = cx[0]; wx[1] = 0.0; }
@@ -776,6 +774,14 @@ __device__ __forceinline__ double2 pval(const LevelDev& F, const LevelDev& Cd, c
             if (w != 0.0 && !(mC & 2u)) s1 += w * xv.y;
         }
     return make_double2(s0, s1);
+}
+template <bool SH = false>
+__device__ __forceinline__ double2 pval(const LevelDev& F, const LevelDev& Cd, const unsigned char* maskc,
+                                        const double* xc, long long v) {  // (P x_c) at fine vertex v
+    const int nvyf = F.ny + 1;
+    const int vi = (int)v;
+    const int fi = vi / nvyf;
+    return pval_ij<SH>(F, Cd, maskc, xc, fi, vi - fi * nvyf);
 }
 template <bool SH = false>
 __device__ __forceinline__ void v_prolong(const LevelDev& F, const LevelDev& Cd, const unsigned char* maskc,
@@ -1193,12 +1199,11 @@ __device__ __forceinline__ void coarse_body(const CoarseArgs& A, const CCoef* co
                     const double2 a = pval(A.L0, C.L, C.L.mask, C.x, v);
                     if (!(m & 1u)) o.x += a.x;
                     if (!(m & 2u)) o.y += a.y;
-                } else {
-                    const long long cell = v - g.nc;
-                    const long long v00 = (cell / g.ny) * g.nvy + cell % g.ny;
-                    const long long cs[4] = {v00, v00 + g.nvy, v00 + 1, v00 + g.nvy + 1};
-                    for (int q = 0; q < 4; ++q) {
-                        const double2 a = pval(A.L0, C.L, C.L.mask, C.x, cs[q]);
+                } else {  // (32-bit index arithmetic: the phase is bound by its instruction stream)
+                    const int cell = (int)(v - g.nc);
+                    const int ci = cell / g.ny, cj = cell - ci * g.ny;
+                    for (int q = 0; q < 4; ++q) {  // corners (ci, cj), (ci+1, cj), (ci, cj+1), (ci+1, cj+1)
+                        const double2 a = pval_ij(A.L0, C.L, C.L.mask, C.x, ci + (q & 1), cj + (q >> 1));
                         o.x += 0.25 * a.x;
                         o.y += 0.25 * a.y;
                     }
